@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""FedHC round hot-path benchmark on B200 (one JSON line on rank 0).
+
+Workload ("femnist-logreg-c10", BASELINE.json configs[1] with the reference's
+model): per GPU 100 participants/round drawn from a 128-per-GPU fleet with
+heterogeneous budgets 10..100 (step 10), each a multinomial-logistic client
+(F = 784 = 28x28x1, C = 10) with 6400 samples and B = 64, i.e. one local
+epoch = 100 SGD steps; theta = 100, resource-aware scheduler, dynamic
+parallelism, 18 executors; sync FedAvg + test accuracy every round.
+
+A "step" is one FL round: selection -> native DES schedule -> local SGD of
+every participant -> sample-weighted FedAvg -> accuracy.  `value` = client
+local-SGD steps per second over the whole job (all ranks), device-resident
+(the round plans are uploaded before the timed region).  `e2e` = the same
+metric through the public round API with host buffers: selection, DES, PCG64
+batch permutations on the host, H2D of the permutations and descriptors,
+kernels, D2H of the accuracy count -- every round.
+
+N > 1 (torchrun): every rank trains its own 100 participants (weak scaling);
+the only data-path collective is one NCCL all-reduce of the fp64 partial
+FedAvg sums per round (+ one int64 all-reduce of the sharded test count).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import random
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+F, C, N_SAMPLES, BATCH, PER_GPU, FLEET_PER_GPU, LR = 784, 10, 6400, 64, 100, 128, 0.1
+EXECUTORS, THETA = 18, 100.0
+BUDGETS = tuple(range(10, 101, 10))
+N_TEST = 16000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(n_gpus):
+    return {
+        "workload": "femnist-logreg-c10: FedHC round, multinomial logistic clients (F=784, C=10)",
+        "model": "multinomial logistic regression (reference fl_core model), F=784, C=10",
+        "participants_per_round": PER_GPU * n_gpus,
+        "fleet": FLEET_PER_GPU * n_gpus,
+        "samples_per_client": N_SAMPLES,
+        "batch": BATCH,
+        "local_steps_per_client": math.ceil(N_SAMPLES / BATCH),
+        "budgets": "10..100 step 10",
+        "theta": THETA,
+        "scheduler": "resource-aware, dynamic parallelism",
+        "max_executors": EXECUTORS,
+        "aggregation": "sync FedAvg (fp64) + accuracy on 16000 test rows every round",
+        "global_batch": BATCH * PER_GPU * n_gpus,
+        "seq_len": 1,
+        "parallelism": f"clients sharded over {n_gpus} GPU(s)" + (", NCCL all-reduce of FedAvg partials" if n_gpus > 1
+                                                                  else ""),
+        "l2": "inputs larger than L2 (2.0 GB of client rows per GPU per round vs 126 MB L2); no flush needed",
+    }
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU reference (oracle port)
+_CPU = {}
+
+
+def _cpu_worker(args):
+    from oracle import flmath as fm
+    i, seed = args
+    sh = _CPU["shards"][i % len(_CPU["shards"])]
+    return fm.local_sgd(_CPU["params"], sh, N_SAMPLES, BATCH, LR, C, seed=seed)
+
+
+def cpu_reference(seconds: float, rounds: int | None = None, warmup: int = 0):
+    """The reference algorithm (oracle port of fl_core/engine) on the host cores.
+
+    Clients of a round run in a fork pool over all host cores (one BLAS
+    thread each); the DES, FedAvg and accuracy run as in the reference.
+    Returns (client-steps/s, cores, sample description, rounds timed).
+    """
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import multiprocessing as mp
+
+    from oracle import flmath as fm
+    from oracle import orchestration as oc
+
+    cores = len(os.sched_getaffinity(0))
+    n_shards = 16
+    rng = np.random.default_rng(0)
+    means = rng.standard_normal((C, F)) * 3.0
+    shards = []
+    for _ in range(n_shards):
+        y = rng.integers(0, C, N_SAMPLES)
+        shards.append(fm.Shard("c", means[y] + rng.standard_normal((N_SAMPLES, F)), y))
+    yt = rng.integers(0, C, N_TEST)
+    test = fm.Data(means[yt] + rng.standard_normal((N_TEST, F)), yt, C)
+    fleet = oc.fleet(FLEET_PER_GPU, 1, budget_levels=BUDGETS, num_samples=N_SAMPLES, batch_size=BATCH)
+    by_id = {c.client_id: c for c in fleet}
+    ids = sorted(by_id)
+    cfg = oc.Config(theta=THETA, max_executors=EXECUTORS, participants_per_round=PER_GPU, seed=1)
+    _CPU["shards"] = shards
+    _CPU["params"] = fm.zeros_params(F, C)
+    pick = random.Random("1:selection")
+    steps_per_client = math.ceil(N_SAMPLES / BATCH)
+    ctx = mp.get_context("fork")
+    done_rounds, t_total = 0, 0.0
+    with ctx.Pool(cores) as pool:
+        r = 0
+        while True:
+            t0 = time.perf_counter()
+            who = pick.sample(ids, PER_GPU)
+            oc.simulate_round(by_id, who, cfg)
+            deltas = pool.map(_cpu_worker, [(i, fm.seed_of("train", 1, r, c)) for i, c in enumerate(who)])
+            _CPU["params"] = fm.weighted_average(deltas, [float(N_SAMPLES)] * PER_GPU, _CPU["params"])
+            fm.accuracy(_CPU["params"], test)
+            dt = time.perf_counter() - t0
+            r += 1
+            if r <= warmup:
+                continue
+            done_rounds += 1
+            t_total += dt
+            if (rounds is not None and done_rounds >= rounds) or (rounds is None and t_total >= seconds):
+                break
+    value = done_rounds * PER_GPU * steps_per_client / t_total
+    sample = (f"{done_rounds} full rounds of {PER_GPU} clients x {steps_per_client} steps (F={F}, C={C}, B={BATCH}) "
+              f"incl. Python DES, FedAvg and 16000-row accuracy; clients in a fork pool of {cores} processes "
+              f"(1 BLAS thread each); shard data cycles over {n_shards} generated shards")
+    return value, cores, sample, done_rounds, t_total
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200 import _abi
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.roundsim import RoundSimulator
+    from paper_2305_15668_b200.training import batch_permutations, fedavg_device, stable_seed, stream_ptr
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+
+    n_fleet = FLEET_PER_GPU * world
+    n_part = PER_GPU * world
+    P = F * C + C
+    steps_per_client = math.ceil(N_SAMPLES / BATCH)
+
+    # ---- device-resident synthetic data (same generator on every rank) ----
+    g = torch.Generator(device=dev).manual_seed(1234)
+    means = torch.randn(C, F, device=dev, generator=g) * 3.0
+    y_all = torch.randint(0, C, (n_fleet * N_SAMPLES,), device=dev, generator=g, dtype=torch.int32)
+    x_all = torch.empty(n_fleet * N_SAMPLES, F, device=dev)
+    chunk = 1 << 20
+    for s in range(0, x_all.shape[0], chunk):
+        e = min(s + chunk, x_all.shape[0])
+        x_all[s:e] = means[y_all[s:e].long()] + torch.randn(e - s, F, device=dev, generator=g)
+    yt = torch.randint(0, C, (N_TEST,), device=dev, generator=g, dtype=torch.int32)
+    xt = means[yt.long()] + torch.randn(N_TEST, F, device=dev, generator=g)
+    lo, hi = rank * N_TEST // world, (rank + 1) * N_TEST // world   # sharded test set
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=N_SAMPLES, batch_size=BATCH),
+                              n_fleet, 1)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    offsets = {cid: (i * N_SAMPLES, N_SAMPLES) for i, cid in enumerate(ids)}
+    fed = DeviceFederation.from_arrays(x_all, y_all, offsets, xt[lo:hi].contiguous(), yt[lo:hi].contiguous(), C)
+    cfg = fh.FleetConfig(theta=THETA, max_executors=EXECUTORS, participants_per_round=n_part, seed=1)
+    sim = RoundSimulator(by_id)
+    stream = torch.cuda.current_stream()
+
+    params = torch.zeros(P, dtype=torch.float64, device=dev)
+    partial = torch.empty(P, dtype=torch.float64, device=dev)
+    deltas = torch.empty(PER_GPU, P, dtype=torch.float32, device=dev)
+    weights_coef = torch.full((PER_GPU,), 1.0 / n_part, dtype=torch.float64, device=dev)
+    one = torch.ones(1, dtype=torch.float64, device=dev)
+
+    def plan_round(r, selector, now):
+        who = selector.sample(ids, n_part)
+        rep, _ = sim.run(who, cfg, t0=now, round_index=r, want_trace=False)
+        mine = who[rank * PER_GPU:(rank + 1) * PER_GPU]
+        wl = [by_id[c].workload for c in mine]
+        seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
+        total = float(sum(float(w.num_samples) for w in (by_id[c].workload for c in who)))
+        coef = [float(w.num_samples) / total for w in wl]
+        return rep, mine, wl, seeds, coef
+
+    def device_round(mine_desc, coef_dev, correct):
+        """train -> FedAvg partial -> (all-reduce) -> apply -> sharded accuracy; returns train events."""
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        _abi.check(_abi.lib.fedhc_local_train(mine_desc.data_ptr(), PER_GPU, params.data_ptr(), F, C, BATCH,
+                                              stream_ptr()))
+        ev1.record()
+        if world == 1:
+            fedavg_device(deltas, coef_dev, params, params)
+        else:
+            fedavg_device(deltas, coef_dev, None, partial)
+            dist.all_reduce(partial)
+            fedavg_device(partial.view(1, -1), one, params, params)
+        _abi.check(_abi.lib.fedhc_eval(fed.x_test.data_ptr(), fed.y_test.data_ptr(), fed.n_test, F, C,
+                                       params.data_ptr(), correct.data_ptr(), stream_ptr()))
+        if world > 1:
+            dist.all_reduce(correct)
+        return ev0, ev1
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- value: device-resident rounds ----------------
+    total_rounds = args.warmup + args.steps
+    selector = random.Random(f"{cfg.seed}:selection")
+    plans, now = [], 0.0
+    for r in range(total_rounds):
+        rep, mine, wl, seeds, coef = plan_round(r, selector, now)
+        now += rep.makespan
+        packed, meta = fed.plan(mine, wl, seeds)
+        perm_dev = torch.from_numpy(packed).to(dev)
+        fed._perm_dev = perm_dev
+        desc = fed.descriptors(mine, meta, LR, deltas)
+        plans.append((perm_dev, desc, torch.tensor(coef, dtype=torch.float64, device=dev)))
+    counts = torch.zeros(total_rounds, dtype=torch.int64, device=dev)
+    for r in range(args.warmup):
+        device_round(plans[r][1], plans[r][2], counts[r:r + 1])
+    barrier()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    train_events = []
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        t_start.record()
+        for r in range(args.warmup, total_rounds):
+            train_events.append(device_round(plans[r][1], plans[r][2], counts[r:r + 1]))
+        t_end.record()
+        barrier()
+    ms = t_start.elapsed_time(t_end)
+    train_ms = float(np.mean([a.elapsed_time(b) for a, b in train_events]))
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    accuracy_last = counts[-1].item() / N_TEST
+    launches_per_round = 3 + (1 if world > 1 else 0)  # train, FedAvg (+apply), eval
+    total_steps = args.steps * n_part * steps_per_client
+    value = total_steps / (ms / 1e3)
+
+    # ---------------- e2e: public round API with host buffers ----------------
+    selector = random.Random(f"{cfg.seed}:selection")
+    params.zero_()
+    now = 0.0
+    correct = torch.zeros(1, dtype=torch.int64, device=dev)
+    h2d = d2h = 0
+
+    def e2e_round(r):
+        nonlocal now, h2d, d2h
+        rep, mine, wl, seeds, coef = plan_round(r, selector, now)
+        now += rep.makespan
+        packed, meta = fed.plan(mine, wl, seeds)
+        fed.upload_plan(packed)
+        desc = fed.descriptors(mine, meta, LR, deltas)
+        coef_dev = torch.tensor(coef, dtype=torch.float64).pin_memory().to(dev, non_blocking=True)
+        correct.zero_()
+        device_round(desc, coef_dev, correct)
+        acc = correct.item() / N_TEST  # D2H of the round's result
+        h2d = packed.nbytes + desc.numel() + coef_dev.numel() * 8
+        d2h = 8
+        return acc
+
+    for r in range(args.warmup):
+        e2e_round(r)
+    barrier()
+    e0 = time.perf_counter()
+    for r in range(args.warmup, total_rounds):
+        e2e_round(r)
+    barrier()
+    e2e_s = time.perf_counter() - e0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = total_steps / e2e_s
+
+    # ---------------- roofline of the dominant kernel (train) ----------------
+    from benchlib import roofline_entry
+    bytes_per_launch = PER_GPU * steps_per_client * BATCH * (4 * F + 8) + PER_GPU * P * 12
+    roof = roofline_entry(bytes_per_launch, train_ms, ROOT)
+
+    result = {
+        "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
+        "value": value,
+        "unit": "client-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32 (3xTF32 tensor-core products, fp32 SGD state, fp64 FedAvg)",
+        "data": "synthetic (on-device Gaussian class clusters, reference generator shape)",
+        "config": workload_config(world),
+        "rounds_per_sec": args.steps / (ms / 1e3),
+        "train_kernel_ms": train_ms,
+        "accuracy_last_round": accuracy_last,
+        "e2e": {"value": e2e_value, "unit": "client-steps/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "rounds_per_sec": args.steps / e2e_s},
+        "roofline": roof,
+        "clocks": clocks.summary(),
+        "gpu_launches": launches_per_round * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _, _ = cpu_reference(args.cpu_seconds, warmup=1)
+        result["cpu_baseline"] = {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port",
+                                  "sample": sample}
+    if dist is not None:
+        dist.destroy_process_group()
+    return result
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
+    if rank != 0:
+        return None
+    v, cores, sample, rounds, secs = cpu_reference(0.0, rounds=args.steps, warmup=args.warmup)
+    return {
+        "impl": "reference",
+        "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
+        "value": v,
+        "unit": "client-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": secs / max(rounds, 1) * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp64 (reference numpy)",
+        "data": "synthetic",
+        "config": workload_config(1),
+        "cpu_baseline": {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "client-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        pass  # torchrun decides the world; --gpus is informational
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

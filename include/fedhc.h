@@ -1,0 +1,192 @@
+/*
+ * fedhc.h -- C ABI of the B200-native FedHC round hot path (libfedhc.so).
+ *
+ * Drop-in boundary for the reference's Python FL-math and round API
+ * (/root/reference/pkg/src/fedsim).  The reference
+ * has no FFI of its own: its boundary is the Python function API of
+ * fl_core.py and engine.py.  Each entry point below replaces one of those
+ * functions (cited per function); the Python package
+ * `paper_2305_15668_b200` binds them with ctypes (INTEGRATION.md shows the
+ * binding a fedsim maintainer would add).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device pointers
+ *    of the current device; "host" pointers are CPU memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Every function returns an int status (FEDHC_OK == 0).  On failure
+ *    fedhc_last_error() returns a thread-local message; the Python layer maps
+ *    the status to the reference's exception type with that message.
+ *  - No entry point allocates device memory on the hot path: all buffers
+ *    are caller-owned.  Kernels are asynchronous on `stream`.
+ *  - Parameter layout is the reference's flat vector
+ *    [W (n_features x n_classes, row-major) ; b (n_classes)]
+ *    (fl_core.py:121-129), P = F*C + C.
+ */
+#ifndef FEDHC_H_
+#define FEDHC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define FEDHC_OK 0
+#define FEDHC_ERR_VALUE 1        /* -> ValueError (bad shapes / arguments)   */
+#define FEDHC_ERR_AGGREGATION 2  /* -> AggregationError (errors.py:12-13)     */
+#define FEDHC_ERR_CONFIG 3       /* -> ConfigError (errors.py:4-5)            */
+#define FEDHC_ERR_CUDA 4         /* CUDA runtime / driver failure             */
+#define FEDHC_ERR_UNSUPPORTED 5  /* shape outside the compiled kernels        */
+#define FEDHC_ERR_RUNTIME 6      /* -> RuntimeError (engine.py:216, :224)     */
+
+const char* fedhc_last_error(void);
+int fedhc_version(void);
+/* SM count / compute capability of `device` (host query, no kernel). */
+int fedhc_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- local training: fl_core.local_train (fl_core.py:163-194) ----------- */
+/*
+ * One descriptor per client.  The batch plan is the reference's: batch s of
+ * the local epoch visits rows perm[e*n_rows + j*batch_size : ... + nb] with
+ * bpe = ceil(n_rows / batch_size), e = s / bpe, j = s % bpe,
+ * nb = min(batch_size, n_rows - j*batch_size)   (fl_core.py:180-189),
+ * i.e. `perm` is the concatenation of the PCG64 permutations the reference
+ * draws (one per started epoch).  Math: fp32 storage, 3xTF32 tensor-core
+ * products (fp32-accurate), fp32 SGD state; delta = W_final - W_initial.
+ */
+typedef struct fedhc_client {
+  const float* x;        /* dev [n_rows, n_features] fp32 row-major          */
+  const int32_t* y;      /* dev [n_rows] class ids in [0, n_classes)           */
+  const int32_t* perm;   /* dev [n_epochs * n_rows] concatenated permutations  */
+  int32_t n_rows;        /* shard length (0 -> zero delta, fl_core.py:178)     */
+  int32_t n_batches;     /* ceil(num_samples / batch_size) (fl_core.py:180)    */
+  int32_t batch_size;    /* >= 1                                               */
+  float lr;              /* SGD step (fl_core.py:193)                          */
+  float* delta;          /* dev [P] fp32 output                                */
+} fedhc_client;
+
+/* Batched local SGD for n_clients clients that all start from `params`
+ * (dev fp64 [P], the round-start model, engine.py:336-347).  `clients` is a
+ * DEVICE array of descriptors.  `max_batch` = max batch_size over clients. */
+int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params,
+                      int n_features, int n_classes, int max_batch, void* stream);
+
+/* ---- loss_and_grad: fl_core.loss_and_grad (fl_core.py:138-151) ---------- */
+/* fp64 throughout.  x dev fp64 [n, F]; y dev int32 [n]; params dev fp64 [P];
+ * grad dev fp64 [P] out; loss dev fp64 [1] out (mean CE, +1e-300 guard);
+ * workspace dev, >= n * n_classes * 8 bytes. */
+int fedhc_loss_and_grad(const double* x, const int32_t* y, int n, int n_features, int n_classes,
+                        const double* params, double* grad, double* loss, double* workspace,
+                        void* stream);
+
+/* ---- FedAvg: fl_core.fedavg (fl_core.py:197-218) ------------------------ */
+/* Host helper: validates weights exactly like fl_core.py:201-209 and writes
+ * coef[i] = w[i] / total with total the CPython>=3.12 float sum of w
+ * (Neumaier-compensated, as `float(sum(weights))` evaluates for a list of
+ * Python floats). */
+int fedhc_fedavg_coefficients(const double* weights, int n, double* coef_out);
+
+#define FEDHC_F32 0
+#define FEDHC_F64 1
+/* out[p] = base[p] + sum_k coef[k] * delta_k[p], accumulated in fp64 in k
+ * order with separately rounded multiply and add -- bit-identical to the
+ * reference's `out += (w/total) * d` loop for fp64 deltas.  Deltas are
+ * either a DEVICE array of K device pointers (`deltas` != NULL) or one
+ * packed dev buffer `packed` with row stride `ld` elements.  `base` may be
+ * NULL (sum starts at +0.0; used for per-GPU partial sums).  coef is a dev
+ * fp64 [K] array.  out may alias base. */
+int fedhc_fedavg(const void* const* deltas, const void* packed, int64_t ld, int dtype,
+                 const double* coef, int n_deltas, const double* base, double* out,
+                 int64_t n, void* stream);
+
+/* ---- evaluate_accuracy (fl_core.py:154-160) ----------------------------- */
+/* x dev fp32 [n, F]; y dev int32 [n]; params dev fp64 [P].
+ * *correct (dev uint64) += number of rows whose first-max argmax == label. */
+int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
+               const double* params, unsigned long long* correct, void* stream);
+
+/* ---- round DES: engine.run_round (engine.py:53-230) --------------------- */
+/* Host-only discrete-event simulation of one round under capped max-min
+ * sharing, with the reference's executor manager (executor_manager.py) and
+ * schedulers (scheduler.py).  Bit-identical event times to the reference
+ * (same fp64 operation order).  See fedhc_des_* below. */
+typedef struct fedhc_des_client {
+  int32_t budget;              /* resource_budget, [1,100] (profiles.py:60)       */
+  int32_t num_samples;         /* WorkloadSpec fields (profiles.py:19-39)          */
+  int32_t batch_size;
+  int32_t model_layers;
+  int32_t seq_len;
+  double extra_model_factor;
+  int32_t n_phases;            /* demand profile (profiles.py:42-54)               */
+  const double* phase_frac;    /* host [n_phases] work fractions                   */
+  const double* phase_demand;  /* host [n_phases] demands in (0,100]               */
+} fedhc_des_client;
+
+typedef struct fedhc_des_config { /* FleetConfig (profiles.py:76-93) */
+  double theta;
+  int32_t max_executors;
+  int32_t scheduler;           /* 0 = resource-aware, 1 = greedy                  */
+  int32_t dynamic_parallelism; /* bool                                            */
+  double alpha, beta;          /* cost coefficients                               */
+  double launch_latency, terminate_latency, upload_latency;
+} fedhc_des_config;
+
+/* Trace event kinds (metrics.py:21-28 plus Alloc / Instruction). */
+#define FEDHC_EV_LAUNCHED 0
+#define FEDHC_EV_PHASE 1
+#define FEDHC_EV_TRAINED 2
+#define FEDHC_EV_UPLOADED 3
+#define FEDHC_EV_SLOT_FREED 4
+#define FEDHC_EV_ROUND_COMPLETE 5
+#define FEDHC_EV_ALLOC 6
+#define FEDHC_EV_INSTRUCTION 7
+
+typedef struct fedhc_des_event {
+  double t;
+  int32_t kind;       /* FEDHC_EV_*                                            */
+  int32_t client;     /* participant index (order given), -1 if none           */
+  int32_t executor;   /* -1 if none                                            */
+  int32_t aux;        /* phase (PHASE), instruction 0..3 (INSTRUCTION), round   */
+  double budget;      /* LAUNCHED / TRAINED / UPLOADED                          */
+  int64_t alloc_off;  /* ALLOC: offset into alloc arrays                        */
+  int32_t alloc_len;  /* ALLOC: number of (client, share) pairs                 */
+  int32_t pad_;
+} fedhc_des_event;
+
+typedef struct fedhc_des_report { /* metrics.RoundReport (metrics.py:31-53) */
+  double makespan, utilization, vacancy_area, throughput;
+  int32_t degenerate;
+  int32_t n_events;       /* trace length (if recorded)                       */
+  int64_t n_alloc_pairs;  /* total alloc pairs (if recorded)                  */
+} fedhc_des_report;
+
+/* Opaque simulator handle (reusable across rounds; owns trace storage). */
+typedef struct fedhc_des fedhc_des;
+fedhc_des* fedhc_des_create(void);
+void fedhc_des_destroy(fedhc_des* sim);
+/* Simulate one round.  `order` = participant indices into `clients` in
+ * arrival order; `client_ids` = their string ids (ties break on byte order,
+ * engine.py:171).  Per-participant outputs (host arrays of length n_order):
+ * start (ClientLaunched time), end (ModelUploaded time).  record_trace != 0
+ * keeps the full event list, readable with fedhc_des_trace(). */
+int fedhc_des_run_round(fedhc_des* sim, const fedhc_des_client* clients, const char* const* client_ids,
+                        const int32_t* order, int n_order, const fedhc_des_config* cfg, double t0,
+                        int round_index, int record_trace, double* start_out, double* end_out,
+                        fedhc_des_report* report);
+/* Borrow the recorded trace: events[n_events], alloc_client[n_alloc_pairs]
+ * (participant indices) and alloc_share[n_alloc_pairs]; parallelism timeline
+ * (time, count) pairs.  Valid until the next run on this handle. */
+int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const int32_t** alloc_client,
+                    const double** alloc_share, const double** par_t, const int32_t** par_n, int* n_par);
+
+/* Standalone cost-model helpers (cost_model.py:33-87), for the API layer. */
+double fedhc_work_units(int num_samples, int batch_size, int model_layers, int seq_len,
+                        double extra_model_factor, double alpha, double beta);
+int fedhc_maxmin_allocate(const double* caps, const double* demands, int n, double capacity,
+                          double* alloc_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEDHC_H_ */

@@ -1,0 +1,153 @@
+"""ctypes binding of libfedhc.so (include/fedhc.h).
+
+The library is built in-tree by ``paper_2305_15668_b200/build.py`` (called
+from ``__graft_entry__.build()``).  There is deliberately no fallback: if the
+library is missing, importing the compute API raises ``ImportError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import AggregationError, ConfigError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfedhc.so")
+
+OK, ERR_VALUE, ERR_AGGREGATION, ERR_CONFIG, ERR_CUDA, ERR_UNSUPPORTED, ERR_RUNTIME = range(7)
+F32, F64 = 0, 1
+
+EV_LAUNCHED, EV_PHASE, EV_TRAINED, EV_UPLOADED, EV_SLOT_FREED, EV_ROUND_COMPLETE, EV_ALLOC, EV_INSTRUCTION = range(8)
+
+
+class FedhcCudaError(RuntimeError):
+    """A CUDA runtime failure inside libfedhc."""
+
+
+class Client(C.Structure):
+    _fields_ = [
+        ("x", C.c_void_p),
+        ("y", C.c_void_p),
+        ("perm", C.c_void_p),
+        ("n_rows", C.c_int32),
+        ("n_batches", C.c_int32),
+        ("batch_size", C.c_int32),
+        ("lr", C.c_float),
+        ("delta", C.c_void_p),
+    ]
+
+
+class DesClient(C.Structure):
+    _fields_ = [
+        ("budget", C.c_int32),
+        ("num_samples", C.c_int32),
+        ("batch_size", C.c_int32),
+        ("model_layers", C.c_int32),
+        ("seq_len", C.c_int32),
+        ("extra_model_factor", C.c_double),
+        ("n_phases", C.c_int32),
+        ("phase_frac", C.POINTER(C.c_double)),
+        ("phase_demand", C.POINTER(C.c_double)),
+    ]
+
+
+class DesConfig(C.Structure):
+    _fields_ = [
+        ("theta", C.c_double),
+        ("max_executors", C.c_int32),
+        ("scheduler", C.c_int32),
+        ("dynamic_parallelism", C.c_int32),
+        ("alpha", C.c_double),
+        ("beta", C.c_double),
+        ("launch_latency", C.c_double),
+        ("terminate_latency", C.c_double),
+        ("upload_latency", C.c_double),
+    ]
+
+
+class DesEvent(C.Structure):
+    _fields_ = [
+        ("t", C.c_double),
+        ("kind", C.c_int32),
+        ("client", C.c_int32),
+        ("executor", C.c_int32),
+        ("aux", C.c_int32),
+        ("budget", C.c_double),
+        ("alloc_off", C.c_int64),
+        ("alloc_len", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
+
+
+class DesReport(C.Structure):
+    _fields_ = [
+        ("makespan", C.c_double),
+        ("utilization", C.c_double),
+        ("vacancy_area", C.c_double),
+        ("throughput", C.c_double),
+        ("degenerate", C.c_int32),
+        ("n_events", C.c_int32),
+        ("n_alloc_pairs", C.c_int64),
+    ]
+
+
+_vp, _i, _i64, _d, _dp = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.POINTER(C.c_double)
+
+SIGNATURES = {
+    "fedhc_last_error": (C.c_char_p, []),
+    "fedhc_version": (_i, []),
+    "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
+    "fedhc_loss_and_grad": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "fedhc_fedavg_coefficients": (_i, [_dp, _i, _dp]),
+    "fedhc_fedavg": (_i, [_vp, _vp, _i64, _i, _vp, _i, _vp, _vp, _i64, _vp]),
+    "fedhc_eval": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]),
+    "fedhc_des_create": (_vp, []),
+    "fedhc_des_destroy": (None, [_vp]),
+    "fedhc_des_run_round": (
+        _i,
+        [_vp, C.POINTER(DesClient), C.POINTER(C.c_char_p), C.POINTER(C.c_int32), _i, C.POINTER(DesConfig), _d, _i,
+         _i, _dp, _dp, C.POINTER(DesReport)],
+    ),
+    "fedhc_des_trace": (
+        _i,
+        [_vp, C.POINTER(C.POINTER(DesEvent)), C.POINTER(C.POINTER(C.c_int32)), C.POINTER(_dp), C.POINTER(_dp),
+         C.POINTER(C.POINTER(C.c_int32)), C.POINTER(_i)],
+    ),
+    "fedhc_work_units": (_d, [_i, _i, _i, _i, _d, _d, _d]),
+    "fedhc_maxmin_allocate": (_i, [_dp, _dp, _i, _d, _dp]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libfedhc.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    """Map a libfedhc status to the reference's exception types."""
+    if status == OK:
+        return
+    msg = lib.fedhc_last_error().decode(errors="replace")
+    if status == ERR_AGGREGATION:
+        raise AggregationError(msg)
+    if status == ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == ERR_VALUE:
+        raise ValueError(msg)
+    if status == ERR_RUNTIME:
+        raise RuntimeError(msg)
+    if status == ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise FedhcCudaError(msg)

@@ -1,0 +1,153 @@
+// Sample-weighted FedAvg -- fl_core.fedavg (fl_core.py:197-218).
+//
+// out[p] = base[p] + sum_k coef[k] * delta_k[p]
+//
+// HBM-bound streaming reduction.  Each thread owns 4 consecutive elements
+// for the whole K loop, so every delta is read exactly once (16-byte loads
+// for fp32, 2x16-byte for fp64), the base once and the output written once:
+// algorithmic traffic (K * esize + 16) * n bytes.  Coefficients and delta
+// pointers are staged through shared memory in blocks of kKTile.  The
+// accumulation is fp64, in list order, with separately rounded multiply and
+// add (no FMA contraction) -- the exact operation sequence of the
+// reference's `out += (w / total) * d` loop, so fp64 inputs give
+// bit-identical results.
+#include "common.cuh"
+
+namespace fedhc {
+
+constexpr int kAvgThreads = 256;
+constexpr int kKTile = 512;
+constexpr int kUnroll = 8;
+
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  static __device__ __forceinline__ void load(const float* p, double (&v)[4]) {
+    const float4 q = __ldcs(reinterpret_cast<const float4*>(p));  // streaming: evict-first
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+  static __device__ __forceinline__ void load_tail(const float* p, int m, double (&v)[4]) {
+    for (int i = 0; i < 4; ++i) v[i] = i < m ? static_cast<double>(p[i]) : 0.0;
+  }
+};
+template <>
+struct Vec4<double> {
+  static __device__ __forceinline__ void load(const double* p, double (&v)[4]) {
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  static __device__ __forceinline__ void load_tail(const double* p, int m, double (&v)[4]) {
+    for (int i = 0; i < 4; ++i) v[i] = i < m ? p[i] : 0.0;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kAvgThreads)
+    fedavg_kernel(const T* const* __restrict__ ptrs, const T* __restrict__ packed, int64_t ld,
+                  const double* __restrict__ coef, int K, const double* base, double* out, int64_t n) {
+  __shared__ double s_coef[kKTile];
+  __shared__ const T* s_ptr[kKTile];
+  const int64_t p0 = ((int64_t)blockIdx.x * kAvgThreads + threadIdx.x) * 4;
+  const bool active = p0 < n;
+  const int m = active ? static_cast<int>(n - p0 < 4 ? n - p0 : 4) : 0;
+  const bool vec = (m == 4);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (base != nullptr && active) {
+    for (int i = 0; i < m; ++i) acc[i] = base[p0 + i];
+  }
+  for (int k0 = 0; k0 < K; k0 += kKTile) {
+    const int kt = min(kKTile, K - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kt; i += kAvgThreads) {
+      s_coef[i] = coef[k0 + i];
+      s_ptr[i] = ptrs != nullptr ? ptrs[k0 + i] : packed + (int64_t)(k0 + i) * ld;
+    }
+    __syncthreads();
+    if (!active) continue;
+    int k = 0;
+    if (vec) {
+      for (; k + kUnroll <= kt; k += kUnroll) {
+        double v[kUnroll][4];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) Vec4<T>::load(s_ptr[k + u] + p0, v[u]);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const double c = s_coef[k + u];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(c, v[u][i]));
+        }
+      }
+    }
+    for (; k < kt; ++k) {
+      double v[4];
+      if (vec)
+        Vec4<T>::load(s_ptr[k] + p0, v);
+      else
+        Vec4<T>::load_tail(s_ptr[k] + p0, m, v);
+      const double c = s_coef[k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(c, v[i]));
+    }
+  }
+  if (!active) return;
+  if (vec) {
+    reinterpret_cast<double2*>(out + p0)[0] = make_double2(acc[0], acc[1]);
+    reinterpret_cast<double2*>(out + p0)[1] = make_double2(acc[2], acc[3]);
+  } else {
+    for (int i = 0; i < m; ++i) out[p0 + i] = acc[i];
+  }
+}
+
+}  // namespace fedhc
+
+using namespace fedhc;
+
+extern "C" int fedhc_fedavg_coefficients(const double* weights, int n, double* coef_out) {
+  // fl_core.py:201-209 (shape checks are the caller's: it owns the arrays)
+  if (n <= 0) return fail(FEDHC_ERR_AGGREGATION, "no deltas to aggregate");
+  for (int i = 0; i < n; ++i)
+    if (weights[i] < 0) return fail(FEDHC_ERR_AGGREGATION, "weights must be non-negative");
+  // CPython >= 3.12 float sum(): Neumaier compensated summation.
+  double s = 0.0, comp = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double x = weights[i];
+    const double t = s + x;
+    if (fabs(s) >= fabs(x))
+      comp += (s - t) + x;
+    else
+      comp += (x - t) + s;
+    s = t;
+  }
+  if (comp != 0.0 && isfinite(comp)) s += comp;
+  if (s == 0.0) return fail(FEDHC_ERR_AGGREGATION, "weights must not all be zero");
+  for (int i = 0; i < n; ++i) coef_out[i] = weights[i] / s;
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_fedavg(const void* const* deltas, const void* packed, int64_t ld, int dtype,
+                            const double* coef, int n_deltas, const double* base, double* out, int64_t n,
+                            void* stream) {
+  if (n_deltas <= 0) return fail(FEDHC_ERR_AGGREGATION, "no deltas to aggregate");
+  if (n < 0) return fail(FEDHC_ERR_VALUE, "fedavg: negative length");
+  if (deltas == nullptr && packed == nullptr) return fail(FEDHC_ERR_VALUE, "fedavg: no delta storage given");
+  if (coef == nullptr || out == nullptr) return fail(FEDHC_ERR_VALUE, "fedavg: null coefficient/output");
+  if (n == 0) return FEDHC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = (n + 4LL * kAvgThreads - 1) / (4LL * kAvgThreads);
+  if (blocks > 0x7fffffffLL) return fail(FEDHC_ERR_UNSUPPORTED, "fedavg: vector too long");
+  if (dtype == FEDHC_F32) {
+    fedavg_kernel<float><<<(unsigned)blocks, kAvgThreads, 0, st>>>(
+        reinterpret_cast<const float* const*>(deltas), static_cast<const float*>(packed), ld, coef, n_deltas, base,
+        out, n);
+  } else if (dtype == FEDHC_F64) {
+    fedavg_kernel<double><<<(unsigned)blocks, kAvgThreads, 0, st>>>(
+        reinterpret_cast<const double* const*>(deltas), static_cast<const double*>(packed), ld, coef, n_deltas,
+        base, out, n);
+  } else {
+    return fail(FEDHC_ERR_VALUE, "fedavg: dtype must be FEDHC_F32 or FEDHC_F64");
+  }
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  return FEDHC_OK;
+}

@@ -1,0 +1,6 @@
+"""Module alias so `from paper_2305_15668_b200.executor_manager import X` works like `from fedsim.executor_manager import X`."""
+
+from .planner import *  # noqa: F401,F403
+from . import planner as _impl
+
+globals().update({k: v for k, v in vars(_impl).items() if not k.startswith("__")})

@@ -1,0 +1,251 @@
+"""Experiment loop with an HBM-resident federation -- drop-in for engine.run_experiment.
+
+`run_experiment` keeps the reference's semantics (engine.py:279-368):
+seeded selection (`random.Random(f"{seed}:selection").sample`), the round
+DES, per-client local SGD from the round-start model, then sync FedAvg or
+async buffered aggregation in (per_client_end, id) order, then accuracy.
+
+What changes is where the work runs.  `DeviceFederation` uploads every
+client's shard and the test set to HBM once; each round then costs
+  host:   selection + native DES + PCG64 batch permutations (the data plan),
+  device: ONE fedhc_local_train launch for all participants (one CTA per
+          client), ONE fedhc_fedavg launch per aggregation and ONE
+          fedhc_eval launch per accuracy point,
+with only the permutations (int32) copied in and the accuracy count copied
+out.  Clients of a round train concurrently because every participant starts
+from the same round-start params (engine.py:336-347).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import random
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from .errors import ConfigError
+from .roundsim import RoundReport, RoundSimulator
+from .spec import ClientProfile, FleetConfig
+from .training import (Dataset, DatasetShard, batch_permutations, check_aggregation, count_correct, device,
+                       fedavg_device, init_params, make_synthetic_dataset, partition_noniid, stable_seed,
+                       stream_ptr)
+
+
+@dataclass
+class TrainParams:
+    enabled: bool = True
+    lr: float = 0.1
+
+
+@dataclass
+class DataParams:
+    features: int = 2
+    classes: int = 4
+    alpha: float = 0.5
+
+
+@dataclass
+class ExperimentReport:
+    rounds: list[RoundReport] = field(default_factory=list)
+    participants: list[list[str]] = field(default_factory=list)
+    accuracy_series: list[tuple[float, float]] = field(default_factory=list)
+    total_time: float = 0.0
+    final_params: np.ndarray | None = None
+
+    def mean_round_time(self) -> float:
+        return sum(r.makespan for r in self.rounds) / len(self.rounds) if self.rounds else 0.0
+
+    def accuracy_at(self, sim_time: float) -> float:
+        acc = 0.0
+        for t, a in self.accuracy_series:
+            if t > sim_time:
+                break
+            acc = a
+        return acc
+
+    def to_json(self) -> str:
+        return json.dumps({"rounds": [r.to_dict() for r in self.rounds], "participants": self.participants,
+                           "accuracy_series": self.accuracy_series, "total_time": self.total_time}, sort_keys=True)
+
+
+class DeviceFederation:
+    """All client shards + the test set resident in HBM; batched round kernels.
+
+    Shards are packed back to back in one fp32 [sum n_i, F] buffer (labels
+    int32); a client's descriptor points at its slice.  Only the round's
+    permutations travel host->device per round (pinned staging).
+    """
+
+    def __init__(self, shards: dict[str, DatasetShard], test: Dataset, n_features: int, n_classes: int):
+        dev = device()
+        self.n_features, self.n_classes = n_features, n_classes
+        self.P = n_features * n_classes + n_classes
+        ids = list(shards)
+        sizes = [len(shards[c].labels) for c in ids]
+        self.offset, off = {}, 0
+        for cid, n in zip(ids, sizes):
+            self.offset[cid] = (off, n)
+            off += n
+        total = max(off, 1)
+        x = np.zeros((total, n_features), dtype=np.float32)
+        y = np.zeros(total, dtype=np.int32)
+        for cid in ids:
+            o, n = self.offset[cid]
+            if n:
+                x[o:o + n] = shards[cid].features
+                y[o:o + n] = shards[cid].labels
+        self.x = torch.from_numpy(x).to(dev)
+        self.y = torch.from_numpy(y).to(dev)
+        self.x_test = torch.from_numpy(np.ascontiguousarray(test.features, dtype=np.float32)).to(dev)
+        self.y_test = torch.from_numpy(np.ascontiguousarray(test.labels, dtype=np.int32)).to(dev)
+        self.n_test = len(test.labels)
+        self._cap = 0
+        self._pinned = None
+        self._perm_dev = None
+
+    @classmethod
+    def from_arrays(cls, x: torch.Tensor, y: torch.Tensor, offsets: dict[str, tuple[int, int]],
+                    x_test: torch.Tensor, y_test: torch.Tensor, n_classes: int) -> "DeviceFederation":
+        """Wrap already-resident device tensors (e.g. on-device synthetic data)."""
+        self = cls.__new__(cls)
+        self.n_features, self.n_classes = int(x.shape[1]), n_classes
+        self.P = self.n_features * n_classes + n_classes
+        self.x, self.y, self.offset = x, y, dict(offsets)
+        self.x_test, self.y_test, self.n_test = x_test, y_test, int(y_test.shape[0])
+        self._cap, self._pinned, self._perm_dev = 0, None, None
+        return self
+
+    # ---- per-round plan (host) ------------------------------------------
+    def plan(self, participants: list[str], workloads, seeds) -> tuple[np.ndarray, list[tuple[int, int, int, int]]]:
+        """PCG64 batch permutations for every participant, packed (int32)."""
+        chunks, meta, at = [], [], 0
+        for cid, wl, sd in zip(participants, workloads, seeds):
+            _, n = self.offset[cid]
+            perm = batch_permutations(n, wl.num_samples, wl.batch_size, sd)
+            chunks.append(perm)
+            meta.append((at, n, math.ceil(wl.num_samples / wl.batch_size), wl.batch_size))
+            at += perm.shape[0]
+        packed = np.concatenate(chunks) if chunks else np.zeros(0, np.int32)
+        return packed, meta
+
+    def upload_plan(self, packed: np.ndarray) -> torch.Tensor:
+        n = packed.shape[0]
+        if getattr(self, "_copied", None) is not None:
+            self._copied.synchronize()  # previous round's H2D must finish before the pinned buffer is reused
+        if n > self._cap:
+            self._cap = max(n, 2 * self._cap)
+            self._pinned = torch.empty(self._cap, dtype=torch.int32, pin_memory=True)
+            self._perm_dev = torch.empty(self._cap, dtype=torch.int32, device=self.x.device)
+        if n:
+            self._pinned[:n].numpy()[:] = packed
+            self._perm_dev[:n].copy_(self._pinned[:n], non_blocking=True)
+            self._copied = torch.cuda.Event()
+            self._copied.record()
+        return self._perm_dev
+
+    def descriptors(self, participants, meta, lr: float, deltas: torch.Tensor) -> torch.Tensor:
+        descs = (_abi.Client * max(len(participants), 1))()
+        xb, yb, pb = self.x.data_ptr(), self.y.data_ptr(), self._perm_dev.data_ptr() if self._perm_dev is not None \
+            else 0
+        F = self.n_features
+        for i, (cid, (at, n, steps, bs)) in enumerate(zip(participants, meta)):
+            o, _ = self.offset[cid]
+            descs[i] = _abi.Client(xb + o * F * 4, yb + o * 4, pb + at * 4, n, steps, bs, float(lr),
+                                   deltas[i].data_ptr())
+        raw = torch.frombuffer(bytearray(descs), dtype=torch.uint8).pin_memory()
+        return raw.to(self.x.device, non_blocking=True)
+
+    # ---- device work --------------------------------------------------
+    def train(self, params: torch.Tensor, participants: list[str], workloads, lr: float, seeds,
+              deltas: torch.Tensor | None = None) -> torch.Tensor:
+        """Local SGD for all participants in one launch; returns fp32 deltas [K, P]."""
+        k = len(participants)
+        if deltas is None:
+            deltas = torch.empty((k, self.P), dtype=torch.float32, device=self.x.device)
+        packed, meta = self.plan(participants, workloads, seeds)
+        self.upload_plan(packed)
+        d_desc = self.descriptors(participants, meta, lr, deltas)
+        max_batch = max((wl.batch_size for wl in workloads), default=1)
+        _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr(), k, params.data_ptr(), self.n_features,
+                                              self.n_classes, max_batch, stream_ptr()))
+        self._keepalive = d_desc
+        return deltas
+
+    def aggregate(self, params: torch.Tensor, deltas: torch.Tensor, weights: list[float],
+                  rows: list[int] | None = None) -> torch.Tensor:
+        """params <- params + sum_i (w_i / sum w) * deltas[rows[i]] (fp64, list order), in place."""
+        sel = deltas if rows is None else deltas[rows]
+        total = check_aggregation(sel, weights, params.shape)
+        coef = torch.tensor([w / total for w in weights], dtype=torch.float64).pin_memory().to(
+            params.device, non_blocking=True)
+        fedavg_device(sel, coef, params, params)
+        return params
+
+    def correct(self, params: torch.Tensor) -> int:
+        if self.n_test == 0:
+            return 0
+        return count_correct(self.x_test, self.y_test, params, self.n_classes)
+
+    def accuracy(self, params: torch.Tensor) -> float:
+        return 0.0 if self.n_test == 0 else self.correct(params) / self.n_test
+
+
+def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParams | None = None,
+                   train: TrainParams | None = None, trace: list[dict] | None = None) -> ExperimentReport:
+    """cfg.rounds seeded rounds: selection -> native DES -> batched GPU training -> FedAvg -> accuracy."""
+    cfg.validate(fleet_size=len(fleet))
+    if cfg.rounds < 1:
+        raise ConfigError("rounds must be >= 1")
+    data = data or DataParams()
+    train = train or TrainParams(enabled=False)
+    by_id = {p.client_id: p for p in fleet}
+    if len(by_id) != len(fleet):
+        raise ConfigError("duplicate client ids in fleet")
+    ids = sorted(by_id)
+    selector = random.Random(f"{cfg.seed}:selection")
+    sim = RoundSimulator(by_id)
+
+    fed = params = None
+    if train.enabled:
+        n_total = sum(p.workload.num_samples for p in fleet)
+        train_ds, test = make_synthetic_dataset(data.features, data.classes, max(math.ceil(n_total / 0.8), 10),
+                                                stable_seed("data", cfg.seed))
+        shards = partition_noniid(train_ds, [(p.client_id, p.workload.num_samples) for p in fleet], data.alpha,
+                                  stable_seed("partition", cfg.seed))
+        fed = DeviceFederation(shards, test, data.features, data.classes)
+        params = torch.from_numpy(init_params(data.features, data.classes)).to(device())
+
+    report = ExperimentReport()
+    now = 0.0
+    for r in range(cfg.rounds):
+        who = selector.sample(ids, cfg.participants_per_round)
+        rep, seg = sim.run(who, cfg, t0=now, round_index=r, want_trace=trace is not None)
+        if trace is not None:
+            trace.extend(seg)
+        report.rounds.append(rep)
+        report.participants.append(list(who))
+        round_end = now + rep.makespan
+        if fed is not None:
+            workloads = [by_id[c].workload for c in who]
+            seeds = [stable_seed("train", cfg.seed, r, c) for c in who]
+            deltas = fed.train(params, who, workloads, train.lr, seeds)
+            weights = [float(w.num_samples) for w in workloads]
+            if cfg.aggregation == "sync":
+                fed.aggregate(params, deltas, weights)
+                report.accuracy_series.append((round_end, fed.accuracy(params)))
+            else:
+                ends = [rep.per_client_end[c] for c in who]
+                order = sorted(range(len(who)), key=lambda i: (ends[i], who[i]))
+                for k in range(0, len(order), cfg.async_buffer):
+                    chunk = order[k:k + cfg.async_buffer]
+                    fed.aggregate(params, deltas, [weights[i] for i in chunk], rows=chunk)
+                    report.accuracy_series.append((ends[chunk[-1]], fed.accuracy(params)))
+        now = round_end
+    report.total_time = now
+    report.final_params = params.cpu().numpy() if params is not None else None
+    return report

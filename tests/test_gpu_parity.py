@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle and the
+reference goldens.
+
+Tolerances (north_star): aggregated weights max-abs <= 1e-4 x max|ref|
+after a round (fp32 storage, 3xTF32 products; observed ~1e-6); FedAvg and
+loss_and_grad are fp64 (FedAvg bit-exact for fp64 deltas); accuracy within
+2 test rows of the oracle (argmax near-ties can flip under fp32 logits).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import flmath as fm
+from oracle import orchestration as oc
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-4
+
+
+def rel_err(got, want):
+    scale = max(np.max(np.abs(want)), 1e-30)
+    return float(np.max(np.abs(np.asarray(got) - np.asarray(want))) / scale)
+
+
+@pytest.fixture(scope="module")
+def fh():
+    import torch
+    torch.cuda.set_device(0)
+    import paper_2305_15668_b200 as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def tr(fh):
+    from paper_2305_15668_b200 import training
+    return training
+
+
+FL = np.load(os.path.join(GOLDEN, "flcore.npz"))
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_local_train_golden_cases(tr, i):
+    F, C, n, ns, b, lr = FL["lt_cases"][i]
+    F, C, n, ns, b = int(F), int(C), int(n), int(ns), int(b)
+    sd = str(FL["lt_seeds"][i])
+    seed = int(sd) if sd.lstrip("-").isdigit() else sd
+    shard = tr.DatasetShard("a", FL[f"lt{i}_x"], FL[f"lt{i}_y"])
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    d = tr.local_train(FL[f"lt{i}_p"], shard, WorkloadSpec(ns, b), float(lr), C, seed=seed)
+    want = FL[f"lt{i}_d"]
+    if n == 0:
+        assert np.all(d == 0)
+    else:
+        assert rel_err(d, want) <= REL
+
+
+@pytest.mark.parametrize("F,C,n,ns,b", [
+    (784, 10, 640, 640, 64),     # FEMNIST-shaped, fast path (NT=2)
+    (784, 10, 300, 1000, 64),    # reshuffles + ragged batch before each reshuffle
+    (784, 10, 100, 100, 32),     # ragged last batch (100 = 3*32 + 4)
+    (784, 32, 256, 256, 64),     # NT=4 fast path
+    (784, 3, 128, 128, 64),      # NT=1
+    (784, 62, 256, 256, 64),     # FEMNIST 62 classes (generic path)
+    (64, 10, 200, 300, 50),      # small F, B not a multiple of 16
+    (20, 7, 90, 90, 1),          # batch of one row
+    (6, 4, 33, 66, 16),          # F % 4 != 0 -> generic path
+])
+def test_local_train_vs_oracle(tr, F, C, n, ns, b):
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    trn, _ = fm.synthetic(F, C, n * 2 + 10, seed=F + C + n)
+    shard = fm.Shard("a", trn.features[:n], trn.labels[:n])
+    params = np.random.default_rng(1).standard_normal(F * C + C) * 0.05
+    want = fm.local_sgd(params, shard, ns, b, 0.1, C, seed=17)
+    got = tr.local_train(params, tr.DatasetShard("a", shard.features, shard.labels), WorkloadSpec(ns, b), 0.1, C,
+                         seed=17)
+    assert rel_err(got, want) <= REL, rel_err(got, want)
+
+
+def test_local_train_does_not_mutate(tr):
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    trn, _ = fm.synthetic(8, 4, 200, seed=9)
+    params = np.zeros(36)
+    tr.local_train(params, tr.DatasetShard("a", trn.features[:100], trn.labels[:100]), WorkloadSpec(100, 32), 0.1, 4)
+    assert np.array_equal(params, np.zeros(36))
+
+
+def test_local_train_deterministic(tr):
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    trn, _ = fm.synthetic(784, 10, 900, seed=3)
+    sh = tr.DatasetShard("a", trn.features[:700], trn.labels[:700])
+    a = tr.local_train(np.zeros(7850), sh, WorkloadSpec(700, 64), 0.1, 10, seed=5)
+    b = tr.local_train(np.zeros(7850), sh, WorkloadSpec(700, 64), 0.1, 10, seed=5)
+    assert np.array_equal(a, b)
+
+
+def test_fedavg_bit_exact(tr):
+    out = tr.fedavg(list(FL["fa_deltas"]), list(FL["fa_w"]), FL["fa_base"])
+    assert np.array_equal(out, FL["fa_out"])
+    base = np.array([1.0, 1.0])
+    ds = [np.array([2.0, 4.0]), np.array([4.0, 6.0])]
+    assert np.array_equal(tr.fedavg(ds, [1.0, 1.0], base), [4.0, 6.0])
+    assert np.array_equal(tr.fedavg(ds, [3.0, 1.0], base), [3.5, 5.5])
+    rng = np.random.default_rng(4)
+    for n, k in [(1, 1), (3, 2), (4097, 9), (100_003, 37)]:
+        base = rng.standard_normal(n)
+        ds = [rng.standard_normal(n) for _ in range(k)]
+        ws = list(rng.uniform(0.1, 5.0, size=k))
+        assert np.array_equal(tr.fedavg(ds, ws, base), fm.weighted_average(ds, ws, base))
+
+
+def test_fedavg_errors(tr):
+    from paper_2305_15668_b200.errors import AggregationError
+    for ds, ws in [([], []), ([np.zeros(2)], [1.0, 2.0]), ([np.zeros(3)], [1.0]), ([np.zeros(2)], [0.0]),
+                   ([np.zeros(2)], [-1.0])]:
+        with pytest.raises(AggregationError):
+            tr.fedavg(ds, ws, np.zeros(2))
+
+
+def test_fedavg_full_size_vs_torch(tr):
+    """Config-5 scale (P = 25M, K = 8, fp32 deltas): bit-exact vs the same sequence in torch fp64."""
+    import torch
+    P, K = 25_000_000, 8
+    g = torch.Generator(device="cuda").manual_seed(0)
+    deltas = torch.randn(K, P, device="cuda", generator=g, dtype=torch.float32) * 1e-3
+    base = torch.randn(P, device="cuda", generator=g, dtype=torch.float64)
+    w = [float(v) for v in torch.randint(1, 1024, (K,), generator=torch.Generator().manual_seed(0))]
+    total = float(sum(w))
+    coef = torch.tensor([x / total for x in w], dtype=torch.float64, device="cuda")
+    out = torch.empty_like(base)
+    tr.fedavg_device(deltas, coef, base, out)
+    ref = base.clone()
+    for k in range(K):
+        ref += coef[k].item() * deltas[k].double()
+    assert torch.equal(out, ref)
+    # properties: single delta with any weight -> base + delta exactly; zero deltas -> base
+    tr.fedavg_device(deltas[:1], torch.tensor([1.0], dtype=torch.float64, device="cuda"), base, out)
+    assert torch.equal(out, base + deltas[0].double())
+
+
+def test_accuracy_vs_oracle(tr):
+    d = fm.Data(FL["acc_x"], FL["acc_y"], 6)
+    assert tr.evaluate_accuracy(FL["acc_p"], tr.Dataset(d.features, d.labels, 6)) == fm.accuracy(FL["acc_p"], d)
+    trn, tst = fm.synthetic(784, 62, 5000, seed=2)
+    p = np.random.default_rng(0).standard_normal(784 * 62 + 62) * 0.01
+    got = tr.evaluate_accuracy(p, tr.Dataset(tst.features, tst.labels, 62))
+    assert abs(got - fm.accuracy(p, tst)) <= 2 / len(tst.labels)
+    assert tr.evaluate_accuracy(p, tr.Dataset(np.zeros((0, 784)), np.zeros(0, int), 62)) == 0.0
+
+
+def test_loss_and_grad_vs_oracle(tr):
+    loss, grad = tr.loss_and_grad(FL["lg_p"], FL["lg_x"], FL["lg_y"], 4)
+    assert loss == pytest.approx(float(FL["lg_loss"]), rel=1e-12)
+    assert rel_err(grad, FL["lg_grad"]) <= 1e-12
+    rng = np.random.default_rng(1)
+    loss, _ = tr.loss_and_grad(np.zeros(15), rng.standard_normal((50, 2)), rng.integers(0, 5, 50), 5)
+    assert loss == pytest.approx(np.log(5))
+
+
+def test_train_experiments_vs_golden(fh):
+    tz = np.load(os.path.join(GOLDEN, "train_small.npz"))
+    meta = json.loads(str(tz["meta"]))
+    for i, m in enumerate(meta):
+        fleet = fh.generate_fleet(fh.DistributionSpec(**m["fleet"]["spec"]), m["fleet"]["n"], m["fleet"]["seed"])
+        rep = fh.run_experiment(fh.FleetConfig(**m["cfg"]), fleet, fh.DataParams(**m["data"]),
+                                fh.TrainParams(enabled=True, lr=m["lr"]))
+        assert rep.participants == m["participants"]
+        assert rel_err(rep.final_params, tz[f"tr{i}_params"]) <= REL
+        acc = np.array(rep.accuracy_series)
+        want = tz[f"tr{i}_acc"]
+        assert np.array_equal(acc[:, 0], want[:, 0])  # aggregation times: bit-exact DES
+        assert np.max(np.abs(acc[:, 1] - want[:, 1])) <= 0.02
+
+
+@pytest.mark.parametrize("classes", [10, 62])
+def test_femnist_round_vs_golden(fh, classes):
+    g = np.load(os.path.join(GOLDEN, f"round_c{classes}.npz"))
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 15, 30, 40, 50, 65, 80), num_samples=6400,
+                                                  batch_size=64), 10, 1)
+    rep = fh.run_experiment(fh.FleetConfig(participants_per_round=10, rounds=1, seed=1), fleet,
+                            fh.DataParams(features=784, classes=classes, alpha=0.5), fh.TrainParams(True, 0.1))
+    assert rep.participants[0] == list(g["participants"])
+    assert rep.rounds[0].makespan == float(g["makespan"])
+    err = rel_err(rep.final_params, g["params"])
+    assert err <= REL, err
+    assert abs(rep.accuracy_series[0][1] - float(g["acc"][0][1])) <= 2 / 16000
+
+
+def test_batched_round_matches_per_client(fh, tr):
+    """DeviceFederation.train (one launch, many clients) == per-client oracle local_train."""
+    import torch
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    trn, tst = fm.synthetic(784, 10, 6000, seed=11)
+    sizes = [640, 700, 0, 64, 1000, 333]
+    shards, at = {}, 0
+    for i, n in enumerate(sizes):
+        shards[f"c{i}"] = tr.DatasetShard(f"c{i}", trn.features[at:at + n], trn.labels[at:at + n])
+        at += n
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, 10), 784, 10)
+    params = np.random.default_rng(2).standard_normal(7850) * 0.01
+    wl = [WorkloadSpec(n if n else 10, 64) for n in sizes]
+    seeds = [fm.seed_of("train", 1, 0, f"c{i}") for i in range(len(sizes))]
+    p = torch.from_numpy(params).cuda()
+    deltas = fed.train(p, list(shards), wl, 0.1, seeds).cpu().numpy()
+    for i, cid in enumerate(shards):
+        want = fm.local_sgd(params, fm.Shard(cid, shards[cid].features, shards[cid].labels), wl[i].num_samples,
+                            wl[i].batch_size, 0.1, 10, seed=seeds[i])
+        if sizes[i] == 0:
+            assert np.all(deltas[i] == 0)
+        else:
+            assert rel_err(deltas[i], want) <= REL
+
+
+def test_full_size_round_properties(fh):
+    """Bench-size round (100 clients x 6400 x 784): finite deltas, determinism, FedAvg linearity."""
+    import torch
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    K, n, F, C = 100, 6400, 784, 10
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(K * n, F, device="cuda", generator=g)
+    y = torch.randint(0, C, (K * n,), device="cuda", generator=g, dtype=torch.int32)
+    offs = {f"c{i:03d}": (i * n, n) for i in range(K)}
+    fed = DeviceFederation.from_arrays(x, y, offs, x[:1000], y[:1000], C)
+    params = torch.zeros(F * C + C, dtype=torch.float64, device="cuda")
+    wl = [WorkloadSpec(n, 64)] * K
+    seeds = list(range(K))
+    d1 = fed.train(params, list(offs), wl, 0.1, seeds).clone()
+    d2 = fed.train(params, list(offs), wl, 0.1, seeds)
+    assert torch.isfinite(d1).all() and torch.equal(d1, d2)
+    # per-client spot check against the oracle on two clients
+    xs, ys = x[:2 * n].cpu().double().numpy(), y[:2 * n].cpu().numpy().astype(int)
+    for i in range(2):
+        want = fm.local_sgd(np.zeros(F * C + C), fm.Shard("c", xs[i * n:(i + 1) * n], ys[i * n:(i + 1) * n]), n, 64,
+                            0.1, C, seed=seeds[i])
+        assert rel_err(d1[i].cpu().numpy(), want) <= REL
+    fed.aggregate(params, d1, [1.0] * K)
+    mean = d1.double().mean(0)
+    assert torch.allclose(params, mean, rtol=1e-12, atol=1e-15)
