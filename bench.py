@@ -128,9 +128,9 @@ _CPU = {}
 
 def _cpu_worker(args):
     from oracle import flmath as fm
-    i, seed = args
+    i, seed, params = args
     sh = _CPU["shards"][i % len(_CPU["shards"])]
-    return fm.local_sgd(_CPU["params"], sh, N_SAMPLES, BATCH, LR, C, seed=seed)
+    return fm.local_sgd(params, sh, N_SAMPLES, BATCH, LR, C, seed=seed)
 
 
 def cpu_reference(seconds: float, rounds: int | None = None, warmup: int = 0):
@@ -172,7 +172,8 @@ def cpu_reference(seconds: float, rounds: int | None = None, warmup: int = 0):
             t0 = time.perf_counter()
             who = pick.sample(ids, PER_GPU)
             oc.simulate_round(by_id, who, cfg)
-            deltas = pool.map(_cpu_worker, [(i, fm.seed_of("train", 1, r, c)) for i, c in enumerate(who)])
+            base = _CPU["params"]
+            deltas = pool.map(_cpu_worker, [(i, fm.seed_of("train", 1, r, c), base) for i, c in enumerate(who)])
             _CPU["params"] = fm.weighted_average(deltas, [float(N_SAMPLES)] * PER_GPU, _CPU["params"])
             fm.accuracy(_CPU["params"], test)
             dt = time.perf_counter() - t0
@@ -237,7 +238,8 @@ def run_ours(args, rank, world, local_rank):
 
     params = torch.zeros(P, dtype=torch.float64, device=dev)
     partial = torch.empty(P, dtype=torch.float64, device=dev)
-    deltas = torch.empty(PER_GPU, P, dtype=torch.float32, device=dev)
+    from paper_2305_15668_b200.experiment import delta_buffer
+    deltas = delta_buffer(PER_GPU, P, dev)
     weights_coef = torch.full((PER_GPU,), 1.0 / n_part, dtype=torch.float64, device=dev)
     one = torch.ones(1, dtype=torch.float64, device=dev)
 

@@ -28,7 +28,8 @@ struct Vec4<float> {
     v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
   }
   static __device__ __forceinline__ void load_tail(const float* p, int m, double (&v)[4]) {
-    for (int i = 0; i < 4; ++i) v[i] = i < m ? static_cast<double>(p[i]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = i < m ? static_cast<double>(__ldcs(p + i)) : 0.0;
   }
 };
 template <>
@@ -39,7 +40,8 @@ struct Vec4<double> {
     v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
   }
   static __device__ __forceinline__ void load_tail(const double* p, int m, double (&v)[4]) {
-    for (int i = 0; i < 4; ++i) v[i] = i < m ? p[i] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = i < m ? __ldcs(p + i) : 0.0;
   }
 };
 
@@ -52,7 +54,6 @@ __global__ void __launch_bounds__(kAvgThreads)
   const int64_t p0 = ((int64_t)blockIdx.x * kAvgThreads + threadIdx.x) * 4;
   const bool active = p0 < n;
   const int m = active ? static_cast<int>(n - p0 < 4 ? n - p0 : 4) : 0;
-  const bool vec = (m == 4);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (base != nullptr && active) {
     for (int i = 0; i < m; ++i) acc[i] = base[p0 + i];
@@ -60,11 +61,15 @@ __global__ void __launch_bounds__(kAvgThreads)
   for (int k0 = 0; k0 < K; k0 += kKTile) {
     const int kt = min(kKTile, K - k0);
     __syncthreads();
+    int misaligned = 0;
     for (int i = threadIdx.x; i < kt; i += kAvgThreads) {
       s_coef[i] = coef[k0 + i];
-      s_ptr[i] = ptrs != nullptr ? ptrs[k0 + i] : packed + (int64_t)(k0 + i) * ld;
+      const T* ptr = ptrs != nullptr ? ptrs[k0 + i] : packed + (int64_t)(k0 + i) * ld;
+      s_ptr[i] = ptr;
+      misaligned |= (reinterpret_cast<uintptr_t>(ptr) & 15) != 0;
     }
-    __syncthreads();
+    // rows are 16-byte aligned (p0 % 4 == 0) -> 16-byte vector loads, else scalar
+    const bool vec = (__syncthreads_or(misaligned) == 0) && m == 4;
     if (!active) continue;
     int k = 0;
     if (vec) {
@@ -92,11 +97,13 @@ __global__ void __launch_bounds__(kAvgThreads)
     }
   }
   if (!active) return;
-  if (vec) {
+  if (m == 4 && (reinterpret_cast<uintptr_t>(out + p0) & 15) == 0) {
     reinterpret_cast<double2*>(out + p0)[0] = make_double2(acc[0], acc[1]);
     reinterpret_cast<double2*>(out + p0)[1] = make_double2(acc[2], acc[3]);
   } else {
-    for (int i = 0; i < m; ++i) out[p0 + i] = acc[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < m) out[p0 + i] = acc[i];
   }
 }
 

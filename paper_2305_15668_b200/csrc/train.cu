@@ -47,7 +47,7 @@ static bool plan_train(int F, int C, int NT, int max_smem, TrainGeom& g) {
     int off = 0;
     g.off_wt = off;   off = align16(off + Cp * g.Fs * 4);
     g.off_bias = off; off = align16(off + Cp * 4);
-    g.off_gb = off;   off = align16(off + Cp * 4);
+    g.off_gb = off;   off = align16(off + kComputeWarps * Cp * 4);
     g.off_x = off;    off = align16(off + stages * kRows * g.Fs * 4);
     g.off_zp = off;   off = align16(off + kComputeWarps * kRows * Cp * 4);
     g.off_e = off;    off = align16(off + kRows * g.Es * 4);
@@ -86,10 +86,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1)
     const int c = i / Fs, f = i - c * Fs;
     Wt[i] = (c < C && f < F) ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
   }
-  for (int i = tid; i < Cp; i += kTrainThreads) {
-    bias[i] = i < C ? static_cast<float>(params[P_w + i]) : 0.f;
-    gbs[i] = 0.f;
-  }
+  for (int i = tid; i < Cp; i += kTrainThreads) bias[i] = i < C ? static_cast<float>(params[P_w + i]) : 0.f;
   for (int i = tid; i < S * kRows * Fs; i += kTrainThreads) Xb[i] = 0.f;
   for (int i = tid; i < kRows * Es; i += kTrainThreads) E[i] = 0.f;
   fence_proxy_async_smem();
@@ -229,7 +226,7 @@ __global__ void __launch_bounds__(kTrainThreads, 1)
         st = (st + 1 == S) ? 0 : st + 1;
       }
       // ---- end of batch: SGD update W -= lr * G, b -= lr * sum(err) ----
-      if (lane < C) atomicAdd(&gbs[lane], gb_reg);
+      if (lane < C) gbs[warp * Cp + lane] = gb_reg;  // per-warp slot: deterministic order below
       gb_reg = 0.f;
 #pragma unroll
       for (int j = 0; j < UMAX; ++j) {
@@ -246,8 +243,10 @@ __global__ void __launch_bounds__(kTrainThreads, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kComputeWarps * 32));
       if (warp == 0 && lane < C) {
-        bias[lane] -= lr * gbs[lane];
-        gbs[lane] = 0.f;
+        float gsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < kComputeWarps; ++w) gsum += gbs[w * Cp + lane];
+        bias[lane] -= lr * gsum;
       }
     }
   }

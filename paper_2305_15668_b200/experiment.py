@@ -166,7 +166,7 @@ class DeviceFederation:
         """Local SGD for all participants in one launch; returns fp32 deltas [K, P]."""
         k = len(participants)
         if deltas is None:
-            deltas = torch.empty((k, self.P), dtype=torch.float32, device=self.x.device)
+            deltas = delta_buffer(k, self.P, self.x.device)
         packed, meta = self.plan(participants, workloads, seeds)
         self.upload_plan(packed)
         d_desc = self.descriptors(participants, meta, lr, deltas)
@@ -193,6 +193,12 @@ class DeviceFederation:
 
     def accuracy(self, params: torch.Tensor) -> float:
         return 0.0 if self.n_test == 0 else self.correct(params) / self.n_test
+
+
+def delta_buffer(k: int, P: int, dev) -> torch.Tensor:
+    """[k, P] fp32 view with a 16-byte aligned row stride (vectorised FedAvg loads)."""
+    ld = (P + 3) // 4 * 4
+    return torch.empty((k, ld), dtype=torch.float32, device=dev)[:, :P]
 
 
 def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParams | None = None,
