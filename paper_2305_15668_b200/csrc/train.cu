@@ -385,6 +385,11 @@ __global__ void lg_grad_kernel(const double* __restrict__ x, const double* __res
 
 }  // namespace fedhc
 
+namespace fedhc {
+bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
+                        int max_smem, cudaStream_t st, int* status);
+}
+
 using namespace fedhc;
 
 extern "C" int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params, int n_features,
@@ -397,6 +402,9 @@ extern "C" int fedhc_local_train(const fedhc_client* clients, int n_clients, con
   int dev = 0, max_smem = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int fused_status = FEDHC_OK;
+  if (launch_train_fused(clients, n_clients, params, n_features, n_classes, max_smem, st, &fused_status))
+    return fused_status;
   const int NT = (n_classes + 7) / 8;
   TrainGeom g{};
   const int NTk = NT == 3 ? 4 : NT;
