@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["round", "fedavg"], default="round",
+                    help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
+    ap.add_argument("--fedavg-k", type=int, default=100)
+    ap.add_argument("--fedavg-p", type=int, default=11_170_000)
     return ap.parse_args()
 
 
@@ -324,14 +328,13 @@ def run_ours(args, rank, world, local_rank):
         nonlocal now, h2d, d2h
         rep, mine, wl, seeds, coef = plan_round(r, selector, now)
         now += rep.makespan
-        packed, meta = fed.plan(mine, wl, seeds)
-        fed.upload_plan(packed)
+        meta, perm_bytes = fed.stage_plan(mine, wl, seeds)
         desc = fed.descriptors(mine, meta, LR, deltas)
         coef_dev = torch.tensor(coef, dtype=torch.float64).pin_memory().to(dev, non_blocking=True)
         correct.zero_()
         device_round(desc, coef_dev, correct)
         acc = correct.item() / N_TEST  # D2H of the round's result
-        h2d = packed.nbytes + desc.numel() + coef_dev.numel() * 8
+        h2d = perm_bytes + desc.numel() + coef_dev.numel() * 8
         d2h = 8
         return acc
 
@@ -386,6 +389,75 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+def run_fedavg(args, rank, world, local_rank):
+    """Config 5: K fp32 client deltas of P params -> fp64 FedAvg (one point of the sweep).
+
+    Each rank aggregates its K deltas (weak scaling) and the ranks all-reduce
+    the fp64 partial sums over NCCL.  Inputs (K*P*4 bytes) exceed L2.
+    """
+    import torch
+
+    from paper_2305_15668_b200.training import fedavg_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+    K, P = args.fedavg_k, args.fedavg_p
+    g = torch.Generator(device=dev).manual_seed(rank)
+    deltas = torch.empty(K, (P + 3) // 4 * 4, device=dev)[:, :P]
+    for k in range(K):
+        deltas[k].normal_(0.0, 1e-3, generator=g)
+    base = torch.randn(P, device=dev, dtype=torch.float64, generator=g)
+    w = torch.randint(1, 1025, (K * world,), generator=torch.Generator().manual_seed(0)).double()
+    coef = (w / w.sum())[rank * K:(rank + 1) * K].to(dev)
+    out = torch.empty_like(base)
+    partial = torch.empty_like(base)
+    one = torch.ones(1, dtype=torch.float64, device=dev)
+
+    def step():
+        if world == 1:
+            fedavg_device(deltas, coef, base, out)
+        else:
+            fedavg_device(deltas, coef, None, partial)
+            dist.all_reduce(partial)
+            fedavg_device(partial.view(1, -1), one, base, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.destroy_process_group()
+    from benchlib import roofline_entry
+    alg_bytes = K * P * 4 + 2 * P * 8
+    res = {
+        "metric": "FedAvg aggregated client-delta bytes/sec (config 5)",
+        "value": world * alg_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 deltas, fp64 accumulation", "data": "synthetic N(0,1e-3) deltas, N(0,1) base",
+        "config": {"workload": f"fedavg K={K} P={P} per GPU", "l2": "inputs larger than L2"},
+        "roofline": roofline_entry(alg_bytes, ms, ROOT, kernel="fedavg_kernel"),
+        "clocks": clocks.summary(), "gpu_launches": args.steps * (1 if world == 1 else 2),
+    }
+    return res
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
     if rank != 0:
@@ -420,6 +492,8 @@ def main():
         pass  # torchrun decides the world; --gpus is informational
     if args.impl == "reference":
         res = run_reference(args, rank, world)
+    elif args.workload == "fedavg":
+        res = run_fedavg(args, rank, world, local_rank)
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:

@@ -72,6 +72,18 @@ typedef struct fedhc_client {
 int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params,
                       int n_features, int n_classes, int max_batch, void* stream);
 
+/* ---- batch order: the PCG64 permutations local_train draws ------------- */
+/* Native, multi-threaded restatement of `np.random.default_rng(seed)` +
+ * repeated `.permutation(n)` (fl_core.py:181-187): SeedSequence -> PCG64
+ * (XSL-RR 128/64) -> Fisher-Yates with random_interval, bit-exact with
+ * numpy.  Client c writes n_perms[c] permutations of n_rows[c] (int32) at
+ * out + offsets[c].  seeds[c] = stable_seed("local_train", seed) (fl_core.py:181).
+ * n_threads <= 0 uses all hardware threads.  Host memory only. */
+int fedhc_batch_permutations(const uint64_t* seeds, const int32_t* n_rows, const int32_t* n_perms,
+                             const int64_t* offsets, int n_clients, int32_t* out, int n_threads);
+/* PCG64 state after seeding (for tests against numpy's bit_generator.state). */
+int fedhc_pcg64_state(uint64_t seed, uint64_t* state_hi, uint64_t* state_lo, uint64_t* inc_hi, uint64_t* inc_lo);
+
 /* ---- loss_and_grad: fl_core.loss_and_grad (fl_core.py:138-151) ---------- */
 /* fp64 throughout.  x dev fp64 [n, F]; y dev int32 [n]; params dev fp64 [P];
  * grad dev fp64 [P] out; loss dev fp64 [1] out (mean CE, +1e-300 guard);

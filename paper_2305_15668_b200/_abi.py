@@ -115,6 +115,9 @@ SIGNATURES = {
          C.POINTER(C.POINTER(C.c_int32)), C.POINTER(_i)],
     ),
     "fedhc_work_units": (_d, [_i, _i, _i, _i, _d, _d, _d]),
+    "fedhc_batch_permutations": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i]),
+    "fedhc_pcg64_state": (_i, [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                C.POINTER(C.c_uint64)]),
     "fedhc_maxmin_allocate": (_i, [_dp, _dp, _i, _d, _dp]),
 }
 

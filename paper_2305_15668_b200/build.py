@@ -1,6 +1,6 @@
 """Build libfedhc.so in-tree (sm_100a only).
 
-    python -m paper_2305_15668_b200.build [--verbose]
+    python paper_2305_15668_b200/build.py [--verbose] [--force]
 
 CUDA sources are compiled with nvcc for `-gencode arch=compute_100a,code=sm_100a`
 (-lineinfo, -O3); the host-only DES is compiled with g++ and
@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
             "-I", os.path.join(ROOT, "include")]
-CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-I", os.path.join(ROOT, "include")]
+CXX_FLAGS = ["-O3", "-march=x86-64-v3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-I", os.path.join(ROOT, "include")]
 
 
 def _sources():

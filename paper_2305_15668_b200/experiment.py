@@ -31,9 +31,9 @@ from . import _abi
 from .errors import ConfigError
 from .roundsim import RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
-from .training import (Dataset, DatasetShard, batch_permutations, check_aggregation, count_correct, device,
-                       fedavg_device, init_params, make_synthetic_dataset, partition_noniid, stable_seed,
-                       stream_ptr)
+from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
+                       init_params, make_synthetic_dataset, n_permutations, native_permutations, partition_noniid,
+                       stable_seed, stream_ptr)
 
 
 @dataclass
@@ -121,26 +121,47 @@ class DeviceFederation:
         return self
 
     # ---- per-round plan (host) ------------------------------------------
-    def plan(self, participants: list[str], workloads, seeds) -> tuple[np.ndarray, list[tuple[int, int, int, int]]]:
-        """PCG64 batch permutations for every participant, packed (int32)."""
-        chunks, meta, at = [], [], 0
+    def plan_meta(self, participants: list[str], workloads, seeds):
+        """Per participant (offset into the packed permutation buffer, n_rows, steps, batch) + native args."""
+        meta, at = [], 0
+        rows, perms, rseeds = [], [], []
         for cid, wl, sd in zip(participants, workloads, seeds):
             _, n = self.offset[cid]
-            perm = batch_permutations(n, wl.num_samples, wl.batch_size, sd)
-            chunks.append(perm)
+            k = n_permutations(n, wl.num_samples, wl.batch_size)
             meta.append((at, n, math.ceil(wl.num_samples / wl.batch_size), wl.batch_size))
-            at += perm.shape[0]
-        packed = np.concatenate(chunks) if chunks else np.zeros(0, np.int32)
-        return packed, meta
+            rows.append(n)
+            perms.append(k)
+            rseeds.append(stable_seed("local_train", sd))
+            at += n * k
+        return meta, at, (rseeds, rows, perms)
 
-    def upload_plan(self, packed: np.ndarray) -> torch.Tensor:
-        n = packed.shape[0]
+    def plan(self, participants: list[str], workloads, seeds) -> tuple[np.ndarray, list[tuple[int, int, int, int]]]:
+        """PCG64 batch permutations for every participant, packed (int32, host)."""
+        meta, total, (rseeds, rows, perms) = self.plan_meta(participants, workloads, seeds)
+        return native_permutations(rseeds, rows, perms), meta
+
+    def _ensure_plan_capacity(self, n: int):
         if getattr(self, "_copied", None) is not None:
-            self._copied.synchronize()  # previous round's H2D must finish before the pinned buffer is reused
+            self._copied.synchronize()  # previous H2D must finish before the pinned buffer is reused
         if n > self._cap:
             self._cap = max(n, 2 * self._cap)
             self._pinned = torch.empty(self._cap, dtype=torch.int32, pin_memory=True)
             self._perm_dev = torch.empty(self._cap, dtype=torch.int32, device=self.x.device)
+
+    def stage_plan(self, participants: list[str], workloads, seeds):
+        """Generate the permutations straight into pinned memory and start the H2D copy."""
+        meta, total, (rseeds, rows, perms) = self.plan_meta(participants, workloads, seeds)
+        self._ensure_plan_capacity(max(total, 1))
+        if total:
+            native_permutations(rseeds, rows, perms, out=self._pinned.numpy())
+            self._perm_dev[:total].copy_(self._pinned[:total], non_blocking=True)
+            self._copied = torch.cuda.Event()
+            self._copied.record()
+        return meta, total * 4
+
+    def upload_plan(self, packed: np.ndarray) -> torch.Tensor:
+        n = packed.shape[0]
+        self._ensure_plan_capacity(max(n, 1))
         if n:
             self._pinned[:n].numpy()[:] = packed
             self._perm_dev[:n].copy_(self._pinned[:n], non_blocking=True)
@@ -167,8 +188,7 @@ class DeviceFederation:
         k = len(participants)
         if deltas is None:
             deltas = delta_buffer(k, self.P, self.x.device)
-        packed, meta = self.plan(participants, workloads, seeds)
-        self.upload_plan(packed)
+        meta, _ = self.stage_plan(participants, workloads, seeds)
         d_desc = self.descriptors(participants, meta, lr, deltas)
         max_batch = max((wl.batch_size for wl in workloads), default=1)
         _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr(), k, params.data_ptr(), self.n_features,

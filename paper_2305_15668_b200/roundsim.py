@@ -13,6 +13,8 @@ import ctypes as C
 import json
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from . import _abi
 from .errors import ConfigError, TraceError
 from .spec import ClientProfile, FleetConfig
@@ -28,6 +30,9 @@ KIND_RANK = {
     "RoundComplete": 5,
 }
 _INSTR = ("launch", "start_training", "upload_model", "terminate")
+_EVENT = np.dtype([("t", "<f8"), ("kind", "<i4"), ("client", "<i4"), ("executor", "<i4"), ("aux", "<i4"),
+                   ("budget", "<f8"), ("alloc_off", "<i8"), ("alloc_len", "<i4"), ("pad_", "<i4")])
+assert _EVENT.itemsize == C.sizeof(_abi.DesEvent)
 
 
 @dataclass
@@ -96,7 +101,8 @@ class RoundSimulator:
         if too_big:
             raise ConfigError(f"clients {too_big} have budgets above theta={cfg.theta} and can never launch")
         n = len(participant_ids)
-        order = (C.c_int32 * max(n, 1))(*[self.index[c] for c in participant_ids])
+        index = self.index
+        order = (C.c_int32 * max(n, 1))(*[index[c] for c in participant_ids])
         conf = _abi.DesConfig(float(cfg.theta), int(cfg.max_executors),
                               0 if cfg.scheduler_kind == "resource-aware" else 1, int(bool(cfg.dynamic_parallelism)),
                               float(cfg.alpha), float(cfg.beta), float(cfg.launch_latency),
@@ -117,27 +123,27 @@ class RoundSimulator:
         _abi.check(_abi.lib.fedhc_des_trace(self._sim, C.byref(ev), C.byref(ac), C.byref(ash), C.byref(pt),
                                             C.byref(pn), C.byref(npar)))
         pid = participant_ids
-        launch_order, upload_order = [], []
-        seg = [] if want_trace else None
-        for k in range(rep.n_events):
-            e = ev[k]
-            kind = e.kind
-            if kind == _abi.EV_LAUNCHED:
-                launch_order.append(e.client)
-            elif kind == _abi.EV_UPLOADED:
-                upload_order.append(e.client)
-            if seg is not None:
-                seg.append(self._event_dict(e, pid, ac, ash))
+        events = np.ctypeslib.as_array(C.cast(ev, C.POINTER(C.c_uint8)), shape=(rep.n_events * _EVENT.itemsize,))
+        events = events.view(_EVENT)
+        kinds, who = events["kind"], events["client"]
+        launch_order = who[kinds == _abi.EV_LAUNCHED].tolist()
+        upload_order = who[kinds == _abi.EV_UPLOADED].tolist()
+        st = np.ctypeslib.as_array(starts, shape=(max(n, 1),))
+        en = np.ctypeslib.as_array(ends, shape=(max(n, 1),))
+        st_l, en_l = st.tolist(), en.tolist()
+        par = list(zip(np.ctypeslib.as_array(pt, shape=(npar.value,)).tolist(),
+                       np.ctypeslib.as_array(pn, shape=(npar.value,)).tolist())) if npar.value else []
+        seg = [self._event_dict(ev[k], pid, ac, ash) for k in range(rep.n_events)] if want_trace else None
         report = RoundReport(
             round_index=round_index,
             makespan=rep.makespan,
             utilization=rep.utilization,
             vacancy_area=rep.vacancy_area,
             throughput=rep.throughput,
-            parallelism_timeline=[(pt[i], pn[i]) for i in range(npar.value)],
-            per_client_times={pid[i]: ends[i] - starts[i] for i in upload_order},
-            per_client_start={pid[i]: starts[i] for i in launch_order},
-            per_client_end={pid[i]: ends[i] for i in upload_order},
+            parallelism_timeline=par,
+            per_client_times={pid[i]: en_l[i] - st_l[i] for i in upload_order},
+            per_client_start={pid[i]: st_l[i] for i in launch_order},
+            per_client_end={pid[i]: en_l[i] for i in upload_order},
             per_client_budget={pid[i]: float(self.budget[pid[i]]) for i in launch_order},
             degenerate=bool(rep.degenerate),
         )

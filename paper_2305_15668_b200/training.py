@@ -124,13 +124,34 @@ def n_permutations(n_rows: int, num_samples: int, batch_size: int) -> int:
     return max(1, math.ceil(steps / per_epoch))
 
 
+def native_permutations(seeds, n_rows, n_perms, out: np.ndarray | None = None, threads: int = 0) -> np.ndarray:
+    """Native (libfedhc, multi-threaded) PCG64 permutations, bit-exact with numpy.
+
+    seeds[c] is the default_rng seed (stable_seed("local_train", seed)); client c
+    gets n_perms[c] concatenated permutations of range(n_rows[c]).
+    """
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    rows = np.ascontiguousarray(n_rows, dtype=np.int32)
+    perms = np.ascontiguousarray(n_perms, dtype=np.int32)
+    sizes = rows.astype(np.int64) * perms
+    offsets = np.zeros(len(sizes), dtype=np.int64)
+    if len(sizes) > 1:
+        np.cumsum(sizes[:-1], out=offsets[1:])
+    total = int(sizes.sum())
+    if out is None:
+        out = np.empty(total, dtype=np.int32)
+    assert out.dtype == np.int32 and out.flags.c_contiguous and out.shape[0] >= total
+    _abi.check(_abi.lib.fedhc_batch_permutations(seeds.ctypes.data, rows.ctypes.data, perms.ctypes.data,
+                                                 offsets.ctypes.data, len(seeds), out.ctypes.data, threads))
+    return out[:total]
+
+
 def batch_permutations(n_rows: int, num_samples: int, batch_size: int, seed) -> np.ndarray:
     """Concatenated PCG64 permutations that local_train's batches walk (int32)."""
     k = n_permutations(n_rows, num_samples, batch_size)
     if k == 0:
         return np.zeros(0, dtype=np.int32)
-    rng = np.random.default_rng(stable_seed("local_train", seed))
-    return np.concatenate([rng.permutation(n_rows) for _ in range(k)]).astype(np.int32)
+    return native_permutations([stable_seed("local_train", seed)], [n_rows], [k])
 
 
 def _dev_array(a: np.ndarray, dtype) -> torch.Tensor:
