@@ -1,27 +1,27 @@
-// Fused per-client local SGD, v2 -- fl_core.local_train (fl_core.py:163-194)
-// for FEMNIST-shaped clients (F <= 784, C <= 16), one CTA per client.
+// Fused per-client local SGD -- fl_core.local_train (fl_core.py:163-194) for
+// FEMNIST-shaped clients (F <= 784, C <= 16), one CTA per client.
 //
 // Per 16-row stage of a batch (rows gathered by the host PCG64 permutation
-// with one 1-D TMA bulk copy per row, producer warp + full/empty mbarriers):
+// with one 1-D TMA bulk copy per row; producer warp + full/empty mbarriers):
 //
-//   forward   Z[16 x 16]  = X[16 x F] . W[F x 16]          (mma.sync bf16, M=16)
-//   softmax   E = (softmax(Z + b) - onehot) / nb            (warp per row)
-//   backward  G^T[16 x F] += E^T[16 x 16] . X[16 x F]       (same X fragments)
+//   forward   Z[16 x 16]  = X[16 x F] . W[F x 16]        (mma.sync m16n8k8 bf16)
+//   softmax   E = (softmax(Z + b) - onehot) / nb          (half-warp per row)
+//   backward  G^T[16 x F] += E^T[16 x 16] . X[16 x F]     (same X fragments)
 //
-// Precision: every fp32 operand is split into bf16 hi + mid (|x - hi - mid|
-// <= 2^-17|x|) and each product is hi*hi + hi*mid + mid*hi with fp32
-// accumulation ("bf16x3"): fp32-level accuracy on the bf16 tensor pipe.
+// Precision ("bf16x3"): every fp32 operand is split into bf16 hi + mid
+// (|x - hi - mid| <= 2^-17 |x|) and each product is hi*hi + hi*mid + mid*hi
+// accumulated in fp32 -- fp32-level accuracy on the bf16 tensor pipe.
 //
-// Data reuse:
-//   * X is read from shared memory ONCE per stage: the forward splits its A
-//     fragments (rows x f) into registers, and the backward re-uses them as B
-//     fragments (rows x f, k = rows) via movmatrix.trans -- no second pass.
-//   * Warp w owns the feature range [112w, 112w + 112): its forward K-slice,
-//     its backward N-slice and therefore exactly the W/G elements its lanes
-//     touch.  The fp32 master W lives in shared memory in a thread-private
-//     fragment-native layout and its bf16 hi/mid split lives in registers, so
-//     the SGD update W -= lr * G is thread-local (no barrier, no conflicts).
-// SGD state is fp32; delta = W_final - W_initial.
+// Work split: 14 compute warps; warp w owns the feature slice
+// [56w, 56w + 56) = 7 k8-steps.  That slice is its forward K range, its
+// backward N range, and therefore exactly the W / G elements its lanes touch:
+//   * X is read from shared memory once per stage; the forward's split A
+//     fragments stay in registers and become the backward's B fragments via
+//     movmatrix.trans (no second pass over X).
+//   * The fp32 master W lives in shared memory in a thread-private,
+//     fragment-native layout and its bf16 hi/mid split lives in registers,
+//     so W -= lr * G is a thread-local update (no barrier, no conflicts).
+// 480 threads (14 + 1 warps) -> <= 128 registers per thread.
 #include <float.h>
 
 #include "common.cuh"
@@ -29,36 +29,37 @@
 namespace fedhc {
 
 constexpr int kFRows = 16;              // rows per stage (MMA M of the forward)
-constexpr int kFWarps = 7;              // compute warps
+constexpr int kFWarps = 14;             // compute warps
 constexpr int kFThreads = (kFWarps + 1) * 32;
-constexpr int kFKMax = 7;               // k16 steps per warp: F <= 7 * 7 * 16 = 784
-constexpr int kFMaxFp = kFWarps * kFKMax * 16;
+constexpr int kFK8 = 7;                 // k8 steps per warp: F <= 14 * 7 * 8 = 784
+constexpr int kFMaxFp = kFWarps * kFK8 * 8;
+constexpr int kFSoftWarps = kFRows / 2; // warps 0..7 run the softmax (2 rows each)
 
 struct FusedGeom {
-  int F, C, Fp, Fs, Es, Zs, stages, nks;
+  int F, C, Fp, Fs, Es, Zs, stages, nk8;
   int off_master, off_x, off_zp, off_e, off_gb, off_lab, off_bar, bytes;
 };
 
 static inline int a16(int v) { return (v + 15) & ~15; }
 
-bool plan_fused(int F, int C, int NT, int max_smem, FusedGeom& g) {
-  if (F % 4 != 0 || C > 8 * NT || NT > 2) return false;
+bool plan_fused(int F, int C, int max_smem, FusedGeom& g) {
+  if (F % 4 != 0 || C > 16) return false;
   g.F = F;
   g.C = C;
-  g.Fp = (F + 15) / 16 * 16;
+  g.Fp = (F + 7) / 8 * 8;
   if (g.Fp > kFMaxFp) return false;
-  g.nks = g.Fp / 16;
+  g.nk8 = g.Fp / 8;
   g.Fs = g.Fp;
   while (g.Fs % 32 != 8) g.Fs += 4;  // conflict-free 64-bit fragment loads
   g.Es = 20;                          // conflict-free E^T fragment loads
-  g.Zs = 8 * NT + 8;
+  g.Zs = 24;                          // conflict-free partial-Z stores
   for (int st = 4; st >= 2; --st) {
     int off = 0;
-    g.off_master = off; off = a16(off + kFWarps * kFKMax * NT * 32 * 16);
+    g.off_master = off; off = a16(off + kFWarps * kFK8 * 32 * 16);
     g.off_x = off;      off = a16(off + st * kFRows * g.Fs * 4);
     g.off_zp = off;     off = a16(off + kFWarps * kFRows * g.Zs * 4);
     g.off_e = off;      off = a16(off + kFRows * g.Es * 4);
-    g.off_gb = off;     off = a16(off + kFWarps * 16 * 4 + 16 * 4);
+    g.off_gb = off;     off = a16(off + kFSoftWarps * 16 * 4 + 16 * 4);
     g.off_lab = off;    off = a16(off + st * kFRows * 4);
     g.off_bar = off;    off = a16(off + 2 * st * 8);
     g.bytes = off;
@@ -68,7 +69,17 @@ bool plan_fused(int F, int C, int NT, int max_smem, FusedGeom& g) {
   return false;
 }
 
-template <int NT>
+// D(16x8, fp32) += A(16x8, bf16, row) * B(8x8, bf16, col)
+__device__ __forceinline__ void mma_bf16_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+
+// FULL: the feature count fills every warp's slice exactly (F = 784), so no
+// per-step guards (and no reconvergence barriers around movmatrix).
+template <bool FULL>
 __global__ void __launch_bounds__(kFThreads, 1)
     train_fused_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params,
                        const FusedGeom g) {
@@ -78,7 +89,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   float* Zp = reinterpret_cast<float*>(smem + g.off_zp);
   float* E = reinterpret_cast<float*>(smem + g.off_e);
   float* gbs = reinterpret_cast<float*>(smem + g.off_gb);
-  float* bias_out = gbs + kFWarps * 16;
+  float* bias_out = gbs + kFSoftWarps * 16;
   int* labels = reinterpret_cast<int*>(smem + g.off_lab);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.off_bar);
   uint64_t* empty = full + g.stages;
@@ -102,28 +113,23 @@ __global__ void __launch_bounds__(kFThreads, 1)
 
   const int n = cl.n_rows, B = cl.batch_size;
   const int steps = n > 0 ? cl.n_batches : 0;
-
-  // W element (f, c) as fp32, zero in the padding.
   auto w_at = [&](int f, int c) -> float {
     return (f < F && c < C) ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
   };
+  auto active = [&](int j) -> bool { return FULL || (warp * kFK8 + j) < g.nk8; };
 
-  // thread-private fragment-native master: [warp][j][nt][lane] -> {W(f0,c), W(f0+1,c), W(f0+8,c), W(f0+9,c)}
-  // with f0 = 16*ks + 2*tq, c = 8*nt + gq, ks = warp*kFKMax + j.
-  uint32_t wh[kFKMax][NT][2], wm[kFKMax][NT][2];
+  // master[warp][j][lane] = {W(f0,c0), W(f0+1,c0), W(f0,c1), W(f0+1,c1)}, f0 = 8*ks + 2*tq,
+  // c0 = gq, c1 = gq + 8, ks = 7*warp + j.  hi/mid copies: wh/wm[j][class tile].
+  uint32_t wh[kFK8][2], wm[kFK8][2];
   if (warp < kFWarps) {
 #pragma unroll
-    for (int j = 0; j < kFKMax; ++j) {
-      const int ks = warp * kFKMax + j;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int f0 = 16 * ks + 2 * tq, c = 8 * nt + gq;
-        float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ks < g.nks) m = make_float4(w_at(f0, c), w_at(f0 + 1, c), w_at(f0 + 8, c), w_at(f0 + 9, c));
-        master[((warp * kFKMax + j) * NT + nt) * 32 + lane] = m;
-        split_bf16x2(m.x, m.y, wh[j][nt][0], wm[j][nt][0]);
-        split_bf16x2(m.z, m.w, wh[j][nt][1], wm[j][nt][1]);
-      }
+    for (int j = 0; j < kFK8; ++j) {
+      const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
+      float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (active(j)) m = make_float4(w_at(f0, gq), w_at(f0 + 1, gq), w_at(f0, gq + 8), w_at(f0 + 1, gq + 8));
+      master[(warp * kFK8 + j) * 32 + lane] = m;
+      split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
+      split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
     }
   }
   __syncthreads();
@@ -155,139 +161,129 @@ __global__ void __launch_bounds__(kFThreads, 1)
       }
     }
   } else {
-    // ===== compute warps =====
-    float G[kFKMax][2][4];
+    // ===== 14 compute warps =====
+    float G[kFK8][4];
 #pragma unroll
-    for (int j = 0; j < kFKMax; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) G[j][h][0] = G[j][h][1] = G[j][h][2] = G[j][h][3] = 0.f;
-    float bias = lane < C ? static_cast<float>(params[FC + lane]) : 0.f;
+    for (int j = 0; j < kFK8; ++j) G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
+    const int cls = lane & 15;                      // softmax: half-warp per row, lane = class
+    const int srow = 2 * warp + (lane >> 4);        // softmax row of this lane (warps 0..7)
+    float bias = cls < C ? static_cast<float>(params[FC + cls]) : 0.f;
     float gb = 0.f;
     const float lr = cl.lr;
     bool bias_pending = false;
     int k = 0, st = 0;
     for (int s = 0; s < steps; ++s) {
       const BatchRef br = batch_ref(s, n, B);
+      const float inv_nb = 1.0f / static_cast<float>(br.rows);
+      (void)inv_nb;
       const float nb = static_cast<float>(br.rows);
       for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
         const int rows = min(kFRows, br.rows - r0);
         mbar_wait(&full[st], (k / S) & 1);
         const float* Xs = Xb + (size_t)st * kFRows * Fs;
 
-        // ---- forward: split A fragments once, keep them for the backward ----
-        uint32_t ah[kFKMax][4], am[kFKMax][4];
-        float acc[2][NT][4];
+        // ---- forward over this warp's 7 k8 steps; A fragments kept for the backward ----
+        uint32_t ah[kFK8][2], am[kFK8][2];
+        float acc[2][4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+        for (int nt = 0; nt < 2; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) acc[e][nt][0] = acc[e][nt][1] = acc[e][nt][2] = acc[e][nt][3] = 0.f;
-#pragma unroll
-        for (int j = 0; j < kFKMax; ++j) {
-          const int ks = warp * kFKMax + j;
-          if (ks < g.nks) {
-            const float* base = Xs + gq * Fs + 16 * ks + 2 * tq;
+        for (int j = 0; j < kFK8; ++j) {
+          if (active(j)) {
+            const float* base = Xs + gq * Fs + 8 * (warp * kFK8 + j) + 2 * tq;
             const float2 v0 = *reinterpret_cast<const float2*>(base);
             const float2 v1 = *reinterpret_cast<const float2*>(base + 8 * Fs);
-            const float2 v2 = *reinterpret_cast<const float2*>(base + 8);
-            const float2 v3 = *reinterpret_cast<const float2*>(base + 8 * Fs + 8);
             split_bf16x2(v0.x, v0.y, ah[j][0], am[j][0]);
             split_bf16x2(v1.x, v1.y, ah[j][1], am[j][1]);
-            split_bf16x2(v2.x, v2.y, ah[j][2], am[j][2]);
-            split_bf16x2(v3.x, v3.y, ah[j][3], am[j][3]);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              mma_bf16(acc[j & 1][nt], am[j], wh[j][nt][0], wh[j][nt][1]);
-              mma_bf16(acc[j & 1][nt], ah[j], wm[j][nt][0], wm[j][nt][1]);
-              mma_bf16(acc[j & 1][nt], ah[j], wh[j][nt][0], wh[j][nt][1]);
+            for (int nt = 0; nt < 2; ++nt) {
+              mma_bf16_k8(acc[nt], am[j][0], am[j][1], wh[j][nt]);
+              mma_bf16_k8(acc[nt], ah[j][0], ah[j][1], wm[j][nt]);
+              mma_bf16_k8(acc[nt], ah[j][0], ah[j][1], wh[j][nt]);
             }
           }
         }
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < 2; ++nt) {
           float* zr = Zp + (size_t)(warp * kFRows + gq) * Zs + nt * 8 + 2 * tq;
-          *reinterpret_cast<float2*>(zr) = make_float2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
-          *reinterpret_cast<float2*>(zr + 8 * Zs) =
-              make_float2(acc[0][nt][2] + acc[1][nt][2], acc[0][nt][3] + acc[1][nt][3]);
+          *reinterpret_cast<float2*>(zr) = make_float2(acc[nt][0], acc[nt][1]);
+          *reinterpret_cast<float2*>(zr + 8 * Zs) = make_float2(acc[nt][2], acc[nt][3]);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kFWarps * 32));
 
-        // ---- pending bias step of the previous batch (identical in every warp) ----
-        if (bias_pending) {
-          float gsum = 0.f;
+        if (warp < kFSoftWarps) {
+          // ---- pending bias step of the previous batch (same value in every lane copy) ----
+          if (bias_pending) {
+            float gsum = 0.f;
 #pragma unroll
-          for (int w = 0; w < kFWarps; ++w) gsum += gbs[w * 16 + (lane & 15)];
-          if (lane < C) bias -= lr * gsum;
-          bias_pending = false;
-        }
-        // ---- softmax + CE error: rows warp, warp+7, warp+14; lane = class ----
-        for (int rr = warp; rr < kFRows; rr += kFWarps) {
-          float z = -FLT_MAX;
-          if (lane < C) {
-            z = bias;
-#pragma unroll
-            for (int w = 0; w < kFWarps; ++w) z += Zp[(size_t)(w * kFRows + rr) * Zs + lane];
+            for (int w = 0; w < kFSoftWarps; ++w) gsum += gbs[w * 16 + cls];
+            if (cls < C) bias -= lr * gsum;
+            bias_pending = false;
           }
-          const float m = warp_max(z);
-          const float ex = lane < C ? expf(z - m) : 0.f;
-          const float ssum = warp_sum(ex);
+          // ---- softmax + CE error ----
+          float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+          for (int w = 0; w < kFWarps; w += 2) {
+            z0 += Zp[(size_t)(w * kFRows + srow) * Zs + cls];
+            z1 += Zp[(size_t)((w + 1) * kFRows + srow) * Zs + cls];
+          }
+          const float z = cls < C ? bias + (z0 + z1) : -FLT_MAX;
+          float m = z;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          const float ex = cls < C ? expf(z - m) : 0.f;
+          float ssum = ex;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
           float err = 0.f;
-          if (rr < rows && lane < C) {
-            err = (ex / ssum - (lane == labels[st * kFRows + rr] ? 1.f : 0.f)) / nb;
+          if (srow < rows && cls < C) {
+            err = (ex / ssum - (cls == labels[st * kFRows + srow] ? 1.f : 0.f)) / nb;
             gb += err;
           }
-          if (lane < 16) E[rr * Es + lane] = err;
+          E[srow * Es + cls] = err;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kFWarps * 32));
         if (tid == 0) mbar_arrive(&empty[st]);  // stage free: X lives on in registers
 
         // ---- backward: G^T += E^T . X, X fragments via movmatrix.trans ----
-        uint32_t eh[4], em[4];
+        uint32_t eh[4], em[4];  // [rows 0-7: c lo, c hi][rows 8-15: c lo, c hi]
         split_bf16x2(E[(2 * tq) * Es + gq], E[(2 * tq + 1) * Es + gq], eh[0], em[0]);
         split_bf16x2(E[(2 * tq) * Es + gq + 8], E[(2 * tq + 1) * Es + gq + 8], eh[1], em[1]);
         split_bf16x2(E[(2 * tq + 8) * Es + gq], E[(2 * tq + 9) * Es + gq], eh[2], em[2]);
         split_bf16x2(E[(2 * tq + 8) * Es + gq + 8], E[(2 * tq + 9) * Es + gq + 8], eh[3], em[3]);
 #pragma unroll
-        for (int j = 0; j < kFKMax; ++j) {
-          const int ks = warp * kFKMax + j;
-          if (ks < g.nks) {
+        for (int j = 0; j < kFK8; ++j) {
+          if (active(j)) {
             const uint32_t t0h = movmatrix_trans(ah[j][0]), t1h = movmatrix_trans(ah[j][1]);
-            const uint32_t t2h = movmatrix_trans(ah[j][2]), t3h = movmatrix_trans(ah[j][3]);
             const uint32_t t0m = movmatrix_trans(am[j][0]), t1m = movmatrix_trans(am[j][1]);
-            const uint32_t t2m = movmatrix_trans(am[j][2]), t3m = movmatrix_trans(am[j][3]);
-            mma_bf16(G[j][0], em, t0h, t1h);
-            mma_bf16(G[j][0], eh, t0m, t1m);
-            mma_bf16(G[j][0], eh, t0h, t1h);
-            mma_bf16(G[j][1], em, t2h, t3h);
-            mma_bf16(G[j][1], eh, t2m, t3m);
-            mma_bf16(G[j][1], eh, t2h, t3h);
+            mma_bf16_k8(G[j], em[0], em[1], t0h);
+            mma_bf16_k8(G[j], eh[0], eh[1], t0m);
+            mma_bf16_k8(G[j], eh[0], eh[1], t0h);
+            mma_bf16_k8(G[j], em[2], em[3], t1h);
+            mma_bf16_k8(G[j], eh[2], eh[3], t1m);
+            mma_bf16_k8(G[j], eh[2], eh[3], t1h);
           }
         }
         ++k;
         st = (st + 1 == S) ? 0 : st + 1;
       }
       // ---- end of batch: thread-local SGD step on the master + re-split ----
-      if (lane < 16) gbs[warp * 16 + lane] = lane < C ? gb : 0.f;
+      if (warp < kFSoftWarps && lane < 16) gbs[warp * 16 + lane] = gb;
       gb = 0.f;
       bias_pending = true;
 #pragma unroll
-      for (int j = 0; j < kFKMax; ++j) {
-        const int ks = warp * kFKMax + j;
-        if (ks < g.nks) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            float4& mref = master[((warp * kFKMax + j) * NT + nt) * 32 + lane];
-            float4 m = mref;
-            const int q = 2 * nt;  // G rows: c = gq (q = 0) or gq + 8 (q = 2)
-            m.x -= lr * G[j][0][q];
-            m.y -= lr * G[j][0][q + 1];
-            m.z -= lr * G[j][1][q];
-            m.w -= lr * G[j][1][q + 1];
-            mref = m;
-            split_bf16x2(m.x, m.y, wh[j][nt][0], wm[j][nt][0]);
-            split_bf16x2(m.z, m.w, wh[j][nt][1], wm[j][nt][1]);
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) G[j][h][0] = G[j][h][1] = G[j][h][2] = G[j][h][3] = 0.f;
+      for (int j = 0; j < kFK8; ++j) {
+        if (active(j)) {
+          float4& mref = master[(warp * kFK8 + j) * 32 + lane];
+          float4 m = mref;
+          m.x -= lr * G[j][0];  // (c = gq,     f0)
+          m.y -= lr * G[j][1];  // (c = gq,     f0 + 1)
+          m.z -= lr * G[j][2];  // (c = gq + 8, f0)
+          m.w -= lr * G[j][3];  // (c = gq + 8, f0 + 1)
+          mref = m;
+          split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
+          split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
+          G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
         }
       }
     }
@@ -296,8 +292,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
       if (bias_pending) {
         float gsum = 0.f;
 #pragma unroll
-        for (int w = 0; w < kFWarps; ++w) gsum += gbs[w * 16 + (lane & 15)];
-        if (lane < C) bias -= lr * gsum;
+        for (int w = 0; w < kFSoftWarps; ++w) gsum += gbs[w * 16 + cls];
+        if (cls < C) bias -= lr * gsum;
       }
       if (lane < C) bias_out[lane] = bias;
     }
@@ -308,21 +304,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
   float* out = cl.delta;
   if (warp < kFWarps) {
 #pragma unroll
-    for (int j = 0; j < kFKMax; ++j) {
-      const int ks = warp * kFKMax + j;
-      if (ks < g.nks) {
+    for (int j = 0; j < kFK8; ++j) {
+      if (active(j)) {
+        const float4 m = master[(warp * kFK8 + j) * 32 + lane];
+        const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
+        const float v[4] = {m.x, m.y, m.z, m.w};
+        const int fo[4] = {f0, f0 + 1, f0, f0 + 1};
+        const int co[4] = {gq, gq, gq + 8, gq + 8};
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const float4 m = master[((warp * kFKMax + j) * NT + nt) * 32 + lane];
-          const int f0 = 16 * ks + 2 * tq, c = 8 * nt + gq;
-          if (c < C) {
-            const float v[4] = {m.x, m.y, m.z, m.w};
-            const int fo[4] = {f0, f0 + 1, f0 + 8, f0 + 9};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (fo[i] < F) out[(size_t)fo[i] * C + c] = v[i] - static_cast<float>(params[(size_t)fo[i] * C + c]);
-          }
-        }
+        for (int i = 0; i < 4; ++i)
+          if (fo[i] < F && co[i] < C)
+            out[(size_t)fo[i] * C + co[i]] = v[i] - static_cast<float>(params[(size_t)fo[i] * C + co[i]]);
       }
     }
   }
@@ -332,16 +324,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // Launch the fused kernel if the shape fits; returns false to fall back.
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
                         int max_smem, cudaStream_t st, int* status) {
-  const int NT = (C + 7) / 8;
   FusedGeom g{};
-  if (NT > 2 || !plan_fused(F, C, NT, max_smem, g)) return false;
+  if (!plan_fused(F, C, max_smem, g)) return false;
   cudaError_t e;
-  if (NT == 1) {
-    e = cudaFuncSetAttribute(train_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
-    if (e == cudaSuccess) train_fused_kernel<1><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
+  if (g.nk8 == kFWarps * kFK8) {
+    e = cudaFuncSetAttribute(train_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
+    if (e == cudaSuccess) train_fused_kernel<true><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
   } else {
-    e = cudaFuncSetAttribute(train_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
-    if (e == cudaSuccess) train_fused_kernel<2><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
+    e = cudaFuncSetAttribute(train_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
+    if (e == cudaSuccess) train_fused_kernel<false><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_fused_kernel launch");
