@@ -175,8 +175,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
     for (int s = 0; s < steps; ++s) {
       const BatchRef br = batch_ref(s, n, B);
       const float inv_nb = 1.0f / static_cast<float>(br.rows);
-      (void)inv_nb;
-      const float nb = static_cast<float>(br.rows);
       for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
         const int rows = min(kFRows, br.rows - r0);
         mbar_wait(&full[st], (k / S) & 1);
@@ -184,9 +182,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
 
         // ---- forward over this warp's 7 k8 steps; A fragments kept for the backward ----
         uint32_t ah[kFK8][2], am[kFK8][2];
-        float acc[2][4];
+        float acc[2][2][4];  // [j parity][class tile]: 4 independent HMMA chains
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) acc[e][nt][0] = acc[e][nt][1] = acc[e][nt][2] = acc[e][nt][3] = 0.f;
 #pragma unroll
         for (int j = 0; j < kFK8; ++j) {
           if (active(j)) {
@@ -197,17 +197,18 @@ __global__ void __launch_bounds__(kFThreads, 1)
             split_bf16x2(v1.x, v1.y, ah[j][1], am[j][1]);
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
-              mma_bf16_k8(acc[nt], am[j][0], am[j][1], wh[j][nt]);
-              mma_bf16_k8(acc[nt], ah[j][0], ah[j][1], wm[j][nt]);
-              mma_bf16_k8(acc[nt], ah[j][0], ah[j][1], wh[j][nt]);
+              mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wh[j][nt]);
+              mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wm[j][nt]);
+              mma_bf16_k8(acc[j & 1][nt], am[j][0], am[j][1], wh[j][nt]);
             }
           }
         }
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           float* zr = Zp + (size_t)(warp * kFRows + gq) * Zs + nt * 8 + 2 * tq;
-          *reinterpret_cast<float2*>(zr) = make_float2(acc[nt][0], acc[nt][1]);
-          *reinterpret_cast<float2*>(zr + 8 * Zs) = make_float2(acc[nt][2], acc[nt][3]);
+          *reinterpret_cast<float2*>(zr) = make_float2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
+          *reinterpret_cast<float2*>(zr + 8 * Zs) =
+              make_float2(acc[0][nt][2] + acc[1][nt][2], acc[0][nt][3] + acc[1][nt][3]);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kFWarps * 32));
 
@@ -221,13 +222,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
             bias_pending = false;
           }
           // ---- softmax + CE error ----
-          float z0 = 0.f, z1 = 0.f;
+          float zp[kFWarps];
 #pragma unroll
-          for (int w = 0; w < kFWarps; w += 2) {
-            z0 += Zp[(size_t)(w * kFRows + srow) * Zs + cls];
-            z1 += Zp[(size_t)((w + 1) * kFRows + srow) * Zs + cls];
-          }
-          const float z = cls < C ? bias + (z0 + z1) : -FLT_MAX;
+          for (int w = 0; w < kFWarps; ++w) zp[w] = Zp[(size_t)(w * kFRows + srow) * Zs + cls];
+#pragma unroll
+          for (int w = 0; w < 7; ++w) zp[w] += zp[w + 7];
+          const float zsum = ((zp[0] + zp[1]) + (zp[2] + zp[3])) + ((zp[4] + zp[5]) + zp[6]);
+          const float z = cls < C ? bias + zsum : -FLT_MAX;
           float m = z;
 #pragma unroll
           for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           for (int o = 8; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
           float err = 0.f;
           if (srow < rows && cls < C) {
-            err = (ex / ssum - (cls == labels[st * kFRows + srow] ? 1.f : 0.f)) / nb;
+            err = (ex * __frcp_rn(ssum) - (cls == labels[st * kFRows + srow] ? 1.f : 0.f)) * inv_nb;
             gb += err;
           }
           E[srow * Es + cls] = err;
@@ -256,18 +257,19 @@ __global__ void __launch_bounds__(kFThreads, 1)
           if (active(j)) {
             const uint32_t t0h = movmatrix_trans(ah[j][0]), t1h = movmatrix_trans(ah[j][1]);
             const uint32_t t0m = movmatrix_trans(am[j][0]), t1m = movmatrix_trans(am[j][1]);
-            mma_bf16_k8(G[j], em[0], em[1], t0h);
-            mma_bf16_k8(G[j], eh[0], eh[1], t0m);
             mma_bf16_k8(G[j], eh[0], eh[1], t0h);
-            mma_bf16_k8(G[j], em[2], em[3], t1h);
-            mma_bf16_k8(G[j], eh[2], eh[3], t1m);
             mma_bf16_k8(G[j], eh[2], eh[3], t1h);
+            mma_bf16_k8(G[j], eh[0], eh[1], t0m);
+            mma_bf16_k8(G[j], eh[2], eh[3], t1m);
+            mma_bf16_k8(G[j], em[0], em[1], t0h);
+            mma_bf16_k8(G[j], em[2], em[3], t1h);
           }
         }
         ++k;
         st = (st + 1 == S) ? 0 : st + 1;
       }
       // ---- end of batch: thread-local SGD step on the master + re-split ----
+      gb += __shfl_xor_sync(0xffffffffu, gb, 16);  // both half-warp rows of this warp
       if (warp < kFSoftWarps && lane < 16) gbs[warp * 16 + lane] = gb;
       gb = 0.f;
       bias_pending = true;
