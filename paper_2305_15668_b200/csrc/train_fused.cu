@@ -195,11 +195,40 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const float2 v1 = *reinterpret_cast<const float2*>(base + 8 * Fs);
             split_bf16x2(v0.x, v0.y, ah[j][0], am[j][0]);
             split_bf16x2(v1.x, v1.y, ah[j][1], am[j][1]);
+          }
+        }
+        if (FULL) {
+          // k8 steps (0,1) (2,3) (4,5) fuse into m16n8k16 with the same fragment registers
+#pragma unroll
+          for (int j = 0; j + 1 < kFK8; j += 2) {
+            const uint32_t AH[4] = {ah[j][0], ah[j][1], ah[j + 1][0], ah[j + 1][1]};
+            const uint32_t AM[4] = {am[j][0], am[j][1], am[j + 1][0], am[j + 1][1]};
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
-              mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wh[j][nt]);
-              mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wm[j][nt]);
-              mma_bf16_k8(acc[j & 1][nt], am[j][0], am[j][1], wh[j][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wm[j][nt], wm[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AM, wh[j][nt], wh[j + 1][nt]);
+            }
+          }
+          if (kFK8 & 1) {
+            constexpr int j = kFK8 - 1;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma_bf16_k8(acc[1][nt], ah[j][0], ah[j][1], wh[j][nt]);
+              mma_bf16_k8(acc[1][nt], ah[j][0], ah[j][1], wm[j][nt]);
+              mma_bf16_k8(acc[1][nt], am[j][0], am[j][1], wh[j][nt]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kFK8; ++j) {
+            if (active(j)) {
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wh[j][nt]);
+                mma_bf16_k8(acc[j & 1][nt], ah[j][0], ah[j][1], wm[j][nt]);
+                mma_bf16_k8(acc[j & 1][nt], am[j][0], am[j][1], wh[j][nt]);
+              }
             }
           }
         }
@@ -257,12 +286,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
           if (active(j)) {
             const uint32_t t0h = movmatrix_trans(ah[j][0]), t1h = movmatrix_trans(ah[j][1]);
             const uint32_t t0m = movmatrix_trans(am[j][0]), t1m = movmatrix_trans(am[j][1]);
-            mma_bf16_k8(G[j], eh[0], eh[1], t0h);
-            mma_bf16_k8(G[j], eh[2], eh[3], t1h);
-            mma_bf16_k8(G[j], eh[0], eh[1], t0m);
-            mma_bf16_k8(G[j], eh[2], eh[3], t1m);
-            mma_bf16_k8(G[j], em[0], em[1], t0h);
-            mma_bf16_k8(G[j], em[2], em[3], t1h);
+            // K = the stage's 16 rows: one m16n8k16 per product
+            mma_bf16(G[j], eh, t0h, t1h);
+            mma_bf16(G[j], eh, t0m, t1m);
+            mma_bf16(G[j], em, t0h, t1h);
           }
         }
         ++k;
