@@ -27,7 +27,7 @@ def profiled_traffic(root: str, kernel: str):
         return None
 
 
-def roofline_entry(bytes_per_launch: float, launch_ms: float, root: str, kernel: str = "train_mma_kernel"):
+def roofline_entry(bytes_per_launch: float, launch_ms: float, root: str, kernel: str = "train_fused_kernel"):
     peak, src = hbm_peak(root)
     achieved = bytes_per_launch / (launch_ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
