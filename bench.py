@@ -318,34 +318,18 @@ def run_ours(args, rank, world, local_rank):
     value = total_steps / (ms / 1e3)
 
     # ---------------- e2e: public round API with host buffers ----------------
-    selector = random.Random(f"{cfg.seed}:selection")
-    params.zero_()
-    now = 0.0
-    correct = torch.zeros(1, dtype=torch.int64, device=dev)
-    h2d = d2h = 0
-
-    def e2e_round(r):
-        nonlocal now, h2d, d2h
-        rep, mine, wl, seeds, coef = plan_round(r, selector, now)
-        now += rep.makespan
-        meta, perm_bytes = fed.stage_plan(mine, wl, seeds)
-        desc = fed.descriptors(mine, meta, LR, deltas)
-        coef_dev = torch.tensor(coef, dtype=torch.float64).pin_memory().to(dev, non_blocking=True)
-        correct.zero_()
-        device_round(desc, coef_dev, correct)
-        acc = correct.item() / N_TEST  # D2H of the round's result
-        h2d = perm_bytes + desc.numel() + coef_dev.numel() * 8
-        d2h = 8
-        return acc
-
-    for r in range(args.warmup):
-        e2e_round(r)
+    # FederatedRunner: per round the host plans (selection, native DES, seeds, PCG64 permutations into
+    # pinned memory), copies the plan H2D, launches train/FedAvg/(all-reduce)/eval and reads the
+    # accuracy count back (D2H); planning of round r+1 overlaps the GPU work of round r.
+    from paper_2305_15668_b200.experiment import FederatedRunner
+    runner = FederatedRunner(fed, by_id, cfg, LR, world=world, rank=rank, group=None)
+    runner.run(args.warmup, n_test_total=N_TEST)
     barrier()
     e0 = time.perf_counter()
-    for r in range(args.warmup, total_rounds):
-        e2e_round(r)
+    series = runner.run(args.steps, n_test_total=N_TEST)
     barrier()
     e2e_s = time.perf_counter() - e0
+    h2d, d2h = runner.h2d_bytes, runner.d2h_bytes
     if dist is not None:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -375,7 +359,9 @@ def run_ours(args, rank, world, local_rank):
         "train_kernel_ms": train_ms,
         "accuracy_last_round": accuracy_last,
         "e2e": {"value": e2e_value, "unit": "client-steps/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "rounds_per_sec": args.steps / e2e_s},
+                "d2h_bytes_per_step": int(d2h), "rounds_per_sec": args.steps / e2e_s,
+                "api": "paper_2305_15668_b200.experiment.FederatedRunner.run (pipelined host planning)",
+                "accuracy_last_round": series[-1][1] if series else None},
         "roofline": roof,
         "clocks": clocks.summary(),
         "gpu_launches": launches_per_round * args.steps,

@@ -81,6 +81,14 @@ int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* 
  * n_threads <= 0 uses all hardware threads.  Host memory only. */
 int fedhc_batch_permutations(const uint64_t* seeds, const int32_t* n_rows, const int32_t* n_perms,
                              const int64_t* offsets, int n_clients, int32_t* out, int n_threads);
+/* Per-round client seeds (fl_core.py:21-24, engine.py:336-347, fl_core.py:181):
+ * train_seeds[i] = stable_seed("train", seed, round_index, cid_i) and
+ * rng_seeds[i] = stable_seed("local_train", train_seeds[i]), i.e. the first 4
+ * bytes (little-endian) of sha256(repr(tuple)).  cid_reprs[i] = Python
+ * repr(cid_i) (NUL-terminated UTF-8), so the hashed strings equal Python's. */
+int fedhc_round_seeds(int64_t seed, int64_t round_index, const char* const* cid_reprs, int n,
+                      uint64_t* train_seeds, uint64_t* rng_seeds);
+uint32_t fedhc_sha256_le32(const char* data, int64_t n);
 /* PCG64 state after seeding (for tests against numpy's bit_generator.state). */
 int fedhc_pcg64_state(uint64_t seed, uint64_t* state_hi, uint64_t* state_lo, uint64_t* inc_hi, uint64_t* inc_lo);
 

@@ -119,6 +119,8 @@ SIGNATURES = {
     "fedhc_pcg64_state": (_i, [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.POINTER(C.c_uint64)]),
     "fedhc_maxmin_allocate": (_i, [_dp, _dp, _i, _d, _dp]),
+    "fedhc_round_seeds": (_i, [_i64, _i64, C.POINTER(C.c_char_p), _i, _vp, _vp]),
+    "fedhc_sha256_le32": (C.c_uint32, [C.c_char_p, _i64]),
 }
 
 

@@ -169,6 +169,25 @@ class DeviceFederation:
             self._copied.record()
         return self._perm_dev
 
+    def descriptor_array(self, participants, meta, lr: float, deltas: torch.Tensor,
+                         perm_base: int | None = None) -> np.ndarray:
+        """fedhc_client records for the round as a numpy structured array (vectorised packing)."""
+        k = len(participants)
+        rec = np.zeros(k, dtype=CLIENT_DTYPE)
+        if k == 0:
+            return rec
+        F = self.n_features
+        off = np.fromiter((self.offset[c][0] for c in participants), dtype=np.int64, count=k)
+        m = np.asarray(meta, dtype=np.int64).reshape(k, 4)
+        pb = self._perm_dev.data_ptr() if perm_base is None else perm_base
+        rec["x"] = self.x.data_ptr() + off * (F * 4)
+        rec["y"] = self.y.data_ptr() + off * 4
+        rec["perm"] = pb + m[:, 0] * 4
+        rec["n_rows"], rec["n_batches"], rec["batch_size"] = m[:, 1], m[:, 2], m[:, 3]
+        rec["lr"] = lr
+        rec["delta"] = deltas.data_ptr() + np.arange(k, dtype=np.int64) * (deltas.stride(0) * 4)
+        return rec
+
     def descriptors(self, participants, meta, lr: float, deltas: torch.Tensor) -> torch.Tensor:
         descs = (_abi.Client * max(len(participants), 1))()
         xb, yb, pb = self.x.data_ptr(), self.y.data_ptr(), self._perm_dev.data_ptr() if self._perm_dev is not None \
@@ -215,6 +234,11 @@ class DeviceFederation:
         return 0.0 if self.n_test == 0 else self.correct(params) / self.n_test
 
 
+CLIENT_DTYPE = np.dtype([("x", "<u8"), ("y", "<u8"), ("perm", "<u8"), ("n_rows", "<i4"), ("n_batches", "<i4"),
+                         ("batch_size", "<i4"), ("lr", "<f4"), ("delta", "<u8")])
+assert CLIENT_DTYPE.itemsize == C.sizeof(_abi.Client)
+
+
 def delta_buffer(k: int, P: int, dev) -> torch.Tensor:
     """[k, P] fp32 view with a 16-byte aligned row stride (vectorised FedAvg loads)."""
     ld = (P + 3) // 4 * 4
@@ -248,6 +272,19 @@ def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParam
 
     report = ExperimentReport()
     now = 0.0
+    if fed is not None and cfg.aggregation == "sync" and trace is None:
+        # the serving path: pipelined planning + one launch per kernel per round
+        runner = FederatedRunner(fed, by_id, cfg, train.lr, params=params)
+
+        def record(plan, acc):
+            report.rounds.append(plan.report)
+            report.participants.append(list(plan.all_participants))
+
+        report.accuracy_series.extend(runner.run(cfg.rounds, on_round=record))
+        now = runner.now
+        report.total_time = now
+        report.final_params = params.cpu().numpy()
+        return report
     for r in range(cfg.rounds):
         who = selector.sample(ids, cfg.participants_per_round)
         rep, seg = sim.run(who, cfg, t0=now, round_index=r, want_trace=trace is not None)
@@ -275,3 +312,192 @@ def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParam
     report.total_time = now
     report.final_params = params.cpu().numpy() if params is not None else None
     return report
+
+
+# ---------------------------------------------------------------------------------------------
+# Pipelined round execution (the serving path)
+# ---------------------------------------------------------------------------------------------
+
+
+@dataclass
+class RoundPlan:
+    """Everything the host decides for one round before the GPU runs it."""
+
+    round_index: int
+    participants: list[str]          # this rank's participants, selection order
+    all_participants: list[str]      # the whole round's selection (all ranks)
+    report: RoundReport
+    t0: float
+    weights: list[float]             # this rank's float(num_samples)
+    coef: np.ndarray                 # this rank's w_i / W (W over all ranks)
+    slot: int                        # pinned / device plan buffer used
+    perm_words: int
+    desc: np.ndarray                 # CLIENT_DTYPE records (delta + perm pointers filled)
+
+
+class FederatedRunner:
+    """Round-after-round FedHC execution with host planning overlapped with the GPU.
+
+    plan(r)   [host, worker thread]  selection -> native DES -> native seeds ->
+              native PCG64 permutations straight into a pinned buffer -> descriptors
+    launch(p) [host -> GPU, one stream]  H2D of the plan, fedhc_local_train (all
+              participants), fedhc_fedavg (partial + NCCL all-reduce when sharded),
+              fedhc_eval; the accuracy count lands in pinned memory.
+    run()     keeps one plan in flight: while the GPU executes round r the worker
+              thread plans round r+1.  Plans use double-buffered pinned/device
+              buffers guarded by CUDA events.
+
+    Sync FedAvg semantics (engine.py:350-353); `world`/`rank` shard participants
+    (weak scaling, one all-reduce of fp64 partial sums per round).
+    """
+
+    def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
+                 params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
+                 plan_threads: int = 0):
+        from concurrent.futures import ThreadPoolExecutor
+
+        from .sharding import shard_bounds
+
+        self.fed, self.cfg, self.lr = fed, cfg, float(lr)
+        self.by_id = fleet
+        self.ids = sorted(fleet)
+        self.sim = RoundSimulator(fleet)
+        self.world, self.rank, self.group = world, rank, group
+        self._shard_bounds = shard_bounds
+        self.selector = random.Random(f"{cfg.seed}:selection")
+        dev = fed.x.device
+        self.dev = dev
+        self.params = params if params is not None else torch.zeros(fed.P, dtype=torch.float64, device=dev)
+        k_max = -(-cfg.participants_per_round // world)
+        self.deltas = delta_buffer(max(k_max, 1), fed.P, dev)
+        self.partial = torch.empty(fed.P, dtype=torch.float64, device=dev)
+        self.one = torch.ones(1, dtype=torch.float64, device=dev)
+        self._repr = {cid: repr(cid).encode() for cid in self.ids}
+        self._cap = [0, 0]
+        self._pinned = [None, None]
+        self._dev_plan = [None, None]
+        self._plan_done = [None, None]   # event: H2D of the slot's plan finished
+        self._desc_dev = [torch.empty(max(k_max, 1) * CLIENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+                          for _ in range(2)]
+        self._desc_pin = [torch.empty(max(k_max, 1) * CLIENT_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+                          for _ in range(2)]
+        self._coef_pin = [torch.empty(max(k_max, 1), dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._coef_dev = [torch.empty(max(k_max, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.correct_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.correct_host = torch.zeros(1, dtype=torch.int64).pin_memory()
+        self._pool = ThreadPoolExecutor(max_workers=1)
+        self.plan_threads = plan_threads
+        self.now = 0.0
+        self.round = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 8
+
+    # ---- host side ---------------------------------------------------------
+    def _ensure(self, slot: int, words: int):
+        if self._plan_done[slot] is not None:
+            self._plan_done[slot].synchronize()   # the GPU finished copying this slot's previous plan
+        if words > self._cap[slot]:
+            cap = max(words, 2 * self._cap[slot])
+            self._cap[slot] = cap
+            self._pinned[slot] = torch.empty(cap, dtype=torch.int32).pin_memory()
+            self._dev_plan[slot] = torch.empty(cap, dtype=torch.int32, device=self.dev)
+
+    def plan(self, r: int, t0: float) -> RoundPlan:
+        cfg = self.cfg
+        who = self.selector.sample(self.ids, cfg.participants_per_round)
+        rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
+        lo, hi = self._shard_bounds(len(who), self.world, self.rank)
+        mine = who[lo:hi]
+        k = len(mine)
+        wls = [self.by_id[c].workload for c in who]
+        weights_all = [float(w.num_samples) for w in wls]
+        total = float(sum(weights_all))
+        coef = np.array([w / total for w in weights_all[lo:hi]], dtype=np.float64)
+        reprs = (C.c_char_p * max(k, 1))(*[self._repr[c] for c in mine])
+        train_seeds = np.zeros(max(k, 1), np.uint64)
+        rng_seeds = np.zeros(max(k, 1), np.uint64)
+        _abi.check(_abi.lib.fedhc_round_seeds(int(cfg.seed), int(r), reprs, k, train_seeds.ctypes.data,
+                                              rng_seeds.ctypes.data))
+        meta, rows, perms, at = [], [], [], 0
+        for cid, wl in zip(mine, wls[lo:hi]):
+            _, n = self.fed.offset[cid]
+            kp = n_permutations(n, wl.num_samples, wl.batch_size)
+            meta.append((at, n, math.ceil(wl.num_samples / wl.batch_size), wl.batch_size))
+            rows.append(n)
+            perms.append(kp)
+            at += n * kp
+        slot = r & 1
+        self._ensure(slot, max(at, 1))
+        if at:
+            native_permutations(rng_seeds[:k], rows, perms, out=self._pinned[slot].numpy(), threads=self.plan_threads)
+        desc = self.fed.descriptor_array(mine, meta, self.lr, self.deltas, perm_base=self._dev_plan[slot].data_ptr())
+        return RoundPlan(r, mine, who, rep, t0, weights_all[lo:hi], coef, slot, at, desc)
+
+    # ---- device side -------------------------------------------------------
+    def launch(self, p: RoundPlan) -> None:
+        """Enqueue the round on the current stream (asynchronous)."""
+        from .sharding import combine_partials
+
+        k = len(p.participants)
+        slot = p.slot
+        if p.perm_words:
+            self._dev_plan[slot][:p.perm_words].copy_(self._pinned[slot][:p.perm_words], non_blocking=True)
+        nb = k * CLIENT_DTYPE.itemsize
+        if k:
+            self._desc_pin[slot].numpy()[:nb] = p.desc.view(np.uint8)
+            self._desc_dev[slot][:nb].copy_(self._desc_pin[slot][:nb], non_blocking=True)
+            self._coef_pin[slot].numpy()[:k] = p.coef
+            self._coef_dev[slot][:k].copy_(self._coef_pin[slot][:k], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._plan_done[slot] = ev
+        self.h2d_bytes = p.perm_words * 4 + nb + k * 8
+        if k:
+            max_b = max(int(x) for x in p.desc["batch_size"])
+            _abi.check(_abi.lib.fedhc_local_train(self._desc_dev[slot].data_ptr(), k, self.params.data_ptr(),
+                                                  self.fed.n_features, self.fed.n_classes, max_b, stream_ptr()))
+        if self.world == 1:
+            if k:
+                fedavg_device(self.deltas[:k], self._coef_dev[slot][:k], self.params, self.params)
+        else:
+            if k:
+                fedavg_device(self.deltas[:k], self._coef_dev[slot][:k], None, self.partial)
+            else:
+                self.partial.zero_()
+            combine_partials(self.partial, self.params,
+                             lambda s, prm: fedavg_device(s.view(1, -1), self.one, prm, prm), self.group)
+        self.correct_dev.zero_()
+        if self.fed.n_test:
+            _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
+                                           self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                                           self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
+        if self.world > 1:
+            from .sharding import all_reduce_count
+            all_reduce_count(self.correct_dev, self.group)
+        self.correct_host.copy_(self.correct_dev, non_blocking=True)
+        self._done = torch.cuda.Event()
+        self._done.record()
+
+    def wait_correct(self) -> int:
+        self._done.synchronize()
+        return int(self.correct_host.item())
+
+    def run(self, rounds: int, n_test_total: int | None = None, on_round=None):
+        """Run `rounds` rounds; returns [(round_end_time, accuracy)] (engine.py:350-353 sync semantics)."""
+        n_test = n_test_total if n_test_total is not None else self.fed.n_test
+        series = []
+        fut = self._pool.submit(self.plan, self.round, self.now)
+        for i in range(rounds):
+            p = fut.result()
+            end = p.t0 + p.report.makespan
+            if i + 1 < rounds:
+                fut = self._pool.submit(self.plan, p.round_index + 1, end)
+            self.launch(p)
+            correct = self.wait_correct()
+            acc = correct / n_test if n_test else 0.0
+            series.append((end, acc))
+            if on_round is not None:
+                on_round(p, acc)
+        self.round += rounds
+        self.now = series[-1][0] if series else self.now
+        return series
