@@ -203,3 +203,30 @@ def test_dataset_partition_and_batch_order():
             e, j = divmod(s, bpe)
             assert np.array_equal(perm[e * n + j * b: e * n + j * b + len(rows_)], rows_)
     assert training.stable_seed("train", 1, 0, "c0000") == int(FL["seeds"][0])
+
+
+def test_native_round_seeds_match_stable_seed():
+    import ctypes as C
+    from paper_2305_15668_b200 import _abi
+    ids = [f"c{i:04d}" for i in range(50)] + ["it's", 'q"x', "ü-id", "a\\b", ""]
+    arr = (C.c_char_p * len(ids))(*[repr(c).encode() for c in ids])
+    ts = np.zeros(len(ids), np.uint64)
+    rs = np.zeros(len(ids), np.uint64)
+    for seed, r in [(1, 0), (17, 5), (-3, 2), (2 ** 40, 123)]:
+        _abi.check(_abi.lib.fedhc_round_seeds(seed, r, arr, len(ids), ts.ctypes.data, rs.ctypes.data))
+        for i, c in enumerate(ids):
+            t = fm.seed_of("train", seed, r, c)
+            assert int(ts[i]) == t and int(rs[i]) == fm.seed_of("local_train", t)
+
+
+def test_native_permutations_match_numpy():
+    seeds = [5, 99, 123456, 4294967295, 0, 31337]
+    rows = [6400, 1, 77, 1000, 2, 300]
+    perms = [1, 3, 2, 1, 4, 2]
+    out = training.native_permutations(seeds, rows, perms)
+    at = 0
+    for s, n, k in zip(seeds, rows, perms):
+        g = np.random.default_rng(s)
+        want = np.concatenate([g.permutation(n) for _ in range(k)])
+        assert np.array_equal(out[at:at + n * k], want)
+        at += n * k
