@@ -200,6 +200,18 @@ int fedhc_des_run_round(fedhc_des* sim, const fedhc_des_client* clients, const c
 int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const int32_t** alloc_client,
                     const double** alloc_share, const double** par_t, const int32_t** par_n, int* n_par);
 
+/* ---- green-context SM partitions (executor slots) ------------------------- */
+/* Split the device's SMs into equal groups of >= min_sms (8 on sm_90+) and
+ * hand out streams whose kernels run only on a contiguous group window; the
+ * B200 replacement for per-process MPS percentages.  Contexts/streams are
+ * created on first use of a window and cached. */
+typedef struct fedhc_gctx_pool fedhc_gctx_pool;
+int fedhc_gctx_pool_create(int device, int min_sms, fedhc_gctx_pool** out, int* n_groups, int* sms_per_group);
+void fedhc_gctx_pool_destroy(fedhc_gctx_pool* pool);
+int fedhc_gctx_stream(fedhc_gctx_pool* pool, int first_group, int n_groups, void** stream, int* sm_count);
+/* Diagnostic: `blocks` CTAs on `stream` each write their %smid to out_dev[i]. */
+int fedhc_probe_smid(void* stream, int blocks, int* out_dev);
+
 /* Standalone cost-model helpers (cost_model.py:33-87), for the API layer. */
 double fedhc_work_units(int num_samples, int batch_size, int model_layers, int seq_len,
                         double extra_model_factor, double alpha, double beta);

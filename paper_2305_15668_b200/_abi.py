@@ -121,6 +121,10 @@ SIGNATURES = {
     "fedhc_maxmin_allocate": (_i, [_dp, _dp, _i, _d, _dp]),
     "fedhc_round_seeds": (_i, [_i64, _i64, C.POINTER(C.c_char_p), _i, _vp, _vp]),
     "fedhc_sha256_le32": (C.c_uint32, [C.c_char_p, _i64]),
+    "fedhc_gctx_pool_create": (_i, [_i, _i, C.POINTER(_vp), C.POINTER(_i), C.POINTER(_i)]),
+    "fedhc_gctx_pool_destroy": (None, [_vp]),
+    "fedhc_gctx_stream": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_i)]),
+    "fedhc_probe_smid": (_i, [_vp, _i, _vp]),
 }
 
 

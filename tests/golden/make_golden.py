@@ -273,8 +273,27 @@ def gen_round(engine, profiles, fl_core, classes):
     )
 
 
+def gen_outputs(engine, profiles):
+    """Reference `simulate` writers (cli.py:38-87) on one untrained experiment."""
+    from pathlib import Path
+
+    from fedsim import cli, metrics
+    out = Path(HERE) / "outputs"
+    out.mkdir(exist_ok=True)
+    case = FLEET_CASES[2]
+    fleet = profiles.generate_fleet(profiles.DistributionSpec(**case["spec"]), case["n"], case["seed"])
+    cfg = profiles.FleetConfig(participants_per_round=12, rounds=2, seed=4, theta=120.0, max_executors=6)
+    trace = []
+    rep = engine.run_experiment(cfg, fleet, trace=trace)
+    metrics.write_trace_jsonl(trace, out / "trace.jsonl")
+    cli._write_rounds_csv(out / "rounds.csv", rep)
+    cli._write_clients_csv(out / "clients.csv", rep)
+    profiles.save_fleet(fleet, out / "fleet.csv")
+
+
 def main():
     fedsim, cost_model, engine, fl_core, profiles, scheduler = _ref()
+    gen_outputs(engine, profiles)
     gen_flcore(fl_core, profiles)
     gen_orchestration(fedsim, cost_model, engine, profiles, scheduler)
     gen_train_experiments(engine, profiles)

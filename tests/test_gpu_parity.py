@@ -243,3 +243,69 @@ def test_full_size_round_properties(fh):
     fed.aggregate(params, d1, [1.0] * K)
     mean = d1.double().mean(0)
     assert torch.allclose(params, mean, rtol=1e-12, atol=1e-15)
+
+
+def test_device_fleet_data_partition(fh):
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    ids = [f"c{i:04d}" for i in range(50)]
+    sizes = [int(v) for v in np.random.default_rng(0).choice([16, 32, 64, 128, 256, 512, 1024], 50)]
+    d = DeviceFleetData(ids, sizes, 64, 10, alpha=0.5, seed=5, n_test=1000)
+    assert d.x.shape == (sum(sizes), 64) and d.y.shape == (sum(sizes),)
+    y = d.y.cpu().numpy()
+    for i, cid in enumerate(ids):
+        o, n = d.offsets[cid]
+        assert n == sizes[i]
+        assert np.array_equal(np.bincount(y[o:o + n], minlength=10), d.counts[i])
+    # features cluster around the class means
+    x = d.x[:2000].double()
+    err = (x - d.means[d.y[:2000].long()].double()).std().item()
+    assert 0.9 < err < 1.1
+    fed = d.federation()
+    assert fed.n_test == 1000 and fed.P == 64 * 10 + 10
+
+
+def test_green_partitions_confine_kernels(fh):
+    from paper_2305_15668_b200.live import GreenPartitions
+    parts = GreenPartitions(0, 8)
+    assert parts.n_groups >= 2 and parts.sms_per_group >= 8
+    a = parts.probe(0, 1)
+    b = parts.probe(1, 2)
+    assert 0 < len(a) <= parts.sms_per_group
+    assert 0 < len(b) <= 2 * parts.sms_per_group
+    assert not (a & b), (a, b)  # disjoint windows -> disjoint SMs
+
+
+def test_live_round_matches_batched(fh, tr):
+    """Real-time dispatch on green-context partitions: same deltas as the batched launch."""
+    import torch
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.live import GreenPartitions, LiveRound
+    F, C = 784, 10
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 15, 30, 40, 50, 65, 80), num_samples=[320, 640],
+                                                  batch_size=64), 12, 3)
+    by_id = {p.client_id: p for p in fleet}
+    trn, tst = fm.synthetic(F, C, 12000, seed=1)
+    shards, at = {}, 0
+    for p in fleet:
+        n = p.workload.num_samples
+        shards[p.client_id] = tr.DatasetShard(p.client_id, trn.features[at:at + n], trn.labels[at:at + n])
+        at += n
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, C), F, C)
+    cfg = fh.FleetConfig(participants_per_round=12, max_executors=6, seed=3)
+    who = sorted(by_id)
+    params = torch.zeros(F * C + C, dtype=torch.float64, device="cuda")
+    live = LiveRound(fed, by_id, cfg, 0.1, GreenPartitions(0, 8))
+    d_live, rep, trace, measured = live.run(params, who, round_index=0)
+    seeds = [fm.seed_of("train", cfg.seed, 0, c) for c in who]
+    d_batch = fed.train(params, who, [by_id[c].workload for c in who], 0.1, seeds)
+    assert torch.equal(d_live, d_batch)
+    assert set(measured) == set(who) and all(v > 0 for v in measured.values())
+    assert rep.makespan > 0 and len(rep.per_client_end) == len(who)
+    # first dispatch wave follows the resource-aware scheduler's kickoff
+    launched = [e["client"] for e in trace if e["kind"] == "ClientLaunched"]
+    mgr = fh.planner.ExecutorManager(6, "resource-aware", 100.0) if hasattr(fh, "planner") else None
+    from paper_2305_15668_b200 import planner
+    m = planner.ExecutorManager(6, "resource-aware", 100.0)
+    m.begin_round([planner.Participant(c, float(by_id[c].resource_budget)) for c in who])
+    first = [e.client_id for e, _ in m.kickoff(0.0)]
+    assert launched[:len(first)] == first

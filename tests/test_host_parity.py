@@ -230,3 +230,31 @@ def test_native_permutations_match_numpy():
         want = np.concatenate([g.permutation(n) for _ in range(k)])
         assert np.array_equal(out[at:at + n * k], want)
         at += n * k
+
+
+def test_output_files_byte_identical(tmp_path):
+    """trace.jsonl / rounds.csv / clients.csv / fleet.csv vs the reference's own writers (cli.py:38-87)."""
+    from paper_2305_15668_b200 import reports
+    case = MG.FLEET_CASES[2]
+    fleet = product_fleet(case)
+    cfg = fh.FleetConfig(participants_per_round=12, rounds=2, seed=4, theta=120.0, max_executors=6)
+    trace = []
+    rep = fh.run_experiment(cfg, fleet, trace=trace)
+    reports.write_outputs(str(tmp_path), rep, trace=trace, fleet=fleet, config=cfg)
+    for name in ("trace.jsonl", "rounds.csv", "clients.csv", "fleet.csv"):
+        want = open(os.path.join(GOLDEN, "outputs", name), "rb").read()
+        assert open(tmp_path / name, "rb").read() == want, name
+    summary = json.load(open(tmp_path / "summary.json"))
+    assert summary["participants"] == rep.participants and summary["total_time"] == rep.total_time
+
+
+def test_dirichlet_counts_quotas():
+    from paper_2305_15668_b200.devicedata import dirichlet_counts
+    sizes = [0, 1, 17, 640, 6400, 1024]
+    c = dirichlet_counts(sizes, 10, 0.5, seed=3)
+    assert c.shape == (6, 10) and (c >= 0).all()
+    assert list(c.sum(axis=1)) == sizes
+    flat = dirichlet_counts([2000] * 20, 4, 1000.0, seed=1)
+    assert np.all(np.abs(flat / 2000 - 0.25) < 0.05)            # alpha -> inf: near IID
+    skew = dirichlet_counts([500] * 30, 4, 0.05, seed=1)
+    assert np.mean(skew.max(axis=1) / 500) > 0.7                 # alpha -> 0: concentrated
