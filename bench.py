@@ -56,13 +56,14 @@ def parse():
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
+    ap.add_argument("--classes", type=int, default=10, help="10 (digits) or 62 (FEMNIST classes, 4-CTA clusters)")
     return ap.parse_args()
 
 
 def workload_config(n_gpus):
     return {
-        "workload": "femnist-logreg-c10: FedHC round, multinomial logistic clients (F=784, C=10)",
-        "model": "multinomial logistic regression (reference fl_core model), F=784, C=10",
+        "workload": f"femnist-logreg-c{C}: FedHC round, multinomial logistic clients (F=784, C={C})",
+        "model": f"multinomial logistic regression (reference fl_core model), F=784, C={C}",
         "participants_per_round": PER_GPU * n_gpus,
         "fleet": FLEET_PER_GPU * n_gpus,
         "samples_per_client": N_SAMPLES,
@@ -464,7 +465,9 @@ def run_reference(args, rank, world):
 
 
 def main():
+    global C
     args = parse()
+    C = args.classes
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

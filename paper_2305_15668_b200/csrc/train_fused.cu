@@ -1,5 +1,8 @@
 // Fused per-client local SGD -- fl_core.local_train (fl_core.py:163-194) for
-// FEMNIST-shaped clients (F <= 784, C <= 16), one CTA per client.
+// FEMNIST-shaped clients (F <= 784): one CTA per client for C <= 16, and a
+// thread-block cluster of 2 / 4 CTAs per client for C <= 32 / 64 (e.g. the
+// 62 FEMNIST classes), each CTA owning 16 classes; the softmax is merged
+// across the cluster with an online (row max, row sum) exchange over DSMEM.
 //
 // Per 16-row stage of a batch (rows gathered by the host PCG64 permutation
 // with one 1-D TMA bulk copy per row; producer warp + full/empty mbarriers):
@@ -37,13 +40,13 @@ constexpr int kFSoftWarps = kFRows / 2; // warps 0..7 run the softmax (2 rows ea
 
 struct FusedGeom {
   int F, C, Fp, Fs, Es, Zs, stages, nk8;
-  int off_master, off_x, off_zp, off_e, off_gb, off_lab, off_bar, bytes;
+  int off_master, off_x, off_zp, off_e, off_gb, off_lab, off_bar, off_xch, bytes;
 };
 
 static inline int a16(int v) { return (v + 15) & ~15; }
 
 bool plan_fused(int F, int C, int max_smem, FusedGeom& g) {
-  if (F % 4 != 0 || C > 16) return false;
+  if (F % 4 != 0 || C > 64) return false;
   g.F = F;
   g.C = C;
   g.Fp = (F + 7) / 8 * 8;
@@ -61,7 +64,8 @@ bool plan_fused(int F, int C, int max_smem, FusedGeom& g) {
     g.off_e = off;      off = a16(off + kFRows * g.Es * 4);
     g.off_gb = off;     off = a16(off + kFSoftWarps * 16 * 4 + 16 * 4);
     g.off_lab = off;    off = a16(off + st * kFRows * 4);
-    g.off_bar = off;    off = a16(off + 2 * st * 8);
+    g.off_bar = off;    off = a16(off + 2 * st * 8 + 2 * 8);
+    g.off_xch = off;    off = a16(off + 2 * kFRows * 2 * 4);  // [parity][row] (max, sum)
     g.bytes = off;
     g.stages = st;
     if (off <= max_smem) return true;
@@ -79,7 +83,43 @@ __device__ __forceinline__ void mma_bf16_k8(float (&d)[4], uint32_t a0, uint32_t
 
 // FULL: the feature count fills every warp's slice exactly (F = 784), so no
 // per-step guards (and no reconvergence barriers around movmatrix).
-template <bool FULL>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ float2 ld_cluster_f2(uint32_t cluster_addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(cluster_addr) : "memory");
+  return v;
+}
+
+template <bool FULL, int CL>  // CL = CTAs per client (cluster size), each owning 16 classes
 __global__ void __launch_bounds__(kFThreads, 1)
     train_fused_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params,
                        const FusedGeom g) {
@@ -93,12 +133,18 @@ __global__ void __launch_bounds__(kFThreads, 1)
   int* labels = reinterpret_cast<int*>(smem + g.off_lab);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.off_bar);
   uint64_t* empty = full + g.stages;
+  uint64_t* xbar = empty + g.stages;                 // [2] cluster softmax exchange barriers
+  float2* xch = reinterpret_cast<float2*>(smem + g.off_xch);  // [2][kFRows] (row max, row sum)
 
-  const fedhc_client cl = clients[blockIdx.x];
-  const int F = g.F, C = g.C, Fs = g.Fs, Es = g.Es, Zs = g.Zs, S = g.stages;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  const fedhc_client cl = clients[blockIdx.x / CL];
+  const int Cg = g.C;                                 // classes of the model
+  const int cbase = 16 * static_cast<int>(crank);     // first class owned by this CTA
+  const int C = min(16, Cg - cbase);                  // classes owned by this CTA
+  const int F = g.F, Fs = g.Fs, Es = g.Es, Zs = g.Zs, S = g.stages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const int FC = F * C;
+  const int FC = F * Cg;
 
   for (int i = tid; i < S * kFRows * Fs; i += kFThreads) Xb[i] = 0.f;
   for (int i = tid; i < kFRows * Es; i += kFThreads) E[i] = 0.f;
@@ -108,13 +154,15 @@ __global__ void __launch_bounds__(kFThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    mbar_init(&xbar[0], CL > 1 ? CL - 1 : 1);
+    mbar_init(&xbar[1], CL > 1 ? CL - 1 : 1);
     fence_mbar_init();
   }
 
   const int n = cl.n_rows, B = cl.batch_size;
   const int steps = n > 0 ? cl.n_batches : 0;
-  auto w_at = [&](int f, int c) -> float {
-    return (f < F && c < C) ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
+  auto w_at = [&](int f, int c) -> float {  // c = class index local to this CTA
+    return (f < F && c < C) ? static_cast<float>(params[(size_t)f * Cg + cbase + c]) : 0.f;
   };
   auto active = [&](int j) -> bool { return FULL || (warp * kFK8 + j) < g.nk8; };
 
@@ -133,6 +181,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     }
   }
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
 
   if (warp == kFWarps) {
     // ===== producer warp: TMA row gather of the batch plan =====
@@ -167,7 +216,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     for (int j = 0; j < kFK8; ++j) G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
     const int cls = lane & 15;                      // softmax: half-warp per row, lane = class
     const int srow = 2 * warp + (lane >> 4);        // softmax row of this lane (warps 0..7)
-    float bias = cls < C ? static_cast<float>(params[FC + cls]) : 0.f;
+    float bias = cls < C ? static_cast<float>(params[FC + cbase + cls]) : 0.f;
     float gb = 0.f;
     const float lr = cl.lr;
     bool bias_pending = false;
@@ -261,13 +310,38 @@ __global__ void __launch_bounds__(kFThreads, 1)
           float m = z;
 #pragma unroll
           for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-          const float ex = cls < C ? expf(z - m) : 0.f;
+          float ex = cls < C ? expf(z - m) : 0.f;
           float ssum = ex;
 #pragma unroll
           for (int o = 8; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+          if (CL > 1) {
+            // online-softmax merge over the cluster: (M, S) = (max_i m_i, sum_i s_i exp(m_i - M))
+            const int par = k & 1;
+            if (cls == 0) xch[par * kFRows + srow] = make_float2(m, ssum);
+            asm volatile("bar.sync 2, %0;" ::"n"(kFSoftWarps * 32));
+            if (tid == 0) {
+              asm volatile("fence.acq_rel.cluster;" ::: "memory");
+#pragma unroll
+              for (int r = 1; r < CL; ++r)
+                mbar_arrive_remote(map_to_rank(smem_u32(&xbar[par]), (crank + r) % CL));
+            }
+            mbar_wait_cluster(&xbar[par], (k >> 1) & 1);
+            float Mx = m;
+            float2 peer[CL > 1 ? CL - 1 : 1];
+#pragma unroll
+            for (int r = 1; r < CL; ++r) {
+              peer[r - 1] = ld_cluster_f2(map_to_rank(smem_u32(&xch[par * kFRows + srow]), (crank + r) % CL));
+              Mx = fmaxf(Mx, peer[r - 1].x);
+            }
+            float St = ssum * expf(m - Mx);
+#pragma unroll
+            for (int r = 1; r < CL; ++r) St += peer[r - 1].y * expf(peer[r - 1].x - Mx);
+            ex = cls < C ? expf(z - Mx) : 0.f;
+            ssum = St;
+          }
           float err = 0.f;
           if (srow < rows && cls < C) {
-            err = (ex * __frcp_rn(ssum) - (cls == labels[st * kFRows + srow] ? 1.f : 0.f)) * inv_nb;
+            err = (ex * __frcp_rn(ssum) - (cbase + cls == labels[st * kFRows + srow] ? 1.f : 0.f)) * inv_nb;
             gb += err;
           }
           E[srow * Es + cls] = err;
@@ -342,12 +416,40 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int co[4] = {gq, gq, gq + 8, gq + 8};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (fo[i] < F && co[i] < C)
-            out[(size_t)fo[i] * C + co[i]] = v[i] - static_cast<float>(params[(size_t)fo[i] * C + co[i]]);
+          if (fo[i] < F && co[i] < C) {
+            const size_t gi = (size_t)fo[i] * Cg + cbase + co[i];
+            out[gi] = v[i] - static_cast<float>(params[gi]);
+          }
       }
     }
   }
-  if (tid < C) out[FC + tid] = bias_out[tid] - static_cast<float>(params[FC + tid]);
+  if (tid < C) out[FC + cbase + tid] = bias_out[tid] - static_cast<float>(params[FC + cbase + tid]);
+  if (CL > 1) cluster_sync_all();  // keep shared memory alive until peers are done with it
+}
+
+template <bool FULL, int CL>
+static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, const double* params,
+                                   const FusedGeom& g, cudaStream_t st) {
+  auto kern = train_fused_kernel<FULL, CL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
+  if (e != cudaSuccess) return e;
+  if (CL == 1) {
+    kern<<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_clients * CL);
+  cfg.blockDim = dim3(kFThreads);
+  cfg.dynamicSmemBytes = g.bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, clients, params, g);
 }
 
 // Launch the fused kernel if the shape fits; returns false to fall back.
@@ -355,15 +457,15 @@ bool launch_train_fused(const fedhc_client* clients, int n_clients, const double
                         int max_smem, cudaStream_t st, int* status) {
   FusedGeom g{};
   if (!plan_fused(F, C, max_smem, g)) return false;
+  const int cl = C <= 16 ? 1 : C <= 32 ? 2 : 4;
+  const bool full = g.nk8 == kFWarps * kFK8;
   cudaError_t e;
-  if (g.nk8 == kFWarps * kFK8) {
-    e = cudaFuncSetAttribute(train_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
-    if (e == cudaSuccess) train_fused_kernel<true><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
-  } else {
-    e = cudaFuncSetAttribute(train_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
-    if (e == cudaSuccess) train_fused_kernel<false><<<n_clients, kFThreads, g.bytes, st>>>(clients, params, g);
-  }
-  if (e == cudaSuccess) e = cudaGetLastError();
+  if (cl == 1) e = full ? launch_fused_cl<true, 1>(clients, n_clients, params, g, st)
+                        : launch_fused_cl<false, 1>(clients, n_clients, params, g, st);
+  else if (cl == 2) e = full ? launch_fused_cl<true, 2>(clients, n_clients, params, g, st)
+                             : launch_fused_cl<false, 2>(clients, n_clients, params, g, st);
+  else e = full ? launch_fused_cl<true, 4>(clients, n_clients, params, g, st)
+                : launch_fused_cl<false, 4>(clients, n_clients, params, g, st);
   *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_fused_kernel launch");
   return true;
 }

@@ -66,7 +66,10 @@ def test_local_train_golden_cases(tr, i):
     (784, 10, 100, 100, 32),     # ragged last batch (100 = 3*32 + 4)
     (784, 32, 256, 256, 64),     # NT=4 fast path
     (784, 3, 128, 128, 64),      # NT=1
-    (784, 62, 256, 256, 64),     # FEMNIST 62 classes (generic path)
+    (784, 62, 256, 256, 64),     # FEMNIST 62 classes (4-CTA cluster, softmax merged over DSMEM)
+    (784, 62, 100, 300, 64),     # 62 classes, ragged + reshuffle
+    (784, 20, 128, 128, 64),     # 2-CTA cluster, partial second class slice
+    (392, 40, 96, 96, 32),       # cluster path, F not filling all warps
     (64, 10, 200, 300, 50),      # small F, B not a multiple of 16
     (20, 7, 90, 90, 1),          # batch of one row
     (6, 4, 33, 66, 16),          # F % 4 != 0 -> generic path
@@ -191,26 +194,27 @@ def test_femnist_round_vs_golden(fh, classes):
     assert abs(rep.accuracy_series[0][1] - float(g["acc"][0][1])) <= 2 / 16000
 
 
-def test_batched_round_matches_per_client(fh, tr):
+@pytest.mark.parametrize("C", [10, 62])
+def test_batched_round_matches_per_client(fh, tr, C):
     """DeviceFederation.train (one launch, many clients) == per-client oracle local_train."""
     import torch
     from paper_2305_15668_b200.experiment import DeviceFederation
     from paper_2305_15668_b200.spec import WorkloadSpec
-    trn, tst = fm.synthetic(784, 10, 6000, seed=11)
+    trn, tst = fm.synthetic(784, C, 6000, seed=11)
     sizes = [640, 700, 0, 64, 1000, 333]
     shards, at = {}, 0
     for i, n in enumerate(sizes):
         shards[f"c{i}"] = tr.DatasetShard(f"c{i}", trn.features[at:at + n], trn.labels[at:at + n])
         at += n
-    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, 10), 784, 10)
-    params = np.random.default_rng(2).standard_normal(7850) * 0.01
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, C), 784, C)
+    params = np.random.default_rng(2).standard_normal(784 * C + C) * 0.01
     wl = [WorkloadSpec(n if n else 10, 64) for n in sizes]
     seeds = [fm.seed_of("train", 1, 0, f"c{i}") for i in range(len(sizes))]
     p = torch.from_numpy(params).cuda()
     deltas = fed.train(p, list(shards), wl, 0.1, seeds).cpu().numpy()
     for i, cid in enumerate(shards):
         want = fm.local_sgd(params, fm.Shard(cid, shards[cid].features, shards[cid].labels), wl[i].num_samples,
-                            wl[i].batch_size, 0.1, 10, seed=seeds[i])
+                            wl[i].batch_size, 0.1, C, seed=seeds[i])
         if sizes[i] == 0:
             assert np.all(deltas[i] == 0)
         else:
