@@ -131,6 +131,12 @@ class ClockSampler:
 _CPU = {}
 
 
+def _cpu_init():
+    # one BLAS thread per worker process (numpy/OpenBLAS is already initialised before the fork)
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+
+
 def _cpu_worker(args):
     from oracle import flmath as fm
     i, seed, params = args
@@ -171,7 +177,7 @@ def cpu_reference(seconds: float, rounds: int | None = None, warmup: int = 0):
     steps_per_client = math.ceil(N_SAMPLES / BATCH)
     ctx = mp.get_context("fork")
     done_rounds, t_total = 0, 0.0
-    with ctx.Pool(cores) as pool:
+    with ctx.Pool(cores, initializer=_cpu_init) as pool:
         r = 0
         while True:
             t0 = time.perf_counter()
