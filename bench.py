@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["round", "fedavg"], default="round",
+    ap.add_argument("--workload", choices=["round", "fedavg", "gemm"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
@@ -445,6 +445,54 @@ def run_fedavg(args, rank, world, local_rank):
     return res
 
 
+def run_gemm(args, rank, world, local_rank):
+    """tcgen05 grouped GEMM primitive: per-client FC1 of the FEMNIST CNN head (3136 -> 2048) on a
+    256-sample slab, all clients of a round in one launch.  Reported against the measured bf16 peak."""
+    import torch
+
+    from paper_2305_15668_b200 import _abi
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    G, M, N, K = 100, 2048, 256, 3136
+    g = torch.Generator(device=dev).manual_seed(0)
+    A = torch.randn(G, M, K, device=dev, generator=g).to(torch.bfloat16)
+    B = torch.randn(G, N, K, device=dev, generator=g).to(torch.bfloat16)
+    D = torch.empty(G, M, N, device=dev)
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def step():
+        _abi.check(_abi.lib.fedhc_gemm_bf16_tn(G, M, N, K, A.data_ptr(), B.data_ptr(), D.data_ptr(), sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    flops = 2.0 * G * M * N * K
+    tf = flops / (ms * 1e-3) / 1e12
+    import json as _json
+    try:
+        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"
+    except (OSError, KeyError, ValueError):
+        peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    return {
+        "metric": "grouped GEMM TFLOP/s (tcgen05, per-client FC layer)", "value": tf, "unit": "TFLOP/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in, fp32 accumulate", "data": "synthetic",
+        "config": {"workload": f"grouped GEMM G={G} M={M} N={N} K={K} (D = A.B^T per group)"},
+        "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                     "traffic": None, "kernel": "grouped_gemm_kernel", "peak_source": src},
+        "clocks": clocks.summary(), "gpu_launches": args.steps,
+    }
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
     if rank != 0:
@@ -483,6 +531,8 @@ def main():
         res = run_reference(args, rank, world)
     elif args.workload == "fedavg":
         res = run_fedavg(args, rank, world, local_rank)
+    elif args.workload == "gemm":
+        res = run_gemm(args, rank, world, local_rank)
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:

@@ -200,6 +200,14 @@ int fedhc_des_run_round(fedhc_des* sim, const fedhc_des_client* clients, const c
 int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const int32_t** alloc_client,
                     const double** alloc_share, const double** par_t, const int32_t** par_n, int* n_par);
 
+/* ---- tcgen05 grouped GEMM (client-model contractions) -------------------- */
+/* D_g[M x N] (fp32) = A_g[M x K] (bf16, row-major) . B_g[N x K]^T (bf16,
+ * row-major) for g in [0, G): one launch for all clients of a round.
+ * TMA (128B swizzle) -> tcgen05.mma (M=128, N=128, K=16) -> TMEM -> tcgen05.ld.
+ * Requires M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned operands.
+ * A, B: dev [G][M][K], [G][N][K]; D: dev [G][M][N]. */
+int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream);
+
 /* ---- green-context SM partitions (executor slots) ------------------------- */
 /* Split the device's SMs into equal groups of >= min_sms (8 on sm_90+) and
  * hand out streams whose kernels run only on a contiguous group window; the

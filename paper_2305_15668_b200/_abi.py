@@ -125,6 +125,7 @@ SIGNATURES = {
     "fedhc_gctx_pool_destroy": (None, [_vp]),
     "fedhc_gctx_stream": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_i)]),
     "fedhc_probe_smid": (_i, [_vp, _i, _vp]),
+    "fedhc_gemm_bf16_tn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -313,3 +313,20 @@ def test_live_round_matches_batched(fh, tr):
     m.begin_round([planner.Participant(c, float(by_id[c].resource_budget)) for c in who])
     first = [e.client_id for e, _ in m.kickoff(0.0)]
     assert launched[:len(first)] == first
+
+
+@pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 64), (3, 256, 384, 512), (5, 2048, 128, 3136 // 64 * 64)])
+def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
+    """tcgen05 grouped GEMM (bf16 in, fp32 accumulate) vs torch fp32 on the same bf16 values."""
+    import torch
+    from paper_2305_15668_b200 import _abi
+    g = torch.Generator(device="cuda").manual_seed(G * 7 + M)
+    A = torch.randn(G, M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    D = torch.full((G, M, N), float("nan"), device="cuda")
+    _abi.check(_abi.lib.fedhc_gemm_bf16_tn(G, M, N, K, A.data_ptr(), B.data_ptr(), D.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream))
+    ref = torch.bmm(A.float(), B.float().transpose(1, 2))
+    assert torch.isfinite(D).all()
+    err = (D - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
