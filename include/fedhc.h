@@ -203,7 +203,7 @@ int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const 
 /* ---- tcgen05 grouped GEMM (client-model contractions) -------------------- */
 /* D_g[M x N] (fp32) = A_g[M x K] (bf16, row-major) . B_g[N x K]^T (bf16,
  * row-major) for g in [0, G): one launch for all clients of a round.
- * TMA (128B swizzle) -> tcgen05.mma (M=128, N=128, K=16) -> TMEM -> tcgen05.ld.
+ * TMA (128B swizzle) -> tcgen05.mma (M=128, N=128|256, K=16) -> TMEM -> tcgen05.ld.
  * Requires M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned operands.
  * A, B: dev [G][M][K], [G][N][K]; D: dev [G][M][N]. */
 int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream);

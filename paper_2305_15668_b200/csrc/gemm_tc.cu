@@ -11,8 +11,9 @@
 //           land 128x64 bf16 A/B tiles in the canonical K-major SW128 layout
 //           into a 4-stage ring (full/empty mbarriers, expect_tx bytes).
 //   warp 1  MMA issuer: one elected thread issues tcgen05.mma.cta_group::1
-//           .kind::f16 (M=128, N=128, K=16) from shared-memory descriptors into
-//           a double-buffered TMEM accumulator (2 x 128 fp32 columns);
+//           .kind::f16 (M=128, N=BN in {128, 256}, K=16) from shared-memory
+//           descriptors into a double-buffered TMEM accumulator (2 x BN fp32
+//           columns; all 512 columns at BN=256);
 //           tcgen05.commit releases ring stages and signals the epilogue.
 //   warps 2-5  epilogue: tcgen05.ld (32x32b.x32) TMEM -> registers -> global,
 //           one TMEM lane quadrant per warp, then release the accumulator.
@@ -29,16 +30,23 @@ namespace fedhc {
 
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 192;
-constexpr int kTileABytes = BM * BK * 2, kTileBBytes = BN * BK * 2;
-constexpr int kStageBytes = kTileABytes + kTileBBytes;
-constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
-constexpr uint32_t kIdesc = (1u << 4)            // D format: f32
-                            | (1u << 7)          // A format: bf16
-                            | (1u << 10)         // B format: bf16
-                            | ((BN >> 3) << 17)  // N
-                            | ((BM >> 4) << 24); // M
+constexpr int kTileABytes = BM * BK * 2;
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int kTileBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kTileABytes + kTileBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr uint32_t kIdesc = (1u << 4)            // D format: f32
+                                     | (1u << 7)          // A format: bf16
+                                     | (1u << 10)         // B format: bf16
+                                     | ((BN >> 3) << 17)  // N
+                                     | ((BM >> 4) << 24); // M
+  static constexpr int smem_bytes() { return STAGES * kStageBytes + 1024 + 256; }
+};
 
 // K-major, 128-byte-swizzled canonical layout: 8-row core groups 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
@@ -91,9 +99,12 @@ __device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, uint32_t (&r)[32])
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         float* __restrict__ D, int G, int M, int N, int K) {
+  constexpr int STAGES = Cfg<BN>::STAGES, kStageBytes = Cfg<BN>::kStageBytes, kTmemCols = Cfg<BN>::kTmemCols;
+  constexpr uint32_t kIdesc = Cfg<BN>::kIdesc;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the SW128 tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -232,13 +243,13 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// bf16 tensor [G][rows][K] -> map with box {64, 128, 1}, 128-byte swizzle
-static int make_map(CUtensorMap* map, const void* base, int G, int rows, int K) {
+// bf16 tensor [G][rows][K] -> map with box {64, box_rows, 1}, 128-byte swizzle
+static int make_map(CUtensorMap* map, const void* base, int G, int rows, int K, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)G};
   cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)rows * K * 2};
-  cuuint32_t box[3] = {BK, 128, 1};
+  cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -252,26 +263,32 @@ static int make_map(CUtensorMap* map, const void* base, int G, int rows, int K) 
 
 using namespace fedhc;
 
-extern "C" int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream) {
+template <int BN>
+static int launch_gemm(int G, int M, int N, int K, const void* A, const void* B, float* D, cudaStream_t st) {
   using namespace fedhc::tc;
-  if (G < 1 || M < 1 || N < 1 || K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
-  if (M % BM || N % BN || K % BK)
-    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: M, N must be multiples of 128 and K of 64");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
-    return fail(FEDHC_ERR_VALUE, "gemm: operands must be 16-byte aligned");
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, G, M, K);
+  int rc = make_map(&ma, A, G, M, K, BM);
   if (rc) return rc;
-  rc = make_map(&mb, B, G, N, K);
+  rc = make_map(&mb, B, G, N, K, BN);
   if (rc) return rc;
   int dev = 0, sms = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int tiles = G * (M / BM) * (N / BN);
-  const int smem = STAGES * kStageBytes + 1024 + 256;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  grouped_gemm_kernel<<<tiles < sms ? tiles : sms, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(ma, mb, D, G, M,
-                                                                                                     N, K);
+  const int smem = Cfg<BN>::smem_bytes();
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  grouped_gemm_kernel<BN><<<tiles < sms ? tiles : sms, kThreads, smem, st>>>(ma, mb, D, G, M, N, K);
   FEDHC_CUDA_TRY(cudaGetLastError());
   return FEDHC_OK;
+}
+
+extern "C" int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream) {
+  using namespace fedhc::tc;
+  if (G < 1 || M < 1 || N < 1 || K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
+  if (M % BM || N % 128 || K % BK)
+    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: M, N must be multiples of 128 and K of 64");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return fail(FEDHC_ERR_VALUE, "gemm: operands must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return N % 256 == 0 ? launch_gemm<256>(G, M, N, K, A, B, D, st) : launch_gemm<128>(G, M, N, K, A, B, D, st);
 }

@@ -315,7 +315,8 @@ def test_live_round_matches_batched(fh, tr):
     assert launched[:len(first)] == first
 
 
-@pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 64), (3, 256, 384, 512), (5, 2048, 128, 3136 // 64 * 64)])
+@pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 64), (3, 256, 384, 512), (5, 2048, 128, 3136 // 64 * 64),
+                                     (2, 256, 512, 1024), (7, 384, 256, 3136 // 64 * 64)])
 def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
     """tcgen05 grouped GEMM (bf16 in, fp32 accumulate) vs torch fp32 on the same bf16 values."""
     import torch
