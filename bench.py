@@ -62,8 +62,10 @@ def parse():
 
 def workload_config(n_gpus):
     return {
-        "workload": f"femnist-logreg-c{C}: FedHC round, multinomial logistic clients (F=784, C={C})",
-        "model": f"multinomial logistic regression (reference fl_core model), F=784, C={C}",
+        "workload": f"femnist-logreg-c{C}: FedHC round of multinomial-logistic clients (reference fl_core model), "
+                    f"F=784, C={C}",
+        "arithmetic": "fp32 storage/SGD state; products on the bf16 tensor pipe as bf16x3 (hi*hi+hi*mid+mid*hi, "
+                      "fp32 accumulate); FedAvg in fp64",
         "participants_per_round": PER_GPU * n_gpus,
         "fleet": FLEET_PER_GPU * n_gpus,
         "samples_per_client": N_SAMPLES,
@@ -74,8 +76,6 @@ def workload_config(n_gpus):
         "scheduler": "resource-aware, dynamic parallelism",
         "max_executors": EXECUTORS,
         "aggregation": "sync FedAvg (fp64) + accuracy on 16000 test rows every round",
-        "global_batch": BATCH * PER_GPU * n_gpus,
-        "seq_len": 1,
         "parallelism": f"clients sharded over {n_gpus} GPU(s)" + (", NCCL all-reduce of FedAvg partials" if n_gpus > 1
                                                                   else ""),
         "l2": "inputs larger than L2 (2.0 GB of client rows per GPU per round vs 126 MB L2); no flush needed",
@@ -352,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp32 (3xTF32 tensor-core products, fp32 SGD state, fp64 FedAvg)",
+        "dtype": "f32",
         "data": "synthetic, generated in HBM: Gaussian class clusters + Dirichlet(0.5) non-IID client label mix "
                 "(reference distributions, not the reference's RNG stream)",
         "config": workload_config(world),
@@ -437,7 +437,7 @@ def run_fedavg(args, rank, world, local_rank):
         "metric": "FedAvg aggregated client-delta bytes/sec (config 5)",
         "value": world * alg_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 deltas, fp64 accumulation", "data": "synthetic N(0,1e-3) deltas, N(0,1) base",
+        "dtype": "f64", "data": "synthetic N(0,1e-3) fp32 deltas, N(0,1) fp64 base",
         "config": {"workload": f"fedavg K={K} P={P} per GPU", "l2": "inputs larger than L2"},
         "roofline": roofline_entry(alg_bytes, ms, ROOT, kernel="fedavg_kernel"),
         "clocks": clocks.summary(), "gpu_launches": args.steps * (1 if world == 1 else 2),
@@ -485,7 +485,7 @@ def run_gemm(args, rank, world, local_rank):
     return {
         "metric": "grouped GEMM TFLOP/s (tcgen05, per-client FC layer)", "value": tf, "unit": "TFLOP/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in, fp32 accumulate", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"grouped GEMM G={G} M={M} N={N} K={K} (D = A.B^T per group)"},
         "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
                      "traffic": None, "kernel": "grouped_gemm_kernel", "peak_source": src},
@@ -510,7 +510,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp64 (reference numpy)",
+        "dtype": "f64",
         "data": "synthetic",
         "config": workload_config(1),
         "cpu_baseline": {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port", "sample": sample},
