@@ -338,24 +338,27 @@ class RoundPlan:
 class FederatedRunner:
     """Round-after-round FedHC execution with host planning overlapped with the GPU.
 
-    plan(r)   [host, worker thread]  selection -> native DES -> native seeds ->
-              native PCG64 permutations straight into a pinned buffer -> descriptors
+    plan(r)   [host, planner thread]  selection -> native DES -> native seeds ->
+              native PCG64 permutations straight into a pinned slot -> descriptors
     launch(p) [host -> GPU, one stream]  H2D of the plan, fedhc_local_train (all
               participants), fedhc_fedavg (partial + NCCL all-reduce when sharded),
-              fedhc_eval; the accuracy count lands in pinned memory.
-    run()     keeps one plan in flight: while the GPU executes round r the worker
-              thread plans round r+1.  Plans use double-buffered pinned/device
-              buffers guarded by CUDA events.
+              fedhc_eval; the accuracy count is copied D2H into the slot's pinned word.
+    run()     a bounded pipeline: the planner thread runs up to two rounds ahead
+              (3 plan slots recycled through a free-slot queue, each guarded by the
+              CUDA event of its H2D copy), and the main thread launches round r+1
+              before reading round r's accuracy, so the GPU always has the next
+              round queued.  Every round still copies its inputs H2D and reads its
+              result D2H.
 
     Sync FedAvg semantics (engine.py:350-353); `world`/`rank` shard participants
     (weak scaling, one all-reduce of fp64 partial sums per round).
     """
 
+    SLOTS = 3
+
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
                  plan_threads: int = 0):
-        from concurrent.futures import ThreadPoolExecutor
-
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -368,24 +371,24 @@ class FederatedRunner:
         dev = fed.x.device
         self.dev = dev
         self.params = params if params is not None else torch.zeros(fed.P, dtype=torch.float64, device=dev)
-        k_max = -(-cfg.participants_per_round // world)
-        self.deltas = delta_buffer(max(k_max, 1), fed.P, dev)
+        k_max = max(-(-cfg.participants_per_round // world), 1)
+        self.deltas = delta_buffer(k_max, fed.P, dev)
         self.partial = torch.empty(fed.P, dtype=torch.float64, device=dev)
         self.one = torch.ones(1, dtype=torch.float64, device=dev)
         self._repr = {cid: repr(cid).encode() for cid in self.ids}
-        self._cap = [0, 0]
-        self._pinned = [None, None]
-        self._dev_plan = [None, None]
-        self._plan_done = [None, None]   # event: H2D of the slot's plan finished
-        self._desc_dev = [torch.empty(max(k_max, 1) * CLIENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-                          for _ in range(2)]
-        self._desc_pin = [torch.empty(max(k_max, 1) * CLIENT_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
-                          for _ in range(2)]
-        self._coef_pin = [torch.empty(max(k_max, 1), dtype=torch.float64).pin_memory() for _ in range(2)]
-        self._coef_dev = [torch.empty(max(k_max, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        n = self.SLOTS
+        self._cap = [0] * n
+        self._pinned = [None] * n
+        self._dev_plan = [None] * n
+        self._plan_done = [None] * n   # event: H2D of the slot's plan finished
+        nb = k_max * CLIENT_DTYPE.itemsize
+        self._desc_dev = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(n)]
+        self._desc_pin = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(n)]
+        self._coef_pin = [torch.empty(k_max, dtype=torch.float64).pin_memory() for _ in range(n)]
+        self._coef_dev = [torch.empty(k_max, dtype=torch.float64, device=dev) for _ in range(n)]
         self.correct_dev = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.correct_host = torch.zeros(1, dtype=torch.int64).pin_memory()
-        self._pool = ThreadPoolExecutor(max_workers=1)
+        self._correct_pin = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(n)]
+        self._result_ev = [None] * n
         self.plan_threads = plan_threads
         self.now = 0.0
         self.round = 0
@@ -402,8 +405,9 @@ class FederatedRunner:
             self._pinned[slot] = torch.empty(cap, dtype=torch.int32).pin_memory()
             self._dev_plan[slot] = torch.empty(cap, dtype=torch.int32, device=self.dev)
 
-    def plan(self, r: int, t0: float) -> RoundPlan:
+    def plan(self, r: int, t0: float, slot: int | None = None) -> RoundPlan:
         cfg = self.cfg
+        slot = (r % self.SLOTS) if slot is None else slot
         who = self.selector.sample(self.ids, cfg.participants_per_round)
         rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
         lo, hi = self._shard_bounds(len(who), self.world, self.rank)
@@ -426,7 +430,6 @@ class FederatedRunner:
             rows.append(n)
             perms.append(kp)
             at += n * kp
-        slot = r & 1
         self._ensure(slot, max(at, 1))
         if at:
             native_permutations(rng_seeds[:k], rows, perms, out=self._pinned[slot].numpy(), threads=self.plan_threads)
@@ -435,8 +438,8 @@ class FederatedRunner:
 
     # ---- device side -------------------------------------------------------
     def launch(self, p: RoundPlan) -> None:
-        """Enqueue the round on the current stream (asynchronous)."""
-        from .sharding import combine_partials
+        """Enqueue the round on the current stream (asynchronous); result lands in slot p.slot."""
+        from .sharding import all_reduce_count, combine_partials
 
         k = len(p.participants)
         slot = p.slot
@@ -472,32 +475,63 @@ class FederatedRunner:
                                            self.fed.n_test, self.fed.n_features, self.fed.n_classes,
                                            self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
         if self.world > 1:
-            from .sharding import all_reduce_count
             all_reduce_count(self.correct_dev, self.group)
-        self.correct_host.copy_(self.correct_dev, non_blocking=True)
-        self._done = torch.cuda.Event()
-        self._done.record()
+        self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        self._result_ev[slot] = done
 
-    def wait_correct(self) -> int:
-        self._done.synchronize()
-        return int(self.correct_host.item())
+    def read_correct(self, slot: int) -> int:
+        self._result_ev[slot].synchronize()
+        return int(self._correct_pin[slot].item())
 
     def run(self, rounds: int, n_test_total: int | None = None, on_round=None):
         """Run `rounds` rounds; returns [(round_end_time, accuracy)] (engine.py:350-353 sync semantics)."""
+        import queue
+        import threading
+
         n_test = n_test_total if n_test_total is not None else self.fed.n_test
-        series = []
-        fut = self._pool.submit(self.plan, self.round, self.now)
-        for i in range(rounds):
-            p = fut.result()
-            end = p.t0 + p.report.makespan
-            if i + 1 < rounds:
-                fut = self._pool.submit(self.plan, p.round_index + 1, end)
+        if rounds <= 0:
+            return []
+        ready: queue.Queue = queue.Queue(maxsize=self.SLOTS - 1)
+        free: queue.Queue = queue.Queue()
+        for sl in range(self.SLOTS):
+            free.put(sl)
+        failure = []
+
+        def planner():
+            t, r0 = self.now, self.round
+            try:
+                for i in range(rounds):
+                    slot = free.get()
+                    pl = self.plan(r0 + i, t, slot)
+                    t = pl.t0 + pl.report.makespan
+                    ready.put(pl)
+            except BaseException as exc:  # surface planner errors in the caller
+                failure.append(exc)
+                ready.put(None)
+
+        th = threading.Thread(target=planner, daemon=True)
+        th.start()
+        series, pending = [], None
+        for _ in range(rounds):
+            p = ready.get()
+            if p is None:
+                raise failure[0]
             self.launch(p)
-            correct = self.wait_correct()
-            acc = correct / n_test if n_test else 0.0
-            series.append((end, acc))
-            if on_round is not None:
-                on_round(p, acc)
+            if pending is not None:   # read the previous round while this one runs
+                series.append(self._finish(pending, n_test, on_round, free))
+            pending = p
+        series.append(self._finish(pending, n_test, on_round, free))
+        th.join()
         self.round += rounds
-        self.now = series[-1][0] if series else self.now
+        self.now = series[-1][0]
         return series
+
+    def _finish(self, p: RoundPlan, n_test: int, on_round, free) -> tuple[float, float]:
+        correct = self.read_correct(p.slot)
+        free.put(p.slot)
+        acc = correct / n_test if n_test else 0.0
+        if on_round is not None:
+            on_round(p, acc)
+        return (p.t0 + p.report.makespan, acc)
