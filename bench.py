@@ -330,6 +330,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     e2e_s = time.perf_counter() - e0
     h2d, d2h = runner.h2d_bytes, runner.d2h_bytes
+    host_ms = {k: round(v / (args.steps + args.warmup) * 1e3, 4) for k, v in runner.host_s.items()}
     if dist is not None:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -362,6 +363,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "client-steps/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "rounds_per_sec": args.steps / e2e_s,
                 "api": "paper_2305_15668_b200.experiment.FederatedRunner.run (pipelined host planning)",
+                "host_ms_per_round": host_ms,
                 "accuracy_last_round": series[-1][1] if series else None},
         "roofline": roof,
         "clocks": clocks.summary(),

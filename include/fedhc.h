@@ -89,6 +89,11 @@ int fedhc_batch_permutations(const uint64_t* seeds, const int32_t* n_rows, const
 int fedhc_round_seeds(int64_t seed, int64_t round_index, const char* const* cid_reprs, int n,
                       uint64_t* train_seeds, uint64_t* rng_seeds);
 uint32_t fedhc_sha256_le32(const char* data, int64_t n);
+/* Same permutations generated on the GPU (device pointers; one CTA per
+ * client; `max_rows` = max n_rows, for the shared-memory staging size). */
+int fedhc_batch_permutations_device(const uint64_t* seeds, const int32_t* n_rows, const int32_t* n_perms,
+                                    const int64_t* offsets, int n_clients, int32_t* out, int max_rows,
+                                    void* stream);
 /* PCG64 state after seeding (for tests against numpy's bit_generator.state). */
 int fedhc_pcg64_state(uint64_t seed, uint64_t* state_hi, uint64_t* state_lo, uint64_t* inc_hi, uint64_t* inc_lo);
 

@@ -116,6 +116,7 @@ SIGNATURES = {
     ),
     "fedhc_work_units": (_d, [_i, _i, _i, _i, _d, _d, _d]),
     "fedhc_batch_permutations": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i]),
+    "fedhc_batch_permutations_device": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp]),
     "fedhc_pcg64_state": (_i, [C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.POINTER(C.c_uint64)]),
     "fedhc_maxmin_allocate": (_i, [_dp, _dp, _i, _d, _dp]),

@@ -22,6 +22,7 @@ import ctypes as C
 import json
 import math
 import random
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -333,6 +334,8 @@ class RoundPlan:
     slot: int                        # pinned / device plan buffer used
     perm_words: int
     desc: np.ndarray                 # CLIENT_DTYPE records (delta + perm pointers filled)
+    meta_bytes: int = 0              # device-plan mode: packed (seed, rows, perms, offset) bytes
+    max_rows: int = 0
 
 
 class FederatedRunner:
@@ -358,7 +361,7 @@ class FederatedRunner:
 
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
-                 plan_threads: int = 0):
+                 plan_threads: int = 0, device_permutations: bool = True):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -390,10 +393,18 @@ class FederatedRunner:
         self._correct_pin = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(n)]
         self._result_ev = [None] * n
         self.plan_threads = plan_threads
+        # device-plan mode: the batch permutations are generated on the GPU (perm_kernel) on a side
+        # stream; the host ships only (seed, n_rows, n_perms, offset) per client.
+        self.device_permutations = device_permutations
+        self._meta_pin = [torch.empty(k_max * 24, dtype=torch.uint8).pin_memory() for _ in range(n)]
+        self._meta_dev = [torch.empty(k_max * 24, dtype=torch.uint8, device=dev) for _ in range(n)]
+        self._plan_stream = torch.cuda.Stream(device=dev)
+        self._train_done = [None] * n   # event: the slot's train kernel retired (plan buffer reusable)
         self.now = 0.0
         self.round = 0
         self.h2d_bytes = 0
         self.d2h_bytes = 8
+        self.host_s = {"select+des": 0.0, "seeds": 0.0, "permutations": 0.0, "descriptors": 0.0, "launch": 0.0}
 
     # ---- host side ---------------------------------------------------------
     def _ensure(self, slot: int, words: int):
@@ -408,8 +419,10 @@ class FederatedRunner:
     def plan(self, r: int, t0: float, slot: int | None = None) -> RoundPlan:
         cfg = self.cfg
         slot = (r % self.SLOTS) if slot is None else slot
+        tick = time.perf_counter()
         who = self.selector.sample(self.ids, cfg.participants_per_round)
         rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
+        t1 = time.perf_counter()
         lo, hi = self._shard_bounds(len(who), self.world, self.rank)
         mine = who[lo:hi]
         k = len(mine)
@@ -422,6 +435,7 @@ class FederatedRunner:
         rng_seeds = np.zeros(max(k, 1), np.uint64)
         _abi.check(_abi.lib.fedhc_round_seeds(int(cfg.seed), int(r), reprs, k, train_seeds.ctypes.data,
                                               rng_seeds.ctypes.data))
+        t2 = time.perf_counter()
         meta, rows, perms, at = [], [], [], 0
         for cid, wl in zip(mine, wls[lo:hi]):
             _, n = self.fed.offset[cid]
@@ -431,19 +445,54 @@ class FederatedRunner:
             perms.append(kp)
             at += n * kp
         self._ensure(slot, max(at, 1))
-        if at:
+        meta_bytes = 0
+        if at and self.device_permutations:
+            buf = self._meta_pin[slot].numpy()
+            sizes = np.asarray(rows, np.int64) * np.asarray(perms, np.int64)
+            offs = np.zeros(k, np.int64)
+            if k > 1:
+                np.cumsum(sizes[:-1], out=offs[1:])
+            buf[:8 * k] = rng_seeds[:k].view(np.uint8)
+            buf[8 * k:12 * k] = np.asarray(rows, np.int32).view(np.uint8)
+            buf[12 * k:16 * k] = np.asarray(perms, np.int32).view(np.uint8)
+            buf[16 * k:24 * k] = offs.view(np.uint8)
+            meta_bytes = 24 * k
+        elif at:
             native_permutations(rng_seeds[:k], rows, perms, out=self._pinned[slot].numpy(), threads=self.plan_threads)
+        t3 = time.perf_counter()
         desc = self.fed.descriptor_array(mine, meta, self.lr, self.deltas, perm_base=self._dev_plan[slot].data_ptr())
-        return RoundPlan(r, mine, who, rep, t0, weights_all[lo:hi], coef, slot, at, desc)
+        t4 = time.perf_counter()
+        hs = self.host_s
+        hs["select+des"] += t1 - tick
+        hs["seeds"] += t2 - t1
+        hs["permutations"] += t3 - t2
+        hs["descriptors"] += t4 - t3
+        return RoundPlan(r, mine, who, rep, t0, weights_all[lo:hi], coef, slot, at, desc, meta_bytes,
+                         max(rows, default=0))
 
     # ---- device side -------------------------------------------------------
     def launch(self, p: RoundPlan) -> None:
         """Enqueue the round on the current stream (asynchronous); result lands in slot p.slot."""
         from .sharding import all_reduce_count, combine_partials
 
+        tick = time.perf_counter()
         k = len(p.participants)
         slot = p.slot
-        if p.perm_words:
+        main = torch.cuda.current_stream()
+        plan_ready = None
+        if p.meta_bytes:
+            ps = self._plan_stream
+            with torch.cuda.stream(ps):
+                if self._train_done[slot] is not None:
+                    ps.wait_event(self._train_done[slot])   # the slot's previous train kernel is done with it
+                self._meta_dev[slot][:p.meta_bytes].copy_(self._meta_pin[slot][:p.meta_bytes], non_blocking=True)
+                md = self._meta_dev[slot].data_ptr()
+                _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
+                                                                    self._dev_plan[slot].data_ptr(), p.max_rows,
+                                                                    ps.cuda_stream))
+                plan_ready = torch.cuda.Event()
+                plan_ready.record(ps)
+        elif p.perm_words:
             self._dev_plan[slot][:p.perm_words].copy_(self._pinned[slot][:p.perm_words], non_blocking=True)
         nb = k * CLIENT_DTYPE.itemsize
         if k:
@@ -453,12 +502,22 @@ class FederatedRunner:
             self._coef_dev[slot][:k].copy_(self._coef_pin[slot][:k], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        self._plan_done[slot] = ev
-        self.h2d_bytes = p.perm_words * 4 + nb + k * 8
+        if plan_ready is not None:
+            main.wait_event(plan_ready)
+            ev2 = torch.cuda.Event()   # pinned meta reusable once the plan stream copied it
+            ev2.record(self._plan_stream)
+            self._plan_done[slot] = ev2
+            self.h2d_bytes = p.meta_bytes + nb + k * 8
+        else:
+            self._plan_done[slot] = ev
+            self.h2d_bytes = p.perm_words * 4 + nb + k * 8
         if k:
-            max_b = max(int(x) for x in p.desc["batch_size"])
+            max_b = int(p.desc["batch_size"].max())
             _abi.check(_abi.lib.fedhc_local_train(self._desc_dev[slot].data_ptr(), k, self.params.data_ptr(),
                                                   self.fed.n_features, self.fed.n_classes, max_b, stream_ptr()))
+        td = torch.cuda.Event()
+        td.record()
+        self._train_done[slot] = td
         if self.world == 1:
             if k:
                 fedavg_device(self.deltas[:k], self._coef_dev[slot][:k], self.params, self.params)
@@ -480,6 +539,7 @@ class FederatedRunner:
         done = torch.cuda.Event()
         done.record()
         self._result_ev[slot] = done
+        self.host_s["launch"] += time.perf_counter() - tick
 
     def read_correct(self, slot: int) -> int:
         self._result_ev[slot].synchronize()

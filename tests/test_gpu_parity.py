@@ -331,3 +331,44 @@ def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
     assert torch.isfinite(D).all()
     err = (D - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+def test_device_permutations_match_numpy(fh):
+    import torch
+    from paper_2305_15668_b200 import _abi
+    seeds = [5, 99, 123456, 4294967295, 0, 31337, 7]
+    rows = [6400, 1, 77, 1000, 2, 300, 70000]   # last one permutes in global memory
+    perms = [1, 3, 2, 1, 4, 2, 1]
+    sizes = np.array(rows, np.int64) * np.array(perms, np.int64)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    dev = lambda a, t: torch.from_numpy(np.ascontiguousarray(a, dtype=t)).cuda()  # noqa: E731
+    s_d, r_d, p_d, o_d = dev(seeds, np.uint64), dev(rows, np.int32), dev(perms, np.int32), dev(offs, np.int64)
+    out = torch.full((int(sizes.sum()),), -1, dtype=torch.int32, device="cuda")
+    _abi.check(_abi.lib.fedhc_batch_permutations_device(s_d.data_ptr(), r_d.data_ptr(), p_d.data_ptr(), o_d.data_ptr(),
+                                                        len(seeds), out.data_ptr(), max(rows[:-1]),
+                                                        torch.cuda.current_stream().cuda_stream))
+    got = out.cpu().numpy()
+    for s, n, k, o in zip(seeds, rows, perms, offs):
+        g = np.random.default_rng(s)
+        assert np.array_equal(got[o:o + n * k], np.concatenate([g.permutation(n) for _ in range(k)]))
+
+
+def test_runner_device_plan_matches_host_plan(fh):
+    """FederatedRunner with GPU-generated batch order == host-generated order, bit for bit, over 3 rounds."""
+    import torch
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.experiment import FederatedRunner
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 30, 50, 80), num_samples=[320, 640, 700],
+                                                  batch_size=[32, 64]), 24, 9)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, 10, 0.5, seed=3, n_test=2000)
+    cfg = fh.FleetConfig(participants_per_round=16, max_executors=8, seed=9)
+    outs = []
+    for device_perm in (False, True):
+        params = torch.zeros(7850, dtype=torch.float64, device="cuda")
+        r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, device_permutations=device_perm)
+        series = r.run(3)
+        outs.append((params.clone(), series))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
