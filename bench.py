@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["round", "fedavg", "gemm"], default="round",
+    ap.add_argument("--workload", choices=["round", "fedavg", "gemm", "des"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
@@ -495,6 +495,45 @@ def run_gemm(args, rank, world, local_rank):
     }
 
 
+def run_des(args):
+    """Round control plane (engine.run_round: schedulers + executor manager + DES + metrics) at
+    N = 100 / 1000 / 2000 participants (resource-aware, theta = 100, 16 executors): native
+    C++ DES vs the reference algorithm (oracle port, Python), same inputs, bit-identical reports."""
+    import paper_2305_15668_b200 as fh
+    from oracle import orchestration as oc
+    from paper_2305_15668_b200.roundsim import RoundSimulator
+    rows = []
+    for n in (100, 1000, 2000):
+        dist = dict(budget_levels=(10, 15, 30, 40, 50, 65, 80))
+        pf = fh.generate_fleet(fh.DistributionSpec(**dist), n, 17)
+        of = oc.fleet(n, 17, **dist)
+        ids = sorted(p.client_id for p in pf)
+        cfg = dict(theta=100.0, max_executors=16, seed=17)
+        sim = RoundSimulator({p.client_id: p for p in pf})
+        reps = max(3, args.steps)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            rep, _ = sim.run(ids, fh.FleetConfig(**cfg), want_trace=False)
+        native = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        orep, _ = oc.simulate_round({c.client_id: c for c in of}, ids, oc.Config(**cfg))
+        ref = time.perf_counter() - t0
+        assert rep.makespan == orep["makespan"] and rep.vacancy_area == orep["vacancy_area"]
+        rows.append({"participants": n, "native_ms": native * 1e3, "reference_ms": ref * 1e3,
+                     "speedup": ref / native, "makespan_s": rep.makespan})
+    top = rows[-1]
+    return {
+        "metric": "round control-plane rounds/sec (schedule + executor manager + DES + metrics)",
+        "value": 1e3 / top["native_ms"], "unit": "rounds/s", "n_gpus": 0, "steps": args.steps, "warmup": 0,
+        "ms_per_step": top["native_ms"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic fleet (generate_fleet, seed 17)",
+        "config": {"workload": "engine.run_round at N=2000 participants, resource-aware, theta=100, 16 executors",
+                   "sweep": rows},
+        "cpu_baseline": {"value": 1e3 / top["reference_ms"], "unit": "rounds/s", "cores": 1, "kind": "port",
+                         "sample": "one round per N with the oracle's Python DES (reference algorithm)"},
+    }
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
     if rank != 0:
@@ -535,6 +574,8 @@ def main():
         res = run_fedavg(args, rank, world, local_rank)
     elif args.workload == "gemm":
         res = run_gemm(args, rank, world, local_rank)
+    elif args.workload == "des":
+        res = run_des(args) if rank == 0 else None
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:
