@@ -213,6 +213,39 @@ int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const 
  * A, B: dev [G][M][K], [G][N][K]; D: dev [G][M][N]. */
 int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream);
 
+/* General form.  Operand storage (per group, bf16, row-major):
+ *   a_mn = 0: A[M][K] (K-major)      a_mn = 1: A[K][M] (MN-major, e.g. W^T of dgrad)
+ *   b_mn = 0: B[N][K]                 b_mn = 1: B[K][N]
+ * Epilogue on acc = A.B^T (fp32), element (g, m, n) at offset g*d_gstride + m*ldd + n:
+ *   FEDHC_EPI_F32            float D
+ *   FEDHC_EPI_BF16           bf16 D
+ *   FEDHC_EPI_BIAS_RELU_BF16 bf16 D = relu(acc + bias), bias[g*bias_gstride + (m or n)]
+ *   FEDHC_EPI_SGD            float master -= lr * acc; bf16 shadow = master (if shadow != NULL)
+ * Requires M % 128 == 0, N % 64 == 0, K % 64 == 0, 16-byte aligned operands,
+ * ldd % 8 == 0 (ldd <= 0 -> N; d_gstride <= 0 -> M*ldd). */
+#define FEDHC_EPI_F32 0
+#define FEDHC_EPI_BF16 1
+#define FEDHC_EPI_BIAS_RELU_BF16 2
+#define FEDHC_EPI_SGD 3
+typedef struct fedhc_gemm_args {
+  int32_t G, M, N, K;
+  int32_t a_mn, b_mn;
+  const void* A;
+  const void* B;
+  int32_t epilogue;
+  int32_t bias_per_row;
+  void* D;
+  int64_t ldd;
+  int64_t d_gstride;
+  const float* bias;
+  int64_t bias_gstride;
+  float* master;
+  void* shadow;
+  float lr;
+  int32_t pad_;
+} fedhc_gemm_args;
+int fedhc_gemm(const fedhc_gemm_args* args, void* stream);
+
 /* ---- green-context SM partitions (executor slots) ------------------------- */
 /* Split the device's SMs into equal groups of >= min_sms (8 on sm_90+) and
  * hand out streams whose kernels run only on a contiguous group window; the

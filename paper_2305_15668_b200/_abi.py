@@ -91,6 +91,20 @@ class DesReport(C.Structure):
     ]
 
 
+class GemmArgs(C.Structure):
+    _fields_ = [
+        ("G", C.c_int32), ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32),
+        ("a_mn", C.c_int32), ("b_mn", C.c_int32),
+        ("A", C.c_void_p), ("B", C.c_void_p),
+        ("epilogue", C.c_int32), ("bias_per_row", C.c_int32),
+        ("D", C.c_void_p), ("ldd", C.c_int64), ("d_gstride", C.c_int64),
+        ("bias", C.c_void_p), ("bias_gstride", C.c_int64),
+        ("master", C.c_void_p), ("shadow", C.c_void_p), ("lr", C.c_float), ("pad_", C.c_int32),
+    ]
+
+
+EPI_F32, EPI_BF16, EPI_BIAS_RELU_BF16, EPI_SGD = range(4)
+
 _vp, _i, _i64, _d, _dp = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.POINTER(C.c_double)
 
 SIGNATURES = {
@@ -127,6 +141,7 @@ SIGNATURES = {
     "fedhc_gctx_stream": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_i)]),
     "fedhc_probe_smid": (_i, [_vp, _i, _vp]),
     "fedhc_gemm_bf16_tn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "fedhc_gemm": (_i, [C.POINTER(GemmArgs), _vp]),
 }
 
 

@@ -1,6 +1,12 @@
 // Grouped GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
-//   D_g[M x N] (fp32) = A_g[M x K] (bf16, K-major) . B_g[N x K]^T (bf16, K-major),  g = 0..G-1
+//   D_g[M x N] = epilogue( A_g[M x K] . B_g[N x K]^T ),  g = 0..G-1, bf16 operands, fp32 accumulate
+//
+// Operands may be K-major ([rows][K], e.g. activations, weights in forward) or
+// MN-major ([K][rows], e.g. the transposed operands of dgrad / wgrad) so no
+// transposes are materialised.  Epilogues: fp32 store, bf16 store,
+// bias (+ per-row or per-column) + ReLU -> bf16, and an in-place SGD step on
+// an fp32 master (W -= lr * acc) with an optional bf16 shadow copy.
 //
 // The per-client dense contraction of the FL client models (one GEMM per
 // client per layer, all clients of a round in one launch): the foundation of
@@ -40,20 +46,29 @@ struct Cfg {
   static constexpr int kTileBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
-  static constexpr uint32_t kIdesc = (1u << 4)            // D format: f32
-                                     | (1u << 7)          // A format: bf16
-                                     | (1u << 10)         // B format: bf16
-                                     | ((BN >> 3) << 17)  // N
-                                     | ((BM >> 4) << 24); // M
   static constexpr int smem_bytes() { return STAGES * kStageBytes + 1024 + 256; }
 };
 
-// K-major, 128-byte-swizzled canonical layout: 8-row core groups 1024 B apart.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+template <int BN, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t idesc() {
+  return (1u << 4)                    // D format: f32
+         | (1u << 7)                  // A format: bf16
+         | (1u << 10)                 // B format: bf16
+         | ((A_MN ? 1u : 0u) << 15)   // A major (1 = MN)
+         | ((B_MN ? 1u : 0u) << 16)   // B major (1 = MN)
+         | ((uint32_t)(BN >> 3) << 17)  // N
+         | ((uint32_t)(BM >> 4) << 24); // M
+}
+
+// Canonical 128-byte-swizzled layouts (CUTLASS make_umma_desc, cute/atom/mma_traits_sm100.hpp):
+//   K-major : 8-row core groups 1024 B apart (SBO), LBO unused; +32 B per K=16 step.
+//   MN-major: 64-element MN atoms 8 KB apart (LBO, one TMA box of 64 K-rows each),
+//             8-row K groups 1024 B apart (SBO); +2048 B per K=16 step.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr, uint32_t lbo_bytes) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);       // start address
-  d |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major) = 1
-  d |= (uint64_t)(1024 >> 4) << 32;                 // SBO = 1024 B
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16; // leading byte offset
+  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset = 1024 B
   d |= (uint64_t)1 << 46;                           // descriptor version (sm100)
   d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
   return d;
@@ -83,11 +98,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-template <int N>
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[N]);
-
-template <>
-__device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -99,14 +110,27 @@ __device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, uint32_t (&r)[32])
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN>
+struct Epilogue {
+  int kind;             // FEDHC_EPI_*
+  void* D;              // F32 / BF16 / BIAS_RELU_BF16 output
+  int64_t ldd, d_gstride;
+  const float* bias;    // BIAS_RELU_BF16
+  int bias_per_row;
+  int64_t bias_gstride;
+  float* master;        // SGD: fp32 master, same indexing as D
+  __nv_bfloat16* shadow;  // SGD: optional bf16 copy
+  float lr;
+};
+
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        float* __restrict__ D, int G, int M, int N, int K) {
+                        int G, int M, int N, int K, const Epilogue ep) {
   constexpr int STAGES = Cfg<BN>::STAGES, kStageBytes = Cfg<BN>::kStageBytes, kTmemCols = Cfg<BN>::kTmemCols;
-  constexpr uint32_t kIdesc = Cfg<BN>::kIdesc;
+  constexpr uint32_t kIdesc = idesc<BN, A_MN, B_MN>();
+  constexpr uint32_t kLboA = A_MN ? 64 * BK * 2 : 16, kLboB = B_MN ? 64 * BK * 2 : 16;
+  constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;  // bytes per K=16
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the SW128 tiles
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   uint64_t* empty = full + STAGES;
@@ -153,9 +177,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], kStageBytes);
-          const uint32_t sa = smem_u32(smem + s * kStageBytes);
-          tma_load_3d(sa, &map_a, &full[s], kb * BK, m0, g);
-          tma_load_3d(sa + kTileABytes, &map_b, &full[s], kb * BK, n0, g);
+          const uint32_t sa = smem_u32(smem + s * kStageBytes), sb = sa + kTileABytes;
+          if (A_MN) {
+#pragma unroll
+            for (int h = 0; h < BM / 64; ++h) tma_load_3d(sa + h * 64 * BK * 2, &map_a, &full[s], m0 + 64 * h, kb * BK, g);
+          } else {
+            tma_load_3d(sa, &map_a, &full[s], kb * BK, m0, g);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int h = 0; h < BN / 64; ++h) tma_load_3d(sb + h * 64 * BK * 2, &map_b, &full[s], n0 + 64 * h, kb * BK, g);
+          } else {
+            tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -177,10 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * kStageBytes);
-          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kTileABytes);
+          const uint64_t da = sw128_desc(sa, kLboA), db = sw128_desc(sa + kTileABytes, kLboB);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the 128-byte swizzle atom
-            umma_bf16(tmem_d, da + 2 * k, db + 2 * k, kIdesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tmem_d, da + (kStepA >> 4) * k, db + (kStepB >> 4) * k, kIdesc, (kb | k) != 0);
           umma_commit(&empty[s]);  // ring stage free once these MMAs retire
           if (++s == STAGES) {
             s = 0;
@@ -191,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
+    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4): thread = one output row
     const int q = warp & 3;
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
@@ -202,16 +236,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int row = m0 + 32 * q + lane;
-      float* drow = D + ((size_t)g * M + row) * N + n0;
-#pragma unroll
+      const int64_t base = (int64_t)g * ep.d_gstride + (int64_t)row * ep.ldd + n0;
+      const float rbias = (ep.kind == FEDHC_EPI_BIAS_RELU_BF16 && ep.bias_per_row)
+                              ? ep.bias[(int64_t)g * ep.bias_gstride + row] : 0.f;
+#pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
-        tmem_ld32<32>(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
+        const int64_t o = base + 32 * c;
+        if (ep.kind == FEDHC_EPI_F32) {
+          float* d = static_cast<float*>(ep.D) + o;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(drow + 32 * c + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                                      __uint_as_float(v[i + 2]),
-                                                                      __uint_as_float(v[i + 3]));
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(d + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        } else if (ep.kind == FEDHC_EPI_SGD) {
+          float* w = ep.master + o;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 m4 = *reinterpret_cast<float4*>(w + i);
+            m4.x -= ep.lr * __uint_as_float(v[i]);
+            m4.y -= ep.lr * __uint_as_float(v[i + 1]);
+            m4.z -= ep.lr * __uint_as_float(v[i + 2]);
+            m4.w -= ep.lr * __uint_as_float(v[i + 3]);
+            *reinterpret_cast<float4*>(w + i) = m4;
+            if (ep.shadow) {
+              __nv_bfloat162* sh = reinterpret_cast<__nv_bfloat162*>(ep.shadow + o + i);
+              sh[0] = __floats2bfloat162_rn(m4.x, m4.y);
+              sh[1] = __floats2bfloat162_rn(m4.z, m4.w);
+            }
+          }
+        } else {
+          const bool relu = ep.kind == FEDHC_EPI_BIAS_RELU_BF16;
+          __nv_bfloat16* d = static_cast<__nv_bfloat16*>(ep.D) + o;
+          const float* cb = (relu && !ep.bias_per_row) ? ep.bias + (int64_t)g * ep.bias_gstride + n0 + 32 * c : nullptr;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float f[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float x = __uint_as_float(v[i + u]);
+              if (relu) x = fmaxf(x + (cb ? cb[i + u] : rbias), 0.f);
+              f[u] = x;
+            }
+            uint4 pk;
+            __nv_bfloat162 t0 = __floats2bfloat162_rn(f[0], f[1]), t1 = __floats2bfloat162_rn(f[2], f[3]);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(f[4], f[5]), t3 = __floats2bfloat162_rn(f[6], f[7]);
+            pk.x = *reinterpret_cast<uint32_t*>(&t0);
+            pk.y = *reinterpret_cast<uint32_t*>(&t1);
+            pk.z = *reinterpret_cast<uint32_t*>(&t2);
+            pk.w = *reinterpret_cast<uint32_t*>(&t3);
+            *reinterpret_cast<uint4*>(d + i) = pk;
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -243,13 +320,13 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// bf16 tensor [G][rows][K] -> map with box {64, box_rows, 1}, 128-byte swizzle
-static int make_map(CUtensorMap* map, const void* base, int G, int rows, int K, int box_rows) {
+// bf16 tensor [G][outer][inner] -> 3-D map, box {64, box_outer, 1}, 128-byte swizzle
+static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)G};
-  cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)rows * K * 2};
-  cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)G};
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)outer * inner * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -258,37 +335,69 @@ static int make_map(CUtensorMap* map, const void* base, int G, int rows, int K, 
   return FEDHC_OK;
 }
 
+template <int BN, bool A_MN, bool B_MN>
+static int launch(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc = A_MN ? make_map(&ma, a.A, a.G, a.K, a.M, 64) : make_map(&ma, a.A, a.G, a.M, a.K, BM);
+  if (rc) return rc;
+  rc = B_MN ? make_map(&mb, a.B, a.G, a.K, a.N, 64) : make_map(&mb, a.B, a.G, a.N, a.K, BN);
+  if (rc) return rc;
+  int dev = 0, sms = 0;
+  FEDHC_CUDA_TRY(cudaGetDevice(&dev));
+  FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int tiles = a.G * (a.M / BM) * (a.N / BN);
+  const int smem = Cfg<BN>::smem_bytes();
+  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN>;
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<tiles < sms ? tiles : sms, kThreads, smem, st>>>(ma, mb, a.G, a.M, a.N, a.K, ep);
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  return FEDHC_OK;
+}
+
+template <int BN>
+static int dispatch_major(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
+  if (a.a_mn && a.b_mn) return launch<BN, true, true>(a, ep, st);
+  if (a.a_mn) return launch<BN, true, false>(a, ep, st);
+  if (a.b_mn) return launch<BN, false, true>(a, ep, st);
+  return launch<BN, false, false>(a, ep, st);
+}
+
 }  // namespace tc
 }  // namespace fedhc
 
 using namespace fedhc;
 
-template <int BN>
-static int launch_gemm(int G, int M, int N, int K, const void* A, const void* B, float* D, cudaStream_t st) {
+extern "C" int fedhc_gemm(const fedhc_gemm_args* args, void* stream) {
   using namespace fedhc::tc;
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, G, M, K, BM);
-  if (rc) return rc;
-  rc = make_map(&mb, B, G, N, K, BN);
-  if (rc) return rc;
-  int dev = 0, sms = 0;
-  FEDHC_CUDA_TRY(cudaGetDevice(&dev));
-  FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int tiles = G * (M / BM) * (N / BN);
-  const int smem = Cfg<BN>::smem_bytes();
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(grouped_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  grouped_gemm_kernel<BN><<<tiles < sms ? tiles : sms, kThreads, smem, st>>>(ma, mb, D, G, M, N, K);
-  FEDHC_CUDA_TRY(cudaGetLastError());
-  return FEDHC_OK;
+  if (!args) return fail(FEDHC_ERR_VALUE, "gemm: null args");
+  const fedhc_gemm_args& a = *args;
+  if (a.G < 1 || a.M < 1 || a.N < 1 || a.K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
+  if (a.M % BM || a.N % 64 || a.K % BK)
+    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: need M % 128 == 0, N % 64 == 0, K % 64 == 0");
+  if ((reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B)) & 15)
+    return fail(FEDHC_ERR_VALUE, "gemm: operands must be 16-byte aligned");
+  Epilogue ep{a.epilogue, a.D, a.ldd > 0 ? a.ldd : a.N, 0, a.bias, a.bias_per_row, a.bias_gstride, a.master,
+              static_cast<__nv_bfloat16*>(a.shadow), a.lr};
+  ep.d_gstride = a.d_gstride > 0 ? a.d_gstride : (int64_t)a.M * ep.ldd;
+  if (ep.kind < FEDHC_EPI_F32 || ep.kind > FEDHC_EPI_SGD) return fail(FEDHC_ERR_VALUE, "gemm: unknown epilogue");
+  if (ep.kind == FEDHC_EPI_SGD ? !ep.master : !ep.D) return fail(FEDHC_ERR_VALUE, "gemm: missing output");
+  if (ep.kind == FEDHC_EPI_BIAS_RELU_BF16 && !ep.bias) return fail(FEDHC_ERR_VALUE, "gemm: missing bias");
+  if (ep.ldd % 8) return fail(FEDHC_ERR_VALUE, "gemm: ldd must be a multiple of 8");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (a.N % 256 == 0) return dispatch_major<256>(a, ep, st);
+  if (a.N % 128 == 0) return dispatch_major<128>(a, ep, st);
+  return dispatch_major<64>(a, ep, st);
 }
 
 extern "C" int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream) {
-  using namespace fedhc::tc;
-  if (G < 1 || M < 1 || N < 1 || K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
-  if (M % BM || N % 128 || K % BK)
-    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: M, N must be multiples of 128 and K of 64");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
-    return fail(FEDHC_ERR_VALUE, "gemm: operands must be 16-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return N % 256 == 0 ? launch_gemm<256>(G, M, N, K, A, B, D, st) : launch_gemm<128>(G, M, N, K, A, B, D, st);
+  fedhc_gemm_args a{};
+  a.G = G;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.A = A;
+  a.B = B;
+  a.epilogue = FEDHC_EPI_F32;
+  a.D = D;
+  return fedhc_gemm(&a, stream);
 }

@@ -333,6 +333,67 @@ def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
     assert err < 1e-5, err
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("G,M,N,K", [(1, 128, 64, 64), (3, 256, 192, 320), (2, 128, 256, 1024), (4, 384, 128, 128)])
+def test_gemm_operand_majors_vs_torch(fh, a_mn, b_mn, G, M, N, K):
+    """Every operand storage (K- or MN-major) and N tile (64/128/256) against torch fp32."""
+    import torch
+    from paper_2305_15668_b200.gemm import gemm
+    g = torch.Generator(device="cuda").manual_seed(G * 1000 + M + N + K + 2 * a_mn + b_mn)
+    A = torch.randn(G, M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    ref = torch.bmm(A.float(), B.float().transpose(1, 2))
+    a_op = A.transpose(1, 2).contiguous() if a_mn else A
+    b_op = B.transpose(1, 2).contiguous() if b_mn else B
+    D = gemm(a_op, b_op, a_mn=a_mn, b_mn=b_mn)
+    err = (D - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("per_row", [False, True])
+def test_gemm_bias_relu_bf16_epilogue(fh, per_row):
+    import torch
+    from paper_2305_15668_b200.gemm import EPI_BF16, EPI_BIAS_RELU_BF16, gemm
+    G, M, N, K = 2, 256, 192, 256
+    g = torch.Generator(device="cuda").manual_seed(11 + per_row)
+    A = torch.randn(G, M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    bias = torch.randn(G, M if per_row else N, device="cuda", generator=g)
+    acc = torch.bmm(A.float(), B.float().transpose(1, 2))
+    ref = torch.relu(acc + (bias[:, :, None] if per_row else bias[:, None, :]))
+    D = gemm(A, B, epilogue=EPI_BIAS_RELU_BF16, bias=bias, bias_per_row=per_row)
+    # bf16 rounding (2^-8 relative) of fp32 values that differ only in accumulation order
+    tol = ref.abs() * 2 ** -8 + 1e-5 * acc.abs().max()
+    assert ((D.float() - ref).abs() <= tol).all()
+    D2 = gemm(A, B, epilogue=EPI_BF16)
+    assert ((D2.float() - acc).abs() <= acc.abs() * 2 ** -8 + 1e-5 * acc.abs().max()).all()
+
+
+def test_gemm_sgd_epilogue_in_place(fh):
+    """master -= lr * (A . B^T) in place, bf16 shadow == master rounded."""
+    import torch
+    from paper_2305_15668_b200.gemm import EPI_SGD, gemm
+    G, M, N, K = 3, 128, 320, 512
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(G, K, M, device="cuda", generator=g).to(torch.bfloat16)   # MN-major, like a wgrad
+    B = torch.randn(G, K, N, device="cuda", generator=g).to(torch.bfloat16)
+    W = torch.randn(G, M, N, device="cuda", generator=g)
+    ref = W - 0.01 * torch.bmm(A.float().transpose(1, 2), B.float())
+    shadow = torch.empty(G, M, N, dtype=torch.bfloat16, device="cuda")
+    gemm(A, B, a_mn=True, b_mn=True, epilogue=EPI_SGD, master=W, shadow=shadow, lr=0.01)
+    assert (W - ref).abs().max().item() < 1e-5 * ref.abs().max().item() + 1e-6
+    assert torch.equal(shadow, W.to(torch.bfloat16))
+
+
+def test_gemm_rejects_bad_shapes(fh):
+    import torch
+    from paper_2305_15668_b200.gemm import gemm
+    A = torch.zeros(1, 100, 64, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(NotImplementedError):
+        gemm(A, B)
+
+
 def test_device_permutations_match_numpy(fh):
     import torch
     from paper_2305_15668_b200 import _abi
