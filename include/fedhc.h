@@ -221,12 +221,15 @@ int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B,
  *   FEDHC_EPI_BF16           bf16 D
  *   FEDHC_EPI_BIAS_RELU_BF16 bf16 D = relu(acc + bias), bias[g*bias_gstride + (m or n)]
  *   FEDHC_EPI_SGD            float master -= lr * acc; bf16 shadow = master (if shadow != NULL)
- * Requires M % 128 == 0, N % 64 == 0, K % 64 == 0, 16-byte aligned operands,
- * ldd % 8 == 0 (ldd <= 0 -> N; d_gstride <= 0 -> M*ldd). */
+ *   FEDHC_EPI_RELU_MASK_BF16 bf16 D = acc * (mask > 0), bf16 mask indexed like D (ReLU backward);
+ *                            optional rowsum[g*M + m] = sum over n of the stored D (N <= 256)
+ * Requires M % 64 == 0, N % 32 == 0 (N % 64 == 0 when b_mn), K % 64 == 0,
+ * 16-byte aligned operands, ldd % 8 == 0 (ldd <= 0 -> N; d_gstride <= 0 -> M*ldd). */
 #define FEDHC_EPI_F32 0
 #define FEDHC_EPI_BF16 1
 #define FEDHC_EPI_BIAS_RELU_BF16 2
 #define FEDHC_EPI_SGD 3
+#define FEDHC_EPI_RELU_MASK_BF16 4
 typedef struct fedhc_gemm_args {
   int32_t G, M, N, K;
   int32_t a_mn, b_mn;
@@ -243,6 +246,8 @@ typedef struct fedhc_gemm_args {
   void* shadow;
   float lr;
   int32_t pad_;
+  const void* mask;
+  float* rowsum;
 } fedhc_gemm_args;
 int fedhc_gemm(const fedhc_gemm_args* args, void* stream);
 

@@ -100,10 +100,11 @@ class GemmArgs(C.Structure):
         ("D", C.c_void_p), ("ldd", C.c_int64), ("d_gstride", C.c_int64),
         ("bias", C.c_void_p), ("bias_gstride", C.c_int64),
         ("master", C.c_void_p), ("shadow", C.c_void_p), ("lr", C.c_float), ("pad_", C.c_int32),
+        ("mask", C.c_void_p), ("rowsum", C.c_void_p),
     ]
 
 
-EPI_F32, EPI_BF16, EPI_BIAS_RELU_BF16, EPI_SGD = range(4)
+EPI_F32, EPI_BF16, EPI_BIAS_RELU_BF16, EPI_SGD, EPI_RELU_MASK_BF16 = range(5)
 
 _vp, _i, _i64, _d, _dp = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.POINTER(C.c_double)
 

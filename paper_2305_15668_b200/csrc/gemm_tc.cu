@@ -14,12 +14,13 @@
 //
 // Structure (one persistent CTA per SM, 192 threads, warp-specialised):
 //   warp 0  TMA producer: 3-D tensor maps {K, rows, G} with 128-byte swizzle
-//           land 128x64 bf16 A/B tiles in the canonical K-major SW128 layout
-//           into a 4-stage ring (full/empty mbarriers, expect_tx bytes).
+//           land BMx64 / BNx64 bf16 tiles in the canonical SW128 layouts
+//           into a 4-8 stage ring (full/empty mbarriers, expect_tx bytes).
 //   warp 1  MMA issuer: one elected thread issues tcgen05.mma.cta_group::1
-//           .kind::f16 (M=128, N=BN in {128, 256}, K=16) from shared-memory
-//           descriptors into a double-buffered TMEM accumulator (2 x BN fp32
-//           columns; all 512 columns at BN=256);
+//           .kind::f16 (M=BM in {64, 128}, N=BN in {32..256}, K=16) from
+//           shared-memory descriptors into a double-buffered TMEM accumulator
+//           (2 x BN fp32 columns; all 512 columns at BN=256).  M=64 keeps the
+//           batch-sized (B=64) client GEMMs on the tensor pipe;
 //           tcgen05.commit releases ring stages and signals the epilogue.
 //   warps 2-5  epilogue: tcgen05.ld (32x32b.x32) TMEM -> registers -> global,
 //           one TMEM lane quadrant per warp, then release the accumulator.
@@ -36,20 +37,22 @@ namespace fedhc {
 
 namespace tc {
 
-constexpr int BM = 128, BK = 64;
+constexpr int BK = 64;
 constexpr int kThreads = 192;
-constexpr int kTileABytes = BM * BK * 2;
 
-template <int BN>
+template <int BM, int BN>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int kTileABytes = BM * BK * 2;
   static constexpr int kTileBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
+  static constexpr int STAGES = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
   static constexpr int smem_bytes() { return STAGES * kStageBytes + 1024 + 256; }
 };
 
-template <int BN, bool A_MN, bool B_MN>
+// M=64 accumulators occupy TMEM lanes 0-15 of each 32-lane quadrant (row = 16*q + lane,
+// CUTLASS cute/atom/mma_traits_sm100.hpp tmem_frg M_MMA == 64); M=128 uses all lanes.
+template <int BM, int BN, bool A_MN, bool B_MN>
 __host__ __device__ constexpr uint32_t idesc() {
   return (1u << 4)                    // D format: f32
          | (1u << 7)                  // A format: bf16
@@ -120,14 +123,18 @@ struct Epilogue {
   float* master;        // SGD: fp32 master, same indexing as D
   __nv_bfloat16* shadow;  // SGD: optional bf16 copy
   float lr;
+  const __nv_bfloat16* mask;  // RELU_MASK_BF16: D = acc * (mask > 0), mask indexed like D
+  float* rowsum;        // RELU_MASK_BF16 (optional, single N tile): rowsum[g*M + m] = sum_n D
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BM, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         int G, int M, int N, int K, const Epilogue ep) {
-  constexpr int STAGES = Cfg<BN>::STAGES, kStageBytes = Cfg<BN>::kStageBytes, kTmemCols = Cfg<BN>::kTmemCols;
-  constexpr uint32_t kIdesc = idesc<BN, A_MN, B_MN>();
+  using CF = Cfg<BM, BN>;
+  constexpr int STAGES = CF::STAGES, kStageBytes = CF::kStageBytes, kTmemCols = CF::kTmemCols;
+  constexpr int kTileABytes = CF::kTileABytes;
+  constexpr uint32_t kIdesc = idesc<BM, BN, A_MN, B_MN>();
   constexpr uint32_t kLboA = A_MN ? 64 * BK * 2 : 16, kLboB = B_MN ? 64 * BK * 2 : 16;
   constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;  // bytes per K=16
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -226,7 +233,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4): thread = one output row
+    // (M=64: lanes 0-15 of the quadrant hold rows 16*q + lane)
     const int q = warp & 3;
+    constexpr int kRowsPerWarp = BM / 4;
+    const bool active = lane < kRowsPerWarp;
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -235,14 +245,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + 32 * q + lane;
+      const int row = m0 + kRowsPerWarp * q + (active ? lane : 0);
       const int64_t base = (int64_t)g * ep.d_gstride + (int64_t)row * ep.ldd + n0;
       const float rbias = (ep.kind == FEDHC_EPI_BIAS_RELU_BF16 && ep.bias_per_row)
                               ? ep.bias[(int64_t)g * ep.bias_gstride + row] : 0.f;
+      float rsum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
+        if (!active) continue;
         const int64_t o = base + 32 * c;
         if (ep.kind == FEDHC_EPI_F32) {
           float* d = static_cast<float*>(ep.D) + o;
@@ -267,16 +279,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-          const bool relu = ep.kind == FEDHC_EPI_BIAS_RELU_BF16;
+          const int kind = ep.kind;
           __nv_bfloat16* d = static_cast<__nv_bfloat16*>(ep.D) + o;
-          const float* cb = (relu && !ep.bias_per_row) ? ep.bias + (int64_t)g * ep.bias_gstride + n0 + 32 * c : nullptr;
+          const float* cb = (kind == FEDHC_EPI_BIAS_RELU_BF16 && !ep.bias_per_row)
+                                ? ep.bias + (int64_t)g * ep.bias_gstride + n0 + 32 * c : nullptr;
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
             float f[8];
+            uint4 mk = make_uint4(0, 0, 0, 0);
+            if (kind == FEDHC_EPI_RELU_MASK_BF16) mk = *reinterpret_cast<const uint4*>(ep.mask + o + i);
+            const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               float x = __uint_as_float(v[i + u]);
-              if (relu) x = fmaxf(x + (cb ? cb[i + u] : rbias), 0.f);
+              if (kind == FEDHC_EPI_BIAS_RELU_BF16) x = fmaxf(x + (cb ? cb[i + u] : rbias), 0.f);
+              if (kind == FEDHC_EPI_RELU_MASK_BF16) x = __bfloat162float(mb[u]) > 0.f ? x : 0.f;
               f[u] = x;
             }
             uint4 pk;
@@ -287,9 +304,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk.z = *reinterpret_cast<uint32_t*>(&t2);
             pk.w = *reinterpret_cast<uint32_t*>(&t3);
             *reinterpret_cast<uint4*>(d + i) = pk;
+            // row sum of the stored (bf16-rounded) values, fixed order -> deterministic
+            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) rsum += __bfloat162float(pb[u]);
           }
         }
       }
+      if (ep.rowsum && active) ep.rowsum[(int64_t)g * M + row] = rsum;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -335,7 +357,7 @@ static int make_map(CUtensorMap* map, const void* base, int G, int outer, int in
   return FEDHC_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BM, int BN, bool A_MN, bool B_MN>
 static int launch(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
   CUtensorMap ma, mb;
   int rc = A_MN ? make_map(&ma, a.A, a.G, a.K, a.M, 64) : make_map(&ma, a.A, a.G, a.M, a.K, BM);
@@ -346,20 +368,32 @@ static int launch(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st)
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int tiles = a.G * (a.M / BM) * (a.N / BN);
-  const int smem = Cfg<BN>::smem_bytes();
-  auto kern = grouped_gemm_kernel<BN, A_MN, B_MN>;
+  const int smem = Cfg<BM, BN>::smem_bytes();
+  auto kern = grouped_gemm_kernel<BM, BN, A_MN, B_MN>;
   FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<tiles < sms ? tiles : sms, kThreads, smem, st>>>(ma, mb, a.G, a.M, a.N, a.K, ep);
   FEDHC_CUDA_TRY(cudaGetLastError());
   return FEDHC_OK;
 }
 
-template <int BN>
+template <int BM, int BN>
 static int dispatch_major(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
-  if (a.a_mn && a.b_mn) return launch<BN, true, true>(a, ep, st);
-  if (a.a_mn) return launch<BN, true, false>(a, ep, st);
-  if (a.b_mn) return launch<BN, false, true>(a, ep, st);
-  return launch<BN, false, false>(a, ep, st);
+  if constexpr (BN >= 64) {
+    if (a.a_mn && a.b_mn) return launch<BM, BN, true, true>(a, ep, st);
+    if (a.b_mn) return launch<BM, BN, false, true>(a, ep, st);
+  } else {
+    if (a.b_mn) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: N = 32 tiles need a K-major B operand");
+  }
+  if (a.a_mn) return launch<BM, BN, true, false>(a, ep, st);
+  return launch<BM, BN, false, false>(a, ep, st);
+}
+
+template <int BM>
+static int dispatch_n(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
+  if (a.N % 256 == 0) return dispatch_major<BM, 256>(a, ep, st);
+  if (a.N % 128 == 0) return dispatch_major<BM, 128>(a, ep, st);
+  if (a.N % 64 == 0) return dispatch_major<BM, 64>(a, ep, st);
+  return dispatch_major<BM, 32>(a, ep, st);
 }
 
 }  // namespace tc
@@ -372,21 +406,24 @@ extern "C" int fedhc_gemm(const fedhc_gemm_args* args, void* stream) {
   if (!args) return fail(FEDHC_ERR_VALUE, "gemm: null args");
   const fedhc_gemm_args& a = *args;
   if (a.G < 1 || a.M < 1 || a.N < 1 || a.K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
-  if (a.M % BM || a.N % 64 || a.K % BK)
-    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: need M % 128 == 0, N % 64 == 0, K % 64 == 0");
+  if (a.M % 64 || a.N % 32 || a.K % BK)
+    return fail(FEDHC_ERR_UNSUPPORTED, "gemm: need M % 64 == 0, N % 32 == 0, K % 64 == 0");
   if ((reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B)) & 15)
     return fail(FEDHC_ERR_VALUE, "gemm: operands must be 16-byte aligned");
   Epilogue ep{a.epilogue, a.D, a.ldd > 0 ? a.ldd : a.N, 0, a.bias, a.bias_per_row, a.bias_gstride, a.master,
-              static_cast<__nv_bfloat16*>(a.shadow), a.lr};
+              static_cast<__nv_bfloat16*>(a.shadow), a.lr, static_cast<const __nv_bfloat16*>(a.mask), a.rowsum};
   ep.d_gstride = a.d_gstride > 0 ? a.d_gstride : (int64_t)a.M * ep.ldd;
-  if (ep.kind < FEDHC_EPI_F32 || ep.kind > FEDHC_EPI_SGD) return fail(FEDHC_ERR_VALUE, "gemm: unknown epilogue");
+  if (ep.kind < FEDHC_EPI_F32 || ep.kind > FEDHC_EPI_RELU_MASK_BF16) return fail(FEDHC_ERR_VALUE, "gemm: unknown epilogue");
   if (ep.kind == FEDHC_EPI_SGD ? !ep.master : !ep.D) return fail(FEDHC_ERR_VALUE, "gemm: missing output");
   if (ep.kind == FEDHC_EPI_BIAS_RELU_BF16 && !ep.bias) return fail(FEDHC_ERR_VALUE, "gemm: missing bias");
-  if (ep.ldd % 8) return fail(FEDHC_ERR_VALUE, "gemm: ldd must be a multiple of 8");
+  if (ep.kind == FEDHC_EPI_RELU_MASK_BF16 && !ep.mask) return fail(FEDHC_ERR_VALUE, "gemm: missing mask");
+  if (ep.rowsum && (ep.kind == FEDHC_EPI_F32 || ep.kind == FEDHC_EPI_SGD))
+    return fail(FEDHC_ERR_VALUE, "gemm: rowsum needs a bf16 epilogue");
+  if (ep.ldd % 8 || ep.d_gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: ldd and d_gstride must be multiples of 8");
+  const int bn = a.N % 256 == 0 ? 256 : a.N % 128 == 0 ? 128 : a.N % 64 == 0 ? 64 : 32;
+  if (ep.rowsum && bn != a.N) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: rowsum needs N to fit one tile (N <= 256)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (a.N % 256 == 0) return dispatch_major<256>(a, ep, st);
-  if (a.N % 128 == 0) return dispatch_major<128>(a, ep, st);
-  return dispatch_major<64>(a, ep, st);
+  return a.M % 128 == 0 ? dispatch_n<128>(a, ep, st) : dispatch_n<64>(a, ep, st);
 }
 
 extern "C" int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream) {

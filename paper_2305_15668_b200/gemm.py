@@ -6,6 +6,8 @@ MN-major storage, so forward, dgrad and wgrad all run without transposes.
 
     A: [G, M, K] (a_mn=False) or [G, K, M] (a_mn=True), bf16, contiguous
     B: [G, N, K] (b_mn=False) or [G, K, N] (b_mn=True), bf16, contiguous
+    M % 64 == 0 (M=64 tiles run the UMMA M=64 shape), N % 32 == 0 (N % 64 == 0
+    when b_mn), K % 64 == 0.
 """
 
 from __future__ import annotations
@@ -15,7 +17,7 @@ import ctypes as C
 import torch
 
 from . import _abi
-from ._abi import EPI_BF16, EPI_BIAS_RELU_BF16, EPI_F32, EPI_SGD  # noqa: F401
+from ._abi import EPI_BF16, EPI_BIAS_RELU_BF16, EPI_F32, EPI_RELU_MASK_BF16, EPI_SGD  # noqa: F401
 
 
 def _dims(A: torch.Tensor, B: torch.Tensor, a_mn: bool, b_mn: bool):
@@ -40,6 +42,7 @@ def _dims(A: torch.Tensor, B: torch.Tensor, a_mn: bool, b_mn: bool):
 def gemm(A: torch.Tensor, B: torch.Tensor, *, a_mn: bool = False, b_mn: bool = False, epilogue: int = EPI_F32,
          out: torch.Tensor | None = None, bias: torch.Tensor | None = None, bias_per_row: bool = False,
          master: torch.Tensor | None = None, shadow: torch.Tensor | None = None, lr: float = 0.0,
+         mask: torch.Tensor | None = None, rowsum: torch.Tensor | None = None,
          stream: int | None = None) -> torch.Tensor | None:
     """Launch one grouped GEMM; returns the output tensor (the master for EPI_SGD)."""
     A, B, G, M, N, K = _dims(A, B, a_mn, b_mn)
@@ -71,6 +74,14 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
             args.bias = bias.data_ptr()
             args.bias_gstride = per if bias.numel() == G * per else 0
             keep.append(bias)
+        if epilogue == EPI_RELU_MASK_BF16:
+            if mask is None or mask.dtype != torch.bfloat16 or mask.numel() != G * M * N:
+                raise ValueError("EPI_RELU_MASK_BF16 needs a bf16 mask shaped like the output")
+            args.mask = mask.data_ptr()
+        if rowsum is not None:
+            if rowsum.dtype != torch.float32 or rowsum.numel() != G * M:
+                raise ValueError("rowsum must be fp32 with G*M elements")
+            args.rowsum = rowsum.data_ptr()
         result = out
     s = torch.cuda.current_stream().cuda_stream if stream is None else stream
     _abi.check(_abi.lib.fedhc_gemm(C.byref(args), s))

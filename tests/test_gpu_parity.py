@@ -334,11 +334,15 @@ def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, False), (False, True), (True, True)])
-@pytest.mark.parametrize("G,M,N,K", [(1, 128, 64, 64), (3, 256, 192, 320), (2, 128, 256, 1024), (4, 384, 128, 128)])
+@pytest.mark.parametrize("G,M,N,K", [(1, 128, 64, 64), (3, 256, 192, 320), (2, 128, 256, 1024), (4, 384, 128, 128),
+                                     (3, 64, 64, 2048), (2, 64, 2048, 64), (5, 192, 96, 128), (2, 64, 32, 512),
+                                     (3, 256, 32, 64)])
 def test_gemm_operand_majors_vs_torch(fh, a_mn, b_mn, G, M, N, K):
     """Every operand storage (K- or MN-major) and N tile (64/128/256) against torch fp32."""
     import torch
     from paper_2305_15668_b200.gemm import gemm
+    if b_mn and N % 64:
+        pytest.skip("N=32 tiles take a K-major B only")
     g = torch.Generator(device="cuda").manual_seed(G * 1000 + M + N + K + 2 * a_mn + b_mn)
     A = torch.randn(G, M, K, device="cuda", generator=g).to(torch.bfloat16)
     B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
@@ -383,6 +387,25 @@ def test_gemm_sgd_epilogue_in_place(fh):
     gemm(A, B, a_mn=True, b_mn=True, epilogue=EPI_SGD, master=W, shadow=shadow, lr=0.01)
     assert (W - ref).abs().max().item() < 1e-5 * ref.abs().max().item() + 1e-6
     assert torch.equal(shadow, W.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("M,N", [(2048, 64), (64, 64), (128, 32)])
+def test_gemm_relu_mask_rowsum_epilogue(fh, M, N):
+    """ReLU backward fused in the epilogue: D = acc * (mask > 0), rowsum = sum_n D (bias gradient)."""
+    import torch
+    from paper_2305_15668_b200.gemm import EPI_RELU_MASK_BF16, gemm
+    G, K = 3, 128
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn(G, K, M, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    mask = torch.relu(torch.randn(G, M, N, device="cuda", generator=g)).to(torch.bfloat16)
+    acc = torch.bmm(A.float().transpose(1, 2), B.float().transpose(1, 2))
+    ref = acc * (mask > 0)
+    rs = torch.full((G, M), float("nan"), device="cuda")
+    D = gemm(A, B, a_mn=True, epilogue=EPI_RELU_MASK_BF16, mask=mask, rowsum=rs)
+    assert ((D.float() - ref).abs() <= ref.abs() * 2 ** -8 + 1e-5 * acc.abs().max()).all()
+    assert torch.equal(D == 0, ref.to(torch.bfloat16) == 0) or ((D == 0) != (ref == 0)).sum() < 4
+    assert torch.allclose(rs, D.float().sum(-1), rtol=1e-5, atol=1e-4)
 
 
 def test_gemm_rejects_bad_shapes(fh):
