@@ -248,6 +248,8 @@ typedef struct fedhc_gemm_args {
   int32_t pad_;
   const void* mask;
   float* rowsum;
+  int64_t a_gstride; /* elements between groups of A (0 = dense) */
+  int64_t b_gstride; /* elements between groups of B (0 = dense) */
 } fedhc_gemm_args;
 int fedhc_gemm(const fedhc_gemm_args* args, void* stream);
 
@@ -268,6 +270,34 @@ double fedhc_work_units(int num_samples, int batch_size, int model_layers, int s
                         double extra_model_factor, double alpha, double beta);
 int fedhc_maxmin_allocate(const double* caps, const double* demands, int n, double capacity,
                           double* alloc_out);
+
+
+/* ---- FEMNIST CNN client engine (BASELINE config 2) --------
+ * Builder-defined model (the reference ships only the linear model):
+ * conv5x5 1->32 +ReLU +pool2, conv5x5 32->64 +ReLU +pool2, fc 3136->2048 +ReLU,
+ * fc 2048->C; softmax-CE, plain SGD; the local loop of fl_core.local_train
+ * (fl_core.py:163-194).  Parameters live in a padded fp64/fp32 layout of
+ * fedhc_cnn_param_count() elements; fedhc_cnn_param_offsets() gives the 8
+ * block offsets (Wc1 [64 taps][32], bc1, Wc2 [896][64], bc2, W1 [2048][3200],
+ * b1, W2 [64][2048], b2); padding entries stay exactly zero.
+ * Input rows are 784 fp32 (28x28x1), labels int32. */
+int fedhc_cnn_param_count(int64_t* padded);
+int fedhc_cnn_param_offsets(int64_t* offsets /* [8] */);
+/* Workspace for up to max_clients clients at batch <= 256 (rounded up to 64). */
+int fedhc_cnn_create(int max_clients, int batch, int n_classes, void** ws);
+int fedhc_cnn_destroy(void* ws);
+/* Local SGD of n_clients clients from `params` (dev fp64, padded layout);
+ * clients = dev fedhc_client array (as fedhc_local_train; delta -> [P] fp32
+ * padded layout; lr taken from `lr`).  max_steps = max n_batches.  With
+ * use_graph the step sequence is captured once per (n_clients, max_steps, lr)
+ * and replayed. */
+int fedhc_cnn_local_train(void* ws, const fedhc_client* clients, int n_clients, const double* params,
+                          int max_steps, float lr, int use_graph, void* stream);
+/* Mean CE loss of each client's last step (dev fp32 [n_clients]). */
+int fedhc_cnn_last_loss(void* ws, float* out, int n_clients, void* stream);
+/* *correct (dev u64) += test rows whose first-max argmax == label. */
+int fedhc_cnn_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                   unsigned long long* correct, void* stream);
 
 #ifdef __cplusplus
 }

@@ -100,7 +100,7 @@ class GemmArgs(C.Structure):
         ("D", C.c_void_p), ("ldd", C.c_int64), ("d_gstride", C.c_int64),
         ("bias", C.c_void_p), ("bias_gstride", C.c_int64),
         ("master", C.c_void_p), ("shadow", C.c_void_p), ("lr", C.c_float), ("pad_", C.c_int32),
-        ("mask", C.c_void_p), ("rowsum", C.c_void_p),
+        ("mask", C.c_void_p), ("rowsum", C.c_void_p), ("a_gstride", C.c_int64), ("b_gstride", C.c_int64),
     ]
 
 
@@ -143,6 +143,13 @@ SIGNATURES = {
     "fedhc_probe_smid": (_i, [_vp, _i, _vp]),
     "fedhc_gemm_bf16_tn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "fedhc_gemm": (_i, [C.POINTER(GemmArgs), _vp]),
+    "fedhc_cnn_param_count": (_i, [C.POINTER(C.c_int64)]),
+    "fedhc_cnn_param_offsets": (_i, [C.POINTER(C.c_int64)]),
+    "fedhc_cnn_create": (_i, [_i, _i, _i, C.POINTER(C.c_void_p)]),
+    "fedhc_cnn_destroy": (_i, [_vp]),
+    "fedhc_cnn_local_train": (_i, [_vp, _vp, _i, _vp, _i, C.c_float, _i, _vp]),
+    "fedhc_cnn_last_loss": (_i, [_vp, _vp, _i, _vp]),
+    "fedhc_cnn_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
 }
 
 

@@ -1,0 +1,752 @@
+// FEMNIST CNN client engine: local SGD of every participant of a round on the
+// tensor cores (BASELINE.json config 2).
+//
+// Model (LEAF FEMNIST CNN, builder-defined -- the reference ships only the
+// linear model): conv5x5 1->32 (pad 2) + ReLU + maxpool2, conv5x5 32->64
+// (pad 2) + ReLU + maxpool2, fc 3136->2048 + ReLU, fc 2048->C (C <= 64),
+// softmax cross-entropy (mean over the batch), plain SGD -- the same local
+// loop as fl_core.local_train (fl_core.py:163-194): ceil(num_samples/B) steps
+// over the PCG64 batch order, Δ = new − old.
+//
+// Execution: all K clients of a round advance in lock step; each layer is ONE
+// grouped tcgen05 GEMM over the K clients (gemm_tc.cu), with the ReLU / bias /
+// ReLU-backward / SGD work fused into the GEMM epilogues.  Small
+// data-movement kernels (batch gather + im2col, pooling, col2im, softmax-CE)
+// sit between them.  Weights: fp32 master + bf16 shadow per client (the
+// shadow is what the tensor cores read; the SGD epilogue writes both).
+//
+// Per client, per step (Bp = batch rounded up to 64; rows past the batch are
+// zero and carry zero gradient, so ragged and finished clients are exact):
+//   gather+im2col1  x[perm] -> cols1 [Bp*784][64]   (25 taps, zero-padded)
+//   conv1  GEMM     cols1 . Wc1^T  + b, ReLU -> a1 [Bp*784][32]        (N=32)
+//   pool1           a1 -> p1 [Bp][14][14][32]
+//   im2col2         p1 -> cols2 [Bp*196][896]          (28 taps x 32, 3 zero)
+//   conv2  GEMM     cols2 . Wc2    + b, ReLU -> a2 [Bp*196][64]
+//   pool2           a2 -> p2 [Bp][3200]                (7*7*64 + 64 zero)
+//   fc1    GEMM     W1 . p2^T      + b, ReLU -> hT [2048][Bp]
+//   fc2    GEMM     h . W2^T                  -> logits [Bp][64] fp32  (M=64)
+//   CE              logits + b2 -> dl [Bp][64] = (softmax - onehot) / rows
+//   fc2 dgrad       W2^T . dl^T, ReLU'(hT)   -> dhT [2048][Bp], rowsum = db1
+//   fc2 wgrad+SGD   W2 -= lr dl^T . h                                  (M=64)
+//   fc1 dgrad       dh . W1                  -> dp2 [Bp][3200]         (M=64)
+//   fc1 wgrad+SGD   W1 -= lr dhT . p2
+//   pool2 bwd       dp2, a2 -> da2 [Bp*196][64] (+ db2 partials)
+//   conv2 dgrad     da2 . Wc2^T              -> dcols2 [Bp*196][896]
+//   conv2 wgrad+SGD Wc2 -= lr cols2^T . da2
+//   col2im+pool1 bwd dcols2, a1 -> da1 [32][Bp*784] (channel-major) (+ db1 partials)
+//   conv1 wgrad+SGD Wc1 -= lr cols1^T . da1                     (M=64, N=32)
+//   bias SGD, Wc1 shadow transpose
+// The step sequence of a round is captured once into a CUDA graph and replayed.
+#include <cuda_bf16.h>
+
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "gemm_tc.cuh"
+
+namespace fedhc {
+namespace cnn {
+
+constexpr int HW0 = 784, W0 = 28;              // input 28x28x1
+constexpr int C1 = 32, W1d = 14, HW1 = 196;    // after conv1 + pool
+constexpr int C2 = 64, W2d = 7, HW2 = 49;      // after conv2 + pool
+constexpr int T1 = 64;                         // conv1 im2col width (25 taps)
+constexpr int TAPS2 = 28, K2 = TAPS2 * C1;     // 896
+constexpr int F1 = 3200;                       // fc1 input: 7*7*64 = 3136 + 64 zero
+constexpr int HID = 2048, NC = 64;
+
+// fp32 master / bf16 shadow layout of one client's parameters (elements)
+constexpr int64_t OFF_WC1 = 0;                       // [64 taps][32]   (shadow: [32][64])
+constexpr int64_t OFF_BC1 = OFF_WC1 + T1 * C1;       // [32] (+32 pad)
+constexpr int64_t OFF_WC2 = OFF_BC1 + 64;            // [896][64]
+constexpr int64_t OFF_BC2 = OFF_WC2 + K2 * C2;       // [64]
+constexpr int64_t OFF_W1 = OFF_BC2 + 64;             // [2048][3200]
+constexpr int64_t OFF_B1 = OFF_W1 + (int64_t)HID * F1;  // [2048]
+constexpr int64_t OFF_W2 = OFF_B1 + HID;             // [64][2048]
+constexpr int64_t OFF_B2 = OFF_W2 + NC * HID;        // [64]
+constexpr int64_t PPAD = OFF_B2 + NC;
+static_assert(OFF_BC1 % 64 == 0 && OFF_WC2 % 64 == 0 && OFF_W1 % 64 == 0 && OFF_W2 % 64 == 0 &&
+                  OFF_B2 % 64 == 0 && PPAD % 64 == 0,
+              "16-byte aligned parameter blocks");
+
+__device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ---- gather + im2col of conv1 ------------------------------------------------
+// grid (Bp, G), 256 threads.  perm == nullptr -> rows taken in order (eval).
+__global__ void __launch_bounds__(256) gather_im2col1_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
+                                                             __nv_bfloat16* __restrict__ cols1,
+                                                             int32_t* __restrict__ labels,
+                                                             int32_t* __restrict__ valid) {
+  __shared__ float img[HW0];
+  const int g = blockIdx.y, b = blockIdx.x;
+  const fedhc_client c = cl[g];
+  int rows = 0;
+  int64_t poff = 0;
+  if (c.n_rows > 0 && step < c.n_batches) {
+    if (c.perm) {
+      const BatchRef r = batch_ref(step, c.n_rows, c.batch_size);
+      rows = r.rows;
+      poff = r.perm_off;
+    } else {
+      rows = c.n_rows < Bp ? c.n_rows : Bp;
+    }
+  }
+  const bool ok = b < rows;
+  const int row = ok ? (c.perm ? c.perm[poff + b] : b) : 0;
+  const float* src = c.x + (int64_t)row * HW0;
+  for (int i = threadIdx.x; i < HW0; i += 256) img[i] = ok ? __ldg(src + i) : 0.f;
+  if (threadIdx.x == 0) {
+    labels[(int64_t)g * Bp + b] = ok ? c.y[row] : 0;
+    if (b == 0) valid[g] = rows;
+  }
+  __syncthreads();
+  __nv_bfloat16* dst = cols1 + ((int64_t)g * Bp + b) * HW0 * T1;
+  for (int p = threadIdx.x; p < HW0; p += 256) {
+    const int h = p / W0, w = p - h * W0;
+    __align__(16) __nv_bfloat16 v[T1];
+#pragma unroll
+    for (int t = 0; t < T1; ++t) {
+      float x = 0.f;
+      if (t < 25) {
+        const int ih = h + t / 5 - 2, iw = w + t % 5 - 2;
+        if (ih >= 0 && ih < W0 && iw >= 0 && iw < W0) x = img[ih * W0 + iw];
+      }
+      v[t] = __float2bfloat16_rn(x);
+    }
+    uint4* o = reinterpret_cast<uint4*>(dst + (int64_t)p * T1);
+#pragma unroll
+    for (int i = 0; i < T1 / 8; ++i) o[i] = reinterpret_cast<const uint4*>(v)[i];
+  }
+}
+
+// ---- 2x2 max pool, NHWC, 8 channels per thread ---------------------------------
+// in [n_img][Hin][Hin][C], out image stride out_ld elements ([Hin/2][Hin/2][C] packed)
+__global__ void __launch_bounds__(256) pool_fwd_kernel(const __nv_bfloat16* __restrict__ in,
+                                                       __nv_bfloat16* __restrict__ out, int64_t n_img, int Hin,
+                                                       int C, int out_ld) {
+  const int Ho = Hin / 2, c8 = C / 8;
+  const int64_t total = n_img * Ho * Ho * c8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cg = (int)(i % c8);
+    int64_t r = i / c8;
+    const int ow = (int)(r % Ho);
+    r /= Ho;
+    const int oh = (int)(r % Ho);
+    const int64_t n = r / Ho;
+    const __nv_bfloat16* base = in + ((n * Hin + 2 * oh) * Hin + 2 * ow) * C + cg * 8;
+    uint4 q0 = *reinterpret_cast<const uint4*>(base);
+    uint4 q1 = *reinterpret_cast<const uint4*>(base + C);
+    uint4 q2 = *reinterpret_cast<const uint4*>(base + (int64_t)Hin * C);
+    uint4 q3 = *reinterpret_cast<const uint4*>(base + (int64_t)Hin * C + C);
+    __nv_bfloat162* a = reinterpret_cast<__nv_bfloat162*>(&q0);
+    const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q2);
+    const __nv_bfloat162* b3 = reinterpret_cast<const __nv_bfloat162*>(&q3);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = __hmax2(__hmax2(a[k], b1[k]), __hmax2(b2[k], b3[k]));
+    *reinterpret_cast<uint4*>(out + n * out_ld + ((int64_t)oh * Ho + ow) * C + cg * 8) = q0;
+  }
+}
+
+// ---- im2col of conv2: p1 [n_img][14][14][32] -> cols2 [n_img*196][896] -----------
+__global__ void __launch_bounds__(256) im2col2_kernel(const __nv_bfloat16* __restrict__ p1,
+                                                      __nv_bfloat16* __restrict__ cols2, int64_t n_img) {
+  const int64_t total = n_img * HW1 * TAPS2 * 4;  // 4 x 16 B per (pixel, tap)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i & 3);
+    const int t = (int)((i >> 2) % TAPS2);
+    const int64_t px = (i >> 2) / TAPS2;
+    const int64_t n = px / HW1;
+    const int p = (int)(px - n * HW1), h = p / W1d, w = p - h * W1d;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t < 25) {
+      const int ih = h + t / 5 - 2, iw = w + t % 5 - 2;
+      if (ih >= 0 && ih < W1d && iw >= 0 && iw < W1d)
+        v = *reinterpret_cast<const uint4*>(p1 + ((n * HW1 + ih * W1d + iw) * C1) + q * 8);
+    }
+    *reinterpret_cast<uint4*>(cols2 + px * K2 + t * C1 + q * 8) = v;
+  }
+}
+
+// ---- softmax cross-entropy + gradient ------------------------------------------
+// one CTA per client, one thread per batch row (Bp <= 1024)
+__global__ void ce_kernel(const float* __restrict__ logits, const float* __restrict__ master, int Bp, int C,
+                          const int32_t* __restrict__ labels, const int32_t* __restrict__ valid,
+                          __nv_bfloat16* __restrict__ dl, float* __restrict__ db2, float* __restrict__ loss) {
+  extern __shared__ float ce_s[];  // [Bp][NC] fp32 gradient
+  const int g = blockIdx.x, i = threadIdx.x;
+  const float* bias = master + (int64_t)g * PPAD + OFF_B2;
+  const int rows = valid[g];
+  const float* z = logits + ((int64_t)g * Bp + i) * NC;
+  float* e = ce_s + (int64_t)i * NC;
+  float li = 0.f;
+  if (i < rows) {
+    float mx = -INFINITY;
+    for (int c = 0; c < C; ++c) mx = fmaxf(mx, z[c] + bias[c]);
+    float sum = 0.f;
+    for (int c = 0; c < C; ++c) {
+      e[c] = __expf(z[c] + bias[c] - mx);
+      sum += e[c];
+    }
+    const int y = labels[(int64_t)g * Bp + i];
+    const float inv = 1.f / sum, scale = 1.f / (float)rows;
+    li = -(z[y] + bias[y] - mx - __logf(sum));
+    for (int c = 0; c < NC; ++c) e[c] = c < C ? (e[c] * inv - (c == y ? 1.f : 0.f)) * scale : 0.f;
+  } else {
+    for (int c = 0; c < NC; ++c) e[c] = 0.f;
+  }
+  __nv_bfloat16* d = dl + ((int64_t)g * Bp + i) * NC;
+  for (int c = 0; c < NC; c += 2)
+    *reinterpret_cast<__nv_bfloat162*>(d + c) = __floats2bfloat162_rn(e[c], e[c + 1]);
+  __syncthreads();
+  // bias gradient: column sums of the stored (bf16) gradient, fixed order
+  for (int c = i; c < NC; c += blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < Bp; ++r) s += __bfloat162float(__float2bfloat16_rn(ce_s[(int64_t)r * NC + c]));
+    db2[(int64_t)g * NC + c] = s;
+  }
+  if (loss) {
+    __shared__ float red[32];
+    float v = li;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((i & 31) == 0) red[i >> 5] = v;
+    __syncthreads();
+    if (i == 0) {
+      float s = 0.f;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[w];
+      loss[g] = rows ? s / rows : 0.f;
+    }
+  }
+}
+
+// eval: first-max argmax over the C real classes (fl_core.py:154-160 semantics)
+__global__ void argmax_kernel(const float* __restrict__ logits, const float* __restrict__ master, int n, int C,
+                              const int32_t* __restrict__ labels, unsigned long long* __restrict__ correct) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int hit = 0;
+  if (i < n) {
+    const float* z = logits + (int64_t)i * NC;
+    const float* bias = master + OFF_B2;
+    int best = 0;
+    float bv = z[0] + bias[0];
+    for (int c = 1; c < C; ++c) {
+      const float v = z[c] + bias[c];
+      if (v > bv) {
+        bv = v;
+        best = c;
+      }
+    }
+    hit = best == labels[i];
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(correct, (unsigned long long)__popc(m));
+}
+
+// ---- maxpool2 backward + ReLU mask (first max of the 2x2 window, row-major) -------
+__device__ __forceinline__ int first_max4(float v0, float v1, float v2, float v3) {
+  int k = 0;
+  float m = v0;
+  if (v1 > m) { m = v1; k = 1; }
+  if (v2 > m) { m = v2; k = 2; }
+  if (v3 > m) { k = 3; }
+  return k;
+}
+
+// grid (Bp, G): dp2 [G][Bp][3200], a2 [G][Bp][196][64] -> da2 (same as a2), part [G][Bp][64]
+__global__ void __launch_bounds__(256) pool2_bwd_kernel(const __nv_bfloat16* __restrict__ dp2,
+                                                        const __nv_bfloat16* __restrict__ a2,
+                                                        __nv_bfloat16* __restrict__ da2, float* __restrict__ part,
+                                                        int Bp) {
+  __shared__ float red[4][C2];
+  const int g = blockIdx.y, b = blockIdx.x;
+  const int64_t img = (int64_t)g * Bp + b;
+  const __nv_bfloat16* d = dp2 + img * F1;
+  const __nv_bfloat16* a = a2 + img * HW1 * C2;
+  __nv_bfloat16* o = da2 + img * HW1 * C2;
+  const int c = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  float acc = 0.f;
+  for (int wdw = grp; wdw < HW2; wdw += 4) {
+    const int ph = wdw / W2d, pw = wdw - ph * W2d;
+    const int p00 = (2 * ph) * W1d + 2 * pw;
+    const int pos[4] = {p00, p00 + 1, p00 + W1d, p00 + W1d + 1};
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = bf(a[pos[k] * C2 + c]);
+    const int k = first_max4(v[0], v[1], v[2], v[3]);
+    const __nv_bfloat16 gz = d[wdw * C2 + c];
+    const bool on = v[k] > 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[pos[j] * C2 + c] = (j == k && on) ? gz : __float2bfloat16_rn(0.f);
+    if (on) acc += bf(gz);
+  }
+  red[grp][c] = acc;
+  __syncthreads();
+  if (threadIdx.x < C2)
+    part[img * C2 + threadIdx.x] = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) +
+                                   red[3][threadIdx.x];
+}
+
+constexpr int kC2iSmem = C1 * HW0 * 2;
+
+// grid (Bp, G): col2im of dcols2 + maxpool1 backward + ReLU mask -> da1 channel-major
+// dcols2 [G][Bp*196][896], a1 [G][Bp][784][32] -> da1 [G][32][Bp*784], part [G][Bp][32]
+__global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat16* __restrict__ dcols2,
+                                                               const __nv_bfloat16* __restrict__ a1,
+                                                               __nv_bfloat16* __restrict__ da1,
+                                                               float* __restrict__ part, int Bp) {
+  extern __shared__ __align__(16) unsigned char c2i_smem[];
+  auto tile = reinterpret_cast<__nv_bfloat16(*)[HW0]>(c2i_smem);  // [C1][HW0], 50 KB (dynamic)
+  __shared__ float red[8][C1];
+  const int g = blockIdx.y, b = blockIdx.x;
+  const int64_t img = (int64_t)g * Bp + b;
+  const __nv_bfloat16* dc = dcols2 + img * HW1 * K2;
+  const __nv_bfloat16* a = a1 + img * HW0 * C1;
+  const int ci = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  float acc = 0.f;
+  for (int p = grp; p < HW1; p += 8) {
+    const int ph = p / W1d, pw = p - ph * W1d;
+    float s = 0.f;
+    for (int kh = 0; kh < 5; ++kh) {
+      const int oh = ph - kh + 2;
+      if (oh < 0 || oh >= W1d) continue;
+      for (int kw = 0; kw < 5; ++kw) {
+        const int ow = pw - kw + 2;
+        if (ow < 0 || ow >= W1d) continue;
+        s += bf(dc[(int64_t)(oh * W1d + ow) * K2 + (kh * 5 + kw) * C1 + ci]);
+      }
+    }
+    const int q00 = (2 * ph) * W0 + 2 * pw;
+    const int pos[4] = {q00, q00 + 1, q00 + W0, q00 + W0 + 1};
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = bf(a[pos[k] * C1 + ci]);
+    const int k = first_max4(v[0], v[1], v[2], v[3]);
+    const bool on = v[k] > 0.f;
+    const __nv_bfloat16 gz = __float2bfloat16_rn(on ? s : 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tile[ci][pos[j]] = j == k ? gz : __float2bfloat16_rn(0.f);
+    acc += bf(gz);
+  }
+  red[grp][ci] = acc;
+  __syncthreads();
+  // channel-major store: da1[g][ci][b*784 + p], 16 B per thread
+  const int64_t P1 = (int64_t)Bp * HW0;
+  for (int i = threadIdx.x; i < C1 * (HW0 / 8); i += 256) {
+    const int c = i / (HW0 / 8), q = i - c * (HW0 / 8);
+    *reinterpret_cast<uint4*>(da1 + ((int64_t)g * C1 + c) * P1 + (int64_t)b * HW0 + q * 8) =
+        *reinterpret_cast<const uint4*>(&tile[c][q * 8]);
+  }
+  if (threadIdx.x < C1) {
+    float s = 0.f;
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    part[img * C1 + threadIdx.x] = s;
+  }
+}
+
+// ---- per-client bias SGD + conv1 shadow -----------------------------------------
+__global__ void __launch_bounds__(256) bias_sgd_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ shadow,
+                                                       const float* __restrict__ part1,
+                                                       const float* __restrict__ part2,
+                                                       const float* __restrict__ db1,
+                                                       const float* __restrict__ db2, int Bp, float lr) {
+  const int g = blockIdx.x;
+  float* m = master + (int64_t)g * PPAD;
+  for (int i = threadIdx.x; i < C1 + C2 + HID + NC; i += blockDim.x) {
+    if (i < C1) {
+      float s = 0.f;
+      for (int b = 0; b < Bp; ++b) s += part1[((int64_t)g * Bp + b) * C1 + i];
+      m[OFF_BC1 + i] -= lr * s;
+    } else if (i < C1 + C2) {
+      const int c = i - C1;
+      float s = 0.f;
+      for (int b = 0; b < Bp; ++b) s += part2[((int64_t)g * Bp + b) * C2 + c];
+      m[OFF_BC2 + c] -= lr * s;
+    } else if (i < C1 + C2 + HID) {
+      const int o = i - C1 - C2;
+      m[OFF_B1 + o] -= lr * db1[(int64_t)g * HID + o];
+    } else {
+      const int c = i - C1 - C2 - HID;
+      m[OFF_B2 + c] -= lr * db2[(int64_t)g * NC + c];
+    }
+  }
+  // conv1 weights: master [64 taps][32] -> shadow [32][64] (the forward B operand, K-major)
+  __nv_bfloat16* s = shadow + (int64_t)g * PPAD + OFF_WC1;
+  for (int i = threadIdx.x; i < T1 * C1; i += blockDim.x) {
+    const int co = i / T1, t = i - co * T1;
+    s[i] = __float2bfloat16_rn(m[OFF_WC1 + t * C1 + co]);
+  }
+}
+
+// ---- round start / end ---------------------------------------------------------
+__global__ void bcast_kernel(const double* __restrict__ params, float* __restrict__ master,
+                             __nv_bfloat16* __restrict__ shadow, int G) {
+  const int64_t total = (int64_t)G * PPAD;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i % PPAD;
+    const float v = (float)params[j];
+    master[i] = v;
+    if (j >= OFF_WC1 + T1 * C1) shadow[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void wc1_shadow_kernel(const float* __restrict__ master, __nv_bfloat16* __restrict__ shadow) {
+  const int g = blockIdx.x;
+  const float* m = master + (int64_t)g * PPAD + OFF_WC1;
+  __nv_bfloat16* s = shadow + (int64_t)g * PPAD + OFF_WC1;
+  for (int i = threadIdx.x; i < T1 * C1; i += blockDim.x) {
+    const int co = i / T1, t = i - co * T1;
+    s[i] = __float2bfloat16_rn(m[t * C1 + co]);
+  }
+}
+
+// delta_g = master_g - float(params)  -> each client's delta pointer
+__global__ void delta_kernel(const fedhc_client* __restrict__ cl, const double* __restrict__ params,
+                             const float* __restrict__ master) {
+  const int g = blockIdx.y;
+  float* out = cl[g].delta;
+  const float* m = master + (int64_t)g * PPAD;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < PPAD; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = m[i] - (float)params[i];
+}
+
+// ---- engine ---------------------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct Engine {
+  int maxG, Bp, C;
+  std::vector<std::unique_ptr<Buf>> bufs;
+  float* master;
+  __nv_bfloat16 *shadow, *cols1, *a1, *p1, *cols2, *a2, *p2, *hT, *dl, *dhT, *dp2, *da2, *dcols2, *da1;
+  float *logits, *db1, *db2, *part1, *part2, *loss;
+  int32_t *labels, *valid;
+  fedhc_client* desc;
+  unsigned long long* correct;
+  // training plans for the current K, eval plans (G=1, batch = maxG*Bp)
+  int planned_G = -1;
+  float planned_lr = 0.f;
+  tc::GemmPlan conv1, conv2, fc1, fc2, fc2_dg, fc2_wg, fc1_dg, fc1_wg, conv2_dg, conv2_wg, conv1_wg;
+  tc::GemmPlan e_conv1, e_conv2, e_fc1, e_fc2;
+  cudaGraphExec_t graph = nullptr;
+  std::tuple<int, int, float> graph_key{-1, -1, 0.f};
+
+  ~Engine() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
+
+  template <typename T>
+  int alloc(T** out, size_t n) {
+    auto b = std::make_unique<Buf>();
+    FEDHC_CUDA_TRY(cudaMalloc(&b->p, n * sizeof(T) + 256));
+    FEDHC_CUDA_TRY(cudaMemset(b->p, 0, n * sizeof(T) + 256));
+    *out = static_cast<T*>(b->p);
+    bufs.push_back(std::move(b));
+    return FEDHC_OK;
+  }
+
+  int init() {
+    const size_t G = maxG, I = (size_t)maxG * Bp;
+    int rc = 0;
+    rc |= alloc(&master, G * PPAD);
+    rc |= alloc(&shadow, G * PPAD);
+    rc |= alloc(&cols1, I * HW0 * T1);
+    rc |= alloc(&a1, I * HW0 * C1);
+    rc |= alloc(&p1, I * HW1 * C1);
+    rc |= alloc(&cols2, I * HW1 * K2);
+    rc |= alloc(&a2, I * HW1 * C2);
+    rc |= alloc(&p2, I * F1);
+    rc |= alloc(&hT, I * HID);
+    rc |= alloc(&logits, I * NC);
+    rc |= alloc(&dl, I * NC);
+    rc |= alloc(&dhT, I * HID);
+    rc |= alloc(&dp2, I * F1);
+    rc |= alloc(&da2, I * HW1 * C2);
+    rc |= alloc(&dcols2, I * HW1 * K2);
+    rc |= alloc(&da1, I * HW0 * C1);
+    rc |= alloc(&db1, G * HID);
+    rc |= alloc(&db2, G * NC);
+    rc |= alloc(&part1, I * C1);
+    rc |= alloc(&part2, I * C2);
+    rc |= alloc(&loss, G);
+    rc |= alloc(&labels, I);
+    rc |= alloc(&valid, G);
+    rc |= alloc(&desc, G);
+    rc |= alloc(&correct, 1);
+    if (rc) return fail(FEDHC_ERR_CUDA, "cnn: workspace allocation failed");
+    return plan_eval();
+  }
+
+  static fedhc_gemm_args args(int G, int M, int N, int K, const void* A, bool a_mn, int64_t ags, const void* B,
+                              bool b_mn, int64_t bgs, int epi) {
+    fedhc_gemm_args a{};
+    a.G = G;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.A = A;
+    a.a_mn = a_mn;
+    a.a_gstride = ags;
+    a.B = B;
+    a.b_mn = b_mn;
+    a.b_gstride = bgs;
+    a.epilogue = epi;
+    return a;
+  }
+
+  // forward plans for G groups of `bp` images each (bp*784 and bp*196 pixel rows)
+  int plan_forward(int G, int bp, tc::GemmPlan* c1, tc::GemmPlan* c2, tc::GemmPlan* f1, tc::GemmPlan* f2) {
+    const int P1 = bp * HW0, P2 = bp * HW1;
+    int rc;
+    // conv1: a1[P1][32] = relu(cols1 . Wc1s^T + bc1)
+    auto a = args(G, P1, C1, T1, cols1, false, 0, shadow + OFF_WC1, false, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
+    a.D = a1;
+    a.bias = master + OFF_BC1;
+    a.bias_gstride = PPAD;
+    if ((rc = tc::gemm_plan(a, c1))) return rc;
+    // conv2: a2[P2][64] = relu(cols2 . Wc2 + bc2), Wc2 stored [896][64] (MN-major B)
+    a = args(G, P2, C2, K2, cols2, false, 0, shadow + OFF_WC2, true, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
+    a.D = a2;
+    a.bias = master + OFF_BC2;
+    a.bias_gstride = PPAD;
+    if ((rc = tc::gemm_plan(a, c2))) return rc;
+    // fc1: hT[2048][bp] = relu(W1 . p2^T + b1)
+    a = args(G, HID, bp, F1, shadow + OFF_W1, false, PPAD, p2, false, 0, FEDHC_EPI_BIAS_RELU_BF16);
+    a.D = hT;
+    a.bias = master + OFF_B1;
+    a.bias_gstride = PPAD;
+    a.bias_per_row = 1;
+    if ((rc = tc::gemm_plan(a, f1))) return rc;
+    // fc2: logits[bp][64] = h . W2^T   (A = hT, MN-major)
+    a = args(G, bp, NC, HID, hT, true, 0, shadow + OFF_W2, false, PPAD, FEDHC_EPI_F32);
+    a.D = logits;
+    return tc::gemm_plan(a, f2);
+  }
+
+  int plan_eval() { return plan_forward(1, maxG * Bp, &e_conv1, &e_conv2, &e_fc1, &e_fc2); }
+
+  int plan_train(int G, float lr) {
+    if (G == planned_G && lr == planned_lr) return FEDHC_OK;
+    int rc = plan_forward(G, Bp, &conv1, &conv2, &fc1, &fc2);
+    if (rc) return rc;
+    const int P1 = Bp * HW0, P2 = Bp * HW1;
+    // fc2 dgrad: dhT[2048][Bp] = (W2^T . dl^T) * (hT > 0), rowsum -> db1
+    auto a = args(G, HID, Bp, NC, shadow + OFF_W2, true, PPAD, dl, false, 0, FEDHC_EPI_RELU_MASK_BF16);
+    a.D = dhT;
+    a.mask = hT;
+    a.rowsum = db1;
+    if ((rc = tc::gemm_plan(a, &fc2_dg))) return rc;
+    // fc2 wgrad: W2[64][2048] -= lr dl^T . h
+    a = args(G, NC, HID, Bp, dl, true, 0, hT, false, 0, FEDHC_EPI_SGD);
+    a.master = master + OFF_W2;
+    a.shadow = shadow + OFF_W2;
+    a.d_gstride = PPAD;
+    a.lr = lr;
+    if ((rc = tc::gemm_plan(a, &fc2_wg))) return rc;
+    // fc1 dgrad: dp2[Bp][3200] = dh . W1  (A = dhT MN-major, B = W1 [2048][3200] MN-major)
+    a = args(G, Bp, F1, HID, dhT, true, 0, shadow + OFF_W1, true, PPAD, FEDHC_EPI_BF16);
+    a.D = dp2;
+    if ((rc = tc::gemm_plan(a, &fc1_dg))) return rc;
+    // fc1 wgrad: W1[2048][3200] -= lr dhT . p2
+    a = args(G, HID, F1, Bp, dhT, false, 0, p2, true, 0, FEDHC_EPI_SGD);
+    a.master = master + OFF_W1;
+    a.shadow = shadow + OFF_W1;
+    a.d_gstride = PPAD;
+    a.lr = lr;
+    if ((rc = tc::gemm_plan(a, &fc1_wg))) return rc;
+    // conv2 dgrad: dcols2[P2][896] = da2 . Wc2^T  (B = Wc2 [896][64] K-major)
+    a = args(G, P2, K2, C2, da2, false, 0, shadow + OFF_WC2, false, PPAD, FEDHC_EPI_BF16);
+    a.D = dcols2;
+    if ((rc = tc::gemm_plan(a, &conv2_dg))) return rc;
+    // conv2 wgrad: Wc2[896][64] -= lr cols2^T . da2
+    a = args(G, K2, C2, P2, cols2, true, 0, da2, true, 0, FEDHC_EPI_SGD);
+    a.master = master + OFF_WC2;
+    a.shadow = shadow + OFF_WC2;
+    a.d_gstride = PPAD;
+    a.lr = lr;
+    if ((rc = tc::gemm_plan(a, &conv2_wg))) return rc;
+    // conv1 wgrad: Wc1[64][32] -= lr cols1^T . da1  (B = da1 channel-major, K-major)
+    a = args(G, T1, C1, P1, cols1, true, 0, da1, false, 0, FEDHC_EPI_SGD);
+    a.master = master + OFF_WC1;
+    a.d_gstride = PPAD;
+    a.lr = lr;
+    if ((rc = tc::gemm_plan(a, &conv1_wg))) return rc;
+    planned_G = G;
+    planned_lr = lr;
+    if (graph) {
+      cudaGraphExecDestroy(graph);
+      graph = nullptr;
+    }
+    graph_key = {-1, -1, 0.f};
+    return FEDHC_OK;
+  }
+
+  static int grid_for(int64_t work) {
+    const int64_t b = (work + 255) / 256;
+    return (int)(b < 148 * 16 ? b : 148 * 16);
+  }
+
+  int forward(int G, int bp, int step, const tc::GemmPlan& c1, const tc::GemmPlan& c2, const tc::GemmPlan& f1,
+              const tc::GemmPlan& f2, cudaStream_t st) {
+    const int64_t n_img = (int64_t)G * bp;
+    int rc;
+    gather_im2col1_kernel<<<dim3(bp, G), 256, 0, st>>>(desc, step, bp, cols1, labels, valid);
+    if ((rc = tc::gemm_run(c1, st))) return rc;
+    pool_fwd_kernel<<<grid_for(n_img * HW1 * C1 / 8), 256, 0, st>>>(a1, p1, n_img, W0, C1, HW1 * C1);
+    im2col2_kernel<<<grid_for(n_img * HW1 * TAPS2 * 4), 256, 0, st>>>(p1, cols2, n_img);
+    if ((rc = tc::gemm_run(c2, st))) return rc;
+    pool_fwd_kernel<<<grid_for(n_img * HW2 * C2 / 8), 256, 0, st>>>(a2, p2, n_img, W1d, C2, F1);
+    if ((rc = tc::gemm_run(f1, st))) return rc;
+    return tc::gemm_run(f2, st);
+  }
+
+  int train_step(int G, int step, float lr, cudaStream_t st) {
+    int rc = forward(G, Bp, step, conv1, conv2, fc1, fc2, st);
+    if (rc) return rc;
+    ce_kernel<<<G, Bp, (size_t)Bp * NC * 4, st>>>(logits, master, Bp, C, labels, valid, dl, db2, loss);
+    if ((rc = tc::gemm_run(fc2_dg, st))) return rc;
+    if ((rc = tc::gemm_run(fc2_wg, st))) return rc;
+    if ((rc = tc::gemm_run(fc1_dg, st))) return rc;
+    if ((rc = tc::gemm_run(fc1_wg, st))) return rc;
+    pool2_bwd_kernel<<<dim3(Bp, G), 256, 0, st>>>(dp2, a2, da2, part2, Bp);
+    if ((rc = tc::gemm_run(conv2_dg, st))) return rc;
+    if ((rc = tc::gemm_run(conv2_wg, st))) return rc;
+    col2im_pool1_bwd_kernel<<<dim3(Bp, G), 256, kC2iSmem, st>>>(dcols2, a1, da1, part1, Bp);
+    if ((rc = tc::gemm_run(conv1_wg, st))) return rc;
+    bias_sgd_kernel<<<G, 256, 0, st>>>(master, shadow, part1, part2, db1, db2, Bp, lr);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
+  }
+};
+
+}  // namespace cnn
+}  // namespace fedhc
+
+using namespace fedhc;
+
+extern "C" int fedhc_cnn_param_count(int64_t* padded) {
+  if (!padded) return fail(FEDHC_ERR_VALUE, "cnn: null output");
+  *padded = cnn::PPAD;
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_param_offsets(int64_t* offsets /* [8] */) {
+  if (!offsets) return fail(FEDHC_ERR_VALUE, "cnn: null output");
+  const int64_t o[8] = {cnn::OFF_WC1, cnn::OFF_BC1, cnn::OFF_WC2, cnn::OFF_BC2,
+                        cnn::OFF_W1,  cnn::OFF_B1,  cnn::OFF_W2,  cnn::OFF_B2};
+  for (int i = 0; i < 8; ++i) offsets[i] = o[i];
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_create(int max_clients, int batch, int n_classes, void** out) {
+  if (!out) return fail(FEDHC_ERR_VALUE, "cnn: null output");
+  if (max_clients < 1 || batch < 1 || batch > 256) return fail(FEDHC_ERR_VALUE, "cnn: bad clients/batch (batch <= 256)");
+  if (n_classes < 2 || n_classes > cnn::NC) return fail(FEDHC_ERR_UNSUPPORTED, "cnn: n_classes must be in [2, 64]");
+  auto e = std::make_unique<cnn::Engine>();
+  e->maxG = max_clients;
+  e->Bp = (batch + 63) / 64 * 64;
+  e->C = n_classes;
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::col2im_pool1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      cnn::kC2iSmem));
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      e->Bp * cnn::NC * 4));
+  int rc = e->init();
+  if (rc) return rc;
+  *out = e.release();
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_destroy(void* ws) {
+  delete static_cast<cnn::Engine*>(ws);
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_local_train(void* ws, const fedhc_client* clients, int n_clients, const double* params,
+                                     int max_steps, float lr, int use_graph, void* stream) {
+  auto* e = static_cast<cnn::Engine*>(ws);
+  if (!e || (!clients && n_clients) || !params) return fail(FEDHC_ERR_VALUE, "cnn: null argument");
+  if (n_clients < 0 || n_clients > e->maxG) return fail(FEDHC_ERR_VALUE, "cnn: too many clients for the workspace");
+  if (max_steps < 0) return fail(FEDHC_ERR_VALUE, "cnn: negative step count");
+  if (n_clients == 0) return FEDHC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = n_clients;
+  int rc = e->plan_train(G, lr);
+  if (rc) return rc;
+  FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, clients, sizeof(fedhc_client) * G, cudaMemcpyDeviceToDevice, st));
+  cnn::bcast_kernel<<<cnn::Engine::grid_for((int64_t)G * cnn::PPAD), 256, 0, st>>>(params, e->master, e->shadow, G);
+  cnn::wc1_shadow_kernel<<<G, 256, 0, st>>>(e->master, e->shadow);
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  if (use_graph) {
+    const auto key = std::make_tuple(G, max_steps, lr);
+    if (!e->graph || e->graph_key != key) {
+      if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+      }
+      cudaStream_t cap;
+      FEDHC_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t g = nullptr;
+      FEDHC_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      for (int s = 0; s < max_steps && !rc; ++s) rc = e->train_step(G, s, lr, cap);
+      cudaError_t ce = cudaStreamEndCapture(cap, &g);
+      cudaStreamDestroy(cap);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      FEDHC_CUDA_TRY(ce);
+      cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
+      cudaGraphDestroy(g);
+      FEDHC_CUDA_TRY(ie);
+      e->graph_key = key;
+    }
+    FEDHC_CUDA_TRY(cudaGraphLaunch(e->graph, st));
+  } else {
+    for (int s = 0; s < max_steps; ++s)
+      if ((rc = e->train_step(G, s, lr, st))) return rc;
+  }
+  cnn::delta_kernel<<<dim3(64, G), 256, 0, st>>>(e->desc, params, e->master);
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_last_loss(void* ws, float* out, int n_clients, void* stream) {
+  auto* e = static_cast<cnn::Engine*>(ws);
+  if (!e || !out || n_clients > e->maxG) return fail(FEDHC_ERR_VALUE, "cnn: bad arguments");
+  FEDHC_CUDA_TRY(cudaMemcpyAsync(out, e->loss, sizeof(float) * n_clients, cudaMemcpyDeviceToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_cnn_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                              unsigned long long* correct, void* stream) {
+  auto* e = static_cast<cnn::Engine*>(ws);
+  if (!e || !params || !correct || (n > 0 && (!x || !y))) return fail(FEDHC_ERR_VALUE, "cnn: null argument");
+  if (n <= 0) return FEDHC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int chunk = e->maxG * e->Bp;
+  cnn::bcast_kernel<<<cnn::Engine::grid_for(cnn::PPAD), 256, 0, st>>>(params, e->master, e->shadow, 1);
+  cnn::wc1_shadow_kernel<<<1, 256, 0, st>>>(e->master, e->shadow);
+  for (int64_t at = 0; at < n; at += chunk) {
+    const int rows = (int)(n - at < chunk ? n - at : chunk);
+    fedhc_client c{};
+    c.x = x + at * cnn::HW0;
+    c.y = y + at;
+    c.perm = nullptr;
+    c.n_rows = rows;
+    c.n_batches = 1;
+    c.batch_size = rows;
+    FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    int rc = e->forward(1, chunk, 0, e->e_conv1, e->e_conv2, e->e_fc1, e->e_fc2, st);
+    if (rc) return rc;
+    cnn::argmax_kernel<<<(rows + 255) / 256, 256, 0, st>>>(e->logits, e->master, rows, e->C, e->labels, correct);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    FEDHC_CUDA_TRY(cudaStreamSynchronize(st));  // host descriptor reused next chunk
+  }
+  return FEDHC_OK;
+}

@@ -31,7 +31,7 @@
 #include <mutex>
 #include <string>
 
-#include "common.cuh"
+#include "gemm_tc.cuh"
 
 namespace fedhc {
 
@@ -113,19 +113,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-struct Epilogue {
-  int kind;             // FEDHC_EPI_*
-  void* D;              // F32 / BF16 / BIAS_RELU_BF16 output
-  int64_t ldd, d_gstride;
-  const float* bias;    // BIAS_RELU_BF16
-  int bias_per_row;
-  int64_t bias_gstride;
-  float* master;        // SGD: fp32 master, same indexing as D
-  __nv_bfloat16* shadow;  // SGD: optional bf16 copy
-  float lr;
-  const __nv_bfloat16* mask;  // RELU_MASK_BF16: D = acc * (mask > 0), mask indexed like D
-  float* rowsum;        // RELU_MASK_BF16 (optional, single N tile): rowsum[g*M + m] = sum_n D
-};
+
 
 template <int BM, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -342,12 +330,16 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// bf16 tensor [G][outer][inner] -> 3-D map, box {64, box_outer, 1}, 128-byte swizzle
-static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer) {
+// bf16 tensor [G][outer][inner] (group stride gstride elements, 0 = dense) -> 3-D map,
+// box {64, box_outer, 1}, 128-byte swizzle
+static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer,
+                    int64_t gstride) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)G};
-  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)outer * inner * 2};
+  if (gstride <= 0) gstride = (int64_t)outer * inner;
+  if (gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: operand group stride must be a multiple of 8 elements");
+  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)gstride * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
@@ -358,53 +350,45 @@ static int make_map(CUtensorMap* map, const void* base, int G, int outer, int in
 }
 
 template <int BM, int BN, bool A_MN, bool B_MN>
-static int launch(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
-  CUtensorMap ma, mb;
-  int rc = A_MN ? make_map(&ma, a.A, a.G, a.K, a.M, 64) : make_map(&ma, a.A, a.G, a.M, a.K, BM);
+static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
+  int rc = A_MN ? make_map(&p->ma, a.A, a.G, a.K, a.M, 64, a.a_gstride)
+                 : make_map(&p->ma, a.A, a.G, a.M, a.K, BM, a.a_gstride);
   if (rc) return rc;
-  rc = B_MN ? make_map(&mb, a.B, a.G, a.K, a.N, 64) : make_map(&mb, a.B, a.G, a.N, a.K, BN);
+  rc = B_MN ? make_map(&p->mb, a.B, a.G, a.K, a.N, 64, a.b_gstride) : make_map(&p->mb, a.B, a.G, a.N, a.K, BN, a.b_gstride);
   if (rc) return rc;
   int dev = 0, sms = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int tiles = a.G * (a.M / BM) * (a.N / BN);
-  const int smem = Cfg<BM, BN>::smem_bytes();
+  p->smem = Cfg<BM, BN>::smem_bytes();
   auto kern = grouped_gemm_kernel<BM, BN, A_MN, B_MN>;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<tiles < sms ? tiles : sms, kThreads, smem, st>>>(ma, mb, a.G, a.M, a.N, a.K, ep);
-  FEDHC_CUDA_TRY(cudaGetLastError());
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+  p->kern = reinterpret_cast<const void*>(kern);
+  p->grid = tiles < sms ? tiles : sms;
   return FEDHC_OK;
 }
 
 template <int BM, int BN>
-static int dispatch_major(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
+static int plan_major(const fedhc_gemm_args& a, GemmPlan* p) {
   if constexpr (BN >= 64) {
-    if (a.a_mn && a.b_mn) return launch<BM, BN, true, true>(a, ep, st);
-    if (a.b_mn) return launch<BM, BN, false, true>(a, ep, st);
+    if (a.a_mn && a.b_mn) return plan_kernel<BM, BN, true, true>(a, p);
+    if (a.b_mn) return plan_kernel<BM, BN, false, true>(a, p);
   } else {
     if (a.b_mn) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: N = 32 tiles need a K-major B operand");
   }
-  if (a.a_mn) return launch<BM, BN, true, false>(a, ep, st);
-  return launch<BM, BN, false, false>(a, ep, st);
+  if (a.a_mn) return plan_kernel<BM, BN, true, false>(a, p);
+  return plan_kernel<BM, BN, false, false>(a, p);
 }
 
 template <int BM>
-static int dispatch_n(const fedhc_gemm_args& a, const Epilogue& ep, cudaStream_t st) {
-  if (a.N % 256 == 0) return dispatch_major<BM, 256>(a, ep, st);
-  if (a.N % 128 == 0) return dispatch_major<BM, 128>(a, ep, st);
-  if (a.N % 64 == 0) return dispatch_major<BM, 64>(a, ep, st);
-  return dispatch_major<BM, 32>(a, ep, st);
+static int plan_n(const fedhc_gemm_args& a, GemmPlan* p) {
+  if (a.N % 256 == 0) return plan_major<BM, 256>(a, p);
+  if (a.N % 128 == 0) return plan_major<BM, 128>(a, p);
+  if (a.N % 64 == 0) return plan_major<BM, 64>(a, p);
+  return plan_major<BM, 32>(a, p);
 }
 
-}  // namespace tc
-}  // namespace fedhc
-
-using namespace fedhc;
-
-extern "C" int fedhc_gemm(const fedhc_gemm_args* args, void* stream) {
-  using namespace fedhc::tc;
-  if (!args) return fail(FEDHC_ERR_VALUE, "gemm: null args");
-  const fedhc_gemm_args& a = *args;
+int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p) {
   if (a.G < 1 || a.M < 1 || a.N < 1 || a.K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
   if (a.M % 64 || a.N % 32 || a.K % BK)
     return fail(FEDHC_ERR_UNSUPPORTED, "gemm: need M % 64 == 0, N % 32 == 0, K % 64 == 0");
@@ -422,8 +406,33 @@ extern "C" int fedhc_gemm(const fedhc_gemm_args* args, void* stream) {
   if (ep.ldd % 8 || ep.d_gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: ldd and d_gstride must be multiples of 8");
   const int bn = a.N % 256 == 0 ? 256 : a.N % 128 == 0 ? 128 : a.N % 64 == 0 ? 64 : 32;
   if (ep.rowsum && bn != a.N) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: rowsum needs N to fit one tile (N <= 256)");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return a.M % 128 == 0 ? dispatch_n<128>(a, ep, st) : dispatch_n<64>(a, ep, st);
+  p->ep = ep;
+  p->G = a.G;
+  p->M = a.M;
+  p->N = a.N;
+  p->K = a.K;
+  return a.M % 128 == 0 ? plan_n<128>(a, p) : plan_n<64>(a, p);
+}
+
+int gemm_run(const GemmPlan& p, cudaStream_t st) {
+  void* args[] = {const_cast<CUtensorMap*>(&p.ma), const_cast<CUtensorMap*>(&p.mb), const_cast<int*>(&p.G),
+                  const_cast<int*>(&p.M), const_cast<int*>(&p.N), const_cast<int*>(&p.K),
+                  const_cast<Epilogue*>(&p.ep)};
+  FEDHC_CUDA_TRY(cudaLaunchKernel(p.kern, dim3(p.grid), dim3(kThreads), args, p.smem, st));
+  return FEDHC_OK;
+}
+
+}  // namespace tc
+}  // namespace fedhc
+
+using namespace fedhc;
+
+extern "C" int fedhc_gemm(const fedhc_gemm_args* args, void* stream) {
+  if (!args) return fail(FEDHC_ERR_VALUE, "gemm: null args");
+  tc::GemmPlan p;
+  int rc = tc::gemm_plan(*args, &p);
+  if (rc) return rc;
+  return tc::gemm_run(p, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int fedhc_gemm_bf16_tn(int G, int M, int N, int K, const void* A, const void* B, float* D, void* stream) {

@@ -1,0 +1,43 @@
+// Grouped tcgen05 GEMM: plan once (tensor maps, kernel choice), launch many times.
+// Used by the C-ABI entry fedhc_gemm and by the CNN client engine (cnn.cu), which
+// builds every per-layer plan when its workspace is created so a training step
+// is launches only (and can be captured into a CUDA graph).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace fedhc {
+namespace tc {
+
+struct Epilogue {
+  int kind;             // FEDHC_EPI_*
+  void* D;              // F32 / BF16 / BIAS_RELU_BF16 output
+  int64_t ldd, d_gstride;
+  const float* bias;    // BIAS_RELU_BF16
+  int bias_per_row;
+  int64_t bias_gstride;
+  float* master;        // SGD: fp32 master, same indexing as D
+  __nv_bfloat16* shadow;  // SGD: optional bf16 copy
+  float lr;
+  const __nv_bfloat16* mask;  // RELU_MASK_BF16: D = acc * (mask > 0), mask indexed like D
+  float* rowsum;        // RELU_MASK_BF16 (optional, single N tile): rowsum[g*M + m] = sum_n D
+};
+
+struct GemmPlan {
+  CUtensorMap ma, mb;
+  Epilogue ep;
+  int G, M, N, K;
+  const void* kern;
+  int grid, smem;
+};
+
+// Validate a problem and build its plan (no launch).  Returns a FEDHC_* status.
+int gemm_plan(const fedhc_gemm_args& a, GemmPlan* plan);
+// Launch a plan on a stream.
+int gemm_run(const GemmPlan& p, cudaStream_t st);
+
+}  // namespace tc
+}  // namespace fedhc
