@@ -131,11 +131,21 @@ class CnnEngine:
         _abi.check(_abi.lib.fedhc_cnn_last_loss(self._h, out.data_ptr(), k, stream_ptr()))
         return out
 
+    def correct_into(self, params: torch.Tensor, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor) -> None:
+        """out (dev int64 [1]) += correctly classified rows; no host synchronisation of the result."""
+        _abi.check(_abi.lib.fedhc_cnn_eval(self._h, params.data_ptr(), x.data_ptr(), y.data_ptr(), int(y.shape[0]),
+                                           out.data_ptr(), stream_ptr()))
+
     def correct(self, params: torch.Tensor, x: torch.Tensor, y: torch.Tensor) -> int:
         cnt = torch.zeros(1, dtype=torch.int64, device=params.device)
-        _abi.check(_abi.lib.fedhc_cnn_eval(self._h, params.data_ptr(), x.data_ptr(), y.data_ptr(), int(y.shape[0]),
-                                           cnt.data_ptr(), stream_ptr()))
+        self.correct_into(params, x, y, cnt)
         return int(cnt.item())
+
+    KERNELS_PER_STEP = 19     # 11 grouped GEMMs + 8 gather/pool/im2col/CE/col2im/bias kernels (csrc/cnn.cu)
+
+    def launches_per_round(self, steps: int) -> int:
+        """Kernels one fedhc_cnn_local_train launches (broadcast, shadow, steps, delta)."""
+        return self.KERNELS_PER_STEP * steps + 3
 
 
 class CnnFederation(DeviceFederation):
@@ -156,8 +166,9 @@ class CnnFederation(DeviceFederation):
             deltas = delta_buffer(k, self.P, self.x.device)
         if k == 0:
             return deltas
-        meta, _ = self.stage_plan(participants, workloads, seeds)
+        meta, perm_bytes = self.stage_plan(participants, workloads, seeds)
         d_desc = self.descriptors(participants, meta, lr, deltas)
+        self.last_h2d_bytes = perm_bytes + d_desc.numel()
         max_steps = max(m[2] for m in meta)
         if max(wl.batch_size for wl in workloads) > self.engine.batch:
             raise ValueError("batch size exceeds the CNN workspace")

@@ -292,44 +292,62 @@ constexpr int kC2iSmem = C1 * HW0 * 2;
 
 // grid (Bp, G): col2im of dcols2 + maxpool1 backward + ReLU mask -> da1 channel-major
 // dcols2 [G][Bp*196][896], a1 [G][Bp][784][32] -> da1 [G][32][Bp*784], part [G][Bp][32]
+// thread item = (pooled pixel p, group of 8 channels): 16-byte loads of every tap's 8 channels.
 __global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat16* __restrict__ dcols2,
                                                                const __nv_bfloat16* __restrict__ a1,
                                                                __nv_bfloat16* __restrict__ da1,
                                                                float* __restrict__ part, int Bp) {
   extern __shared__ __align__(16) unsigned char c2i_smem[];
   auto tile = reinterpret_cast<__nv_bfloat16(*)[HW0]>(c2i_smem);  // [C1][HW0], 50 KB (dynamic)
-  __shared__ float red[8][C1];
+  __shared__ float red[256][9];
   const int g = blockIdx.y, b = blockIdx.x;
   const int64_t img = (int64_t)g * Bp + b;
   const __nv_bfloat16* dc = dcols2 + img * HW1 * K2;
   const __nv_bfloat16* a = a1 + img * HW0 * C1;
-  const int ci = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  float acc = 0.f;
-  for (int p = grp; p < HW1; p += 8) {
-    const int ph = p / W1d, pw = p - ph * W1d;
-    float s = 0.f;
+  const int cg = threadIdx.x & 3;            // channels [8 cg, 8 cg + 8) (256 % 4 == 0: fixed per thread)
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int item = threadIdx.x; item < HW1 * 4; item += 256) {
+    const int p = item >> 2, ph = p / W1d, pw = p - ph * W1d;
+    float s[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e] = 0.f;
     for (int kh = 0; kh < 5; ++kh) {
       const int oh = ph - kh + 2;
       if (oh < 0 || oh >= W1d) continue;
+#pragma unroll
       for (int kw = 0; kw < 5; ++kw) {
         const int ow = pw - kw + 2;
         if (ow < 0 || ow >= W1d) continue;
-        s += bf(dc[(int64_t)(oh * W1d + ow) * K2 + (kh * 5 + kw) * C1 + ci]);
+        const uint4 v = *reinterpret_cast<const uint4*>(dc + (int64_t)(oh * W1d + ow) * K2 + (kh * 5 + kw) * C1 +
+                                                        cg * 8);
+        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] += bf(vb[e]);
       }
     }
     const int q00 = (2 * ph) * W0 + 2 * pw;
     const int pos[4] = {q00, q00 + 1, q00 + W0, q00 + W0 + 1};
-    float v[4];
+    uint4 av[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = bf(a[pos[k] * C1 + ci]);
-    const int k = first_max4(v[0], v[1], v[2], v[3]);
-    const bool on = v[k] > 0.f;
-    const __nv_bfloat16 gz = __float2bfloat16_rn(on ? s : 0.f);
+    for (int k = 0; k < 4; ++k) av[k] = *reinterpret_cast<const uint4*>(a + pos[k] * C1 + cg * 8);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tile[ci][pos[j]] = j == k ? gz : __float2bfloat16_rn(0.f);
-    acc += bf(gz);
+    for (int e = 0; e < 8; ++e) {
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = bf(reinterpret_cast<const __nv_bfloat16*>(&av[k])[e]);
+      const int k = first_max4(v[0], v[1], v[2], v[3]);
+      const bool on = v[k] > 0.f;
+      const __nv_bfloat16 gz = __float2bfloat16_rn(on ? s[e] : 0.f);
+      const int ci = cg * 8 + e;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tile[ci][pos[j]] = j == k ? gz : __float2bfloat16_rn(0.f);
+      acc[e] += bf(gz);
+    }
   }
-  red[grp][ci] = acc;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[threadIdx.x][e] = acc[e];
   __syncthreads();
   // channel-major store: da1[g][ci][b*784 + p], 16 B per thread
   const int64_t P1 = (int64_t)Bp * HW0;
@@ -338,10 +356,11 @@ __global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat
     *reinterpret_cast<uint4*>(da1 + ((int64_t)g * C1 + c) * P1 + (int64_t)b * HW0 + q * 8) =
         *reinterpret_cast<const uint4*>(&tile[c][q * 8]);
   }
-  if (threadIdx.x < C1) {
+  if (threadIdx.x < C1) {  // fixed-order sum over the 64 threads that own this channel
+    const int c = threadIdx.x, grp = c >> 3, e = c & 7;
     float s = 0.f;
-    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
-    part[img * C1 + threadIdx.x] = s;
+    for (int t = grp; t < 256; t += 4) s += red[t][e];
+    part[img * C1 + c] = s;
   }
 }
 

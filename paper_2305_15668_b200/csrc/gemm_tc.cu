@@ -45,9 +45,7 @@ struct Cfg {
   static constexpr int kTileABytes = BM * BK * 2;
   static constexpr int kTileBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
-  static constexpr int STAGES = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
-  static constexpr int smem_bytes() { return STAGES * kStageBytes + 1024 + 256; }
 };
 
 // M=64 accumulators occupy TMEM lanes 0-15 of each 32-lane quadrant (row = 16*q + lane,
@@ -115,23 +113,78 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t smem_src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most n - 1 bulk groups of this thread are still reading shared memory
+__device__ __forceinline__ void bulk_wait_read_keep(int n) {
+  if (n >= 8) asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory");
+  else if (n >= 4) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+  else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__host__ __device__ constexpr bool epi_loads(int kind) {
+  return kind == FEDHC_EPI_SGD || kind == FEDHC_EPI_RELU_MASK_BF16;
+}
+
+// Epilogue staging (per epilogue warp, one 32-column chunk of its R = BM/4 rows at a time):
+//   load ring  kEpiLoad slots: the fp32 master (SGD) or bf16 mask (ReLU backward) chunk, prefetched by
+//              the TMA producer warp as soon as the tile's operand loads are issued;
+//   store bufs nst slots (2, 4 or 8; host-chosen: many when K is short and the GEMM is
+//              store-bound): the chunk's output (fp32 / bf16 D, or the SGD bf16 shadow),
+//              written to global by TMA tensor stores, nst - 1 bulk groups kept in flight.
+// Slots hold R rows of 128 B (fp32, SWIZZLE_128B: 16-B chunk j of row r at j ^ (r & 7)) or of 64 B
+// (bf16, SWIZZLE_64B: chunk j at j ^ ((r >> 1) & 3)); thread = row, so both are bank-conflict free.
+constexpr int kEpiLoad = 4;
+
+template <int BM>
+__host__ __device__ constexpr int epi_slot_bytes() { return (BM / 4) * 128; }
+
+template <int BM>
+__host__ __device__ constexpr int epi_bytes(int kind, int nst) {
+  return 4 * (nst + (epi_loads(kind) ? kEpiLoad : 0)) * epi_slot_bytes<BM>();
+}
+
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+__device__ __forceinline__ uint32_t sw64_off(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
 template <int BM, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        int G, int M, int N, int K, const Epilogue ep) {
+                        const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_s,
+                        const __grid_constant__ CUtensorMap map_l, int G, int M, int N, int K, int STAGES,
+                        int nst, const Epilogue ep) {
   using CF = Cfg<BM, BN>;
-  constexpr int STAGES = CF::STAGES, kStageBytes = CF::kStageBytes, kTmemCols = CF::kTmemCols;
+  constexpr int kStageBytes = CF::kStageBytes, kTmemCols = CF::kTmemCols;
   constexpr int kTileABytes = CF::kTileABytes;
+  constexpr int R = BM / 4;                      // output rows per epilogue warp
+  constexpr int kSlot = epi_slot_bytes<BM>();
   constexpr uint32_t kIdesc = idesc<BM, BN, A_MN, B_MN>();
   constexpr uint32_t kLboA = A_MN ? 64 * BK * 2 : 16, kLboB = B_MN ? 64 * BK * 2 : 16;
   constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;  // bytes per K=16
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  const int kind = ep.kind;
+  const bool loads = epi_loads(kind);
+  unsigned char* st_buf = smem + STAGES * kStageBytes;            // [4 warps][nst] slots
+  unsigned char* ld_buf = st_buf + 4 * nst * kSlot;                // [4 warps][kEpiLoad] slots (if loads)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ld_buf + (loads ? 4 * kEpiLoad * kSlot : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* lfull = tempty + 2;       // [4][kEpiLoad] epilogue chunk landed
+  uint64_t* lempty = lfull + 4 * kEpiLoad;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lempty + 4 * kEpiLoad);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = M / BM, tiles_n = N / BN;
@@ -146,6 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    for (int i = 0; i < 4 * kEpiLoad; ++i) {
+      mbar_init(&lfull[i], 1);
+      mbar_init(&lempty[i], 1);
     }
     fence_mbar_init();
   }
@@ -165,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
       int s = 0;
       uint32_t ph = 0;
+      uint32_t u = 0;  // epilogue chunk counter (same sequence the epilogue warps consume)
+      const uint32_t lbytes = kind == FEDHC_EPI_SGD ? R * 128 : R * 64;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int g = t / (tiles_m * tiles_n);
         const int r = t - g * tiles_m * tiles_n;
@@ -188,6 +247,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
+          }
+        }
+        if (loads) {  // prefetch the tile's epilogue inputs (master / mask chunks) per warp
+          for (int c = 0; c < BN / 32; ++c, ++u) {
+            const int slot = u % kEpiLoad;
+            const uint32_t lph = (u / kEpiLoad) & 1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint64_t* fb = &lfull[q * kEpiLoad + slot];
+              mbar_wait(&lempty[q * kEpiLoad + slot], lph ^ 1);
+              mbar_arrive_expect_tx(fb, lbytes);
+              tma_load_3d(smem_u32(ld_buf + (q * kEpiLoad + slot) * kSlot), &map_l, fb, n0 + 32 * c, m0 + R * q, g);
+            }
           }
         }
       }
@@ -220,12 +292,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4): thread = one output row
+    // epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4: thread = one output row
     // (M=64: lanes 0-15 of the quadrant hold rows 16*q + lane)
     const int q = warp & 3;
-    constexpr int kRowsPerWarp = BM / 4;
-    const bool active = lane < kRowsPerWarp;
+    const bool active = lane < R;
+    const int rr = active ? lane : 0;
     int it = 0;
+    uint32_t u = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
       const int g = t / (tiles_m * tiles_n);
@@ -233,77 +306,92 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + kRowsPerWarp * q + (active ? lane : 0);
-      const int64_t base = (int64_t)g * ep.d_gstride + (int64_t)row * ep.ldd + n0;
-      const float rbias = (ep.kind == FEDHC_EPI_BIAS_RELU_BF16 && ep.bias_per_row)
+      const int row = m0 + R * q + rr;
+      const float rbias = (kind == FEDHC_EPI_BIAS_RELU_BF16 && ep.bias_per_row)
                               ? ep.bias[(int64_t)g * ep.bias_gstride + row] : 0.f;
       float rsum = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < BN / 32; ++c, ++u) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
-        if (!active) continue;
-        const int64_t o = base + 32 * c;
-        if (ep.kind == FEDHC_EPI_F32) {
-          float* d = static_cast<float*>(ep.D) + o;
+        const int lslot = q * kEpiLoad + (int)(u % kEpiLoad);
+        unsigned char* lb = ld_buf + lslot * kSlot;
+        unsigned char* sb = st_buf + (q * nst + (int)(u % nst)) * kSlot;
+        if (loads) mbar_wait(&lfull[lslot], (u / kEpiLoad) & 1);
+        if (active) {
+          if (kind == FEDHC_EPI_SGD) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(d + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-        } else if (ep.kind == FEDHC_EPI_SGD) {
-          float* w = ep.master + o;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 m4 = *reinterpret_cast<float4*>(w + i);
-            m4.x -= ep.lr * __uint_as_float(v[i]);
-            m4.y -= ep.lr * __uint_as_float(v[i + 1]);
-            m4.z -= ep.lr * __uint_as_float(v[i + 2]);
-            m4.w -= ep.lr * __uint_as_float(v[i + 3]);
-            *reinterpret_cast<float4*>(w + i) = m4;
-            if (ep.shadow) {
-              __nv_bfloat162* sh = reinterpret_cast<__nv_bfloat162*>(ep.shadow + o + i);
-              sh[0] = __floats2bfloat162_rn(m4.x, m4.y);
-              sh[1] = __floats2bfloat162_rn(m4.z, m4.w);
+            for (int j = 0; j < 8; j += 2) {
+              float4* p0 = reinterpret_cast<float4*>(lb + sw128_off(rr, j));
+              float4* p1 = reinterpret_cast<float4*>(lb + sw128_off(rr, j + 1));
+              float4 a = *p0, b = *p1;
+              a.x -= ep.lr * __uint_as_float(v[4 * j + 0]);
+              a.y -= ep.lr * __uint_as_float(v[4 * j + 1]);
+              a.z -= ep.lr * __uint_as_float(v[4 * j + 2]);
+              a.w -= ep.lr * __uint_as_float(v[4 * j + 3]);
+              b.x -= ep.lr * __uint_as_float(v[4 * j + 4]);
+              b.y -= ep.lr * __uint_as_float(v[4 * j + 5]);
+              b.z -= ep.lr * __uint_as_float(v[4 * j + 6]);
+              b.w -= ep.lr * __uint_as_float(v[4 * j + 7]);
+              *p0 = a;
+              *p1 = b;
+              *reinterpret_cast<uint4*>(sb + sw64_off(rr, j >> 1)) =
+                  make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                             pack_bf16x2(b.z, b.w));
             }
-          }
-        } else {
-          const int kind = ep.kind;
-          __nv_bfloat16* d = static_cast<__nv_bfloat16*>(ep.D) + o;
-          const float* cb = (kind == FEDHC_EPI_BIAS_RELU_BF16 && !ep.bias_per_row)
-                                ? ep.bias + (int64_t)g * ep.bias_gstride + n0 + 32 * c : nullptr;
+          } else if (kind == FEDHC_EPI_F32) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float f[8];
-            uint4 mk = make_uint4(0, 0, 0, 0);
-            if (kind == FEDHC_EPI_RELU_MASK_BF16) mk = *reinterpret_cast<const uint4*>(ep.mask + o + i);
-            const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(sb + sw128_off(rr, j)) = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                                                            v[4 * j + 3]);
+          } else {
+            const float* cb = (kind == FEDHC_EPI_BIAS_RELU_BF16 && !ep.bias_per_row)
+                                  ? ep.bias + (int64_t)g * ep.bias_gstride + n0 + 32 * c : nullptr;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              float x = __uint_as_float(v[i + u]);
-              if (kind == FEDHC_EPI_BIAS_RELU_BF16) x = fmaxf(x + (cb ? cb[i + u] : rbias), 0.f);
-              if (kind == FEDHC_EPI_RELU_MASK_BF16) x = __bfloat162float(mb[u]) > 0.f ? x : 0.f;
-              f[u] = x;
+            for (int j = 0; j < 4; ++j) {
+              float f[8];
+              uint4 mk = make_uint4(0, 0, 0, 0);
+              if (kind == FEDHC_EPI_RELU_MASK_BF16) mk = *reinterpret_cast<const uint4*>(lb + sw64_off(rr, j));
+              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                float x = __uint_as_float(v[8 * j + e]);
+                if (kind == FEDHC_EPI_BIAS_RELU_BF16) x = fmaxf(x + (cb ? cb[8 * j + e] : rbias), 0.f);
+                if (kind == FEDHC_EPI_RELU_MASK_BF16) x = __bfloat162float(mb[e]) > 0.f ? x : 0.f;
+                f[e] = x;
+              }
+              uint4 pk = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                    pack_bf16x2(f[6], f[7]));
+              *reinterpret_cast<uint4*>(sb + sw64_off(rr, j)) = pk;
+              // row sum of the stored (bf16-rounded) values, fixed order -> deterministic
+              const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) rsum += __bfloat162float(pb[e]);
             }
-            uint4 pk;
-            __nv_bfloat162 t0 = __floats2bfloat162_rn(f[0], f[1]), t1 = __floats2bfloat162_rn(f[2], f[3]);
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(f[4], f[5]), t3 = __floats2bfloat162_rn(f[6], f[7]);
-            pk.x = *reinterpret_cast<uint32_t*>(&t0);
-            pk.y = *reinterpret_cast<uint32_t*>(&t1);
-            pk.z = *reinterpret_cast<uint32_t*>(&t2);
-            pk.w = *reinterpret_cast<uint32_t*>(&t3);
-            *reinterpret_cast<uint4*>(d + i) = pk;
-            // row sum of the stored (bf16-rounded) values, fixed order -> deterministic
-            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) rsum += __bfloat162float(pb[u]);
           }
         }
+        fence_proxy_async_smem();  // generic smem writes -> visible to the TMA (async proxy) stores
+        __syncwarp();
+        if (lane == 0) {
+          const int c0 = n0 + 32 * c, c1 = m0 + R * q;
+          if (kind == FEDHC_EPI_SGD) {
+            tma_store_3d(&map_o, smem_u32(lb), c0, c1, g);
+            if (ep.shadow) tma_store_3d(&map_s, smem_u32(sb), c0, c1, g);
+          } else {
+            tma_store_3d(&map_o, smem_u32(sb), c0, c1, g);
+          }
+          bulk_commit();
+          bulk_wait_read_keep(nst);  // chunk u - nst + 1's stores have read their slots
+          if (loads && u > 0) mbar_arrive(&lempty[q * kEpiLoad + (int)((u - 1) % kEpiLoad)]);
+        }
+        __syncwarp();
       }
       if (ep.rowsum && active) ep.rowsum[(int64_t)g * M + row] = rsum;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 1) {
@@ -330,23 +418,39 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// bf16 tensor [G][outer][inner] (group stride gstride elements, 0 = dense) -> 3-D map,
-// box {64, box_outer, 1}, 128-byte swizzle
-static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer,
-                    int64_t gstride) {
+// tensor [G][outer][inner] (row stride ld elements, group stride gstride elements; 0 = dense) -> 3-D map
+static int make_map_ex(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize, int G, int outer,
+                       int inner, int64_t ld, int64_t gstride, int box_inner, int box_outer, CUtensorMapSwizzle sw) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
+  if (ld <= 0) ld = inner;
+  if (gstride <= 0) gstride = (int64_t)outer * ld;
+  if ((gstride * esize) % 16 || (ld * esize) % 16)
+    return fail(FEDHC_ERR_VALUE, "gemm: operand row / group strides must be multiples of 16 bytes");
+  if (reinterpret_cast<uintptr_t>(base) & 15) return fail(FEDHC_ERR_VALUE, "gemm: tensors must be 16-byte aligned");
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)G};
-  if (gstride <= 0) gstride = (int64_t)outer * inner;
-  if (gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: operand group stride must be a multiple of 8 elements");
-  cuuint64_t strides[2] = {(cuuint64_t)inner * 2, (cuuint64_t)gstride * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_outer, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * esize, (cuuint64_t)gstride * esize};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FEDHC_ERR_CUDA, "gemm: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return FEDHC_OK;
+}
+
+// bf16 operand [G][outer][inner] -> box {64, box_outer, 1}, 128-byte swizzle
+static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer,
+                    int64_t gstride) {
+  if (gstride > 0 && gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: operand group stride must be a multiple of 8 elements");
+  return make_map_ex(map, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, G, outer, inner, 0, gstride, 64, box_outer,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// epilogue tile maps: 32-column x R-row chunks, fp32 (128-B rows, SW128) or bf16 (64-B rows, SW64)
+static int make_epi_map(CUtensorMap* map, const void* base, bool f32, const GemmPlan& p, int rows) {
+  return make_map_ex(map, base, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f32 ? 4 : 2,
+                     p.G, p.M, p.N, p.ep.ldd, p.ep.d_gstride, 32, rows,
+                     f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 template <int BM, int BN, bool A_MN, bool B_MN>
@@ -356,13 +460,37 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   if (rc) return rc;
   rc = B_MN ? make_map(&p->mb, a.B, a.G, a.K, a.N, 64, a.b_gstride) : make_map(&p->mb, a.B, a.G, a.N, a.K, BN, a.b_gstride);
   if (rc) return rc;
-  int dev = 0, sms = 0;
+  const int kind = p->ep.kind, R = BM / 4;
+  p->ms = p->ml = p->mo = CUtensorMap{};
+  if (kind == FEDHC_EPI_SGD) {
+    if ((rc = make_epi_map(&p->mo, p->ep.master, true, *p, R))) return rc;
+    p->ml = p->mo;
+    if (p->ep.shadow && (rc = make_epi_map(&p->ms, p->ep.shadow, false, *p, R))) return rc;
+  } else {
+    if ((rc = make_epi_map(&p->mo, p->ep.D, kind == FEDHC_EPI_F32, *p, R))) return rc;
+    if (kind == FEDHC_EPI_RELU_MASK_BF16 && (rc = make_epi_map(&p->ml, p->ep.mask, false, *p, R))) return rc;
+  }
+  int dev = 0, sms = 0, max_smem = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int tiles = a.G * (a.M / BM) * (a.N / BN);
-  p->smem = Cfg<BM, BN>::smem_bytes();
+  // short-K GEMMs are epilogue (store) bound: spend shared memory on in-flight TMA stores
+  // (load epilogues keep 2: their in-place SGD stores read the load slot, released one chunk later)
+  int nst = (a.K / BK <= 4 && !epi_loads(kind)) ? 8 : 2, stages = 0, fixed = 0;
+  for (;; nst /= 2) {
+    fixed = 1024 + epi_bytes<BM>(kind, nst) + 512;  // alignment slack + epilogue staging + barriers
+    stages = (max_smem - fixed) / Cfg<BM, BN>::kStageBytes;
+    if (stages >= 3 || nst == 2) break;
+  }
+  if (stages > 8) stages = 8;
+  if (stages < 2) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: tile does not fit shared memory");
+  p->stages = stages;
+  p->nst = nst;
+  p->smem = fixed + stages * Cfg<BM, BN>::kStageBytes;
   auto kern = grouped_gemm_kernel<BM, BN, A_MN, B_MN>;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+  // plans of one kernel instance differ in smem (epilogue staging): allow the device maximum once
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   p->kern = reinterpret_cast<const void*>(kern);
   p->grid = tiles < sms ? tiles : sms;
   return FEDHC_OK;
@@ -415,9 +543,10 @@ int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p) {
 }
 
 int gemm_run(const GemmPlan& p, cudaStream_t st) {
-  void* args[] = {const_cast<CUtensorMap*>(&p.ma), const_cast<CUtensorMap*>(&p.mb), const_cast<int*>(&p.G),
+  void* args[] = {const_cast<CUtensorMap*>(&p.ma), const_cast<CUtensorMap*>(&p.mb), const_cast<CUtensorMap*>(&p.mo),
+                  const_cast<CUtensorMap*>(&p.ms), const_cast<CUtensorMap*>(&p.ml), const_cast<int*>(&p.G),
                   const_cast<int*>(&p.M), const_cast<int*>(&p.N), const_cast<int*>(&p.K),
-                  const_cast<Epilogue*>(&p.ep)};
+                  const_cast<int*>(&p.stages), const_cast<int*>(&p.nst), const_cast<Epilogue*>(&p.ep)};
   FEDHC_CUDA_TRY(cudaLaunchKernel(p.kern, dim3(p.grid), dim3(kThreads), args, p.smem, st));
   return FEDHC_OK;
 }

@@ -27,11 +27,14 @@ struct Epilogue {
 };
 
 struct GemmPlan {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb;   // operands
+  CUtensorMap mo;       // epilogue store target: D, or the SGD fp32 master
+  CUtensorMap ms;       // SGD bf16 shadow (optional)
+  CUtensorMap ml;       // epilogue load source: SGD master or ReLU-backward mask
   Epilogue ep;
   int G, M, N, K;
   const void* kern;
-  int grid, smem;
+  int grid, smem, stages, nst;
 };
 
 // Validate a problem and build its plan (no launch).  Returns a FEDHC_* status.
