@@ -26,6 +26,7 @@
 //     so W -= lr * G is a thread-local update (no barrier, no conflicts).
 // 480 threads (14 + 1 warps) -> <= 128 registers per thread.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -427,6 +428,340 @@ __global__ void __launch_bounds__(kFThreads, 1)
   if (CL > 1) cluster_sync_all();  // keep shared memory alive until peers are done with it
 }
 
+// ============================================================================
+// v4 "pipelined" variant for one CTA per client (C <= 16, F = 784): the
+// softmax moves to a dedicated warp and the compute warps software-pipeline
+// the stages of a batch, so the softmax of stage i overlaps the forward of
+// stage i + 1 and the backward of stage i - 1 instead of stalling 14 warps on
+// two CTA barriers per stage (v3: 23% of warp samples were barrier stalls).
+//
+//   warps 0..13  compute: fwd(i) -> [ZFREE] store partial Z(i) -> [arrive ZFULL]
+//                -> bwd(i - 1) (waits EFULL(i - 1); re-reads and re-splits X(i - 1)
+//                from shared memory instead of keeping two stages of fragments in
+//                registers) -> release X(i - 1) to the producer.  The pipeline
+//                drains at each batch end (W update needs every stage's gradient).
+//   warp 14      TMA row gather (as v3).
+//   warp 15      softmax + CE error + bias (owns b and its gradient): waits
+//                ZFULL(i), sums the 14 partials, arrives ZFREE, writes E(i) into
+//                a parity double buffer, arrives EFULL(i & 1).
+// Named barriers (producer arrive / consumer sync, 448 + 32 threads each):
+//   1 ZFULL, 2 ZFREE, 3 + (i & 1) EFULL.
+// ============================================================================
+constexpr int kPWarps = 14, kPThreads = 16 * 32, kPStages = 3;
+constexpr int kPSoft = 15, kPProd = 14;
+
+struct PipeGeom {
+  int Fs, Es, Zs;
+  int off_master, off_x, off_zp, off_e, off_lab, off_bar, off_bias, bytes;
+};
+
+static bool plan_pipe(int F, int C, int max_smem, PipeGeom& g) {
+  if (F != kFWarps * kFK8 * 8 || C > 16) return false;
+  g.Fs = F;
+  while (g.Fs % 32 != 8) g.Fs += 4;
+  g.Es = 20;  // 5 x 16 B per row: conflict-free 128-bit row accesses by 8 consecutive rows
+  g.Zs = 20;
+  int off = 0;
+  g.off_master = off; off = a16(off + kPWarps * kFK8 * 32 * 16);
+  g.off_x = off;      off = a16(off + kPStages * kFRows * g.Fs * 4);
+  g.off_zp = off;     off = a16(off + kPWarps * kFRows * g.Zs * 4);
+  g.off_e = off;      off = a16(off + 2 * kFRows * g.Es * 4);
+  g.off_lab = off;    off = a16(off + kPStages * kFRows * 4);
+  g.off_bar = off;    off = a16(off + 2 * kPStages * 8);
+  g.off_bias = off;   off = a16(off + 16 * 4);
+  g.bytes = off;
+  return off <= max_smem;
+}
+
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kPThreads, 1)
+    train_pipe_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const int F,
+                      const int C, const PipeGeom g) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* master = reinterpret_cast<float4*>(smem + g.off_master);
+  float* Xb = reinterpret_cast<float*>(smem + g.off_x);
+  float* Zp = reinterpret_cast<float*>(smem + g.off_zp);
+  float* Eb = reinterpret_cast<float*>(smem + g.off_e);  // [2][16][Es]
+  int* labels = reinterpret_cast<int*>(smem + g.off_lab);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.off_bar);
+  uint64_t* empty = full + kPStages;
+  float* bias_out = reinterpret_cast<float*>(smem + g.off_bias);
+  constexpr int S = kPStages, NCOMP = kPWarps * 32 + 32;  // barrier participants: compute + softmax warp
+  const int Fs = g.Fs, Es = g.Es, Zs = g.Zs;
+  const fedhc_client cl = clients[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int FC = F * C;
+
+  for (int i = tid; i < S * kFRows * Fs; i += kPThreads) Xb[i] = 0.f;
+  for (int i = tid; i < 2 * kFRows * Es; i += kPThreads) Eb[i] = 0.f;
+  fence_proxy_async_smem();
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPWarps);  // every compute warp releases a stage after its backward
+    }
+    fence_mbar_init();
+  }
+  const int n = cl.n_rows, B = cl.batch_size;
+  const int steps = n > 0 ? cl.n_batches : 0;
+  auto w_at = [&](int f, int c) -> float { return c < C ? static_cast<float>(params[(size_t)f * C + c]) : 0.f; };
+
+  uint32_t wh[kFK8][2], wm[kFK8][2];
+  if (warp < kPWarps) {
+#pragma unroll
+    for (int j = 0; j < kFK8; ++j) {
+      const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
+      const float4 m = make_float4(w_at(f0, gq), w_at(f0 + 1, gq), w_at(f0, gq + 8), w_at(f0 + 1, gq + 8));
+      master[(warp * kFK8 + j) * 32 + lane] = m;
+      split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
+      split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
+    }
+  }
+  __syncthreads();
+
+  if (warp == kPProd) {
+    // ===== producer: TMA row gather (one bulk copy per row) =====
+    int k = 0, st = 0;
+    for (int s = 0; s < steps; ++s) {
+      const BatchRef br = batch_ref(s, n, B);
+      for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
+        const int rows = min(kFRows, br.rows - r0);
+        if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+        int idx = 0;
+        if (lane < rows) {
+          idx = cl.perm[br.perm_off + r0 + lane];
+          labels[st * kFRows + lane] = cl.y[idx];
+          __threadfence_block();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows * F * 4));
+        __syncwarp();
+        if (lane < rows) {
+          fence_proxy_async_smem();
+          bulk_g2s(Xb + (size_t)(st * kFRows + lane) * Fs, cl.x + (size_t)idx * F, static_cast<uint32_t>(F * 4),
+                   &full[st]);
+        }
+        ++k;
+        st = (st + 1 == S) ? 0 : st + 1;
+      }
+    }
+  } else if (warp == kPSoft) {
+    // ===== softmax warp: lane = (row r = lane & 15, class half h = lane >> 4): 8 classes per lane,
+    // 128-bit partial loads, in-thread max / sum, one cross-half exchange per reduction =====
+    const int r = lane & 15, h = lane >> 4, c0 = 8 * h;
+    float bias[8], gb[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      bias[e] = c0 + e < C ? static_cast<float>(params[FC + c0 + e]) : 0.f;
+      gb[e] = 0.f;
+    }
+    const float lr = cl.lr;
+    named_arrive(2, NCOMP);  // Z buffer initially free
+    int k = 0, st = 0;
+    for (int s = 0; s < steps; ++s) {
+      const BatchRef br = batch_ref(s, n, B);
+      const float inv_nb = 1.0f / static_cast<float>(br.rows);
+      for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
+        const int rows = min(kFRows, br.rows - r0);
+        mbar_wait(&full[st], (k / S) & 1);  // labels of this stage
+        const int y = labels[st * kFRows + r];
+        named_sync(1, NCOMP);               // ZFULL
+        float z[8];
+        {
+          const float* zr = Zp + (size_t)r * Zs + c0;
+          float4 a0 = *reinterpret_cast<const float4*>(zr), a1 = *reinterpret_cast<const float4*>(zr + 4);
+          float4 b0 = *reinterpret_cast<const float4*>(zr + kFRows * Zs),
+                 b1 = *reinterpret_cast<const float4*>(zr + kFRows * Zs + 4);
+#pragma unroll
+          for (int w = 2; w < kPWarps; w += 2) {
+            const float* p0 = zr + (size_t)w * kFRows * Zs;
+            const float* p1 = p0 + kFRows * Zs;
+            const float4 u0 = *reinterpret_cast<const float4*>(p0), u1 = *reinterpret_cast<const float4*>(p0 + 4);
+            const float4 v0 = *reinterpret_cast<const float4*>(p1), v1 = *reinterpret_cast<const float4*>(p1 + 4);
+            a0.x += u0.x; a0.y += u0.y; a0.z += u0.z; a0.w += u0.w;
+            a1.x += u1.x; a1.y += u1.y; a1.z += u1.z; a1.w += u1.w;
+            b0.x += v0.x; b0.y += v0.y; b0.z += v0.z; b0.w += v0.w;
+            b1.x += v1.x; b1.y += v1.y; b1.z += v1.z; b1.w += v1.w;
+          }
+          z[0] = a0.x + b0.x; z[1] = a0.y + b0.y; z[2] = a0.z + b0.z; z[3] = a0.w + b0.w;
+          z[4] = a1.x + b1.x; z[5] = a1.y + b1.y; z[6] = a1.z + b1.z; z[7] = a1.w + b1.w;
+        }
+        named_arrive(2, NCOMP);             // ZFREE: partials consumed
+        float m = -FLT_MAX;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          z[e] = c0 + e < C ? bias[e] + z[e] : -FLT_MAX;
+          m = fmaxf(m, z[e]);
+        }
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        float ssum = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          z[e] = c0 + e < C ? expf(z[e] - m) : 0.f;
+          ssum += z[e];
+        }
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, 16);
+        const float inv = __frcp_rn(ssum);
+        float err[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          err[e] = (r < rows && c0 + e < C) ? (z[e] * inv - (c0 + e == y ? 1.f : 0.f)) * inv_nb : 0.f;
+          gb[e] += err[e];
+        }
+        float* E = Eb + (k & 1) * kFRows * Es + r * Es + c0;
+        *reinterpret_cast<float4*>(E) = make_float4(err[0], err[1], err[2], err[3]);
+        *reinterpret_cast<float4*>(E + 4) = make_float4(err[4], err[5], err[6], err[7]);
+        __syncwarp();
+        named_arrive(3 + (k & 1), NCOMP);   // EFULL(k)
+        ++k;
+        st = (st + 1 == S) ? 0 : st + 1;
+      }
+      // bias step: column sums over the batch rows (the 16 lanes of this half), fixed order
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float v = gb[e];
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (c0 + e < C) bias[e] -= lr * v;
+        gb[e] = 0.f;
+      }
+    }
+    if (r == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) bias_out[c0 + e] = bias[e];
+    }
+  } else {
+    // ===== 14 compute warps =====
+    float G[kFK8][4];
+#pragma unroll
+    for (int j = 0; j < kFK8; ++j) G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
+    const float lr = cl.lr;
+    // load + split this warp's 7 k8 slices of X rows (gq, gq + 8) from stage buffer Xs
+    auto load_split = [&](const float* Xs, uint32_t (&ah)[kFK8][2], uint32_t (&am)[kFK8][2]) {
+#pragma unroll
+      for (int j = 0; j < kFK8; ++j) {
+        const float* base = Xs + gq * Fs + 8 * (warp * kFK8 + j) + 2 * tq;
+        const float2 v0 = *reinterpret_cast<const float2*>(base);
+        const float2 v1 = *reinterpret_cast<const float2*>(base + 8 * Fs);
+        split_bf16x2(v0.x, v0.y, ah[j][0], am[j][0]);
+        split_bf16x2(v1.x, v1.y, ah[j][1], am[j][1]);
+      }
+    };
+    auto backward = [&](int kk, int sst) {
+      named_sync(3 + (kk & 1), NCOMP);  // EFULL(kk)
+      const float* E = Eb + (kk & 1) * kFRows * Es;
+      uint32_t eh[4], em[4];
+      split_bf16x2(E[(2 * tq) * Es + gq], E[(2 * tq + 1) * Es + gq], eh[0], em[0]);
+      split_bf16x2(E[(2 * tq) * Es + gq + 8], E[(2 * tq + 1) * Es + gq + 8], eh[1], em[1]);
+      split_bf16x2(E[(2 * tq + 8) * Es + gq], E[(2 * tq + 9) * Es + gq], eh[2], em[2]);
+      split_bf16x2(E[(2 * tq + 8) * Es + gq + 8], E[(2 * tq + 9) * Es + gq + 8], eh[3], em[3]);
+      uint32_t ah[kFK8][2], am[kFK8][2];
+      load_split(Xb + (size_t)sst * kFRows * Fs, ah, am);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sst]);  // X(kk) read into registers: stage free
+#pragma unroll
+      for (int j = 0; j < kFK8; ++j) {
+        const uint32_t t0h = movmatrix_trans(ah[j][0]), t1h = movmatrix_trans(ah[j][1]);
+        const uint32_t t0m = movmatrix_trans(am[j][0]), t1m = movmatrix_trans(am[j][1]);
+        mma_bf16(G[j], eh, t0h, t1h);
+        mma_bf16(G[j], eh, t0m, t1m);
+        mma_bf16(G[j], em, t0h, t1h);
+      }
+    };
+    int k = 0, st = 0;
+    for (int s = 0; s < steps; ++s) {
+      const BatchRef br = batch_ref(s, n, B);
+      int prev_k = -1, prev_st = 0;
+      for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
+        mbar_wait(&full[st], (k / S) & 1);
+        const float* Xs = Xb + (size_t)st * kFRows * Fs;
+        float acc[2][2][4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) acc[e][nt][0] = acc[e][nt][1] = acc[e][nt][2] = acc[e][nt][3] = 0.f;
+        {
+          uint32_t ah[kFK8][2], am[kFK8][2];
+          load_split(Xs, ah, am);
+#pragma unroll
+          for (int j = 0; j + 1 < kFK8; j += 2) {
+            const uint32_t AH[4] = {ah[j][0], ah[j][1], ah[j + 1][0], ah[j + 1][1]};
+            const uint32_t AM[4] = {am[j][0], am[j][1], am[j + 1][0], am[j + 1][1]};
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wm[j][nt], wm[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AM, wh[j][nt], wh[j + 1][nt]);
+            }
+          }
+          constexpr int jl = kFK8 - 1;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            mma_bf16_k8(acc[1][nt], ah[jl][0], ah[jl][1], wh[jl][nt]);
+            mma_bf16_k8(acc[1][nt], ah[jl][0], ah[jl][1], wm[jl][nt]);
+            mma_bf16_k8(acc[1][nt], am[jl][0], am[jl][1], wh[jl][nt]);
+          }
+        }
+        named_sync(2, NCOMP);  // ZFREE: the softmax warp has consumed the previous partials
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          float* zr = Zp + (size_t)(warp * kFRows + gq) * Zs + nt * 8 + 2 * tq;
+          *reinterpret_cast<float2*>(zr) = make_float2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
+          *reinterpret_cast<float2*>(zr + 8 * Zs) =
+              make_float2(acc[0][nt][2] + acc[1][nt][2], acc[0][nt][3] + acc[1][nt][3]);
+        }
+        named_arrive(1, NCOMP);  // ZFULL
+        if (prev_k >= 0) backward(prev_k, prev_st);
+        prev_k = k;
+        prev_st = st;
+        ++k;
+        st = (st + 1 == S) ? 0 : st + 1;
+      }
+      if (prev_k >= 0) backward(prev_k, prev_st);
+      // ---- end of batch: thread-local SGD step on the master + re-split ----
+#pragma unroll
+      for (int j = 0; j < kFK8; ++j) {
+        float4& mref = master[(warp * kFK8 + j) * 32 + lane];
+        float4 m = mref;
+        m.x -= lr * G[j][0];
+        m.y -= lr * G[j][1];
+        m.z -= lr * G[j][2];
+        m.w -= lr * G[j][3];
+        mref = m;
+        split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
+        split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
+        G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
+      }
+    }
+    named_sync(2, NCOMP);  // match the softmax warp's last ZFREE arrival
+  }
+  __syncthreads();
+
+  // ---- epilogue: delta = W_final - W_initial ----
+  float* out = cl.delta;
+  if (warp < kPWarps) {
+#pragma unroll
+    for (int j = 0; j < kFK8; ++j) {
+      const float4 m = master[(warp * kFK8 + j) * 32 + lane];
+      const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
+      const float v[4] = {m.x, m.y, m.z, m.w};
+      const int fo[4] = {f0, f0 + 1, f0, f0 + 1};
+      const int co[4] = {gq, gq, gq + 8, gq + 8};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (co[i] < C) {
+          const size_t gi = (size_t)fo[i] * C + co[i];
+          out[gi] = v[i] - static_cast<float>(params[gi]);
+        }
+    }
+  }
+  if (tid < C) out[FC + tid] = (steps > 0 ? bias_out[tid] : static_cast<float>(params[FC + tid])) -
+                               static_cast<float>(params[FC + tid]);
+}
+
 template <bool FULL, int CL>
 static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, const double* params,
                                    const FusedGeom& g, cudaStream_t st) {
@@ -455,6 +790,17 @@ static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, c
 // Launch the fused kernel if the shape fits; returns false to fall back.
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
                         int max_smem, cudaStream_t st, int* status) {
+  static const bool v3_only = getenv("FEDHC_TRAIN_V3") != nullptr;
+  PipeGeom pg{};
+  if (!v3_only && plan_pipe(F, C, max_smem, pg)) {
+    cudaError_t e = cudaFuncSetAttribute(train_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.bytes);
+    if (e == cudaSuccess) {
+      train_pipe_kernel<<<n_clients, kPThreads, pg.bytes, st>>>(clients, params, F, C, pg);
+      e = cudaGetLastError();
+    }
+    *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_pipe_kernel launch");
+    return true;
+  }
   FusedGeom g{};
   if (!plan_fused(F, C, max_smem, g)) return false;
   const int cl = C <= 16 ? 1 : C <= 32 ? 2 : 4;
