@@ -298,6 +298,12 @@ int fedhc_cnn_last_loss(void* ws, float* out, int n_clients, void* stream);
 /* *correct (dev u64) += test rows whose first-max argmax == label. */
 int fedhc_cnn_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
                    unsigned long long* correct, void* stream);
+/* conv2 of the engine as one implicit GEMM on caller tensors (tests / tooling): mode 1 forward
+ * (out = relu(conv(p1x, w) + bias)), 2 data gradient (out = dL/dp1 from act = dL/da2), 3 weight
+ * gradient + SGD (out = fp32 master [G][1024][64] -= lr * grad; act = p1x, act2 = dL/da2).
+ * NHWC bf16 activations [G*bp][14][14][C]; w bf16 [G][1024][64] tap-pair layout. */
+int fedhc_cnn_conv2(int mode, int G, int bp, const void* act, const void* act2, const void* w, const float* bias,
+                    void* out, float lr, void* stream);
 
 #ifdef __cplusplus
 }

@@ -57,9 +57,10 @@ class CnnLayout:
         w1[:25] = np.asarray(p["conv1.weight"]).reshape(32, 25).T
         v[o["conv1.weight"]:o["conv1.weight"] + 64 * 32] = w1.ravel()
         v[o["conv1.bias"]:o["conv1.bias"] + 32] = p["conv1.bias"]
-        w2 = np.zeros((28, 32, 64))
-        w2[:25] = np.asarray(p["conv2.weight"]).reshape(64, 32, 25).transpose(2, 1, 0)
-        v[o["conv2.weight"]:o["conv2.weight"] + 896 * 64] = w2.ravel()
+        # [pair = kh*3 + kw//2][kw % 2][ci][co]; kw = 5 and pair 15 are zero padding (csrc/cnn.cu)
+        w2 = np.zeros((5, 6, 32, 64))
+        w2[:, :5] = np.asarray(p["conv2.weight"]).transpose(2, 3, 1, 0)
+        v[o["conv2.weight"]:o["conv2.weight"] + 15 * 64 * 64] = w2.ravel()
         v[o["conv2.bias"]:o["conv2.bias"] + 64] = p["conv2.bias"]
         f1 = np.zeros((2048, 3200))
         f1[:, :3136] = np.asarray(p["fc1.weight"]).reshape(2048, 64, 7, 7).transpose(0, 2, 3, 1).reshape(2048, 3136)
@@ -75,13 +76,13 @@ class CnnLayout:
         v = np.asarray(v.detach().cpu().numpy() if isinstance(v, torch.Tensor) else v, dtype=np.float64)
         c, o = self.n_classes, self.off
         w1 = v[o["conv1.weight"]:o["conv1.weight"] + 64 * 32].reshape(64, 32)
-        w2 = v[o["conv2.weight"]:o["conv2.weight"] + 896 * 64].reshape(28, 32, 64)
+        w2 = v[o["conv2.weight"]:o["conv2.weight"] + 15 * 64 * 64].reshape(5, 6, 32, 64)[:, :5]
         f1 = v[o["fc1.weight"]:o["fc1.weight"] + 2048 * 3200].reshape(2048, 3200)
         f2 = v[o["fc2.weight"]:o["fc2.weight"] + 64 * 2048].reshape(64, 2048)
         return {
             "conv1.weight": w1[:25].T.reshape(32, 1, 5, 5).copy(),
             "conv1.bias": v[o["conv1.bias"]:o["conv1.bias"] + 32].copy(),
-            "conv2.weight": w2[:25].transpose(2, 1, 0).reshape(64, 32, 5, 5).copy(),
+            "conv2.weight": w2.transpose(3, 2, 0, 1).copy(),
             "conv2.bias": v[o["conv2.bias"]:o["conv2.bias"] + 64].copy(),
             "fc1.weight": f1[:, :3136].reshape(2048, 7, 7, 64).transpose(0, 3, 1, 2).reshape(2048, 3136).copy(),
             "fc1.bias": v[o["fc1.bias"]:o["fc1.bias"] + 2048].copy(),

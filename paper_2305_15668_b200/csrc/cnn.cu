@@ -19,9 +19,9 @@
 // zero and carry zero gradient, so ragged and finished clients are exact):
 //   gather+im2col1  x[perm] -> cols1 [Bp*784][64]   (25 taps, zero-padded)
 //   conv1  GEMM     cols1 . Wc1^T  + b, ReLU -> a1 [Bp*784][32]        (N=32)
-//   pool1           a1 -> p1 [Bp][14][14][32]
-//   im2col2         p1 -> cols2 [Bp*196][896]          (28 taps x 32, 3 zero)
-//   conv2  GEMM     cols2 . Wc2    + b, ReLU -> a2 [Bp*196][64]
+//   pool1           a1 -> p1x [Bp][14][15][64]  channel pairs p1(y,x-1) | p1(y,x)
+//   conv2  implicit GEMM (TMA 4-D boxes, OOB = zero padding): 15 tap pairs x 64
+//                   p1x . Wc2 + b, ReLU -> a2 [Bp][14][14][64]
 //   pool2           a2 -> p2 [Bp][3200]                (7*7*64 + 64 zero)
 //   fc1    GEMM     W1 . p2^T      + b, ReLU -> hT [2048][Bp]
 //   fc2    GEMM     h . W2^T                  -> logits [Bp][64] fp32  (M=64)
@@ -31,9 +31,9 @@
 //   fc1 dgrad       dh . W1                  -> dp2 [Bp][3200]         (M=64)
 //   fc1 wgrad+SGD   W1 -= lr dhT . p2
 //   pool2 bwd       dp2, a2 -> da2 [Bp*196][64] (+ db2 partials)
-//   conv2 dgrad     da2 . Wc2^T              -> dcols2 [Bp*196][896]
-//   conv2 wgrad+SGD Wc2 -= lr cols2^T . da2
-//   col2im+pool1 bwd dcols2, a1 -> da1 [32][Bp*784] (channel-major) (+ db1 partials)
+//   conv2 dgrad     implicit GEMM over 25 taps: da2 (shifted) . Wc2[tap] -> dp1 [Bp][14][14][32]
+//   conv2 wgrad+SGD implicit GEMM over 8x8 pixel blocks: Wc2 -= lr p1x(shifted)^T . da2
+//   pool1 bwd       dp1, a1 -> da1 [32][Bp*784] (channel-major) (+ db1 partials)
 //   conv1 wgrad+SGD Wc1 -= lr cols1^T . da1                     (M=64, N=32)
 //   bias SGD, Wc1 shadow transpose
 // The step sequence of a round is captured once into a CUDA graph and replayed.
@@ -53,15 +53,16 @@ constexpr int HW0 = 784, W0 = 28;              // input 28x28x1
 constexpr int C1 = 32, W1d = 14, HW1 = 196;    // after conv1 + pool
 constexpr int C2 = 64, W2d = 7, HW2 = 49;      // after conv2 + pool
 constexpr int T1 = 64;                         // conv1 im2col width (25 taps)
-constexpr int TAPS2 = 28, K2 = TAPS2 * C1;     // 896
+constexpr int WR2 = 16 * 64;                   // conv2 weight rows: 16 tap pairs x (2 taps x 32 ci)
 constexpr int F1 = 3200;                       // fc1 input: 7*7*64 = 3136 + 64 zero
 constexpr int HID = 2048, NC = 64;
 
 // fp32 master / bf16 shadow layout of one client's parameters (elements)
 constexpr int64_t OFF_WC1 = 0;                       // [64 taps][32]   (shadow: [32][64])
 constexpr int64_t OFF_BC1 = OFF_WC1 + T1 * C1;       // [32] (+32 pad)
-constexpr int64_t OFF_WC2 = OFF_BC1 + 64;            // [896][64]
-constexpr int64_t OFF_BC2 = OFF_WC2 + K2 * C2;       // [64]
+// conv2 weights [pair = kh*3 + kw/2][kw%2][ci][co]; kw = 5 rows and pair 15 are zero padding
+constexpr int64_t OFF_WC2 = OFF_BC1 + 64;            // [1024][64]
+constexpr int64_t OFF_BC2 = OFF_WC2 + WR2 * C2;      // [64]
 constexpr int64_t OFF_W1 = OFF_BC2 + 64;             // [2048][3200]
 constexpr int64_t OFF_B1 = OFF_W1 + (int64_t)HID * F1;  // [2048]
 constexpr int64_t OFF_W2 = OFF_B1 + HID;             // [64][2048]
@@ -150,23 +151,35 @@ __global__ void __launch_bounds__(256) pool_fwd_kernel(const __nv_bfloat16* __re
   }
 }
 
-// ---- im2col of conv2: p1 [n_img][14][14][32] -> cols2 [n_img*196][896] -----------
-__global__ void __launch_bounds__(256) im2col2_kernel(const __nv_bfloat16* __restrict__ p1,
-                                                      __nv_bfloat16* __restrict__ cols2, int64_t n_img) {
-  const int64_t total = n_img * HW1 * TAPS2 * 4;  // 4 x 16 B per (pixel, tap)
+// ---- pool1 into the channel-pair layout of the conv2 implicit GEMM -----------------
+// a1 [n_img][28][28][32] -> p1x [n_img][14][15][64]: column xx = x + 1 holds p1(y, x) | p1(y, x + 1)
+// (zero outside the 14x14 map), so one 128-byte TMA row = the two horizontally adjacent taps of a tap
+// pair, including the pair straddling the left edge (x = -1).
+constexpr int W1X = 15;
+__global__ void __launch_bounds__(256) pool1_pairs_kernel(const __nv_bfloat16* __restrict__ a1,
+                                                          __nv_bfloat16* __restrict__ p1x, int64_t n_img) {
+  const int64_t total = n_img * HW1 * 4;  // (image, pooled pixel, 8-channel group)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(i & 3);
-    const int t = (int)((i >> 2) % TAPS2);
-    const int64_t px = (i >> 2) / TAPS2;
+    const int cg = (int)(i & 3);
+    const int64_t px = i >> 2;
     const int64_t n = px / HW1;
-    const int p = (int)(px - n * HW1), h = p / W1d, w = p - h * W1d;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (t < 25) {
-      const int ih = h + t / 5 - 2, iw = w + t % 5 - 2;
-      if (ih >= 0 && ih < W1d && iw >= 0 && iw < W1d)
-        v = *reinterpret_cast<const uint4*>(p1 + ((n * HW1 + ih * W1d + iw) * C1) + q * 8);
-    }
-    *reinterpret_cast<uint4*>(cols2 + px * K2 + t * C1 + q * 8) = v;
+    const int p = (int)(px - n * HW1), oh = p / W1d, ow = p - oh * W1d;
+    const __nv_bfloat16* base = a1 + ((n * W0 + 2 * oh) * W0 + 2 * ow) * C1 + cg * 8;
+    uint4 q0 = *reinterpret_cast<const uint4*>(base);
+    const uint4 q1 = *reinterpret_cast<const uint4*>(base + C1);
+    const uint4 q2 = *reinterpret_cast<const uint4*>(base + (int64_t)W0 * C1);
+    const uint4 q3 = *reinterpret_cast<const uint4*>(base + (int64_t)W0 * C1 + C1);
+    __nv_bfloat162* a = reinterpret_cast<__nv_bfloat162*>(&q0);
+    const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q2);
+    const __nv_bfloat162* b3 = reinterpret_cast<const __nv_bfloat162*>(&q3);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = __hmax2(__hmax2(a[k], b1[k]), __hmax2(b2[k], b3[k]));
+    __nv_bfloat16* row = p1x + (n * W1d + oh) * W1X * 64;
+    *reinterpret_cast<uint4*>(row + (ow + 1) * 64 + cg * 8) = q0;   // column x + 1, low half
+    *reinterpret_cast<uint4*>(row + ow * 64 + 32 + cg * 8) = q0;    // column x, high half
+    if (ow == 0) *reinterpret_cast<uint4*>(row + cg * 8) = make_uint4(0, 0, 0, 0);
+    if (ow == W1d - 1) *reinterpret_cast<uint4*>(row + W1d * 64 + 32 + cg * 8) = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -288,21 +301,21 @@ __global__ void __launch_bounds__(256) pool2_bwd_kernel(const __nv_bfloat16* __r
                                    red[3][threadIdx.x];
 }
 
-constexpr int kC2iSmem = C1 * HW0 * 2;
+constexpr int kP1bSmem = C1 * HW0 * 2;
 
-// grid (Bp, G): col2im of dcols2 + maxpool1 backward + ReLU mask -> da1 channel-major
-// dcols2 [G][Bp*196][896], a1 [G][Bp][784][32] -> da1 [G][32][Bp*784], part [G][Bp][32]
-// thread item = (pooled pixel p, group of 8 channels): 16-byte loads of every tap's 8 channels.
-__global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat16* __restrict__ dcols2,
-                                                               const __nv_bfloat16* __restrict__ a1,
-                                                               __nv_bfloat16* __restrict__ da1,
-                                                               float* __restrict__ part, int Bp) {
-  extern __shared__ __align__(16) unsigned char c2i_smem[];
-  auto tile = reinterpret_cast<__nv_bfloat16(*)[HW0]>(c2i_smem);  // [C1][HW0], 50 KB (dynamic)
+// grid (Bp, G): maxpool1 backward + ReLU mask of dp1 -> da1 channel-major
+// dp1 [G][Bp][196][32], a1 [G][Bp][784][32] -> da1 [G][32][Bp*784], part [G][Bp][32]
+// thread item = (pooled pixel p, group of 8 channels)
+__global__ void __launch_bounds__(256) pool1_bwd_kernel(const __nv_bfloat16* __restrict__ dp1,
+                                                        const __nv_bfloat16* __restrict__ a1,
+                                                        __nv_bfloat16* __restrict__ da1, float* __restrict__ part,
+                                                        int Bp) {
+  extern __shared__ __align__(16) unsigned char p1b_smem[];
+  auto tile = reinterpret_cast<__nv_bfloat16(*)[HW0]>(p1b_smem);  // [C1][HW0], 50 KB (dynamic)
   __shared__ float red[256][9];
   const int g = blockIdx.y, b = blockIdx.x;
   const int64_t img = (int64_t)g * Bp + b;
-  const __nv_bfloat16* dc = dcols2 + img * HW1 * K2;
+  const __nv_bfloat16* d = dp1 + img * HW1 * C1;
   const __nv_bfloat16* a = a1 + img * HW0 * C1;
   const int cg = threadIdx.x & 3;            // channels [8 cg, 8 cg + 8) (256 % 4 == 0: fixed per thread)
   float acc[8];
@@ -310,23 +323,7 @@ __global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   for (int item = threadIdx.x; item < HW1 * 4; item += 256) {
     const int p = item >> 2, ph = p / W1d, pw = p - ph * W1d;
-    float s[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) s[e] = 0.f;
-    for (int kh = 0; kh < 5; ++kh) {
-      const int oh = ph - kh + 2;
-      if (oh < 0 || oh >= W1d) continue;
-#pragma unroll
-      for (int kw = 0; kw < 5; ++kw) {
-        const int ow = pw - kw + 2;
-        if (ow < 0 || ow >= W1d) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(dc + (int64_t)(oh * W1d + ow) * K2 + (kh * 5 + kw) * C1 +
-                                                        cg * 8);
-        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s[e] += bf(vb[e]);
-      }
-    }
+    const uint4 dv = *reinterpret_cast<const uint4*>(d + p * C1 + cg * 8);
     const int q00 = (2 * ph) * W0 + 2 * pw;
     const int pos[4] = {q00, q00 + 1, q00 + W0, q00 + W0 + 1};
     uint4 av[4];
@@ -339,7 +336,7 @@ __global__ void __launch_bounds__(256) col2im_pool1_bwd_kernel(const __nv_bfloat
       for (int k = 0; k < 4; ++k) v[k] = bf(reinterpret_cast<const __nv_bfloat16*>(&av[k])[e]);
       const int k = first_max4(v[0], v[1], v[2], v[3]);
       const bool on = v[k] > 0.f;
-      const __nv_bfloat16 gz = __float2bfloat16_rn(on ? s[e] : 0.f);
+      const __nv_bfloat16 gz = on ? reinterpret_cast<const __nv_bfloat16*>(&dv)[e] : __float2bfloat16_rn(0.f);
       const int ci = cg * 8 + e;
 #pragma unroll
       for (int j = 0; j < 4; ++j) tile[ci][pos[j]] = j == k ? gz : __float2bfloat16_rn(0.f);
@@ -389,6 +386,14 @@ __global__ void __launch_bounds__(256) bias_sgd_kernel(float* __restrict__ maste
       const int c = i - C1 - C2 - HID;
       m[OFF_B2 + c] -= lr * db2[(int64_t)g * NC + c];
     }
+  }
+  // conv2 padding taps (kw = 5: second half of every kh's third pair) stay exactly zero
+  __nv_bfloat16* sh2 = shadow + (int64_t)g * PPAD + OFF_WC2;
+  for (int i = threadIdx.x; i < 5 * 32 * C2; i += blockDim.x) {
+    const int kh = i / (32 * C2), r = i - kh * 32 * C2;
+    const int64_t o = (int64_t)(kh * 3 + 2) * 64 * C2 + 32 * C2 + r;
+    m[OFF_WC2 + o] = 0.f;
+    sh2[o] = __float2bfloat16_rn(0.f);
   }
   // conv1 weights: master [64 taps][32] -> shadow [32][64] (the forward B operand, K-major)
   __nv_bfloat16* s = shadow + (int64_t)g * PPAD + OFF_WC1;
@@ -442,7 +447,7 @@ struct Engine {
   int maxG, Bp, C;
   std::vector<std::unique_ptr<Buf>> bufs;
   float* master;
-  __nv_bfloat16 *shadow, *cols1, *a1, *p1, *cols2, *a2, *p2, *hT, *dl, *dhT, *dp2, *da2, *dcols2, *da1;
+  __nv_bfloat16 *shadow, *cols1, *a1, *p1x, *a2, *p2, *hT, *dl, *dhT, *dp2, *da2, *dp1, *da1;
   float *logits, *db1, *db2, *part1, *part2, *loss;
   int32_t *labels, *valid;
   fedhc_client* desc;
@@ -476,8 +481,7 @@ struct Engine {
     rc |= alloc(&shadow, G * PPAD);
     rc |= alloc(&cols1, I * HW0 * T1);
     rc |= alloc(&a1, I * HW0 * C1);
-    rc |= alloc(&p1, I * HW1 * C1);
-    rc |= alloc(&cols2, I * HW1 * K2);
+    rc |= alloc(&p1x, I * W1d * W1X * 64);
     rc |= alloc(&a2, I * HW1 * C2);
     rc |= alloc(&p2, I * F1);
     rc |= alloc(&hT, I * HID);
@@ -486,7 +490,7 @@ struct Engine {
     rc |= alloc(&dhT, I * HID);
     rc |= alloc(&dp2, I * F1);
     rc |= alloc(&da2, I * HW1 * C2);
-    rc |= alloc(&dcols2, I * HW1 * K2);
+    rc |= alloc(&dp1, I * HW1 * C1);
     rc |= alloc(&da1, I * HW0 * C1);
     rc |= alloc(&db1, G * HID);
     rc |= alloc(&db2, G * NC);
@@ -528,12 +532,13 @@ struct Engine {
     a.bias = master + OFF_BC1;
     a.bias_gstride = PPAD;
     if ((rc = tc::gemm_plan(a, c1))) return rc;
-    // conv2: a2[P2][64] = relu(cols2 . Wc2 + bc2), Wc2 stored [896][64] (MN-major B)
-    a = args(G, P2, C2, K2, cols2, false, 0, shadow + OFF_WC2, true, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
+    // conv2 (implicit GEMM): a2[img][14][14][64] = relu(conv(p1x, Wc2) + bc2), 15 tap pairs, Wc2 MN-major
+    const tc::ConvSpec cf{tc::CONV_FWD, bp};
+    a = args(G, 256 * bp, C2, 15 * 64, p1x, false, 0, shadow + OFF_WC2, true, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
     a.D = a2;
     a.bias = master + OFF_BC2;
     a.bias_gstride = PPAD;
-    if ((rc = tc::gemm_plan(a, c2))) return rc;
+    if ((rc = tc::gemm_plan(a, c2, &cf))) return rc;
     // fc1: hT[2048][bp] = relu(W1 . p2^T + b1)
     a = args(G, HID, bp, F1, shadow + OFF_W1, false, PPAD, p2, false, 0, FEDHC_EPI_BIAS_RELU_BF16);
     a.D = hT;
@@ -578,17 +583,19 @@ struct Engine {
     a.d_gstride = PPAD;
     a.lr = lr;
     if ((rc = tc::gemm_plan(a, &fc1_wg))) return rc;
-    // conv2 dgrad: dcols2[P2][896] = da2 . Wc2^T  (B = Wc2 [896][64] K-major)
-    a = args(G, P2, K2, C2, da2, false, 0, shadow + OFF_WC2, false, PPAD, FEDHC_EPI_BF16);
-    a.D = dcols2;
-    if ((rc = tc::gemm_plan(a, &conv2_dg))) return rc;
-    // conv2 wgrad: Wc2[896][64] -= lr cols2^T . da2
-    a = args(G, K2, C2, P2, cols2, true, 0, da2, true, 0, FEDHC_EPI_SGD);
+    // conv2 dgrad (implicit GEMM over the 25 taps): dp1[img][14][14][32] = sum_t shift_t(da2) . Wc2[t]
+    const tc::ConvSpec cd{tc::CONV_DGRAD, Bp};
+    a = args(G, 256 * Bp, C1, 25 * 64, da2, false, 0, shadow + OFF_WC2, false, PPAD, FEDHC_EPI_BF16);
+    a.D = dp1;
+    if ((rc = tc::gemm_plan(a, &conv2_dg, &cd))) return rc;
+    // conv2 wgrad (implicit GEMM over 8x8 pixel blocks): Wc2[1024][64] -= lr p1x(shifted)^T . da2
+    const tc::ConvSpec cw{tc::CONV_WGRAD, Bp};
+    a = args(G, WR2, C2, 256 * Bp, p1x, true, 0, da2, true, 0, FEDHC_EPI_SGD);
     a.master = master + OFF_WC2;
     a.shadow = shadow + OFF_WC2;
     a.d_gstride = PPAD;
     a.lr = lr;
-    if ((rc = tc::gemm_plan(a, &conv2_wg))) return rc;
+    if ((rc = tc::gemm_plan(a, &conv2_wg, &cw))) return rc;
     // conv1 wgrad: Wc1[64][32] -= lr cols1^T . da1  (B = da1 channel-major, K-major)
     a = args(G, T1, C1, P1, cols1, true, 0, da1, false, 0, FEDHC_EPI_SGD);
     a.master = master + OFF_WC1;
@@ -616,8 +623,7 @@ struct Engine {
     int rc;
     gather_im2col1_kernel<<<dim3(bp, G), 256, 0, st>>>(desc, step, bp, cols1, labels, valid);
     if ((rc = tc::gemm_run(c1, st))) return rc;
-    pool_fwd_kernel<<<grid_for(n_img * HW1 * C1 / 8), 256, 0, st>>>(a1, p1, n_img, W0, C1, HW1 * C1);
-    im2col2_kernel<<<grid_for(n_img * HW1 * TAPS2 * 4), 256, 0, st>>>(p1, cols2, n_img);
+    pool1_pairs_kernel<<<grid_for(n_img * HW1 * 4), 256, 0, st>>>(a1, p1x, n_img);
     if ((rc = tc::gemm_run(c2, st))) return rc;
     pool_fwd_kernel<<<grid_for(n_img * HW2 * C2 / 8), 256, 0, st>>>(a2, p2, n_img, W1d, C2, F1);
     if ((rc = tc::gemm_run(f1, st))) return rc;
@@ -635,7 +641,7 @@ struct Engine {
     pool2_bwd_kernel<<<dim3(Bp, G), 256, 0, st>>>(dp2, a2, da2, part2, Bp);
     if ((rc = tc::gemm_run(conv2_dg, st))) return rc;
     if ((rc = tc::gemm_run(conv2_wg, st))) return rc;
-    col2im_pool1_bwd_kernel<<<dim3(Bp, G), 256, kC2iSmem, st>>>(dcols2, a1, da1, part1, Bp);
+    pool1_bwd_kernel<<<dim3(Bp, G), 256, kP1bSmem, st>>>(dp1, a1, da1, part1, Bp);
     if ((rc = tc::gemm_run(conv1_wg, st))) return rc;
     bias_sgd_kernel<<<G, 256, 0, st>>>(master, shadow, part1, part2, db1, db2, Bp, lr);
     FEDHC_CUDA_TRY(cudaGetLastError());
@@ -670,8 +676,8 @@ extern "C" int fedhc_cnn_create(int max_clients, int batch, int n_classes, void*
   e->maxG = max_clients;
   e->Bp = (batch + 63) / 64 * 64;
   e->C = n_classes;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::col2im_pool1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      cnn::kC2iSmem));
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::pool1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      cnn::kP1bSmem));
   FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       e->Bp * cnn::NC * 4));
   int rc = e->init();
@@ -768,4 +774,36 @@ extern "C" int fedhc_cnn_eval(void* ws, const double* params, const float* x, co
     FEDHC_CUDA_TRY(cudaStreamSynchronize(st));  // host descriptor reused next chunk
   }
   return FEDHC_OK;
+}
+
+// ---- implicit-GEMM conv2 entry (tests / tooling): one mode on caller tensors ------------------
+// mode 1 FWD:   out bf16 [G*bp][14][14][64] = relu(conv(act = p1x [G*bp][14][15][64], w) + bias[g])
+// mode 2 DGRAD: out bf16 [G*bp][14][14][32] = conv^T(act = da2 [G*bp][14][14][64], w)
+// mode 3 WGRAD: master fp32 [G][1024][64] -= lr * (act = p1x)^T (*) (act2 = da2)
+// w: bf16 [G][1024][64] in the engine's tap-pair layout (csrc/cnn.cu OFF_WC2 block).
+extern "C" int fedhc_cnn_conv2(int mode, int G, int bp, const void* act, const void* act2, const void* w,
+                               const float* bias, void* out, float lr, void* stream) {
+  if (G < 1 || bp < 1 || !act || !out) return fail(FEDHC_ERR_VALUE, "cnn_conv2: bad arguments");
+  fedhc_gemm_args a{};
+  a.G = G;
+  tc::ConvSpec cs{mode, bp};
+  if (mode == tc::CONV_FWD) {
+    if (!w || !bias) return fail(FEDHC_ERR_VALUE, "cnn_conv2: missing weights / bias");
+    a.M = 256 * bp; a.N = 64; a.K = 960; a.A = act; a.B = w; a.b_mn = 1; a.b_gstride = cnn::WR2 * 64;
+    a.epilogue = FEDHC_EPI_BIAS_RELU_BF16; a.D = out; a.bias = bias; a.bias_gstride = 64;
+  } else if (mode == tc::CONV_DGRAD) {
+    if (!w) return fail(FEDHC_ERR_VALUE, "cnn_conv2: missing weights");
+    a.M = 256 * bp; a.N = 32; a.K = 1600; a.A = act; a.B = w; a.b_gstride = cnn::WR2 * 64;
+    a.epilogue = FEDHC_EPI_BF16; a.D = out;
+  } else if (mode == tc::CONV_WGRAD) {
+    if (!act2) return fail(FEDHC_ERR_VALUE, "cnn_conv2: missing da2");
+    a.M = cnn::WR2; a.N = 64; a.K = 256 * bp; a.A = act; a.a_mn = 1; a.B = act2; a.b_mn = 1;
+    a.epilogue = FEDHC_EPI_SGD; a.master = static_cast<float*>(out); a.d_gstride = cnn::WR2 * 64; a.lr = lr;
+  } else {
+    return fail(FEDHC_ERR_VALUE, "cnn_conv2: unknown mode");
+  }
+  tc::GemmPlan p;
+  int rc = tc::gemm_plan(a, &p, &cs);
+  if (rc) return rc;
+  return tc::gemm_run(p, static_cast<cudaStream_t>(stream));
 }

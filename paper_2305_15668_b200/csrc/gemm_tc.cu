@@ -84,6 +84,15 @@ __device__ __forceinline__ void tma_load_3d(uint32_t smem_dst, const CUtensorMap
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(uint32_t smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -117,6 +126,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sm
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t smem_src, int c0, int c1, int c2,
+                                             int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -158,12 +174,48 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 
+// ---- implicit-GEMM convolution operand loads (5x5 'same' conv on 14x14 NHWC maps) ---------------
+// Activations are 4-D tensor maps {C, 14 (x), 14 (y), images}; TMA zero-fills out-of-bounds
+// coordinates, which is the convolution's zero padding (and the x, y in [14, 16) slack of a tile).
+//   FWD   D[pixel slot][co] = sum_{pair} A[slot][64] . Wt[pair]   A = p1x [img][14][15][64]: column xx holds the
+//         channel pair p1(y, xx - 1) | p1(y, xx) (zero outside the map), so the pair's left tap may sit at x = -1
+//         M tile = 8 rows x 16 columns of one image (y0 = 0 / 8); K block = tap pair (kh, kw = 2pk, 2pk + 1)
+//   DGRAD D[pixel slot][ci] = sum_{tap} A[slot - shift][64 co] . W[tap][ci][co]   A = dL/da2
+//   WGRAD D[pair row][co]   = sum_{pixels} p1x[pixel + shift(pair)][64] . dL/da2[pixel][co]
+//         K block = one 8x8 pixel block of one image; M tile = 2 tap pairs (pair 15 is padding: a fully
+//         out-of-bounds box, i.e. zeros)
+template <int BM, int BN>
+__device__ __forceinline__ void conv_loads(const ConvSpec& cv, uint32_t sa, uint32_t sb, const CUtensorMap* map_a,
+                                           const CUtensorMap* map_b, uint64_t* bar, int g, int m0, int n0, int kb) {
+  const int mt = m0 / BM;
+  if (cv.mode == CONV_FWD) {
+    const int img = g * cv.bp + (mt >> 1), y0 = (mt & 1) * 8;
+    const int kh = kb / 3, pk = kb - 3 * kh;
+    tma_load_4d(sa, map_a, bar, 0, 2 * pk - 1, y0 + kh - 2, img);  // p1x column xx = x + 1
+#pragma unroll
+    for (int h = 0; h < BN / 64; ++h) tma_load_3d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, kb * BK, g);
+  } else if (cv.mode == CONV_DGRAD) {
+    const int img = g * cv.bp + (mt >> 1), y0 = (mt & 1) * 8;
+    const int kh = kb / 5, kw = kb - 5 * kh;
+    tma_load_4d(sa, map_a, bar, 0, 2 - kw, y0 + 2 - kh, img);
+    tma_load_3d(sb, map_b, bar, 0, (kh * 3 + (kw >> 1)) * 64 + (kw & 1) * 32 + n0, g);
+  } else {  // CONV_WGRAD
+    const int b = kb >> 2, blk = kb & 3, x0 = (blk & 1) * 8, y0 = (blk >> 1) * 8, img = g * cv.bp + b;
+#pragma unroll
+    for (int h = 0; h < BM / 64; ++h) {
+      const int pi = mt * (BM / 64) + h, kh = pi / 3, pk = pi - 3 * kh;
+      tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, 0, x0 + 2 * pk - 1, pi < 15 ? y0 + kh - 2 : -64, img);
+    }
+    tma_load_4d(sb, map_b, bar, 0, x0, y0, img);
+  }
+}
+
 template <int BM, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_s,
                         const __grid_constant__ CUtensorMap map_l, int G, int M, int N, int K, int STAGES,
-                        int nst, const Epilogue ep) {
+                        int nst, const Epilogue ep, const ConvSpec conv) {
   using CF = Cfg<BM, BN>;
   constexpr int kStageBytes = CF::kStageBytes, kTmemCols = CF::kTmemCols;
   constexpr int kTileABytes = CF::kTileABytes;
@@ -232,17 +284,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], kStageBytes);
           const uint32_t sa = smem_u32(smem + s * kStageBytes), sb = sa + kTileABytes;
-          if (A_MN) {
+          if (conv.mode == CONV_NONE) {
+            if (A_MN) {
 #pragma unroll
-            for (int h = 0; h < BM / 64; ++h) tma_load_3d(sa + h * 64 * BK * 2, &map_a, &full[s], m0 + 64 * h, kb * BK, g);
-          } else {
-            tma_load_3d(sa, &map_a, &full[s], kb * BK, m0, g);
-          }
-          if (B_MN) {
+              for (int h = 0; h < BM / 64; ++h)
+                tma_load_3d(sa + h * 64 * BK * 2, &map_a, &full[s], m0 + 64 * h, kb * BK, g);
+            } else {
+              tma_load_3d(sa, &map_a, &full[s], kb * BK, m0, g);
+            }
+            if (B_MN) {
 #pragma unroll
-            for (int h = 0; h < BN / 64; ++h) tma_load_3d(sb + h * 64 * BK * 2, &map_b, &full[s], n0 + 64 * h, kb * BK, g);
+              for (int h = 0; h < BN / 64; ++h)
+                tma_load_3d(sb + h * 64 * BK * 2, &map_b, &full[s], n0 + 64 * h, kb * BK, g);
+            } else {
+              tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
+            }
           } else {
-            tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
+            conv_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
           }
           if (++s == STAGES) {
             s = 0;
@@ -377,6 +435,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kind == FEDHC_EPI_SGD) {
             tma_store_3d(&map_o, smem_u32(lb), c0, c1, g);
             if (ep.shadow) tma_store_3d(&map_s, smem_u32(sb), c0, c1, g);
+          } else if (conv.mode == CONV_FWD || conv.mode == CONV_DGRAD) {
+            // output rows = pixel slots (y0 + row / 16, row % 16) of an NHWC 14x14 map; TMA clips x, y >= 14
+            const int mt = m0 / BM;
+            tma_store_4d(&map_o, smem_u32(sb), c0, 0, (mt & 1) * 8 + 2 * q, g * conv.bp + (mt >> 1));
           } else {
             tma_store_3d(&map_o, smem_u32(sb), c0, c1, g);
           }
@@ -453,6 +515,45 @@ static int make_epi_map(CUtensorMap* map, const void* base, bool f32, const Gemm
                      f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
+// NHWC activation maps [images][14][W][C] (bf16) -> 4-D map {C, W, 14, images}
+static int make_act_map(CUtensorMap* map, const void* base, int C, int64_t n_img, int box_c, int box_x, int box_y,
+                        CUtensorMapSwizzle sw, int W = 14) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) & 15) return fail(FEDHC_ERR_VALUE, "gemm: tensors must be 16-byte aligned");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, 14, (cuuint64_t)n_img};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * W * 2, (cuuint64_t)C * W * 14 * 2};
+  cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)box_x, (cuuint32_t)box_y, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FEDHC_ERR_CUDA, "gemm: cuTensorMapEncodeTiled (4-D) failed (" + std::to_string(r) + ")");
+  return FEDHC_OK;
+}
+
+// operand / output maps of the implicit-GEMM convolution modes (replace the generic ones)
+static int plan_conv_maps(const fedhc_gemm_args& a, GemmPlan* p) {
+  const int64_t n_img = (int64_t)a.G * p->conv.bp;
+  const CUtensorMapSwizzle S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  int rc;
+  switch (p->conv.mode) {
+    case CONV_FWD:  // A = p1x [img][14][14][64]; B = generic MN-major weights; D = a2 [img][14][14][64]
+      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 8, S128, 15))) return rc;
+      return make_act_map(&p->mo, a.D, 64, n_img, 32, 16, 2, S64);
+    case CONV_DGRAD:  // A = da2; B = weight rows [1024][64] (box of 32 rows); D = dp1 [img][14][14][32]
+      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 8, S128))) return rc;
+      if ((rc = make_map_ex(&p->mb, a.B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.G, 1024, 64, 64, a.b_gstride, 64, 32,
+                            S128)))
+        return rc;
+      return make_act_map(&p->mo, a.D, 32, n_img, 32, 16, 2, S64);
+    case CONV_WGRAD:  // A = p1x, B = da2: 8x8 pixel blocks; D = SGD on the weights (generic epilogue maps)
+      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 8, 8, S128, 15))) return rc;
+      return make_act_map(&p->mb, a.B, 64, n_img, 64, 8, 8, S128);
+  }
+  return FEDHC_OK;
+}
+
 template <int BM, int BN, bool A_MN, bool B_MN>
 static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   int rc = A_MN ? make_map(&p->ma, a.A, a.G, a.K, a.M, 64, a.a_gstride)
@@ -470,6 +571,7 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
     if ((rc = make_epi_map(&p->mo, p->ep.D, kind == FEDHC_EPI_F32, *p, R))) return rc;
     if (kind == FEDHC_EPI_RELU_MASK_BF16 && (rc = make_epi_map(&p->ml, p->ep.mask, false, *p, R))) return rc;
   }
+  if (p->conv.mode != CONV_NONE && (rc = plan_conv_maps(a, p))) return rc;
   int dev = 0, sms = 0, max_smem = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -516,8 +618,19 @@ static int plan_n(const fedhc_gemm_args& a, GemmPlan* p) {
   return plan_major<BM, 32>(a, p);
 }
 
-int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p) {
+int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p, const ConvSpec* conv) {
   if (a.G < 1 || a.M < 1 || a.N < 1 || a.K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
+  p->conv = conv ? *conv : ConvSpec{CONV_NONE, 0};
+  if (p->conv.mode != CONV_NONE) {
+    const int bp = p->conv.bp;
+    const int m = p->conv.mode;
+    const bool ok = bp > 0 && a.M % 128 == 0 &&
+                    ((m == CONV_FWD && a.M == 256 * bp && a.N == 64 && a.K == 960 && !a.a_mn && a.b_mn) ||
+                     (m == CONV_DGRAD && a.M == 256 * bp && a.N == 32 && a.K == 1600 && !a.a_mn && !a.b_mn) ||
+                     (m == CONV_WGRAD && a.M == 1024 && a.N == 64 && a.K == 256 * bp && a.a_mn && a.b_mn &&
+                      a.epilogue == FEDHC_EPI_SGD));
+    if (!ok) return fail(FEDHC_ERR_VALUE, "gemm: inconsistent implicit-GEMM convolution shape");
+  }
   if (a.M % 64 || a.N % 32 || a.K % BK)
     return fail(FEDHC_ERR_UNSUPPORTED, "gemm: need M % 64 == 0, N % 32 == 0, K % 64 == 0");
   if ((reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B)) & 15)
@@ -534,6 +647,7 @@ int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p) {
   if (ep.ldd % 8 || ep.d_gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: ldd and d_gstride must be multiples of 8");
   const int bn = a.N % 256 == 0 ? 256 : a.N % 128 == 0 ? 128 : a.N % 64 == 0 ? 64 : 32;
   if (ep.rowsum && bn != a.N) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: rowsum needs N to fit one tile (N <= 256)");
+  if (p->conv.mode != CONV_NONE && ep.rowsum) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: conv epilogue without rowsum");
   p->ep = ep;
   p->G = a.G;
   p->M = a.M;
@@ -546,7 +660,8 @@ int gemm_run(const GemmPlan& p, cudaStream_t st) {
   void* args[] = {const_cast<CUtensorMap*>(&p.ma), const_cast<CUtensorMap*>(&p.mb), const_cast<CUtensorMap*>(&p.mo),
                   const_cast<CUtensorMap*>(&p.ms), const_cast<CUtensorMap*>(&p.ml), const_cast<int*>(&p.G),
                   const_cast<int*>(&p.M), const_cast<int*>(&p.N), const_cast<int*>(&p.K),
-                  const_cast<int*>(&p.stages), const_cast<int*>(&p.nst), const_cast<Epilogue*>(&p.ep)};
+                  const_cast<int*>(&p.stages), const_cast<int*>(&p.nst), const_cast<Epilogue*>(&p.ep),
+                  const_cast<ConvSpec*>(&p.conv)};
   FEDHC_CUDA_TRY(cudaLaunchKernel(p.kern, dim3(p.grid), dim3(kThreads), args, p.smem, st));
   return FEDHC_OK;
 }

@@ -26,19 +26,30 @@ struct Epilogue {
   float* rowsum;        // RELU_MASK_BF16 (optional, single N tile): rowsum[g*M + m] = sum_n D
 };
 
+// Implicit-GEMM convolution modes (CNN conv2: 5x5 'same' on 14x14 NHWC maps; see gemm_tc.cu conv_loads).
+enum { CONV_NONE = 0, CONV_FWD = 1, CONV_DGRAD = 2, CONV_WGRAD = 3 };
+struct ConvSpec {
+  int mode;   // CONV_*
+  int bp;     // images per group
+};
+
 struct GemmPlan {
   CUtensorMap ma, mb;   // operands
   CUtensorMap mo;       // epilogue store target: D, or the SGD fp32 master
   CUtensorMap ms;       // SGD bf16 shadow (optional)
   CUtensorMap ml;       // epilogue load source: SGD master or ReLU-backward mask
   Epilogue ep;
+  ConvSpec conv;
   int G, M, N, K;
   const void* kern;
   int grid, smem, stages, nst;
 };
 
 // Validate a problem and build its plan (no launch).  Returns a FEDHC_* status.
-int gemm_plan(const fedhc_gemm_args& a, GemmPlan* plan);
+// conv != nullptr: implicit-GEMM convolution (a.A / a.B / a.D are the activation / weight / output
+// tensors of the mode, M / N / K its virtual GEMM shape; conv2 fwd: M = 256 * bp, N = 64, K = 960;
+// dgrad: M = 256 * bp, N = 32, K = 1600; wgrad: M = 1024, N = 64, K = 256 * bp, SGD epilogue).
+int gemm_plan(const fedhc_gemm_args& a, GemmPlan* plan, const ConvSpec* conv = nullptr);
 // Launch a plan on a stream.
 int gemm_run(const GemmPlan& p, cudaStream_t st);
 

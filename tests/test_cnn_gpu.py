@@ -109,3 +109,77 @@ def test_cnn_eval_matches_oracle_predictions(setup):
     margin = np.sort(logits, axis=1)
     close = int(((margin[:, -1] - margin[:, -2]) < 0.05 * np.abs(margin[:, -1]).max()).sum())
     assert abs(got - want) <= max(2, close), (got, want, close)
+
+
+# ---- conv2 implicit GEMM (TMA 4-D boxes, OOB zero padding) vs torch fp32 on bf16 operands ----------
+def _pairs_layout(w):
+    """torch conv2 weight [64 co, 32 ci, 5, 5] -> engine [16 pairs][2][32 ci][64 co] (kw = 5, pair 15 zero)."""
+    import torch
+    t = torch.zeros(5, 6, 32, 64)
+    t[:, :5] = w.permute(2, 3, 1, 0)
+    out = torch.zeros(16, 2, 32, 64)
+    out[:15] = t.reshape(15, 2, 32, 64)
+    return out.reshape(1024, 64)
+
+
+def _p1x(p1):
+    """p1 NHWC [n,14,14,32] -> channel pairs [n,14,15,64]: column xx = p1(y,xx-1) | p1(y,xx), zero outside."""
+    import torch
+    n = p1.shape[0]
+    pad = torch.zeros(n, 14, 16, 32)
+    pad[:, :, 1:15] = p1
+    return torch.cat([pad[:, :, 0:15], pad[:, :, 1:16]], dim=3)
+
+
+@pytest.mark.parametrize("G,bp", [(1, 1), (3, 2)])
+def test_conv2_implicit_gemm_modes(G, bp):
+    import torch
+    import torch.nn.functional as Fn
+    from paper_2305_15668_b200 import _abi
+    torch.manual_seed(G * 10 + bp)
+    dev = "cuda"
+    n = G * bp
+    bf = lambda t: t.to(torch.bfloat16).float()
+    p1 = bf(torch.randn(n, 14, 14, 32))
+    w = [bf(torch.randn(64, 32, 5, 5) * 0.05) for _ in range(G)]
+    bias = torch.randn(G, 64) * 0.1
+    da2 = bf(torch.randn(n, 14, 14, 64))
+    wl = torch.stack([_pairs_layout(x) for x in w]).to(torch.bfloat16).to(dev)
+    p1x = _p1x(p1).to(torch.bfloat16).to(dev).contiguous()
+    sp = torch.cuda.current_stream().cuda_stream
+    # forward
+    out = torch.zeros(n, 14, 14, 64, dtype=torch.bfloat16, device=dev)
+    b_dev = bias.to(dev).contiguous()
+    _abi.check(_abi.lib.fedhc_cnn_conv2(1, G, bp, p1x.data_ptr(), None, wl.data_ptr(), b_dev.data_ptr(),
+                                        out.data_ptr(), 0.0, sp))
+    ref = torch.cat([Fn.conv2d(p1[g * bp:(g + 1) * bp].permute(0, 3, 1, 2), w[g], bias[g], padding=2)
+                     for g in range(G)]).relu().permute(0, 2, 3, 1)
+    torch.cuda.synchronize()
+    err = (out.float().cpu() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+    # data gradient: dL/dp1 = conv_transpose(dL/da2)
+    dp1 = torch.zeros(n, 14, 14, 32, dtype=torch.bfloat16, device=dev)
+    da2_dev = da2.to(torch.bfloat16).to(dev).contiguous()
+    _abi.check(_abi.lib.fedhc_cnn_conv2(2, G, bp, da2_dev.data_ptr(), None, wl.data_ptr(), None, dp1.data_ptr(),
+                                        0.0, sp))
+    ref = torch.cat([Fn.conv_transpose2d(da2[g * bp:(g + 1) * bp].permute(0, 3, 1, 2), w[g], padding=2)
+                     for g in range(G)]).permute(0, 2, 3, 1)
+    torch.cuda.synchronize()
+    err = (dp1.float().cpu() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+    # weight gradient + SGD on an fp32 master (zero start): master = -lr * grad
+    master = torch.zeros(G, 1024, 64, device=dev)
+    _abi.check(_abi.lib.fedhc_cnn_conv2(3, G, bp, p1x.data_ptr(), da2_dev.data_ptr(), None, None, master.data_ptr(),
+                                        1.0, sp))
+    torch.cuda.synchronize()
+    for g in range(G):
+        x = p1[g * bp:(g + 1) * bp].permute(0, 3, 1, 2)
+        gy = da2[g * bp:(g + 1) * bp].permute(0, 3, 1, 2)
+        gw = torch.nn.grad.conv2d_weight(x, (64, 32, 5, 5), gy, padding=2)
+        want = -_pairs_layout(gw)
+        got = master[g].cpu()
+        pad = _pairs_layout(torch.ones(64, 32, 5, 5)) == 0          # kw = 5 rows, pair 15
+        real = ~pad
+        err = (got[real] - want[real]).abs().max().item() / want.abs().max().item()
+        assert err < 1e-3, (g, err)
+        assert not got.reshape(16, 2, 32, 64)[15].any()           # padding pair: fully out-of-bounds boxes
