@@ -341,7 +341,8 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- roofline of the dominant kernel (train) ----------------
     from benchlib import roofline_entry
     bytes_per_launch = PER_GPU * steps_per_client * BATCH * (4 * F + 8) + PER_GPU * P * 12
-    roof = roofline_entry(bytes_per_launch, train_ms, ROOT)
+    roof = roofline_entry(bytes_per_launch, train_ms, ROOT,
+                          kernel="train_pipe_kernel" if C <= 16 else "train_fused_kernel")
 
     result = {
         "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
@@ -726,6 +727,10 @@ def run_cnn(args, rank, world, local_rank):
     except (OSError, KeyError, ValueError):
         peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
     tf = flops / (train_ms * 1e-3) / 1e12
+    from benchlib import hbm_peak
+    hbm_peak_v, hbm_src = hbm_peak(ROOT)
+    p_canon = fed.layout.canonical_count
+    hbm_alg = float(per_gpu * steps_per_client * (8 * p_canon + bs * (784 * 4 + 4)))
     n_launch = fed.engine.launches_per_round(steps_per_client)
     res = {
         "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
@@ -746,11 +751,18 @@ def run_cnn(args, rank, world, local_rank):
         "e2e": {"value": total_steps / e2e_s, "unit": "client-steps/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": 8, "rounds_per_sec": args.steps / e2e_s,
                 "api": "CnnFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"},
-        "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                     "traffic": None, "kernel": "train phase (grouped_gemm_kernel launches + data-movement "
-                                                "kernels, one CUDA graph)",
-                     "algorithmic_flop_per_launch": flops, "flop_per_sample": cnn_flop_per_sample(nc),
-                     "peak_source": src},
+        # one SGD step streams every client's fp32 master weights in and out (8 B / param, the
+        # algorithmic minimum of per-client SGD; AI = 123 flop/B < the 260 flop/B ridge): HBM-bound
+        "roofline": {"bound": "hbm", "achieved": hbm_alg / (train_ms * 1e-3) / 1e9, "peak": hbm_peak_v,
+                     "unit": "GB/s", "frac": hbm_alg / (train_ms * 1e-3) / 1e9 / hbm_peak_v, "traffic": None,
+                     "kernel": "train phase (one CUDA graph: grouped_gemm_kernel launches incl. implicit-GEMM "
+                               "conv2 + conv1/pool/CE kernels)",
+                     "algorithmic_bytes_per_launch": hbm_alg,
+                     "bytes_per_client_step": "8 x params (fp32 master read + write) + B x (784 x 4 + 4) input",
+                     "peak_source": hbm_src},
+        "roofline_tensor": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                            "algorithmic_flop_per_launch": flops, "flop_per_sample": cnn_flop_per_sample(nc),
+                            "peak_source": src},
         "clocks": clocks.summary(),
         "gpu_launches": args.steps * (n_launch + 2 + (1 if world > 1 else 0)),
     }

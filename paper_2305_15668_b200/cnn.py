@@ -8,8 +8,10 @@ LEAF FEMNIST CNN.  This module is its host side:
   [out,in], fc1 input flattened (c, h, w));
 * ``init_cnn_params`` -- torch-default-style uniform init from a PCG64 seed;
 * ``CnnFederation`` -- DeviceFederation whose ``train`` runs the CNN engine
-  (``fedhc_cnn_local_train``: every layer of every client as grouped tcgen05
-  GEMMs, one CUDA graph per round) and whose ``correct`` runs
+  (``fedhc_cnn_local_train``: conv2 / fc1 / fc2 forward, data and weight
+  gradients of every client as grouped tcgen05 GEMMs -- conv2 as implicit
+  GEMMs over 4-D TMA boxes -- conv1 (1 input channel, K = 25) fused with
+  pooling on the CUDA cores, one CUDA graph per round) and whose ``correct`` runs
   ``fedhc_cnn_eval``.  Plans, permutations, descriptors and FedAvg are the
   linear path's (the round structure of engine.run_experiment does not depend
   on the model).
@@ -142,11 +144,11 @@ class CnnEngine:
         self.correct_into(params, x, y, cnt)
         return int(cnt.item())
 
-    KERNELS_PER_STEP = 19     # 11 grouped GEMMs + 8 gather/pool/im2col/CE/col2im/bias kernels (csrc/cnn.cu)
+    KERNELS_PER_STEP = 15     # 9 grouped GEMMs (3 implicit-GEMM conv2) + conv1 fwd/bwd, pool2 fwd/bwd, CE, bias SGD
 
     def launches_per_round(self, steps: int) -> int:
-        """Kernels one fedhc_cnn_local_train launches (broadcast, shadow, steps, delta)."""
-        return self.KERNELS_PER_STEP * steps + 3
+        """Kernels one fedhc_cnn_local_train launches (broadcast, steps, delta)."""
+        return self.KERNELS_PER_STEP * steps + 2
 
 
 class CnnFederation(DeviceFederation):

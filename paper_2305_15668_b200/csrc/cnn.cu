@@ -17,9 +17,9 @@
 //
 // Per client, per step (Bp = batch rounded up to 64; rows past the batch are
 // zero and carry zero gradient, so ragged and finished clients are exact):
-//   gather+im2col1  x[perm] -> cols1 [Bp*784][64]   (25 taps, zero-padded)
-//   conv1  GEMM     cols1 . Wc1^T  + b, ReLU -> a1 [Bp*784][32]        (N=32)
-//   pool1           a1 -> p1x [Bp][14][15][64]  channel pairs p1(y,x-1) | p1(y,x)
+//   conv1 fused     x[perm] (TMA-free row gather) -> 5x5 conv (1 -> 32 ch, CUDA cores: K = 25 is far too
+//                   thin for the tensor pipe) + bias + ReLU + maxpool2 -> p1x [Bp][14][15][64]
+//                   (channel pairs p1(y,x-1) | p1(y,x)), pool mask (argmax | on) [Bp][196][32], xin bf16
 //   conv2  implicit GEMM (TMA 4-D boxes, OOB = zero padding): 15 tap pairs x 64
 //                   p1x . Wc2 + b, ReLU -> a2 [Bp][14][14][64]
 //   pool2           a2 -> p2 [Bp][3200]                (7*7*64 + 64 zero)
@@ -33,8 +33,8 @@
 //   pool2 bwd       dp2, a2 -> da2 [Bp*196][64] (+ db2 partials)
 //   conv2 dgrad     implicit GEMM over 25 taps: da2 (shifted) . Wc2[tap] -> dp1 [Bp][14][14][32]
 //   conv2 wgrad+SGD implicit GEMM over 8x8 pixel blocks: Wc2 -= lr p1x(shifted)^T . da2
-//   pool1 bwd       dp1, a1 -> da1 [32][Bp*784] (channel-major) (+ db1 partials)
-//   conv1 wgrad+SGD Wc1 -= lr cols1^T . da1                     (M=64, N=32)
+//   conv1 bwd fused pool1 backward (mask) + conv1 weight gradient per image -> [Bp][25*32] partials
+//                   (+ bias partials); the per-client fixed-order sum and SGD run in bias_sgd
 //   bias SGD, Wc1 shadow transpose
 // The step sequence of a round is captured once into a CUDA graph and replayed.
 #include <cuda_bf16.h>
@@ -52,7 +52,7 @@ namespace cnn {
 constexpr int HW0 = 784, W0 = 28;              // input 28x28x1
 constexpr int C1 = 32, W1d = 14, HW1 = 196;    // after conv1 + pool
 constexpr int C2 = 64, W2d = 7, HW2 = 49;      // after conv2 + pool
-constexpr int T1 = 64;                         // conv1 im2col width (25 taps)
+constexpr int T1 = 64;                         // conv1 weight rows (25 taps + zero padding)
 constexpr int WR2 = 16 * 64;                   // conv2 weight rows: 16 tap pairs x (2 taps x 32 ci)
 constexpr int F1 = 3200;                       // fc1 input: 7*7*64 = 3136 + 64 zero
 constexpr int HID = 2048, NC = 64;
@@ -74,13 +74,34 @@ static_assert(OFF_BC1 % 64 == 0 && OFF_WC2 % 64 == 0 && OFF_W1 % 64 == 0 && OFF_
 
 __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
 
-// ---- gather + im2col of conv1 ------------------------------------------------
-// grid (Bp, G), 256 threads.  perm == nullptr -> rows taken in order (eval).
-__global__ void __launch_bounds__(256) gather_im2col1_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
-                                                             __nv_bfloat16* __restrict__ cols1,
-                                                             int32_t* __restrict__ labels,
-                                                             int32_t* __restrict__ valid) {
-  __shared__ float img[HW0];
+// first max of a 2x2 pooling window (row-major order), as torch / the oracle pick it
+__device__ __forceinline__ int first_max4(float v0, float v1, float v2, float v3) {
+  int k = 0;
+  float m = v0;
+  if (v1 > m) { m = v1; k = 1; }
+  if (v2 > m) { m = v2; k = 2; }
+  if (v3 > m) { k = 3; }
+  return k;
+}
+
+
+
+// ---- conv1 forward, fused: row gather + 5x5 conv (1 -> 32) + bias + ReLU + maxpool2 -------------
+// grid (Bp, G), 256 threads.  perm == nullptr -> rows taken in order (eval).  Operands are rounded
+// to bf16 exactly where the tensor-core engine rounds them (input, weights, activation); products
+// are exact in fp32 and summed in fp32.
+// Outputs: xin [G*Bp][784] bf16 (the input, for the weight gradient), p1x (channel-pair layout of
+// conv2's implicit GEMM, see pool1 below), pmask [G*Bp][196][32] = argmax(0..3) | (max > 0) << 2.
+constexpr int W1X = 15;
+// thread = output channel (lane), warp = a strided set of pooled pixels: the 25 weights live in
+// registers and every image value is a shared-memory broadcast (6x6 patch per pooled pixel).
+__global__ void __launch_bounds__(256) conv1_fwd_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
+                                                        const float* __restrict__ master,
+                                                        __nv_bfloat16* __restrict__ xin,
+                                                        int32_t* __restrict__ labels, int32_t* __restrict__ valid,
+                                                        __nv_bfloat16* __restrict__ p1x,
+                                                        uint8_t* __restrict__ pmask) {
+  __shared__ __align__(16) float img[32][32];  // 28x28 + 2-pixel zero border
   const int g = blockIdx.y, b = blockIdx.x;
   const fedhc_client c = cl[g];
   int rows = 0;
@@ -97,28 +118,58 @@ __global__ void __launch_bounds__(256) gather_im2col1_kernel(const fedhc_client*
   const bool ok = b < rows;
   const int row = ok ? (c.perm ? c.perm[poff + b] : b) : 0;
   const float* src = c.x + (int64_t)row * HW0;
-  for (int i = threadIdx.x; i < HW0; i += 256) img[i] = ok ? __ldg(src + i) : 0.f;
+  const int64_t im = (int64_t)g * Bp + b;
+  for (int i = threadIdx.x; i < 32 * 32; i += 256) (&img[0][0])[i] = 0.f;
   if (threadIdx.x == 0) {
-    labels[(int64_t)g * Bp + b] = ok ? c.y[row] : 0;
+    labels[im] = ok ? c.y[row] : 0;
     if (b == 0) valid[g] = rows;
   }
+  const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* mw = master + (int64_t)g * PPAD;
+  float w[25];
+#pragma unroll
+  for (int t = 0; t < 25; ++t) w[t] = bf(__float2bfloat16_rn(mw[OFF_WC1 + t * C1 + ch]));
+  const float bias = mw[OFF_BC1 + ch];
   __syncthreads();
-  __nv_bfloat16* dst = cols1 + ((int64_t)g * Bp + b) * HW0 * T1;
-  for (int p = threadIdx.x; p < HW0; p += 256) {
-    const int h = p / W0, w = p - h * W0;
-    __align__(16) __nv_bfloat16 v[T1];
+  for (int i = threadIdx.x; i < HW0; i += 256) {
+    const __nv_bfloat16 v = __float2bfloat16_rn(ok ? __ldg(src + i) : 0.f);
+    xin[im * HW0 + i] = v;
+    img[2 + i / W0][2 + i % W0] = bf(v);
+  }
+  __syncthreads();
+  __nv_bfloat16* prow0 = p1x + (int64_t)im * W1d * W1X * 64;
+  for (int p = warp; p < HW1; p += 8) {
+    const int oh = p / W1d, ow = p - oh * W1d;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // output pixel (2oh + i, 2ow + j), tap (kh, kw) reads img[2oh + i + kh][2ow + j + kw] (border-padded)
 #pragma unroll
-    for (int t = 0; t < T1; ++t) {
-      float x = 0.f;
-      if (t < 25) {
-        const int ih = h + t / 5 - 2, iw = w + t % 5 - 2;
-        if (ih >= 0 && ih < W0 && iw >= 0 && iw < W0) x = img[ih * W0 + iw];
+    for (int dy = 0; dy < 6; ++dy) {
+      const float2* rp = reinterpret_cast<const float2*>(&img[2 * oh + dy][2 * ow]);
+      const float2 r0 = rp[0], r1 = rp[1], r2 = rp[2];
+      const float v[6] = {r0.x, r0.y, r1.x, r1.y, r2.x, r2.y};
+#pragma unroll
+      for (int dx = 0; dx < 6; ++dx) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int kh = dy - i, kw = dx - j;
+            if (kh >= 0 && kh <= 4 && kw >= 0 && kw <= 4) acc[i * 2 + j] += v[dx] * w[kh * 5 + kw];
+          }
+        }
       }
-      v[t] = __float2bfloat16_rn(x);
     }
-    uint4* o = reinterpret_cast<uint4*>(dst + (int64_t)p * T1);
+    float q[4];
 #pragma unroll
-    for (int i = 0; i < T1 / 8; ++i) o[i] = reinterpret_cast<const uint4*>(v)[i];
+    for (int k = 0; k < 4; ++k) q[k] = bf(__float2bfloat16_rn(fmaxf(acc[k] + bias, 0.f)));
+    const int k = first_max4(q[0], q[1], q[2], q[3]);
+    pmask[(im * HW1 + p) * C1 + ch] = (uint8_t)(k | (q[k] > 0.f ? 4 : 0));
+    const __nv_bfloat16 pooled = __float2bfloat16_rn(q[k]);
+    __nv_bfloat16* prow = prow0 + (int64_t)oh * W1X * 64;
+    prow[(ow + 1) * 64 + ch] = pooled;      // column x + 1, low half
+    prow[ow * 64 + 32 + ch] = pooled;       // column x, high half
+    if (ow == 0) prow[ch] = __float2bfloat16_rn(0.f);
+    if (ow == W1d - 1) prow[W1d * 64 + 32 + ch] = __float2bfloat16_rn(0.f);
   }
 }
 
@@ -151,37 +202,10 @@ __global__ void __launch_bounds__(256) pool_fwd_kernel(const __nv_bfloat16* __re
   }
 }
 
-// ---- pool1 into the channel-pair layout of the conv2 implicit GEMM -----------------
-// a1 [n_img][28][28][32] -> p1x [n_img][14][15][64]: column xx = x + 1 holds p1(y, x) | p1(y, x + 1)
-// (zero outside the 14x14 map), so one 128-byte TMA row = the two horizontally adjacent taps of a tap
-// pair, including the pair straddling the left edge (x = -1).
-constexpr int W1X = 15;
-__global__ void __launch_bounds__(256) pool1_pairs_kernel(const __nv_bfloat16* __restrict__ a1,
-                                                          __nv_bfloat16* __restrict__ p1x, int64_t n_img) {
-  const int64_t total = n_img * HW1 * 4;  // (image, pooled pixel, 8-channel group)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i & 3);
-    const int64_t px = i >> 2;
-    const int64_t n = px / HW1;
-    const int p = (int)(px - n * HW1), oh = p / W1d, ow = p - oh * W1d;
-    const __nv_bfloat16* base = a1 + ((n * W0 + 2 * oh) * W0 + 2 * ow) * C1 + cg * 8;
-    uint4 q0 = *reinterpret_cast<const uint4*>(base);
-    const uint4 q1 = *reinterpret_cast<const uint4*>(base + C1);
-    const uint4 q2 = *reinterpret_cast<const uint4*>(base + (int64_t)W0 * C1);
-    const uint4 q3 = *reinterpret_cast<const uint4*>(base + (int64_t)W0 * C1 + C1);
-    __nv_bfloat162* a = reinterpret_cast<__nv_bfloat162*>(&q0);
-    const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&q2);
-    const __nv_bfloat162* b3 = reinterpret_cast<const __nv_bfloat162*>(&q3);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = __hmax2(__hmax2(a[k], b1[k]), __hmax2(b2[k], b3[k]));
-    __nv_bfloat16* row = p1x + (n * W1d + oh) * W1X * 64;
-    *reinterpret_cast<uint4*>(row + (ow + 1) * 64 + cg * 8) = q0;   // column x + 1, low half
-    *reinterpret_cast<uint4*>(row + ow * 64 + 32 + cg * 8) = q0;    // column x, high half
-    if (ow == 0) *reinterpret_cast<uint4*>(row + cg * 8) = make_uint4(0, 0, 0, 0);
-    if (ow == W1d - 1) *reinterpret_cast<uint4*>(row + W1d * 64 + 32 + cg * 8) = make_uint4(0, 0, 0, 0);
-  }
-}
+// ---- pool1 layout for conv2's implicit GEMM -------------------------------------------------------
+// p1x [n_img][14][15][64]: column xx = x + 1 holds p1(y, x) | p1(y, x + 1) (zero outside the 14x14
+// map), so one 128-byte TMA row = the two horizontally adjacent taps of a tap pair, including the pair
+// straddling the left edge (x = -1).  Written by conv1_fwd_kernel.
 
 // ---- softmax cross-entropy + gradient ------------------------------------------
 // one CTA per client, one thread per batch row (Bp <= 1024)
@@ -257,16 +281,6 @@ __global__ void argmax_kernel(const float* __restrict__ logits, const float* __r
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(correct, (unsigned long long)__popc(m));
 }
 
-// ---- maxpool2 backward + ReLU mask (first max of the 2x2 window, row-major) -------
-__device__ __forceinline__ int first_max4(float v0, float v1, float v2, float v3) {
-  int k = 0;
-  float m = v0;
-  if (v1 > m) { m = v1; k = 1; }
-  if (v2 > m) { m = v2; k = 2; }
-  if (v3 > m) { k = 3; }
-  return k;
-}
-
 // grid (Bp, G): dp2 [G][Bp][3200], a2 [G][Bp][196][64] -> da2 (same as a2), part [G][Bp][64]
 __global__ void __launch_bounds__(256) pool2_bwd_kernel(const __nv_bfloat16* __restrict__ dp2,
                                                         const __nv_bfloat16* __restrict__ a2,
@@ -301,63 +315,64 @@ __global__ void __launch_bounds__(256) pool2_bwd_kernel(const __nv_bfloat16* __r
                                    red[3][threadIdx.x];
 }
 
-constexpr int kP1bSmem = C1 * HW0 * 2;
-
-// grid (Bp, G): maxpool1 backward + ReLU mask of dp1 -> da1 channel-major
-// dp1 [G][Bp][196][32], a1 [G][Bp][784][32] -> da1 [G][32][Bp*784], part [G][Bp][32]
-// thread item = (pooled pixel p, group of 8 channels)
-__global__ void __launch_bounds__(256) pool1_bwd_kernel(const __nv_bfloat16* __restrict__ dp1,
-                                                        const __nv_bfloat16* __restrict__ a1,
-                                                        __nv_bfloat16* __restrict__ da1, float* __restrict__ part,
-                                                        int Bp) {
-  extern __shared__ __align__(16) unsigned char p1b_smem[];
-  auto tile = reinterpret_cast<__nv_bfloat16(*)[HW0]>(p1b_smem);  // [C1][HW0], 50 KB (dynamic)
-  __shared__ float red[256][9];
-  const int g = blockIdx.y, b = blockIdx.x;
-  const int64_t img = (int64_t)g * Bp + b;
-  const __nv_bfloat16* d = dp1 + img * HW1 * C1;
-  const __nv_bfloat16* a = a1 + img * HW0 * C1;
-  const int cg = threadIdx.x & 3;            // channels [8 cg, 8 cg + 8) (256 % 4 == 0: fixed per thread)
-  float acc[8];
+// grid (Bp, G): maxpool1 backward (pool mask) + conv1 weight gradient of one image.
+// dp1 [G*Bp][196][32] bf16, pmask, xin [G*Bp][784] bf16 -> dw [G*Bp][25*32] fp32 partials,
+// part [G*Bp][32] (bias).  dL/da1 is nonzero only at each window's first max (if > 0).  Thread =
+// channel, warp = strided pooled pixels: the gradient is routed to the 4 window positions with a
+// select (3 of 4 zero) so every image value is a broadcast; 25 accumulators per thread, then a
+// fixed-order reduction over the 8 warps.
+__global__ void __launch_bounds__(256) conv1_bwd_kernel(const __nv_bfloat16* __restrict__ dp1,
+                                                        const uint8_t* __restrict__ pmask,
+                                                        const __nv_bfloat16* __restrict__ xin,
+                                                        float* __restrict__ dw, float* __restrict__ part, int Bp) {
+  __shared__ __align__(16) float img[32][32];
+  __shared__ float red[8][26][32];
+  const int64_t im = (int64_t)blockIdx.y * Bp + blockIdx.x;
+  for (int i = threadIdx.x; i < 32 * 32; i += 256) (&img[0][0])[i] = 0.f;
+  __syncthreads();
+  for (int i = threadIdx.x; i < HW0; i += 256) img[2 + i / W0][2 + i % W0] = bf(xin[im * HW0 + i]);
+  __syncthreads();
+  const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float acc[25], sb = 0.f;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  for (int item = threadIdx.x; item < HW1 * 4; item += 256) {
-    const int p = item >> 2, ph = p / W1d, pw = p - ph * W1d;
-    const uint4 dv = *reinterpret_cast<const uint4*>(d + p * C1 + cg * 8);
-    const int q00 = (2 * ph) * W0 + 2 * pw;
-    const int pos[4] = {q00, q00 + 1, q00 + W0, q00 + W0 + 1};
-    uint4 av[4];
+  for (int t = 0; t < 25; ++t) acc[t] = 0.f;
+  for (int p = warp; p < HW1; p += 8) {
+    const int oh = p / W1d, ow = p - oh * W1d;
+    const uint8_t m = pmask[(im * HW1 + p) * C1 + ch];
+    const float gv = (m & 4) ? bf(dp1[(im * HW1 + p) * C1 + ch]) : 0.f;
+    sb += gv;
+    float gk[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) av[k] = *reinterpret_cast<const uint4*>(a + pos[k] * C1 + cg * 8);
+    for (int k = 0; k < 4; ++k) gk[k] = (m & 3) == k ? gv : 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float v[4];
+    for (int dy = 0; dy < 6; ++dy) {
+      const float2* rp = reinterpret_cast<const float2*>(&img[2 * oh + dy][2 * ow]);
+      const float2 r0 = rp[0], r1 = rp[1], r2 = rp[2];
+      const float v[6] = {r0.x, r0.y, r1.x, r1.y, r2.x, r2.y};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = bf(reinterpret_cast<const __nv_bfloat16*>(&av[k])[e]);
-      const int k = first_max4(v[0], v[1], v[2], v[3]);
-      const bool on = v[k] > 0.f;
-      const __nv_bfloat16 gz = on ? reinterpret_cast<const __nv_bfloat16*>(&dv)[e] : __float2bfloat16_rn(0.f);
-      const int ci = cg * 8 + e;
+      for (int dx = 0; dx < 6; ++dx) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) tile[ci][pos[j]] = j == k ? gz : __float2bfloat16_rn(0.f);
-      acc[e] += bf(gz);
+        for (int i = 0; i < 2; ++i) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int kh = dy - i, kw = dx - j;
+            if (kh >= 0 && kh <= 4 && kw >= 0 && kw <= 4) acc[kh * 5 + kw] += gk[i * 2 + j] * v[dx];
+          }
+        }
+      }
     }
   }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) red[threadIdx.x][e] = acc[e];
+  for (int t = 0; t < 25; ++t) red[warp][t][ch] = acc[t];
+  red[warp][25][ch] = sb;
   __syncthreads();
-  // channel-major store: da1[g][ci][b*784 + p], 16 B per thread
-  const int64_t P1 = (int64_t)Bp * HW0;
-  for (int i = threadIdx.x; i < C1 * (HW0 / 8); i += 256) {
-    const int c = i / (HW0 / 8), q = i - c * (HW0 / 8);
-    *reinterpret_cast<uint4*>(da1 + ((int64_t)g * C1 + c) * P1 + (int64_t)b * HW0 + q * 8) =
-        *reinterpret_cast<const uint4*>(&tile[c][q * 8]);
-  }
-  if (threadIdx.x < C1) {  // fixed-order sum over the 64 threads that own this channel
-    const int c = threadIdx.x, grp = c >> 3, e = c & 7;
+  for (int i = threadIdx.x; i < 26 * C1; i += 256) {
+    const int t = i / C1, c = i - t * C1;
     float s = 0.f;
-    for (int t = grp; t < 256; t += 4) s += red[t][e];
-    part[img * C1 + c] = s;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][t][c];
+    if (t < 25) dw[im * 25 * C1 + i] = s;
+    else part[im * C1 + c] = s;
   }
 }
 
@@ -366,9 +381,16 @@ __global__ void __launch_bounds__(256) bias_sgd_kernel(float* __restrict__ maste
                                                        const float* __restrict__ part1,
                                                        const float* __restrict__ part2,
                                                        const float* __restrict__ db1,
-                                                       const float* __restrict__ db2, int Bp, float lr) {
+                                                       const float* __restrict__ db2,
+                                                       const float* __restrict__ dw1, int Bp, float lr) {
   const int g = blockIdx.x;
   float* m = master + (int64_t)g * PPAD;
+  // conv1 weights: per-image partials summed in image order (deterministic)
+  for (int i = threadIdx.x; i < 25 * C1; i += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < Bp; ++b) s += dw1[((int64_t)g * Bp + b) * 25 * C1 + i];
+    m[OFF_WC1 + i] -= lr * s;
+  }
   for (int i = threadIdx.x; i < C1 + C2 + HID + NC; i += blockDim.x) {
     if (i < C1) {
       float s = 0.f;
@@ -395,12 +417,6 @@ __global__ void __launch_bounds__(256) bias_sgd_kernel(float* __restrict__ maste
     m[OFF_WC2 + o] = 0.f;
     sh2[o] = __float2bfloat16_rn(0.f);
   }
-  // conv1 weights: master [64 taps][32] -> shadow [32][64] (the forward B operand, K-major)
-  __nv_bfloat16* s = shadow + (int64_t)g * PPAD + OFF_WC1;
-  for (int i = threadIdx.x; i < T1 * C1; i += blockDim.x) {
-    const int co = i / T1, t = i - co * T1;
-    s[i] = __float2bfloat16_rn(m[OFF_WC1 + t * C1 + co]);
-  }
 }
 
 // ---- round start / end ---------------------------------------------------------
@@ -412,16 +428,6 @@ __global__ void bcast_kernel(const double* __restrict__ params, float* __restric
     const float v = (float)params[j];
     master[i] = v;
     if (j >= OFF_WC1 + T1 * C1) shadow[i] = __float2bfloat16_rn(v);
-  }
-}
-
-__global__ void wc1_shadow_kernel(const float* __restrict__ master, __nv_bfloat16* __restrict__ shadow) {
-  const int g = blockIdx.x;
-  const float* m = master + (int64_t)g * PPAD + OFF_WC1;
-  __nv_bfloat16* s = shadow + (int64_t)g * PPAD + OFF_WC1;
-  for (int i = threadIdx.x; i < T1 * C1; i += blockDim.x) {
-    const int co = i / T1, t = i - co * T1;
-    s[i] = __float2bfloat16_rn(m[t * C1 + co]);
   }
 }
 
@@ -447,16 +453,17 @@ struct Engine {
   int maxG, Bp, C;
   std::vector<std::unique_ptr<Buf>> bufs;
   float* master;
-  __nv_bfloat16 *shadow, *cols1, *a1, *p1x, *a2, *p2, *hT, *dl, *dhT, *dp2, *da2, *dp1, *da1;
-  float *logits, *db1, *db2, *part1, *part2, *loss;
+  __nv_bfloat16 *shadow, *xin, *p1x, *a2, *p2, *hT, *dl, *dhT, *dp2, *da2, *dp1;
+  uint8_t* pmask;
+  float *logits, *db1, *db2, *part1, *part2, *dw1, *loss;
   int32_t *labels, *valid;
   fedhc_client* desc;
   unsigned long long* correct;
   // training plans for the current K, eval plans (G=1, batch = maxG*Bp)
   int planned_G = -1;
   float planned_lr = 0.f;
-  tc::GemmPlan conv1, conv2, fc1, fc2, fc2_dg, fc2_wg, fc1_dg, fc1_wg, conv2_dg, conv2_wg, conv1_wg;
-  tc::GemmPlan e_conv1, e_conv2, e_fc1, e_fc2;
+  tc::GemmPlan conv2, fc1, fc2, fc2_dg, fc2_wg, fc1_dg, fc1_wg, conv2_dg, conv2_wg;
+  tc::GemmPlan e_conv2, e_fc1, e_fc2;
   cudaGraphExec_t graph = nullptr;
   std::tuple<int, int, float> graph_key{-1, -1, 0.f};
 
@@ -479,8 +486,8 @@ struct Engine {
     int rc = 0;
     rc |= alloc(&master, G * PPAD);
     rc |= alloc(&shadow, G * PPAD);
-    rc |= alloc(&cols1, I * HW0 * T1);
-    rc |= alloc(&a1, I * HW0 * C1);
+    rc |= alloc(&xin, I * HW0);
+    rc |= alloc(&pmask, I * HW1 * C1);
     rc |= alloc(&p1x, I * W1d * W1X * 64);
     rc |= alloc(&a2, I * HW1 * C2);
     rc |= alloc(&p2, I * F1);
@@ -491,7 +498,7 @@ struct Engine {
     rc |= alloc(&dp2, I * F1);
     rc |= alloc(&da2, I * HW1 * C2);
     rc |= alloc(&dp1, I * HW1 * C1);
-    rc |= alloc(&da1, I * HW0 * C1);
+    rc |= alloc(&dw1, I * 25 * C1);
     rc |= alloc(&db1, G * HID);
     rc |= alloc(&db2, G * NC);
     rc |= alloc(&part1, I * C1);
@@ -523,15 +530,9 @@ struct Engine {
   }
 
   // forward plans for G groups of `bp` images each (bp*784 and bp*196 pixel rows)
-  int plan_forward(int G, int bp, tc::GemmPlan* c1, tc::GemmPlan* c2, tc::GemmPlan* f1, tc::GemmPlan* f2) {
-    const int P1 = bp * HW0, P2 = bp * HW1;
+  int plan_forward(int G, int bp, tc::GemmPlan* c2, tc::GemmPlan* f1, tc::GemmPlan* f2) {
     int rc;
-    // conv1: a1[P1][32] = relu(cols1 . Wc1s^T + bc1)
-    auto a = args(G, P1, C1, T1, cols1, false, 0, shadow + OFF_WC1, false, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
-    a.D = a1;
-    a.bias = master + OFF_BC1;
-    a.bias_gstride = PPAD;
-    if ((rc = tc::gemm_plan(a, c1))) return rc;
+    fedhc_gemm_args a;
     // conv2 (implicit GEMM): a2[img][14][14][64] = relu(conv(p1x, Wc2) + bc2), 15 tap pairs, Wc2 MN-major
     const tc::ConvSpec cf{tc::CONV_FWD, bp};
     a = args(G, 256 * bp, C2, 15 * 64, p1x, false, 0, shadow + OFF_WC2, true, PPAD, FEDHC_EPI_BIAS_RELU_BF16);
@@ -552,13 +553,12 @@ struct Engine {
     return tc::gemm_plan(a, f2);
   }
 
-  int plan_eval() { return plan_forward(1, maxG * Bp, &e_conv1, &e_conv2, &e_fc1, &e_fc2); }
+  int plan_eval() { return plan_forward(1, maxG * Bp, &e_conv2, &e_fc1, &e_fc2); }
 
   int plan_train(int G, float lr) {
     if (G == planned_G && lr == planned_lr) return FEDHC_OK;
-    int rc = plan_forward(G, Bp, &conv1, &conv2, &fc1, &fc2);
+    int rc = plan_forward(G, Bp, &conv2, &fc1, &fc2);
     if (rc) return rc;
-    const int P1 = Bp * HW0, P2 = Bp * HW1;
     // fc2 dgrad: dhT[2048][Bp] = (W2^T . dl^T) * (hT > 0), rowsum -> db1
     auto a = args(G, HID, Bp, NC, shadow + OFF_W2, true, PPAD, dl, false, 0, FEDHC_EPI_RELU_MASK_BF16);
     a.D = dhT;
@@ -596,12 +596,6 @@ struct Engine {
     a.d_gstride = PPAD;
     a.lr = lr;
     if ((rc = tc::gemm_plan(a, &conv2_wg, &cw))) return rc;
-    // conv1 wgrad: Wc1[64][32] -= lr cols1^T . da1  (B = da1 channel-major, K-major)
-    a = args(G, T1, C1, P1, cols1, true, 0, da1, false, 0, FEDHC_EPI_SGD);
-    a.master = master + OFF_WC1;
-    a.d_gstride = PPAD;
-    a.lr = lr;
-    if ((rc = tc::gemm_plan(a, &conv1_wg))) return rc;
     planned_G = G;
     planned_lr = lr;
     if (graph) {
@@ -617,13 +611,11 @@ struct Engine {
     return (int)(b < 148 * 16 ? b : 148 * 16);
   }
 
-  int forward(int G, int bp, int step, const tc::GemmPlan& c1, const tc::GemmPlan& c2, const tc::GemmPlan& f1,
-              const tc::GemmPlan& f2, cudaStream_t st) {
+  int forward(int G, int bp, int step, const tc::GemmPlan& c2, const tc::GemmPlan& f1, const tc::GemmPlan& f2,
+              cudaStream_t st) {
     const int64_t n_img = (int64_t)G * bp;
     int rc;
-    gather_im2col1_kernel<<<dim3(bp, G), 256, 0, st>>>(desc, step, bp, cols1, labels, valid);
-    if ((rc = tc::gemm_run(c1, st))) return rc;
-    pool1_pairs_kernel<<<grid_for(n_img * HW1 * 4), 256, 0, st>>>(a1, p1x, n_img);
+    conv1_fwd_kernel<<<dim3(bp, G), 256, 0, st>>>(desc, step, bp, master, xin, labels, valid, p1x, pmask);
     if ((rc = tc::gemm_run(c2, st))) return rc;
     pool_fwd_kernel<<<grid_for(n_img * HW2 * C2 / 8), 256, 0, st>>>(a2, p2, n_img, W1d, C2, F1);
     if ((rc = tc::gemm_run(f1, st))) return rc;
@@ -631,7 +623,7 @@ struct Engine {
   }
 
   int train_step(int G, int step, float lr, cudaStream_t st) {
-    int rc = forward(G, Bp, step, conv1, conv2, fc1, fc2, st);
+    int rc = forward(G, Bp, step, conv2, fc1, fc2, st);
     if (rc) return rc;
     ce_kernel<<<G, Bp, (size_t)Bp * NC * 4, st>>>(logits, master, Bp, C, labels, valid, dl, db2, loss);
     if ((rc = tc::gemm_run(fc2_dg, st))) return rc;
@@ -641,9 +633,8 @@ struct Engine {
     pool2_bwd_kernel<<<dim3(Bp, G), 256, 0, st>>>(dp2, a2, da2, part2, Bp);
     if ((rc = tc::gemm_run(conv2_dg, st))) return rc;
     if ((rc = tc::gemm_run(conv2_wg, st))) return rc;
-    pool1_bwd_kernel<<<dim3(Bp, G), 256, kP1bSmem, st>>>(dp1, a1, da1, part1, Bp);
-    if ((rc = tc::gemm_run(conv1_wg, st))) return rc;
-    bias_sgd_kernel<<<G, 256, 0, st>>>(master, shadow, part1, part2, db1, db2, Bp, lr);
+    conv1_bwd_kernel<<<dim3(Bp, G), 256, 0, st>>>(dp1, pmask, xin, dw1, part1, Bp);
+    bias_sgd_kernel<<<G, 256, 0, st>>>(master, shadow, part1, part2, db1, db2, dw1, Bp, lr);
     FEDHC_CUDA_TRY(cudaGetLastError());
     return FEDHC_OK;
   }
@@ -676,8 +667,6 @@ extern "C" int fedhc_cnn_create(int max_clients, int batch, int n_classes, void*
   e->maxG = max_clients;
   e->Bp = (batch + 63) / 64 * 64;
   e->C = n_classes;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::pool1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      cnn::kP1bSmem));
   FEDHC_CUDA_TRY(cudaFuncSetAttribute(cnn::ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       e->Bp * cnn::NC * 4));
   int rc = e->init();
@@ -704,7 +693,6 @@ extern "C" int fedhc_cnn_local_train(void* ws, const fedhc_client* clients, int 
   if (rc) return rc;
   FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, clients, sizeof(fedhc_client) * G, cudaMemcpyDeviceToDevice, st));
   cnn::bcast_kernel<<<cnn::Engine::grid_for((int64_t)G * cnn::PPAD), 256, 0, st>>>(params, e->master, e->shadow, G);
-  cnn::wc1_shadow_kernel<<<G, 256, 0, st>>>(e->master, e->shadow);
   FEDHC_CUDA_TRY(cudaGetLastError());
   if (use_graph) {
     const auto key = std::make_tuple(G, max_steps, lr);
@@ -756,7 +744,6 @@ extern "C" int fedhc_cnn_eval(void* ws, const double* params, const float* x, co
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int chunk = e->maxG * e->Bp;
   cnn::bcast_kernel<<<cnn::Engine::grid_for(cnn::PPAD), 256, 0, st>>>(params, e->master, e->shadow, 1);
-  cnn::wc1_shadow_kernel<<<1, 256, 0, st>>>(e->master, e->shadow);
   for (int64_t at = 0; at < n; at += chunk) {
     const int rows = (int)(n - at < chunk ? n - at : chunk);
     fedhc_client c{};
@@ -767,7 +754,7 @@ extern "C" int fedhc_cnn_eval(void* ws, const double* params, const float* x, co
     c.n_batches = 1;
     c.batch_size = rows;
     FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, &c, sizeof(c), cudaMemcpyHostToDevice, st));
-    int rc = e->forward(1, chunk, 0, e->e_conv1, e->e_conv2, e->e_fc1, e->e_fc2, st);
+    int rc = e->forward(1, chunk, 0, e->e_conv2, e->e_fc1, e->e_fc2, st);
     if (rc) return rc;
     cnn::argmax_kernel<<<(rows + 255) / 256, 256, 0, st>>>(e->logits, e->master, rows, e->C, e->labels, correct);
     FEDHC_CUDA_TRY(cudaGetLastError());
