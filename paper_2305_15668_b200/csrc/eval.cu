@@ -95,8 +95,12 @@ extern "C" int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_fea
   const int Fs = (n_features + 3) / 4 * 4;
   const size_t smem = ((size_t)n_classes * Fs + n_classes) * 4;
   if (smem > (size_t)max_smem) return fail(FEDHC_ERR_UNSUPPORTED, "eval: model too large for shared memory");
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+  static int smem_set = 0;  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs)
+  if ((int)smem > smem_set) {
+    FEDHC_CUDA_TRY(cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    smem_set = (int)smem;
+  }
   const int64_t need = (n + (kEvalThreads / 32) - 1) / (kEvalThreads / 32);
   const int blocks = static_cast<int>(std::min<int64_t>(need, (int64_t)sms));
   eval_kernel<<<blocks, kEvalThreads, smem, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);

@@ -793,7 +793,12 @@ bool launch_train_fused(const fedhc_client* clients, int n_clients, const double
   static const bool v3_only = getenv("FEDHC_TRAIN_V3") != nullptr;
   PipeGeom pg{};
   if (!v3_only && plan_pipe(F, C, max_smem, pg)) {
-    cudaError_t e = cudaFuncSetAttribute(train_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.bytes);
+    static int smem_set = 0;  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs)
+    cudaError_t e = cudaSuccess;
+    if (pg.bytes > smem_set) {
+      e = cudaFuncSetAttribute(train_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.bytes);
+      if (e == cudaSuccess) smem_set = pg.bytes;
+    }
     if (e == cudaSuccess) {
       train_pipe_kernel<<<n_clients, kPThreads, pg.bytes, st>>>(clients, params, F, C, pg);
       e = cudaGetLastError();

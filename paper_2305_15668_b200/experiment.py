@@ -361,7 +361,7 @@ class FederatedRunner:
 
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
-                 plan_threads: int = 0, device_permutations: bool = True):
+                 plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = True):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -400,6 +400,36 @@ class FederatedRunner:
         self._meta_dev = [torch.empty(k_max * 24, dtype=torch.uint8, device=dev) for _ in range(n)]
         self._plan_stream = torch.cuda.Stream(device=dev)
         self._train_done = [None] * n   # event: the slot's train kernel retired (plan buffer reusable)
+        # one pinned / device staging block per slot for the device-plan mode: [meta 24k | desc | coef 8k],
+        # copied H2D in one transfer on the plan stream
+        self._stage_pin = [torch.empty(k_max * (24 + CLIENT_DTYPE.itemsize + 8), dtype=torch.uint8).pin_memory()
+                           for _ in range(n)]
+        self._stage_dev = [torch.empty(k_max * (24 + CLIENT_DTYPE.itemsize + 8), dtype=torch.uint8, device=dev)
+                           for _ in range(n)]
+        self._ev_plan = [torch.cuda.Event() for _ in range(n)]
+        self._ev_train = [torch.cuda.Event() for _ in range(n)]
+        self._ev_result = [torch.cuda.Event() for _ in range(n)]
+        # per-client constants, indexed like self.ids (vectorised planning)
+        F = fed.n_features
+        off = np.array([fed.offset[c][0] for c in self.ids], np.int64)
+        self._c_rows = np.array([fed.offset[c][1] for c in self.ids], np.int64)
+        ns = np.array([fleet[c].workload.num_samples for c in self.ids], np.int64)
+        bs = np.array([fleet[c].workload.batch_size for c in self.ids], np.int64)
+        self._c_w = ns.astype(np.float64)
+        self._c_bs = bs
+        self._c_steps = -(-ns // bs)
+        per_epoch = -(-self._c_rows // bs)
+        self._c_nperm = np.where(self._c_rows == 0, 0,
+                                 np.maximum(1, -(-self._c_steps // np.maximum(per_epoch, 1))))
+        self._rows_max = int(self._c_rows.max()) if len(self._c_rows) else 0
+        self._bs_max = int(bs.max()) if len(bs) else 1
+        # CUDA graphs per slot (world == 1, device plans): [H2D + permutations] on the plan stream and
+        # [train + FedAvg + eval + D2H] on the main stream, each replayed with one launch per round
+        self.use_graphs = use_graphs and device_permutations and world == 1
+        self._graphs = [None] * n
+        self._cap_stream = torch.cuda.Stream(device=dev)
+        self._c_xptr = fed.x.data_ptr() + off * (F * 4)
+        self._c_yptr = fed.y.data_ptr() + off * 4
         self.now = 0.0
         self.round = 0
         self.h2d_bytes = 0
@@ -420,47 +450,56 @@ class FederatedRunner:
         cfg = self.cfg
         slot = (r % self.SLOTS) if slot is None else slot
         tick = time.perf_counter()
-        who = self.selector.sample(self.ids, cfg.participants_per_round)
+        # random.sample draws indices from len(population) only: sampling range(n) is the same draw
+        # sequence as sampling the ids (engine.py:327), and gives the fleet indices directly
+        who_idx = self.selector.sample(range(len(self.ids)), cfg.participants_per_round)
+        who = [self.ids[i] for i in who_idx]
         rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
         t1 = time.perf_counter()
         lo, hi = self._shard_bounds(len(who), self.world, self.rank)
         mine = who[lo:hi]
+        mi = np.asarray(who_idx[lo:hi], np.int64)
         k = len(mine)
-        wls = [self.by_id[c].workload for c in who]
-        weights_all = [float(w.num_samples) for w in wls]
-        total = float(sum(weights_all))
-        coef = np.array([w / total for w in weights_all[lo:hi]], dtype=np.float64)
+        weights_all = self._c_w[np.asarray(who_idx, np.int64)].tolist()
+        total = float(sum(weights_all))                      # CPython float sum, as the reference
+        coef = np.asarray(weights_all[lo:hi], np.float64) / total
         reprs = (C.c_char_p * max(k, 1))(*[self._repr[c] for c in mine])
         train_seeds = np.zeros(max(k, 1), np.uint64)
         rng_seeds = np.zeros(max(k, 1), np.uint64)
         _abi.check(_abi.lib.fedhc_round_seeds(int(cfg.seed), int(r), reprs, k, train_seeds.ctypes.data,
                                               rng_seeds.ctypes.data))
         t2 = time.perf_counter()
-        meta, rows, perms, at = [], [], [], 0
-        for cid, wl in zip(mine, wls[lo:hi]):
-            _, n = self.fed.offset[cid]
-            kp = n_permutations(n, wl.num_samples, wl.batch_size)
-            meta.append((at, n, math.ceil(wl.num_samples / wl.batch_size), wl.batch_size))
-            rows.append(n)
-            perms.append(kp)
-            at += n * kp
+        rows = self._c_rows[mi]
+        perms = self._c_nperm[mi]
+        sizes = rows * perms
+        offs = np.zeros(k, np.int64)
+        if k > 1:
+            np.cumsum(sizes[:-1], out=offs[1:])
+        at = int(sizes.sum()) if k else 0
         self._ensure(slot, max(at, 1))
         meta_bytes = 0
         if at and self.device_permutations:
-            buf = self._meta_pin[slot].numpy()
-            sizes = np.asarray(rows, np.int64) * np.asarray(perms, np.int64)
-            offs = np.zeros(k, np.int64)
-            if k > 1:
-                np.cumsum(sizes[:-1], out=offs[1:])
+            buf = self._stage_pin[slot].numpy()
             buf[:8 * k] = rng_seeds[:k].view(np.uint8)
-            buf[8 * k:12 * k] = np.asarray(rows, np.int32).view(np.uint8)
-            buf[12 * k:16 * k] = np.asarray(perms, np.int32).view(np.uint8)
+            buf[8 * k:12 * k] = rows.astype(np.int32).view(np.uint8)
+            buf[12 * k:16 * k] = perms.astype(np.int32).view(np.uint8)
             buf[16 * k:24 * k] = offs.view(np.uint8)
             meta_bytes = 24 * k
+            self._stage_pin[slot].numpy()[meta_bytes + k * CLIENT_DTYPE.itemsize:][:8 * k] = coef.view(np.uint8)
         elif at:
-            native_permutations(rng_seeds[:k], rows, perms, out=self._pinned[slot].numpy(), threads=self.plan_threads)
+            native_permutations(rng_seeds[:k], rows.tolist(), perms.tolist(), out=self._pinned[slot].numpy(),
+                                threads=self.plan_threads)
         t3 = time.perf_counter()
-        desc = self.fed.descriptor_array(mine, meta, self.lr, self.deltas, perm_base=self._dev_plan[slot].data_ptr())
+        desc = np.zeros(k, dtype=CLIENT_DTYPE)
+        if k:
+            desc["x"] = self._c_xptr[mi]
+            desc["y"] = self._c_yptr[mi]
+            desc["perm"] = self._dev_plan[slot].data_ptr() + offs * 4
+            desc["n_rows"] = rows
+            desc["n_batches"] = self._c_steps[mi]
+            desc["batch_size"] = self._c_bs[mi]
+            desc["lr"] = self.lr
+            desc["delta"] = self.deltas.data_ptr() + np.arange(k, dtype=np.int64) * (self.deltas.stride(0) * 4)
         t4 = time.perf_counter()
         hs = self.host_s
         hs["select+des"] += t1 - tick
@@ -468,9 +507,38 @@ class FederatedRunner:
         hs["permutations"] += t3 - t2
         hs["descriptors"] += t4 - t3
         return RoundPlan(r, mine, who, rep, t0, weights_all[lo:hi], coef, slot, at, desc, meta_bytes,
-                         max(rows, default=0))
+                         int(rows.max()) if k else 0)
 
     # ---- device side -------------------------------------------------------
+    def _graph_key(self, p: RoundPlan):
+        return (len(p.participants), p.meta_bytes, self._dev_plan[p.slot].data_ptr())
+
+    def _capture(self, p: RoundPlan):
+        """Capture the slot's two graphs (no execution); replayed from the next use of the slot on."""
+        k, slot, mb = len(p.participants), p.slot, p.meta_bytes
+        nb = k * CLIENT_DTYPE.itemsize
+        tot = mb + nb + 8 * k
+        dev = self._stage_dev[slot]
+        md = dev.data_ptr()
+        coef_t = dev[mb + nb:mb + nb + 8 * k].view(torch.float64)
+        gp, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gp, stream=self._cap_stream, capture_error_mode="thread_local"):
+            dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
+            _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
+                                                                self._dev_plan[slot].data_ptr(), self._rows_max,
+                                                                stream_ptr()))
+        with torch.cuda.graph(gr, stream=self._cap_stream, capture_error_mode="thread_local"):
+            _abi.check(_abi.lib.fedhc_local_train(md + mb, k, self.params.data_ptr(), self.fed.n_features,
+                                                  self.fed.n_classes, self._bs_max, stream_ptr()))
+            fedavg_device(self.deltas[:k], coef_t, self.params, self.params)
+            self.correct_dev.zero_()
+            if self.fed.n_test:
+                _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
+                                               self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                                               self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
+            self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
+        self._graphs[slot] = (self._graph_key(p), gp, gr)
+
     def launch(self, p: RoundPlan) -> None:
         """Enqueue the round on the current stream (asynchronous); result lands in slot p.slot."""
         from .sharding import all_reduce_count, combine_partials
@@ -479,51 +547,72 @@ class FederatedRunner:
         k = len(p.participants)
         slot = p.slot
         main = torch.cuda.current_stream()
-        plan_ready = None
-        if p.meta_bytes:
+        nb = k * CLIENT_DTYPE.itemsize
+        gs = self._graphs[slot]
+        if self.use_graphs and k and p.meta_bytes and gs is not None and gs[0] == self._graph_key(p):
+            mb = p.meta_bytes
+            self._stage_pin[slot].numpy()[mb:mb + nb] = p.desc.view(np.uint8)   # (coefficients: plan())
             ps = self._plan_stream
             with torch.cuda.stream(ps):
-                if self._train_done[slot] is not None:
-                    ps.wait_event(self._train_done[slot])   # the slot's previous train kernel is done with it
-                self._meta_dev[slot][:p.meta_bytes].copy_(self._meta_pin[slot][:p.meta_bytes], non_blocking=True)
-                md = self._meta_dev[slot].data_ptr()
+                gs[1].replay()
+                self._ev_plan[slot].record(ps)
+            main.wait_event(self._ev_plan[slot])
+            self._plan_done[slot] = self._ev_plan[slot]
+            gs[2].replay()
+            self._ev_train[slot].record()
+            self._train_done[slot] = self._ev_train[slot]
+            self._ev_result[slot].record()
+            self._result_ev[slot] = self._ev_result[slot]
+            self.h2d_bytes = mb + nb + 8 * k
+            self.host_s["launch"] += time.perf_counter() - tick
+            return
+        if p.meta_bytes:
+            # one H2D transfer of [meta | descriptors | coefficients] on the plan stream, then the
+            # device PCG64 permutations; the main stream waits for both
+            ps = self._plan_stream
+            mb = p.meta_bytes
+            stage = self._stage_pin[slot].numpy()
+            stage[mb:mb + nb] = p.desc.view(np.uint8)
+            stage[mb + nb:mb + nb + 8 * k] = p.coef.view(np.uint8)
+            tot = mb + nb + 8 * k
+            dev = self._stage_dev[slot]
+            md = dev.data_ptr()
+            with torch.cuda.stream(ps):
+                ps.wait_event(self._ev_train[slot])      # the slot's previous train kernel is done with it
+                dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
                 _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
                                                                     self._dev_plan[slot].data_ptr(), p.max_rows,
                                                                     ps.cuda_stream))
-                plan_ready = torch.cuda.Event()
-                plan_ready.record(ps)
-        elif p.perm_words:
-            self._dev_plan[slot][:p.perm_words].copy_(self._pinned[slot][:p.perm_words], non_blocking=True)
-        nb = k * CLIENT_DTYPE.itemsize
-        if k:
-            self._desc_pin[slot].numpy()[:nb] = p.desc.view(np.uint8)
-            self._desc_dev[slot][:nb].copy_(self._desc_pin[slot][:nb], non_blocking=True)
-            self._coef_pin[slot].numpy()[:k] = p.coef
-            self._coef_dev[slot][:k].copy_(self._coef_pin[slot][:k], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        if plan_ready is not None:
-            main.wait_event(plan_ready)
-            ev2 = torch.cuda.Event()   # pinned meta reusable once the plan stream copied it
-            ev2.record(self._plan_stream)
-            self._plan_done[slot] = ev2
-            self.h2d_bytes = p.meta_bytes + nb + k * 8
+                self._ev_plan[slot].record(ps)
+            main.wait_event(self._ev_plan[slot])
+            self._plan_done[slot] = self._ev_plan[slot]
+            desc_ptr, coef_t = md + mb, dev[mb + nb:mb + nb + 8 * k].view(torch.float64)
+            self.h2d_bytes = tot
         else:
+            if p.perm_words:
+                self._dev_plan[slot][:p.perm_words].copy_(self._pinned[slot][:p.perm_words], non_blocking=True)
+            if k:
+                self._desc_pin[slot].numpy()[:nb] = p.desc.view(np.uint8)
+                self._desc_dev[slot][:nb].copy_(self._desc_pin[slot][:nb], non_blocking=True)
+                self._coef_pin[slot].numpy()[:k] = p.coef
+                self._coef_dev[slot][:k].copy_(self._coef_pin[slot][:k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
             self._plan_done[slot] = ev
+            desc_ptr, coef_t = self._desc_dev[slot].data_ptr(), self._coef_dev[slot][:k]
             self.h2d_bytes = p.perm_words * 4 + nb + k * 8
         if k:
             max_b = int(p.desc["batch_size"].max())
-            _abi.check(_abi.lib.fedhc_local_train(self._desc_dev[slot].data_ptr(), k, self.params.data_ptr(),
-                                                  self.fed.n_features, self.fed.n_classes, max_b, stream_ptr()))
-        td = torch.cuda.Event()
-        td.record()
-        self._train_done[slot] = td
+            _abi.check(_abi.lib.fedhc_local_train(desc_ptr, k, self.params.data_ptr(), self.fed.n_features,
+                                                  self.fed.n_classes, max_b, stream_ptr()))
+        self._ev_train[slot].record()
+        self._train_done[slot] = self._ev_train[slot]
         if self.world == 1:
             if k:
-                fedavg_device(self.deltas[:k], self._coef_dev[slot][:k], self.params, self.params)
+                fedavg_device(self.deltas[:k], coef_t, self.params, self.params)
         else:
             if k:
-                fedavg_device(self.deltas[:k], self._coef_dev[slot][:k], None, self.partial)
+                fedavg_device(self.deltas[:k], coef_t, None, self.partial)
             else:
                 self.partial.zero_()
             combine_partials(self.partial, self.params,
@@ -536,9 +625,10 @@ class FederatedRunner:
         if self.world > 1:
             all_reduce_count(self.correct_dev, self.group)
         self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record()
-        self._result_ev[slot] = done
+        self._ev_result[slot].record()
+        self._result_ev[slot] = self._ev_result[slot]
+        if self.use_graphs and k and p.meta_bytes and (gs is None or gs[0] != self._graph_key(p)):
+            self._capture(p)
         self.host_s["launch"] += time.perf_counter() - tick
 
     def read_correct(self, slot: int) -> int:
