@@ -93,15 +93,28 @@ __device__ __forceinline__ int first_max4(float v0, float v1, float v2, float v3
 // Outputs: xin [G*Bp][784] bf16 (the input, for the weight gradient), p1x (channel-pair layout of
 // conv2's implicit GEMM, see pool1 below), pmask [G*Bp][196][32] = argmax(0..3) | (max > 0) << 2.
 constexpr int W1X = 15;
-// thread = output channel (lane), warp = a strided set of pooled pixels: the 25 weights live in
-// registers and every image value is a shared-memory broadcast (6x6 patch per pooled pixel).
-__global__ void __launch_bounds__(256) conv1_fwd_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
-                                                        const float* __restrict__ master,
-                                                        __nv_bfloat16* __restrict__ xin,
-                                                        int32_t* __restrict__ labels, int32_t* __restrict__ valid,
-                                                        __nv_bfloat16* __restrict__ p1x,
-                                                        uint8_t* __restrict__ pmask) {
-  __shared__ __align__(16) float img[32][32];  // 28x28 + 2-pixel zero border
+// Tensor-core conv1 (mma.sync m16n8k16 bf16, fp32 accumulate): out[pixel][ch] = im2col[pixel][tap] . W[tap][ch]
+// with K = 32 taps (25 + 7 zero-weight taps).  An m16 tile = 2 image rows x 8 columns (rows 0-7 y = 2a,
+// rows 8-15 y = 2a + 1), so every 2x2 pooling window sits in one tile: the y pair in one lane's c0/c2,
+// the x pair across lanes gq, gq ^ 1.  A fragments are gathered from the zero-bordered image in smem.
+constexpr int IMW = 40;  // padded image row stride: x + kw <= 31 + 4
+
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+__device__ __forceinline__ int tap_off(int t) { return t < 25 ? (t / 5) * IMW + (t % 5) : 0; }
+
+__global__ void __launch_bounds__(256, 4) conv1_fwd_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
+                                                           const float* __restrict__ master,
+                                                           __nv_bfloat16* __restrict__ xin,
+                                                           int32_t* __restrict__ labels, int32_t* __restrict__ valid,
+                                                           __nv_bfloat16* __restrict__ p1x,
+                                                           uint8_t* __restrict__ pmask) {
+  __shared__ __align__(16) __nv_bfloat16 img[32 * IMW];  // 28x28, 2-pixel zero border, x padded to 40
+  __shared__ __align__(16) __nv_bfloat16 pooled[HW1 * C1];  // staged outputs, written out coalesced
+  __shared__ __align__(16) uint8_t pm[HW1 * C1];
   const int g = blockIdx.y, b = blockIdx.x;
   const fedhc_client c = cl[g];
   int rows = 0;
@@ -119,58 +132,96 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const fedhc_client* __re
   const int row = ok ? (c.perm ? c.perm[poff + b] : b) : 0;
   const float* src = c.x + (int64_t)row * HW0;
   const int64_t im = (int64_t)g * Bp + b;
-  for (int i = threadIdx.x; i < 32 * 32; i += 256) (&img[0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < 32 * IMW / 2; i += 256) reinterpret_cast<uint32_t*>(img)[i] = 0u;
   if (threadIdx.x == 0) {
     labels[im] = ok ? c.y[row] : 0;
     if (b == 0) valid[g] = rows;
   }
-  const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, tq = lane & 3;
+  // B fragments (weights, bf16): [k16 step][n8 tile][2] ; B[k][n] = W[tap k][ch n]
   const float* mw = master + (int64_t)g * PPAD;
-  float w[25];
+  uint32_t bw[2][4][2];
 #pragma unroll
-  for (int t = 0; t < 25; ++t) w[t] = bf(__float2bfloat16_rn(mw[OFF_WC1 + t * C1 + ch]));
-  const float bias = mw[OFF_BC1 + ch];
+  for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int n = nt * 8 + gq, k0 = ks * 16 + 2 * tq;
+      auto wv = [&](int t) { return t < 25 ? mw[OFF_WC1 + t * C1 + n] : 0.f; };
+      bw[ks][nt][0] = pack_bf2(wv(k0), wv(k0 + 1));
+      bw[ks][nt][1] = pack_bf2(wv(k0 + 8), wv(k0 + 9));
+    }
+  float bias[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    bias[nt][0] = mw[OFF_BC1 + nt * 8 + 2 * tq];
+    bias[nt][1] = mw[OFF_BC1 + nt * 8 + 2 * tq + 1];
+  }
+  int toff[2][4];  // this lane's A-fragment taps: k = 2tq, 2tq + 1, 2tq + 8, 2tq + 9 (+16 per k step)
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    toff[ks][0] = tap_off(ks * 16 + 2 * tq);
+    toff[ks][1] = tap_off(ks * 16 + 2 * tq + 1);
+    toff[ks][2] = tap_off(ks * 16 + 2 * tq + 8);
+    toff[ks][3] = tap_off(ks * 16 + 2 * tq + 9);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < HW0; i += 256) {
     const __nv_bfloat16 v = __float2bfloat16_rn(ok ? __ldg(src + i) : 0.f);
     xin[im * HW0 + i] = v;
-    img[2 + i / W0][2 + i % W0] = bf(v);
+    img[(2 + i / W0) * IMW + 2 + i % W0] = v;
   }
   __syncthreads();
-  __nv_bfloat16* prow0 = p1x + (int64_t)im * W1d * W1X * 64;
-  for (int p = warp; p < HW1; p += 8) {
-    const int oh = p / W1d, ow = p - oh * W1d;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    // output pixel (2oh + i, 2ow + j), tap (kh, kw) reads img[2oh + i + kh][2ow + j + kw] (border-padded)
+  const unsigned short* imu = reinterpret_cast<const unsigned short*>(img);
+  for (int tile = warp; tile < 14 * 4; tile += 8) {
+    const int a = tile >> 2, bx = tile & 3;
+    const int y0 = 2 * a, x = 8 * bx + gq;
+    const int base0 = y0 * IMW + x, base1 = base0 + IMW;  // padded coords: tap (kh, kw) adds kh*IMW + kw
+    float acc[4][4];
 #pragma unroll
-    for (int dy = 0; dy < 6; ++dy) {
-      const float2* rp = reinterpret_cast<const float2*>(&img[2 * oh + dy][2 * ow]);
-      const float2 r0 = rp[0], r1 = rp[1], r2 = rp[2];
-      const float v[6] = {r0.x, r0.y, r1.x, r1.y, r2.x, r2.y};
+    for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
 #pragma unroll
-      for (int dx = 0; dx < 6; ++dx) {
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t af[4];
+      af[0] = imu[base0 + toff[ks][0]] | ((uint32_t)imu[base0 + toff[ks][1]] << 16);
+      af[1] = imu[base1 + toff[ks][0]] | ((uint32_t)imu[base1 + toff[ks][1]] << 16);
+      af[2] = imu[base0 + toff[ks][2]] | ((uint32_t)imu[base0 + toff[ks][3]] << 16);
+      af[3] = imu[base1 + toff[ks][2]] | ((uint32_t)imu[base1 + toff[ks][3]] << 16);
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+      for (int nt = 0; nt < 4; ++nt) mma_bf16(acc[nt], af, bw[ks][nt][0], bw[ks][nt][1]);
+    }
+    // epilogue: bias + ReLU + bf16, 2x2 max pool (first max, row-major window order), pool mask -> smem
+    const bool own = (gq & 1) == 0 && x < W0;  // the even-x lane of the x pair owns the window
+    const int pp = a * W1d + (x >> 1);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int kh = dy - i, kw = dx - j;
-            if (kh >= 0 && kh <= 4 && kw >= 0 && kw <= 4) acc[i * 2 + j] += v[dx] * w[kh * 5 + kw];
-          }
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float v0 = bf(__float2bfloat16_rn(fmaxf(acc[nt][e] + bias[nt][e], 0.f)));
+        const float v2 = bf(__float2bfloat16_rn(fmaxf(acc[nt][2 + e] + bias[nt][e], 0.f)));
+        const float v1 = __shfl_xor_sync(0xffffffffu, v0, 4);   // partner lane: x + 1
+        const float v3 = __shfl_xor_sync(0xffffffffu, v2, 4);
+        const int k = first_max4(v0, v1, v2, v3);
+        const float m = fmaxf(fmaxf(v0, v1), fmaxf(v2, v3));
+        if (own) {
+          const int ch = nt * 8 + 2 * tq + e;
+          pooled[pp * C1 + ch] = __float2bfloat16_rn(m);
+          pm[pp * C1 + ch] = (uint8_t)(k | (m > 0.f ? 4 : 0));
         }
       }
     }
-    float q[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = bf(__float2bfloat16_rn(fmaxf(acc[k] + bias, 0.f)));
-    const int k = first_max4(q[0], q[1], q[2], q[3]);
-    pmask[(im * HW1 + p) * C1 + ch] = (uint8_t)(k | (q[k] > 0.f ? 4 : 0));
-    const __nv_bfloat16 pooled = __float2bfloat16_rn(q[k]);
-    __nv_bfloat16* prow = prow0 + (int64_t)oh * W1X * 64;
-    prow[(ow + 1) * 64 + ch] = pooled;      // column x + 1, low half
-    prow[ow * 64 + 32 + ch] = pooled;       // column x, high half
-    if (ow == 0) prow[ch] = __float2bfloat16_rn(0.f);
-    if (ow == W1d - 1) prow[W1d * 64 + 32 + ch] = __float2bfloat16_rn(0.f);
   }
+  __syncthreads();
+  // p1x rows: column xx = [pooled(y, xx - 1) | pooled(y, xx)] (zero outside), 16-byte stores
+  uint4* dst = reinterpret_cast<uint4*>(p1x + (int64_t)im * W1d * W1X * 64);
+  const uint4* src4 = reinterpret_cast<const uint4*>(pooled);
+  for (int i = threadIdx.x; i < W1d * W1X * 8; i += 256) {
+    const int q = i & 7, col = (i >> 3) % W1X, yy = (i >> 3) / W1X;   // q: 16-byte chunk of the 128-byte row
+    const int xs = q < 4 ? col - 1 : col;                                // low half: x - 1, high half: x
+    dst[i] = (xs >= 0 && xs < W1d) ? src4[(yy * W1d + xs) * 4 + (q & 3)] : make_uint4(0, 0, 0, 0);
+  }
+  uint4* pdst = reinterpret_cast<uint4*>(pmask + im * HW1 * C1);
+  const uint4* psrc = reinterpret_cast<const uint4*>(pm);
+  for (int i = threadIdx.x; i < HW1 * C1 / 16; i += 256) pdst[i] = psrc[i];
 }
 
 // ---- 2x2 max pool, NHWC, 8 channels per thread ---------------------------------
@@ -315,64 +366,106 @@ __global__ void __launch_bounds__(256) pool2_bwd_kernel(const __nv_bfloat16* __r
                                    red[3][threadIdx.x];
 }
 
-// grid (Bp, G): maxpool1 backward (pool mask) + conv1 weight gradient of one image.
-// dp1 [G*Bp][196][32] bf16, pmask, xin [G*Bp][784] bf16 -> dw [G*Bp][25*32] fp32 partials,
-// part [G*Bp][32] (bias).  dL/da1 is nonzero only at each window's first max (if > 0).  Thread =
-// channel, warp = strided pooled pixels: the gradient is routed to the 4 window positions with a
-// select (3 of 4 zero) so every image value is a broadcast; 25 accumulators per thread, then a
-// fixed-order reduction over the 8 warps.
+// grid (Bp, G): maxpool1 backward (pool mask) + conv1 weight gradient of one image on the tensor pipe:
+// dW[tap][ch] = sum_pixels im2col[pixel][tap] . dL/da1[pixel][ch]  (mma.sync m16n8k16: M = 32 taps,
+// N = 32 channels, K = pixels in the same 2x8 tiles as the forward; dL/da1 = dp1 routed to each pool
+// window's first max when it is > 0).  The 8 warps' partial dW are summed in a fixed order.
+// dp1 [G*Bp][196][32] bf16, pmask, xin [G*Bp][784] bf16 -> dw [G*Bp][25*32], part [G*Bp][32] (bias).
 __global__ void __launch_bounds__(256) conv1_bwd_kernel(const __nv_bfloat16* __restrict__ dp1,
                                                         const uint8_t* __restrict__ pmask,
                                                         const __nv_bfloat16* __restrict__ xin,
                                                         float* __restrict__ dw, float* __restrict__ part, int Bp) {
-  __shared__ __align__(16) float img[32][32];
-  __shared__ float red[8][26][32];
+  __shared__ __align__(16) __nv_bfloat16 img[32 * IMW];
+  // scratch: [gz masked pooled gradient | kk argmax position] during the MMAs, then the warps' partial dW
+  __shared__ __align__(16) unsigned char scratch[8 * 25 * 32 * 4];
+  auto gz = reinterpret_cast<__nv_bfloat16(*)[C1 + 2]>(scratch);
+  auto kk = reinterpret_cast<uint8_t(*)[C1 + 4]>(scratch + HW1 * (C1 + 2) * 2);
+  auto red = reinterpret_cast<float(*)[25][32]>(scratch);
+  static_assert(HW1 * (C1 + 2) * 2 + HW1 * (C1 + 4) <= 8 * 25 * 32 * 4, "scratch too small");
   const int64_t im = (int64_t)blockIdx.y * Bp + blockIdx.x;
-  for (int i = threadIdx.x; i < 32 * 32; i += 256) (&img[0][0])[i] = 0.f;
+  for (int i = threadIdx.x; i < 32 * IMW / 2; i += 256) reinterpret_cast<uint32_t*>(img)[i] = 0u;
   __syncthreads();
-  for (int i = threadIdx.x; i < HW0; i += 256) img[2 + i / W0][2 + i % W0] = bf(xin[im * HW0 + i]);
+  for (int i = threadIdx.x; i < HW0; i += 256) img[(2 + i / W0) * IMW + 2 + i % W0] = xin[im * HW0 + i];
+  for (int i = threadIdx.x; i < HW1 * C1; i += 256) {
+    const int p = i / C1, c = i - p * C1;
+    const uint8_t m = pmask[im * HW1 * C1 + i];
+    gz[p][c] = (m & 4) ? dp1[im * HW1 * C1 + i] : __float2bfloat16_rn(0.f);
+    kk[p][c] = m & 3;
+  }
   __syncthreads();
-  const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float acc[25], sb = 0.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, tq = lane & 3;
+  const unsigned short* imu = reinterpret_cast<const unsigned short*>(img);
+  const int off_m0 = tap_off(gq), off_m1 = tap_off(gq + 8), off_m2 = tap_off(gq + 16), off_m3 = tap_off(gq + 24);
+  float acc[2][4][4];
 #pragma unroll
-  for (int t = 0; t < 25; ++t) acc[t] = 0.f;
-  for (int p = warp; p < HW1; p += 8) {
-    const int oh = p / W1d, ow = p - oh * W1d;
-    const uint8_t m = pmask[(im * HW1 + p) * C1 + ch];
-    const float gv = (m & 4) ? bf(dp1[(im * HW1 + p) * C1 + ch]) : 0.f;
-    sb += gv;
-    float gk[4];
+  for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) gk[k] = (m & 3) == k ? gv : 0.f;
+    for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+  for (int tile = warp; tile < 14 * 4; tile += 8) {
+    const int a = tile >> 2, bx = tile & 3, y0 = 2 * a;
+    // this lane's K (pixel) indices: 2tq, 2tq + 1 (row y0) and 2tq + 8, 2tq + 9 (row y0 + 1), x = 8bx + ...
+    const int xa = 8 * bx + 2 * tq;
+    const int pix_base[4] = {y0 * IMW + xa, y0 * IMW + xa + 1, (y0 + 1) * IMW + xa, (y0 + 1) * IMW + xa + 1};
+    // A fragments: A[tap m][pixel k]
+    uint32_t af[2][4];
+    {
+      const int o[4] = {off_m0, off_m1, off_m2, off_m3};
 #pragma unroll
-    for (int dy = 0; dy < 6; ++dy) {
-      const float2* rp = reinterpret_cast<const float2*>(&img[2 * oh + dy][2 * ow]);
-      const float2 r0 = rp[0], r1 = rp[1], r2 = rp[2];
-      const float v[6] = {r0.x, r0.y, r1.x, r1.y, r2.x, r2.y};
-#pragma unroll
-      for (int dx = 0; dx < 6; ++dx) {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int kh = dy - i, kw = dx - j;
-            if (kh >= 0 && kh <= 4 && kw >= 0 && kw <= 4) acc[kh * 5 + kw] += gk[i * 2 + j] * v[dx];
-          }
-        }
+      for (int mt = 0; mt < 2; ++mt) {
+        af[mt][0] = imu[pix_base[0] + o[2 * mt]] | ((uint32_t)imu[pix_base[1] + o[2 * mt]] << 16);
+        af[mt][1] = imu[pix_base[0] + o[2 * mt + 1]] | ((uint32_t)imu[pix_base[1] + o[2 * mt + 1]] << 16);
+        af[mt][2] = imu[pix_base[2] + o[2 * mt]] | ((uint32_t)imu[pix_base[3] + o[2 * mt]] << 16);
+        af[mt][3] = imu[pix_base[2] + o[2 * mt + 1]] | ((uint32_t)imu[pix_base[3] + o[2 * mt + 1]] << 16);
       }
     }
-  }
+    // B fragments: B[pixel k][ch n] = dL/da1 at (pixel, n = nt*8 + gq); the 4 pixels of this lane share
+    // one pooling window (x pair 2tq.., y pair) -> pooled pixel (a, 4bx + tq)
+    const bool valid = xa < W0;
+    const int pp = a * W1d + 4 * bx + tq;
 #pragma unroll
-  for (int t = 0; t < 25; ++t) red[warp][t][ch] = acc[t];
-  red[warp][25][ch] = sb;
+    for (int nt = 0; nt < 4; ++nt) {
+      const int n = nt * 8 + gq;
+      unsigned short gv = 0;
+      int k = 0;
+      if (valid) {
+        gv = reinterpret_cast<const unsigned short&>(gz[pp][n]);
+        k = kk[pp][n];
+      }
+      // window positions: 0 (y0, x), 1 (y0, x + 1), 2 (y0 + 1, x), 3 (y0 + 1, x + 1)
+      const uint32_t b0 = (k == 0 ? gv : 0u) | ((uint32_t)(k == 1 ? gv : 0u) << 16);
+      const uint32_t b1 = (k == 2 ? gv : 0u) | ((uint32_t)(k == 3 ? gv : 0u) << 16);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) mma_bf16(acc[mt][nt], af[mt], b0, b1);
+    }
+  }
+  if (threadIdx.x < C1) {  // bias: column sums of the routed gradient, fixed order
+    float s = 0.f;
+    for (int p = 0; p < HW1; ++p) s += bf(gz[p][threadIdx.x]);
+    part[im * C1 + threadIdx.x] = s;
+  }
+  __syncthreads();  // gz / kk dead: scratch becomes the partial-dW buffer
+  // accumulator layout: acc[mt][nt] = D[tap mt*16 + gq (+8)][ch nt*8 + 2tq (+1)]; taps >= 25 dropped
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int t0 = mt * 16 + gq, t1 = t0 + 8, c0 = nt * 8 + 2 * tq;
+      if (t0 < 25) {
+        red[warp][t0][c0] = acc[mt][nt][0];
+        red[warp][t0][c0 + 1] = acc[mt][nt][1];
+      }
+      if (t1 < 25) {
+        red[warp][t1][c0] = acc[mt][nt][2];
+        red[warp][t1][c0 + 1] = acc[mt][nt][3];
+      }
+    }
   __syncthreads();
-  for (int i = threadIdx.x; i < 26 * C1; i += 256) {
+  for (int i = threadIdx.x; i < 25 * C1; i += 256) {
     const int t = i / C1, c = i - t * C1;
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][t][c];
-    if (t < 25) dw[im * 25 * C1 + i] = s;
-    else part[im * C1 + c] = s;
+    for (int w = 0; w < 8; ++w) s += red[w][t][c];
+    dw[im * 25 * C1 + i] = s;
   }
 }
 
