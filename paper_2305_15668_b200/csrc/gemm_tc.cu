@@ -40,10 +40,17 @@ namespace tc {
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BM, int BN>
+// WIN: windowed implicit-GEMM convolution stages (0 = one K block per stage).  A stage holds a
+// 12-row x 16-column activation window (192 rows of 128 B, loaded once) plus the weights of the 5 taps
+// that share it; the MMAs of tap kh read the window through a descriptor shifted by whole 16-pixel
+// rows (2048 B, a multiple of the 1024-B swizzle atom).  WIN 1 = conv2 forward (window per tap-pair
+// column, 5 MN-major 64x64 weight blocks), WIN 2 = conv2 data gradient (window per kw, 5 K-major 32x64
+// weight blocks).
+template <int BM, int BN, int WIN = 0>
 struct Cfg {
-  static constexpr int kTileABytes = BM * BK * 2;
-  static constexpr int kTileBBytes = BN * BK * 2;
+  static constexpr int kTileABytes = WIN ? 192 * 128 : BM * BK * 2;
+  static constexpr int kTapBBytes = BN * BK * 2;
+  static constexpr int kTileBBytes = WIN ? 5 * kTapBBytes : kTapBBytes;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
 };
@@ -210,13 +217,13 @@ __device__ __forceinline__ void conv_loads(const ConvSpec& cv, uint32_t sa, uint
   }
 }
 
-template <int BM, int BN, bool A_MN, bool B_MN>
+template <int BM, int BN, bool A_MN, bool B_MN, int WIN = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_o, const __grid_constant__ CUtensorMap map_s,
                         const __grid_constant__ CUtensorMap map_l, int G, int M, int N, int K, int STAGES,
                         int nst, const Epilogue ep, const ConvSpec conv) {
-  using CF = Cfg<BM, BN>;
+  using CF = Cfg<BM, BN, WIN>;
   constexpr int kStageBytes = CF::kStageBytes, kTmemCols = CF::kTmemCols;
   constexpr int kTileABytes = CF::kTileABytes;
   constexpr int R = BM / 4;                      // output rows per epilogue warp
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = M / BM, tiles_n = N / BN;
   const int n_tiles = G * tiles_m * tiles_n;
-  const int kblocks = K / BK;
+  const int kblocks = WIN == 1 ? 3 : WIN == 2 ? 5 : K / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -299,8 +306,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
             }
-          } else {
+          } else if (WIN == 0) {
             conv_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
+          } else {
+            const int mt = m0 / BM, img = g * conv.bp + (mt >> 1), y0 = (mt & 1) * 8;
+            if (WIN == 1) {  // forward: tap-pair column pk = kb; window rows y0 - 2 .. y0 + 9
+              tma_load_4d(sa, &map_a, &full[s], 0, 2 * kb - 1, y0 - 2, img);
+#pragma unroll
+              for (int kh = 0; kh < 5; ++kh)
+                tma_load_3d(sb + kh * CF::kTapBBytes, &map_b, &full[s], n0, (kh * 3 + kb) * 64, g);
+            } else {         // data gradient: kw = kb; window rows y0 - 2 .. y0 + 9 of dL/da2
+              tma_load_4d(sa, &map_a, &full[s], 0, 2 - kb, y0 - 2, img);
+#pragma unroll
+              for (int kh = 0; kh < 5; ++kh)
+                tma_load_3d(sb + kh * CF::kTapBBytes, &map_b, &full[s], 0, (kh * 3 + (kb >> 1)) * 64 + (kb & 1) * 32,
+                            g);
+            }
           }
           if (++s == STAGES) {
             s = 0;
@@ -336,10 +357,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * kStageBytes);
-          const uint64_t da = sw128_desc(sa, kLboA), db = sw128_desc(sa + kTileABytes, kLboB);
+          if (WIN == 0) {
+            const uint64_t da = sw128_desc(sa, kLboA), db = sw128_desc(sa + kTileABytes, kLboB);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tmem_d, da + (kStepA >> 4) * k, db + (kStepB >> 4) * k, kIdesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(tmem_d, da + (kStepA >> 4) * k, db + (kStepB >> 4) * k, kIdesc, (kb | k) != 0);
+          } else {
+#pragma unroll
+            for (int kh = 0; kh < 5; ++kh) {
+              // forward reads input row y + kh - 2, data gradient y + 2 - kh: window row offset
+              const int wr = WIN == 1 ? kh : 4 - kh;
+              const uint64_t da = sw128_desc(sa + wr * 2048, kLboA);
+              const uint64_t db = sw128_desc(sa + kTileABytes + kh * CF::kTapBBytes, kLboB);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma_bf16(tmem_d, da + (kStepA >> 4) * k, db + (kStepB >> 4) * k, kIdesc, (kb | kh | k) != 0);
+            }
+          }
           umma_commit(&empty[s]);  // ring stage free once these MMAs retire
           if (++s == STAGES) {
             s = 0;
@@ -538,11 +572,11 @@ static int plan_conv_maps(const fedhc_gemm_args& a, GemmPlan* p) {
   const CUtensorMapSwizzle S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
   int rc;
   switch (p->conv.mode) {
-    case CONV_FWD:  // A = p1x [img][14][14][64]; B = generic MN-major weights; D = a2 [img][14][14][64]
-      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 8, S128, 15))) return rc;
+    case CONV_FWD:  // A = p1x [img][14][15][64] (12-row windows); B = generic MN-major weights; D = a2
+      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 12, S128, 15))) return rc;
       return make_act_map(&p->mo, a.D, 64, n_img, 32, 16, 2, S64);
-    case CONV_DGRAD:  // A = da2; B = weight rows [1024][64] (box of 32 rows); D = dp1 [img][14][14][32]
-      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 8, S128))) return rc;
+    case CONV_DGRAD:  // A = da2 (12-row windows); B = weight rows [1024][64] (box of 32 rows); D = dp1
+      if ((rc = make_act_map(&p->ma, a.A, 64, n_img, 64, 16, 12, S128))) return rc;
       if ((rc = make_map_ex(&p->mb, a.B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.G, 1024, 64, 64, a.b_gstride, 64, 32,
                             S128)))
         return rc;
@@ -554,7 +588,7 @@ static int plan_conv_maps(const fedhc_gemm_args& a, GemmPlan* p) {
   return FEDHC_OK;
 }
 
-template <int BM, int BN, bool A_MN, bool B_MN>
+template <int BM, int BN, bool A_MN, bool B_MN, int WIN = 0>
 static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   int rc = A_MN ? make_map(&p->ma, a.A, a.G, a.K, a.M, 64, a.a_gstride)
                  : make_map(&p->ma, a.A, a.G, a.M, a.K, BM, a.a_gstride);
@@ -582,15 +616,15 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   int nst = (a.K / BK <= 4 && !epi_loads(kind)) ? 8 : 2, stages = 0, fixed = 0;
   for (;; nst /= 2) {
     fixed = 1024 + epi_bytes<BM>(kind, nst) + 512;  // alignment slack + epilogue staging + barriers
-    stages = (max_smem - fixed) / Cfg<BM, BN>::kStageBytes;
+    stages = (max_smem - fixed) / Cfg<BM, BN, WIN>::kStageBytes;
     if (stages >= 3 || nst == 2) break;
   }
   if (stages > 8) stages = 8;
   if (stages < 2) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: tile does not fit shared memory");
   p->stages = stages;
   p->nst = nst;
-  p->smem = fixed + stages * Cfg<BM, BN>::kStageBytes;
-  auto kern = grouped_gemm_kernel<BM, BN, A_MN, B_MN>;
+  p->smem = fixed + stages * Cfg<BM, BN, WIN>::kStageBytes;
+  auto kern = grouped_gemm_kernel<BM, BN, A_MN, B_MN, WIN>;
   // plans of one kernel instance differ in smem (epilogue staging): allow the device maximum once
   FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   p->kern = reinterpret_cast<const void*>(kern);
@@ -600,6 +634,12 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
 
 template <int BM, int BN>
 static int plan_major(const fedhc_gemm_args& a, GemmPlan* p) {
+  if constexpr (BM == 128 && BN == 64) {
+    if (p->conv.mode == CONV_FWD) return plan_kernel<128, 64, false, true, 1>(a, p);
+  }
+  if constexpr (BM == 128 && BN == 32) {
+    if (p->conv.mode == CONV_DGRAD) return plan_kernel<128, 32, false, false, 2>(a, p);
+  }
   if constexpr (BN >= 64) {
     if (a.a_mn && a.b_mn) return plan_kernel<BM, BN, true, true>(a, p);
     if (a.b_mn) return plan_kernel<BM, BN, false, true>(a, p);
