@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // Named barriers (producer arrive / consumer sync, 448 + 32 threads each):
 //   1 ZFULL, 2 ZFREE, 3 + (i & 1) EFULL.
 // ============================================================================
-constexpr int kPWarps = 14, kPThreads = 16 * 32, kPStages = 3;
+constexpr int kPWarps = 14, kPThreads = 16 * 32, kPStages = 4;
 constexpr int kPSoft = 15, kPProd = 14;
 
 struct PipeGeom {
@@ -462,15 +462,45 @@ static bool plan_pipe(int F, int C, int max_smem, PipeGeom& g) {
   g.Es = 20;  // 5 x 16 B per row: conflict-free 128-bit row accesses by 8 consecutive rows
   g.Zs = 20;
   int off = 0;
-  g.off_master = off; off = a16(off + kPWarps * kFK8 * 32 * 16);
+  g.off_master = off;  // the fp32 master W lives in TMEM (train_pipe_kernel), not in shared memory
   g.off_x = off;      off = a16(off + kPStages * kFRows * g.Fs * 4);
   g.off_zp = off;     off = a16(off + kPWarps * kFRows * g.Zs * 4);
   g.off_e = off;      off = a16(off + 2 * kFRows * g.Es * 4);
   g.off_lab = off;    off = a16(off + kPStages * kFRows * 4);
   g.off_bar = off;    off = a16(off + 2 * kPStages * 8);
-  g.off_bias = off;   off = a16(off + 16 * 4);
+  g.off_bias = off;   off = a16(off + 16 * 4 + 16);  // + the TMEM base address slot
   g.bytes = off;
   return off <= max_smem;
+}
+
+// fp32 master W in tensor memory: compute warp w owns TMEM lanes 32 (w % 4) .. + 31 (its hardware lane
+// quadrant) and columns 32 (w / 4) .. + 31; lane l keeps its 7 float4 master fragments (28 values) there.
+// Moving W out of shared memory frees room for a 4th X stage (deeper TMA prefetch of the row gather).
+__device__ __forceinline__ void tmem_st28(uint32_t taddr, const float4 (&m)[kFK8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(m[0].x), "f"(m[0].y), "f"(m[0].z), "f"(m[0].w), "f"(m[1].x), "f"(m[1].y), "f"(m[1].z), "f"(m[1].w),
+      "f"(m[2].x), "f"(m[2].y), "f"(m[2].z), "f"(m[2].w), "f"(m[3].x), "f"(m[3].y), "f"(m[3].z), "f"(m[3].w),
+      "f"(m[4].x), "f"(m[4].y), "f"(m[4].z), "f"(m[4].w), "f"(m[5].x), "f"(m[5].y), "f"(m[5].z), "f"(m[5].w),
+      "f"(m[6].x), "f"(m[6].y), "f"(m[6].z), "f"(m[6].w), "f"(0.f), "f"(0.f), "f"(0.f), "f"(0.f)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld28(uint32_t taddr, float4 (&m)[kFK8]) {
+  float d0, d1, d2, d3;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=f"(m[0].x), "=f"(m[0].y), "=f"(m[0].z), "=f"(m[0].w), "=f"(m[1].x), "=f"(m[1].y), "=f"(m[1].z),
+        "=f"(m[1].w), "=f"(m[2].x), "=f"(m[2].y), "=f"(m[2].z), "=f"(m[2].w), "=f"(m[3].x), "=f"(m[3].y),
+        "=f"(m[3].z), "=f"(m[3].w), "=f"(m[4].x), "=f"(m[4].y), "=f"(m[4].z), "=f"(m[4].w), "=f"(m[5].x),
+        "=f"(m[5].y), "=f"(m[5].z), "=f"(m[5].w), "=f"(m[6].x), "=f"(m[6].y), "=f"(m[6].z), "=f"(m[6].w),
+        "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3)
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -480,7 +510,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
     train_pipe_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const int F,
                       const int C, const PipeGeom g) {
   extern __shared__ __align__(128) unsigned char smem[];
-  float4* master = reinterpret_cast<float4*>(smem + g.off_master);
   float* Xb = reinterpret_cast<float*>(smem + g.off_x);
   float* Zp = reinterpret_cast<float*>(smem + g.off_zp);
   float* Eb = reinterpret_cast<float*>(smem + g.off_e);  // [2][16][Es]
@@ -488,6 +517,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.off_bar);
   uint64_t* empty = full + kPStages;
   float* bias_out = reinterpret_cast<float*>(smem + g.off_bias);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + g.off_bias + 16 * 4);
   constexpr int S = kPStages, NCOMP = kPWarps * 32 + 32;  // barrier participants: compute + softmax warp
   const int Fs = g.Fs, Es = g.Es, Zs = g.Zs;
   const fedhc_client cl = clients[blockIdx.x];
@@ -509,16 +539,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int steps = n > 0 ? cl.n_batches : 0;
   auto w_at = [&](int f, int c) -> float { return c < C ? static_cast<float>(params[(size_t)f * C + c]) : 0.f; };
 
+  if (warp == 0) {  // 128 TMEM columns: 4 warps per lane quadrant x 32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_w = *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + 32 * (warp >> 2);
+
   uint32_t wh[kFK8][2], wm[kFK8][2];
   if (warp < kPWarps) {
+    float4 m0[kFK8];
 #pragma unroll
     for (int j = 0; j < kFK8; ++j) {
       const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
       const float4 m = make_float4(w_at(f0, gq), w_at(f0 + 1, gq), w_at(f0, gq + 8), w_at(f0 + 1, gq + 8));
-      master[(warp * kFK8 + j) * 32 + lane] = m;
+      m0[j] = m;
       split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
       split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
     }
+    tmem_st28(tmem_w, m0);
   }
   __syncthreads();
 
@@ -721,20 +762,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
         st = (st + 1 == S) ? 0 : st + 1;
       }
       if (prev_k >= 0) backward(prev_k, prev_st);
-      // ---- end of batch: thread-local SGD step on the master + re-split ----
+      // ---- end of batch: thread-local SGD step on the master (TMEM) + re-split ----
+      float4 m[kFK8];
+      tmem_ld28(tmem_w, m);
 #pragma unroll
       for (int j = 0; j < kFK8; ++j) {
-        float4& mref = master[(warp * kFK8 + j) * 32 + lane];
-        float4 m = mref;
-        m.x -= lr * G[j][0];
-        m.y -= lr * G[j][1];
-        m.z -= lr * G[j][2];
-        m.w -= lr * G[j][3];
-        mref = m;
-        split_bf16x2(m.x, m.y, wh[j][0], wm[j][0]);
-        split_bf16x2(m.z, m.w, wh[j][1], wm[j][1]);
+        m[j].x -= lr * G[j][0];
+        m[j].y -= lr * G[j][1];
+        m[j].z -= lr * G[j][2];
+        m[j].w -= lr * G[j][3];
+        split_bf16x2(m[j].x, m[j].y, wh[j][0], wm[j][0]);
+        split_bf16x2(m[j].z, m[j].w, wh[j][1], wm[j][1]);
         G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
       }
+      tmem_st28(tmem_w, m);
     }
     named_sync(2, NCOMP);  // match the softmax warp's last ZFREE arrival
   }
@@ -743,9 +784,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // ---- epilogue: delta = W_final - W_initial ----
   float* out = cl.delta;
   if (warp < kPWarps) {
+    float4 mf[kFK8];
+    tmem_ld28(tmem_w, mf);
 #pragma unroll
     for (int j = 0; j < kFK8; ++j) {
-      const float4 m = master[(warp * kFK8 + j) * 32 + lane];
+      const float4 m = mf[j];
       const int f0 = 8 * (warp * kFK8 + j) + 2 * tq;
       const float v[4] = {m.x, m.y, m.z, m.w};
       const int fo[4] = {f0, f0 + 1, f0, f0 + 1};
@@ -760,6 +803,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   if (tid < C) out[FC + tid] = (steps > 0 ? bias_out[tid] : static_cast<float>(params[FC + tid])) -
                                static_cast<float>(params[FC + tid]);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tmem_slot));
+  }
 }
 
 template <bool FULL, int CL>
