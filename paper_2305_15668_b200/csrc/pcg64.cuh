@@ -87,7 +87,21 @@ struct Pcg64 {
     state += initstate;
     step();
   }
-  FEDHC_HD inline void step() { state = state * FEDHC_PCG_MULT + inc; }
+  FEDHC_HD inline void step() {
+#ifdef __CUDA_ARCH__
+    // 128-bit LCG step from four 64-bit products (the generic u128 multiply compiles to a longer chain)
+    constexpr uint64_t MH = 0x2360ED051FC65DA4ull, ML = 0x4385DF649FCCF645ull;
+    const uint64_t lo = static_cast<uint64_t>(state), hi = static_cast<uint64_t>(state >> 64);
+    const uint64_t ilo = static_cast<uint64_t>(inc), ihi = static_cast<uint64_t>(inc >> 64);
+    const uint64_t p_lo = lo * ML;
+    uint64_t p_hi = __umul64hi(lo, ML) + hi * ML + lo * MH;
+    const uint64_t n_lo = p_lo + ilo;
+    p_hi += ihi + (n_lo < p_lo ? 1ull : 0ull);
+    state = (static_cast<u128>(p_hi) << 64) | n_lo;
+#else
+    state = state * FEDHC_PCG_MULT + inc;
+#endif
+  }
   FEDHC_HD inline uint64_t next64() {
     step();
     const uint64_t x = static_cast<uint64_t>(state >> 64) ^ static_cast<uint64_t>(state);

@@ -336,6 +336,7 @@ class RoundPlan:
     desc: np.ndarray                 # CLIENT_DTYPE records (delta + perm pointers filled)
     meta_bytes: int = 0              # device-plan mode: packed (seed, rows, perms, offset) bytes
     max_rows: int = 0
+    plan_launched: bool = False      # its [H2D + permutations] graph is already queued
 
 
 class FederatedRunner:
@@ -500,6 +501,8 @@ class FederatedRunner:
             desc["batch_size"] = self._c_bs[mi]
             desc["lr"] = self.lr
             desc["delta"] = self.deltas.data_ptr() + np.arange(k, dtype=np.int64) * (self.deltas.stride(0) * 4)
+            if meta_bytes:  # device-plan staging block [meta | descriptors | coefficients] complete
+                self._stage_pin[slot].numpy()[meta_bytes:meta_bytes + k * CLIENT_DTYPE.itemsize] = desc.view(np.uint8)
         t4 = time.perf_counter()
         hs = self.host_s
         hs["select+des"] += t1 - tick
@@ -539,6 +542,24 @@ class FederatedRunner:
             self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
         self._graphs[slot] = (self._graph_key(p), gp, gr)
 
+    def _graph_ready(self, p: RoundPlan) -> bool:
+        gs = self._graphs[p.slot]
+        return bool(self.use_graphs and p.participants and p.meta_bytes and gs is not None
+                    and gs[0] == self._graph_key(p))
+
+    def launch_plan(self, p: RoundPlan) -> None:
+        """Queue the round's [H2D + device permutations] graph on the plan stream (no-op without graphs).
+
+        run() calls this for round r+1 before launching round r's training, so the permutations of the
+        next round are generated on the SMs the current round leaves idle."""
+        if p.plan_launched or not self._graph_ready(p):
+            return
+        ps = self._plan_stream
+        with torch.cuda.stream(ps):
+            self._graphs[p.slot][1].replay()
+            self._ev_plan[p.slot].record(ps)
+        p.plan_launched = True
+
     def launch(self, p: RoundPlan) -> None:
         """Enqueue the round on the current stream (asynchronous); result lands in slot p.slot."""
         from .sharding import all_reduce_count, combine_partials
@@ -548,14 +569,10 @@ class FederatedRunner:
         slot = p.slot
         main = torch.cuda.current_stream()
         nb = k * CLIENT_DTYPE.itemsize
-        gs = self._graphs[slot]
-        if self.use_graphs and k and p.meta_bytes and gs is not None and gs[0] == self._graph_key(p):
-            mb = p.meta_bytes
-            self._stage_pin[slot].numpy()[mb:mb + nb] = p.desc.view(np.uint8)   # (coefficients: plan())
-            ps = self._plan_stream
-            with torch.cuda.stream(ps):
-                gs[1].replay()
-                self._ev_plan[slot].record(ps)
+        if self._graph_ready(p):
+            if not p.plan_launched:
+                self.launch_plan(p)
+            gs = self._graphs[slot]
             main.wait_event(self._ev_plan[slot])
             self._plan_done[slot] = self._ev_plan[slot]
             gs[2].replay()
@@ -563,9 +580,10 @@ class FederatedRunner:
             self._train_done[slot] = self._ev_train[slot]
             self._ev_result[slot].record()
             self._result_ev[slot] = self._ev_result[slot]
-            self.h2d_bytes = mb + nb + 8 * k
+            self.h2d_bytes = p.meta_bytes + nb + 8 * k
             self.host_s["launch"] += time.perf_counter() - tick
             return
+        gs = self._graphs[slot]
         if p.meta_bytes:
             # one H2D transfer of [meta | descriptors | coefficients] on the plan stream, then the
             # device PCG64 permutations; the main stream waits for both
@@ -663,11 +681,19 @@ class FederatedRunner:
 
         th = threading.Thread(target=planner, daemon=True)
         th.start()
-        series, pending = [], None
-        for _ in range(rounds):
-            p = ready.get()
+        series, pending, nxt = [], None, None
+        for i in range(rounds):
+            p = nxt if nxt is not None else ready.get()
+            nxt = None
             if p is None:
                 raise failure[0]
+            if i + 1 < rounds:
+                try:                       # next round already planned: queue its permutations now so they
+                    nxt = ready.get_nowait()  # overlap this round's training (never wait for the planner)
+                except queue.Empty:
+                    nxt = None
+                if nxt is not None:
+                    self.launch_plan(nxt)
             self.launch(p)
             if pending is not None:   # read the previous round while this one runs
                 series.append(self._finish(pending, n_test, on_round, free))
