@@ -52,8 +52,11 @@ extern "C" int fedhc_batch_permutations_device(const uint64_t* seeds, const int3
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int smem_rows = max_rows * 4 <= max_smem ? max_rows : 0;  // larger shards permute in global memory
   const int smem = smem_rows * 4;
-  if (smem > 48 * 1024)
+  static int smem_set = 48 * 1024;  // raise the opt-in only when needed (keeps launches graph-capturable)
+  if (smem > smem_set) {
     FEDHC_CUDA_TRY(cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set = smem;
+  }
   perm_kernel<<<n_clients, kPermThreads, smem, static_cast<cudaStream_t>(stream)>>>(seeds, n_rows, n_perms, offsets,
                                                                                    out, smem_rows);
   FEDHC_CUDA_TRY(cudaGetLastError());

@@ -550,8 +550,8 @@ class FederatedRunner:
     def launch_plan(self, p: RoundPlan) -> None:
         """Queue the round's [H2D + device permutations] graph on the plan stream (no-op without graphs).
 
-        run() calls this for round r+1 before launching round r's training, so the permutations of the
-        next round are generated on the SMs the current round leaves idle."""
+        The planner thread calls this as soon as a round is planned, so its permutations are generated
+        on the SMs the running round leaves idle."""
         if p.plan_launched or not self._graph_ready(p):
             return
         ps = self._plan_stream
@@ -673,6 +673,9 @@ class FederatedRunner:
                 for i in range(rounds):
                     slot = free.get()
                     pl = self.plan(r0 + i, t, slot)
+                    # queue the round's [H2D + device permutations] graph right away, so the batch
+                    # order is generated on the SMs the running round leaves idle
+                    self.launch_plan(pl)
                     t = pl.t0 + pl.report.makespan
                     ready.put(pl)
             except BaseException as exc:  # surface planner errors in the caller
@@ -681,22 +684,19 @@ class FederatedRunner:
 
         th = threading.Thread(target=planner, daemon=True)
         th.start()
-        series, pending, nxt = [], None, None
-        for i in range(rounds):
-            p = nxt if nxt is not None else ready.get()
-            nxt = None
+        series, pending = [], None
+        hs = self.host_s
+        for _ in range(rounds):
+            t0 = time.perf_counter()
+            p = ready.get()
+            hs["wait_plan"] = hs.get("wait_plan", 0.0) + time.perf_counter() - t0
             if p is None:
                 raise failure[0]
-            if i + 1 < rounds:
-                try:                       # next round already planned: queue its permutations now so they
-                    nxt = ready.get_nowait()  # overlap this round's training (never wait for the planner)
-                except queue.Empty:
-                    nxt = None
-                if nxt is not None:
-                    self.launch_plan(nxt)
             self.launch(p)
             if pending is not None:   # read the previous round while this one runs
+                t0 = time.perf_counter()
                 series.append(self._finish(pending, n_test, on_round, free))
+                hs["wait_gpu"] = hs.get("wait_gpu", 0.0) + time.perf_counter() - t0
             pending = p
         series.append(self._finish(pending, n_test, on_round, free))
         th.join()
