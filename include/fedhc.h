@@ -305,6 +305,15 @@ int fedhc_cnn_eval(void* ws, const double* params, const float* x, const int32_t
 int fedhc_cnn_conv2(int mode, int G, int bp, const void* act, const void* act2, const void* w, const float* bias,
                     void* out, float lr, void* stream);
 
+/* ---- ResNet client models (config 3, builder-defined) ---------------------- */
+/* One k x k (1 or 3) 'same' convolution layer of G clients x bp images as an implicit tcgen05 GEMM
+ * over 4-D TMA boxes; NHWC bf16 maps, channels multiple of 64, output width <= 32.
+ * mode 4 forward: out = conv(x, w) (bf16 [G*bp][H/s][W/s][cout]); mode 5 data gradient (s = 1):
+ * out = conv^T(dy, w) (bf16 [G*bp][H][W][cin]); mode 6 weight gradient + SGD: out = fp32 master
+ * [G][k*k*cin][cout] -= lr * grad (bf16 shadow updated when non-NULL).  w bf16 [G][k*k*cin][cout]. */
+int fedhc_nhwc_conv(int mode, int G, int bp, int H, int W, int cin, int cout, int k, int s, const void* x,
+                    const void* dy, const void* w, void* out, void* shadow, float lr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

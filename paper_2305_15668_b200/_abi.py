@@ -151,6 +151,7 @@ SIGNATURES = {
     "fedhc_cnn_last_loss": (_i, [_vp, _vp, _i, _vp]),
     "fedhc_cnn_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "fedhc_cnn_conv2": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.c_float, _vp]),
+    "fedhc_nhwc_conv": (_i, [_i] * 9 + [_vp, _vp, _vp, _vp, _vp, C.c_float, _vp]),
 }
 
 

@@ -217,6 +217,57 @@ __device__ __forceinline__ void conv_loads(const ConvSpec& cv, uint32_t sa, uint
   }
 }
 
+// ---- generic NHWC implicit-GEMM loads (ResNet layers) -------------------------------------------
+// M tile (FWD / DGRAD) = ib images x hb rows x wo columns = 128 output pixel slots; a K block = one tap x
+// 64 input channels.  WGRAD: K block = 64 output pixels (kib x khb x wo), M = tap * cin + channel.
+__device__ __forceinline__ void nhwc_tile_origin(const ConvSpec& cv, int g, int mt, int& img0, int& y0) {
+  if (cv.ib > 1) {
+    img0 = g * cv.bp + mt * cv.ib;
+    y0 = 0;
+  } else {
+    const int tpi = cv.ho / cv.hb;  // tiles per image
+    img0 = g * cv.bp + mt / tpi;
+    y0 = (mt % tpi) * cv.hb;
+  }
+}
+
+template <int BM, int BN>
+__device__ __forceinline__ void nhwc_loads(const ConvSpec& cv, uint32_t sa, uint32_t sb, const CUtensorMap* map_a,
+                                           const CUtensorMap* map_b, uint64_t* bar, int g, int m0, int n0, int kb) {
+  const int pad = cv.k >> 1;
+  if (cv.mode == NHWC_FWD || cv.mode == NHWC_DGRAD) {
+    int img0, y0;
+    nhwc_tile_origin(cv, g, m0 / BM, img0, y0);
+    const int cblocks = (cv.mode == NHWC_FWD ? cv.cin : cv.cout) >> 6;
+    const int tap = kb / cblocks, cb = kb - tap * cblocks, kh = tap / cv.k, kw = tap - kh * cv.k;
+    if (cv.mode == NHWC_FWD) {
+      tma_load_4d(sa, map_a, bar, cb * 64, kw - pad, y0 * cv.s + kh - pad, img0);
+#pragma unroll
+      for (int h = 0; h < BN / 64; ++h) tma_load_3d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, kb * BK, g);
+    } else {  // data gradient (stride 1): flipped taps, weights [tap][cin][cout] as K-major rows
+      tma_load_4d(sa, map_a, bar, cb * 64, pad - kw, y0 + pad - kh, img0);
+      tma_load_3d(sb, map_b, bar, cb * 64, tap * cv.cin + n0, g);
+    }
+  } else {  // NHWC_WGRAD
+    int img0, y0;
+    if (cv.kib > 1) {
+      img0 = g * cv.bp + kb * cv.kib;
+      y0 = 0;
+    } else {
+      const int bpi = cv.ho / cv.khb;
+      img0 = g * cv.bp + kb / bpi;
+      y0 = (kb % bpi) * cv.khb;
+    }
+#pragma unroll
+    for (int h = 0; h < BM / 64; ++h) {
+      const int m = m0 + 64 * h, tap = m / cv.cin, c = m - tap * cv.cin, kh = tap / cv.k, kw = tap - kh * cv.k;
+      tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, c, kw - pad, y0 * cv.s + kh - pad, img0);
+    }
+#pragma unroll
+    for (int h = 0; h < BN / 64; ++h) tma_load_4d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, 0, y0, img0);
+  }
+}
+
 template <int BM, int BN, bool A_MN, bool B_MN, int WIN = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -306,6 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
             }
+          } else if (WIN == 0 && conv.mode >= NHWC_FWD) {
+            nhwc_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
           } else if (WIN == 0) {
             conv_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
           } else {
@@ -473,6 +526,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // output rows = pixel slots (y0 + row / 16, row % 16) of an NHWC 14x14 map; TMA clips x, y >= 14
             const int mt = m0 / BM;
             tma_store_4d(&map_o, smem_u32(sb), c0, 0, (mt & 1) * 8 + 2 * q, g * conv.bp + (mt >> 1));
+          } else if (conv.mode == NHWC_FWD || conv.mode == NHWC_DGRAD) {
+            // rows 32q .. 32q + 31 of the (ib, hb, wo) tile: a {32 ch, wo, rows, images} box
+            int img0, y0;
+            nhwc_tile_origin(conv, g, m0 / BM, img0, y0);
+            const int r0 = 32 * q, per_img = conv.hb * conv.wo;
+            tma_store_4d(&map_o, smem_u32(sb), c0, 0, y0 + (r0 % per_img) / conv.wo, img0 + r0 / per_img);
           } else {
             tma_store_3d(&map_o, smem_u32(sb), c0, c1, g);
           }
@@ -566,8 +625,48 @@ static int make_act_map(CUtensorMap* map, const void* base, int C, int64_t n_img
   return FEDHC_OK;
 }
 
+// NHWC map [images][H][W][C] bf16 -> {C, W, H, images}, box {bc, bw, bh, bi}, traversal strides {1, s, s, 1}
+static int make_nhwc_map(CUtensorMap* map, const void* base, int C, int W, int H, int64_t n_img, int bc, int bw,
+                         int bh, int bi, int s, CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FEDHC_ERR_UNSUPPORTED, "gemm: cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) & 15) return fail(FEDHC_ERR_VALUE, "gemm: tensors must be 16-byte aligned");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n_img};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * W * 2, (cuuint64_t)C * W * H * 2};
+  cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)(bw * s), (cuuint32_t)(bh * s), (cuuint32_t)bi};
+  cuuint32_t estr[4] = {1, (cuuint32_t)s, (cuuint32_t)s, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FEDHC_ERR_CUDA, "gemm: cuTensorMapEncodeTiled (NHWC) failed (" + std::to_string(r) + ")");
+  return FEDHC_OK;
+}
+
 // operand / output maps of the implicit-GEMM convolution modes (replace the generic ones)
 static int plan_conv_maps(const fedhc_gemm_args& a, GemmPlan* p) {
+  const ConvSpec& c = p->conv;
+  if (c.mode >= NHWC_FWD) {
+    const int64_t n = (int64_t)a.G * c.bp;
+    const CUtensorMapSwizzle S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
+    const int rs = c.hb < 32 / c.wo ? c.hb : (32 / c.wo > 0 ? 32 / c.wo : 1);  // store box rows per warp
+    const int is = 32 / (c.wo * rs) > 0 ? 32 / (c.wo * rs) : 1;
+    int rc;
+    if (c.mode == NHWC_FWD) {
+      if ((rc = make_nhwc_map(&p->ma, a.A, c.cin, c.W, c.H, n, 64, c.wo, c.hb, c.ib, c.s, S128))) return rc;
+      return make_nhwc_map(&p->mo, a.D, c.cout, c.wo, c.ho, n, 32, c.wo, rs, is, 1, S64);
+    }
+    if (c.mode == NHWC_DGRAD) {  // A = dL/dY (H x W x cout, stride-1 geometry), D = dL/dX (H x W x cin)
+      if ((rc = make_nhwc_map(&p->ma, a.A, c.cout, c.W, c.H, n, 64, c.wo, c.hb, c.ib, 1, S128))) return rc;
+      if ((rc = make_map_ex(&p->mb, a.B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.G, c.k * c.k * c.cin, c.cout, c.cout,
+                            a.b_gstride, 64, p->N >= 256 && p->N % 256 == 0 ? 256 : p->N % 128 == 0 ? 128 : 64,
+                            S128)))
+        return rc;
+      return make_nhwc_map(&p->mo, a.D, c.cin, c.W, c.H, n, 32, c.wo, rs, is, 1, S64);
+    }
+    // NHWC_WGRAD: A = X (strided 64-pixel blocks), B = dL/dY (64-pixel blocks)
+    if ((rc = make_nhwc_map(&p->ma, a.A, c.cin, c.W, c.H, n, 64, c.wo, c.khb, c.kib, c.s, S128))) return rc;
+    return make_nhwc_map(&p->mb, a.B, c.cout, c.wo, c.ho, n, 64, c.wo, c.khb, c.kib, 1, S128);
+  }
   const int64_t n_img = (int64_t)a.G * p->conv.bp;
   const CUtensorMapSwizzle S128 = CU_TENSOR_MAP_SWIZZLE_128B, S64 = CU_TENSOR_MAP_SWIZZLE_64B;
   int rc;
@@ -661,7 +760,32 @@ static int plan_n(const fedhc_gemm_args& a, GemmPlan* p) {
 int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p, const ConvSpec* conv) {
   if (a.G < 1 || a.M < 1 || a.N < 1 || a.K < 1) return fail(FEDHC_ERR_VALUE, "gemm: empty problem");
   p->conv = conv ? *conv : ConvSpec{CONV_NONE, 0};
-  if (p->conv.mode != CONV_NONE) {
+  if (p->conv.mode >= NHWC_FWD) {
+    ConvSpec& c = p->conv;
+    const bool geo = c.bp > 0 && (c.k == 1 || c.k == 3) && (c.s == 1 || c.s == 2) && c.cin % 64 == 0 &&
+                     c.cout % 64 == 0 && c.H % c.s == 0 && c.W % c.s == 0 && c.W / c.s <= 32 &&
+                     !(c.mode == NHWC_DGRAD && c.s != 1);
+    if (!geo) return fail(FEDHC_ERR_VALUE, "gemm: unsupported NHWC convolution geometry");
+    c.ho = c.H / c.s;
+    c.wo = c.W / c.s;
+    const int px = c.ho * c.wo;  // output pixels per image
+    c.hb = 128 / c.wo < c.ho ? 128 / c.wo : c.ho;
+    c.ib = 128 / (c.hb * c.wo);
+    c.khb = 64 / c.wo < c.ho ? 64 / c.wo : c.ho;
+    c.kib = 64 / (c.khb * c.wo);
+    const int64_t slots = (int64_t)c.bp * px;
+    const int kk = c.k * c.k;
+    bool ok = slots % 128 == 0 && c.hb * c.wo * c.ib == 128 && c.khb * c.wo * c.kib == 64 &&
+              c.ho % c.hb == 0 && (c.ib == 1 || c.bp % c.ib == 0) && (c.kib == 1 || c.bp % c.kib == 0) &&
+              c.ho % c.khb == 0;
+    if (c.mode == NHWC_FWD)
+      ok = ok && a.M == slots && a.N == c.cout && a.K == kk * c.cin && !a.a_mn && a.b_mn;
+    else if (c.mode == NHWC_DGRAD)
+      ok = ok && a.M == slots && a.N == c.cin && a.K == kk * c.cout && !a.a_mn && !a.b_mn;
+    else
+      ok = ok && a.M == kk * c.cin && a.N == c.cout && a.K == slots && a.a_mn && a.b_mn && a.epilogue == FEDHC_EPI_SGD;
+    if (!ok) return fail(FEDHC_ERR_VALUE, "gemm: inconsistent NHWC implicit-GEMM shape");
+  } else if (p->conv.mode != CONV_NONE) {
     const int bp = p->conv.bp;
     const int m = p->conv.mode;
     const bool ok = bp > 0 && a.M % 128 == 0 &&
@@ -693,6 +817,8 @@ int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p, const ConvSpec* conv) {
   p->M = a.M;
   p->N = a.N;
   p->K = a.K;
+  if ((p->conv.mode == NHWC_FWD || p->conv.mode == NHWC_DGRAD) && a.M % 128)
+    return fail(FEDHC_ERR_VALUE, "gemm: NHWC conv needs 128-row tiles");
   return a.M % 128 == 0 ? plan_n<128>(a, p) : plan_n<64>(a, p);
 }
 

@@ -26,11 +26,19 @@ struct Epilogue {
   float* rowsum;        // RELU_MASK_BF16 (optional, single N tile): rowsum[g*M + m] = sum_n D
 };
 
-// Implicit-GEMM convolution modes (CNN conv2: 5x5 'same' on 14x14 NHWC maps; see gemm_tc.cu conv_loads).
-enum { CONV_NONE = 0, CONV_FWD = 1, CONV_DGRAD = 2, CONV_WGRAD = 3 };
+// Implicit-GEMM convolution modes (see gemm_tc.cu conv_loads / nhwc_loads).
+//   CONV_FWD/DGRAD/WGRAD: the FEMNIST CNN's conv2 (5x5 'same' on 14x14 maps, channel-pair layout).
+//   NHWC_FWD/DGRAD/WGRAD: k x k (1 or 3) 'same' convolutions with stride s (1 or 2) on [img][H][W][C]
+//   bf16 maps, C multiple of 64 (ResNet client models).  DGRAD is stride 1 only: a stride-2 data gradient
+//   runs on the zero-upsampled output gradient.
+enum { CONV_NONE = 0, CONV_FWD = 1, CONV_DGRAD = 2, CONV_WGRAD = 3, NHWC_FWD = 4, NHWC_DGRAD = 5, NHWC_WGRAD = 6 };
 struct ConvSpec {
-  int mode;   // CONV_*
+  int mode;   // CONV_* / NHWC_*
   int bp;     // images per group
+  // NHWC_*: input map H x W x cin, kernel k, stride s, output (H / s) x (W / s) x cout
+  int H, W, cin, cout, k, s;
+  // derived (gemm_plan): 128-slot M tile = ib images x hb rows x wo columns; 64-slot WGRAD K block
+  int ho, wo, hb, ib, khb, kib;
 };
 
 struct GemmPlan {
