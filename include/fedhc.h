@@ -313,6 +313,20 @@ int fedhc_cnn_conv2(int mode, int G, int bp, const void* act, const void* act2, 
  * [G][k*k*cin][cout] -= lr * grad (bf16 shadow updated when non-NULL).  w bf16 [G][k*k*cin][cout]. */
 int fedhc_nhwc_conv(int mode, int G, int bp, int H, int W, int cin, int cout, int k, int s, const void* x,
                     const void* dy, const void* w, void* out, void* shadow, float lr, void* stream);
+/* CIFAR ResNet-18 client engine (same conventions as the CNN engine): padded parameter layout
+ * (fedhc_resnet_param_count / _offsets: torch state_dict order without num_batches_tracked), a workspace
+ * for max_clients x batch images (batch multiple of 8, <= 64), local SGD of n_clients clients from
+ * `params` (rows = NHWC fp32 [32][32][3]; batch norm in training mode, running statistics updated and
+ * part of the delta), and accuracy with running statistics. */
+int fedhc_resnet_param_count(int n_classes, int64_t* padded);
+int fedhc_resnet_param_offsets(int n_classes, int64_t* offsets, int cap, int* count);
+int fedhc_resnet_create(int max_clients, int batch, int n_classes, void** ws);
+int fedhc_resnet_destroy(void* ws);
+int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, int n_clients, const double* params,
+                             int max_steps, float lr, int use_graph, void* stream);
+int fedhc_resnet_last_loss(void* ws, float* out, int n_clients, void* stream);
+int fedhc_resnet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                      unsigned long long* correct, void* stream);
 
 #ifdef __cplusplus
 }

@@ -152,6 +152,13 @@ SIGNATURES = {
     "fedhc_cnn_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "fedhc_cnn_conv2": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.c_float, _vp]),
     "fedhc_nhwc_conv": (_i, [_i] * 9 + [_vp, _vp, _vp, _vp, _vp, C.c_float, _vp]),
+    "fedhc_resnet_param_count": (_i, [_i, _vp]),
+    "fedhc_resnet_param_offsets": (_i, [_i, _vp, _i, _vp]),
+    "fedhc_resnet_create": (_i, [_i, _i, _i, _vp]),
+    "fedhc_resnet_destroy": (_i, [_vp]),
+    "fedhc_resnet_local_train": (_i, [_vp, _vp, _i, _vp, _i, C.c_float, _i, _vp]),
+    "fedhc_resnet_last_loss": (_i, [_vp, _vp, _i, _vp]),
+    "fedhc_resnet_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
 }
 
 

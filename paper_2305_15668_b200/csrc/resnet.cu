@@ -51,3 +51,1005 @@ extern "C" int fedhc_nhwc_conv(int mode, int G, int bp, int H, int W, int cin, i
   if (rc) return rc;
   return tc::gemm_run(p, static_cast<cudaStream_t>(stream));
 }
+
+// ==========================================================================================
+// CIFAR ResNet-18 client engine (32x32x3 inputs, 3x3 stem without max-pool, BasicBlocks 64-128-256-512,
+// batch-norm in training mode, global average pool, linear classifier).  All K clients of a round run
+// one SGD step in lock step; every convolution (forward, data gradient, weight gradient + SGD) of every
+// client is one grouped tcgen05 implicit GEMM; batch norm, ReLU, residual adds, pooling and the
+// classifier are vectorised NHWC kernels.  Local loop = fl_core.local_train (fl_core.py:163-194): the
+// PCG64 batch order, ceil(num_samples / B) steps, delta = new - old (fp32 master, bf16 shadow for the
+// tensor cores).  The step sequence of a round is captured into a CUDA graph.
+// ==========================================================================================
+#include <cmath>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+namespace fedhc {
+namespace rn {
+
+constexpr int IMG = 32, IMG_C = 3, IMG_F = IMG * IMG * IMG_C;  // input rows: NHWC fp32 [32][32][3]
+constexpr int NB = 8;                                          // BasicBlocks
+constexpr int MAXC = 512, NCMAX = 64;
+constexpr int BN_SPLIT = 16;                                   // row splits of the BN reductions
+constexpr float BN_EPS = 1e-5f, BN_MOM = 0.1f;
+
+struct BlockDef {
+  int cin, cout, s, H;  // H: input map size
+};
+constexpr BlockDef kBlocks[NB] = {{64, 64, 1, 32},   {64, 64, 1, 32},   {64, 128, 2, 32}, {128, 128, 1, 16},
+                                  {128, 256, 2, 16}, {256, 256, 1, 8}, {256, 512, 2, 8}, {512, 512, 1, 4}};
+
+struct BnOff {
+  int C;
+  int64_t gamma, beta, rmean, rvar;
+};
+
+// parameter layout (fp32 master / bf16 shadow, elements; every block 64-aligned), torch state_dict order
+struct Layout {
+  int64_t stem_w;  // [64 rows: (kh*3 + kw)*3 + c, 27 real][64]
+  BnOff bn0;
+  int64_t c1[NB], c2[NB], cs[NB];  // [k*k*cin][cout]; cs = -1 without projection
+  BnOff bn1[NB], bn2[NB], bns[NB];
+  int64_t fc_w, fc_b;  // [nc][512], [nc]
+  int64_t P;
+  int nc;
+};
+
+static int64_t al64(int64_t v) { return (v + 63) / 64 * 64; }
+
+static Layout make_layout(int nc) {
+  Layout L{};
+  L.nc = nc;
+  int64_t off = 0;
+  auto bn = [&](int C) {
+    BnOff b{C, 0, 0, 0, 0};
+    b.gamma = off; off = al64(off + C);
+    b.beta = off; off = al64(off + C);
+    b.rmean = off; off = al64(off + C);
+    b.rvar = off; off = al64(off + C);
+    return b;
+  };
+  L.stem_w = off; off = al64(off + 64 * 64);
+  L.bn0 = bn(64);
+  for (int i = 0; i < NB; ++i) {
+    const BlockDef& d = kBlocks[i];
+    L.c1[i] = off; off = al64(off + (int64_t)9 * d.cin * d.cout);
+    L.bn1[i] = bn(d.cout);
+    L.c2[i] = off; off = al64(off + (int64_t)9 * d.cout * d.cout);
+    L.bn2[i] = bn(d.cout);
+    if (d.s != 1 || d.cin != d.cout) {
+      L.cs[i] = off; off = al64(off + (int64_t)d.cin * d.cout);
+      L.bns[i] = bn(d.cout);
+    } else {
+      L.cs[i] = -1;
+    }
+  }
+  L.fc_w = off; off = al64(off + (int64_t)nc * 512);
+  L.fc_b = off; off = al64(off + NCMAX);
+  L.P = off;
+  return L;
+}
+
+__device__ __forceinline__ float bf(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ---- stem im2col: gather the batch rows (PCG64 order) -> cols [n][1024][64] bf16 ------------------
+// column (kh*3 + kw)*3 + c, 27 real taps; rows past the client's batch are zero images.
+__global__ void __launch_bounds__(256) stem_im2col_kernel(const fedhc_client* __restrict__ cl, int step, int Bp,
+                                                          __nv_bfloat16* __restrict__ cols,
+                                                          int32_t* __restrict__ labels, int32_t* __restrict__ valid) {
+  __shared__ float img[34][34][3];
+  const int g = blockIdx.y, b = blockIdx.x;
+  const fedhc_client c = cl[g];
+  int rows = 0;
+  int64_t poff = 0;
+  if (c.n_rows > 0 && step < c.n_batches) {
+    if (c.perm) {
+      const BatchRef r = batch_ref(step, c.n_rows, c.batch_size);
+      rows = r.rows;
+      poff = r.perm_off;
+    } else {
+      rows = c.n_rows < Bp ? c.n_rows : Bp;
+    }
+  }
+  const bool ok = b < rows;
+  const int row = ok ? (c.perm ? c.perm[poff + b] : b) : 0;
+  const float* src = c.x + (int64_t)row * IMG_F;
+  const int64_t im = (int64_t)g * Bp + b;
+  for (int i = threadIdx.x; i < 34 * 34 * 3; i += 256) (&img[0][0][0])[i] = 0.f;
+  if (threadIdx.x == 0) {
+    labels[im] = ok ? c.y[row] : 0;
+    if (b == 0) valid[g] = rows;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < IMG_F; i += 256) {
+    const int p = i / 3, ch = i - p * 3;
+    img[1 + p / IMG][1 + p % IMG][ch] = ok ? bf(__float2bfloat16_rn(__ldg(src + i))) : 0.f;
+  }
+  __syncthreads();
+  __nv_bfloat16* dst = cols + im * 1024 * 64;
+  for (int i = threadIdx.x; i < 1024 * 8; i += 256) {  // 8 x 16 B per pixel row
+    const int p = i >> 3, q = i & 7, y = p / IMG, x = p % IMG;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = q * 8 + e;
+      float f = 0.f;
+      if (k < 27) {
+        const int t = k / 3, ch = k - t * 3;
+        f = img[y + t / 3][x + t % 3][ch];
+      }
+      v[e] = __float2bfloat16_rn(f);
+    }
+    *reinterpret_cast<uint4*>(dst + (int64_t)p * 64 + q * 8) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+// ---- batch norm (training mode statistics over the client's valid images) -------------------------
+// x [G*Bp][HW][C] bf16.  part [G][BN_SPLIT][C][2] fp32 (sum, sum of squares) or (sum dz, sum dz*xhat).
+// grid (C/64, G, BN_SPLIT), 256 threads = 64 channels x 4 row lanes.
+template <bool BWD>
+__global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                                                         const __nv_bfloat16* __restrict__ dz,
+                                                         const float* __restrict__ stats,  // BWD: [G][C][2]
+                                                         const int32_t* __restrict__ valid, int Bp, int HW, int C,
+                                                         float* __restrict__ part) {
+  __shared__ float red[4][64][2];
+  const int c = blockIdx.x * 64 + (threadIdx.x & 63), rl = threadIdx.x >> 6, g = blockIdx.y, sp = blockIdx.z;
+  const int64_t nr = (int64_t)valid[g] * HW;
+  const int64_t r0 = nr * sp / BN_SPLIT, r1 = nr * (sp + 1) / BN_SPLIT;
+  const int64_t base = (int64_t)g * Bp * HW;
+  float mean = 0.f, rstd = 0.f;
+  if (BWD) {
+    mean = stats[((int64_t)g * C + c) * 2];
+    rstd = stats[((int64_t)g * C + c) * 2 + 1];
+  }
+  float s0 = 0.f, s1 = 0.f;
+  for (int64_t r = r0 + rl; r < r1; r += 4) {
+    const float v = bf(x[(base + r) * C + c]);
+    if (BWD) {
+      const float d = bf(dz[(base + r) * C + c]);
+      s0 += d;
+      s1 += d * (v - mean) * rstd;
+    } else {
+      s0 += v;
+      s1 += v * v;
+    }
+  }
+  red[rl][threadIdx.x & 63][0] = s0;
+  red[rl][threadIdx.x & 63][1] = s1;
+  __syncthreads();
+  if (rl == 0) {
+    const int t = threadIdx.x & 63;
+    float* o = part + (((int64_t)g * BN_SPLIT + sp) * C + c) * 2;
+    o[0] = (red[0][t][0] + red[1][t][0]) + (red[2][t][0] + red[3][t][0]);
+    o[1] = (red[0][t][1] + red[1][t][1]) + (red[2][t][1] + red[3][t][1]);
+  }
+}
+
+// forward: stats [G][C] = (mean, rstd); running statistics updated (momentum 0.1, unbiased variance).
+// backward: gsum [G][C][2] = (dbeta = sum dz, dgamma = sum dz * xhat).   grid G, block C.
+template <bool BWD>
+__global__ void bn_finalize_kernel(const float* __restrict__ part, const int32_t* __restrict__ valid, int HW, int C,
+                                   float* __restrict__ out, float* __restrict__ master, int64_t pstride,
+                                   int64_t rm_off, int64_t rv_off) {
+  const int g = blockIdx.x, c = threadIdx.x;
+  if (c >= C) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int sp = 0; sp < BN_SPLIT; ++sp) {
+    const float* p = part + (((int64_t)g * BN_SPLIT + sp) * C + c) * 2;
+    s0 += p[0];
+    s1 += p[1];
+  }
+  float* o = out + ((int64_t)g * C + c) * 2;
+  if (BWD) {
+    o[0] = (float)s0;
+    o[1] = (float)s1;
+    return;
+  }
+  const double n = (double)valid[g] * HW;
+  if (n <= 0) {
+    o[0] = 0.f;
+    o[1] = 1.f;
+    return;
+  }
+  const double mean = s0 / n, var = fmax(s1 / n - mean * mean, 0.0);
+  o[0] = (float)mean;
+  o[1] = (float)(1.0 / sqrt(var + (double)BN_EPS));
+  float* m = master + (int64_t)g * pstride;
+  m[rm_off + c] = (1.f - BN_MOM) * m[rm_off + c] + BN_MOM * (float)mean;
+  m[rv_off + c] = (1.f - BN_MOM) * m[rv_off + c] + BN_MOM * (float)(n > 1 ? var * n / (n - 1) : var);
+}
+
+// y = relu?(gamma (x - mean) rstd + beta [+ res | + bn_s(xs)]), 8 channels per thread.
+// eval: running statistics (master rmean / rvar) instead of batch statistics.
+struct BnApply {
+  const __nv_bfloat16 *x, *res, *xs;
+  const float *stats, *stats_s;
+  int64_t gamma, beta, rmean, rvar, gamma_s, beta_s, rmean_s, rvar_s;  // master offsets
+  int relu, eval;
+};
+
+__global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* __restrict__ master, int64_t pstride,
+                                                       int Bp, int HW, int C, int64_t total8,
+                                                       __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = i * 8;
+    const int c0 = (int)(e0 % C);
+    const int g = (int)(e0 / ((int64_t)Bp * HW * C));
+    const float* m = master + (int64_t)g * pstride;
+    const uint4 xv = *reinterpret_cast<const uint4*>(a.x + e0);
+    uint4 rv = make_uint4(0, 0, 0, 0), sv = make_uint4(0, 0, 0, 0);
+    if (a.res) rv = *reinterpret_cast<const uint4*>(a.res + e0);
+    if (a.xs) sv = *reinterpret_cast<const uint4*>(a.xs + e0);
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = c0 + e;
+      float mean, rstd;
+      if (a.eval) {
+        mean = m[a.rmean + c];
+        rstd = rsqrtf(m[a.rvar + c] + BN_EPS);
+      } else {
+        mean = a.stats[((int64_t)g * C + c) * 2];
+        rstd = a.stats[((int64_t)g * C + c) * 2 + 1];
+      }
+      float v = (bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) - mean) * rstd * m[a.gamma + c] + m[a.beta + c];
+      if (a.res) v += bf(reinterpret_cast<const __nv_bfloat16*>(&rv)[e]);
+      if (a.xs) {
+        float ms, rs;
+        if (a.eval) {
+          ms = m[a.rmean_s + c];
+          rs = rsqrtf(m[a.rvar_s + c] + BN_EPS);
+        } else {
+          ms = a.stats_s[((int64_t)g * C + c) * 2];
+          rs = a.stats_s[((int64_t)g * C + c) * 2 + 1];
+        }
+        v += (bf(reinterpret_cast<const __nv_bfloat16*>(&sv)[e]) - ms) * rs * m[a.gamma_s + c] + m[a.beta_s + c];
+      }
+      if (a.relu) v = fmaxf(v, 0.f);
+      o[e] = __float2bfloat16_rn(v);
+    }
+    *reinterpret_cast<uint4*>(out + e0) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
+// dx = gamma rstd (dz - (dbeta + xhat dgamma) / n) on the valid images, 0 on padding images.
+__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dz,
+                                                           const __nv_bfloat16* __restrict__ x,
+                                                           const float* __restrict__ stats,
+                                                           const float* __restrict__ gsum,
+                                                           const float* __restrict__ master, int64_t pstride,
+                                                           int64_t gamma_off, const int32_t* __restrict__ valid,
+                                                           int Bp, int HW, int C, int64_t total8,
+                                                           __nv_bfloat16* __restrict__ dx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = i * 8;
+    const int c0 = (int)(e0 % C);
+    const int64_t img = e0 / ((int64_t)HW * C);
+    const int g = (int)(img / Bp), b = (int)(img % Bp);
+    __align__(16) __nv_bfloat16 o[8];
+    if (b >= valid[g]) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = __float2bfloat16_rn(0.f);
+    } else {
+      const float n = (float)valid[g] * HW;
+      const uint4 dv = *reinterpret_cast<const uint4*>(dz + e0), xv = *reinterpret_cast<const uint4*>(x + e0);
+      const float* m = master + (int64_t)g * pstride;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int c = c0 + e;
+        const float mean = stats[((int64_t)g * C + c) * 2], rstd = stats[((int64_t)g * C + c) * 2 + 1];
+        const float db = gsum[((int64_t)g * C + c) * 2], dg = gsum[((int64_t)g * C + c) * 2 + 1];
+        const float xh = (bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) - mean) * rstd;
+        const float d = bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]);
+        o[e] = __float2bfloat16_rn(m[gamma_off + c] * rstd * (d - (db + xh * dg) / n));
+      }
+    }
+    *reinterpret_cast<uint4*>(dx + e0) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
+// elementwise helpers (8 bf16 per thread): out = a * (mask > 0) ; out += b ; zero-upsample by 2
+__global__ void __launch_bounds__(256) relu_mask_kernel(const __nv_bfloat16* __restrict__ a,
+                                                        const __nv_bfloat16* __restrict__ mask, int64_t total8,
+                                                        __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 av = reinterpret_cast<const uint4*>(a)[i], mv = reinterpret_cast<const uint4*>(mask)[i];
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      o[e] = bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f ? reinterpret_cast<const __nv_bfloat16*>(&av)[e]
+                                                                      : __float2bfloat16_rn(0.f);
+    reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
+__global__ void __launch_bounds__(256) add_kernel(__nv_bfloat16* __restrict__ acc, const __nv_bfloat16* __restrict__ b,
+                                                  int64_t total8) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 av = reinterpret_cast<const uint4*>(acc)[i], bv = reinterpret_cast<const uint4*>(b)[i];
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      o[e] = __float2bfloat16_rn(bf(reinterpret_cast<const __nv_bfloat16*>(&av)[e]) +
+                                 bf(reinterpret_cast<const __nv_bfloat16*>(&bv)[e]));
+    reinterpret_cast<uint4*>(acc)[i] = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
+// in [n][h][w][C] -> out [n][2h][2w][C], values at even (y, x), zeros elsewhere
+__global__ void __launch_bounds__(256) upsample2_kernel(const __nv_bfloat16* __restrict__ in, int64_t n, int h, int w,
+                                                        int C, __nv_bfloat16* __restrict__ out) {
+  const int64_t total8 = n * 4 * h * w * C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = i * 8;
+    const int c0 = (int)(e0 % C);
+    int64_t p = e0 / C;
+    const int x = (int)(p % (2 * w));
+    p /= 2 * w;
+    const int y = (int)(p % (2 * h));
+    const int64_t img = p / (2 * h);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (!(x & 1) && !(y & 1)) v = *reinterpret_cast<const uint4*>(in + ((img * h + y / 2) * w + x / 2) * C + c0);
+    reinterpret_cast<uint4*>(out)[i] = v;
+  }
+}
+
+// global average pool: y [n][16][512] bf16 -> p [n][512] fp32
+__global__ void __launch_bounds__(256) avgpool_kernel(const __nv_bfloat16* __restrict__ y, int64_t n,
+                                                      float* __restrict__ p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * MAXC; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = i / MAXC;
+    const int c = (int)(i % MAXC);
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s += bf(y[(img * 16 + q) * MAXC + c]);
+    p[i] = s * (1.f / 16.f);
+  }
+}
+
+// classifier + softmax cross-entropy + its SGD step, one CTA per client (fp32):
+// logits = p W^T + b; dl = (softmax - onehot) / valid; dY4 (avg-pool backward, bf16) = (dl W) / 16
+// broadcast over the 4x4 map; W -= lr dl^T p; b -= lr sum dl.  Dynamic smem: p [Bp][512] + dl [Bp][64].
+__global__ void __launch_bounds__(256) fc_ce_kernel(const float* __restrict__ pooled, const int32_t* __restrict__ labels,
+                                                    const int32_t* __restrict__ valid, float* __restrict__ master,
+                                                    __nv_bfloat16* __restrict__ shadow, int64_t pstride,
+                                                    int64_t fcw, int64_t fcb, int nc, int Bp, float lr,
+                                                    __nv_bfloat16* __restrict__ dy4, float* __restrict__ loss) {
+  extern __shared__ float fsm[];
+  float* P = fsm;                   // [Bp][512]
+  float* D = fsm + Bp * MAXC;       // [Bp][NCMAX] logits -> dl
+  const int g = blockIdx.x, rows = valid[g];
+  float* m = master + (int64_t)g * pstride;
+  const float* W = m + fcw;
+  for (int i = threadIdx.x; i < Bp * MAXC; i += blockDim.x) P[i] = pooled[(int64_t)g * Bp * MAXC + i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < Bp * nc; i += blockDim.x) {
+    const int r = i / nc, c = i - r * nc;
+    float s = m[fcb + c];
+    for (int k = 0; k < MAXC; ++k) s += P[r * MAXC + k] * W[c * MAXC + k];
+    D[r * NCMAX + c] = s;
+  }
+  __syncthreads();
+  __shared__ float lsum[256];
+  float li = 0.f;
+  for (int r = threadIdx.x; r < Bp; r += blockDim.x) {
+    float* z = D + r * NCMAX;
+    if (r >= rows) {
+      for (int c = 0; c < nc; ++c) z[c] = 0.f;
+      continue;
+    }
+    float mx = -INFINITY;
+    for (int c = 0; c < nc; ++c) mx = fmaxf(mx, z[c]);
+    float sum = 0.f;
+    for (int c = 0; c < nc; ++c) sum += expf(z[c] - mx);
+    const int y = labels[(int64_t)g * Bp + r];
+    li += -(z[y] - mx - logf(sum));
+    for (int c = 0; c < nc; ++c) z[c] = (expf(z[c] - mx) / sum - (c == y ? 1.f : 0.f)) / (float)rows;
+  }
+  lsum[threadIdx.x] = li;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss) {
+    float s = 0.f;
+    for (int t = 0; t < (int)blockDim.x; ++t) s += lsum[t];
+    loss[g] = rows ? s / rows : 0.f;
+  }
+  // dY4 = (dl W) / 16, broadcast to the 16 pixels (W before its update)
+  for (int i = threadIdx.x; i < Bp * MAXC; i += blockDim.x) {
+    const int r = i / MAXC, k = i - r * MAXC;
+    float s = 0.f;
+    for (int c = 0; c < nc; ++c) s += D[r * NCMAX + c] * W[c * MAXC + k];
+    const __nv_bfloat16 v = __float2bfloat16_rn(s * (1.f / 16.f));
+    __nv_bfloat16* o = dy4 + ((int64_t)g * Bp + r) * 16 * MAXC + k;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) o[q * MAXC] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc * MAXC; i += blockDim.x) {
+    const int c = i / MAXC, k = i - c * MAXC;
+    float s = 0.f;
+    for (int r = 0; r < Bp; ++r) s += D[r * NCMAX + c] * P[r * MAXC + k];
+    m[fcw + i] -= lr * s;
+  }
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < Bp; ++r) s += D[r * NCMAX + c];
+    m[fcb + c] -= lr * s;
+  }
+}
+
+// eval: logits of n rows with the client-0 classifier; correct += first-max argmax == label
+__global__ void fc_eval_kernel(const float* __restrict__ pooled, const float* __restrict__ master, int64_t fcw,
+                               int64_t fcb, int nc, int n, const int32_t* __restrict__ labels,
+                               unsigned long long* __restrict__ correct) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int hit = 0;
+  if (i < n) {
+    const float* p = pooled + (int64_t)i * MAXC;
+    int best = 0;
+    float bv = -INFINITY;
+    for (int c = 0; c < nc; ++c) {
+      float s = master[fcb + c];
+      for (int k = 0; k < MAXC; ++k) s += p[k] * master[fcw + (int64_t)c * MAXC + k];
+      if (s > bv) {
+        bv = s;
+        best = c;
+      }
+    }
+    hit = best == labels[i];
+  }
+  const unsigned msk = __ballot_sync(0xffffffffu, hit);
+  if ((threadIdx.x & 31) == 0 && msk) atomicAdd(correct, (unsigned long long)__popc(msk));
+}
+
+// batch-norm affine parameters: gamma -= lr dgamma, beta -= lr dbeta for every BN layer of every client
+struct BnSgdTable {
+  int n;
+  int C[2 * NB + 8];
+  int64_t gamma[2 * NB + 8], beta[2 * NB + 8], gs_off[2 * NB + 8];
+};
+
+__global__ void bn_sgd_kernel(BnSgdTable t, float* __restrict__ master, int64_t pstride,
+                              const float* __restrict__ gsum, float lr) {
+  const int g = blockIdx.y, l = blockIdx.x;
+  if (l >= t.n) return;
+  float* m = master + (int64_t)g * pstride;
+  const float* gs = gsum + t.gs_off[l] + (int64_t)g * t.C[l] * 2;
+  for (int c = threadIdx.x; c < t.C[l]; c += blockDim.x) {
+    m[t.beta[l] + c] -= lr * gs[c * 2];
+    m[t.gamma[l] + c] -= lr * gs[c * 2 + 1];
+  }
+}
+
+__global__ void bcast_kernel(const double* __restrict__ params, float* __restrict__ master,
+                             __nv_bfloat16* __restrict__ shadow, int64_t P, int G) {
+  const int64_t total = (int64_t)G * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = (float)params[i % P];
+    master[i] = v;
+    shadow[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void delta_kernel(const fedhc_client* __restrict__ cl, const double* __restrict__ params,
+                             const float* __restrict__ master, int64_t P) {
+  const int g = blockIdx.y;
+  float* out = cl[g].delta;
+  const float* m = master + (int64_t)g * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = m[i] - (float)params[i];
+}
+
+struct Buf {
+  void* p = nullptr;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct BlockPlans {
+  tc::GemmPlan c1f, c2f, csf, c1d, c2d, csd, c1w, c2w, csw;
+};
+
+struct Engine {
+  int maxG, Bp, nc;
+  Layout L;
+  std::vector<std::unique_ptr<Buf>> bufs;
+  float *master, *pooled, *part, *stats, *gsum, *loss;
+  __nv_bfloat16 *shadow, *cols0, *c0, *a0, *dy4;
+  __nv_bfloat16 *c1[NB], *a1[NB], *c2[NB], *cs[NB], *y[NB];
+  __nv_bfloat16 *g0, *g1, *g2, *g3, *up;  // backward scratch (max per-image tensor each)
+  int32_t *labels, *valid;
+  fedhc_client* desc;
+  unsigned long long* correct;
+  // stats / gsum slots: BN layer index -> offset (floats) of its [maxG][C][2] block
+  int64_t st_off[2 * NB + 8];
+  int64_t st_stride;  // total floats
+  int bn_count;
+  int planned_G = -1;
+  float planned_lr = 0.f;
+  tc::GemmPlan stem_f, stem_w;
+  BlockPlans bp[NB];
+  tc::GemmPlan e_stem_f;
+  BlockPlans ebp[NB];
+  cudaGraphExec_t graph = nullptr;
+  std::tuple<int, int, float> graph_key{-1, -1, 0.f};
+  BnSgdTable bnt{};
+
+  ~Engine() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
+
+  template <typename T>
+  int alloc(T** out, size_t n) {
+    auto b = std::make_unique<Buf>();
+    FEDHC_CUDA_TRY(cudaMalloc(&b->p, n * sizeof(T) + 256));
+    FEDHC_CUDA_TRY(cudaMemset(b->p, 0, n * sizeof(T) + 256));
+    *out = static_cast<T*>(b->p);
+    bufs.push_back(std::move(b));
+    return FEDHC_OK;
+  }
+
+  // BN layer ids: 0 stem, 1 + 3i (bn1), 2 + 3i (bn2), 3 + 3i (bns)
+  int init() {
+    L = make_layout(nc);
+    int64_t off = 0;  // layer-major slots: [layer][maxG][C][2]
+    auto slot = [&](int id, int C) {
+      st_off[id] = off;
+      off += (int64_t)maxG * C * 2;
+    };
+    slot(0, 64);
+    for (int i = 0; i < NB; ++i) {
+      slot(1 + 3 * i, kBlocks[i].cout);
+      slot(2 + 3 * i, kBlocks[i].cout);
+      slot(3 + 3 * i, kBlocks[i].cout);
+    }
+    st_stride = off;
+    bn_count = 1 + 3 * NB;
+    const size_t G = maxG, I = (size_t)maxG * Bp;
+    int rc = 0;
+    rc |= alloc(&master, G * L.P);
+    rc |= alloc(&shadow, G * L.P);
+    rc |= alloc(&cols0, I * 1024 * 64);
+    rc |= alloc(&c0, I * 1024 * 64);
+    rc |= alloc(&a0, I * 1024 * 64);
+    for (int i = 0; i < NB; ++i) {
+      const int ho = kBlocks[i].H / kBlocks[i].s;
+      const size_t sz = I * ho * ho * kBlocks[i].cout;
+      rc |= alloc(&c1[i], sz);
+      rc |= alloc(&a1[i], sz);
+      rc |= alloc(&c2[i], sz);
+      rc |= alloc(&y[i], sz);
+      cs[i] = nullptr;
+      if (L.cs[i] >= 0) rc |= alloc(&cs[i], sz);
+    }
+    const size_t scratch = I * 32 * 32 * 128;  // largest per-image tensor: the 32x32x128 upsampled gradient
+    rc |= alloc(&g0, scratch);
+    rc |= alloc(&g1, scratch);
+    rc |= alloc(&g2, scratch);
+    rc |= alloc(&g3, scratch);
+    rc |= alloc(&up, scratch);
+    rc |= alloc(&dy4, I * 16 * MAXC);
+    rc |= alloc(&pooled, I * MAXC);
+    rc |= alloc(&part, G * BN_SPLIT * MAXC * 2);
+    rc |= alloc(&stats, st_stride);
+    rc |= alloc(&gsum, st_stride);
+    rc |= alloc(&loss, G);
+    rc |= alloc(&labels, I);
+    rc |= alloc(&valid, G);
+    rc |= alloc(&desc, G);
+    rc |= alloc(&correct, 1);
+    if (rc) return fail(FEDHC_ERR_CUDA, "resnet: workspace allocation failed");
+    // BN SGD table (trained affine parameters of every BN layer)
+    int n = 0;
+    auto add = [&](const BnOff& b, int id) {
+      bnt.C[n] = b.C;
+      bnt.gamma[n] = b.gamma;
+      bnt.beta[n] = b.beta;
+      bnt.gs_off[n] = st_off[id];
+      ++n;
+    };
+    add(L.bn0, 0);
+    for (int i = 0; i < NB; ++i) {
+      add(L.bn1[i], 1 + 3 * i);
+      add(L.bn2[i], 2 + 3 * i);
+      if (L.cs[i] >= 0) add(L.bns[i], 3 + 3 * i);
+    }
+    bnt.n = n;
+    return plan_forward(1, maxG * Bp, &e_stem_f, ebp, false, 0.f);
+  }
+
+  static fedhc_gemm_args gargs(int G, int M, int N, int K, const void* A, bool a_mn, const void* B, bool b_mn,
+                               int64_t bgs, int epi) {
+    fedhc_gemm_args a{};
+    a.G = G;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.A = A;
+    a.a_mn = a_mn;
+    a.B = B;
+    a.b_mn = b_mn;
+    a.b_gstride = bgs;
+    a.epilogue = epi;
+    return a;
+  }
+
+  static tc::ConvSpec spec(int mode, int bp, int H, int cin, int cout, int k, int s) {
+    tc::ConvSpec c{};
+    c.mode = mode;
+    c.bp = bp;
+    c.H = H;
+    c.W = H;
+    c.cin = cin;
+    c.cout = cout;
+    c.k = k;
+    c.s = s;
+    return c;
+  }
+
+  int conv_fwd_plan(int G, int bp, const __nv_bfloat16* x, int64_t woff, __nv_bfloat16* out, int H, int cin,
+                    int cout, int k, int s, tc::GemmPlan* p) {
+    const int ho = H / s;
+    auto a = gargs(G, bp * ho * ho, cout, k * k * cin, x, false, shadow + woff, true, L.P, FEDHC_EPI_BF16);
+    a.D = out;
+    const tc::ConvSpec cs_ = spec(tc::NHWC_FWD, bp, H, cin, cout, k, s);
+    return tc::gemm_plan(a, p, &cs_);
+  }
+
+  int plan_forward(int G, int bp, tc::GemmPlan* sf, BlockPlans* bps, bool train, float lr) {
+    int rc;
+    // stem: c0 [bp*1024][64] = cols0 . Wstem (MN-major [64 taps][64])
+    auto a = gargs(G, bp * 1024, 64, 64, cols0, false, shadow + L.stem_w, true, L.P, FEDHC_EPI_BF16);
+    a.D = c0;
+    if ((rc = tc::gemm_plan(a, sf))) return rc;
+    for (int i = 0; i < NB; ++i) {
+      const BlockDef& d = kBlocks[i];
+      const __nv_bfloat16* x = i ? y[i - 1] : a0;
+      const int ho = d.H / d.s;
+      if ((rc = conv_fwd_plan(G, bp, x, L.c1[i], c1[i], d.H, d.cin, d.cout, 3, d.s, &bps[i].c1f))) return rc;
+      if ((rc = conv_fwd_plan(G, bp, a1[i], L.c2[i], c2[i], ho, d.cout, d.cout, 3, 1, &bps[i].c2f))) return rc;
+      if (L.cs[i] >= 0 &&
+          (rc = conv_fwd_plan(G, bp, x, L.cs[i], cs[i], d.H, d.cin, d.cout, 1, d.s, &bps[i].csf)))
+        return rc;
+      if (!train) continue;
+      // data gradients (stride 1 geometry at the input resolution; stride-2 layers read the upsampled grad)
+      // c2: dA1 (g1) = conv^T(dC2 (g0), W2)
+      a = gargs(G, bp * ho * ho, d.cout, 9 * d.cout, g0, false, shadow + L.c2[i], false, L.P, FEDHC_EPI_BF16);
+      a.D = g1;
+      tc::ConvSpec c = spec(tc::NHWC_DGRAD, bp, ho, d.cout, d.cout, 3, 1);
+      if ((rc = tc::gemm_plan(a, &bps[i].c2d, &c))) return rc;
+      // c1: dX (g2) = conv^T(dC1 (s1: g0 ; s2: up), W1)
+      a = gargs(G, bp * d.H * d.H, d.cin, 9 * d.cout, d.s == 1 ? g0 : up, false, shadow + L.c1[i], false, L.P,
+                FEDHC_EPI_BF16);
+      a.D = g2;
+      c = spec(tc::NHWC_DGRAD, bp, d.H, d.cin, d.cout, 3, 1);
+      if ((rc = tc::gemm_plan(a, &bps[i].c1d, &c))) return rc;
+      if (L.cs[i] >= 0) {  // shortcut: dXs (g3) = conv1x1^T(upsampled dCS (up), Ws)
+        a = gargs(G, bp * d.H * d.H, d.cin, d.cout, up, false, shadow + L.cs[i], false, L.P, FEDHC_EPI_BF16);
+        a.D = g3;
+        c = spec(tc::NHWC_DGRAD, bp, d.H, d.cin, d.cout, 1, 1);
+        if ((rc = tc::gemm_plan(a, &bps[i].csd, &c))) return rc;
+      }
+      // weight gradients + SGD
+      auto wg = [&](const __nv_bfloat16* xin, const __nv_bfloat16* dy, int64_t woff, int H, int cin, int cout, int k,
+                    int s, tc::GemmPlan* p) {
+        const int h2 = H / s;
+        auto w = gargs(G, k * k * cin, cout, bp * h2 * h2, xin, true, dy, true, 0, FEDHC_EPI_SGD);
+        w.master = master + woff;
+        w.shadow = shadow + woff;
+        w.d_gstride = L.P;
+        w.lr = lr;
+        tc::ConvSpec cw = spec(tc::NHWC_WGRAD, bp, H, cin, cout, k, s);
+        return tc::gemm_plan(w, p, &cw);
+      };
+      if ((rc = wg(a1[i], g0, L.c2[i], ho, d.cout, d.cout, 3, 1, &bps[i].c2w))) return rc;
+      if ((rc = wg(x, g0, L.c1[i], d.H, d.cin, d.cout, 3, d.s, &bps[i].c1w))) return rc;
+      if (L.cs[i] >= 0 && (rc = wg(x, g3, L.cs[i], d.H, d.cin, d.cout, 1, d.s, &bps[i].csw))) return rc;
+    }
+    if (train) {  // stem weight gradient: Wstem [64][64] -= lr cols0^T . dC0 (g0)
+      a = gargs(G, 64, 64, bp * 1024, cols0, true, g0, true, 0, FEDHC_EPI_SGD);
+      a.master = master + L.stem_w;
+      a.shadow = shadow + L.stem_w;
+      a.d_gstride = L.P;
+      a.lr = lr;
+      if ((rc = tc::gemm_plan(a, &stem_w))) return rc;
+    }
+    return FEDHC_OK;
+  }
+
+  int plan_train(int G, float lr) {
+    if (G == planned_G && lr == planned_lr) return FEDHC_OK;
+    int rc = plan_forward(G, Bp, &stem_f, bp, true, lr);
+    if (rc) return rc;
+    planned_G = G;
+    planned_lr = lr;
+    if (graph) {
+      cudaGraphExecDestroy(graph);
+      graph = nullptr;
+    }
+    graph_key = {-1, -1, 0.f};
+    return FEDHC_OK;
+  }
+
+  static int grid_for(int64_t work) {
+    const int64_t b = (work + 255) / 256;
+    return (int)(b < 148 * 16 ? b : 148 * 16);
+  }
+
+  // batch statistics of x [G*bp][HW][C] into stats slot `id`, running stats at (rm, rv)
+  void bn_stats(int G, int bp, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b, cudaStream_t st) {
+    bn_partial_kernel<false><<<dim3(C / 64, G, BN_SPLIT), 256, 0, st>>>(x, nullptr, nullptr, valid, bp, HW, C, part);
+    bn_finalize_kernel<false><<<G, C, 0, st>>>(part, valid, HW, C, stats + st_off[id], master, L.P, b.rmean,
+                                               b.rvar);
+  }
+
+  void bn_apply(int G, int bp, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b, const __nv_bfloat16* res,
+                const __nv_bfloat16* xs, int ids, const BnOff* bs, bool relu, bool eval, __nv_bfloat16* out,
+                cudaStream_t st) {
+    BnApply a{};
+    a.x = x;
+    a.res = res;
+    a.xs = xs;
+    a.stats = stats + st_off[id];
+    a.gamma = b.gamma;
+    a.beta = b.beta;
+    a.rmean = b.rmean;
+    a.rvar = b.rvar;
+    if (xs) {
+      a.stats_s = stats + st_off[ids];
+      a.gamma_s = bs->gamma;
+      a.beta_s = bs->beta;
+      a.rmean_s = bs->rmean;
+      a.rvar_s = bs->rvar;
+    }
+    a.relu = relu;
+    a.eval = eval;
+    const int64_t total8 = (int64_t)G * bp * HW * C / 8;
+    bn_apply_kernel<<<grid_for(total8), 256, 0, st>>>(a, master, L.P, bp, HW, C, total8, out);
+  }
+
+  // dC = BN backward of dz through x (stats slot id), dgamma / dbeta into gsum slot id
+  void bn_backward(int G, const __nv_bfloat16* dz, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b,
+                   __nv_bfloat16* dc, cudaStream_t st) {
+    bn_partial_kernel<true><<<dim3(C / 64, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C,
+                                                                       part);
+    bn_finalize_kernel<true><<<G, C, 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
+    const int64_t total8 = (int64_t)G * Bp * HW * C / 8;
+    bn_bwd_apply_kernel<<<grid_for(total8), 256, 0, st>>>(dz, x, stats + st_off[id], gsum + st_off[id], master, L.P,
+                                                          b.gamma, valid, Bp, HW, C, total8, dc);
+  }
+
+  int forward(int G, int bp, int step, bool eval, const tc::GemmPlan& sf, const BlockPlans* bps, cudaStream_t st) {
+    int rc;
+    stem_im2col_kernel<<<dim3(bp, G), 256, 0, st>>>(desc, step, bp, cols0, labels, valid);
+    if ((rc = tc::gemm_run(sf, st))) return rc;
+    if (!eval) bn_stats(G, bp, c0, 1024, 64, 0, L.bn0, st);
+    bn_apply(G, bp, c0, 1024, 64, 0, L.bn0, nullptr, nullptr, 0, nullptr, true, eval, a0, st);
+    for (int i = 0; i < NB; ++i) {
+      const BlockDef& d = kBlocks[i];
+      const int ho = d.H / d.s, hw = ho * ho;
+      const __nv_bfloat16* x = i ? y[i - 1] : a0;
+      if ((rc = tc::gemm_run(bps[i].c1f, st))) return rc;
+      if (!eval) bn_stats(G, bp, c1[i], hw, d.cout, 1 + 3 * i, L.bn1[i], st);
+      bn_apply(G, bp, c1[i], hw, d.cout, 1 + 3 * i, L.bn1[i], nullptr, nullptr, 0, nullptr, true, eval, a1[i], st);
+      if ((rc = tc::gemm_run(bps[i].c2f, st))) return rc;
+      if (!eval) bn_stats(G, bp, c2[i], hw, d.cout, 2 + 3 * i, L.bn2[i], st);
+      if (L.cs[i] >= 0) {
+        if ((rc = tc::gemm_run(bps[i].csf, st))) return rc;
+        if (!eval) bn_stats(G, bp, cs[i], hw, d.cout, 3 + 3 * i, L.bns[i], st);
+        bn_apply(G, bp, c2[i], hw, d.cout, 2 + 3 * i, L.bn2[i], nullptr, cs[i], 3 + 3 * i, &L.bns[i], true, eval,
+                 y[i], st);
+      } else {
+        bn_apply(G, bp, c2[i], hw, d.cout, 2 + 3 * i, L.bn2[i], x, nullptr, 0, nullptr, true, eval, y[i], st);
+      }
+    }
+    const int64_t n = (int64_t)G * bp;
+    avgpool_kernel<<<grid_for(n * MAXC), 256, 0, st>>>(y[NB - 1], n, pooled);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
+  }
+
+  int train_step(int G, int step, float lr, cudaStream_t st) {
+    int rc = forward(G, Bp, step, false, stem_f, bp, st);
+    if (rc) return rc;
+    const size_t fsm = ((size_t)Bp * MAXC + (size_t)Bp * NCMAX) * 4;
+    fc_ce_kernel<<<G, 256, fsm, st>>>(pooled, labels, valid, master, shadow, L.P, L.fc_w, L.fc_b, nc, Bp, lr, dy4, loss);
+    const __nv_bfloat16* dy = dy4;  // gradient w.r.t. the current block output
+    for (int i = NB - 1; i >= 0; --i) {
+      const BlockDef& d = kBlocks[i];
+      const int ho = d.H / d.s, hw = ho * ho;
+      const int64_t n8o = (int64_t)G * Bp * hw * d.cout / 8, n8i = (int64_t)G * Bp * d.H * d.H * d.cin / 8;
+      // g3 <- dZ = dY (y > 0)   (g3 is free until the shortcut data gradient below)
+      __nv_bfloat16* dz = g3;
+      relu_mask_kernel<<<grid_for(n8o), 256, 0, st>>>(dy, y[i], n8o, dz);
+      bn_backward(G, dz, c2[i], hw, d.cout, 2 + 3 * i, L.bn2[i], g0, st);  // g0 = dC2
+      if ((rc = tc::gemm_run(bp[i].c2d, st))) return rc;                     // g1 = dA1
+      if ((rc = tc::gemm_run(bp[i].c2w, st))) return rc;                     // W2 SGD (a1, dC2)
+      relu_mask_kernel<<<grid_for(n8o), 256, 0, st>>>(g1, a1[i], n8o, g1);   // g1 = dZ1
+      bn_backward(G, g1, c1[i], hw, d.cout, 1 + 3 * i, L.bn1[i], g0, st);   // g0 = dC1
+      if (d.s == 1) {
+        if ((rc = tc::gemm_run(bp[i].c1d, st))) return rc;  // g2 = dX (from g0)
+      } else {
+        upsample2_kernel<<<grid_for(n8i / d.cin * d.cout), 256, 0, st>>>(g0, (int64_t)G * Bp, ho, ho, d.cout, up);
+        if ((rc = tc::gemm_run(bp[i].c1d, st))) return rc;  // g2 = dX (from up)
+      }
+      if ((rc = tc::gemm_run(bp[i].c1w, st))) return rc;  // W1 SGD (x, dC1 in g0)
+      if (L.cs[i] >= 0) {
+        // shortcut: dCS (g1) = bn_s backward of dZ (g3); upsample -> up; dXs -> g3; Ws SGD (x, dCS)
+        bn_backward(G, dz, cs[i], hw, d.cout, 3 + 3 * i, L.bns[i], g1, st);
+        upsample2_kernel<<<grid_for(n8i / d.cin * d.cout), 256, 0, st>>>(g1, (int64_t)G * Bp, ho, ho, d.cout, up);
+        // the shortcut weight-gradient plan reads dCS from g3 (dZ is dead by now)
+        FEDHC_CUDA_TRY(cudaMemcpyAsync(g3, g1, (size_t)G * Bp * hw * d.cout * 2, cudaMemcpyDeviceToDevice, st));
+        if ((rc = tc::gemm_run(bp[i].csw, st))) return rc;  // Ws SGD (x, dCS = g3)
+        if ((rc = tc::gemm_run(bp[i].csd, st))) return rc;  // g3 = dXs (from up)
+        add_kernel<<<grid_for(n8i), 256, 0, st>>>(g2, g3, n8i);
+      } else {
+        add_kernel<<<grid_for(n8i), 256, 0, st>>>(g2, dz, n8i);  // identity shortcut
+      }
+      // the next (earlier) block's output gradient: move g2 out of the scratch the next block reuses
+      const size_t bytes = (size_t)n8i * 16;
+      FEDHC_CUDA_TRY(cudaMemcpyAsync(up, g2, bytes, cudaMemcpyDeviceToDevice, st));
+      dy = up;
+    }
+    // stem: dZ0 = dY (a0 > 0); bn0 backward -> dC0 (g0); Wstem SGD
+    const int64_t n80 = (int64_t)G * Bp * 1024 * 64 / 8;
+    relu_mask_kernel<<<grid_for(n80), 256, 0, st>>>(dy, a0, n80, g1);
+    bn_backward(G, g1, c0, 1024, 64, 0, L.bn0, g0, st);
+    if ((rc = tc::gemm_run(stem_w, st))) return rc;
+    bn_sgd_kernel<<<dim3(bnt.n, G), 256, 0, st>>>(bnt, master, L.P, gsum, lr);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
+  }
+};
+
+}  // namespace rn
+}  // namespace fedhc
+
+extern "C" int fedhc_resnet_param_count(int n_classes, int64_t* padded) {
+  if (!padded || n_classes < 2 || n_classes > rn::NCMAX) return fail(FEDHC_ERR_VALUE, "resnet: bad arguments");
+  *padded = rn::make_layout(n_classes).P;
+  return FEDHC_OK;
+}
+
+// Padded offsets of the canonical tensors in torch state_dict order (without num_batches_tracked):
+// conv1.weight, bn1.{weight, bias, running_mean, running_var}, then per block conv1.weight, bn1.*,
+// conv2.weight, bn2.*, [shortcut.0.weight, shortcut.1.*], linear.weight, linear.bias.  Returns the count.
+extern "C" int fedhc_resnet_param_offsets(int n_classes, int64_t* offsets, int cap, int* count) {
+  if (!offsets || !count || n_classes < 2 || n_classes > rn::NCMAX) return fail(FEDHC_ERR_VALUE, "resnet: bad arguments");
+  const rn::Layout L = rn::make_layout(n_classes);
+  std::vector<int64_t> o;
+  auto bn = [&](const rn::BnOff& b) {
+    o.push_back(b.gamma);
+    o.push_back(b.beta);
+    o.push_back(b.rmean);
+    o.push_back(b.rvar);
+  };
+  o.push_back(L.stem_w);
+  bn(L.bn0);
+  for (int i = 0; i < rn::NB; ++i) {
+    o.push_back(L.c1[i]);
+    bn(L.bn1[i]);
+    o.push_back(L.c2[i]);
+    bn(L.bn2[i]);
+    if (L.cs[i] >= 0) {
+      o.push_back(L.cs[i]);
+      bn(L.bns[i]);
+    }
+  }
+  o.push_back(L.fc_w);
+  o.push_back(L.fc_b);
+  if ((int)o.size() > cap) return fail(FEDHC_ERR_VALUE, "resnet: offsets buffer too small");
+  for (size_t i = 0; i < o.size(); ++i) offsets[i] = o[i];
+  *count = (int)o.size();
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_resnet_create(int max_clients, int batch, int n_classes, void** out) {
+  if (!out) return fail(FEDHC_ERR_VALUE, "resnet: null output");
+  if (max_clients < 1 || batch < 8 || batch > 64 || batch % 8)
+    return fail(FEDHC_ERR_VALUE, "resnet: batch must be a multiple of 8 in [8, 64]");
+  if (n_classes < 2 || n_classes > rn::NCMAX) return fail(FEDHC_ERR_UNSUPPORTED, "resnet: n_classes must be in [2, 64]");
+  auto e = std::make_unique<rn::Engine>();
+  e->maxG = max_clients;
+  e->Bp = batch;
+  e->nc = n_classes;
+  const size_t fsm = ((size_t)batch * rn::MAXC + (size_t)batch * rn::NCMAX) * 4;
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(rn::fc_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+  int rc = e->init();
+  if (rc) return rc;
+  *out = e.release();
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_resnet_destroy(void* ws) {
+  delete static_cast<rn::Engine*>(ws);
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, int n_clients, const double* params,
+                                        int max_steps, float lr, int use_graph, void* stream) {
+  auto* e = static_cast<rn::Engine*>(ws);
+  if (!e || (!clients && n_clients) || !params) return fail(FEDHC_ERR_VALUE, "resnet: null argument");
+  if (n_clients < 0 || n_clients > e->maxG) return fail(FEDHC_ERR_VALUE, "resnet: too many clients for the workspace");
+  if (max_steps < 0) return fail(FEDHC_ERR_VALUE, "resnet: negative step count");
+  if (n_clients == 0) return FEDHC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = n_clients;
+  int rc = e->plan_train(G, lr);
+  if (rc) return rc;
+  FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, clients, sizeof(fedhc_client) * G, cudaMemcpyDeviceToDevice, st));
+  rn::bcast_kernel<<<rn::Engine::grid_for((int64_t)G * e->L.P), 256, 0, st>>>(params, e->master, e->shadow, e->L.P, G);
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  if (use_graph) {
+    const auto key = std::make_tuple(G, max_steps, lr);
+    if (!e->graph || e->graph_key != key) {
+      if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+      }
+      cudaStream_t cap;
+      FEDHC_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t g = nullptr;
+      FEDHC_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+      for (int s = 0; s < max_steps && !rc; ++s) rc = e->train_step(G, s, lr, cap);
+      cudaError_t ce = cudaStreamEndCapture(cap, &g);
+      cudaStreamDestroy(cap);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      FEDHC_CUDA_TRY(ce);
+      cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
+      cudaGraphDestroy(g);
+      FEDHC_CUDA_TRY(ie);
+      e->graph_key = key;
+    }
+    FEDHC_CUDA_TRY(cudaGraphLaunch(e->graph, st));
+  } else {
+    for (int s = 0; s < max_steps; ++s)
+      if ((rc = e->train_step(G, s, lr, st))) return rc;
+  }
+  rn::delta_kernel<<<dim3(64, G), 256, 0, st>>>(e->desc, params, e->master, e->L.P);
+  FEDHC_CUDA_TRY(cudaGetLastError());
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_resnet_last_loss(void* ws, float* out, int n_clients, void* stream) {
+  auto* e = static_cast<rn::Engine*>(ws);
+  if (!e || !out || n_clients > e->maxG) return fail(FEDHC_ERR_VALUE, "resnet: bad arguments");
+  FEDHC_CUDA_TRY(cudaMemcpyAsync(out, e->loss, sizeof(float) * n_clients, cudaMemcpyDeviceToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+  return FEDHC_OK;
+}
+
+// *correct (dev u64) += test rows whose first-max argmax == label (BN with running statistics)
+extern "C" int fedhc_resnet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                                 unsigned long long* correct, void* stream) {
+  auto* e = static_cast<rn::Engine*>(ws);
+  if (!e || !params || !correct || (n > 0 && (!x || !y))) return fail(FEDHC_ERR_VALUE, "resnet: null argument");
+  if (n <= 0) return FEDHC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int chunk = e->maxG * e->Bp;
+  rn::bcast_kernel<<<rn::Engine::grid_for(e->L.P), 256, 0, st>>>(params, e->master, e->shadow, e->L.P, 1);
+  for (int64_t at = 0; at < n; at += chunk) {
+    const int rows = (int)(n - at < chunk ? n - at : chunk);
+    fedhc_client c{};
+    c.x = x + at * rn::IMG_F;
+    c.y = y + at;
+    c.perm = nullptr;
+    c.n_rows = rows;
+    c.n_batches = 1;
+    c.batch_size = rows;
+    FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+    int rc = e->forward(1, chunk, 0, true, e->e_stem_f, e->ebp, st);
+    if (rc) return rc;
+    rn::fc_eval_kernel<<<(rows + 255) / 256, 256, 0, st>>>(e->pooled, e->master, e->L.fc_w, e->L.fc_b, e->nc, rows,
+                                                          e->labels, correct);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    FEDHC_CUDA_TRY(cudaStreamSynchronize(st));  // host descriptor reused next chunk
+  }
+  return FEDHC_OK;
+}
