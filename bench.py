@@ -52,11 +52,13 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["round", "cnn", "fedavg", "gemm", "des"], default="round",
+    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "fedavg", "gemm", "des"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
     ap.add_argument("--cnn-samples", type=int, default=6400, help="samples per client for --workload cnn")
+    ap.add_argument("--resnet-clients", type=int, default=25, help="ResNet-18 clients per GPU (config 3: 200 / 8)")
+    ap.add_argument("--resnet-samples", type=int, default=250, help="samples per ResNet-18 client")
     ap.add_argument("--classes", type=int, default=10, help="10 (digits) or 62 (FEMNIST classes, 4-CTA clusters)")
     return ap.parse_args()
 
@@ -775,6 +777,234 @@ def run_cnn(args, rank, world, local_rank):
     return res
 
 
+RESNET_FLOP_PER_SAMPLE = 3.329e9  # CIFAR ResNet-18 fwd + wgrad + dgrad (no stem dgrad), SURVEY §8a a14
+
+
+def resnet_flop_per_sample(n_classes: int) -> float:
+    """Algorithmic FLOPs of one training sample: 3 x forward convolutions minus the stem's data gradient."""
+    macs, stem = 0, 32 * 32 * 64 * 27
+    for ci, co, s, H in [(64, 64, 1, 32), (64, 64, 1, 32), (64, 128, 2, 32), (128, 128, 1, 16), (128, 256, 2, 16),
+                         (256, 256, 1, 8), (256, 512, 2, 8), (512, 512, 1, 4)]:
+        ho = H // s
+        macs += ho * ho * co * 9 * ci + ho * ho * co * 9 * co + (ho * ho * co * ci if (s != 1 or ci != co) else 0)
+    macs_fc = 512 * n_classes
+    return float(2 * (3 * (macs + macs_fc) + 2 * stem))
+
+
+def resnet_cpu_reference(seconds: float, n_classes: int, batch: int):
+    """ResNet-18 local SGD on the host cores (torch CPU, all threads): CPU restatement (no reference CNN)."""
+    import torch
+    import torch.nn as nn
+
+    from oracle.resnet import ResNet18
+    cores = len(os.sched_getaffinity(0))
+    torch.set_num_threads(cores)
+    torch.manual_seed(0)
+    model = ResNet18(n_classes)
+    model.train()
+    opt = torch.optim.SGD(model.parameters(), lr=0.05)
+    x = torch.randn(256, 3, 32, 32)
+    y = torch.randint(0, n_classes, (256,))
+    lossf = nn.CrossEntropyLoss()
+
+    def one(i):
+        s0 = (i * batch) % (256 - batch)
+        opt.zero_grad(set_to_none=True)
+        lossf(model(x[s0:s0 + batch]), y[s0:s0 + batch]).backward()
+        opt.step()
+
+    for i in range(2):
+        one(i)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        one(n)
+        n += 1
+    dt = time.perf_counter() - t0
+    return n / dt, cores, (f"{n} local SGD steps (B={batch}) of one ResNet-18 client, torch CPU fp32 with {cores} "
+                           f"threads (CPU restatement: the reference has no CNN)"), n, dt
+
+
+def run_resnet(args, rank, world, local_rank):
+    """BASELINE config 3 with its named model: CIFAR ResNet-18 clients, 200 participants per round sharded
+    over the GPUs (25 per GPU at 8 GPUs; --resnet-clients per GPU), 250 samples each, B = 32."""
+    import torch
+
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.experiment import delta_buffer
+    from paper_2305_15668_b200.resnet import ResnetFederation, init_resnet_params
+    from paper_2305_15668_b200.roundsim import RoundSimulator
+    from paper_2305_15668_b200.sharding import shard_bounds
+    from paper_2305_15668_b200.training import fedavg_device, stable_seed
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+    nc, n_samp, bs, lr = 10, args.resnet_samples, 32, 0.05
+    per_gpu = args.resnet_clients
+    n_part, n_fleet = per_gpu * world, (per_gpu + per_gpu // 4) * world
+    steps_per_client = math.ceil(n_samp / bs)
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=bs),
+                              n_fleet, 3)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    n_test = 2048
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 3072, nc, alpha=0.5, seed=4321,
+                           n_test=n_test)
+    lo, hi = shard_bounds(n_test, world, rank)
+    fed = ResnetFederation.from_arrays(data.x, data.y, data.offsets, data.x_test[lo:hi].contiguous(),
+                                       data.y_test[lo:hi].contiguous(), nc).attach_engine(per_gpu, bs)
+    P = fed.P
+    params = torch.tensor(fed.layout.to_padded(init_resnet_params(nc, 1)), dtype=torch.float64, device=dev)
+    deltas = delta_buffer(per_gpu, P, dev)
+    partial = torch.empty(P, dtype=torch.float64, device=dev)
+    one = torch.ones(1, dtype=torch.float64, device=dev)
+    cfg = fh.FleetConfig(theta=THETA, max_executors=EXECUTORS, participants_per_round=n_part, seed=3)
+    sim = RoundSimulator(by_id)
+    selector = random.Random(f"{cfg.seed}:selection")
+    total_rounds = args.warmup + args.steps
+
+    def plan_round(r, now):
+        who = selector.sample(ids, n_part)
+        rep, _ = sim.run(who, cfg, t0=now, round_index=r, want_trace=False)
+        mine = who[rank * per_gpu:(rank + 1) * per_gpu]
+        wl = [by_id[c].workload for c in mine]
+        seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
+        coef = torch.tensor([float(w.num_samples) / float(n_part * n_samp) for w in wl], dtype=torch.float64,
+                            device=dev)
+        return rep, mine, wl, seeds, coef
+
+    def aggregate(coef):
+        if world == 1:
+            fedavg_device(deltas, coef, params, params)
+        else:
+            fedavg_device(deltas, coef, None, partial)
+            dist.all_reduce(partial)
+            fedavg_device(partial.view(1, -1), one, params, params)
+
+    plans, now = [], 0.0
+    for r in range(total_rounds):
+        rep, mine, wl, seeds, coef = plan_round(r, now)
+        now += rep.makespan
+        packed, meta = fed.plan(mine, wl, seeds)
+        perm_dev = torch.from_numpy(packed).to(dev)
+        fed._perm_dev = perm_dev
+        desc = fed.descriptors(mine, meta, lr, deltas)
+        plans.append((perm_dev, desc, coef, max(m[2] for m in meta)))
+    counts = torch.zeros(total_rounds, dtype=torch.int64, device=dev)
+
+    def device_round(r):
+        _, desc, coef, steps = plans[r]
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps, lr, True)
+        ev1.record()
+        aggregate(coef)
+        fed.engine.correct_into(params, fed.x_test, fed.y_test, counts[r:r + 1])
+        if world > 1:
+            dist.all_reduce(counts[r:r + 1])
+        return ev0, ev1
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for r in range(args.warmup):
+        device_round(r)
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tev = []
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        t0.record()
+        for r in range(args.warmup, total_rounds):
+            tev.append(device_round(r))
+        t1.record()
+        barrier()
+    ms = t0.elapsed_time(t1)
+    train_ms = float(np.mean([a.elapsed_time(b) for a, b in tev]))
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_steps = args.steps * n_part * steps_per_client
+    value = total_steps / (ms / 1e3)
+
+    # e2e: public API per round (selection, DES, host PCG64 plan + H2D, train, FedAvg, D2H accuracy)
+    def e2e_round(r, now):
+        rep, mine, wl, seeds, coef = plan_round(r, now)
+        fed.train(params, mine, wl, lr, seeds, deltas=deltas)
+        if world == 1:
+            fed.aggregate(params, deltas, [float(w.num_samples) for w in wl])
+        else:
+            aggregate(coef)
+        fed.correct(params)
+        return now + rep.makespan
+
+    now = 0.0
+    for r in range(args.warmup):
+        now = e2e_round(total_rounds + r, now)
+    barrier()
+    e0 = time.perf_counter()
+    for r in range(args.steps):
+        now = e2e_round(total_rounds + args.warmup + r, now)
+    barrier()
+    e2e_s = time.perf_counter() - e0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    flops = resnet_flop_per_sample(nc) * per_gpu * n_samp
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (cuBLAS, measured)"
+    except (OSError, KeyError, ValueError):
+        peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    tf = flops / (train_ms * 1e-3) / 1e12
+    res = {
+        "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
+        "value": value, "unit": "client-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic CIFAR-shaped 32x32x3 rows generated in HBM (Gaussian class clusters, "
+                                 "Dirichlet(0.5) label mix); random-init ResNet-18",
+        "config": {"workload": "cifar-resnet18: BASELINE config 3 model, ResNet-18 (3x3 stem, BasicBlocks "
+                               "64-128-256-512, batch norm), 10 classes",
+                   "arithmetic": "bf16 tensor-core operands and activations (tcgen05), fp32 accumulation, batch "
+                                 "norm and master weights; FedAvg in fp64",
+                   "participants_per_round": n_part, "per_gpu": per_gpu, "fleet": n_fleet,
+                   "samples_per_client": n_samp, "batch": bs, "local_steps_per_client": steps_per_client,
+                   "budgets": "10..100 step 10", "theta": THETA, "scheduler": "resource-aware, dynamic parallelism",
+                   "parallelism": f"clients sharded over {world} GPU(s)" + (" (config 3: 200 over 8)"
+                                                                             if world < 8 else ""),
+                   "l2": "per-client weights + activations (~4 GB/round) exceed L2; no flush needed"},
+        "rounds_per_sec": args.steps / (ms / 1e3), "train_ms": train_ms,
+        "accuracy_last_round": counts[-1].item() / n_test,
+        "e2e": {"value": total_steps / e2e_s, "unit": "client-steps/s",
+                "h2d_bytes_per_step": int(fed.last_h2d_bytes + per_gpu * 8), "d2h_bytes_per_step": 8,
+                "rounds_per_sec": args.steps / e2e_s,
+                "api": "ResnetFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"},
+        "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                     "traffic": None, "kernel": "train phase (one CUDA graph: implicit-GEMM grouped_gemm_kernel "
+                                                "launches + batch-norm / elementwise kernels)",
+                     "algorithmic_flop_per_launch": flops, "flop_per_sample": resnet_flop_per_sample(nc),
+                     "peak_source": src},
+        "clocks": clocks.summary(),
+        "gpu_launches": None,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _, _ = resnet_cpu_reference(args.cpu_seconds, nc, bs)
+        res["cpu_baseline"] = {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port", "sample": sample}
+    if dist is not None:
+        dist.destroy_process_group()
+    return res
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
     if rank != 0:
@@ -815,6 +1045,8 @@ def main():
         res = run_fedavg(args, rank, world, local_rank)
     elif args.workload == "cnn":
         res = run_cnn(args, rank, world, local_rank)
+    elif args.workload == "resnet":
+        res = run_resnet(args, rank, world, local_rank)
     elif args.workload == "gemm":
         res = run_gemm(args, rank, world, local_rank)
     elif args.workload == "des":

@@ -195,36 +195,64 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
                                                          const float* __restrict__ stats,  // BWD: [G][C][2]
                                                          const int32_t* __restrict__ valid, int Bp, int HW, int C,
                                                          float* __restrict__ part) {
-  __shared__ float red[4][64][2];
-  const int c = blockIdx.x * 64 + (threadIdx.x & 63), rl = threadIdx.x >> 6, g = blockIdx.y, sp = blockIdx.z;
-  const int64_t nr = (int64_t)valid[g] * HW;
-  const int64_t r0 = nr * sp / BN_SPLIT, r1 = nr * (sp + 1) / BN_SPLIT;
-  const int64_t base = (int64_t)g * Bp * HW;
-  float mean = 0.f, rstd = 0.f;
-  if (BWD) {
-    mean = stats[((int64_t)g * C + c) * 2];
-    rstd = stats[((int64_t)g * C + c) * 2 + 1];
-  }
-  float s0 = 0.f, s1 = 0.f;
-  for (int64_t r = r0 + rl; r < r1; r += 4) {
-    const float v = bf(x[(base + r) * C + c]);
+  // grid (1, G, BN_SPLIT); thread = (8-channel group cg, row lane rl): C / 8 groups x (256 / (C / 8)) lanes
+  __shared__ float red[256][17];
+  const int g = blockIdx.y, sp = blockIdx.z, groups = C >> 3, lanes = 256 / groups;
+  const int cg = threadIdx.x % groups, rl = threadIdx.x / groups;
+  const int nr = valid[g] * HW;
+  const int r0 = (int)((int64_t)nr * sp / BN_SPLIT), r1 = (int)((int64_t)nr * (sp + 1) / BN_SPLIT);
+  const __nv_bfloat16* xb = x + (int64_t)g * Bp * HW * C + cg * 8;
+  const __nv_bfloat16* db = BWD ? dz + (int64_t)g * Bp * HW * C + cg * 8 : nullptr;
+  float mean[8], rstd[8], s0[8], s1[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    s0[e] = s1[e] = 0.f;
+    mean[e] = rstd[e] = 0.f;
     if (BWD) {
-      const float d = bf(dz[(base + r) * C + c]);
-      s0 += d;
-      s1 += d * (v - mean) * rstd;
-    } else {
-      s0 += v;
-      s1 += v * v;
+      mean[e] = stats[((int64_t)g * C + cg * 8 + e) * 2];
+      rstd[e] = stats[((int64_t)g * C + cg * 8 + e) * 2 + 1];
     }
   }
-  red[rl][threadIdx.x & 63][0] = s0;
-  red[rl][threadIdx.x & 63][1] = s1;
+  if (rl < lanes) {
+    for (int r = r0 + rl; r < r1; r += lanes) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xb + (int64_t)r * C);
+      const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
+      if (BWD) {
+        const uint4 dv = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
+        const __nv_bfloat16* de = reinterpret_cast<const __nv_bfloat16*>(&dv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = bf(de[e]);
+          s0[e] += d;
+          s1[e] += d * (bf(xe[e]) - mean[e]) * rstd[e];
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = bf(xe[e]);
+          s0[e] += v;
+          s1[e] += v * v;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[threadIdx.x][e] = s0[e];
+    red[threadIdx.x][8 + e] = s1[e];
+  }
   __syncthreads();
-  if (rl == 0) {
-    const int t = threadIdx.x & 63;
+  // fixed-order reduction over the row lanes: thread t < C handles channel t
+  for (int c = threadIdx.x; c < C; c += 256) {
+    const int gq = c >> 3, e = c & 7;
+    float a0 = 0.f, a1 = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      a0 += red[l * groups + gq][e];
+      a1 += red[l * groups + gq][8 + e];
+    }
     float* o = part + (((int64_t)g * BN_SPLIT + sp) * C + c) * 2;
-    o[0] = (red[0][t][0] + red[1][t][0]) + (red[2][t][0] + red[3][t][0]);
-    o[1] = (red[0][t][1] + red[1][t][1]) + (red[2][t][1] + red[3][t][1]);
+    o[0] = a0;
+    o[1] = a1;
   }
 }
 
@@ -271,14 +299,42 @@ struct BnApply {
   int relu, eval;
 };
 
+// grid (blocks, G): per-channel scale / shift staged in shared memory; y = x * k + b (+ xs * ks + bs) (+ res)
 __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* __restrict__ master, int64_t pstride,
-                                                       int Bp, int HW, int C, int64_t total8,
-                                                       __nv_bfloat16* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = i * 8;
-    const int c0 = (int)(e0 % C);
-    const int g = (int)(e0 / ((int64_t)Bp * HW * C));
-    const float* m = master + (int64_t)g * pstride;
+                                                       int Bp, int HW, int C, __nv_bfloat16* __restrict__ out) {
+  __shared__ float k0[MAXC], b0[MAXC], k1[MAXC], b1[MAXC];
+  const int g = blockIdx.y;
+  const float* m = master + (int64_t)g * pstride;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float mean, rstd;
+    if (a.eval) {
+      mean = m[a.rmean + c];
+      rstd = rsqrtf(m[a.rvar + c] + BN_EPS);
+    } else {
+      mean = a.stats[((int64_t)g * C + c) * 2];
+      rstd = a.stats[((int64_t)g * C + c) * 2 + 1];
+    }
+    k0[c] = rstd * m[a.gamma + c];
+    b0[c] = m[a.beta + c] - mean * k0[c];
+    if (a.xs) {
+      float ms, rs;
+      if (a.eval) {
+        ms = m[a.rmean_s + c];
+        rs = rsqrtf(m[a.rvar_s + c] + BN_EPS);
+      } else {
+        ms = a.stats_s[((int64_t)g * C + c) * 2];
+        rs = a.stats_s[((int64_t)g * C + c) * 2 + 1];
+      }
+      k1[c] = rs * m[a.gamma_s + c];
+      b1[c] = m[a.beta_s + c] - ms * k1[c];
+    }
+  }
+  __syncthreads();
+  const int n8 = Bp * HW * (C >> 3), cmask = (C >> 3) - 1;  // C / 8 is a power of two
+  const int64_t base = (int64_t)g * Bp * HW * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const int64_t e0 = base + (int64_t)i * 8;
+    const int c0 = (i & cmask) * 8;
     const uint4 xv = *reinterpret_cast<const uint4*>(a.x + e0);
     uint4 rv = make_uint4(0, 0, 0, 0), sv = make_uint4(0, 0, 0, 0);
     if (a.res) rv = *reinterpret_cast<const uint4*>(a.res + e0);
@@ -287,27 +343,9 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int c = c0 + e;
-      float mean, rstd;
-      if (a.eval) {
-        mean = m[a.rmean + c];
-        rstd = rsqrtf(m[a.rvar + c] + BN_EPS);
-      } else {
-        mean = a.stats[((int64_t)g * C + c) * 2];
-        rstd = a.stats[((int64_t)g * C + c) * 2 + 1];
-      }
-      float v = (bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) - mean) * rstd * m[a.gamma + c] + m[a.beta + c];
+      float v = bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) * k0[c] + b0[c];
       if (a.res) v += bf(reinterpret_cast<const __nv_bfloat16*>(&rv)[e]);
-      if (a.xs) {
-        float ms, rs;
-        if (a.eval) {
-          ms = m[a.rmean_s + c];
-          rs = rsqrtf(m[a.rvar_s + c] + BN_EPS);
-        } else {
-          ms = a.stats_s[((int64_t)g * C + c) * 2];
-          rs = a.stats_s[((int64_t)g * C + c) * 2 + 1];
-        }
-        v += (bf(reinterpret_cast<const __nv_bfloat16*>(&sv)[e]) - ms) * rs * m[a.gamma_s + c] + m[a.beta_s + c];
-      }
+      if (a.xs) v += bf(reinterpret_cast<const __nv_bfloat16*>(&sv)[e]) * k1[c] + b1[c];
       if (a.relu) v = fmaxf(v, 0.f);
       o[e] = __float2bfloat16_rn(v);
     }
@@ -315,36 +353,45 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
   }
 }
 
-// dx = gamma rstd (dz - (dbeta + xhat dgamma) / n) on the valid images, 0 on padding images.
+// dx = gamma rstd (dz - (dbeta + xhat dgamma) / n) = A dz + B x + D on the valid images, 0 on padding
+// images; grid (blocks, G), per-channel A, B, D in shared memory.
 __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dz,
                                                            const __nv_bfloat16* __restrict__ x,
                                                            const float* __restrict__ stats,
                                                            const float* __restrict__ gsum,
                                                            const float* __restrict__ master, int64_t pstride,
                                                            int64_t gamma_off, const int32_t* __restrict__ valid,
-                                                           int Bp, int HW, int C, int64_t total8,
-                                                           __nv_bfloat16* __restrict__ dx) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = i * 8;
-    const int c0 = (int)(e0 % C);
-    const int64_t img = e0 / ((int64_t)HW * C);
-    const int g = (int)(img / Bp), b = (int)(img % Bp);
+                                                           int Bp, int HW, int C, __nv_bfloat16* __restrict__ dx) {
+  __shared__ float cA[MAXC], cB[MAXC], cD[MAXC];
+  const int g = blockIdx.y, rows = valid[g];
+  const float n = (float)rows * HW;
+  const float* m = master + (int64_t)g * pstride;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float mean = stats[((int64_t)g * C + c) * 2], rstd = stats[((int64_t)g * C + c) * 2 + 1];
+    const float db = gsum[((int64_t)g * C + c) * 2], dg = gsum[((int64_t)g * C + c) * 2 + 1];
+    const float A = m[gamma_off + c] * rstd;
+    cA[c] = A;
+    cB[c] = n > 0.f ? -A * rstd * dg / n : 0.f;
+    cD[c] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
+  }
+  __syncthreads();
+  const int per_img8 = HW * (C >> 3), cmask = (C >> 3) - 1;
+  const int n8 = Bp * per_img8, valid8 = rows * per_img8;
+  const int64_t base = (int64_t)g * Bp * HW * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const int64_t e0 = base + (int64_t)i * 8;
     __align__(16) __nv_bfloat16 o[8];
-    if (b >= valid[g]) {
+    if (i >= valid8) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = __float2bfloat16_rn(0.f);
     } else {
-      const float n = (float)valid[g] * HW;
+      const int c0 = (i & cmask) * 8;
       const uint4 dv = *reinterpret_cast<const uint4*>(dz + e0), xv = *reinterpret_cast<const uint4*>(x + e0);
-      const float* m = master + (int64_t)g * pstride;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int c = c0 + e;
-        const float mean = stats[((int64_t)g * C + c) * 2], rstd = stats[((int64_t)g * C + c) * 2 + 1];
-        const float db = gsum[((int64_t)g * C + c) * 2], dg = gsum[((int64_t)g * C + c) * 2 + 1];
-        const float xh = (bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) - mean) * rstd;
-        const float d = bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]);
-        o[e] = __float2bfloat16_rn(m[gamma_off + c] * rstd * (d - (db + xh * dg) / n));
+        o[e] = __float2bfloat16_rn(cA[c] * bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]) +
+                                   cB[c] * bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) + cD[c]);
       }
     }
     *reinterpret_cast<uint4*>(dx + e0) = *reinterpret_cast<const uint4*>(o);
@@ -379,21 +426,17 @@ __global__ void __launch_bounds__(256) add_kernel(__nv_bfloat16* __restrict__ ac
   }
 }
 
-// in [n][h][w][C] -> out [n][2h][2w][C], values at even (y, x), zeros elsewhere
-__global__ void __launch_bounds__(256) upsample2_kernel(const __nv_bfloat16* __restrict__ in, int64_t n, int h, int w,
-                                                        int C, __nv_bfloat16* __restrict__ out) {
-  const int64_t total8 = n * 4 * h * w * C / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = i * 8;
-    const int c0 = (int)(e0 % C);
-    int64_t p = e0 / C;
-    const int x = (int)(p % (2 * w));
-    p /= 2 * w;
-    const int y = (int)(p % (2 * h));
-    const int64_t img = p / (2 * h);
+// in [n][h][w][C] -> out [n][2h][2w][C], values at even (y, x), zeros elsewhere; grid (blocks, n)
+__global__ void __launch_bounds__(256) upsample2_kernel(const __nv_bfloat16* __restrict__ in, int h, int w, int C,
+                                                        __nv_bfloat16* __restrict__ out) {
+  const int c8 = C >> 3, per8 = 4 * h * w * c8;
+  const __nv_bfloat16* src = in + (int64_t)blockIdx.y * h * w * C;
+  uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)blockIdx.y * 4 * h * w * C);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per8; i += gridDim.x * blockDim.x) {
+    const int cg = i % c8, p = i / c8, x = p % (2 * w), y = p / (2 * w);
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (!(x & 1) && !(y & 1)) v = *reinterpret_cast<const uint4*>(in + ((img * h + y / 2) * w + x / 2) * C + c0);
-    reinterpret_cast<uint4*>(out)[i] = v;
+    if (!(x & 1) && !(y & 1)) v = *reinterpret_cast<const uint4*>(src + ((y >> 1) * w + (x >> 1)) * C + cg * 8);
+    dst[i] = v;
   }
 }
 
@@ -523,13 +566,16 @@ __global__ void bn_sgd_kernel(BnSgdTable t, float* __restrict__ master, int64_t 
   }
 }
 
+// grid (blocks, G)
 __global__ void bcast_kernel(const double* __restrict__ params, float* __restrict__ master,
                              __nv_bfloat16* __restrict__ shadow, int64_t P, int G) {
-  const int64_t total = (int64_t)G * P;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = (float)params[i % P];
-    master[i] = v;
-    shadow[i] = __float2bfloat16_rn(v);
+  float* m = master + (int64_t)blockIdx.y * P;
+  __nv_bfloat16* sh = shadow + (int64_t)blockIdx.y * P;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 2; i < P; i += (int64_t)gridDim.x * blockDim.x * 2) {
+    const double2 v = *reinterpret_cast<const double2*>(params + i);  // P % 64 == 0
+    const float a = (float)v.x, b = (float)v.y;
+    *reinterpret_cast<float2*>(m + i) = make_float2(a, b);
+    *reinterpret_cast<__nv_bfloat162*>(sh + i) = __floats2bfloat162_rn(a, b);
   }
 }
 
@@ -538,8 +584,11 @@ __global__ void delta_kernel(const fedhc_client* __restrict__ cl, const double* 
   const int g = blockIdx.y;
   float* out = cl[g].delta;
   const float* m = master + (int64_t)g * P;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = m[i] - (float)params[i];
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 2; i < P; i += (int64_t)gridDim.x * blockDim.x * 2) {
+    const double2 v = *reinterpret_cast<const double2*>(params + i);
+    const float2 w = *reinterpret_cast<const float2*>(m + i);
+    *reinterpret_cast<float2*>(out + i) = make_float2(w.x - (float)v.x, w.y - (float)v.y);
+  }
 }
 
 struct Buf {
@@ -778,10 +827,16 @@ struct Engine {
     const int64_t b = (work + 255) / 256;
     return (int)(b < 148 * 16 ? b : 148 * 16);
   }
+  static int up_blocks(int H, int C) { return (H * H * C / 8 + 255) / 256; }
+  // per-client grid x for work items of 256 threads, about 16 CTAs per SM over all G clients
+  static int blocks_for(int64_t work, int G) {
+    const int64_t b = (work + 255) / 256, cap = (148 * 16 + G - 1) / G;
+    return (int)(b < cap ? b : (cap > 0 ? cap : 1));
+  }
 
   // batch statistics of x [G*bp][HW][C] into stats slot `id`, running stats at (rm, rv)
   void bn_stats(int G, int bp, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b, cudaStream_t st) {
-    bn_partial_kernel<false><<<dim3(C / 64, G, BN_SPLIT), 256, 0, st>>>(x, nullptr, nullptr, valid, bp, HW, C, part);
+    bn_partial_kernel<false><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, nullptr, nullptr, valid, bp, HW, C, part);
     bn_finalize_kernel<false><<<G, C, 0, st>>>(part, valid, HW, C, stats + st_off[id], master, L.P, b.rmean,
                                                b.rvar);
   }
@@ -807,19 +862,16 @@ struct Engine {
     }
     a.relu = relu;
     a.eval = eval;
-    const int64_t total8 = (int64_t)G * bp * HW * C / 8;
-    bn_apply_kernel<<<grid_for(total8), 256, 0, st>>>(a, master, L.P, bp, HW, C, total8, out);
+    bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), 256, 0, st>>>(a, master, L.P, bp, HW, C, out);
   }
 
   // dC = BN backward of dz through x (stats slot id), dgamma / dbeta into gsum slot id
   void bn_backward(int G, const __nv_bfloat16* dz, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b,
                    __nv_bfloat16* dc, cudaStream_t st) {
-    bn_partial_kernel<true><<<dim3(C / 64, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C,
-                                                                       part);
+    bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C, part);
     bn_finalize_kernel<true><<<G, C, 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
-    const int64_t total8 = (int64_t)G * Bp * HW * C / 8;
-    bn_bwd_apply_kernel<<<grid_for(total8), 256, 0, st>>>(dz, x, stats + st_off[id], gsum + st_off[id], master, L.P,
-                                                          b.gamma, valid, Bp, HW, C, total8, dc);
+    bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), 256, 0, st>>>(
+        dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc);
   }
 
   int forward(int G, int bp, int step, bool eval, const tc::GemmPlan& sf, const BlockPlans* bps, cudaStream_t st) {
@@ -873,14 +925,14 @@ struct Engine {
       if (d.s == 1) {
         if ((rc = tc::gemm_run(bp[i].c1d, st))) return rc;  // g2 = dX (from g0)
       } else {
-        upsample2_kernel<<<grid_for(n8i / d.cin * d.cout), 256, 0, st>>>(g0, (int64_t)G * Bp, ho, ho, d.cout, up);
+        upsample2_kernel<<<dim3(up_blocks(d.H, d.cout), G * Bp), 256, 0, st>>>(g0, ho, ho, d.cout, up);
         if ((rc = tc::gemm_run(bp[i].c1d, st))) return rc;  // g2 = dX (from up)
       }
       if ((rc = tc::gemm_run(bp[i].c1w, st))) return rc;  // W1 SGD (x, dC1 in g0)
       if (L.cs[i] >= 0) {
         // shortcut: dCS (g1) = bn_s backward of dZ (g3); upsample -> up; dXs -> g3; Ws SGD (x, dCS)
         bn_backward(G, dz, cs[i], hw, d.cout, 3 + 3 * i, L.bns[i], g1, st);
-        upsample2_kernel<<<grid_for(n8i / d.cin * d.cout), 256, 0, st>>>(g1, (int64_t)G * Bp, ho, ho, d.cout, up);
+        upsample2_kernel<<<dim3(up_blocks(d.H, d.cout), G * Bp), 256, 0, st>>>(g1, ho, ho, d.cout, up);
         // the shortcut weight-gradient plan reads dCS from g3 (dZ is dead by now)
         FEDHC_CUDA_TRY(cudaMemcpyAsync(g3, g1, (size_t)G * Bp * hw * d.cout * 2, cudaMemcpyDeviceToDevice, st));
         if ((rc = tc::gemm_run(bp[i].csw, st))) return rc;  // Ws SGD (x, dCS = g3)
@@ -981,7 +1033,8 @@ extern "C" int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, i
   int rc = e->plan_train(G, lr);
   if (rc) return rc;
   FEDHC_CUDA_TRY(cudaMemcpyAsync(e->desc, clients, sizeof(fedhc_client) * G, cudaMemcpyDeviceToDevice, st));
-  rn::bcast_kernel<<<rn::Engine::grid_for((int64_t)G * e->L.P), 256, 0, st>>>(params, e->master, e->shadow, e->L.P, G);
+  rn::bcast_kernel<<<dim3(rn::Engine::blocks_for(e->L.P / 2, G), G), 256, 0, st>>>(params, e->master, e->shadow,
+                                                                                   e->L.P, G);
   FEDHC_CUDA_TRY(cudaGetLastError());
   if (use_graph) {
     const auto key = std::make_tuple(G, max_steps, lr);
@@ -1012,7 +1065,8 @@ extern "C" int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, i
     for (int s = 0; s < max_steps; ++s)
       if ((rc = e->train_step(G, s, lr, st))) return rc;
   }
-  rn::delta_kernel<<<dim3(64, G), 256, 0, st>>>(e->desc, params, e->master, e->L.P);
+  rn::delta_kernel<<<dim3(rn::Engine::blocks_for(e->L.P / 2, G), G), 256, 0, st>>>(e->desc, params, e->master,
+                                                                                   e->L.P);
   FEDHC_CUDA_TRY(cudaGetLastError());
   return FEDHC_OK;
 }
@@ -1033,7 +1087,8 @@ extern "C" int fedhc_resnet_eval(void* ws, const double* params, const float* x,
   if (n <= 0) return FEDHC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int chunk = e->maxG * e->Bp;
-  rn::bcast_kernel<<<rn::Engine::grid_for(e->L.P), 256, 0, st>>>(params, e->master, e->shadow, e->L.P, 1);
+  rn::bcast_kernel<<<dim3(rn::Engine::blocks_for(e->L.P / 2, 1), 1), 256, 0, st>>>(params, e->master, e->shadow,
+                                                                                   e->L.P, 1);
   for (int64_t at = 0; at < n; at += chunk) {
     const int rows = (int)(n - at < chunk ? n - at : chunk);
     fedhc_client c{};
