@@ -261,7 +261,9 @@ __device__ __forceinline__ void nhwc_loads(const ConvSpec& cv, uint32_t sa, uint
 #pragma unroll
     for (int h = 0; h < BM / 64; ++h) {
       const int m = m0 + 64 * h, tap = m / cv.cin, c = m - tap * cv.cin, kh = tap / cv.k, kw = tap - kh * cv.k;
-      tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, c, kw - pad, y0 * cv.s + kh - pad, img0);
+      // rows past k*k*cin (ragged last tile): a box entirely out of bounds loads zeros
+      tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, tap < cv.k * cv.k ? c : 0, kw - pad,
+                  tap < cv.k * cv.k ? y0 * cv.s + kh - pad : -4096, img0);
     }
 #pragma unroll
     for (int h = 0; h < BN / 64; ++h) tma_load_4d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, 0, y0, img0);
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lempty + 4 * kEpiLoad);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_m = M / BM, tiles_n = N / BN;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = N / BN;  // ragged M only for NHWC_WGRAD (rows clipped)
   const int n_tiles = G * tiles_m * tiles_n;
   const int kblocks = WIN == 1 ? 3 : WIN == 2 ? 5 : K / BK;
 
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      if (ep.rowsum && active) ep.rowsum[(int64_t)g * M + row] = rsum;
+      if (ep.rowsum && active && row < M) ep.rowsum[(int64_t)g * M + row] = rsum;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -709,7 +711,7 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int tiles = a.G * (a.M / BM) * (a.N / BN);
+  const int tiles = a.G * ((a.M + BM - 1) / BM) * (a.N / BN);
   // short-K GEMMs are epilogue (store) bound: spend shared memory on in-flight TMA stores
   // (load epilogues keep 2: their in-place SGD stores read the load slot, released one chunk later)
   int nst = (a.K / BK <= 4 && !epi_loads(kind)) ? 8 : 2, stages = 0, fixed = 0;
@@ -819,6 +821,9 @@ int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p, const ConvSpec* conv) {
   p->K = a.K;
   if ((p->conv.mode == NHWC_FWD || p->conv.mode == NHWC_DGRAD) && a.M % 128)
     return fail(FEDHC_ERR_VALUE, "gemm: NHWC conv needs 128-row tiles");
+  // NHWC weight gradients: 128-row tiles even when k*k*cin % 128 != 0 (e.g. 576 = 9 x 64): the last tile's
+  // extra rows load zeros and its stores / master loads are clipped by the tensor maps at M
+  if (p->conv.mode == NHWC_WGRAD) return plan_n<128>(a, p);
   return a.M % 128 == 0 ? plan_n<128>(a, p) : plan_n<64>(a, p);
 }
 
