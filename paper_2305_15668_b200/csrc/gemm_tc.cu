@@ -45,12 +45,14 @@ constexpr int kThreads = 192;
 // that share it; the MMAs of tap kh read the window through a descriptor shifted by whole 16-pixel
 // rows (2048 B, a multiple of the 1024-B swizzle atom).  WIN 1 = conv2 forward (window per tap-pair
 // column, 5 MN-major 64x64 weight blocks), WIN 2 = conv2 data gradient (window per kw, 5 K-major 32x64
-// weight blocks).
+// weight blocks).  WIN 3 / 4 = the same for NHWC 3x3 stride-1 forward / data gradient on 32- or 16-wide
+// maps: a (hb + 2)-row window per (input-channel block, kw), 3 taps per stage, row shift = wo * 128 B.
 template <int BM, int BN, int WIN = 0>
 struct Cfg {
   static constexpr int kTileABytes = WIN ? 192 * 128 : BM * BK * 2;
   static constexpr int kTapBBytes = BN * BK * 2;
-  static constexpr int kTileBBytes = WIN ? 5 * kTapBBytes : kTapBBytes;
+  static constexpr int kTaps = (WIN == 1 || WIN == 2) ? 5 : 3;  // taps sharing one window (one kernel column)
+  static constexpr int kTileBBytes = WIN ? kTaps * kTapBBytes : kTapBBytes;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
 };
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = N / BN;  // ragged M only for NHWC_WGRAD (rows clipped)
   const int n_tiles = G * tiles_m * tiles_n;
-  const int kblocks = WIN == 1 ? 3 : WIN == 2 ? 5 : K / BK;
+  const int kblocks = WIN == 1 ? 3 : WIN == 2 ? 5 : (WIN >= 3 ? K / (3 * BK) : K / BK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -342,7 +344,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          mbar_arrive_expect_tx(&full[s], WIN >= 3 ? (uint32_t)((conv.hb + 2) * conv.wo * 128 + CF::kTileBBytes)
+                                                   : (uint32_t)kStageBytes);
           const uint32_t sa = smem_u32(smem + s * kStageBytes), sb = sa + kTileABytes;
           if (conv.mode == CONV_NONE) {
             if (A_MN) {
@@ -363,6 +366,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             nhwc_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
           } else if (WIN == 0) {
             conv_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
+          } else if (WIN >= 3) {  // NHWC 3x3 stride 1: window of hb + 2 rows, shifted by kw, 3 taps (kh)
+            int img0, y0;
+            nhwc_tile_origin(conv, g, m0 / BM, img0, y0);
+            const int kw = kb % 3, cb = kb / 3;
+            if (WIN == 3) {
+              tma_load_4d(sa, &map_a, &full[s], cb * 64, kw - 1, y0 - 1, img0);
+#pragma unroll
+              for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+                for (int h = 0; h < BN / 64; ++h)
+                  tma_load_3d(sb + kh * CF::kTapBBytes + h * 64 * BK * 2, &map_b, &full[s], n0 + 64 * h,
+                              (kh * 3 + kw) * conv.cin + cb * 64, g);
+            } else {
+              tma_load_4d(sa, &map_a, &full[s], cb * 64, 1 - kw, y0 - 1, img0);
+#pragma unroll
+              for (int kh = 0; kh < 3; ++kh)
+                tma_load_3d(sb + kh * CF::kTapBBytes, &map_b, &full[s], cb * 64, (kh * 3 + kw) * conv.cin + n0, g);
+            }
           } else {
             const int mt = m0 / BM, img = g * conv.bp + (mt >> 1), y0 = (mt & 1) * 8;
             if (WIN == 1) {  // forward: tap-pair column pk = kb; window rows y0 - 2 .. y0 + 9
@@ -418,11 +439,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16(tmem_d, da + (kStepA >> 4) * k, db + (kStepB >> 4) * k, kIdesc, (kb | k) != 0);
           } else {
+            const uint32_t rowb = WIN >= 3 ? (uint32_t)conv.wo * 128 : 2048;  // one window row of pixels
 #pragma unroll
-            for (int kh = 0; kh < 5; ++kh) {
-              // forward reads input row y + kh - 2, data gradient y + 2 - kh: window row offset
-              const int wr = WIN == 1 ? kh : 4 - kh;
-              const uint64_t da = sw128_desc(sa + wr * 2048, kLboA);
+            for (int kh = 0; kh < CF::kTaps; ++kh) {
+              // forward reads input row y + kh - pad, data gradient y + pad - kh: window row offset
+              const int wr = (WIN == 1 || WIN == 3) ? kh : CF::kTaps - 1 - kh;
+              const uint64_t da = sw128_desc(sa + wr * rowb, kLboA);
               const uint64_t db = sw128_desc(sa + kTileABytes + kh * CF::kTapBBytes, kLboB);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
@@ -707,6 +729,12 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
     if (kind == FEDHC_EPI_RELU_MASK_BF16 && (rc = make_epi_map(&p->ml, p->ep.mask, false, *p, R))) return rc;
   }
   if (p->conv.mode != CONV_NONE && (rc = plan_conv_maps(a, p))) return rc;
+  if (WIN >= 3) {  // windowed NHWC: the A box covers hb + 2 rows of one image
+    const ConvSpec& c = p->conv;
+    if ((rc = make_nhwc_map(&p->ma, a.A, WIN == 3 ? c.cin : c.cout, c.W, c.H, (int64_t)a.G * c.bp, 64, c.wo,
+                            c.hb + 2, 1, 1, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
   int dev = 0, sms = 0, max_smem = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -735,6 +763,14 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
 
 template <int BM, int BN>
 static int plan_major(const fedhc_gemm_args& a, GemmPlan* p) {
+  static const bool no_window = getenv("FEDHC_NO_CONV_WINDOW") != nullptr;
+  const ConvSpec& cv = p->conv;
+  const bool win_ok = !no_window && cv.k == 3 && cv.s == 1 && cv.ib == 1 && (cv.wo == 32 || cv.wo == 16) &&
+                      (cv.hb + 2) * cv.wo * 128 <= 192 * 128;
+  if constexpr (BM == 128 && (BN == 64 || BN == 128)) {
+    if (cv.mode == NHWC_FWD && win_ok) return plan_kernel<128, BN, false, true, 3>(a, p);
+    if (cv.mode == NHWC_DGRAD && win_ok) return plan_kernel<128, BN, false, false, 4>(a, p);
+  }
   if constexpr (BM == 128 && BN == 64) {
     if (p->conv.mode == CONV_FWD) return plan_kernel<128, 64, false, true, 1>(a, p);
   }
