@@ -362,7 +362,8 @@ class FederatedRunner:
 
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
-                 plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = True):
+                 plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = True,
+                 green_plan: bool = False):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -400,6 +401,23 @@ class FederatedRunner:
         self._meta_pin = [torch.empty(k_max * 24, dtype=torch.uint8).pin_memory() for _ in range(n)]
         self._meta_dev = [torch.empty(k_max * 24, dtype=torch.uint8, device=dev) for _ in range(n)]
         self._plan_stream = torch.cuda.Stream(device=dev)
+        # Optional (green_plan=True, experimental): green-context SM partition for the batch-order kernel: the
+        # one-CTA-per-client train kernel needs
+        # k_max SMs with all their shared memory; confining perm_kernel to the remaining SM groups keeps its
+        # CTAs off the SMs the next round's training will claim (otherwise a resident permutation CTA makes
+        # a train CTA wait for it).  Falls back to an ordinary stream without green-context support.
+        self._green = None
+        if green_plan and device_permutations:
+            try:
+                from .live import GreenPartitions
+                gp = GreenPartitions(dev.index if dev.index is not None else 0)
+                need = -(-k_max // gp.sms_per_group)
+                if gp.n_groups - need >= 1:
+                    raw = gp.stream(need, gp.n_groups - need)
+                    self._green = gp
+                    self._plan_stream = torch.cuda.ExternalStream(raw, device=dev)
+            except Exception:  # no green-context support in this driver: keep the ordinary stream
+                self._green = None
         self._train_done = [None] * n   # event: the slot's train kernel retired (plan buffer reusable)
         # one pinned / device staging block per slot for the device-plan mode: [meta 24k | desc | coef 8k],
         # copied H2D in one transfer on the plan stream
@@ -548,6 +566,24 @@ class FederatedRunner:
                     and gs[0] == self._graph_key(p))
 
     def launch_plan(self, p: RoundPlan) -> None:
+        if self._green is not None and not p.plan_launched and p.meta_bytes and p.participants:
+            # eager on the green-context stream (kernel confined to the spare SM groups)
+            k, slot, mb = len(p.participants), p.slot, p.meta_bytes
+            tot = mb + k * CLIENT_DTYPE.itemsize + 8 * k
+            ps = self._plan_stream
+            dev = self._stage_dev[slot]
+            md = dev.data_ptr()
+            with torch.cuda.stream(ps):
+                dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
+                _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
+                                                                    self._dev_plan[slot].data_ptr(), self._rows_max,
+                                                                    ps.cuda_stream))
+                self._ev_plan[slot].record(ps)
+            p.plan_launched = True
+            return
+        self._launch_plan_graph(p)
+
+    def _launch_plan_graph(self, p: RoundPlan) -> None:
         """Queue the round's [H2D + device permutations] graph on the plan stream (no-op without graphs).
 
         The planner thread calls this as soon as a round is planned, so its permutations are generated
@@ -595,13 +631,14 @@ class FederatedRunner:
             tot = mb + nb + 8 * k
             dev = self._stage_dev[slot]
             md = dev.data_ptr()
-            with torch.cuda.stream(ps):
-                ps.wait_event(self._ev_train[slot])      # the slot's previous train kernel is done with it
-                dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
-                _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
-                                                                    self._dev_plan[slot].data_ptr(), p.max_rows,
-                                                                    ps.cuda_stream))
-                self._ev_plan[slot].record(ps)
+            if not p.plan_launched:
+                with torch.cuda.stream(ps):
+                    ps.wait_event(self._ev_train[slot])      # the slot's previous train kernel is done with it
+                    dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
+                    _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k,
+                                                                        k, self._dev_plan[slot].data_ptr(),
+                                                                        p.max_rows, ps.cuda_stream))
+                    self._ev_plan[slot].record(ps)
             main.wait_event(self._ev_plan[slot])
             self._plan_done[slot] = self._ev_plan[slot]
             desc_ptr, coef_t = md + mb, dev[mb + nb:mb + nb + 8 * k].view(torch.float64)
@@ -670,6 +707,7 @@ class FederatedRunner:
         def planner():
             t, r0 = self.now, self.round
             try:
+                torch.cuda.set_device(self.dev)  # bind the device context in this thread (it launches plan work)
                 for i in range(rounds):
                     slot = free.get()
                     pl = self.plan(r0 + i, t, slot)
