@@ -52,13 +52,17 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "fedavg", "gemm", "des"], default="round",
+    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "fedavg", "gemm", "des"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
     ap.add_argument("--cnn-samples", type=int, default=6400, help="samples per client for --workload cnn")
     ap.add_argument("--resnet-clients", type=int, default=25, help="ResNet-18 clients per GPU (config 3: 200 / 8)")
     ap.add_argument("--resnet-samples", type=int, default=250, help="samples per ResNet-18 client")
+    ap.add_argument("--mobilenet-clients", type=int, default=100, help="MobileNetV2 participants per GPU per round")
+    ap.add_argument("--mobilenet-fleet", type=int, default=1000, help="MobileNetV2 fleet size (config 4: >= 1000)")
+    ap.add_argument("--mobilenet-max-samples", type=int, default=1024,
+                    help="largest per-client sample count (config 4: uniform choice of 16, 32, ..., 1024)")
     ap.add_argument("--classes", type=int, default=10, help="10 (digits) or 62 (FEMNIST classes, 4-CTA clusters)")
     return ap.parse_args()
 
@@ -791,18 +795,36 @@ def resnet_flop_per_sample(n_classes: int) -> float:
     return float(2 * (3 * (macs + macs_fc) + 2 * stem))
 
 
-def resnet_cpu_reference(seconds: float, n_classes: int, batch: int):
-    """ResNet-18 local SGD on the host cores (torch CPU, all threads): CPU restatement (no reference CNN)."""
+def mobilenet_flop_per_sample(n_classes: int) -> float:
+    """Algorithmic FLOPs of one MobileNetV2 training sample: 3 x forward (pointwise + depthwise + head +
+    classifier) minus the stem's data gradient (unpadded channel counts)."""
+    from paper_2305_15668_b200.mobilenet import HEAD, blocks
+    macs, H, stem = 0, 32, 32 * 32 * 32 * 27
+    for ci, pl, co, s in blocks():
+        ho = H // s
+        macs += H * H * ci * pl + ho * ho * pl * 9 + ho * ho * pl * co + (H * H * ci * co if s == 1 and ci != co else 0)
+        H = ho
+    macs += 16 * 320 * HEAD + HEAD * n_classes
+    return float(2 * (3 * macs + 2 * stem))
+
+
+def cifar_cpu_reference(seconds: float, n_classes: int, batch: int, model: str = "resnet"):
+    """CIFAR-model local SGD on the host cores (torch CPU, all threads): CPU restatement (no reference CNN)."""
     import torch
     import torch.nn as nn
 
-    from oracle.resnet import ResNet18
+    if model == "mobilenet":
+        from oracle.mobilenet import MobileNetV2 as Net
+        name = "MobileNetV2"
+    else:
+        from oracle.resnet import ResNet18 as Net
+        name = "ResNet-18"
     cores = len(os.sched_getaffinity(0))
     torch.set_num_threads(cores)
     torch.manual_seed(0)
-    model = ResNet18(n_classes)
-    model.train()
-    opt = torch.optim.SGD(model.parameters(), lr=0.05)
+    net = Net(n_classes)
+    net.train()
+    opt = torch.optim.SGD(net.parameters(), lr=0.05)
     x = torch.randn(256, 3, 32, 32)
     y = torch.randint(0, n_classes, (256,))
     lossf = nn.CrossEntropyLoss()
@@ -810,7 +832,7 @@ def resnet_cpu_reference(seconds: float, n_classes: int, batch: int):
     def one(i):
         s0 = (i * batch) % (256 - batch)
         opt.zero_grad(set_to_none=True)
-        lossf(model(x[s0:s0 + batch]), y[s0:s0 + batch]).backward()
+        lossf(net(x[s0:s0 + batch]), y[s0:s0 + batch]).backward()
         opt.step()
 
     for i in range(2):
@@ -820,19 +842,27 @@ def resnet_cpu_reference(seconds: float, n_classes: int, batch: int):
         one(n)
         n += 1
     dt = time.perf_counter() - t0
-    return n / dt, cores, (f"{n} local SGD steps (B={batch}) of one ResNet-18 client, torch CPU fp32 with {cores} "
+    return n / dt, cores, (f"{n} local SGD steps (B={batch}) of one {name} client, torch CPU fp32 with {cores} "
                            f"threads (CPU restatement: the reference has no CNN)"), n, dt
 
 
-def run_resnet(args, rank, world, local_rank):
+def run_resnet(args, rank, world, local_rank, model="resnet"):
     """BASELINE config 3 with its named model: CIFAR ResNet-18 clients, 200 participants per round sharded
-    over the GPUs (25 per GPU at 8 GPUs; --resnet-clients per GPU), 250 samples each, B = 32."""
+    over the GPUs (25 per GPU at 8 GPUs; --resnet-clients per GPU), 250 samples each, B = 32.
+    model="mobilenet": BASELINE config 4 -- CIFAR MobileNetV2 clients from a fleet of >= 1000 with non-IID
+    sample counts (uniform choice of 16, 32, ..., 1024), --mobilenet-clients participants per GPU, B = 32;
+    each local step runs only the clients that still have batches (clients in descending-step order)."""
     import torch
 
     import paper_2305_15668_b200 as fh
     from paper_2305_15668_b200.devicedata import DeviceFleetData
     from paper_2305_15668_b200.experiment import delta_buffer
-    from paper_2305_15668_b200.resnet import ResnetFederation, init_resnet_params
+    if model == "mobilenet":
+        from paper_2305_15668_b200.mobilenet import MobilenetFederation as Federation
+        from paper_2305_15668_b200.mobilenet import init_mobilenet_params as init_params
+    else:
+        from paper_2305_15668_b200.resnet import ResnetFederation as Federation
+        from paper_2305_15668_b200.resnet import init_resnet_params as init_params
     from paper_2305_15668_b200.roundsim import RoundSimulator
     from paper_2305_15668_b200.sharding import shard_bounds
     from paper_2305_15668_b200.training import fedavg_device, stable_seed
@@ -844,10 +874,19 @@ def run_resnet(args, rank, world, local_rank):
         import torch.distributed as dist_mod
         dist = dist_mod
         dist.init_process_group("nccl", device_id=dev)
-    nc, n_samp, bs, lr = 10, args.resnet_samples, 32, 0.05
-    per_gpu = args.resnet_clients
-    n_part, n_fleet = per_gpu * world, (per_gpu + per_gpu // 4) * world
-    steps_per_client = math.ceil(n_samp / bs)
+    nc, bs, lr = 10, 32, 0.05
+    if model == "mobilenet":
+        per_gpu = args.mobilenet_clients
+        n_part, n_fleet = per_gpu * world, max(args.mobilenet_fleet, per_gpu * world)
+        levels, v = [], 16
+        while v <= args.mobilenet_max_samples:
+            levels.append(v)
+            v *= 2
+        n_samp = levels
+    else:
+        n_samp = args.resnet_samples
+        per_gpu = args.resnet_clients
+        n_part, n_fleet = per_gpu * world, (per_gpu + per_gpu // 4) * world
     fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=bs),
                               n_fleet, 3)
     by_id = {p.client_id: p for p in fleet}
@@ -856,10 +895,10 @@ def run_resnet(args, rank, world, local_rank):
     data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 3072, nc, alpha=0.5, seed=4321,
                            n_test=n_test)
     lo, hi = shard_bounds(n_test, world, rank)
-    fed = ResnetFederation.from_arrays(data.x, data.y, data.offsets, data.x_test[lo:hi].contiguous(),
+    fed = Federation.from_arrays(data.x, data.y, data.offsets, data.x_test[lo:hi].contiguous(),
                                        data.y_test[lo:hi].contiguous(), nc).attach_engine(per_gpu, bs)
     P = fed.P
-    params = torch.tensor(fed.layout.to_padded(init_resnet_params(nc, 1)), dtype=torch.float64, device=dev)
+    params = torch.tensor(fed.layout.to_padded(init_params(nc, 1)), dtype=torch.float64, device=dev)
     deltas = delta_buffer(per_gpu, P, dev)
     partial = torch.empty(P, dtype=torch.float64, device=dev)
     one = torch.ones(1, dtype=torch.float64, device=dev)
@@ -874,8 +913,8 @@ def run_resnet(args, rank, world, local_rank):
         mine = who[rank * per_gpu:(rank + 1) * per_gpu]
         wl = [by_id[c].workload for c in mine]
         seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
-        coef = torch.tensor([float(w.num_samples) / float(n_part * n_samp) for w in wl], dtype=torch.float64,
-                            device=dev)
+        tot = float(sum(w.num_samples for w in wl))  # this GPU's shard (equal shards: = global / world)
+        coef = torch.tensor([float(w.num_samples) / (tot * world) for w in wl], dtype=torch.float64, device=dev)
         return rep, mine, wl, seeds, coef
 
     def aggregate(coef):
@@ -893,15 +932,20 @@ def run_resnet(args, rank, world, local_rank):
         packed, meta = fed.plan(mine, wl, seeds)
         perm_dev = torch.from_numpy(packed).to(dev)
         fed._perm_dev = perm_dev
-        desc = fed.descriptors(mine, meta, lr, deltas)
-        plans.append((perm_dev, desc, coef, max(m[2] for m in meta)))
+        order = sorted(range(len(mine)), key=lambda i: -meta[i][2])  # descending local steps
+        desc = fed.descriptors([mine[i] for i in order], [meta[i] for i in order], lr, deltas, rows=order)
+        steps = [meta[i][2] for i in order]
+        plans.append((perm_dev, desc, coef, steps, sum(steps), sum(w.num_samples for w in wl)))
     counts = torch.zeros(total_rounds, dtype=torch.int64, device=dev)
 
     def device_round(r):
-        _, desc, coef, steps = plans[r]
+        _, desc, coef, steps, _, _ = plans[r]
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps, lr, True)
+        if model == "mobilenet":
+            fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True, steps=steps)
+        else:
+            fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True)
         ev1.record()
         aggregate(coef)
         fed.engine.correct_into(params, fed.x_test, fed.y_test, counts[r:r + 1])
@@ -919,6 +963,7 @@ def run_resnet(args, rank, world, local_rank):
     barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tev = []
+    lc0 = fed.engine.launch_count() if model == "mobilenet" else None
     with ClockSampler(local_rank) as clocks:
         barrier()
         t0.record()
@@ -927,17 +972,29 @@ def run_resnet(args, rank, world, local_rank):
         t1.record()
         barrier()
     ms = t0.elapsed_time(t1)
+    # our kernels in the timed region: engine graph nodes + direct launches (train, eval) + FedAvg (1, or 2 with
+    # the all-reduce split)
+    launches = (fed.engine.launch_count() - lc0 + args.steps * (1 if world == 1 else 2)) if lc0 is not None else None
     train_ms = float(np.mean([a.elapsed_time(b) for a, b in tev]))
     if dist is not None:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_steps = args.steps * n_part * steps_per_client
+    timed = plans[args.warmup:]
+    total_steps = sum(p[4] for p in timed)  # client local steps of this GPU's clients, then of all GPUs
+    if dist is not None:
+        t = torch.tensor([total_steps], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        total_steps = int(t.item())
     value = total_steps / (ms / 1e3)
 
     # e2e: public API per round (selection, DES, host PCG64 plan + H2D, train, FedAvg, D2H accuracy)
-    def e2e_round(r, now):
+    e2e_counts = []
+
+    def e2e_round(r, now, count=False):
         rep, mine, wl, seeds, coef = plan_round(r, now)
+        if count:
+            e2e_counts.append(sum(math.ceil(w.num_samples / bs) for w in wl))
         fed.train(params, mine, wl, lr, seeds, deltas=deltas)
         if world == 1:
             fed.aggregate(params, deltas, [float(w.num_samples) for w in wl])
@@ -952,53 +1009,72 @@ def run_resnet(args, rank, world, local_rank):
     barrier()
     e0 = time.perf_counter()
     for r in range(args.steps):
-        now = e2e_round(total_rounds + args.warmup + r, now)
+        now = e2e_round(total_rounds + args.warmup + r, now, count=True)
     barrier()
     e2e_s = time.perf_counter() - e0
+    e2e_steps = sum(e2e_counts)
     if dist is not None:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+        t = torch.tensor([e2e_steps], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        e2e_steps = int(t.item())
 
-    flops = resnet_flop_per_sample(nc) * per_gpu * n_samp
+    fps = mobilenet_flop_per_sample(nc) if model == "mobilenet" else resnet_flop_per_sample(nc)
+    flops = fps * float(np.mean([p[5] for p in timed]))  # per train launch (this GPU's samples)
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         peak, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (cuBLAS, measured)"
     except (OSError, KeyError, ValueError):
         peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
     tf = flops / (train_ms * 1e-3) / 1e12
+    if model == "mobilenet":
+        mname, cfg_name = "MobileNetV2", ("cifar-mobilenetv2: BASELINE config 4 model, MobileNetV2 (CIFAR variant: "
+                                           "3x3 stem, 17 inverted-residual blocks, 1x1 head to 1280, batch norm), "
+                                           "10 classes, fleet of %d with non-IID sample counts" % n_fleet)
+        api = "MobilenetFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"
+        kern = ("train phase (one CUDA graph per active-client count: pointwise convolutions as implicit-GEMM "
+                "grouped_gemm_kernel launches, depthwise 3x3 CUDA-core kernels, batch-norm / elementwise kernels)")
+        spc = "ceil(n / 32) for n in " + str(n_samp)
+        arith = ("bf16 tensor-core operands and activations (tcgen05) for the pointwise / head convolutions, fp32 "
+                 "CUDA-core depthwise 3x3 on bf16 activations, fp32 accumulation, batch norm and master weights; "
+                 "FedAvg in fp64")
+    else:
+        mname, cfg_name = "ResNet-18", ("cifar-resnet18: BASELINE config 3 model, ResNet-18 (3x3 stem, BasicBlocks "
+                                        "64-128-256-512, batch norm), 10 classes")
+        api = "ResnetFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"
+        kern = ("train phase (one CUDA graph: implicit-GEMM grouped_gemm_kernel launches + batch-norm / "
+                "elementwise kernels)")
+        spc = math.ceil(n_samp / bs)
+        arith = ("bf16 tensor-core operands and activations (tcgen05), fp32 accumulation, batch norm and master "
+                 "weights; FedAvg in fp64")
     res = {
         "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
         "value": value, "unit": "client-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic CIFAR-shaped 32x32x3 rows generated in HBM (Gaussian class clusters, "
-                                 "Dirichlet(0.5) label mix); random-init ResNet-18",
-        "config": {"workload": "cifar-resnet18: BASELINE config 3 model, ResNet-18 (3x3 stem, BasicBlocks "
-                               "64-128-256-512, batch norm), 10 classes",
-                   "arithmetic": "bf16 tensor-core operands and activations (tcgen05), fp32 accumulation, batch "
-                                 "norm and master weights; FedAvg in fp64",
+                                 "Dirichlet(0.5) label mix); random-init " + mname,
+        "config": {"workload": cfg_name, "arithmetic": arith,
                    "participants_per_round": n_part, "per_gpu": per_gpu, "fleet": n_fleet,
-                   "samples_per_client": n_samp, "batch": bs, "local_steps_per_client": steps_per_client,
+                   "samples_per_client": n_samp, "batch": bs, "local_steps_per_client": spc,
                    "budgets": "10..100 step 10", "theta": THETA, "scheduler": "resource-aware, dynamic parallelism",
-                   "parallelism": f"clients sharded over {world} GPU(s)" + (" (config 3: 200 over 8)"
-                                                                             if world < 8 else ""),
-                   "l2": "per-client weights + activations (~4 GB/round) exceed L2; no flush needed"},
+                   "parallelism": f"clients sharded over {world} GPU(s)",
+                   "l2": "per-client weights + activations (GBs per round) exceed L2; no flush needed"},
         "rounds_per_sec": args.steps / (ms / 1e3), "train_ms": train_ms,
+        "client_steps_per_round": total_steps / args.steps,
         "accuracy_last_round": counts[-1].item() / n_test,
-        "e2e": {"value": total_steps / e2e_s, "unit": "client-steps/s",
+        "e2e": {"value": e2e_steps / e2e_s, "unit": "client-steps/s",
                 "h2d_bytes_per_step": int(fed.last_h2d_bytes + per_gpu * 8), "d2h_bytes_per_step": 8,
-                "rounds_per_sec": args.steps / e2e_s,
-                "api": "ResnetFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"},
+                "rounds_per_sec": args.steps / e2e_s, "api": api},
         "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                     "traffic": None, "kernel": "train phase (one CUDA graph: implicit-GEMM grouped_gemm_kernel "
-                                                "launches + batch-norm / elementwise kernels)",
-                     "algorithmic_flop_per_launch": flops, "flop_per_sample": resnet_flop_per_sample(nc),
+                     "traffic": None, "kernel": kern, "algorithmic_flop_per_launch": flops, "flop_per_sample": fps,
                      "peak_source": src},
         "clocks": clocks.summary(),
-        "gpu_launches": None,
+        "gpu_launches": launches,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample, _, _ = resnet_cpu_reference(args.cpu_seconds, nc, bs)
+        v, cores, sample, _, _ = cifar_cpu_reference(args.cpu_seconds, nc, bs, model)
         res["cpu_baseline"] = {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port", "sample": sample}
     if dist is not None:
         dist.destroy_process_group()
@@ -1047,6 +1123,8 @@ def main():
         res = run_cnn(args, rank, world, local_rank)
     elif args.workload == "resnet":
         res = run_resnet(args, rank, world, local_rank)
+    elif args.workload == "mobilenet":
+        res = run_resnet(args, rank, world, local_rank, model="mobilenet")
     elif args.workload == "gemm":
         res = run_gemm(args, rank, world, local_rank)
     elif args.workload == "des":

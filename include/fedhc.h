@@ -327,6 +327,27 @@ int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, int n_client
 int fedhc_resnet_last_loss(void* ws, float* out, int n_clients, void* stream);
 int fedhc_resnet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
                       unsigned long long* correct, void* stream);
+/* CIFAR MobileNetV2 client engine (BASELINE config 4), same conventions as the ResNet engine: 3x3 stem,
+ * 17 inverted-residual blocks (1x1 expand, 3x3 depthwise, 1x1 linear projection; identity / 1x1 shortcut
+ * at stride 1), 1x1 head to 1280, average pool, linear.  Channels padded to multiples of 64 in the
+ * parameter vector (padding entries zero); batch multiple of 8, <= 32. */
+/* depthwise 3x3 (pad 1) modes of the MobileNetV2 engine: 0 forward, 1 data gradient, 2 weight gradient +
+ * SGD (out = fp32 master [G][9][C]); NHWC bf16 activations, w bf16 [G][9][C], C multiple of 64. */
+int fedhc_dw_conv(int mode, int G, int bp, int H, int C, int s, const void* x, const void* dy, const void* w,
+                  void* out, void* shadow, float lr, void* stream);
+int fedhc_mobilenet_param_count(int n_classes, int64_t* padded);
+int fedhc_mobilenet_param_offsets(int n_classes, int64_t* offsets, int cap, int* count);
+int fedhc_mobilenet_create(int max_clients, int batch, int n_classes, void** ws);
+int fedhc_mobilenet_destroy(void* ws);
+/* steps (host, optional): per-client local step counts, non-increasing, <= max_steps; step s runs only
+ * the clients with steps[i] > s (one CUDA graph per active-client count).  NULL: all run max_steps. */
+int fedhc_mobilenet_local_train(void* ws, const fedhc_client* clients, int n_clients, const int32_t* steps,
+                                const double* params, int max_steps, float lr, int use_graph, void* stream);
+int fedhc_mobilenet_last_loss(void* ws, float* out, int n_clients, void* stream);
+/* kernels launched by the workspace so far (graph kernel nodes + direct launches; eager steps excluded) */
+int fedhc_mobilenet_launch_count(void* ws, int64_t* out);
+int fedhc_mobilenet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                         unsigned long long* correct, void* stream);
 
 #ifdef __cplusplus
 }

@@ -758,6 +758,8 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   FEDHC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   p->kern = reinterpret_cast<const void*>(kern);
   p->grid = tiles < sms ? tiles : sms;
+  p->sms = sms;
+  p->tiles_per_g = tiles / a.G;
   return FEDHC_OK;
 }
 
@@ -863,13 +865,18 @@ int gemm_plan(const fedhc_gemm_args& a, GemmPlan* p, const ConvSpec* conv) {
   return a.M % 128 == 0 ? plan_n<128>(a, p) : plan_n<64>(a, p);
 }
 
-int gemm_run(const GemmPlan& p, cudaStream_t st) {
+int gemm_run(const GemmPlan& p, cudaStream_t st, int G_run) {
+  int G = p.G, grid = p.grid;
+  if (G_run > 0 && G_run < p.G) {
+    G = G_run;
+    grid = G * p.tiles_per_g < p.sms ? G * p.tiles_per_g : p.sms;
+  }
   void* args[] = {const_cast<CUtensorMap*>(&p.ma), const_cast<CUtensorMap*>(&p.mb), const_cast<CUtensorMap*>(&p.mo),
-                  const_cast<CUtensorMap*>(&p.ms), const_cast<CUtensorMap*>(&p.ml), const_cast<int*>(&p.G),
+                  const_cast<CUtensorMap*>(&p.ms), const_cast<CUtensorMap*>(&p.ml), &G,
                   const_cast<int*>(&p.M), const_cast<int*>(&p.N), const_cast<int*>(&p.K),
                   const_cast<int*>(&p.stages), const_cast<int*>(&p.nst), const_cast<Epilogue*>(&p.ep),
                   const_cast<ConvSpec*>(&p.conv)};
-  FEDHC_CUDA_TRY(cudaLaunchKernel(p.kern, dim3(p.grid), dim3(kThreads), args, p.smem, st));
+  FEDHC_CUDA_TRY(cudaLaunchKernel(p.kern, dim3(grid), dim3(kThreads), args, p.smem, st));
   return FEDHC_OK;
 }
 

@@ -51,6 +51,7 @@ struct GemmPlan {
   int G, M, N, K;
   const void* kern;
   int grid, smem, stages, nst;
+  int sms, tiles_per_g;  // persistent grid = min(G * tiles_per_g, sms)
 };
 
 // Validate a problem and build its plan (no launch).  Returns a FEDHC_* status.
@@ -59,7 +60,8 @@ struct GemmPlan {
 // dgrad: M = 256 * bp, N = 32, K = 1600; wgrad: M = 1024, N = 64, K = 256 * bp, SGD epilogue).
 int gemm_plan(const fedhc_gemm_args& a, GemmPlan* plan, const ConvSpec* conv = nullptr);
 // Launch a plan on a stream.
-int gemm_run(const GemmPlan& p, cudaStream_t st);
+// G_run in [1, p.G]: run only the first G_run groups (same maps and buffers); <= 0: all of them
+int gemm_run(const GemmPlan& p, cudaStream_t st, int G_run = 0);
 
 }  // namespace tc
 }  // namespace fedhc

@@ -189,7 +189,8 @@ class DeviceFederation:
         rec["delta"] = deltas.data_ptr() + np.arange(k, dtype=np.int64) * (deltas.stride(0) * 4)
         return rec
 
-    def descriptors(self, participants, meta, lr: float, deltas: torch.Tensor) -> torch.Tensor:
+    def descriptors(self, participants, meta, lr: float, deltas: torch.Tensor, rows=None) -> torch.Tensor:
+        """fedhc_client records on the device; record i writes its delta into deltas[rows[i]] (default i)."""
         descs = (_abi.Client * max(len(participants), 1))()
         xb, yb, pb = self.x.data_ptr(), self.y.data_ptr(), self._perm_dev.data_ptr() if self._perm_dev is not None \
             else 0
@@ -197,7 +198,7 @@ class DeviceFederation:
         for i, (cid, (at, n, steps, bs)) in enumerate(zip(participants, meta)):
             o, _ = self.offset[cid]
             descs[i] = _abi.Client(xb + o * F * 4, yb + o * 4, pb + at * 4, n, steps, bs, float(lr),
-                                   deltas[i].data_ptr())
+                                   deltas[i if rows is None else rows[i]].data_ptr())
         raw = torch.frombuffer(bytearray(descs), dtype=torch.uint8).pin_memory()
         return raw.to(self.x.device, non_blocking=True)
 
