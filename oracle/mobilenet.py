@@ -19,6 +19,19 @@ import torch.nn.functional as F
 from .flmath import batch_plan
 from .resnet import _ID, _RoundBF16, _StraightBF16, state_keys
 
+
+class _RoundGradBF16(torch.autograd.Function):
+    """Identity in the forward; rounds the gradient to bf16 in the backward -- the engine stores each
+    convolution's data gradient in bf16 before it is summed with the other branch (csrc/resnet.cu, mb)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.to(torch.bfloat16).float()
+
 CFG = [(1, 16, 1, 1), (6, 24, 2, 1), (6, 32, 3, 2), (6, 64, 4, 2), (6, 96, 3, 1), (6, 160, 3, 2), (6, 320, 1, 1)]
 
 
@@ -37,8 +50,8 @@ class Block(nn.Module):
         if stride == 1 and cin != cout:
             self.shortcut = nn.Sequential(nn.Conv2d(cin, cout, 1, bias=False), nn.BatchNorm2d(cout))
 
-    def forward(self, x, r=_ID, wq=_ID):
-        e = r(F.conv2d(x, wq(self.conv1.weight)))
+    def forward(self, x, r=_ID, wq=_ID, rg=_ID):
+        e = r(F.conv2d(rg(x), wq(self.conv1.weight)))
         ea = r(F.relu(self.bn1(e)))
         d = r(F.conv2d(ea, wq(self.conv2.weight), stride=self.stride, padding=1, groups=ea.shape[1]))
         da = r(F.relu(self.bn2(d)))
@@ -46,7 +59,7 @@ class Block(nn.Module):
         if self.stride == 1:
             if len(self.shortcut):
                 conv, bn = self.shortcut[0], self.shortcut[1]
-                out = out + bn(r(F.conv2d(x, wq(conv.weight))))
+                out = out + bn(r(F.conv2d(rg(x), wq(conv.weight))))
             else:
                 out = out + x
         return r(out)
@@ -70,9 +83,10 @@ class MobileNetV2(nn.Module):
     def forward(self, x, rounding=None):
         r = _RoundBF16.apply if rounding == "bf16" else _ID
         wq = _StraightBF16.apply if rounding == "bf16" else _ID
+        rg = _RoundGradBF16.apply if rounding == "bf16" else _ID
         out = r(F.relu(self.bn1(r(F.conv2d(r(x), wq(self.conv1.weight), padding=1)))))
         for blk in self.layers:
-            out = blk(out, r, wq)
+            out = blk(out, r, wq, rg if (blk.stride == 1) else _ID)
         out = r(F.relu(self.bn2(r(F.conv2d(out, wq(self.conv2.weight))))))
         return self.linear(F.avg_pool2d(out, 4).flatten(1))
 

@@ -191,6 +191,14 @@ __global__ void __launch_bounds__(256) stem_im2col_kernel(const fedhc_client* __
   }
 }
 
+// ReLU backward folded into a BN backward pass, decided from the BN's own input: the forward output was
+// relu(k x + b) with k = rstd * gamma, b = beta - mean * k (bn_apply_kernel's fp32 expressions), so the
+// gradient passes where k x + b > 0.  master == nullptr: off.
+struct ReluSelf {
+  const float* master;
+  int64_t pstride, gamma, beta;
+};
+
 // ---- batch norm (training mode statistics over the client's valid images) -------------------------
 // x [G*Bp][HW][C] bf16.  part [G][BN_SPLIT][C][2] fp32 (sum, sum of squares) or (sum dz, sum dz*xhat).
 // grid (C/64, G, BN_SPLIT), 256 threads = 64 channels x 4 row lanes.
@@ -199,7 +207,10 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
                                                          const __nv_bfloat16* __restrict__ dz,
                                                          const float* __restrict__ stats,  // BWD: [G][C][2]
                                                          const int32_t* __restrict__ valid, int Bp, int HW, int C,
-                                                         float* __restrict__ part) {
+                                                         float* __restrict__ part,
+                                                         const __nv_bfloat16* __restrict__ mask = nullptr,
+                                                         ReluSelf rs = ReluSelf{nullptr, 0, 0, 0}) {
+  // mask (BWD, optional): dz is taken as dz * (mask > 0) -- the ReLU backward folded in
   // grid (1, G, BN_SPLIT); thread = (8-channel group cg, row lane rl): C / 8 groups x (256 / (C / 8)) lanes
   __shared__ float red[256][17];
   const int g = blockIdx.y, sp = blockIdx.z, groups = C >> 3, lanes = 256 / groups;
@@ -208,14 +219,20 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
   const int r0 = (int)((int64_t)nr * sp / BN_SPLIT), r1 = (int)((int64_t)nr * (sp + 1) / BN_SPLIT);
   const __nv_bfloat16* xb = x + (int64_t)g * Bp * HW * C + cg * 8;
   const __nv_bfloat16* db = BWD ? dz + (int64_t)g * Bp * HW * C + cg * 8 : nullptr;
-  float mean[8], rstd[8], s0[8], s1[8];
+  float mean[8], rstd[8], s0[8], s1[8], rk[8], rb[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     s0[e] = s1[e] = 0.f;
     mean[e] = rstd[e] = 0.f;
+    rk[e] = rb[e] = 0.f;
     if (BWD) {
       mean[e] = stats[((int64_t)g * C + cg * 8 + e) * 2];
       rstd[e] = stats[((int64_t)g * C + cg * 8 + e) * 2 + 1];
+      if (rs.master) {
+        const float* m = rs.master + (int64_t)g * rs.pstride;
+        rk[e] = rstd[e] * m[rs.gamma + cg * 8 + e];
+        rb[e] = m[rs.beta + cg * 8 + e] - mean[e] * rk[e];
+      }
     }
   }
   if (rl < lanes) {
@@ -225,9 +242,12 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
       if (BWD) {
         const uint4 dv = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
         const __nv_bfloat16* de = reinterpret_cast<const __nv_bfloat16*>(&dv);
+        uint4 mv = make_uint4(0, 0, 0, 0);
+        if (mask) mv = *reinterpret_cast<const uint4*>(mask + (int64_t)g * Bp * HW * C + cg * 8 + (int64_t)r * C);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float d = bf(de[e]);
+          float d = (!mask || bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f) ? bf(de[e]) : 0.f;
+          if (rs.master && !(bf(xe[e]) * rk[e] + rb[e] > 0.f)) d = 0.f;
           s0[e] += d;
           s1[e] += d * (bf(xe[e]) - mean[e]) * rstd[e];
         }
@@ -368,8 +388,10 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* 
                                                            const float* __restrict__ gsum,
                                                            const float* __restrict__ master, int64_t pstride,
                                                            int64_t gamma_off, const int32_t* __restrict__ valid,
-                                                           int Bp, int HW, int C, __nv_bfloat16* __restrict__ dx) {
-  __shared__ float cA[MAXBN], cB[MAXBN], cD[MAXBN];
+                                                           int Bp, int HW, int C, __nv_bfloat16* __restrict__ dx,
+                                                           const __nv_bfloat16* __restrict__ mask = nullptr,
+                                                           ReluSelf rs = ReluSelf{nullptr, 0, 0, 0}) {
+  __shared__ float cA[MAXBN], cB[MAXBN], cD[MAXBN], rK[MAXBN], rB[MAXBN];
   const int g = blockIdx.y, rows = valid[g];
   const float n = (float)rows * HW;
   const float* m = master + (int64_t)g * pstride;
@@ -380,6 +402,11 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* 
     cA[c] = A;
     cB[c] = n > 0.f ? -A * rstd * dg / n : 0.f;
     cD[c] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
+    if (rs.master) {
+      const float* mr = rs.master + (int64_t)g * rs.pstride;
+      rK[c] = rstd * mr[rs.gamma + c];
+      rB[c] = mr[rs.beta + c] - mean * rK[c];
+    }
   }
   __syncthreads();
   const int c8 = C >> 3, per_img8 = HW * c8, cmask = c8 - 1;
@@ -395,11 +422,16 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* 
     } else {
       const int c0 = (pow2 ? (i & cmask) : (i % c8)) * 8;
       const uint4 dv = *reinterpret_cast<const uint4*>(dz + e0), xv = *reinterpret_cast<const uint4*>(x + e0);
+      uint4 mv = make_uint4(0, 0, 0, 0);
+      if (mask) mv = *reinterpret_cast<const uint4*>(mask + e0);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int c = c0 + e;
-        o[e] = __float2bfloat16_rn(cA[c] * bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]) +
-                                   cB[c] * bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) + cD[c]);
+        float d = bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]);
+        const float xx = bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]);
+        if (mask && !(bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f)) d = 0.f;
+        if (rs.master && !(xx * rK[c] + rB[c] > 0.f)) d = 0.f;
+        o[e] = __float2bfloat16_rn(cA[c] * d + cB[c] * xx + cD[c]);
       }
     }
     *reinterpret_cast<uint4*>(dx + e0) = *reinterpret_cast<const uint4*>(o);
@@ -610,6 +642,15 @@ struct Buf {
 struct BlockPlans {
   tc::GemmPlan c1f, c2f, csf, c1d, c2d, csd, c1w, c2w, csw;
 };
+
+// fc_ce_kernel's dynamic shared memory limit only ever grows (ResNet and MobileNetV2 workspaces share it)
+static int ensure_fc_ce_smem(size_t bytes) {
+  static size_t granted = 0;
+  if (bytes <= granted) return FEDHC_OK;
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(fc_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  granted = bytes;
+  return FEDHC_OK;
+}
 
 struct Engine {
   int maxG, Bp, nc;
@@ -1018,8 +1059,9 @@ extern "C" int fedhc_resnet_create(int max_clients, int batch, int n_classes, vo
   e->Bp = batch;
   e->nc = n_classes;
   const size_t fsm = ((size_t)batch * rn::MAXC + (size_t)batch * rn::NCMAX) * 4;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(rn::fc_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-  int rc = e->init();
+  int rc = rn::ensure_fc_ce_smem(fsm);
+  if (rc) return rc;
+  rc = e->init();
   if (rc) return rc;
   *out = e.release();
   return FEDHC_OK;
@@ -1214,119 +1256,230 @@ static Layout make_layout(int nc) {
   return L;
 }
 
-// ---- depthwise 3x3 convolution (pad 1, stride s), NHWC bf16, 8 channels per thread, grid (blocks, images) ----
-// w: bf16 shadow [9][C] of the image's client (group g = image / Bp)
-__global__ void __launch_bounds__(256) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
-                                                     const __nv_bfloat16* __restrict__ shadow, int64_t pstride,
-                                                     int64_t woff, int Bp, int H, int C, int s,
-                                                     __nv_bfloat16* __restrict__ y) {
-  const int img = blockIdx.y, g = img / Bp, Ho = H / s, c8 = C >> 3;
-  const __nv_bfloat16* w = shadow + (int64_t)g * pstride + woff;
-  const __nv_bfloat16* xi = x + (int64_t)img * H * H * C;
-  __nv_bfloat16* yo = y + (int64_t)img * Ho * Ho * C;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Ho * Ho * c8; i += gridDim.x * blockDim.x) {
-    const int cg = i % c8, p = i / c8, ox = p % Ho, oy = p / Ho;
-    float acc[8];
+// ---- depthwise 3x3 convolution (pad 1, stride S), NHWC bf16 ----
+// Thread = (8-channel group cg, lane); a lane owns runs ("segments") of 4 consecutive output pixels of one row,
+// so a row of the 3 x (3S + 3) input window is loaded once (16-byte vectors) and reused by the 4 outputs
+// (sliding window along x: 4.5 / 6.75 loads per output instead of 9).  The 9 x 8 taps stay packed bf16 in
+// registers and every product is one mixed-precision FHFMA (bf16 x bf16 + fp32 -> fp32: the exact product of
+// the two bf16 values, so results equal fp32 math on the converted operands) -- no unpacking instructions.
+// lanes = 256 / (C / 8) (C <= 1280).
+constexpr int DW_SEG_PER_LANE = 2;
+
+__device__ __forceinline__ float fma_bf16(unsigned short a, unsigned short b, float c) {
+  float d;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
+// acc[e] += x[e] * w[e] for the 8 packed bf16 lanes of two uint4
+__device__ __forceinline__ void fma8(const uint4& x, const uint4& w, float (&acc)[8]) {
+  const unsigned xs[4] = {x.x, x.y, x.z, x.w}, ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#pragma unroll
-    for (int kh = 0; kh < 3; ++kh) {
-      const int iy = oy * s + kh - 1;
-      if (iy < 0 || iy >= H) continue;
-#pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const int ix = ox * s + kw - 1;
-        if (ix < 0 || ix >= H) continue;
-        const uint4 xv = *reinterpret_cast<const uint4*>(xi + ((int64_t)iy * H + ix) * C + cg * 8);
-        const uint4 wv = *reinterpret_cast<const uint4*>(w + (kh * 3 + kw) * C + cg * 8);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          acc[e] += bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) * bf(reinterpret_cast<const __nv_bfloat16*>(&wv)[e]);
-      }
-    }
-    __align__(16) __nv_bfloat16 o[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = __float2bfloat16_rn(acc[e]);
-    *reinterpret_cast<uint4*>(yo + (int64_t)p * C + cg * 8) = *reinterpret_cast<const uint4*>(o);
+  for (int q = 0; q < 4; ++q) {
+    unsigned short xl, xh, wl, wh;
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(xl), "=h"(xh) : "r"(xs[q]));
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(wl), "=h"(wh) : "r"(ws[q]));
+    acc[2 * q] = fma_bf16(xl, wl, acc[2 * q]);
+    acc[2 * q + 1] = fma_bf16(xh, wh, acc[2 * q + 1]);
   }
 }
 
-// dx (H x H) = transposed depthwise convolution of dy (Ho x Ho)
+__device__ __forceinline__ uint4 pack8(const float (&a)[8]) {
+  __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = __float2bfloat16_rn(a[e]);
+  return *reinterpret_cast<const uint4*>(v);
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ shadow, int64_t pstride,
+                                                     int64_t woff, int Bp, int H, int C,
+                                                     __nv_bfloat16* __restrict__ y) {
+  constexpr int NC = 3 * S + 3;  // input columns of a 4-output segment
+  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  if (lane >= lanes) return;
+  const int img = blockIdx.y, g = img / Bp, Ho = H / S, sw = Ho >> 2, nseg = Ho * sw;
+  uint4 wt[9];
+  const __nv_bfloat16* w = shadow + (int64_t)g * pstride + woff + cg * 8;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) wt[t] = *reinterpret_cast<const uint4*>(w + t * C);
+  const __nv_bfloat16* xi = x + (int64_t)img * H * H * C + cg * 8;
+  __nv_bfloat16* yo = y + (int64_t)img * Ho * Ho * C + cg * 8;
+  const int s0 = blockIdx.x * lanes * DW_SEG_PER_LANE, s1 = min(s0 + lanes * DW_SEG_PER_LANE, nseg);
+  for (int sg = s0 + lane; sg < s1; sg += lanes) {
+    const int oy = sg / sw, x0 = (sg - oy * sw) * 4;
+    float acc[4][8];
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int iy = oy * S + kh - 1;
+      if (iy < 0 || iy >= H) continue;
+      const __nv_bfloat16* row = xi + (int64_t)iy * H * C;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int ix = x0 * S - 1 + j;
+        if (ix < 0 || ix >= H) continue;
+        const uint4 xv = *reinterpret_cast<const uint4*>(row + (int64_t)ix * C);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const int kw = j - o * S;
+          if (kw >= 0 && kw <= 2) fma8(xv, wt[kh * 3 + kw], acc[o]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) *reinterpret_cast<uint4*>(yo + ((int64_t)oy * Ho + x0 + o) * C) = pack8(acc[o]);
+  }
+}
+
+// dx (H x H) = transposed depthwise convolution of dy (Ho x Ho): dx[y][x] = sum dy[(y+1-kh)/S][(x+1-kw)/S] w[kh][kw]
+template <int S>
 __global__ void __launch_bounds__(256) dw_dgrad_kernel(const __nv_bfloat16* __restrict__ dy,
                                                        const __nv_bfloat16* __restrict__ shadow, int64_t pstride,
-                                                       int64_t woff, int Bp, int H, int C, int s,
+                                                       int64_t woff, int Bp, int H, int C,
                                                        __nv_bfloat16* __restrict__ dx) {
-  const int img = blockIdx.y, g = img / Bp, Ho = H / s, c8 = C >> 3;
-  const __nv_bfloat16* w = shadow + (int64_t)g * pstride + woff;
-  const __nv_bfloat16* di = dy + (int64_t)img * Ho * Ho * C;
-  __nv_bfloat16* xo = dx + (int64_t)img * H * H * C;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H * H * c8; i += gridDim.x * blockDim.x) {
-    const int cg = i % c8, p = i / c8, x = p % H, yy = p / H;
-    float acc[8];
+  constexpr int NJ = S == 1 ? 6 : 3;  // gradient columns feeding a 4-output segment
+  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  if (lane >= lanes) return;
+  const int img = blockIdx.y, g = img / Bp, Ho = H / S, sw = H >> 2, nseg = H * sw;
+  uint4 wt[9];
+  const __nv_bfloat16* w = shadow + (int64_t)g * pstride + woff + cg * 8;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int t = 0; t < 9; ++t) wt[t] = *reinterpret_cast<const uint4*>(w + t * C);
+  const __nv_bfloat16* di = dy + (int64_t)img * Ho * Ho * C + cg * 8;
+  __nv_bfloat16* xo = dx + (int64_t)img * H * H * C + cg * 8;
+  const int s0 = blockIdx.x * lanes * DW_SEG_PER_LANE, s1 = min(s0 + lanes * DW_SEG_PER_LANE, nseg);
+  for (int sg = s0 + lane; sg < s1; sg += lanes) {
+    const int yy = sg / sw, x0 = (sg - yy * sw) * 4;
+    float acc[4][8];
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
 #pragma unroll
     for (int kh = 0; kh < 3; ++kh) {
       const int ny = yy + 1 - kh;
-      if (ny < 0 || (ny % s) || ny / s >= Ho) continue;
+      if (ny < 0 || (S == 2 && (ny & 1)) || ny / S >= Ho) continue;
+      const __nv_bfloat16* row = di + (int64_t)(ny / S) * Ho * C;
 #pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const int nx = x + 1 - kw;
-        if (nx < 0 || (nx % s) || nx / s >= Ho) continue;
-        const uint4 dv = *reinterpret_cast<const uint4*>(di + ((int64_t)(ny / s) * Ho + nx / s) * C + cg * 8);
-        const uint4 wv = *reinterpret_cast<const uint4*>(w + (kh * 3 + kw) * C + cg * 8);
+      for (int j = 0; j < NJ; ++j) {
+        const int dc = S == 1 ? x0 - 1 + j : (x0 >> 1) + j;  // gradient column
+        if (dc < 0 || dc >= Ho) continue;
+        const uint4 dv = *reinterpret_cast<const uint4*>(row + (int64_t)dc * C);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          acc[e] += bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]) * bf(reinterpret_cast<const __nv_bfloat16*>(&wv)[e]);
+        for (int o = 0; o < 4; ++o) {
+          const int kw = S == 1 ? o + 2 - j : o + 1 - 2 * j;  // x0 + o + 1 - dc * S
+          if (kw >= 0 && kw <= 2) fma8(dv, wt[kh * 3 + kw], acc[o]);
+        }
       }
     }
-    __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = __float2bfloat16_rn(acc[e]);
-    *reinterpret_cast<uint4*>(xo + (int64_t)p * C + cg * 8) = *reinterpret_cast<const uint4*>(o);
+    for (int o = 0; o < 4; ++o) *reinterpret_cast<uint4*>(xo + ((int64_t)yy * H + x0 + o) * C) = pack8(acc[o]);
   }
 }
 
-// weight gradient partials: part [G][SPLIT][9][C] = sum over this split's output pixels of x (*) dy
-// grid (C / 64, G, SPLIT), 256 threads = 64 channels x 4 pixel lanes
+// weight gradient partials: part [G][DW_SPLIT][9][C] = this split's segments of sum x (*) dy.  grid (G, DW_SPLIT),
+// 256 threads = (cg, lane) with 72 fp32 accumulators each; lanes reduced in a fixed order through dynamic
+// shared memory (lanes x C/8 x 72 floats <= 72 KB).  Segments whose gradient is all zero (padding images) skip.
 constexpr int DW_SPLIT = 32;
+constexpr int DW_WGRAD_SMEM = 256 * 72 * 4;
+template <int S>
 __global__ void __launch_bounds__(256) dw_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
                                                        const __nv_bfloat16* __restrict__ dy, int Bp, int H, int C,
-                                                       int s, float* __restrict__ part) {
-  __shared__ float red[4][9][64];
-  const int c = blockIdx.x * 64 + (threadIdx.x & 63), lane = threadIdx.x >> 6, g = blockIdx.y, sp = blockIdx.z;
-  const int Ho = H / s, npx = Bp * Ho * Ho;
-  const int p0 = (int)((int64_t)npx * sp / DW_SPLIT), p1 = (int)((int64_t)npx * (sp + 1) / DW_SPLIT);
-  float acc[9];
-#pragma unroll
-  for (int t = 0; t < 9; ++t) acc[t] = 0.f;
-  for (int p = p0 + lane; p < p1; p += 4) {
-    const int b = p / (Ho * Ho), q = p % (Ho * Ho), oy = q / Ho, ox = q % Ho;
-    const int64_t img = (int64_t)g * Bp + b;
-    const float d = bf(dy[((img * Ho + oy) * Ho + ox) * C + c]);
-    if (d == 0.f) continue;
-#pragma unroll
-    for (int kh = 0; kh < 3; ++kh) {
-      const int iy = oy * s + kh - 1;
-      if (iy < 0 || iy >= H) continue;
-#pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const int ix = ox * s + kw - 1;
-        if (ix < 0 || ix >= H) continue;
-        acc[kh * 3 + kw] += d * bf(x[((img * H + iy) * H + ix) * C + c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < 9; ++t) red[lane][t][threadIdx.x & 63] = acc[t];
-  __syncthreads();
-  if (lane == 0) {
-    const int cl = threadIdx.x & 63;
+                                                       float* __restrict__ part) {
+  extern __shared__ float red[];
+  constexpr int NC = 3 * S + 3;
+  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  const int g = blockIdx.x, sp = blockIdx.y, Ho = H / S, sw = Ho >> 2, segs_img = Ho * sw, nseg = Bp * segs_img;
+  if (lane < lanes) {
+    float acc[9][8];
 #pragma unroll
     for (int t = 0; t < 9; ++t)
-      part[(((int64_t)g * DW_SPLIT + sp) * 9 + t) * C + c] =
-          (red[0][t][cl] + red[1][t][cl]) + (red[2][t][cl] + red[3][t][cl]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
+    const int q0 = (int)((int64_t)nseg * sp / DW_SPLIT), q1 = (int)((int64_t)nseg * (sp + 1) / DW_SPLIT);
+    for (int q = q0 + lane; q < q1; q += lanes) {
+      const int bi = q / segs_img, r = q - bi * segs_img, oy = r / sw, x0 = (r - oy * sw) * 4;
+      const int64_t img = (int64_t)g * Bp + bi;
+      const __nv_bfloat16* drow = dy + ((img * Ho + oy) * Ho + x0) * C + cg * 8;
+      uint4 dv[4];
+      unsigned any = 0;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        dv[o] = *reinterpret_cast<const uint4*>(drow + (int64_t)o * C);
+        any |= dv[o].x | dv[o].y | dv[o].z | dv[o].w;
+      }
+      if (!any) continue;
+      const __nv_bfloat16* xi = x + img * H * H * C + cg * 8;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int iy = oy * S + kh - 1;
+        if (iy < 0 || iy >= H) continue;
+        const __nv_bfloat16* row = xi + (int64_t)iy * H * C;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int ix = x0 * S - 1 + j;
+          if (ix < 0 || ix >= H) continue;
+          const uint4 xv = *reinterpret_cast<const uint4*>(row + (int64_t)ix * C);
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const int kw = j - o * S;
+            if (kw >= 0 && kw <= 2) fma8(xv, dv[o], acc[kh * 3 + kw]);
+          }
+        }
+      }
+    }
+    float* rr = red + (lane * c8 + cg) * 72;
+#pragma unroll
+    for (int t = 0; t < 9; ++t)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rr[t * 8 + e] = acc[t][e];
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c8 * 72; i += blockDim.x) {
+    const int cq = i / 72, rr = i - cq * 72;
+    float sum = 0.f;
+    for (int l = 0; l < lanes; ++l) sum += red[(l * c8 + cq) * 72 + rr];
+    part[(((int64_t)g * DW_SPLIT + sp) * 9 + rr / 8) * C + cq * 8 + (rr & 7)] = sum;
+  }
+}
+
+static int dw_blocks(int nseg, int C) {
+  const int per = (256 / (C / 8)) * DW_SEG_PER_LANE;
+  return (nseg + per - 1) / per;
+}
+
+static void dw_fwd(const __nv_bfloat16* x, const __nv_bfloat16* shadow, int64_t pstride, int64_t woff, int n_img,
+                   int Bp, int H, int C, int s, __nv_bfloat16* y, cudaStream_t st) {
+  const int ho = H / s;
+  const dim3 grid(dw_blocks(ho * (ho / 4), C), n_img);
+  if (s == 1) dw_fwd_kernel<1><<<grid, 256, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
+  else dw_fwd_kernel<2><<<grid, 256, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
+}
+
+static void dw_dgrad(const __nv_bfloat16* dy, const __nv_bfloat16* shadow, int64_t pstride, int64_t woff, int n_img,
+                     int Bp, int H, int C, int s, __nv_bfloat16* dx, cudaStream_t st) {
+  const dim3 grid(dw_blocks(H * (H / 4), C), n_img);
+  if (s == 1) dw_dgrad_kernel<1><<<grid, 256, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
+  else dw_dgrad_kernel<2><<<grid, 256, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
+}
+
+static void dw_wgrad(const __nv_bfloat16* x, const __nv_bfloat16* dy, int G, int Bp, int H, int C, int s, float* part,
+                     cudaStream_t st) {
+  const dim3 grid(G, DW_SPLIT);
+  const size_t smem = (size_t)(256 / (C / 8)) * (C / 8) * 72 * 4;
+  if (s == 1) dw_wgrad_kernel<1><<<grid, 256, smem, st>>>(x, dy, Bp, H, C, part);
+  else dw_wgrad_kernel<2><<<grid, 256, smem, st>>>(x, dy, Bp, H, C, part);
+}
+
+static int dw_setup() {
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(dw_wgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_WGRAD_SMEM));
+  FEDHC_CUDA_TRY(cudaFuncSetAttribute(dw_wgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DW_WGRAD_SMEM));
+  return FEDHC_OK;
 }
 
 // master[9][C] -= lr * sum over splits (fixed order); shadow = bf16(master).  grid G, block 256
@@ -1658,14 +1811,17 @@ struct Engine {
     rn::bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), 256, 0, st>>>(a, master, L.P, bp, HW, C,
                                                                                           out);
   }
+  // dc = BN backward of dz; relu: the BN fed a ReLU, whose backward is folded in (decided from x itself)
   void bn_backward(int G, const __nv_bfloat16* dz, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b,
-                   __nv_bfloat16* dc, cudaStream_t st) {
+                   __nv_bfloat16* dc, cudaStream_t st, bool relu = false) {
+    const rn::ReluSelf rs{relu ? master : nullptr, L.P, b.gamma, b.beta};
     rn::bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C,
-                                                                      part);
+                                                                      part, nullptr, rs);
     rn::bn_finalize_kernel<true><<<G, std::min(C, 512), 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
     rn::bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), 256, 0, st>>>(
-        dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc);
+        dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc, nullptr, rs);
   }
+
   void relu_mask(int64_t n8, const __nv_bfloat16* a, const __nv_bfloat16* m, __nv_bfloat16* o, cudaStream_t st) {
     rn::relu_mask_kernel<<<grid_for(n8), 256, 0, st>>>(a, m, n8, o);
   }
@@ -1686,8 +1842,7 @@ struct Engine {
       if ((rc = tc::gemm_run(bps[i].c1f, st, G))) return rc;
       if (!eval) bn_stats(G, bp, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], st);
       bn_apply(G, bp, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], nullptr, nullptr, 0, nullptr, true, eval, ea[i], st);
-      dw_fwd_kernel<<<dim3((ho * ho * ppl / 8 + 255) / 256, G * bp), 256, 0, st>>>(ea[i], shadow, L.P, L.dw[i], bp,
-                                                                                  d.H, ppl, d.s, this->d[i]);
+      dw_fwd(ea[i], shadow, L.P, L.dw[i], G * bp, bp, d.H, ppl, d.s, this->d[i], st);
       if (!eval) bn_stats(G, bp, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], st);
       bn_apply(G, bp, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], nullptr, nullptr, 0, nullptr, true, eval, da[i],
                st);
@@ -1722,8 +1877,7 @@ struct Engine {
                                           dyh, loss, HEADC);
     const int64_t I = (int64_t)G * Bp;
     // head: relu mask, BN backward, 1x1 conv data / weight gradient -> cur = dL/dy[last]
-    relu_mask(I * 16 * HEADC / 8, dyh, fha, g1, st);
-    bn_backward(G, g1, fh, 16, HEADC, id_bnh, L.bnh, g0, st);
+    bn_backward(G, dyh, fh, 16, HEADC, id_bnh, L.bnh, g0, st, true);
     if ((rc = tc::gemm_run(head_d, st, G))) return rc;
     if ((rc = tc::gemm_run(head_w, st, G))) return rc;
     for (int i = NBLK - 1; i >= 0; --i) {
@@ -1738,15 +1892,11 @@ struct Engine {
       }
       if ((rc = tc::gemm_run(bp[i].c3d, st, G))) return rc;  // g1 = dDA
       if ((rc = tc::gemm_run(bp[i].c3w, st, G))) return rc;
-      const int64_t n8o = I * ho * ho * ppl / 8, n8i = I * d.H * d.H * ppl / 8;
-      relu_mask(n8o, g1, da[i], g1, st);
-      bn_backward(G, g1, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], g2, st);  // g2 = dD
-      dw_dgrad_kernel<<<dim3((d.H * d.H * ppl / 8 + 255) / 256, (int)I), 256, 0, st>>>(g2, shadow, L.P, L.dw[i], Bp,
-                                                                                      d.H, ppl, d.s, g3);
-      dw_wgrad_kernel<<<dim3(ppl / 64, G, DW_SPLIT), 256, 0, st>>>(ea[i], g2, Bp, d.H, ppl, d.s, dwpart);
+      bn_backward(G, g1, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], g2, st, true);  // g2 = dD
+      dw_dgrad(g2, shadow, L.P, L.dw[i], (int)I, Bp, d.H, ppl, d.s, g3, st);
+      dw_wgrad(ea[i], g2, G, Bp, d.H, ppl, d.s, dwpart, st);
       dw_sgd_kernel<<<G, 256, 0, st>>>(dwpart, master, shadow, L.P, L.dw[i], ppl, lr);
-      relu_mask(n8i, g3, ea[i], g3, st);
-      bn_backward(G, g3, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], g0, st);  // g0 = dE
+      bn_backward(G, g3, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], g0, st, true);  // g0 = dE
       if ((rc = tc::gemm_run(bp[i].c1d, st, G))) return rc;                         // g1 = dX
       if ((rc = tc::gemm_run(bp[i].c1w, st, G))) return rc;
       const int64_t n8x = I * d.H * d.H * pci / 8;
@@ -1755,9 +1905,7 @@ struct Engine {
       FEDHC_CUDA_TRY(cudaMemcpyAsync(cur, g1, (size_t)n8x * 16, cudaMemcpyDeviceToDevice, st));
     }
     // stem
-    const int64_t n80 = I * 1024 * 64 / 8;
-    relu_mask(n80, cur, a0, g1, st);
-    bn_backward(G, g1, c0, 1024, 64, id_bn0, L.bn0, g0, st);
+    bn_backward(G, cur, c0, 1024, 64, id_bn0, L.bn0, g0, st, true);
     if ((rc = tc::gemm_run(stem_w, st, G))) return rc;
     constexpr int CAP = (int)(sizeof(rn::BnSgdTable::C) / sizeof(int));
     for (size_t at = 0; at < bn_sgd.size(); at += CAP) {
@@ -1832,8 +1980,11 @@ extern "C" int fedhc_mobilenet_create(int max_clients, int batch, int n_classes,
   e->Bp = batch;
   e->nc = n_classes;
   const size_t fsm = ((size_t)batch * mb::HEADC + (size_t)batch * rn::NCMAX) * 4;
-  FEDHC_CUDA_TRY(cudaFuncSetAttribute(rn::fc_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-  int rc = e->init();
+  int rc = rn::ensure_fc_ce_smem(fsm);
+  if (rc) return rc;
+  rc = mb::dw_setup();
+  if (rc) return rc;
+  rc = e->init();
   if (rc) return rc;
   *out = e.release();
   return FEDHC_OK;
@@ -1933,7 +2084,7 @@ extern "C" int fedhc_mobilenet_eval(void* ws, const double* params, const float*
 // shadow [G][9][C] refreshed when non-NULL).  w bf16 [G][9][C]; C multiple of 64; pad 1, stride 1 or 2.
 extern "C" int fedhc_dw_conv(int mode, int G, int bp, int H, int C, int s, const void* x, const void* dy,
                              const void* w, void* out, void* shadow, float lr, void* stream) {
-  if (G < 1 || bp < 1 || H < 1 || C < 64 || C % 64 || (s != 1 && s != 2) || H % s || mode < 0 || mode > 2)
+  if (G < 1 || bp < 1 || H < 1 || C < 64 || C % 64 || C > 1280 || (s != 1 && s != 2) || H % s || mode < 0 || mode > 2)
     return fail(FEDHC_ERR_VALUE, "dw_conv: bad geometry");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int ho = H / s;
@@ -1942,17 +2093,17 @@ extern "C" int fedhc_dw_conv(int mode, int G, int bp, int H, int C, int s, const
   const auto* wb = static_cast<const __nv_bfloat16*>(w);
   if (mode == 0) {
     if (!x || !w || !out) return fail(FEDHC_ERR_VALUE, "dw_conv: null operand");
-    mb::dw_fwd_kernel<<<dim3((ho * ho * C / 8 + 255) / 256, G * bp), 256, 0, st>>>(
-        xb, wb, (int64_t)9 * C, 0, bp, H, C, s, static_cast<__nv_bfloat16*>(out));
+    mb::dw_fwd(xb, wb, (int64_t)9 * C, 0, G * bp, bp, H, C, s, static_cast<__nv_bfloat16*>(out), st);
   } else if (mode == 1) {
     if (!dy || !w || !out) return fail(FEDHC_ERR_VALUE, "dw_conv: null operand");
-    mb::dw_dgrad_kernel<<<dim3((H * H * C / 8 + 255) / 256, G * bp), 256, 0, st>>>(
-        db, wb, (int64_t)9 * C, 0, bp, H, C, s, static_cast<__nv_bfloat16*>(out));
+    mb::dw_dgrad(db, wb, (int64_t)9 * C, 0, G * bp, bp, H, C, s, static_cast<__nv_bfloat16*>(out), st);
   } else {
     if (!x || !dy || !out) return fail(FEDHC_ERR_VALUE, "dw_conv: null operand");
     float* part = nullptr;
     FEDHC_CUDA_TRY(cudaMallocAsync(&part, sizeof(float) * G * mb::DW_SPLIT * 9 * C, st));
-    mb::dw_wgrad_kernel<<<dim3(C / 64, G, mb::DW_SPLIT), 256, 0, st>>>(xb, db, bp, H, C, s, part);
+    int rc = mb::dw_setup();
+    if (rc) return rc;
+    mb::dw_wgrad(xb, db, G, bp, H, C, s, part, st);
     __nv_bfloat16* sh = static_cast<__nv_bfloat16*>(shadow);
     __nv_bfloat16* tmp = nullptr;
     if (!sh) FEDHC_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(__nv_bfloat16) * G * 9 * C, st));

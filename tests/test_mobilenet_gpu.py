@@ -92,7 +92,8 @@ def test_mobilenet_local_train_vs_oracle(msetup):
     ill-conditioned than ResNet-18's: rounding the activations to bf16 alone moves most per-tensor deltas
     by 60-100% (spread = rel(bf16 oracle, fp32 oracle)), and some tensors' exact gradients vanish by
     symmetry (BN bias / running mean behind a BN-linear-BN chain) so only rounding noise is left
-    (spread > 2).  Bars: padding entries stay zero; noise-dominated tensors within 2 x spread of fp32;
+    (spread > 2).  Bars: padding entries stay zero; noise-dominated tensors no larger than 3 x the
+    oracles' noise;
     running statistics (the forward) within 0.75 x spread + 1e-2 of the bf16-faithful oracle (observed
     0 in the first blocks); every other tensor within 1.5 x spread + 2e-2 of fp32 and closer to the
     bf16 oracle than 1.25 x the fp32 distance (e16 <= 1.25 spread + 2e-2).  The functional check is the
@@ -123,8 +124,8 @@ def test_mobilenet_local_train_vs_oracle(msetup):
                 continue
             spread = _rel(b16[k], f32[k])
             e16, e32 = _rel(got[k], b16[k]), _rel(got[k], f32[k])
-            if spread > 2:
-                ok = e32 <= 2 * spread
+            if spread > 2:  # vanishing by symmetry: only rounding noise, compare magnitudes
+                ok = np.linalg.norm(got[k]) <= 3 * max(np.linalg.norm(b16[k]), np.linalg.norm(f32[k])) + 1e-6
             elif k.endswith(("running_mean", "running_var")):
                 ok = e16 <= 0.75 * spread + 1e-2
             else:
@@ -178,9 +179,10 @@ def test_mobilenet_update_decreases_loss_like_oracle(msetup):
 
 
 def test_mobilenet_loss_trajectory_matches_oracle(msetup):
-    """Mean CE loss of the last local step after 1, 2 and 4 SGD steps within 5% of the fp32 oracle
-    (observed 0.1% / 1.7% / 3.6%: at lr 0.05 the early trajectory of this network is jumpy and the bf16
-    oracle itself drifts by up to 1%)."""
+    """Mean CE loss of the last local step after 1, 2, 4 and 8 SGD steps within 3% of the fp32 oracle at
+    lr 0.01 (observed <= 1.4%, the bf16-faithful oracle's own drift is the same size).  At lr 0.05 this
+    network's first steps are chaotic (the loss jumps up at step 4 in every arithmetic) and the bf16
+    trajectories drift 5-9% from fp32 by step 6-8, so the trajectory is checked where it is stable."""
     import numpy as np
     import torch
     from oracle import flmath as fm
@@ -188,21 +190,19 @@ def test_mobilenet_loss_trajectory_matches_oracle(msetup):
     from paper_2305_15668_b200 import training as tr
     from paper_2305_15668_b200.mobilenet import MobilenetFederation
     s = msetup
-    C = s["C"]
+    C, lr = s["C"], 0.01
     trn, tst = tr.make_synthetic_dataset(3072, C, 800, 23)
     shards = tr.partition_noniid(trn, [("t0", 256)], 0.5, 4)
     fed = MobilenetFederation(shards, tst, 3072, C).attach_engine(1, 32)
     params = torch.tensor(fed.layout.to_padded(s["p"]), dtype=torch.float64, device="cuda")
     p32 = {k: v.astype(np.float32).astype(np.float64) for k, v in s["p"].items()}
     seeds = [fm.seed_of("train", 1, 0, "t0")]
+    _, l32 = omb.local_train_mobilenet(p32, shards["t0"].features, shards["t0"].labels, 256, 32, lr, seeds[0], C)
     res = []
-    for steps in (1, 2, 4):
-        fed.train(params, ["t0"], [_WL(32 * steps, 32)], 0.05, seeds)
-        got = float(fed.engine.last_loss(1).cpu()[0])
-        _, l32 = omb.local_train_mobilenet(p32, shards["t0"].features, shards["t0"].labels, 32 * steps, 32, 0.05,
-                                           seeds[0], C)
-        res.append((steps, got, l32[-1]))
-    assert all(abs(g - w) <= 0.05 * abs(w) for _, g, w in res), res
+    for steps in (1, 2, 4, 8):
+        fed.train(params, ["t0"], [_WL(32 * steps, 32)], lr, seeds)
+        res.append((steps, float(fed.engine.last_loss(1).cpu()[0]), l32[steps - 1]))
+    assert all(abs(g - w) <= 0.03 * abs(w) for _, g, w in res), res
 
 
 def test_mobilenet_graph_equals_eager(msetup):
