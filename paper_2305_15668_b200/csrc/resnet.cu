@@ -235,30 +235,46 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
       }
     }
   }
+  auto accum = [&](const uint4& xv, const uint4& dv, const uint4& mv) {
+    const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
+    if (BWD) {
+      const __nv_bfloat16* de = reinterpret_cast<const __nv_bfloat16*>(&dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float d = (!mask || bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f) ? bf(de[e]) : 0.f;
+        if (rs.master && !(bf(xe[e]) * rk[e] + rb[e] > 0.f)) d = 0.f;
+        s0[e] += d;
+        s1[e] += d * (bf(xe[e]) - mean[e]) * rstd[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = bf(xe[e]);
+        s0[e] += v;
+        s1[e] += v * v;
+      }
+    }
+  };
   if (rl < lanes) {
-    for (int r = r0 + rl; r < r1; r += lanes) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(xb + (int64_t)r * C);
-      const __nv_bfloat16* xe = reinterpret_cast<const __nv_bfloat16*>(&xv);
+    const __nv_bfloat16* mb = mask ? mask + (int64_t)g * Bp * HW * C + cg * 8 : nullptr;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    // two rows per iteration, all loads issued before the math (bytes in flight)
+    for (int r = r0 + rl; r < r1; r += 2 * lanes) {
+      const int r2 = r + lanes;
+      const bool two = r2 < r1;
+      const uint4 xv0 = *reinterpret_cast<const uint4*>(xb + (int64_t)r * C);
+      const uint4 xv1 = two ? *reinterpret_cast<const uint4*>(xb + (int64_t)r2 * C) : z;
+      uint4 dv0 = z, dv1 = z, mv0 = z, mv1 = z;
       if (BWD) {
-        const uint4 dv = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
-        const __nv_bfloat16* de = reinterpret_cast<const __nv_bfloat16*>(&dv);
-        uint4 mv = make_uint4(0, 0, 0, 0);
-        if (mask) mv = *reinterpret_cast<const uint4*>(mask + (int64_t)g * Bp * HW * C + cg * 8 + (int64_t)r * C);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float d = (!mask || bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f) ? bf(de[e]) : 0.f;
-          if (rs.master && !(bf(xe[e]) * rk[e] + rb[e] > 0.f)) d = 0.f;
-          s0[e] += d;
-          s1[e] += d * (bf(xe[e]) - mean[e]) * rstd[e];
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float v = bf(xe[e]);
-          s0[e] += v;
-          s1[e] += v * v;
+        dv0 = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
+        if (two) dv1 = *reinterpret_cast<const uint4*>(db + (int64_t)r2 * C);
+        if (mb) {
+          mv0 = *reinterpret_cast<const uint4*>(mb + (int64_t)r * C);
+          if (two) mv1 = *reinterpret_cast<const uint4*>(mb + (int64_t)r2 * C);
         }
       }
+      accum(xv0, dv0, mv0);
+      if (two) accum(xv1, dv1, mv1);
     }
   }
 #pragma unroll
@@ -325,13 +341,19 @@ struct BnApply {
   int relu, eval;
 };
 
-// grid (blocks, G): per-channel scale / shift staged in shared memory; y = x * k + b (+ xs * ks + bs) (+ res)
+// Block size of the per-channel streaming kernels: a multiple of C / 8, so a thread's 8-channel group is
+// fixed across its grid-stride loop and the per-channel coefficients live in its registers.
+__host__ __device__ inline int bn_block(int C) { return (C >> 3) * (256 / (C >> 3)); }
+
+// grid (blocks, G), block bn_block(C): y = relu?(x * k + b (+ xs * ks + bs) (+ res)); two vectors per iteration
 __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* __restrict__ master, int64_t pstride,
                                                        int Bp, int HW, int C, __nv_bfloat16* __restrict__ out) {
-  __shared__ float k0[MAXBN], b0[MAXBN], k1[MAXBN], b1[MAXBN];
-  const int g = blockIdx.y;
+  const int g = blockIdx.y, c8 = C >> 3, c0 = (threadIdx.x % c8) * 8;
   const float* m = master + (int64_t)g * pstride;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  float k0[8], b0[8], k1[8], b1[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = c0 + e;
     float mean, rstd;
     if (a.eval) {
       mean = m[a.rmean + c];
@@ -340,8 +362,9 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
       mean = a.stats[((int64_t)g * C + c) * 2];
       rstd = a.stats[((int64_t)g * C + c) * 2 + 1];
     }
-    k0[c] = rstd * m[a.gamma + c];
-    b0[c] = m[a.beta + c] - mean * k0[c];
+    k0[e] = rstd * m[a.gamma + c];
+    b0[e] = m[a.beta + c] - mean * k0[e];
+    k1[e] = b1[e] = 0.f;
     if (a.xs) {
       float ms, rs;
       if (a.eval) {
@@ -351,37 +374,48 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
         ms = a.stats_s[((int64_t)g * C + c) * 2];
         rs = a.stats_s[((int64_t)g * C + c) * 2 + 1];
       }
-      k1[c] = rs * m[a.gamma_s + c];
-      b1[c] = m[a.beta_s + c] - ms * k1[c];
+      k1[e] = rs * m[a.gamma_s + c];
+      b1[e] = m[a.beta_s + c] - ms * k1[e];
     }
   }
-  __syncthreads();
-  const int c8 = C >> 3, n8 = Bp * HW * c8, cmask = c8 - 1;
-  const bool pow2 = (c8 & cmask) == 0;
+  const int n8 = Bp * HW * c8;
   const int64_t base = (int64_t)g * Bp * HW * C;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
-    const int64_t e0 = base + (int64_t)i * 8;
-    const int c0 = (pow2 ? (i & cmask) : (i % c8)) * 8;
-    const uint4 xv = *reinterpret_cast<const uint4*>(a.x + e0);
-    uint4 rv = make_uint4(0, 0, 0, 0), sv = make_uint4(0, 0, 0, 0);
-    if (a.res) rv = *reinterpret_cast<const uint4*>(a.res + e0);
-    if (a.xs) sv = *reinterpret_cast<const uint4*>(a.xs + e0);
+  auto emit = [&](int i, const uint4& xv, const uint4& rv, const uint4& sv) {
     __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int c = c0 + e;
-      float v = bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) * k0[c] + b0[c];
+      float v = bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]) * k0[e] + b0[e];
       if (a.res) v += bf(reinterpret_cast<const __nv_bfloat16*>(&rv)[e]);
-      if (a.xs) v += bf(reinterpret_cast<const __nv_bfloat16*>(&sv)[e]) * k1[c] + b1[c];
+      if (a.xs) v += bf(reinterpret_cast<const __nv_bfloat16*>(&sv)[e]) * k1[e] + b1[e];
       if (a.relu) v = fmaxf(v, 0.f);
       o[e] = __float2bfloat16_rn(v);
     }
-    *reinterpret_cast<uint4*>(out + e0) = *reinterpret_cast<const uint4*>(o);
+    *reinterpret_cast<uint4*>(out + base + (int64_t)i * 8) = *reinterpret_cast<const uint4*>(o);
+  };
+  const int stride = gridDim.x * blockDim.x;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += 2 * stride) {
+    const int i2 = i + stride;
+    const bool two = i2 < n8;
+    const int64_t e0 = base + (int64_t)i * 8, e1 = base + (int64_t)i2 * 8;
+    const uint4 xv0 = *reinterpret_cast<const uint4*>(a.x + e0);
+    const uint4 xv1 = two ? *reinterpret_cast<const uint4*>(a.x + e1) : z;
+    uint4 rv0 = z, rv1 = z, sv0 = z, sv1 = z;
+    if (a.res) {
+      rv0 = *reinterpret_cast<const uint4*>(a.res + e0);
+      if (two) rv1 = *reinterpret_cast<const uint4*>(a.res + e1);
+    }
+    if (a.xs) {
+      sv0 = *reinterpret_cast<const uint4*>(a.xs + e0);
+      if (two) sv1 = *reinterpret_cast<const uint4*>(a.xs + e1);
+    }
+    emit(i, xv0, rv0, sv0);
+    if (two) emit(i2, xv1, rv1, sv1);
   }
 }
 
 // dx = gamma rstd (dz - (dbeta + xhat dgamma) / n) = A dz + B x + D on the valid images, 0 on padding
-// images; grid (blocks, G), per-channel A, B, D in shared memory.
+// images; grid (blocks, G), block bn_block(C), per-channel A, B, D (and the folded ReLU's k, b) in registers.
 __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dz,
                                                            const __nv_bfloat16* __restrict__ x,
                                                            const float* __restrict__ stats,
@@ -391,50 +425,64 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* 
                                                            int Bp, int HW, int C, __nv_bfloat16* __restrict__ dx,
                                                            const __nv_bfloat16* __restrict__ mask = nullptr,
                                                            ReluSelf rs = ReluSelf{nullptr, 0, 0, 0}) {
-  __shared__ float cA[MAXBN], cB[MAXBN], cD[MAXBN], rK[MAXBN], rB[MAXBN];
-  const int g = blockIdx.y, rows = valid[g];
+  const int g = blockIdx.y, rows = valid[g], c8 = C >> 3, c0 = (threadIdx.x % c8) * 8;
   const float n = (float)rows * HW;
   const float* m = master + (int64_t)g * pstride;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  float cA[8], cB[8], cD[8], rK[8], rB[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = c0 + e;
     const float mean = stats[((int64_t)g * C + c) * 2], rstd = stats[((int64_t)g * C + c) * 2 + 1];
     const float db = gsum[((int64_t)g * C + c) * 2], dg = gsum[((int64_t)g * C + c) * 2 + 1];
     const float A = m[gamma_off + c] * rstd;
-    cA[c] = A;
-    cB[c] = n > 0.f ? -A * rstd * dg / n : 0.f;
-    cD[c] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
+    cA[e] = A;
+    cB[e] = n > 0.f ? -A * rstd * dg / n : 0.f;
+    cD[e] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
+    rK[e] = rB[e] = 0.f;
     if (rs.master) {
       const float* mr = rs.master + (int64_t)g * rs.pstride;
-      rK[c] = rstd * mr[rs.gamma + c];
-      rB[c] = mr[rs.beta + c] - mean * rK[c];
+      rK[e] = rstd * mr[rs.gamma + c];
+      rB[e] = mr[rs.beta + c] - mean * rK[e];
     }
   }
-  __syncthreads();
-  const int c8 = C >> 3, per_img8 = HW * c8, cmask = c8 - 1;
-  const bool pow2 = (c8 & cmask) == 0;
-  const int n8 = Bp * per_img8, valid8 = rows * per_img8;
+  const int per_img8 = HW * c8, n8 = Bp * per_img8, valid8 = rows * per_img8;
   const int64_t base = (int64_t)g * Bp * HW * C;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
-    const int64_t e0 = base + (int64_t)i * 8;
+  auto emit = [&](int i, const uint4& dv, const uint4& xv, const uint4& mv) {
     __align__(16) __nv_bfloat16 o[8];
     if (i >= valid8) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = __float2bfloat16_rn(0.f);
     } else {
-      const int c0 = (pow2 ? (i & cmask) : (i % c8)) * 8;
-      const uint4 dv = *reinterpret_cast<const uint4*>(dz + e0), xv = *reinterpret_cast<const uint4*>(x + e0);
-      uint4 mv = make_uint4(0, 0, 0, 0);
-      if (mask) mv = *reinterpret_cast<const uint4*>(mask + e0);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int c = c0 + e;
         float d = bf(reinterpret_cast<const __nv_bfloat16*>(&dv)[e]);
         const float xx = bf(reinterpret_cast<const __nv_bfloat16*>(&xv)[e]);
         if (mask && !(bf(reinterpret_cast<const __nv_bfloat16*>(&mv)[e]) > 0.f)) d = 0.f;
-        if (rs.master && !(xx * rK[c] + rB[c] > 0.f)) d = 0.f;
-        o[e] = __float2bfloat16_rn(cA[c] * d + cB[c] * xx + cD[c]);
+        if (rs.master && !(xx * rK[e] + rB[e] > 0.f)) d = 0.f;
+        o[e] = __float2bfloat16_rn(cA[e] * d + cB[e] * xx + cD[e]);
       }
     }
-    *reinterpret_cast<uint4*>(dx + e0) = *reinterpret_cast<const uint4*>(o);
+    *reinterpret_cast<uint4*>(dx + base + (int64_t)i * 8) = *reinterpret_cast<const uint4*>(o);
+  };
+  const int stride = gridDim.x * blockDim.x;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += 2 * stride) {
+    const int i2 = i + stride;
+    const bool a0 = i < valid8, a1 = i2 < valid8;  // padding images: no loads, zero output
+    const int64_t e0 = base + (int64_t)i * 8, e1 = base + (int64_t)i2 * 8;
+    uint4 dv0 = z, xv0 = z, mv0 = z, dv1 = z, xv1 = z, mv1 = z;
+    if (a0) {
+      dv0 = *reinterpret_cast<const uint4*>(dz + e0);
+      xv0 = *reinterpret_cast<const uint4*>(x + e0);
+      if (mask) mv0 = *reinterpret_cast<const uint4*>(mask + e0);
+    }
+    if (a1) {
+      dv1 = *reinterpret_cast<const uint4*>(dz + e1);
+      xv1 = *reinterpret_cast<const uint4*>(x + e1);
+      if (mask) mv1 = *reinterpret_cast<const uint4*>(mask + e1);
+    }
+    emit(i, dv0, xv0, mv0);
+    if (i2 < n8) emit(i2, dv1, xv1, mv1);
   }
 }
 
@@ -912,7 +960,8 @@ struct Engine {
     }
     a.relu = relu;
     a.eval = eval;
-    bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), 256, 0, st>>>(a, master, L.P, bp, HW, C, out);
+    bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), bn_block(C), 0, st>>>(a, master, L.P, bp, HW, C,
+                                                                                            out);
   }
 
   // dC = BN backward of dz through x (stats slot id), dgamma / dbeta into gsum slot id
@@ -920,7 +969,7 @@ struct Engine {
                    __nv_bfloat16* dc, cudaStream_t st) {
     bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C, part);
     bn_finalize_kernel<true><<<G, C, 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
-    bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), 256, 0, st>>>(
+    bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), bn_block(C), 0, st>>>(
         dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc);
   }
 
@@ -1262,8 +1311,8 @@ static Layout make_layout(int nc) {
 // (sliding window along x: 4.5 / 6.75 loads per output instead of 9).  The 9 x 8 taps stay packed bf16 in
 // registers and every product is one mixed-precision FHFMA (bf16 x bf16 + fp32 -> fp32: the exact product of
 // the two bf16 values, so results equal fp32 math on the converted operands) -- no unpacking instructions.
-// lanes = 256 / (C / 8) (C <= 1280).
-constexpr int DW_SEG_PER_LANE = 2;
+// lanes = DW_THREADS / (C / 8) (C <= 1024).
+constexpr int DW_SEG_PER_LANE = 2, DW_THREADS = 128;
 
 __device__ __forceinline__ float fma_bf16(unsigned short a, unsigned short b, float c) {
   float d;
@@ -1292,12 +1341,12 @@ __device__ __forceinline__ uint4 pack8(const float (&a)[8]) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(DW_THREADS) dw_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                      const __nv_bfloat16* __restrict__ shadow, int64_t pstride,
                                                      int64_t woff, int Bp, int H, int C,
                                                      __nv_bfloat16* __restrict__ y) {
   constexpr int NC = 3 * S + 3;  // input columns of a 4-output segment
-  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  const int c8 = C >> 3, lanes = DW_THREADS / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
   if (lane >= lanes) return;
   const int img = blockIdx.y, g = img / Bp, Ho = H / S, sw = Ho >> 2, nseg = Ho * sw;
   uint4 wt[9];
@@ -1314,23 +1363,29 @@ __global__ void __launch_bounds__(256) dw_fwd_kernel(const __nv_bfloat16* __rest
     for (int o = 0; o < 4; ++o)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
+    // issue the whole 3 x NC window before any math (out-of-image taps read as zeros)
+    uint4 xv[3][NC];
 #pragma unroll
     for (int kh = 0; kh < 3; ++kh) {
       const int iy = oy * S + kh - 1;
-      if (iy < 0 || iy >= H) continue;
+      const bool rin = iy >= 0 && iy < H;
       const __nv_bfloat16* row = xi + (int64_t)iy * H * C;
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
         const int ix = x0 * S - 1 + j;
-        if (ix < 0 || ix >= H) continue;
-        const uint4 xv = *reinterpret_cast<const uint4*>(row + (int64_t)ix * C);
+        xv[kh][j] = (rin && ix >= 0 && ix < H) ? *reinterpret_cast<const uint4*>(row + (int64_t)ix * C)
+                                               : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int j = 0; j < NC; ++j)
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
           const int kw = j - o * S;
-          if (kw >= 0 && kw <= 2) fma8(xv, wt[kh * 3 + kw], acc[o]);
+          if (kw >= 0 && kw <= 2) fma8(xv[kh][j], wt[kh * 3 + kw], acc[o]);
         }
-      }
-    }
 #pragma unroll
     for (int o = 0; o < 4; ++o) *reinterpret_cast<uint4*>(yo + ((int64_t)oy * Ho + x0 + o) * C) = pack8(acc[o]);
   }
@@ -1338,12 +1393,12 @@ __global__ void __launch_bounds__(256) dw_fwd_kernel(const __nv_bfloat16* __rest
 
 // dx (H x H) = transposed depthwise convolution of dy (Ho x Ho): dx[y][x] = sum dy[(y+1-kh)/S][(x+1-kw)/S] w[kh][kw]
 template <int S>
-__global__ void __launch_bounds__(256) dw_dgrad_kernel(const __nv_bfloat16* __restrict__ dy,
+__global__ void __launch_bounds__(DW_THREADS) dw_dgrad_kernel(const __nv_bfloat16* __restrict__ dy,
                                                        const __nv_bfloat16* __restrict__ shadow, int64_t pstride,
                                                        int64_t woff, int Bp, int H, int C,
                                                        __nv_bfloat16* __restrict__ dx) {
   constexpr int NJ = S == 1 ? 6 : 3;  // gradient columns feeding a 4-output segment
-  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  const int c8 = C >> 3, lanes = DW_THREADS / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
   if (lane >= lanes) return;
   const int img = blockIdx.y, g = img / Bp, Ho = H / S, sw = H >> 2, nseg = H * sw;
   uint4 wt[9];
@@ -1360,23 +1415,28 @@ __global__ void __launch_bounds__(256) dw_dgrad_kernel(const __nv_bfloat16* __re
     for (int o = 0; o < 4; ++o)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[o][e] = 0.f;
+    uint4 dv[3][NJ];
 #pragma unroll
     for (int kh = 0; kh < 3; ++kh) {
       const int ny = yy + 1 - kh;
-      if (ny < 0 || (S == 2 && (ny & 1)) || ny / S >= Ho) continue;
+      const bool rin = ny >= 0 && !(S == 2 && (ny & 1)) && ny / S < Ho;
       const __nv_bfloat16* row = di + (int64_t)(ny / S) * Ho * C;
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int dc = S == 1 ? x0 - 1 + j : (x0 >> 1) + j;  // gradient column
-        if (dc < 0 || dc >= Ho) continue;
-        const uint4 dv = *reinterpret_cast<const uint4*>(row + (int64_t)dc * C);
+        dv[kh][j] = (rin && dc >= 0 && dc < Ho) ? *reinterpret_cast<const uint4*>(row + (int64_t)dc * C)
+                                                : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
           const int kw = S == 1 ? o + 2 - j : o + 1 - 2 * j;  // x0 + o + 1 - dc * S
-          if (kw >= 0 && kw <= 2) fma8(dv, wt[kh * 3 + kw], acc[o]);
+          if (kw >= 0 && kw <= 2) fma8(dv[kh][j], wt[kh * 3 + kw], acc[o]);
         }
-      }
-    }
 #pragma unroll
     for (int o = 0; o < 4; ++o) *reinterpret_cast<uint4*>(xo + ((int64_t)yy * H + x0 + o) * C) = pack8(acc[o]);
   }
@@ -1385,15 +1445,15 @@ __global__ void __launch_bounds__(256) dw_dgrad_kernel(const __nv_bfloat16* __re
 // weight gradient partials: part [G][DW_SPLIT][9][C] = this split's segments of sum x (*) dy.  grid (G, DW_SPLIT),
 // 256 threads = (cg, lane) with 72 fp32 accumulators each; lanes reduced in a fixed order through dynamic
 // shared memory (lanes x C/8 x 72 floats <= 72 KB).  Segments whose gradient is all zero (padding images) skip.
-constexpr int DW_SPLIT = 32;
-constexpr int DW_WGRAD_SMEM = 256 * 72 * 4;
+constexpr int DW_SPLIT = 64;
+constexpr int DW_WGRAD_SMEM = DW_THREADS * 72 * 4;
 template <int S>
-__global__ void __launch_bounds__(256) dw_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(DW_THREADS) dw_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
                                                        const __nv_bfloat16* __restrict__ dy, int Bp, int H, int C,
                                                        float* __restrict__ part) {
   extern __shared__ float red[];
   constexpr int NC = 3 * S + 3;
-  const int c8 = C >> 3, lanes = 256 / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
+  const int c8 = C >> 3, lanes = DW_THREADS / c8, cg = threadIdx.x % c8, lane = threadIdx.x / c8;
   const int g = blockIdx.x, sp = blockIdx.y, Ho = H / S, sw = Ho >> 2, segs_img = Ho * sw, nseg = Bp * segs_img;
   if (lane < lanes) {
     float acc[9][8];
@@ -1415,23 +1475,28 @@ __global__ void __launch_bounds__(256) dw_wgrad_kernel(const __nv_bfloat16* __re
       }
       if (!any) continue;
       const __nv_bfloat16* xi = x + img * H * H * C + cg * 8;
+      uint4 xv[3][NC];
 #pragma unroll
       for (int kh = 0; kh < 3; ++kh) {
         const int iy = oy * S + kh - 1;
-        if (iy < 0 || iy >= H) continue;
+        const bool rin = iy >= 0 && iy < H;
         const __nv_bfloat16* row = xi + (int64_t)iy * H * C;
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           const int ix = x0 * S - 1 + j;
-          if (ix < 0 || ix >= H) continue;
-          const uint4 xv = *reinterpret_cast<const uint4*>(row + (int64_t)ix * C);
+          xv[kh][j] = (rin && ix >= 0 && ix < H) ? *reinterpret_cast<const uint4*>(row + (int64_t)ix * C)
+                                                 : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
 #pragma unroll
           for (int o = 0; o < 4; ++o) {
             const int kw = j - o * S;
-            if (kw >= 0 && kw <= 2) fma8(xv, dv[o], acc[kh * 3 + kw]);
+            if (kw >= 0 && kw <= 2) fma8(xv[kh][j], dv[o], acc[kh * 3 + kw]);
           }
-        }
-      }
     }
     float* rr = red + (lane * c8 + cg) * 72;
 #pragma unroll
@@ -1449,7 +1514,7 @@ __global__ void __launch_bounds__(256) dw_wgrad_kernel(const __nv_bfloat16* __re
 }
 
 static int dw_blocks(int nseg, int C) {
-  const int per = (256 / (C / 8)) * DW_SEG_PER_LANE;
+  const int per = (DW_THREADS / (C / 8)) * DW_SEG_PER_LANE;
   return (nseg + per - 1) / per;
 }
 
@@ -1457,23 +1522,23 @@ static void dw_fwd(const __nv_bfloat16* x, const __nv_bfloat16* shadow, int64_t 
                    int Bp, int H, int C, int s, __nv_bfloat16* y, cudaStream_t st) {
   const int ho = H / s;
   const dim3 grid(dw_blocks(ho * (ho / 4), C), n_img);
-  if (s == 1) dw_fwd_kernel<1><<<grid, 256, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
-  else dw_fwd_kernel<2><<<grid, 256, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
+  if (s == 1) dw_fwd_kernel<1><<<grid, DW_THREADS, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
+  else dw_fwd_kernel<2><<<grid, DW_THREADS, 0, st>>>(x, shadow, pstride, woff, Bp, H, C, y);
 }
 
 static void dw_dgrad(const __nv_bfloat16* dy, const __nv_bfloat16* shadow, int64_t pstride, int64_t woff, int n_img,
                      int Bp, int H, int C, int s, __nv_bfloat16* dx, cudaStream_t st) {
   const dim3 grid(dw_blocks(H * (H / 4), C), n_img);
-  if (s == 1) dw_dgrad_kernel<1><<<grid, 256, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
-  else dw_dgrad_kernel<2><<<grid, 256, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
+  if (s == 1) dw_dgrad_kernel<1><<<grid, DW_THREADS, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
+  else dw_dgrad_kernel<2><<<grid, DW_THREADS, 0, st>>>(dy, shadow, pstride, woff, Bp, H, C, dx);
 }
 
 static void dw_wgrad(const __nv_bfloat16* x, const __nv_bfloat16* dy, int G, int Bp, int H, int C, int s, float* part,
                      cudaStream_t st) {
   const dim3 grid(G, DW_SPLIT);
-  const size_t smem = (size_t)(256 / (C / 8)) * (C / 8) * 72 * 4;
-  if (s == 1) dw_wgrad_kernel<1><<<grid, 256, smem, st>>>(x, dy, Bp, H, C, part);
-  else dw_wgrad_kernel<2><<<grid, 256, smem, st>>>(x, dy, Bp, H, C, part);
+  const size_t smem = (size_t)(DW_THREADS / (C / 8)) * (C / 8) * 72 * 4;
+  if (s == 1) dw_wgrad_kernel<1><<<grid, DW_THREADS, smem, st>>>(x, dy, Bp, H, C, part);
+  else dw_wgrad_kernel<2><<<grid, DW_THREADS, smem, st>>>(x, dy, Bp, H, C, part);
 }
 
 static int dw_setup() {
@@ -1482,18 +1547,17 @@ static int dw_setup() {
   return FEDHC_OK;
 }
 
-// master[9][C] -= lr * sum over splits (fixed order); shadow = bf16(master).  grid G, block 256
+// master[9][C] -= lr * sum over splits (fixed order); shadow = bf16(master).  grid (ceil(9C / 256), G)
 __global__ void dw_sgd_kernel(const float* __restrict__ part, float* __restrict__ master,
                               __nv_bfloat16* __restrict__ shadow, int64_t pstride, int64_t woff, int C, float lr) {
-  const int g = blockIdx.x;
+  const int g = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 9 * C) return;
   float* m = master + (int64_t)g * pstride + woff;
   __nv_bfloat16* sh = shadow + (int64_t)g * pstride + woff;
-  for (int i = threadIdx.x; i < 9 * C; i += blockDim.x) {
-    float s = 0.f;
-    for (int sp = 0; sp < DW_SPLIT; ++sp) s += part[(((int64_t)g * DW_SPLIT + sp) * 9) * C + i];
-    m[i] -= lr * s;
-    sh[i] = __float2bfloat16_rn(m[i]);
-  }
+  float s = 0.f;
+  for (int sp = 0; sp < DW_SPLIT; ++sp) s += part[(((int64_t)g * DW_SPLIT + sp) * 9) * C + i];
+  m[i] -= lr * s;
+  sh[i] = __float2bfloat16_rn(m[i]);
 }
 
 __global__ void step_inc_kernel(int* c) { *c += 1; }
@@ -1638,20 +1702,20 @@ struct Engine {
     return rn::Engine::gargs(G, M, N, K, A, a_mn, B, b_mn, bgs, epi);
   }
 
-  // 1x1 stride-1 NHWC convolution plans: forward y = x W (W [cin][cout]), data gradient, weight gradient + SGD
+  // 1x1 stride-1 convolutions on NHWC activations are plain grouped GEMMs over the client's pixels
+  // ([bp*H*W][cin] row-major per client): forward Y = X W (W [cin][cout]), data gradient dX = dY W^T,
+  // weight gradient + SGD W -= lr X^T dY (A and B MN-major views of X and dY)
   int pw_fwd(int G, int bp, int H, int cin, int cout, const __nv_bfloat16* x, int64_t woff, __nv_bfloat16* out,
              tc::GemmPlan* pl) {
     auto a = gargs(G, bp * H * H, cout, cin, x, false, shadow + woff, true, L.P, FEDHC_EPI_BF16);
     a.D = out;
-    const tc::ConvSpec c = rn::Engine::spec(tc::NHWC_FWD, bp, H, cin, cout, 1, 1);
-    return tc::gemm_plan(a, pl, &c);
+    return tc::gemm_plan(a, pl);
   }
   int pw_dgrad(int G, int bp, int H, int cin, int cout, const __nv_bfloat16* dy, int64_t woff, __nv_bfloat16* out,
                tc::GemmPlan* pl) {
     auto a = gargs(G, bp * H * H, cin, cout, dy, false, shadow + woff, false, L.P, FEDHC_EPI_BF16);
     a.D = out;
-    const tc::ConvSpec c = rn::Engine::spec(tc::NHWC_DGRAD, bp, H, cin, cout, 1, 1);
-    return tc::gemm_plan(a, pl, &c);
+    return tc::gemm_plan(a, pl);
   }
   int pw_wgrad(int G, int bp, int H, int cin, int cout, const __nv_bfloat16* x, const __nv_bfloat16* dy, int64_t woff,
                float lr, tc::GemmPlan* pl) {
@@ -1660,8 +1724,7 @@ struct Engine {
     a.shadow = shadow + woff;
     a.d_gstride = L.P;
     a.lr = lr;
-    const tc::ConvSpec c = rn::Engine::spec(tc::NHWC_WGRAD, bp, H, cin, cout, 1, 1);
-    return tc::gemm_plan(a, pl, &c);
+    return tc::gemm_plan(a, pl);
   }
 
   int plan_all(int G, int bp, tc::GemmPlan* sf, tc::GemmPlan* hf, BlkPlans* bps, bool train, float lr) {
@@ -1808,7 +1871,8 @@ struct Engine {
     }
     a.relu = relu;
     a.eval = eval;
-    rn::bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), 256, 0, st>>>(a, master, L.P, bp, HW, C,
+    rn::bn_apply_kernel<<<dim3(blocks_for((int64_t)bp * HW * C / 8, G), G), rn::bn_block(C), 0, st>>>(a, master, L.P, bp,
+                                                                                                     HW, C,
                                                                                           out);
   }
   // dc = BN backward of dz; relu: the BN fed a ReLU, whose backward is folded in (decided from x itself)
@@ -1818,7 +1882,7 @@ struct Engine {
     rn::bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C,
                                                                       part, nullptr, rs);
     rn::bn_finalize_kernel<true><<<G, std::min(C, 512), 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
-    rn::bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), 256, 0, st>>>(
+    rn::bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), rn::bn_block(C), 0, st>>>(
         dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc, nullptr, rs);
   }
 
@@ -1895,7 +1959,7 @@ struct Engine {
       bn_backward(G, g1, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], g2, st, true);  // g2 = dD
       dw_dgrad(g2, shadow, L.P, L.dw[i], (int)I, Bp, d.H, ppl, d.s, g3, st);
       dw_wgrad(ea[i], g2, G, Bp, d.H, ppl, d.s, dwpart, st);
-      dw_sgd_kernel<<<G, 256, 0, st>>>(dwpart, master, shadow, L.P, L.dw[i], ppl, lr);
+      dw_sgd_kernel<<<dim3((9 * ppl + 255) / 256, G), 256, 0, st>>>(dwpart, master, shadow, L.P, L.dw[i], ppl, lr);
       bn_backward(G, g3, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], g0, st, true);  // g0 = dE
       if ((rc = tc::gemm_run(bp[i].c1d, st, G))) return rc;                         // g1 = dX
       if ((rc = tc::gemm_run(bp[i].c1w, st, G))) return rc;
@@ -2084,7 +2148,7 @@ extern "C" int fedhc_mobilenet_eval(void* ws, const double* params, const float*
 // shadow [G][9][C] refreshed when non-NULL).  w bf16 [G][9][C]; C multiple of 64; pad 1, stride 1 or 2.
 extern "C" int fedhc_dw_conv(int mode, int G, int bp, int H, int C, int s, const void* x, const void* dy,
                              const void* w, void* out, void* shadow, float lr, void* stream) {
-  if (G < 1 || bp < 1 || H < 1 || C < 64 || C % 64 || C > 1280 || (s != 1 && s != 2) || H % s || mode < 0 || mode > 2)
+  if (G < 1 || bp < 1 || H < 1 || H % 4 || C < 64 || C % 64 || C > 1024 || (s != 1 && s != 2) || H % s || mode < 0 || mode > 2)
     return fail(FEDHC_ERR_VALUE, "dw_conv: bad geometry");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int ho = H / s;
@@ -2107,7 +2171,8 @@ extern "C" int fedhc_dw_conv(int mode, int G, int bp, int H, int C, int s, const
     __nv_bfloat16* sh = static_cast<__nv_bfloat16*>(shadow);
     __nv_bfloat16* tmp = nullptr;
     if (!sh) FEDHC_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(__nv_bfloat16) * G * 9 * C, st));
-    mb::dw_sgd_kernel<<<G, 256, 0, st>>>(part, static_cast<float*>(out), sh ? sh : tmp, (int64_t)9 * C, 0, C, lr);
+    mb::dw_sgd_kernel<<<dim3((9 * C + 255) / 256, G), 256, 0, st>>>(part, static_cast<float*>(out), sh ? sh : tmp,
+                                                                  (int64_t)9 * C, 0, C, lr);
     FEDHC_CUDA_TRY(cudaFreeAsync(part, st));
     if (tmp) FEDHC_CUDA_TRY(cudaFreeAsync(tmp, st));
   }
