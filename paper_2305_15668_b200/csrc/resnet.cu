@@ -258,23 +258,14 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
   if (rl < lanes) {
     const __nv_bfloat16* mb = mask ? mask + (int64_t)g * Bp * HW * C + cg * 8 : nullptr;
     const uint4 z = make_uint4(0, 0, 0, 0);
-    // two rows per iteration, all loads issued before the math (bytes in flight)
-    for (int r = r0 + rl; r < r1; r += 2 * lanes) {
-      const int r2 = r + lanes;
-      const bool two = r2 < r1;
-      const uint4 xv0 = *reinterpret_cast<const uint4*>(xb + (int64_t)r * C);
-      const uint4 xv1 = two ? *reinterpret_cast<const uint4*>(xb + (int64_t)r2 * C) : z;
-      uint4 dv0 = z, dv1 = z, mv0 = z, mv1 = z;
+    for (int r = r0 + rl; r < r1; r += lanes) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xb + (int64_t)r * C);
+      uint4 dv = z, mv = z;
       if (BWD) {
-        dv0 = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
-        if (two) dv1 = *reinterpret_cast<const uint4*>(db + (int64_t)r2 * C);
-        if (mb) {
-          mv0 = *reinterpret_cast<const uint4*>(mb + (int64_t)r * C);
-          if (two) mv1 = *reinterpret_cast<const uint4*>(mb + (int64_t)r2 * C);
-        }
+        dv = *reinterpret_cast<const uint4*>(db + (int64_t)r * C);
+        if (mb) mv = *reinterpret_cast<const uint4*>(mb + (int64_t)r * C);
       }
-      accum(xv0, dv0, mv0);
-      if (two) accum(xv1, dv1, mv1);
+      accum(xv, dv, mv);
     }
   }
 #pragma unroll
@@ -348,12 +339,12 @@ __host__ __device__ inline int bn_block(int C) { return (C >> 3) * (256 / (C >> 
 // grid (blocks, G), block bn_block(C): y = relu?(x * k + b (+ xs * ks + bs) (+ res)); two vectors per iteration
 __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* __restrict__ master, int64_t pstride,
                                                        int Bp, int HW, int C, __nv_bfloat16* __restrict__ out) {
+  // per-channel coefficients: computed once per block into shared memory, then each thread keeps its
+  // 8 channels' values in registers (its channel group is fixed, see bn_block)
+  __shared__ __align__(16) float sk0[MAXBN], sb0[MAXBN], sk1[MAXBN], sb1[MAXBN];
   const int g = blockIdx.y, c8 = C >> 3, c0 = (threadIdx.x % c8) * 8;
   const float* m = master + (int64_t)g * pstride;
-  float k0[8], b0[8], k1[8], b1[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int c = c0 + e;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float mean, rstd;
     if (a.eval) {
       mean = m[a.rmean + c];
@@ -362,9 +353,9 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
       mean = a.stats[((int64_t)g * C + c) * 2];
       rstd = a.stats[((int64_t)g * C + c) * 2 + 1];
     }
-    k0[e] = rstd * m[a.gamma + c];
-    b0[e] = m[a.beta + c] - mean * k0[e];
-    k1[e] = b1[e] = 0.f;
+    sk0[c] = rstd * m[a.gamma + c];
+    sb0[c] = m[a.beta + c] - mean * sk0[c];
+    sk1[c] = sb1[c] = 0.f;
     if (a.xs) {
       float ms, rs;
       if (a.eval) {
@@ -374,9 +365,18 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(BnApply a, const float* _
         ms = a.stats_s[((int64_t)g * C + c) * 2];
         rs = a.stats_s[((int64_t)g * C + c) * 2 + 1];
       }
-      k1[e] = rs * m[a.gamma_s + c];
-      b1[e] = m[a.beta_s + c] - ms * k1[e];
+      sk1[c] = rs * m[a.gamma_s + c];
+      sb1[c] = m[a.beta_s + c] - ms * sk1[c];
     }
+  }
+  __syncthreads();
+  float k0[8], b0[8], k1[8], b1[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    k0[e] = sk0[c0 + e];
+    b0[e] = sb0[c0 + e];
+    k1[e] = sk1[c0 + e];
+    b1[e] = sb1[c0 + e];
   }
   const int n8 = Bp * HW * c8;
   const int64_t base = (int64_t)g * Bp * HW * C;
@@ -425,25 +425,33 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __nv_bfloat16* 
                                                            int Bp, int HW, int C, __nv_bfloat16* __restrict__ dx,
                                                            const __nv_bfloat16* __restrict__ mask = nullptr,
                                                            ReluSelf rs = ReluSelf{nullptr, 0, 0, 0}) {
+  __shared__ __align__(16) float sA[MAXBN], sB[MAXBN], sD[MAXBN], sK[MAXBN], sR[MAXBN];
   const int g = blockIdx.y, rows = valid[g], c8 = C >> 3, c0 = (threadIdx.x % c8) * 8;
   const float n = (float)rows * HW;
   const float* m = master + (int64_t)g * pstride;
-  float cA[8], cB[8], cD[8], rK[8], rB[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int c = c0 + e;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const float mean = stats[((int64_t)g * C + c) * 2], rstd = stats[((int64_t)g * C + c) * 2 + 1];
     const float db = gsum[((int64_t)g * C + c) * 2], dg = gsum[((int64_t)g * C + c) * 2 + 1];
     const float A = m[gamma_off + c] * rstd;
-    cA[e] = A;
-    cB[e] = n > 0.f ? -A * rstd * dg / n : 0.f;
-    cD[e] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
-    rK[e] = rB[e] = 0.f;
+    sA[c] = A;
+    sB[c] = n > 0.f ? -A * rstd * dg / n : 0.f;
+    sD[c] = n > 0.f ? -A * db / n + A * rstd * dg * mean / n : 0.f;
+    sK[c] = sR[c] = 0.f;
     if (rs.master) {
       const float* mr = rs.master + (int64_t)g * rs.pstride;
-      rK[e] = rstd * mr[rs.gamma + c];
-      rB[e] = mr[rs.beta + c] - mean * rK[e];
+      sK[c] = rstd * mr[rs.gamma + c];
+      sR[c] = mr[rs.beta + c] - mean * sK[c];
     }
+  }
+  __syncthreads();
+  float cA[8], cB[8], cD[8], rK[8], rB[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    cA[e] = sA[c0 + e];
+    cB[e] = sB[c0 + e];
+    cD[e] = sD[c0 + e];
+    rK[e] = sK[c0 + e];
+    rB[e] = sR[c0 + e];
   }
   const int per_img8 = HW * c8, n8 = Bp * per_img8, valid8 = rows * per_img8;
   const int64_t base = (int64_t)g * Bp * HW * C;
