@@ -38,7 +38,11 @@ namespace fedhc {
 namespace tc {
 
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+// warps: 0 TMA producer, 1 MMA issuer, 2 .. 2 + 4 * kEpiHalves - 1 epilogue.  Epilogues without loads
+// (bf16 / fp32 / bias-ReLU stores) split each tile's 32-column chunks over two warps per TMEM lane quadrant
+// (short-K GEMMs are epilogue-latency bound); load epilogues (SGD, ReLU mask) and row sums use one.
+constexpr int kEpiHalves = 2;
+constexpr int kThreads = 64 + 128 * kEpiHalves;
 
 // WIN: windowed implicit-GEMM convolution stages (0 = one K block per stage).  A stage holds a
 // 12-row x 16-column activation window (192 rows of 128 B, loaded once) plus the weights of the 5 taps
@@ -54,7 +58,7 @@ struct Cfg {
   static constexpr int kTaps = (WIN == 1 || WIN == 2) ? 5 : 3;  // taps sharing one window (one kernel column)
   static constexpr int kTileBBytes = WIN ? kTaps * kTapBBytes : kTapBBytes;
   static constexpr int kStageBytes = kTileABytes + kTileBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;  // double-buffered fp32 accumulator (power-of-two allocation)
 };
 
 // M=64 accumulators occupy TMEM lanes 0-15 of each 32-lane quadrant (row = 16*q + lane,
@@ -170,9 +174,13 @@ constexpr int kEpiLoad = 4;
 template <int BM>
 __host__ __device__ constexpr int epi_slot_bytes() { return (BM / 4) * 128; }
 
+__host__ __device__ constexpr int epi_halves(int kind, bool rowsum) {
+  return (epi_loads(kind) || rowsum) ? 1 : kEpiHalves;
+}
+
 template <int BM>
-__host__ __device__ constexpr int epi_bytes(int kind, int nst) {
-  return 4 * (nst + (epi_loads(kind) ? kEpiLoad : 0)) * epi_slot_bytes<BM>();
+__host__ __device__ constexpr int epi_bytes(int kind, int nst, bool rowsum) {
+  return 4 * (epi_halves(kind, rowsum) * nst + (epi_loads(kind) ? kEpiLoad : 0)) * epi_slot_bytes<BM>();
 }
 
 __device__ __forceinline__ uint32_t sw128_off(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
@@ -290,8 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int kind = ep.kind;
   const bool loads = epi_loads(kind);
-  unsigned char* st_buf = smem + STAGES * kStageBytes;            // [4 warps][nst] slots
-  unsigned char* ld_buf = st_buf + 4 * nst * kSlot;                // [4 warps][kEpiLoad] slots (if loads)
+  const int nh = epi_halves(kind, ep.rowsum != nullptr);           // epilogue warps per lane quadrant
+  unsigned char* st_buf = smem + STAGES * kStageBytes;            // [4 * nh warps][nst] slots
+  unsigned char* ld_buf = st_buf + 4 * nh * nst * kSlot;           // [4 warps][kEpiLoad] slots (if loads)
   uint64_t* full = reinterpret_cast<uint64_t*>(ld_buf + (loads ? 4 * kEpiLoad * kSlot : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], 4 * nh);  // one arrive per active epilogue warp
     }
     for (int i = 0; i < 4 * kEpiLoad; ++i) {
       mbar_init(&lfull[i], 1);
@@ -460,10 +469,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4: thread = one output row
+  } else if (warp - 2 < 4 * nh) {
+    // epilogue warps -> TMEM lane quadrant q = warp % 4: thread = one output row; half h takes chunks
+    // c = h, h + nh, ... of each tile
     // (M=64: lanes 0-15 of the quadrant hold rows 16*q + lane)
-    const int q = warp & 3;
+    const int q = warp & 3, h = (warp - 2) >> 2, widx = h * 4 + q;
     const bool active = lane < R;
     const int rr = active ? lane : 0;
     int it = 0;
@@ -480,12 +490,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                               ? ep.bias[(int64_t)g * ep.bias_gstride + row] : 0.f;
       float rsum = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c, ++u) {
+      for (int c = h; c < BN / 32; c += nh, ++u) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
         const int lslot = q * kEpiLoad + (int)(u % kEpiLoad);
         unsigned char* lb = ld_buf + lslot * kSlot;
-        unsigned char* sb = st_buf + (q * nst + (int)(u % nst)) * kSlot;
+        unsigned char* sb = st_buf + (widx * nst + (int)(u % nst)) * kSlot;
         if (loads) mbar_wait(&lfull[lslot], (u / kEpiLoad) & 1);
         if (active) {
           if (kind == FEDHC_EPI_SGD) {
@@ -744,7 +754,7 @@ static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
   // (load epilogues keep 2: their in-place SGD stores read the load slot, released one chunk later)
   int nst = (a.K / BK <= 4 && !epi_loads(kind)) ? 8 : 2, stages = 0, fixed = 0;
   for (;; nst /= 2) {
-    fixed = 1024 + epi_bytes<BM>(kind, nst) + 512;  // alignment slack + epilogue staging + barriers
+    fixed = 1024 + epi_bytes<BM>(kind, nst, a.rowsum != nullptr) + 512;  // alignment slack + epilogue staging + barriers
     stages = (max_smem - fixed) / Cfg<BM, BN, WIN>::kStageBytes;
     if (stages >= 3 || nst == 2) break;
   }

@@ -336,7 +336,7 @@ def test_tcgen05_grouped_gemm_vs_torch(fh, G, M, N, K):
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("G,M,N,K", [(1, 128, 64, 64), (3, 256, 192, 320), (2, 128, 256, 1024), (4, 384, 128, 128),
                                      (3, 64, 64, 2048), (2, 64, 2048, 64), (5, 192, 96, 128), (2, 64, 32, 512),
-                                     (3, 256, 32, 64)])
+                                     (3, 256, 32, 64), (2, 128, 576, 64), (2, 64, 960, 128)])
 def test_gemm_operand_majors_vs_torch(fh, a_mn, b_mn, G, M, N, K):
     """Every operand storage (K- or MN-major) and N tile (64/128/256) against torch fp32."""
     import torch
