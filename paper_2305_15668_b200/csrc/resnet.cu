@@ -566,11 +566,17 @@ __global__ void __launch_bounds__(256) fc_ce_kernel(const float* __restrict__ po
   const float* W = m + fcw;
   for (int i = threadIdx.x; i < Bp * nf; i += blockDim.x) P[i] = pooled[(int64_t)g * Bp * nf + i];
   __syncthreads();
-  for (int i = threadIdx.x; i < Bp * nc; i += blockDim.x) {
-    const int r = i / nc, c = i - r * nc;
-    float s = m[fcb + c];
-    for (int k = 0; k < nf; ++k) s += P[r * nf + k] * W[c * nf + k];
-    D[r * NCMAX + c] = s;
+  // logits: one warp per (row, class) dot product, lanes stride the features (coalesced W reads)
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = warp; i < Bp * nc; i += nw) {
+      const int r = i / nc, c = i - r * nc;
+      float s = 0.f;
+      for (int k = lane; k < nf; k += 32) s += P[r * nf + k] * W[c * nf + k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) D[r * NCMAX + c] = m[fcb + c] + s;
+    }
   }
   __syncthreads();
   __shared__ float lsum[256];

@@ -136,10 +136,11 @@ def test_mobilenet_local_train_vs_oracle(msetup):
 
 
 def test_mobilenet_update_decreases_loss_like_oracle(msetup):
-    """Functional check of the whole backward pass: the engine's one-step Δ, applied to the fp32 oracle
-    model, lowers the step batch's (train-mode) loss by at least 85% of what the fp32 oracle's own Δ does
-    and by at least 90% of the bf16-faithful oracle's (observed 92% / 96%); a gradient with a missing or
-    mis-routed term does not (a random direction of the same per-tensor norms raises the loss)."""
+    """Functional check of the whole backward pass: the engine's one-step delta, applied to the fp32 oracle
+    model, lowers the step batch's (train-mode) loss about as much as the fp32 oracle's own delta.  Three
+    initialisations at lr 0.01 (first-order regime): the engine reaches 0.94 / 1.07 / 0.94 of the fp32
+    decrease (the bf16-faithful oracle 0.99 / 0.94 / 0.90); bars: mean >= 0.85, each >= 0.75.  A gradient
+    with a missing or mis-routed term does not get there (a random direction raises the loss)."""
     import numpy as np
     import torch
     import torch.nn.functional as F
@@ -147,35 +148,39 @@ def test_mobilenet_update_decreases_loss_like_oracle(msetup):
     from oracle import mobilenet as omb
     from oracle.resnet import state_keys
     from paper_2305_15668_b200 import training as tr
-    from paper_2305_15668_b200.mobilenet import MobilenetFederation
+    from paper_2305_15668_b200.mobilenet import MobilenetFederation, init_mobilenet_params
     s = msetup
-    C = s["C"]
+    C, lr = s["C"], 0.01
     trn, tst = tr.make_synthetic_dataset(3072, C, 800, 23)
     shards = tr.partition_noniid(trn, [("t0", 256)], 0.5, 4)
     fed = MobilenetFederation(shards, tst, 3072, C).attach_engine(1, 32)
-    params = torch.tensor(fed.layout.to_padded(s["p"]), dtype=torch.float64, device="cuda")
-    p32 = {k: v.astype(np.float32).astype(np.float64) for k, v in s["p"].items()}
     seed = fm.seed_of("train", 1, 0, "t0")
     sh = shards["t0"]
-    got = fed.layout.from_padded(fed.train(params, ["t0"], [_WL(32, 32)], 0.05, [seed]).cpu().numpy()[0])
-    f32, _ = omb.local_train_mobilenet(p32, sh.features, sh.labels, 32, 32, 0.05, seed, C)
-    b16, _ = omb.local_train_mobilenet(p32, sh.features, sh.labels, 32, 32, 0.05, seed, C, rounding="bf16")
     idx = fm.batch_plan(len(sh.labels), 32, 32, seed)[0]
     xt = torch.tensor(sh.features[idx], dtype=torch.float32).reshape(-1, 32, 32, 3).permute(0, 3, 1, 2)
     yt = torch.tensor(sh.labels[idx], dtype=torch.int64)
+    ratios = []
+    for pseed in (3, 4, 5):
+        p = init_mobilenet_params(C, pseed)
+        params = torch.tensor(fed.layout.to_padded(p), dtype=torch.float64, device="cuda")
+        p32 = {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
 
-    def loss(delta):
-        m = omb.MobileNetV2(C)
-        sd = m.state_dict()
-        for k in state_keys(m):
-            sd[k].copy_(torch.tensor(p32[k] + (delta[k] if delta is not None else 0.0), dtype=torch.float32))
-        m.train()
-        with torch.no_grad():
-            return float(F.cross_entropy(m(xt), yt))
+        def loss(delta):
+            m = omb.MobileNetV2(C)
+            sd = m.state_dict()
+            for k in state_keys(m):
+                sd[k].copy_(torch.tensor(p32[k] + (delta[k] if delta is not None else 0.0), dtype=torch.float32))
+            m.train()
+            with torch.no_grad():
+                return float(F.cross_entropy(m(xt), yt))
 
-    l0 = loss(None)
-    d32, d16, de = l0 - loss(f32), l0 - loss(b16), l0 - loss(got)
-    assert d32 > 0 and de >= 0.85 * d32 and de >= 0.9 * d16, (l0, d32, d16, de)
+        got = fed.layout.from_padded(fed.train(params, ["t0"], [_WL(32, 32)], lr, [seed]).cpu().numpy()[0])
+        f32, _ = omb.local_train_mobilenet(p32, sh.features, sh.labels, 32, 32, lr, seed, C)
+        l0 = loss(None)
+        d32 = l0 - loss(f32)
+        assert d32 > 0
+        ratios.append((l0 - loss(got)) / d32)
+    assert np.mean(ratios) >= 0.85 and min(ratios) >= 0.75, ratios
 
 
 def test_mobilenet_loss_trajectory_matches_oracle(msetup):
