@@ -325,6 +325,8 @@ int fedhc_resnet_destroy(void* ws);
 int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, int n_clients, const double* params,
                              int max_steps, float lr, int use_graph, void* stream);
 int fedhc_resnet_last_loss(void* ws, float* out, int n_clients, void* stream);
+/* kernels launched by the workspace so far (graph kernel nodes + direct launches; eager steps excluded) */
+int fedhc_resnet_launch_count(void* ws, int64_t* out);
 int fedhc_resnet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
                       unsigned long long* correct, void* stream);
 /* CIFAR MobileNetV2 client engine (BASELINE config 4), same conventions as the ResNet engine: 3x3 stem,

@@ -158,6 +158,7 @@ SIGNATURES = {
     "fedhc_resnet_destroy": (_i, [_vp]),
     "fedhc_resnet_local_train": (_i, [_vp, _vp, _i, _vp, _i, C.c_float, _i, _vp]),
     "fedhc_resnet_last_loss": (_i, [_vp, _vp, _i, _vp]),
+    "fedhc_resnet_launch_count": (_i, [_vp, _vp]),
     "fedhc_resnet_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "fedhc_dw_conv": (_i, [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.c_float, _vp]),
     "fedhc_mobilenet_param_count": (_i, [_i, _vp]),

@@ -199,6 +199,20 @@ struct ReluSelf {
   int64_t pstride, gamma, beta;
 };
 
+// kernel nodes of a captured graph (the engine's launch accounting)
+inline int count_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return 0;
+  std::vector<cudaGraphNode_t> v(n);
+  if (cudaGraphGetNodes(g, v.data(), &n) != cudaSuccess) return 0;
+  int k = 0;
+  for (auto x : v) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(x, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 // ---- batch norm (training mode statistics over the client's valid images) -------------------------
 // x [G*Bp][HW][C] bf16.  part [G][BN_SPLIT][C][2] fp32 (sum, sum of squares) or (sum dz, sum dz*xhat).
 // grid (C/64, G, BN_SPLIT), 256 threads = 64 channels x 4 row lanes.
@@ -737,6 +751,8 @@ struct Engine {
   BlockPlans ebp[NB];
   cudaGraphExec_t graph = nullptr;
   std::tuple<int, int, float> graph_key{-1, -1, 0.f};
+  int graph_kernels = 0, eval_kernels = -1;  // kernel nodes of the round graph / of one eval chunk
+  int64_t launches = 0;                      // kernels launched (graph nodes + direct; eager steps excluded)
   BnSgdTable bnt{};
 
   ~Engine() {
@@ -1169,12 +1185,14 @@ extern "C" int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, i
         return rc;
       }
       FEDHC_CUDA_TRY(ce);
+      e->graph_kernels = rn::count_kernel_nodes(g);
       cudaError_t ie = cudaGraphInstantiate(&e->graph, g, 0);
       cudaGraphDestroy(g);
       FEDHC_CUDA_TRY(ie);
       e->graph_key = key;
     }
     FEDHC_CUDA_TRY(cudaGraphLaunch(e->graph, st));
+    e->launches += e->graph_kernels;
   } else {
     for (int s = 0; s < max_steps; ++s)
       if ((rc = e->train_step(G, s, lr, st))) return rc;
@@ -1182,6 +1200,14 @@ extern "C" int fedhc_resnet_local_train(void* ws, const fedhc_client* clients, i
   rn::delta_kernel<<<dim3(rn::Engine::blocks_for(e->L.P / 2, G), G), 256, 0, st>>>(e->desc, params, e->master,
                                                                                    e->L.P);
   FEDHC_CUDA_TRY(cudaGetLastError());
+  e->launches += 2;
+  return FEDHC_OK;
+}
+
+extern "C" int fedhc_resnet_launch_count(void* ws, int64_t* out) {
+  auto* e = static_cast<rn::Engine*>(ws);
+  if (!e || !out) return fail(FEDHC_ERR_VALUE, "resnet: bad arguments");
+  *out = e->launches;
   return FEDHC_OK;
 }
 
@@ -1201,9 +1227,26 @@ extern "C" int fedhc_resnet_eval(void* ws, const double* params, const float* x,
   if (n <= 0) return FEDHC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int chunk = e->maxG * e->Bp;
+  if (e->eval_kernels < 0) {  // count the eval forward's launches once (captured, never run)
+    cudaStream_t cap;
+    FEDHC_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    FEDHC_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int rc0 = e->forward(1, chunk, 0, true, e->e_stem_f, e->ebp, cap);
+    const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+    cudaStreamDestroy(cap);
+    if (g) {
+      e->eval_kernels = rn::count_kernel_nodes(g) + 1;  // + fc_eval
+      cudaGraphDestroy(g);
+    }
+    if (rc0) return rc0;
+    FEDHC_CUDA_TRY(ce);
+  }
   rn::bcast_kernel<<<dim3(rn::Engine::blocks_for(e->L.P / 2, 1), 1), 256, 0, st>>>(params, e->master, e->shadow,
                                                                                    e->L.P, 1);
+  e->launches += 1;
   for (int64_t at = 0; at < n; at += chunk) {
+    e->launches += e->eval_kernels;
     const int rows = (int)(n - at < chunk ? n - at : chunk);
     fedhc_client c{};
     c.x = x + at * rn::IMG_F;
@@ -1229,7 +1272,7 @@ extern "C" int fedhc_resnet_eval(void* ws, const double* params, const float* x,
 // 1x1 linear projection + BN, identity / 1x1-projection shortcut when stride 1), 1x1 head to 1280 + BN +
 // ReLU, global average pool, linear.  Channels are padded to multiples of 64 in HBM (the padded channels
 // stay exactly zero: zero weights, gamma = beta = 0), so every pointwise convolution -- forward, data and
-// weight gradient + SGD -- is a grouped implicit tcgen05 GEMM (k = 1 NHWC mode); the depthwise 3x3
+// weight gradient + SGD -- is a plain grouped tcgen05 GEMM over the client's pixels; the depthwise 3x3
 // convolutions (K = 9 per channel, no contraction worth the tensor pipe) are vectorised CUDA-core
 // kernels, their weight gradients a two-pass deterministic reduction.
 // ==========================================================================================
@@ -1577,19 +1620,6 @@ __global__ void dw_sgd_kernel(const float* __restrict__ part, float* __restrict_
 __global__ void step_inc_kernel(int* c) { *c += 1; }
 __global__ void add_count_kernel(unsigned long long* dst, const unsigned long long* src) { *dst += *src; }
 
-// kernel nodes of a captured graph (the engine's launch accounting)
-static int count_kernel_nodes(cudaGraph_t g) {
-  size_t n = 0;
-  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return 0;
-  std::vector<cudaGraphNode_t> v(n);
-  if (cudaGraphGetNodes(g, v.data(), &n) != cudaSuccess) return 0;
-  int k = 0;
-  for (auto x : v) {
-    cudaGraphNodeType t;
-    if (cudaGraphNodeGetType(x, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
-  }
-  return k;
-}
 
 struct BlkPlans {
   tc::GemmPlan c1f, c1d, c1w, c3f, c3d, c3w, csf, csd, csw;
@@ -1813,7 +1843,7 @@ struct Engine {
       }
       FEDHC_CUDA_TRY(ce);
       cudaGraphExec_t ex = nullptr;
-      const int nk = count_kernel_nodes(g);
+      const int nk = rn::count_kernel_nodes(g);
       cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
       cudaGraphDestroy(g);
       FEDHC_CUDA_TRY(ie);
@@ -1845,7 +1875,7 @@ struct Engine {
       }
       FEDHC_CUDA_TRY(ce);
       cudaGraphExec_t ex = nullptr;
-      const int nk = count_kernel_nodes(g);
+      const int nk = rn::count_kernel_nodes(g);
       cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
       cudaGraphDestroy(g);
       FEDHC_CUDA_TRY(ie);

@@ -143,6 +143,11 @@ class ResnetEngine:
         _abi.check(_abi.lib.fedhc_resnet_last_loss(self._h, out.data_ptr(), k, stream_ptr()))
         return out
 
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _abi.check(_abi.lib.fedhc_resnet_launch_count(self._h, C.byref(n)))
+        return n.value
+
     def correct_into(self, params: torch.Tensor, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor) -> None:
         _abi.check(_abi.lib.fedhc_resnet_eval(self._h, params.data_ptr(), x.data_ptr(), y.data_ptr(),
                                               int(y.shape[0]), out.data_ptr(), stream_ptr()))
