@@ -47,7 +47,8 @@ N_TEST = 16000
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 100 rounds for the ~1 ms logistic round, 20 otherwise)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
@@ -64,7 +65,10 @@ def parse():
     ap.add_argument("--mobilenet-max-samples", type=int, default=1024,
                     help="largest per-client sample count (config 4: uniform choice of 16, 32, ..., 1024)")
     ap.add_argument("--classes", type=int, default=10, help="10 (digits) or 62 (FEMNIST classes, 4-CTA clusters)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 100 if (args.workload == "round" and args.impl != "reference") else 20
+    return args
 
 
 def workload_config(n_gpus):
