@@ -6,7 +6,6 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import flmath as fm  # noqa: E402  (seeds only)
 from paper_2305_15668_b200 import training as tr  # noqa: E402
 
 
@@ -28,7 +27,7 @@ def main():
     fed = Fed(shards, tst, 3072, 10).attach_engine(G, 32)
     params = torch.tensor(fed.layout.to_padded(init(10, 1)), dtype=torch.float64, device="cuda")
     wls = [WL(32, 32)] * G
-    seeds = [fm.seed_of("train", 1, 0, c) for c in ids]
+    seeds = [tr.stable_seed("train", 1, 0, c) for c in ids]
     fed.train(params, ids, wls, 0.05, seeds, use_graph=False)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("prof")
