@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "fedavg", "gemm", "des"], default="round",
+    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "shufflenet", "fedavg", "gemm", "des"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
@@ -828,6 +828,31 @@ def mobilenet_bytes_per_sample() -> float:
     return float(4 * 2 * el)
 
 
+def shufflenet_flop_per_sample(n_classes: int) -> float:
+    """Algorithmic FLOPs of one ShuffleNetV2 x1.0 training sample (3 x forward minus the stem's data gradient)."""
+    from paper_2305_15668_b200.shufflenet import HEAD, STAGES
+    stem = 32 * 32 * 24 * 27
+    macs = stem
+    for cin, cout, nb, H in STAGES:
+        mid, ho2 = cout // 2, (H // 2) ** 2
+        macs += ho2 * cin * 9 + ho2 * cin * mid + H * H * cin * mid + ho2 * mid * 9 + ho2 * mid * mid
+        macs += nb * (2 * ho2 * mid * mid + ho2 * mid * 9)
+    macs += 16 * STAGES[2][1] * HEAD + HEAD * n_classes
+    return float(2 * (3 * macs - stem))
+
+
+def shufflenet_bytes_per_sample() -> float:
+    """HBM roofline of the unfused ShuffleNetV2 layer graph per sample (as mobilenet_bytes_per_sample)."""
+    from paper_2305_15668_b200.shufflenet import HEAD, STAGES
+    el = 2 * 32 * 32 * 24
+    for cin, cout, nb, H in STAGES:
+        mid, ho2 = cout // 2, (H // 2) ** 2
+        el += 2 * ho2 * cin + 2 * ho2 * mid + 2 * H * H * mid + 4 * ho2 * mid + ho2 * cout
+        el += nb * (6 * ho2 * mid + ho2 * cout)
+    el += 2 * 16 * HEAD
+    return float(4 * 2 * el)
+
+
 def cifar_cpu_reference(seconds: float, n_classes: int, batch: int, model: str = "resnet"):
     """CIFAR-model local SGD on the host cores (torch CPU, all threads): CPU restatement (no reference CNN)."""
     import torch
@@ -836,6 +861,9 @@ def cifar_cpu_reference(seconds: float, n_classes: int, batch: int, model: str =
     if model == "mobilenet":
         from oracle.mobilenet import MobileNetV2 as Net
         name = "MobileNetV2"
+    elif model == "shufflenet":
+        from oracle.shufflenet import ShuffleNetV2 as Net
+        name = "ShuffleNetV2"
     else:
         from oracle.resnet import ResNet18 as Net
         name = "ResNet-18"
@@ -880,6 +908,9 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
     if model == "mobilenet":
         from paper_2305_15668_b200.mobilenet import MobilenetFederation as Federation
         from paper_2305_15668_b200.mobilenet import init_mobilenet_params as init_params
+    elif model == "shufflenet":
+        from paper_2305_15668_b200.shufflenet import ShufflenetFederation as Federation
+        from paper_2305_15668_b200.shufflenet import init_shufflenet_params as init_params
     else:
         from paper_2305_15668_b200.resnet import ResnetFederation as Federation
         from paper_2305_15668_b200.resnet import init_resnet_params as init_params
@@ -895,7 +926,8 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         dist = dist_mod
         dist.init_process_group("nccl", device_id=dev)
     nc, bs, lr = 10, 32, 0.05
-    if model == "mobilenet":
+    config4 = model in ("mobilenet", "shufflenet")
+    if config4:
         per_gpu = args.mobilenet_clients
         n_part, n_fleet = per_gpu * world, max(args.mobilenet_fleet, per_gpu * world)
         levels, v = [], 16
@@ -962,7 +994,7 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         _, desc, coef, steps, _, _ = plans[r]
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        if model == "mobilenet":
+        if config4:
             fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True, steps=steps)
         else:
             fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True)
@@ -1041,7 +1073,8 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         dist.all_reduce(t)
         e2e_steps = int(t.item())
 
-    fps = mobilenet_flop_per_sample(nc) if model == "mobilenet" else resnet_flop_per_sample(nc)
+    fps = (mobilenet_flop_per_sample(nc) if model == "mobilenet" else shufflenet_flop_per_sample(nc)
+           if model == "shufflenet" else resnet_flop_per_sample(nc))
     flops = fps * float(np.mean([p[5] for p in timed]))  # per train launch (this GPU's samples)
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -1050,22 +1083,34 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
     tf = flops / (train_ms * 1e-3) / 1e12
     hbm_roof = None
-    if model == "mobilenet":
+    if config4:
         try:
             hpk, hsrc = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, measured)"
         except (NameError, KeyError, ValueError):
             hpk, hsrc = 6543.7, "fallback 6.54 TB/s (SURVEY §8d)"
         p_canon = fed.layout.canonical_count
         steps_round = float(np.mean([p[4] for p in timed]))
-        bytes_launch = mobilenet_bytes_per_sample() * float(np.mean([p[5] for p in timed])) + 8.0 * p_canon * steps_round
+        bps_ = mobilenet_bytes_per_sample() if model == "mobilenet" else shufflenet_bytes_per_sample()
+        bytes_launch = bps_ * float(np.mean([p[5] for p in timed])) + 8.0 * p_canon * steps_round
         gbs = bytes_launch / (train_ms * 1e-3) / 1e9
         hbm_roof = {"bound": "hbm", "achieved": gbs, "peak": hpk, "unit": "GB/s", "frac": gbs / hpk, "traffic": None,
                     "kernel": "train phase (see roofline_tensor for the kernels)",
                     "algorithmic_bytes_per_launch": bytes_launch,
-                    "bytes_per_sample": mobilenet_bytes_per_sample(), "weight_bytes_per_client_step": 8.0 * p_canon,
+                    "bytes_per_sample": bps_, "weight_bytes_per_client_step": 8.0 * p_canon,
                     "peak_source": hsrc,
-                    "note": "arithmetic intensity ~15 flop/B (545 MFLOP vs 36 MB per sample) << ridge: HBM-bound"}
-    if model == "mobilenet":
+                    "note": f"arithmetic intensity {fps / bps_:.0f} flop/B << ridge (~260): HBM-bound"}
+    if model == "shufflenet":
+        mname, cfg_name = "ShuffleNetV2", ("cifar-shufflenetv2: BASELINE config 4 model, ShuffleNetV2 x1.0 (CIFAR "
+                                           "variant: 3x3 stem, stages 116-232-464 with channel split / shuffle, "
+                                           "1x1 head to 1024, batch norm), 10 classes, fleet of %d with non-IID "
+                                           "sample counts" % n_fleet)
+        api = "ShufflenetFederation.train / aggregate / correct (host selection, DES, PCG64 plan, H2D, D2H)"
+        kern = ("train phase (one CUDA graph per active-client count: 1x1 convolutions as grouped tcgen05 GEMMs with "
+                "strided split-form operands, depthwise 3x3 kernels, shuffle / BN kernels)")
+        spc = "ceil(n / 32) for n in " + str(n_samp)
+        arith = ("bf16 tensor-core operands and activations (tcgen05) for the 1x1 convolutions, FHFMA depthwise "
+                 "3x3, fp32 accumulation, batch norm and master weights; FedAvg in fp64")
+    elif model == "mobilenet":
         mname, cfg_name = "MobileNetV2", ("cifar-mobilenetv2: BASELINE config 4 model, MobileNetV2 (CIFAR variant: "
                                            "3x3 stem, 17 inverted-residual blocks, 1x1 head to 1280, batch norm), "
                                            "10 classes, fleet of %d with non-IID sample counts" % n_fleet)
@@ -1164,6 +1209,8 @@ def main():
         res = run_resnet(args, rank, world, local_rank)
     elif args.workload == "mobilenet":
         res = run_resnet(args, rank, world, local_rank, model="mobilenet")
+    elif args.workload == "shufflenet":
+        res = run_resnet(args, rank, world, local_rank, model="shufflenet")
     elif args.workload == "gemm":
         res = run_gemm(args, rank, world, local_rank)
     elif args.workload == "des":

@@ -250,6 +250,8 @@ typedef struct fedhc_gemm_args {
   float* rowsum;
   int64_t a_gstride; /* elements between groups of A (0 = dense) */
   int64_t b_gstride; /* elements between groups of B (0 = dense) */
+  int64_t lda;       /* elements between rows of A as stored (0 = dense: K, or M when a_mn) */
+  int64_t ldb;       /* elements between rows of B as stored (0 = dense) */
 } fedhc_gemm_args;
 int fedhc_gemm(const fedhc_gemm_args* args, void* stream);
 
@@ -350,6 +352,18 @@ int fedhc_mobilenet_last_loss(void* ws, float* out, int n_clients, void* stream)
 int fedhc_mobilenet_launch_count(void* ws, int64_t* out);
 int fedhc_mobilenet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
                          unsigned long long* correct, void* stream);
+/* CIFAR ShuffleNetV2 x1.0 client engine (BASELINE config 4's other model), same conventions as MobileNetV2:
+ * activations in "split form" ([X1 | X2] halves of each block output, padded to multiples of 64). */
+int fedhc_shufflenet_param_count(int n_classes, int64_t* padded);
+int fedhc_shufflenet_param_offsets(int n_classes, int64_t* offsets, int cap, int* count);
+int fedhc_shufflenet_create(int max_clients, int batch, int n_classes, void** ws);
+int fedhc_shufflenet_destroy(void* ws);
+int fedhc_shufflenet_local_train(void* ws, const fedhc_client* clients, int n_clients, const int32_t* steps,
+                                 const double* params, int max_steps, float lr, int use_graph, void* stream);
+int fedhc_shufflenet_last_loss(void* ws, float* out, int n_clients, void* stream);
+int fedhc_shufflenet_launch_count(void* ws, int64_t* out);
+int fedhc_shufflenet_eval(void* ws, const double* params, const float* x, const int32_t* y, int64_t n,
+                          unsigned long long* correct, void* stream);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,7 @@ class GemmArgs(C.Structure):
         ("bias", C.c_void_p), ("bias_gstride", C.c_int64),
         ("master", C.c_void_p), ("shadow", C.c_void_p), ("lr", C.c_float), ("pad_", C.c_int32),
         ("mask", C.c_void_p), ("rowsum", C.c_void_p), ("a_gstride", C.c_int64), ("b_gstride", C.c_int64),
+        ("lda", C.c_int64), ("ldb", C.c_int64),
     ]
 
 
@@ -169,6 +170,14 @@ SIGNATURES = {
     "fedhc_mobilenet_last_loss": (_i, [_vp, _vp, _i, _vp]),
     "fedhc_mobilenet_launch_count": (_i, [_vp, _vp]),
     "fedhc_mobilenet_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "fedhc_shufflenet_param_count": (_i, [_i, _vp]),
+    "fedhc_shufflenet_param_offsets": (_i, [_i, _vp, _i, _vp]),
+    "fedhc_shufflenet_create": (_i, [_i, _i, _i, _vp]),
+    "fedhc_shufflenet_destroy": (_i, [_vp]),
+    "fedhc_shufflenet_local_train": (_i, [_vp, _vp, _i, _vp, _vp, _i, C.c_float, _i, _vp]),
+    "fedhc_shufflenet_last_loss": (_i, [_vp, _vp, _i, _vp]),
+    "fedhc_shufflenet_launch_count": (_i, [_vp, _vp]),
+    "fedhc_shufflenet_eval": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
 }
 
 

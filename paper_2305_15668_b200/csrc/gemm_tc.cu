@@ -629,9 +629,10 @@ static int make_map_ex(CUtensorMap* map, const void* base, CUtensorMapDataType d
 
 // bf16 operand [G][outer][inner] -> box {64, box_outer, 1}, 128-byte swizzle
 static int make_map(CUtensorMap* map, const void* base, int G, int outer, int inner, int box_outer,
-                    int64_t gstride) {
+                    int64_t gstride, int64_t ld = 0) {
   if (gstride > 0 && gstride % 8) return fail(FEDHC_ERR_VALUE, "gemm: operand group stride must be a multiple of 8 elements");
-  return make_map_ex(map, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, G, outer, inner, 0, gstride, 64, box_outer,
+  if (ld > 0 && ld < inner) return fail(FEDHC_ERR_VALUE, "gemm: operand row stride shorter than the row");
+  return make_map_ex(map, base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, G, outer, inner, ld, gstride, 64, box_outer,
                      CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -723,10 +724,11 @@ static int plan_conv_maps(const fedhc_gemm_args& a, GemmPlan* p) {
 
 template <int BM, int BN, bool A_MN, bool B_MN, int WIN = 0>
 static int plan_kernel(const fedhc_gemm_args& a, GemmPlan* p) {
-  int rc = A_MN ? make_map(&p->ma, a.A, a.G, a.K, a.M, 64, a.a_gstride)
-                 : make_map(&p->ma, a.A, a.G, a.M, a.K, BM, a.a_gstride);
+  int rc = A_MN ? make_map(&p->ma, a.A, a.G, a.K, a.M, 64, a.a_gstride, a.lda)
+                 : make_map(&p->ma, a.A, a.G, a.M, a.K, BM, a.a_gstride, a.lda);
   if (rc) return rc;
-  rc = B_MN ? make_map(&p->mb, a.B, a.G, a.K, a.N, 64, a.b_gstride) : make_map(&p->mb, a.B, a.G, a.N, a.K, BN, a.b_gstride);
+  rc = B_MN ? make_map(&p->mb, a.B, a.G, a.K, a.N, 64, a.b_gstride, a.ldb)
+            : make_map(&p->mb, a.B, a.G, a.N, a.K, BN, a.b_gstride, a.ldb);
   if (rc) return rc;
   const int kind = p->ep.kind, R = BM / 4;
   p->ms = p->ml = p->mo = CUtensorMap{};
