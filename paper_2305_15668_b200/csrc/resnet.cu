@@ -995,12 +995,15 @@ struct Engine {
   }
 
   // dC = BN backward of dz through x (stats slot id), dgamma / dbeta into gsum slot id
+  // relu: the BN fed a ReLU whose backward is folded in (decided from x itself, see ReluSelf)
   void bn_backward(int G, const __nv_bfloat16* dz, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b,
-                   __nv_bfloat16* dc, cudaStream_t st) {
-    bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C, part);
+                   __nv_bfloat16* dc, cudaStream_t st, bool relu = false) {
+    const ReluSelf rs{relu ? master : nullptr, L.P, b.gamma, b.beta};
+    bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C, part,
+                                                                  nullptr, rs);
     bn_finalize_kernel<true><<<G, C, 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
     bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), bn_block(C), 0, st>>>(
-        dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc);
+        dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc, nullptr, rs);
   }
 
   int forward(int G, int bp, int step, bool eval, const tc::GemmPlan& sf, const BlockPlans* bps, cudaStream_t st) {
@@ -1049,8 +1052,7 @@ struct Engine {
       bn_backward(G, dz, c2[i], hw, d.cout, 2 + 3 * i, L.bn2[i], g0, st);  // g0 = dC2
       if ((rc = tc::gemm_run(bp[i].c2d, st))) return rc;                     // g1 = dA1
       if ((rc = tc::gemm_run(bp[i].c2w, st))) return rc;                     // W2 SGD (a1, dC2)
-      relu_mask_kernel<<<grid_for(n8o), 256, 0, st>>>(g1, a1[i], n8o, g1);   // g1 = dZ1
-      bn_backward(G, g1, c1[i], hw, d.cout, 1 + 3 * i, L.bn1[i], g0, st);   // g0 = dC1
+      bn_backward(G, g1, c1[i], hw, d.cout, 1 + 3 * i, L.bn1[i], g0, st, true);  // g0 = dC1 (ReLU folded in)
       if (d.s == 1) {
         if ((rc = tc::gemm_run(bp[i].c1d, st))) return rc;  // g2 = dX (from g0)
       } else {
@@ -1075,10 +1077,8 @@ struct Engine {
       FEDHC_CUDA_TRY(cudaMemcpyAsync(up, g2, bytes, cudaMemcpyDeviceToDevice, st));
       dy = up;
     }
-    // stem: dZ0 = dY (a0 > 0); bn0 backward -> dC0 (g0); Wstem SGD
-    const int64_t n80 = (int64_t)G * Bp * 1024 * 64 / 8;
-    relu_mask_kernel<<<grid_for(n80), 256, 0, st>>>(dy, a0, n80, g1);
-    bn_backward(G, g1, c0, 1024, 64, 0, L.bn0, g0, st);
+    // stem: bn0 backward of dY with the ReLU folded in -> dC0 (g0); Wstem SGD
+    bn_backward(G, dy, c0, 1024, 64, 0, L.bn0, g0, st, true);
     if ((rc = tc::gemm_run(stem_w, st))) return rc;
     bn_sgd_kernel<<<dim3(bnt.n, G), 256, 0, st>>>(bnt, master, L.P, gsum, lr);
     FEDHC_CUDA_TRY(cudaGetLastError());
