@@ -74,7 +74,8 @@ constexpr int IMG = 32, IMG_C = 3, IMG_F = IMG * IMG * IMG_C;  // input rows: NH
 constexpr int NB = 8;                                          // BasicBlocks
 constexpr int MAXC = 512, NCMAX = 64;
 constexpr int MAXBN = 1280;  // widest batch-norm layer of the client models (MobileNetV2 head)
-constexpr int BN_SPLIT = 16;                                   // row splits of the BN reductions
+constexpr int BN_SPLIT = 16;  // default row splits of the BN reductions (per engine; a client's result never
+                              // depends on how many clients train with it: the split is fixed per engine)
 constexpr float BN_EPS = 1e-5f, BN_MOM = 0.1f;
 
 struct BlockDef {
@@ -214,8 +215,8 @@ inline int count_kernel_nodes(cudaGraph_t g) {
 }
 
 // ---- batch norm (training mode statistics over the client's valid images) -------------------------
-// x [G*Bp][HW][C] bf16.  part [G][BN_SPLIT][C][2] fp32 (sum, sum of squares) or (sum dz, sum dz*xhat).
-// grid (C/64, G, BN_SPLIT), 256 threads = 64 channels x 4 row lanes.
+// x [G*Bp][HW][C] bf16.  part [G][splits][C][2] fp32 (sum, sum of squares) or (sum dz, sum dz*xhat).
+// grid (1, G, splits), 256 threads = 64 channels x 4 row lanes.
 template <bool BWD>
 __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __restrict__ x,
                                                          const __nv_bfloat16* __restrict__ dz,
@@ -225,12 +226,12 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
                                                          const __nv_bfloat16* __restrict__ mask = nullptr,
                                                          ReluSelf rs = ReluSelf{nullptr, 0, 0, 0}) {
   // mask (BWD, optional): dz is taken as dz * (mask > 0) -- the ReLU backward folded in
-  // grid (1, G, BN_SPLIT); thread = (8-channel group cg, row lane rl): C / 8 groups x (256 / (C / 8)) lanes
+  // grid (1, G, splits = gridDim.z); thread = (8-channel group cg, row lane rl): C / 8 groups x (256 / (C / 8)) lanes
   __shared__ float red[256][17];
   const int g = blockIdx.y, sp = blockIdx.z, groups = C >> 3, lanes = 256 / groups;
   const int cg = threadIdx.x % groups, rl = threadIdx.x / groups;
   const int nr = valid[g] * HW;
-  const int r0 = (int)((int64_t)nr * sp / BN_SPLIT), r1 = (int)((int64_t)nr * (sp + 1) / BN_SPLIT);
+  const int ns = gridDim.z, r0 = (int)((int64_t)nr * sp / ns), r1 = (int)((int64_t)nr * (sp + 1) / ns);
   const __nv_bfloat16* xb = x + (int64_t)g * Bp * HW * C + cg * 8;
   const __nv_bfloat16* db = BWD ? dz + (int64_t)g * Bp * HW * C + cg * 8 : nullptr;
   float mean[8], rstd[8], s0[8], s1[8], rk[8], rb[8];
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
       a0 += red[l * groups + gq][e];
       a1 += red[l * groups + gq][8 + e];
     }
-    float* o = part + (((int64_t)g * BN_SPLIT + sp) * C + c) * 2;
+    float* o = part + (((int64_t)g * gridDim.z + sp) * C + c) * 2;
     o[0] = a0;
     o[1] = a1;
   }
@@ -307,12 +308,12 @@ __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloat16* __
 template <bool BWD>
 __global__ void bn_finalize_kernel(const float* __restrict__ part, const int32_t* __restrict__ valid, int HW, int C,
                                    float* __restrict__ out, float* __restrict__ master, int64_t pstride,
-                                   int64_t rm_off, int64_t rv_off) {
+                                   int64_t rm_off, int64_t rv_off, int nsplit = BN_SPLIT) {
   const int g = blockIdx.x;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
-    for (int sp = 0; sp < BN_SPLIT; ++sp) {
-      const float* p = part + (((int64_t)g * BN_SPLIT + sp) * C + c) * 2;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float* p = part + (((int64_t)g * nsplit + sp) * C + c) * 2;
       s0 += p[0];
       s1 += p[1];
     }
@@ -1280,7 +1281,7 @@ namespace fedhc {
 namespace mb {
 
 using rn::BnOff;
-using rn::BN_SPLIT;
+constexpr int BN_SPLIT = 32;  // BN reduction splits: late local steps train few clients, keep the GPU covered
 using rn::bf;
 
 constexpr int NBLK = 17, HEADC = 1280, MAXBNL = 64;
@@ -1892,7 +1893,7 @@ struct Engine {
   void bn_stats(int G, int bp, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b, cudaStream_t st) {
     rn::bn_partial_kernel<false><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, nullptr, nullptr, valid, bp, HW, C, part);
     rn::bn_finalize_kernel<false><<<G, std::min(C, 512), 0, st>>>(part, valid, HW, C, stats + st_off[id], master, L.P, b.rmean,
-                                                   b.rvar);
+                                                   b.rvar, BN_SPLIT);
   }
   void bn_apply(int G, int bp, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b, const __nv_bfloat16* res,
                 const __nv_bfloat16* xs, int ids, const BnOff* bs, bool relu, bool eval, __nv_bfloat16* out,
@@ -1925,7 +1926,8 @@ struct Engine {
     const rn::ReluSelf rs{relu ? master : nullptr, L.P, b.gamma, b.beta};
     rn::bn_partial_kernel<true><<<dim3(1, G, BN_SPLIT), 256, 0, st>>>(x, dz, stats + st_off[id], valid, Bp, HW, C,
                                                                       part, nullptr, rs);
-    rn::bn_finalize_kernel<true><<<G, std::min(C, 512), 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0);
+    rn::bn_finalize_kernel<true><<<G, std::min(C, 512), 0, st>>>(part, valid, HW, C, gsum + st_off[id], nullptr, 0, 0, 0,
+                                                                 BN_SPLIT);
     rn::bn_bwd_apply_kernel<<<dim3(blocks_for((int64_t)Bp * HW * C / 8, G), G), rn::bn_block(C), 0, st>>>(
         dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc, nullptr, rs);
   }
