@@ -1622,8 +1622,41 @@ __global__ void step_inc_kernel(int* c) { *c += 1; }
 __global__ void add_count_kernel(unsigned long long* dst, const unsigned long long* src) { *dst += *src; }
 
 
+// Weight gradient + SGD of a 1x1 layer.  Few output tiles per client (e.g. 64 x 192 = 3 tiles) leave most
+// SMs idle when few clients train (late local steps), so those layers split K (the client's pixels) over S
+// image groups: the GEMM runs as G*S groups writing fp32 partials, wgrad_sgd_kernel sums them in fixed order
+// and applies SGD.  S depends on the layer shape only, never on how many clients train together.
+struct WgPlan {
+  tc::GemmPlan gemm;
+  int S = 1;
+  int64_t woff = 0, mn = 0;
+};
+
+__global__ void wgrad_sgd_kernel(const float* __restrict__ part, int S, int64_t mn, float* __restrict__ master,
+                                 __nv_bfloat16* __restrict__ shadow, int64_t pstride, int64_t woff, float lr) {
+  const int g = blockIdx.y;
+  float* m = master + (int64_t)g * pstride + woff;
+  __nv_bfloat16* sh = shadow + (int64_t)g * pstride + woff;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mn; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < S; ++k) acc += part[((int64_t)g * S + k) * mn + i];
+    const float v = m[i] - lr * acc;
+    m[i] = v;
+    sh[i] = __float2bfloat16_rn(v);
+  }
+}
+
+static int wg_split(int M, int N, int bp) {
+  const int bm = M % 128 == 0 ? 128 : 64, bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64;
+  const int tpc = ((M + bm - 1) / bm) * (N / bn);
+  int S = 1;
+  while (tpc * S < 16 && S < 8 && bp % (2 * S) == 0) S *= 2;
+  return S;
+}
+
 struct BlkPlans {
-  tc::GemmPlan c1f, c1d, c1w, c3f, c3d, c3w, csf, csd, csw;
+  tc::GemmPlan c1f, c1d, c3f, c3d, csf, csd;
+  WgPlan c1w, c3w, csw;
 };
 
 struct Engine {
@@ -1646,7 +1679,9 @@ struct Engine {
   std::vector<std::tuple<int, int64_t, int64_t, int64_t>> bn_sgd;  // (C, gamma, beta, slot)
   int planned_G = -1;
   float planned_lr = 0.f;
-  tc::GemmPlan stem_f, stem_w, head_f, head_d, head_w, e_stem_f, e_head_f;
+  tc::GemmPlan stem_f, stem_w, head_f, head_d, e_stem_f, e_head_f;
+  WgPlan head_w;
+  float* wpart = nullptr;  // split-K weight-gradient partials
   BlkPlans bp[NBLK], ebp[NBLK];
   std::map<int, std::pair<cudaGraphExec_t, int>> step_graphs;  // active clients -> (graph, kernel nodes)
   std::map<int, std::pair<cudaGraphExec_t, int>> eval_graphs;  // rows -> (graph, kernel nodes)
@@ -1738,6 +1773,15 @@ struct Engine {
     rc |= alloc(&desc, G);
     rc |= alloc(&step_ctr, 1);
     rc |= alloc(&ecorrect, 1);
+    size_t wneed = (size_t)wg_split(320, HEADC, Bp) * 320 * HEADC;
+    for (int i = 0; i < NBLK; ++i) {
+      const BlkDef& d = B[i];
+      const int pci = pad64(d.cin), ppl = pad64(d.pl), pco = pad64(d.cout);
+      wneed = std::max(wneed, (size_t)wg_split(pci, ppl, Bp) * pci * ppl);
+      wneed = std::max(wneed, (size_t)wg_split(ppl, pco, Bp) * ppl * pco);
+      wneed = std::max(wneed, (size_t)wg_split(pci, pco, Bp) * pci * pco);
+    }
+    rc |= alloc(&wpart, G * wneed);
     if (rc) return fail(FEDHC_ERR_CUDA, "mobilenet: workspace allocation failed");
     return plan_all(1, maxG * Bp, &e_stem_f, &e_head_f, ebp, false, 0.f);
   }
@@ -1763,13 +1807,29 @@ struct Engine {
     return tc::gemm_plan(a, pl);
   }
   int pw_wgrad(int G, int bp, int H, int cin, int cout, const __nv_bfloat16* x, const __nv_bfloat16* dy, int64_t woff,
-               float lr, tc::GemmPlan* pl) {
-    auto a = gargs(G, cin, cout, bp * H * H, x, true, dy, true, 0, FEDHC_EPI_SGD);
-    a.master = master + woff;
-    a.shadow = shadow + woff;
-    a.d_gstride = L.P;
-    a.lr = lr;
-    return tc::gemm_plan(a, pl);
+               float lr, WgPlan* pl) {
+    const int S = wg_split(cin, cout, bp);
+    pl->S = S;
+    pl->woff = woff;
+    pl->mn = (int64_t)cin * cout;
+    if (S == 1) {
+      auto a = gargs(G, cin, cout, bp * H * H, x, true, dy, true, 0, FEDHC_EPI_SGD);
+      a.master = master + woff;
+      a.shadow = shadow + woff;
+      a.d_gstride = L.P;
+      a.lr = lr;
+      return tc::gemm_plan(a, &pl->gemm);
+    }
+    auto a = gargs(G * S, cin, cout, (bp / S) * H * H, x, true, dy, true, 0, FEDHC_EPI_F32);
+    a.D = wpart;
+    return tc::gemm_plan(a, &pl->gemm);
+  }
+  int run_wg(const WgPlan& p, int G, float lr, cudaStream_t st) {
+    int rc = tc::gemm_run(p.gemm, st, G * p.S);
+    if (rc || p.S == 1) return rc;
+    wgrad_sgd_kernel<<<dim3(blocks_for(p.mn, G), G), 256, 0, st>>>(wpart, p.S, p.mn, master, shadow, L.P, p.woff, lr);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
   }
 
   int plan_all(int G, int bp, tc::GemmPlan* sf, tc::GemmPlan* hf, BlkPlans* bps, bool train, float lr) {
@@ -1989,7 +2049,7 @@ struct Engine {
     // head: relu mask, BN backward, 1x1 conv data / weight gradient -> cur = dL/dy[last]
     bn_backward(G, dyh, fh, 16, HEADC, id_bnh, L.bnh, g0, st, true);
     if ((rc = tc::gemm_run(head_d, st, G))) return rc;
-    if ((rc = tc::gemm_run(head_w, st, G))) return rc;
+    if ((rc = run_wg(head_w, G, lr, st))) return rc;
     for (int i = NBLK - 1; i >= 0; --i) {
       const BlkDef& d = B[i];
       const int ho = d.H / d.s, pci = pad64(d.cin), ppl = pad64(d.pl), pco = pad64(d.cout);
@@ -1998,17 +2058,17 @@ struct Engine {
       if (has_proj(d)) {
         bn_backward(G, cur, sc[i], ho * ho, pco, id_b[i][3], L.bns[i], g1, st);  // g1 = dSC
         if ((rc = tc::gemm_run(bp[i].csd, st, G))) return rc;                       // g4 = dXs
-        if ((rc = tc::gemm_run(bp[i].csw, st, G))) return rc;
+        if ((rc = run_wg(bp[i].csw, G, lr, st))) return rc;
       }
       if ((rc = tc::gemm_run(bp[i].c3d, st, G))) return rc;  // g1 = dDA
-      if ((rc = tc::gemm_run(bp[i].c3w, st, G))) return rc;
+      if ((rc = run_wg(bp[i].c3w, G, lr, st))) return rc;
       bn_backward(G, g1, this->d[i], ho * ho, ppl, id_b[i][1], L.bn2[i], g2, st, true);  // g2 = dD
       dw_dgrad(g2, shadow, L.P, L.dw[i], (int)I, Bp, d.H, ppl, d.s, g3, st);
       dw_wgrad(ea[i], g2, G, Bp, d.H, ppl, d.s, dwpart, st);
       dw_sgd_kernel<<<dim3((9 * ppl + 255) / 256, G), 256, 0, st>>>(dwpart, master, shadow, L.P, L.dw[i], ppl, lr);
       bn_backward(G, g3, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], g0, st, true);  // g0 = dE
       if ((rc = tc::gemm_run(bp[i].c1d, st, G))) return rc;                         // g1 = dX
-      if ((rc = tc::gemm_run(bp[i].c1w, st, G))) return rc;
+      if ((rc = run_wg(bp[i].c1w, G, lr, st))) return rc;
       const int64_t n8x = I * d.H * d.H * pci / 8;
       if (has_proj(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(g1, g4, n8x);
       if (has_ident(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(g1, cur, n8x);
