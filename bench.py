@@ -1169,6 +1169,23 @@ def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU implementation (oracle port), rank 0 only."""
     if rank != 0:
         return None
+    if args.workload in ("cnn", "resnet", "mobilenet", "shufflenet"):
+        # the reference has no CNN: its arm for the CNN workloads is the torch-CPU restatement of the same
+        # client step (the CPU baseline of those workloads), on all host threads
+        if args.workload == "cnn":
+            v, cores, sample, _, secs = cnn_cpu_reference(args.cpu_seconds, args.classes, 64)
+        else:
+            v, cores, sample, _, secs = cifar_cpu_reference(args.cpu_seconds, 10, 32, args.workload)
+        return {
+            "impl": "reference", "metric": "client local-steps/sec (FedHC round: local SGD of all participants + "
+                                           "FedAvg + accuracy)",
+            "value": v, "unit": "client-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / v if v else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: torch-CPU restatement of one client's local SGD step"},
+            "cpu_baseline": {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "client-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
     v, cores, sample, rounds, secs = cpu_reference(0.0, rounds=args.steps, warmup=args.warmup)
     return {
         "impl": "reference",
