@@ -1,5 +1,5 @@
 """One eager local-SGD step of G CIFAR clients inside an NVTX range "prof" (for ncu --nvtx-include prof/),
-then the CUDA-graph step time.  Usage: python tools/profile_step.py {mobilenet|resnet} [G]."""
+then the CUDA-graph step time.  Usage: python tools/profile_step.py {mobilenet|shufflenet|resnet} [G]."""
 import os
 import sys
 
@@ -16,9 +16,11 @@ class WL:
 
 def main():
     model = sys.argv[1] if len(sys.argv) > 1 else "mobilenet"
-    G = int(sys.argv[2]) if len(sys.argv) > 2 else (100 if model == "mobilenet" else 25)
+    G = int(sys.argv[2]) if len(sys.argv) > 2 else (25 if model == "resnet" else 100)
     if model == "mobilenet":
         from paper_2305_15668_b200.mobilenet import MobilenetFederation as Fed, init_mobilenet_params as init
+    elif model == "shufflenet":
+        from paper_2305_15668_b200.shufflenet import ShufflenetFederation as Fed, init_shufflenet_params as init
     else:
         from paper_2305_15668_b200.resnet import ResnetFederation as Fed, init_resnet_params as init
     ids = [f"c{i}" for i in range(G)]
