@@ -1992,9 +1992,6 @@ struct Engine {
         dz, x, stats + st_off[id], gsum + st_off[id], master, L.P, b.gamma, valid, Bp, HW, C, dc, nullptr, rs);
   }
 
-  void relu_mask(int64_t n8, const __nv_bfloat16* a, const __nv_bfloat16* m, __nv_bfloat16* o, cudaStream_t st) {
-    rn::relu_mask_kernel<<<grid_for(n8), 256, 0, st>>>(a, m, n8, o);
-  }
 
   int forward(int G, int bp, int step, bool eval, const tc::GemmPlan& sf, const tc::GemmPlan& hf,
               const BlkPlans* bps, cudaStream_t st) {
