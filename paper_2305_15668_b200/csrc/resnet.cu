@@ -2399,6 +2399,69 @@ __global__ void shuffle_split_kernel(const __nv_bfloat16* __restrict__ A, int sa
   }
 }
 
+// One side of a shuffle: a raw tensor, or the BN + ReLU of one (its batch / running statistics).
+struct ShufSide {
+  const __nv_bfloat16* x;
+  int stride;
+  const float* stats;  // nullptr: raw
+  int64_t gamma, beta, rmean, rvar;
+};
+
+// Y = split(shuffle(cat[fA(A), fB(B)])) with the branch-output BN + ReLU fused in (the activations
+// relu(bn(.)) exist only inside this kernel; the backward decides the ReLU from the BN input).  Values are
+// rounded to bf16 exactly as bn_apply_kernel would.  grid (blocks, G), per-client coefficients in smem.
+__global__ void __launch_bounds__(256) bn_shuffle_kernel(ShufSide A, ShufSide B, const float* __restrict__ master,
+                                                         int64_t pstride, int eval, int h, int Ph, int bp, int hw,
+                                                         __nv_bfloat16* __restrict__ Y) {
+  __shared__ float kA[256], bA[256], kB[256], bB[256];
+  const int g = blockIdx.y;
+  const float* m = master + (int64_t)g * pstride;
+  auto coef = [&](const ShufSide& sd, float* kk, float* bb) {
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      float mean, rstd;
+      if (eval) {
+        mean = m[sd.rmean + c];
+        rstd = rsqrtf(m[sd.rvar + c] + rn::BN_EPS);
+      } else {
+        mean = sd.stats[((int64_t)g * Ph + c) * 2];
+        rstd = sd.stats[((int64_t)g * Ph + c) * 2 + 1];
+      }
+      kk[c] = rstd * m[sd.gamma + c];
+      bb[c] = m[sd.beta + c] - mean * kk[c];
+    }
+  };
+  if (A.stats || (eval && A.rvar)) coef(A, kA, bA);
+  if (B.stats || (eval && B.rvar)) coef(B, kB, bB);
+  __syncthreads();
+  const bool ta = A.stats || (eval && A.rvar), tb = B.stats || (eval && B.rvar);
+  const int g8 = (2 * Ph) >> 3;
+  const int64_t n = (int64_t)bp * hw * g8, p0 = (int64_t)g * bp * hw;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = p0 + t / g8;
+    const int e0 = (int)(t % g8) * 8;
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q;
+      const int c = e < Ph ? e : h + e - Ph;
+      const bool ok = e < Ph ? e < h : e - Ph < h;
+      float v = 0.f;
+      if (ok) {
+        const int j = c >> 1;
+        if (c & 1) {
+          v = bf(B.x[p * B.stride + j]);
+          if (tb) v = bf(__float2bfloat16_rn(fmaxf(v * kB[j] + bB[j], 0.f)));
+        } else {
+          v = bf(A.x[p * A.stride + j]);
+          if (ta) v = bf(__float2bfloat16_rn(fmaxf(v * kA[j] + bA[j], 0.f)));
+        }
+      }
+      o[q] = __float2bfloat16_rn(v);
+    }
+    *reinterpret_cast<uint4*>(Y + p * 2 * Ph + e0) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
 // backward: dA[:, k] = dS[2k], dB[:, k] = dS[2k + 1] (k < h; 0 on the padding up to Ph) with dS read from
 // the split-form gradient dY [npx][2Ph].  dA / dB have row strides sa / sb.  Thread = (pixel, 8 k's).
 __global__ void unshuffle_kernel(const __nv_bfloat16* __restrict__ dY, int h, int Ph, int64_t npx,
@@ -2432,11 +2495,11 @@ struct BasicPlans {
   tc::GemmPlan b1f, b3f, w3d, w3w, w1d, w1w;
 };
 struct DownAct {
-  __nv_bfloat16 *L1, *L1a, *L2, *L2a, *R1, *R1a, *R2, *R2a, *R3, *R3a, *Y;
+  __nv_bfloat16 *L1, *L1a, *L2, *R1, *R1a, *R2, *R2a, *R3, *Y;  // relu(bn(L2 / R3)) live only in the shuffle
   int id[5];
 };
 struct BasicAct {
-  __nv_bfloat16 *B1, *B1a, *B2, *B2a, *B3, *B3a, *Y;
+  __nv_bfloat16 *B1, *B1a, *B2, *B2a, *B3, *Y;  // relu(bn(B3)) lives only in the shuffle
   int id[3];
 };
 
@@ -2518,13 +2581,11 @@ struct Engine {
       rc |= alloc(&d.L1, I * ho * S.pin);
       rc |= alloc(&d.L1a, I * ho * S.pin);
       rc |= alloc(&d.L2, I * ho * S.pm);
-      rc |= alloc(&d.L2a, I * ho * S.pm);
       rc |= alloc(&d.R1, I * hi * S.pm);
       rc |= alloc(&d.R1a, I * hi * S.pm);
       rc |= alloc(&d.R2, I * ho * S.pm);
       rc |= alloc(&d.R2a, I * ho * S.pm);
       rc |= alloc(&d.R3, I * ho * S.pm);
-      rc |= alloc(&d.R3a, I * ho * S.pm);
       rc |= alloc(&d.Y, I * ho * 2 * S.pm);
       for (int j = 0; j < S.nb; ++j) {
         BasicAct& b = ba[s][j];
@@ -2533,7 +2594,6 @@ struct Engine {
         rc |= alloc(&b.B2, I * ho * S.pm);
         rc |= alloc(&b.B2a, I * ho * S.pm);
         rc |= alloc(&b.B3, I * ho * S.pm);
-        rc |= alloc(&b.B3a, I * ho * S.pm);
         rc |= alloc(&b.Y, I * ho * 2 * S.pm);
       }
     }
@@ -2686,6 +2746,14 @@ struct Engine {
     if (!eval) bn_stats(G, bp, x, HW, C, id, b, st);
     bn_apply(G, bp, x, HW, C, id, b, relu, eval, out, st);
   }
+  ShufSide side(const __nv_bfloat16* x, int stride, int id, const BnOff& b, bool eval) const {
+    return ShufSide{x, stride, eval ? nullptr : stats + st_off[id], b.gamma, b.beta, b.rmean, b.rvar};
+  }
+  void shuffle(int G, int bp, int hw, const Stage& S, const ShufSide& A, const ShufSide& B, bool eval,
+               __nv_bfloat16* Y, cudaStream_t st) {
+    bn_shuffle_kernel<<<dim3(blocks_for((int64_t)bp * hw * S.pm / 4, G), G), 256, 0, st>>>(A, B, master, L.P, eval,
+                                                                                          S.mid, S.pm, bp, hw, Y);
+  }
   void bn_backward(int G, const __nv_bfloat16* dz, const __nv_bfloat16* x, int HW, int C, int id, const BnOff& b,
                    __nv_bfloat16* dc, bool relu, cudaStream_t st) {
     const rn::ReluSelf rs{relu ? master : nullptr, L.P, b.gamma, b.beta};
@@ -2718,15 +2786,15 @@ struct Engine {
       mb::dw_fwd(x, shadow, L.P, o.w1, (int)n, bp, S.H, S.pin, 2, d.L1, st);
       bn(G, bp, d.L1, ho, S.pin, d.id[0], o.b1, false, eval, d.L1a, st);
       if ((rc = tc::gemm_run(dps[s].l2f, st, G))) return rc;
-      bn(G, bp, d.L2, ho, S.pm, d.id[1], o.b2, true, eval, d.L2a, st);
+      if (!eval) bn_stats(G, bp, d.L2, ho, S.pm, d.id[1], o.b2, st);  // applied inside the shuffle
       if ((rc = tc::gemm_run(dps[s].r1f, st, G))) return rc;
       bn(G, bp, d.R1, hi, S.pm, d.id[2], o.b3, true, eval, d.R1a, st);
       mb::dw_fwd(d.R1a, shadow, L.P, o.w4, (int)n, bp, S.H, S.pm, 2, d.R2, st);
       bn(G, bp, d.R2, ho, S.pm, d.id[3], o.b4, false, eval, d.R2a, st);
       if ((rc = tc::gemm_run(dps[s].r3f, st, G))) return rc;
-      bn(G, bp, d.R3, ho, S.pm, d.id[4], o.b5, true, eval, d.R3a, st);
-      shuffle_split_kernel<<<grid_for(n * ho * S.pm / 4), 256, 0, st>>>(d.L2a, S.pm, d.R3a, S.pm, S.mid, S.pm, n * ho,
-                                                                        d.Y);
+      if (!eval) bn_stats(G, bp, d.R3, ho, S.pm, d.id[4], o.b5, st);
+      shuffle(G, bp, ho, S, side(d.L2, S.pm, d.id[1], o.b2, eval), side(d.R3, S.pm, d.id[4], o.b5, eval), eval, d.Y,
+              st);
       x = d.Y;
       for (int j = 0; j < S.nb; ++j) {
         const BasicOff& bo = L.bb[s][j];
@@ -2736,9 +2804,9 @@ struct Engine {
         mb::dw_fwd(b.B1a, shadow, L.P, bo.w2, (int)n, bp, Ho, S.pm, 1, b.B2, st);
         bn(G, bp, b.B2, ho, S.pm, b.id[1], bo.b2, false, eval, b.B2a, st);
         if ((rc = tc::gemm_run(bps[s][j].b3f, st, G))) return rc;
-        bn(G, bp, b.B3, ho, S.pm, b.id[2], bo.b3, true, eval, b.B3a, st);
-        shuffle_split_kernel<<<grid_for(n * ho * S.pm / 4), 256, 0, st>>>(x, 2 * S.pm, b.B3a, S.pm, S.mid, S.pm, n * ho,
-                                                                          b.Y);
+        if (!eval) bn_stats(G, bp, b.B3, ho, S.pm, b.id[2], bo.b3, st);
+        shuffle(G, bp, ho, S, ShufSide{x, 2 * S.pm, nullptr, 0, 0, 0, 0}, side(b.B3, S.pm, b.id[2], bo.b3, eval), eval,
+                b.Y, st);
         x = b.Y;
       }
     }
