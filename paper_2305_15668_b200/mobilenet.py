@@ -1,6 +1,6 @@
 """CIFAR MobileNetV2 clients on the B200 (BASELINE.json config 4, builder-defined).
 
-Host side of the MobileNetV2 engine (csrc/resnet.cu, namespace ``mb``): the architecture table, the padded
+Host side of the MobileNetV2 engine (csrc/mobilenet.cu): the architecture table, the padded
 parameter layout (every channel count rounded up to a multiple of 64; the padding entries are zero and stay
 zero) and its conversion to / from torch's canonical state tensors, a torch-default-style initialisation
 from a PCG64 seed, and ``MobilenetFederation`` -- a DeviceFederation whose ``train`` runs

@@ -1,6 +1,6 @@
 """CIFAR ShuffleNetV2 x1.0 clients on the B200 (BASELINE.json config 4's other model; builder-defined).
 
-Host side of the ShuffleNetV2 engine (csrc/resnet.cu, namespace ``sn``): the architecture table, the padded
+Host side of the ShuffleNetV2 engine (csrc/shufflenet.cu): the architecture table, the padded
 parameter layout and its conversion to / from torch's canonical state tensors, a torch-default-style
 initialisation from a PCG64 seed, and ``ShufflenetFederation`` (same contract as MobilenetFederation:
 per-client step counts, descending-step order, delta rows kept in participant order).
