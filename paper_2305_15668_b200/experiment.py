@@ -279,7 +279,7 @@ def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParam
         runner = FederatedRunner(fed, by_id, cfg, train.lr, params=params)
 
         def record(plan, acc):
-            report.rounds.append(plan.report)
+            report.rounds.append(plan.report.full() if hasattr(plan.report, "full") else plan.report)
             report.participants.append(list(plan.all_participants))
 
         report.accuracy_series.extend(runner.run(cfg.rounds, on_round=record))
@@ -382,6 +382,12 @@ class FederatedRunner:
         self.partial = torch.empty(fed.P, dtype=torch.float64, device=dev)
         self.one = torch.ones(1, dtype=torch.float64, device=dev)
         self._repr = {cid: repr(cid).encode() for cid in self.ids}
+        # per-round host work in plain arrays: repr pointers for the native seed hash, simulator indices,
+        # the one-time budget > theta screen (such participants take sim.run's error path)
+        self._repr_keep = [C.c_char_p(self._repr[c]) for c in self.ids]
+        self._repr_ptr = np.array([C.cast(b, C.c_void_p).value for b in self._repr_keep], dtype=np.uint64)
+        self._sim_idx = np.array([self.sim.index[c] for c in self.ids], dtype=np.int32)
+        self._over_theta = np.array([fleet[c].resource_budget > cfg.theta for c in self.ids], dtype=bool)
         n = self.SLOTS
         self._cap = [0] * n
         self._pinned = [None] * n
@@ -474,7 +480,11 @@ class FederatedRunner:
         # sequence as sampling the ids (engine.py:327), and gives the fleet indices directly
         who_idx = self.selector.sample(range(len(self.ids)), cfg.participants_per_round)
         who = [self.ids[i] for i in who_idx]
-        rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
+        wi = np.asarray(who_idx, np.int64)
+        if self._over_theta[wi].any():   # sim.run raises the reference's ConfigError
+            rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
+        else:
+            rep = self.sim.run_lean(self._sim_idx[wi], who, cfg, t0=t0, round_index=r)
         t1 = time.perf_counter()
         lo, hi = self._shard_bounds(len(who), self.world, self.rank)
         mine = who[lo:hi]
@@ -483,11 +493,11 @@ class FederatedRunner:
         weights_all = self._c_w[np.asarray(who_idx, np.int64)].tolist()
         total = float(sum(weights_all))                      # CPython float sum, as the reference
         coef = np.asarray(weights_all[lo:hi], np.float64) / total
-        reprs = (C.c_char_p * max(k, 1))(*[self._repr[c] for c in mine])
+        reprs = self._repr_ptr[mi] if k else self._repr_ptr[:1]   # const char* per participant
         train_seeds = np.zeros(max(k, 1), np.uint64)
         rng_seeds = np.zeros(max(k, 1), np.uint64)
-        _abi.check(_abi.lib.fedhc_round_seeds(int(cfg.seed), int(r), reprs, k, train_seeds.ctypes.data,
-                                              rng_seeds.ctypes.data))
+        _abi.check(_abi.lib.fedhc_round_seeds(int(cfg.seed), int(r), reprs.ctypes.data_as(C.POINTER(C.c_char_p)), k,
+                                              train_seeds.ctypes.data, rng_seeds.ctypes.data))
         t2 = time.perf_counter()
         rows = self._c_rows[mi]
         perms = self._c_nperm[mi]

@@ -85,6 +85,7 @@ class RoundSimulator:
         self._id_arr = (C.c_char_p * max(n, 1))(*self._id_bytes)
         self.budget = {cid: fleet[cid].resource_budget for cid in self.ids}
         self._sim = _abi.lib.fedhc_des_create()
+        self._lean_cap, self._lean_key, self._lean_conf = 0, None, None
 
     def __del__(self):
         sim = getattr(self, "_sim", None)
@@ -149,6 +150,53 @@ class RoundSimulator:
         )
         return report, seg
 
+    def run_lean(self, order: np.ndarray, participant_ids: list[str], cfg: FleetConfig, t0: float = 0.0,
+                 round_index: int = 0) -> "LeanRoundReport":
+        """`run` for the serving loop: `order` are this simulator's client indices (int32) of participants the
+        caller has already validated; buffers and the config block are reused, and the per-client dicts of
+        the RoundReport are built only if someone asks (LeanRoundReport.full / attribute access)."""
+        n = int(order.shape[0])
+        if n > self._lean_cap:
+            self._lean_cap = max(n, 2 * self._lean_cap)
+            self._lean_order = (C.c_int32 * self._lean_cap)()
+            self._lean_starts = (C.c_double * self._lean_cap)()
+            self._lean_ends = (C.c_double * self._lean_cap)()
+        C.memmove(self._lean_order, np.ascontiguousarray(order, dtype=np.int32).ctypes.data, 4 * n)
+        key = (cfg.theta, cfg.max_executors, cfg.scheduler_kind, cfg.dynamic_parallelism, cfg.alpha, cfg.beta,
+               cfg.launch_latency, cfg.terminate_latency, cfg.upload_latency)
+        if self._lean_key != key:
+            if cfg.scheduler_kind not in ("resource-aware", "greedy"):
+                raise KeyError(cfg.scheduler_kind)
+            self._lean_conf = _abi.DesConfig(float(cfg.theta), int(cfg.max_executors),
+                                             0 if cfg.scheduler_kind == "resource-aware" else 1,
+                                             int(bool(cfg.dynamic_parallelism)), float(cfg.alpha), float(cfg.beta),
+                                             float(cfg.launch_latency), float(cfg.terminate_latency),
+                                             float(cfg.upload_latency))
+            self._lean_key = key
+        rep = _abi.DesReport()
+        _abi.check(_abi.lib.fedhc_des_run_round(self._sim, self._clients, self._id_arr, self._lean_order, n,
+                                                C.byref(self._lean_conf), float(t0), int(round_index), 1,
+                                                self._lean_starts, self._lean_ends, C.byref(rep)))
+        ev = C.POINTER(_abi.DesEvent)()
+        ac = C.POINTER(C.c_int32)()
+        ash = C.POINTER(C.c_double)()
+        pt = C.POINTER(C.c_double)()
+        pn = C.POINTER(C.c_int32)()
+        npar = C.c_int()
+        _abi.check(_abi.lib.fedhc_des_trace(self._sim, C.byref(ev), C.byref(ac), C.byref(ash), C.byref(pt),
+                                            C.byref(pn), C.byref(npar)))
+        events = np.ctypeslib.as_array(C.cast(ev, C.POINTER(C.c_uint8)), shape=(rep.n_events * _EVENT.itemsize,))
+        events = events.view(_EVENT)
+        kinds, who = events["kind"], events["client"]
+        return LeanRoundReport(
+            round_index, rep.makespan, rep.utilization, rep.vacancy_area, rep.throughput, bool(rep.degenerate),
+            participant_ids, who[kinds == _abi.EV_LAUNCHED].copy(), who[kinds == _abi.EV_UPLOADED].copy(),
+            np.ctypeslib.as_array(self._lean_starts, shape=(self._lean_cap,))[:n].copy(),
+            np.ctypeslib.as_array(self._lean_ends, shape=(self._lean_cap,))[:n].copy(),
+            np.ctypeslib.as_array(pt, shape=(npar.value,)).copy() if npar.value else None,
+            np.ctypeslib.as_array(pn, shape=(npar.value,)).copy() if npar.value else None,
+            self.budget)
+
     @staticmethod
     def _event_dict(e, pid, ac, ash) -> dict:
         kind = e.kind
@@ -168,6 +216,38 @@ class RoundSimulator:
         name = {_abi.EV_LAUNCHED: "ClientLaunched", _abi.EV_TRAINED: "ClientTrainingComplete",
                 _abi.EV_UPLOADED: "ModelUploaded"}[kind]
         return {"t": e.t, "kind": name, "client": pid[e.client], "executor": e.executor, "budget": e.budget}
+
+
+class LeanRoundReport:
+    """A RoundReport whose per-client dicts are built on first use (the scalar fields are plain attributes)."""
+
+    def __init__(self, round_index, makespan, utilization, vacancy_area, throughput, degenerate, pid, launch, upload,
+                 starts, ends, par_t, par_n, budget):
+        self.round_index, self.makespan, self.utilization = round_index, makespan, utilization
+        self.vacancy_area, self.throughput, self.degenerate = vacancy_area, throughput, degenerate
+        self._raw = (pid, launch, upload, starts, ends, par_t, par_n, budget)
+        self._full = None
+
+    def full(self) -> RoundReport:
+        if self._full is None:
+            pid, launch, upload, starts, ends, par_t, par_n, budget = self._raw
+            st_l, en_l = starts.tolist(), ends.tolist()
+            lo, up = launch.tolist(), upload.tolist()
+            self._full = RoundReport(
+                round_index=self.round_index, makespan=self.makespan, utilization=self.utilization,
+                vacancy_area=self.vacancy_area, throughput=self.throughput,
+                parallelism_timeline=list(zip(par_t.tolist(), par_n.tolist())) if par_t is not None else [],
+                per_client_times={pid[i]: en_l[i] - st_l[i] for i in up},
+                per_client_start={pid[i]: st_l[i] for i in lo},
+                per_client_end={pid[i]: en_l[i] for i in up},
+                per_client_budget={pid[i]: float(budget[pid[i]]) for i in lo},
+                degenerate=self.degenerate)
+        return self._full
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.full(), name)
 
 
 def run_round(fleet: dict[str, ClientProfile], participant_ids: list[str], cfg: FleetConfig, t0: float = 0.0,
