@@ -146,7 +146,9 @@ struct Engine {
   __nv_bfloat16 *shadow, *cols0, *c0, *a0, *dyh;
   __nv_bfloat16 *e[NBLK], *ea[NBLK], *d[NBLK], *da[NBLK], *p[NBLK], *sc[NBLK], *y[NBLK];
   __nv_bfloat16 *fh, *fha;  // head conv output / post-BN-ReLU [n][16][1280]
-  __nv_bfloat16 *cur, *g0, *g1, *g2, *g3, *g4;
+  // gb[k & 1] = dL/d(output) of the k-th block in backward order, gb[(k + 1) & 1] its dL/d(input); the
+  // data-gradient GEMM plans capture these addresses, so the alternation is fixed (no copies between blocks)
+  __nv_bfloat16 *cur, *gx, *gb[2], *g0, *g1, *g2, *g3, *g4;
   int32_t *labels, *valid;
   int* step_ctr;  // device local-step counter (graphs are step-invariant)
   unsigned long long* ecorrect;  // eval graphs count here; added to the caller's counter afterwards
@@ -236,6 +238,9 @@ struct Engine {
     rc |= alloc(&fha, I * 16 * HEADC);
     rc |= alloc(&dyh, I * 16 * HEADC);
     rc |= alloc(&cur, I * scratch);
+    rc |= alloc(&gx, I * scratch);
+    gb[0] = cur;
+    gb[1] = gx;
     rc |= alloc(&g0, I * scratch);
     rc |= alloc(&g1, I * scratch);
     rc |= alloc(&g2, I * scratch);
@@ -325,10 +330,11 @@ struct Engine {
       if ((rc = pw_fwd(G, bp, ho, ppl, pco, da[i], L.c3[i], p[i], &bps[i].c3f))) return rc;
       if (has_proj(d) && (rc = pw_fwd(G, bp, d.H, pci, pco, x, L.cs[i], sc[i], &bps[i].csf))) return rc;
       if (!train) continue;
-      // backward buffers: g0 = dP, g1 = dDA, g0 (later) = dE, g1 (later) = dX, g4 = dXs, g1 (early) = dSC
+      // backward buffers: g0 = dP, g1 = dDA, g0 (later) = dE, gb[(k + 1) & 1] = dX (k = NBLK - 1 - i),
+      // g4 = dXs, g1 (early) = dSC
       if ((rc = pw_dgrad(G, bp, ho, ppl, pco, g0, L.c3[i], g1, &bps[i].c3d))) return rc;
       if ((rc = pw_wgrad(G, bp, ho, ppl, pco, da[i], g0, L.c3[i], lr, &bps[i].c3w))) return rc;
-      if ((rc = pw_dgrad(G, bp, d.H, pci, ppl, g0, L.c1[i], g1, &bps[i].c1d))) return rc;
+      if ((rc = pw_dgrad(G, bp, d.H, pci, ppl, g0, L.c1[i], gb[(NBLK - i) & 1], &bps[i].c1d))) return rc;
       if ((rc = pw_wgrad(G, bp, d.H, pci, ppl, x, g0, L.c1[i], lr, &bps[i].c1w))) return rc;
       if (has_proj(d)) {
         if ((rc = pw_dgrad(G, bp, d.H, pci, pco, g1, L.cs[i], g4, &bps[i].csd))) return rc;
@@ -529,6 +535,7 @@ struct Engine {
     for (int i = NBLK - 1; i >= 0; --i) {
       const BlkDef& d = B[i];
       const int ho = d.H / d.s, pci = pad64(d.cin), ppl = pad64(d.pl), pco = pad64(d.cout);
+      __nv_bfloat16 *cur = gb[(NBLK - 1 - i) & 1], *nx = gb[(NBLK - i) & 1];
       // cur = dL/dy[i] (no ReLU at the block output)
       bn_backward(G, cur, p[i], ho * ho, pco, id_b[i][2], L.bn3[i], g0, st);  // g0 = dP
       if (has_proj(d)) {
@@ -543,15 +550,14 @@ struct Engine {
       dw_wgrad(ea[i], g2, G, Bp, d.H, ppl, d.s, dwpart, st);
       dw_sgd_kernel<<<dim3((9 * ppl + 255) / 256, G), 256, 0, st>>>(dwpart, master, shadow, L.P, L.dw[i], ppl, lr);
       bn_backward(G, g3, e[i], d.H * d.H, ppl, id_b[i][0], L.bn1[i], g0, st, true);  // g0 = dE
-      if ((rc = tc::gemm_run(bp[i].c1d, st, G))) return rc;                         // g1 = dX
+      if ((rc = tc::gemm_run(bp[i].c1d, st, G))) return rc;                         // nx = dX
       if ((rc = run_wg(bp[i].c1w, G, lr, st))) return rc;
       const int64_t n8x = I * d.H * d.H * pci / 8;
-      if (has_proj(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(g1, g4, n8x);
-      if (has_ident(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(g1, cur, n8x);
-      FEDHC_CUDA_TRY(cudaMemcpyAsync(cur, g1, (size_t)n8x * 16, cudaMemcpyDeviceToDevice, st));
+      if (has_proj(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(nx, g4, n8x);
+      if (has_ident(d)) rn::add_kernel<<<grid_for(n8x), 256, 0, st>>>(nx, cur, n8x);
     }
-    // stem
-    bn_backward(G, cur, c0, 1024, 64, id_bn0, L.bn0, g0, st, true);
+    // stem: block 0's input gradient
+    bn_backward(G, gb[NBLK & 1], c0, 1024, 64, id_bn0, L.bn0, g0, st, true);
     if ((rc = tc::gemm_run(stem_w, st, G))) return rc;
     constexpr int CAP = (int)(sizeof(rn::BnSgdTable::C) / sizeof(int));
     for (size_t at = 0; at < bn_sgd.size(); at += CAP) {
