@@ -438,10 +438,9 @@ struct Engine {
       } else {
         add_kernel<<<grid_for(n8i), 256, 0, st>>>(g2, dz, n8i);  // identity shortcut
       }
-      // the next (earlier) block's output gradient: move g2 out of the scratch the next block reuses
-      const size_t bytes = (size_t)n8i * 16;
-      FEDHC_CUDA_TRY(cudaMemcpyAsync(up, g2, bytes, cudaMemcpyDeviceToDevice, st));
-      dy = up;
+      // the next (earlier) block's output gradient stays in g2: that block reads it once (its ReLU mask into
+      // g3) before anything writes g2 again
+      dy = g2;
     }
     // stem: bn0 backward of dY with the ReLU folded in -> dC0 (g0); Wstem SGD
     bn_backward(G, dy, c0, 1024, 64, 0, L.bn0, g0, st, true);
