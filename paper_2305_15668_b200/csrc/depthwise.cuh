@@ -152,7 +152,7 @@ static __global__ void __launch_bounds__(DW_THREADS) dw_dgrad_kernel(const __nv_
 constexpr int DW_SPLIT = 64;
 constexpr int DW_WGRAD_SMEM = DW_THREADS * 72 * 4;
 template <int S>
-static __global__ void __launch_bounds__(DW_THREADS) dw_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
+static __global__ void __launch_bounds__(DW_THREADS, 3) dw_wgrad_kernel(const __nv_bfloat16* __restrict__ x,
                                                        const __nv_bfloat16* __restrict__ dy, int Bp, int H, int C,
                                                        float* __restrict__ part) {
   extern __shared__ float red[];
