@@ -456,3 +456,36 @@ def test_runner_device_plan_matches_host_plan(fh):
         outs.append((params.clone(), series))
     assert torch.equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+def test_gemm_strided_operands_vs_torch(fh, a_mn):
+    """Row strides (fedhc_gemm_args.lda / ldd): A read as a column slice of a wider row-major tensor (the
+    ShuffleNetV2 engine's split-form X2 view) and D written into a column slice of a wider output."""
+    import ctypes as C
+    import torch
+    from paper_2305_15668_b200 import _abi
+    G, M, N, K, wide = 3, 256, 128, 64, 192
+    g = torch.Generator(device="cuda").manual_seed(7 + int(a_mn))
+    B = torch.randn(G, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    if a_mn:  # A stored [G][K][wide] MN-major, the GEMM reads columns [64, 64 + M') of each row
+        Mw = 64
+        big = torch.randn(G, K, wide, device="cuda", generator=g).to(torch.bfloat16)
+        A_view, lda, Mv = big[:, :, 64:64 + Mw], wide, Mw
+        ref = torch.bmm(A_view.float().transpose(1, 2), B.float().transpose(1, 2))
+        a_ptr = big.data_ptr() + 64 * 2
+    else:     # A stored [G][M][wide] K-major, the GEMM reads columns [64, 128)
+        big = torch.randn(G, M, wide, device="cuda", generator=g).to(torch.bfloat16)
+        A_view, lda, Mv = big[:, :, 64:64 + K], wide, M
+        ref = torch.bmm(A_view.float(), B.float().transpose(1, 2))
+        a_ptr = big.data_ptr() + 64 * 2
+    Dbig = torch.zeros(G, Mv, N + 64, dtype=torch.bfloat16, device="cuda")
+    args = _abi.GemmArgs(G=G, M=Mv, N=N, K=K, a_mn=int(a_mn), b_mn=0, A=a_ptr, B=B.data_ptr(),
+                         epilogue=1, D=Dbig.data_ptr() + 64 * 2, ldd=N + 64, lda=lda,
+                         a_gstride=big.shape[1] * wide)
+    _abi.check(_abi.lib.fedhc_gemm(C.byref(args), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    got = Dbig[:, :, 64:].float()
+    err = (got - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+    assert not Dbig[:, :, :64].any()  # columns outside the view untouched

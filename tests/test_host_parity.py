@@ -258,3 +258,23 @@ def test_dirichlet_counts_quotas():
     assert np.all(np.abs(flat / 2000 - 0.25) < 0.05)            # alpha -> inf: near IID
     skew = dirichlet_counts([500] * 30, 4, 0.05, seed=1)
     assert np.mean(skew.max(axis=1) / 500) > 0.7                 # alpha -> 0: concentrated
+
+
+def test_lean_round_report_matches_full_run():
+    """RoundSimulator.run_lean (the serving planner's DES call: reused buffers, per-client dicts on demand)
+    produces exactly RoundSimulator.run's report."""
+    import numpy as np
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200.roundsim import RoundSimulator
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 30, 50, 80)), 40, 5)
+    by_id = {p.client_id: p for p in fleet}
+    cfg = fh.FleetConfig(theta=100.0, max_executors=6, participants_per_round=12, seed=3)
+    sim = RoundSimulator(by_id)
+    rng = np.random.default_rng(1)
+    for r in range(4):
+        who = [sim.ids[i] for i in rng.choice(len(sim.ids), 12, replace=False)]
+        full, _ = sim.run(who, cfg, t0=1.5 * r, round_index=r, want_trace=False)
+        lean = sim.run_lean(np.array([sim.index[c] for c in who], np.int32), who, cfg, t0=1.5 * r, round_index=r)
+        assert lean.makespan == full.makespan
+        assert lean.full() == full
+        assert lean.per_client_times == full.per_client_times  # attribute access materialises
