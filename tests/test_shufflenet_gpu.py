@@ -218,3 +218,19 @@ def test_shufflenet_heterogeneous_steps_match_solo_runs(ssetup):
         assert np.array_equal(together[i], solo), cid
     loss = fed.engine.last_loss(1).cpu().numpy()
     assert np.isfinite(loss).all()
+
+
+def test_shufflenet_eval_spans_several_chunks(ssetup):
+    """Accuracy over a test set far larger than the workspace (one client x batch 8: eleven 8-row chunks, the
+    last one ragged) equals a workspace that takes the whole set in one chunk."""
+    import torch
+    from paper_2305_15668_b200 import training as tr
+    from paper_2305_15668_b200.shufflenet import ShufflenetFederation
+    s = ssetup
+    trn, tst = tr.make_synthetic_dataset(3072, s["C"], 420, 31)
+    shards = tr.partition_noniid(trn, [("e0", 16)], 0.5, 4)
+    small = ShufflenetFederation(shards, tst, 3072, s["C"]).attach_engine(1, 8)
+    big = ShufflenetFederation(shards, tst, 3072, s["C"]).attach_engine(3, 32)
+    assert small.n_test > 8 and small.n_test % 8 and small.n_test <= 96
+    params = torch.tensor(small.layout.to_padded(s["p"]), dtype=torch.float64, device="cuda")
+    assert small.correct(params) == big.correct(params)
