@@ -363,7 +363,7 @@ class FederatedRunner:
 
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
-                 plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = True,
+                 plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = False,
                  green_plan: bool = False):
         from .sharding import shard_bounds
 

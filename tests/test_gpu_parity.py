@@ -438,7 +438,8 @@ def test_device_permutations_match_numpy(fh):
 
 
 def test_runner_device_plan_matches_host_plan(fh):
-    """FederatedRunner with GPU-generated batch order == host-generated order, bit for bit, over 3 rounds."""
+    """FederatedRunner with GPU-generated batch order == host-generated order, and CUDA-graph replay == eager
+    launches, bit for bit, over 4 rounds (graphs are captured at a slot's first use, replayed after)."""
     import torch
     from paper_2305_15668_b200.devicedata import DeviceFleetData
     from paper_2305_15668_b200.experiment import FederatedRunner
@@ -449,13 +450,16 @@ def test_runner_device_plan_matches_host_plan(fh):
     data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, 10, 0.5, seed=3, n_test=2000)
     cfg = fh.FleetConfig(participants_per_round=16, max_executors=8, seed=9)
     outs = []
-    for device_perm in (False, True):
+    # host plan, device plan (eager launches, the default), device plan replayed from per-slot CUDA graphs
+    for device_perm, graphs in ((False, False), (True, False), (True, True)):
         params = torch.zeros(7850, dtype=torch.float64, device="cuda")
-        r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, device_permutations=device_perm)
-        series = r.run(3)
+        r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, device_permutations=device_perm,
+                            use_graphs=graphs)
+        series = r.run(4)
         outs.append((params.clone(), series))
-    assert torch.equal(outs[0][0], outs[1][0])
-    assert outs[0][1] == outs[1][1]
+    for o in outs[1:]:
+        assert torch.equal(outs[0][0], o[0])
+        assert outs[0][1] == o[1]
 
 
 @pytest.mark.parametrize("a_mn", [False, True])
