@@ -458,6 +458,7 @@ class FederatedRunner:
         self._c_yptr = fed.y.data_ptr() + off * 4
         self.now = 0.0
         self.round = 0
+        self._prefetch = None  # next run()'s first RoundPlan, planned during the previous run
         self.h2d_bytes = 0
         self.d2h_bytes = 8
         self.host_s = {"select+des": 0.0, "seeds": 0.0, "permutations": 0.0, "descriptors": 0.0, "launch": 0.0}
@@ -711,15 +712,25 @@ class FederatedRunner:
             return []
         ready: queue.Queue = queue.Queue(maxsize=self.SLOTS - 1)
         free: queue.Queue = queue.Queue()
+        # the previous call planned this call's first round while its last round drained (no pipeline fill)
+        pre, self._prefetch = self._prefetch, None
         for sl in range(self.SLOTS):
-            free.put(sl)
+            if not isinstance(pre, RoundPlan) or sl != pre.slot:
+                free.put(sl)
         failure = []
 
         def planner():
             t, r0 = self.now, self.round
             try:
                 torch.cuda.set_device(self.dev)  # bind the device context in this thread (it launches plan work)
-                for i in range(rounds):
+                start = 0
+                if isinstance(pre, BaseException):  # planning this round failed during the previous call
+                    raise pre
+                if pre is not None:
+                    t = pre.t0 + pre.report.makespan
+                    ready.put(pre)
+                    start = 1
+                for i in range(start, rounds):
                     slot = free.get()
                     pl = self.plan(r0 + i, t, slot)
                     # queue the round's [H2D + device permutations] graph right away, so the batch
@@ -730,6 +741,12 @@ class FederatedRunner:
             except BaseException as exc:  # surface planner errors in the caller
                 failure.append(exc)
                 ready.put(None)
+                return
+            try:  # plan the next call's first round now (overlaps this call's last round)
+                slot = free.get()
+                self._prefetch = self.plan(r0 + rounds, t, slot)
+            except BaseException as exc:  # e.g. a ConfigError for that round: raised by the next call
+                self._prefetch = exc
 
         th = threading.Thread(target=planner, daemon=True)
         th.start()

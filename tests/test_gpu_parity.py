@@ -457,6 +457,11 @@ def test_runner_device_plan_matches_host_plan(fh):
                             use_graphs=graphs)
         series = r.run(4)
         outs.append((params.clone(), series))
+    # the same 4 rounds as run(1) + run(3): each call plans the next call's first round while draining
+    params = torch.zeros(7850, dtype=torch.float64, device="cuda")
+    r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params)
+    outs.append((None, r.run(1) + r.run(3)))
+    outs[-1] = (params.clone(), outs[-1][1])
     for o in outs[1:]:
         assert torch.equal(outs[0][0], o[0])
         assert outs[0][1] == o[1]
