@@ -268,24 +268,43 @@ def run_ours(args, rank, world, local_rank):
         coef = [float(w.num_samples) / total for w in wl]
         return rep, mine, wl, seeds, coef
 
+    eval_stream = torch.cuda.Stream()
+    eval_done = [None]
+
     def device_round(mine_desc, coef_dev, correct):
-        """train -> FedAvg partial -> (all-reduce) -> apply -> sharded accuracy; returns train events."""
+        """train -> FedAvg partial -> (all-reduce) -> apply -> sharded accuracy; returns train events.
+        Single GPU: the accuracy runs on its own stream, overlapping the next round's training (both only
+        read the params; the next FedAvg waits for it), as FederatedRunner does."""
+        main = torch.cuda.current_stream()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         _abi.check(_abi.lib.fedhc_local_train(mine_desc.data_ptr(), PER_GPU, params.data_ptr(), F, C, BATCH,
                                               stream_ptr()))
         ev1.record()
         if world == 1:
+            if eval_done[0] is not None:
+                main.wait_event(eval_done[0])
             fedavg_device(deltas, coef_dev, params, params)
-        else:
-            fedavg_device(deltas, coef_dev, None, partial)
-            dist.all_reduce(partial)
-            fedavg_device(partial.view(1, -1), one, params, params)
+            agg = torch.cuda.Event()
+            agg.record(main)
+            eval_stream.wait_event(agg)
+            _abi.check(_abi.lib.fedhc_eval(fed.x_test.data_ptr(), fed.y_test.data_ptr(), fed.n_test, F, C,
+                                           params.data_ptr(), correct.data_ptr(), eval_stream.cuda_stream))
+            done = torch.cuda.Event()
+            done.record(eval_stream)
+            eval_done[0] = done
+            return ev0, ev1
+        fedavg_device(deltas, coef_dev, None, partial)
+        dist.all_reduce(partial)
+        fedavg_device(partial.view(1, -1), one, params, params)
         _abi.check(_abi.lib.fedhc_eval(fed.x_test.data_ptr(), fed.y_test.data_ptr(), fed.n_test, F, C,
                                        params.data_ptr(), correct.data_ptr(), stream_ptr()))
-        if world > 1:
-            dist.all_reduce(correct)
+        dist.all_reduce(correct)
         return ev0, ev1
+
+    def join_eval():
+        if eval_done[0] is not None:
+            torch.cuda.current_stream().wait_event(eval_done[0])
 
     def barrier():
         if dist is not None:
@@ -315,6 +334,7 @@ def run_ours(args, rank, world, local_rank):
         t_start.record()
         for r in range(args.warmup, total_rounds):
             train_events.append(device_round(plans[r][1], plans[r][2], counts[r:r + 1]))
+        join_eval()  # the last round's accuracy belongs to the timed region
         t_end.record()
         barrier()
     ms = t_start.elapsed_time(t_end)

@@ -435,6 +435,11 @@ class FederatedRunner:
         self._ev_plan = [torch.cuda.Event() for _ in range(n)]
         self._ev_train = [torch.cuda.Event() for _ in range(n)]
         self._ev_result = [torch.cuda.Event() for _ in range(n)]
+        # single-GPU eager rounds: accuracy of round r runs on its own stream, overlapping round r + 1's
+        # training (both only read the params); round r + 1's FedAvg waits for it before writing them
+        self._eval_stream = torch.cuda.Stream(device=dev)
+        self._ev_agg = [torch.cuda.Event() for _ in range(n)]
+        self._eval_done = None
         # per-client constants, indexed like self.ids (vectorised planning)
         F = fed.n_features
         off = np.array([fed.offset[c][0] for c in self.ids], np.int64)
@@ -622,6 +627,9 @@ class FederatedRunner:
                 self.launch_plan(p)
             gs = self._graphs[slot]
             main.wait_event(self._ev_plan[slot])
+            if self._eval_done is not None:  # an eager round's accuracy may still be reading the params
+                main.wait_event(self._eval_done)
+                self._eval_done = None
             self._plan_done[slot] = self._ev_plan[slot]
             gs[2].replay()
             self._ev_train[slot].record()
@@ -675,6 +683,8 @@ class FederatedRunner:
         self._ev_train[slot].record()
         self._train_done[slot] = self._ev_train[slot]
         if self.world == 1:
+            if self._eval_done is not None:
+                main.wait_event(self._eval_done)  # the previous round's accuracy is done reading the params
             if k:
                 fedavg_device(self.deltas[:k], coef_t, self.params, self.params)
         else:
@@ -684,15 +694,29 @@ class FederatedRunner:
                 self.partial.zero_()
             combine_partials(self.partial, self.params,
                              lambda s, prm: fedavg_device(s.view(1, -1), self.one, prm, prm), self.group)
-        self.correct_dev.zero_()
-        if self.fed.n_test:
-            _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
-                                           self.fed.n_test, self.fed.n_features, self.fed.n_classes,
-                                           self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
-        if self.world > 1:
+        if self.world == 1:
+            es = self._eval_stream
+            self._ev_agg[slot].record(main)
+            es.wait_event(self._ev_agg[slot])
+            with torch.cuda.stream(es):
+                self.correct_dev.zero_()
+                if self.fed.n_test:
+                    _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
+                                                   self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                                                   self.params.data_ptr(), self.correct_dev.data_ptr(),
+                                                   es.cuda_stream))
+                self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
+                self._ev_result[slot].record(es)
+            self._eval_done = self._ev_result[slot]
+        else:
+            self.correct_dev.zero_()
+            if self.fed.n_test:
+                _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
+                                               self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                                               self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
             all_reduce_count(self.correct_dev, self.group)
-        self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
-        self._ev_result[slot].record()
+            self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
+            self._ev_result[slot].record()
         self._result_ev[slot] = self._ev_result[slot]
         if self.use_graphs and k and p.meta_bytes and (gs is None or gs[0] != self._graph_key(p)):
             self._capture(p)
