@@ -269,6 +269,8 @@ def run_ours(args, rank, world, local_rank):
         return rep, mine, wl, seeds, coef
 
     eval_stream = torch.cuda.Stream()
+    # the accuracy overlaps the next round's training (one CTA per client): keep it on the idle SMs
+    eval_ctas = max(8, torch.cuda.get_device_properties(dev).multi_processor_count - PER_GPU)
     eval_done = [None]
 
     def device_round(mine_desc, coef_dev, correct):
@@ -288,8 +290,9 @@ def run_ours(args, rank, world, local_rank):
             agg = torch.cuda.Event()
             agg.record(main)
             eval_stream.wait_event(agg)
-            _abi.check(_abi.lib.fedhc_eval(fed.x_test.data_ptr(), fed.y_test.data_ptr(), fed.n_test, F, C,
-                                           params.data_ptr(), correct.data_ptr(), eval_stream.cuda_stream))
+            _abi.check(_abi.lib.fedhc_eval_ctas(fed.x_test.data_ptr(), fed.y_test.data_ptr(), fed.n_test, F, C,
+                                                params.data_ptr(), correct.data_ptr(), eval_ctas,
+                                                eval_stream.cuda_stream))
             done = torch.cuda.Event()
             done.record(eval_stream)
             eval_done[0] = done

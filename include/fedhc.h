@@ -130,6 +130,11 @@ int fedhc_fedavg(const void* const* deltas, const void* packed, int64_t ld, int 
  * *correct (dev uint64) += number of rows whose first-max argmax == label. */
 int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
                const double* params, unsigned long long* correct, void* stream);
+/* Same, on at most max_ctas SMs (<= 0: all).  The round loop runs round r's
+ * accuracy concurrently with round r+1's training (one CTA per client) and
+ * caps it to the SMs the training leaves idle. */
+int fedhc_eval_ctas(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
+                    const double* params, unsigned long long* correct, int max_ctas, void* stream);
 
 /* ---- round DES: engine.run_round (engine.py:53-230) --------------------- */
 /* Host-only discrete-event simulation of one round under capped max-min

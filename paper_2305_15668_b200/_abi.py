@@ -118,6 +118,7 @@ SIGNATURES = {
     "fedhc_fedavg_coefficients": (_i, [_dp, _i, _dp]),
     "fedhc_fedavg": (_i, [_vp, _vp, _i64, _i, _vp, _i, _vp, _vp, _i64, _vp]),
     "fedhc_eval": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]),
+    "fedhc_eval_ctas": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _i, _vp]),
     "fedhc_des_create": (_vp, []),
     "fedhc_des_destroy": (None, [_vp]),
     "fedhc_des_run_round": (

@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(kEvalThreads, 1)
 
 using namespace fedhc;
 
-extern "C" int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
-                          const double* params, unsigned long long* correct, void* stream) {
+extern "C" int fedhc_eval_ctas(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
+                               const double* params, unsigned long long* correct, int max_ctas, void* stream) {
   if (n_features < 1 || n_classes < 1) return fail(FEDHC_ERR_VALUE, "eval: bad shape");
   if (n <= 0) return FEDHC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -102,8 +102,14 @@ extern "C" int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_fea
     smem_set = (int)smem;
   }
   const int64_t need = (n + (kEvalThreads / 32) - 1) / (kEvalThreads / 32);
-  const int blocks = static_cast<int>(std::min<int64_t>(need, (int64_t)sms));
+  const int cap = max_ctas > 0 ? std::min(max_ctas, sms) : sms;
+  const int blocks = static_cast<int>(std::min<int64_t>(need, (int64_t)cap));
   eval_kernel<<<blocks, kEvalThreads, smem, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);
   FEDHC_CUDA_TRY(cudaGetLastError());
   return FEDHC_OK;
+}
+
+extern "C" int fedhc_eval(const float* x, const int32_t* y, int64_t n, int n_features, int n_classes,
+                          const double* params, unsigned long long* correct, void* stream) {
+  return fedhc_eval_ctas(x, y, n, n_features, n_classes, params, correct, 0, stream);
 }

@@ -11,6 +11,13 @@
 // add (no FMA contraction) -- the exact operation sequence of the
 // reference's `out += (w / total) * d` loop, so fp64 inputs give
 // bit-identical results.
+//
+// Short vectors (fewer than one 4-element thread per SM of the streaming
+// kernel -- the logistic model has P = 7850) are latency-bound instead: a
+// thread's K dependent loads cost ~K/8 memory round trips.  There
+// `fedavg_tile_kernel` gives each CTA 128 elements, stages a [KT][128] tile of
+// all its delta rows into shared memory with cp.async (every load in flight
+// at once), then runs the same list-order fp64 chain from shared memory.
 #include "common.cuh"
 
 namespace fedhc {
@@ -107,6 +114,69 @@ __global__ void __launch_bounds__(kAvgThreads)
   }
 }
 
+constexpr int kTileE = 128;          // elements (= threads) per CTA
+constexpr int kTileBytes = 64 << 10;  // delta tile per K block
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTileE)
+    fedavg_tile_kernel(const T* const* __restrict__ ptrs, const T* __restrict__ packed, int64_t ld,
+                       const double* __restrict__ coef, int K, const double* base, double* out, int64_t n) {
+  constexpr int KT = kTileBytes / (kTileE * (int)sizeof(T));  // delta rows per block
+  constexpr int kPer = 16 / (int)sizeof(T);                   // elements per 16-byte chunk
+  constexpr int kCpr = kTileE / kPer;                         // chunks per row
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* tile = reinterpret_cast<T*>(smem);  // [KT][kTileE]
+  __shared__ double s_coef[KT];
+  __shared__ const T* s_ptr[KT];
+  const int tid = threadIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * kTileE;
+  const int64_t e = e0 + tid;
+  double acc = (base != nullptr && e < n) ? base[e] : 0.0;
+  for (int k0 = 0; k0 < K; k0 += KT) {
+    const int kt = min(KT, K - k0);
+    __syncthreads();  // previous block's tile fully consumed
+    int misaligned = 0;
+    for (int i = tid; i < kt; i += kTileE) {
+      s_coef[i] = coef[k0 + i];
+      const T* ptr = ptrs != nullptr ? ptrs[k0 + i] : packed + (int64_t)(k0 + i) * ld;
+      s_ptr[i] = ptr;
+      misaligned |= (reinterpret_cast<uintptr_t>(ptr) & 15) != 0;
+    }
+    const bool vec = __syncthreads_or(misaligned) == 0;
+    if (vec) {
+      for (int i = tid; i < kt * kCpr; i += kTileE) {
+        const int r = i / kCpr, c = i - r * kCpr;
+        const int64_t idx = e0 + (int64_t)c * kPer;
+        const int64_t rem = n - idx;
+        const int bytes = rem <= 0 ? 0 : (rem >= kPer ? 16 : static_cast<int>(rem) * (int)sizeof(T));
+        cp_async16(tile + r * kTileE + c * kPer, bytes ? s_ptr[r] + idx : s_ptr[r], bytes);  // zero-fills
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;\n" ::: "memory");
+    } else {
+      for (int r = 0; r < kt; ++r) tile[r * kTileE + tid] = e < n ? s_ptr[r][e] : T(0);
+    }
+    __syncthreads();
+    if (e < n) {
+      int k = 0;
+      for (; k + 4 <= kt; k += 4) {
+        const T v0 = tile[k * kTileE + tid], v1 = tile[(k + 1) * kTileE + tid];
+        const T v2 = tile[(k + 2) * kTileE + tid], v3 = tile[(k + 3) * kTileE + tid];
+        acc = __dadd_rn(acc, __dmul_rn(s_coef[k], static_cast<double>(v0)));
+        acc = __dadd_rn(acc, __dmul_rn(s_coef[k + 1], static_cast<double>(v1)));
+        acc = __dadd_rn(acc, __dmul_rn(s_coef[k + 2], static_cast<double>(v2)));
+        acc = __dadd_rn(acc, __dmul_rn(s_coef[k + 3], static_cast<double>(v3)));
+      }
+      for (; k < kt; ++k) acc = __dadd_rn(acc, __dmul_rn(s_coef[k], static_cast<double>(tile[k * kTileE + tid])));
+    }
+  }
+  if (e < n) out[e] = acc;
+}
+
 }  // namespace fedhc
 
 using namespace fedhc;
@@ -144,6 +214,35 @@ extern "C" int fedhc_fedavg(const void* const* deltas, const void* packed, int64
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t blocks = (n + 4LL * kAvgThreads - 1) / (4LL * kAvgThreads);
   if (blocks > 0x7fffffffLL) return fail(FEDHC_ERR_UNSUPPORTED, "fedavg: vector too long");
+  if (dtype != FEDHC_F32 && dtype != FEDHC_F64)
+    return fail(FEDHC_ERR_VALUE, "fedavg: dtype must be FEDHC_F32 or FEDHC_F64");
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    FEDHC_CUDA_TRY(cudaGetDevice(&dev));
+    FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (blocks < sms) {  // short vector: latency-bound, stage every delta row through shared memory at once
+    static bool attr = false;
+    if (!attr) {
+      FEDHC_CUDA_TRY(cudaFuncSetAttribute(fedavg_tile_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kTileBytes));
+      FEDHC_CUDA_TRY(cudaFuncSetAttribute(fedavg_tile_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kTileBytes));
+      attr = true;
+    }
+    const unsigned tb = static_cast<unsigned>((n + kTileE - 1) / kTileE);
+    if (dtype == FEDHC_F32)
+      fedavg_tile_kernel<float><<<tb, kTileE, kTileBytes, st>>>(
+          reinterpret_cast<const float* const*>(deltas), static_cast<const float*>(packed), ld, coef, n_deltas,
+          base, out, n);
+    else
+      fedavg_tile_kernel<double><<<tb, kTileE, kTileBytes, st>>>(
+          reinterpret_cast<const double* const*>(deltas), static_cast<const double*>(packed), ld, coef, n_deltas,
+          base, out, n);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
+  }
   if (dtype == FEDHC_F32) {
     fedavg_kernel<float><<<(unsigned)blocks, kAvgThreads, 0, st>>>(
         reinterpret_cast<const float* const*>(deltas), static_cast<const float*>(packed), ld, coef, n_deltas, base,

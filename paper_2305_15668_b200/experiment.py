@@ -438,6 +438,7 @@ class FederatedRunner:
         # single-GPU eager rounds: accuracy of round r runs on its own stream, overlapping round r + 1's
         # training (both only read the params); round r + 1's FedAvg waits for it before writing them
         self._eval_stream = torch.cuda.Stream(device=dev)
+        self._sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self._ev_agg = [torch.cuda.Event() for _ in range(n)]
         self._eval_done = None
         # per-client constants, indexed like self.ids (vectorised planning)
@@ -701,10 +702,12 @@ class FederatedRunner:
             with torch.cuda.stream(es):
                 self.correct_dev.zero_()
                 if self.fed.n_test:
-                    _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
-                                                   self.fed.n_test, self.fed.n_features, self.fed.n_classes,
-                                                   self.params.data_ptr(), self.correct_dev.data_ptr(),
-                                                   es.cuda_stream))
+                    # overlaps the next round's training (one CTA per client): stay on the idle SMs
+                    ctas = max(8, self._sms - k)
+                    _abi.check(_abi.lib.fedhc_eval_ctas(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
+                                                        self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                                                        self.params.data_ptr(), self.correct_dev.data_ptr(), ctas,
+                                                        es.cuda_stream))
                 self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
                 self._ev_result[slot].record(es)
             self._eval_done = self._ev_result[slot]

@@ -117,6 +117,28 @@ def test_fedavg_bit_exact(tr):
         assert np.array_equal(tr.fedavg(ds, ws, base), fm.weighted_average(ds, ws, base))
 
 
+def test_fedavg_short_vectors_pointer_rows(tr):
+    """The shared-memory tile kernel (short vectors): fp32 pointer-table rows as the round loop passes them,
+    16-byte aligned and misaligned, K above one staged tile, ragged tails; bit-exact vs torch fp64 in list order."""
+    import torch
+    from paper_2305_15668_b200 import _abi
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for n, k, shift in [(7850, 100, 0), (7850, 100, 1), (130, 300, 0), (1, 3, 0), (129, 129, 3)]:
+        ld = (n + 3) // 4 * 4 + 4
+        store = torch.randn(k, ld, device="cuda", generator=g, dtype=torch.float32)
+        rows = store[:, shift:shift + n]
+        table = torch.tensor([r.data_ptr() for r in rows], dtype=torch.int64, device="cuda")
+        coef = torch.rand(k, device="cuda", generator=g, dtype=torch.float64)
+        base = torch.randn(n, device="cuda", generator=g, dtype=torch.float64)
+        out = torch.empty_like(base)
+        _abi.check(_abi.lib.fedhc_fedavg(table.data_ptr(), None, 0, _abi.F32, coef.data_ptr(), k, base.data_ptr(),
+                                         out.data_ptr(), n, torch.cuda.current_stream().cuda_stream))
+        ref = base.clone()
+        for i in range(k):
+            ref += coef[i].item() * rows[i].double()
+        assert torch.equal(out, ref), (n, k, shift)
+
+
 def test_fedavg_errors(tr):
     from paper_2305_15668_b200.errors import AggregationError
     for ds, ws in [([], []), ([np.zeros(2)], [1.0, 2.0]), ([np.zeros(3)], [1.0]), ([np.zeros(2)], [0.0]),
