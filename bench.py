@@ -359,10 +359,18 @@ def run_ours(args, rank, world, local_rank):
     runner = FederatedRunner(fed, by_id, cfg, LR, world=world, rank=rank, group=None)
     runner.run(args.warmup, n_test_total=N_TEST)
     barrier()
+    trace = os.environ.get("FEDHC_TRACE")  # optional: kernel timeline of the e2e rounds (torch.profiler / CUPTI)
+    if trace:
+        prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA,
+                                                  torch.profiler.ProfilerActivity.CPU])
+        prof.__enter__()
     e0 = time.perf_counter()
     series = runner.run(args.steps, n_test_total=N_TEST)
     barrier()
     e2e_s = time.perf_counter() - e0
+    if trace:
+        prof.__exit__(None, None, None)
+        prof.export_chrome_trace(trace)
     h2d, d2h = runner.h2d_bytes, runner.d2h_bytes
     host_ms = {k: round(v / (args.steps + args.warmup) * 1e3, 4) for k, v in runner.host_s.items()}
     if dist is not None:

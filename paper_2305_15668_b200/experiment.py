@@ -584,14 +584,18 @@ class FederatedRunner:
                     and gs[0] == self._graph_key(p))
 
     def launch_plan(self, p: RoundPlan) -> None:
-        if self._green is not None and not p.plan_launched and p.meta_bytes and p.participants:
-            # eager on the green-context stream (kernel confined to the spare SM groups)
+        if (self._green is not None or not self.use_graphs) and not p.plan_launched and p.meta_bytes \
+                and p.participants:
+            # eager, from the planner thread as soon as the round is planned: the batch order is generated
+            # while earlier rounds train, off the next train kernel's critical path (on the green-context
+            # stream, if any, the kernel is confined to the spare SM groups)
             k, slot, mb = len(p.participants), p.slot, p.meta_bytes
             tot = mb + k * CLIENT_DTYPE.itemsize + 8 * k
             ps = self._plan_stream
             dev = self._stage_dev[slot]
             md = dev.data_ptr()
             with torch.cuda.stream(ps):
+                ps.wait_event(self._ev_train[slot])  # the slot's previous train kernel is done with its buffers
                 dev[:tot].copy_(self._stage_pin[slot][:tot], non_blocking=True)
                 _abi.check(_abi.lib.fedhc_batch_permutations_device(md, md + 8 * k, md + 12 * k, md + 16 * k, k,
                                                                     self._dev_plan[slot].data_ptr(), self._rows_max,
