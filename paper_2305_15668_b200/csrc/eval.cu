@@ -95,7 +95,9 @@ extern "C" int fedhc_eval_ctas(const float* x, const int32_t* y, int64_t n, int 
   const int Fs = (n_features + 3) / 4 * 4;
   const size_t smem = ((size_t)n_classes * Fs + n_classes) * 4;
   if (smem > (size_t)max_smem) return fail(FEDHC_ERR_UNSUPPORTED, "eval: model too large for shared memory");
-  static int smem_set = 0;  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs)
+  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs); per device
+  static int smem_set_of[64] = {0};
+  int& smem_set = smem_set_of[dev & 63];
   if ((int)smem > smem_set) {
     FEDHC_CUDA_TRY(cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));

@@ -842,8 +842,11 @@ bool launch_train_fused(const fedhc_client* clients, int n_clients, const double
   static const bool v3_only = getenv("FEDHC_TRAIN_V3") != nullptr;
   PipeGeom pg{};
   if (!v3_only && plan_pipe(F, C, max_smem, pg)) {
-    static int smem_set = 0;  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs)
-    cudaError_t e = cudaSuccess;
+    // raise the opt-in only when needed (keeps launches capturable into CUDA graphs); per device
+    static int smem_set_of[64] = {0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    int& smem_set = smem_set_of[dev & 63];
     if (pg.bytes > smem_set) {
       e = cudaFuncSetAttribute(train_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.bytes);
       if (e == cudaSuccess) smem_set = pg.bytes;
