@@ -178,6 +178,28 @@ def test_accuracy_vs_oracle(tr):
     assert tr.evaluate_accuracy(p, tr.Dataset(np.zeros((0, 784)), np.zeros(0, int), 62)) == 0.0
 
 
+def test_accuracy_cta_cap_invariant():
+    """fedhc_eval_ctas (the round loop's accuracy on the SMs training leaves idle) counts exactly what
+    fedhc_eval counts, for any CTA cap, on ragged row counts."""
+    import torch
+    from paper_2305_15668_b200 import _abi
+    g = torch.Generator(device="cuda").manual_seed(7)
+    for n, F, C in [(16000, 784, 10), (1001, 784, 62), (33, 60, 3)]:
+        x = torch.randn(n, F, device="cuda", generator=g)
+        y = torch.randint(0, C, (n,), device="cuda", generator=g, dtype=torch.int32)
+        p = torch.randn(F * C + C, device="cuda", generator=g, dtype=torch.float64) * 0.05
+        st = torch.cuda.current_stream().cuda_stream
+        ref = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _abi.check(_abi.lib.fedhc_eval(x.data_ptr(), y.data_ptr(), n, F, C, p.data_ptr(), ref.data_ptr(), st))
+        expect = int(((x.double() @ p[:F * C].view(F, C) + p[F * C:]).argmax(1) == y.long()).sum())
+        assert abs(int(ref.item()) - expect) <= max(2, n // 2000)  # fp32 vs fp64 near-ties only
+        for cap in (1, 8, 48, 0, 10_000):
+            got = torch.zeros(1, dtype=torch.int64, device="cuda")
+            _abi.check(_abi.lib.fedhc_eval_ctas(x.data_ptr(), y.data_ptr(), n, F, C, p.data_ptr(), got.data_ptr(),
+                                                cap, st))
+            assert int(got.item()) == int(ref.item()), (n, cap)
+
+
 def test_loss_and_grad_vs_oracle(tr):
     loss, grad = tr.loss_and_grad(FL["lg_p"], FL["lg_x"], FL["lg_y"], 4)
     assert loss == pytest.approx(float(FL["lg_loss"]), rel=1e-12)
