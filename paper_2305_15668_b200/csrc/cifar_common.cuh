@@ -205,16 +205,26 @@ static __global__ void __launch_bounds__(256) bn_partial_kernel(const __nv_bfloa
 // forward: stats [G][C] = (mean, rstd); running statistics updated (momentum 0.1, unbiased variance).
 // backward: gsum [G][C][2] = (dbeta = sum dz, dgamma = sum dz * xhat).   grid G, block C.
 template <bool BWD>
-static __global__ void bn_finalize_kernel(const float* __restrict__ part, const int32_t* __restrict__ valid, int HW, int C,
+static __global__ void __launch_bounds__(1024) bn_finalize_kernel(const float* __restrict__ part, const int32_t* __restrict__ valid, int HW, int C,
                                    float* __restrict__ out, float* __restrict__ master, int64_t pstride,
                                    int64_t rm_off, int64_t rv_off, int nsplit = BN_SPLIT) {
   const int g = blockIdx.x;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    // 16 split partials in flight at once (a dependent load per split made this launch latency-bound),
+    // summed in split order (deterministic, independent of the launch shape)
     double s0 = 0.0, s1 = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) {
-      const float* p = part + (((int64_t)g * nsplit + sp) * C + c) * 2;
-      s0 += p[0];
-      s1 += p[1];
+    for (int sp0 = 0; sp0 < nsplit; sp0 += 16) {
+      float2 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (sp0 + u < nsplit)
+          v[u] = *reinterpret_cast<const float2*>(part + (((int64_t)g * nsplit + sp0 + u) * C + c) * 2);
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (sp0 + u < nsplit) {
+          s0 += v[u].x;
+          s1 += v[u].y;
+        }
     }
     float* o = out + ((int64_t)g * C + c) * 2;
     if (BWD) {
