@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--cnn-samples", type=int, default=6400, help="samples per client for --workload cnn")
     ap.add_argument("--resnet-clients", type=int, default=25, help="ResNet-18 clients per GPU (config 3: 200 / 8)")
     ap.add_argument("--resnet-samples", type=int, default=250, help="samples per ResNet-18 client")
+    ap.add_argument("--strong", action="store_true",
+                    help="resnet/mobilenet/shufflenet: fixed total participants per round (config 3: --resnet-total "
+                         "200 over --gpus N, LPT-sharded) instead of a fixed count per GPU")
+    ap.add_argument("--resnet-total", type=int, default=200, help="participants per round with --strong (config 3)")
     ap.add_argument("--mobilenet-clients", type=int, default=100, help="MobileNetV2 participants per GPU per round")
     ap.add_argument("--mobilenet-fleet", type=int, default=1000, help="MobileNetV2 fleet size (config 4: >= 1000)")
     ap.add_argument("--mobilenet-max-samples", type=int, default=1024,
@@ -238,7 +242,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- device-resident synthetic non-IID data (same seed on every rank) ----
     from paper_2305_15668_b200.devicedata import DeviceFleetData
-    from paper_2305_15668_b200.sharding import shard_bounds
+    from paper_2305_15668_b200.sharding import client_cost, lpt_shards, shard_bounds
     fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=N_SAMPLES, batch_size=BATCH),
                               n_fleet, 1)
     by_id = {p.client_id: p for p in fleet}
@@ -261,7 +265,8 @@ def run_ours(args, rank, world, local_rank):
     def plan_round(r, selector, now):
         who = selector.sample(ids, n_part)
         rep, _ = sim.run(who, cfg, t0=now, round_index=r, want_trace=False)
-        mine = who[rank * PER_GPU:(rank + 1) * PER_GPU]
+        mine = [who[j] for j in lpt_shards([client_cost(by_id[c].workload.num_samples, BATCH) for c in who],
+                                           world)[rank]]
         wl = [by_id[c].workload for c in mine]
         seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
         total = float(sum(float(w.num_samples) for w in (by_id[c].workload for c in who)))
@@ -356,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
     # pinned memory), copies the plan H2D, launches train/FedAvg/(all-reduce)/eval and reads the
     # accuracy count back (D2H); planning of round r+1 overlaps the GPU work of round r.
     from paper_2305_15668_b200.experiment import FederatedRunner
-    runner = FederatedRunner(fed, by_id, cfg, LR, world=world, rank=rank, group=None)
+    runner = FederatedRunner(fed, by_id, cfg, LR, world=world, rank=rank, group=None, test_sharded=True)
     runner.run(args.warmup, n_test_total=N_TEST)
     barrier()
     trace = os.environ.get("FEDHC_TRACE")  # optional: kernel timeline of the e2e rounds (torch.profiler / CUPTI)
@@ -628,7 +633,7 @@ def run_cnn(args, rank, world, local_rank):
     from paper_2305_15668_b200.devicedata import DeviceFleetData
     from paper_2305_15668_b200.experiment import delta_buffer
     from paper_2305_15668_b200.roundsim import RoundSimulator
-    from paper_2305_15668_b200.sharding import shard_bounds
+    from paper_2305_15668_b200.sharding import client_cost, lpt_shards, shard_bounds
     from paper_2305_15668_b200.training import fedavg_device, stable_seed
 
     torch.cuda.set_device(local_rank)
@@ -664,7 +669,8 @@ def run_cnn(args, rank, world, local_rank):
     def plan_round(r, now):
         who = selector.sample(ids, n_part)
         rep, _ = sim.run(who, cfg, t0=now, round_index=r, want_trace=False)
-        mine = who[rank * per_gpu:(rank + 1) * per_gpu]
+        mine = [who[j] for j in lpt_shards([client_cost(by_id[c].workload.num_samples, bs) for c in who],
+                                           world)[rank]]
         wl = [by_id[c].workload for c in mine]
         seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
         total = float(sum(float(by_id[c].workload.num_samples) for c in who))
@@ -970,10 +976,24 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         n_samp = args.resnet_samples
         per_gpu = args.resnet_clients
         n_part, n_fleet = per_gpu * world, (per_gpu + per_gpu // 4) * world
+    if args.strong:  # config 3: a fixed round (e.g. 200 participants) split over the ranks
+        n_part = args.resnet_total
+        n_fleet = max(n_fleet, n_part + n_part // 4) if not config4 else max(args.mobilenet_fleet, n_part)
     fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=bs),
                               n_fleet, 3)
     by_id = {p.client_id: p for p in fleet}
     ids = sorted(by_id)
+    from paper_2305_15668_b200.sharding import client_cost, lpt_shards
+    total_rounds = args.warmup + args.steps
+
+    def my_share(who):
+        """LPT shard of the round's selection for this rank (rows processed per client), selection order."""
+        costs = [client_cost(by_id[c].workload.num_samples, bs) for c in who]
+        return [who[j] for j in lpt_shards(costs, world)[rank]]
+
+    # engine capacity = the largest share this rank gets in any round (device-resident + e2e rounds)
+    _sel = random.Random("3:selection")
+    per_gpu = max(len(my_share(_sel.sample(ids, n_part))) for _ in range(2 * total_rounds + args.warmup))
     n_test = 2048
     data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 3072, nc, alpha=0.5, seed=4321,
                            n_test=n_test)
@@ -988,23 +1008,26 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
     cfg = fh.FleetConfig(theta=THETA, max_executors=EXECUTORS, participants_per_round=n_part, seed=3)
     sim = RoundSimulator(by_id)
     selector = random.Random(f"{cfg.seed}:selection")
-    total_rounds = args.warmup + args.steps
 
     def plan_round(r, now):
         who = selector.sample(ids, n_part)
         rep, _ = sim.run(who, cfg, t0=now, round_index=r, want_trace=False)
-        mine = who[rank * per_gpu:(rank + 1) * per_gpu]
+        mine = my_share(who)
         wl = [by_id[c].workload for c in mine]
         seeds = [stable_seed("train", cfg.seed, r, c) for c in mine]
-        tot = float(sum(w.num_samples for w in wl))  # this GPU's shard (equal shards: = global / world)
-        coef = torch.tensor([float(w.num_samples) / (tot * world) for w in wl], dtype=torch.float64, device=dev)
+        tot = float(sum(float(by_id[c].workload.num_samples) for c in who))  # W over the whole round
+        coef = torch.tensor([float(w.num_samples) / tot for w in wl], dtype=torch.float64, device=dev)
         return rep, mine, wl, seeds, coef
 
-    def aggregate(coef):
+    def aggregate(coef, k=None):
+        k = coef.shape[0] if k is None else k
         if world == 1:
-            fedavg_device(deltas, coef, params, params)
+            fedavg_device(deltas[:k], coef, params, params)
         else:
-            fedavg_device(deltas, coef, None, partial)
+            if k:
+                fedavg_device(deltas[:k], coef, None, partial)
+            else:
+                partial.zero_()
             dist.all_reduce(partial)
             fedavg_device(partial.view(1, -1), one, params, params)
 
@@ -1026,9 +1049,9 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         if config4:
-            fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True, steps=steps)
+            fed.engine.local_train(desc.data_ptr(), len(steps), params, steps[0], lr, True, steps=steps)
         else:
-            fed.engine.local_train(desc.data_ptr(), per_gpu, params, steps[0], lr, True)
+            fed.engine.local_train(desc.data_ptr(), len(steps), params, steps[0], lr, True)
         ev1.record()
         aggregate(coef)
         fed.engine.correct_into(params, fed.x_test, fed.y_test, counts[r:r + 1])
@@ -1082,7 +1105,7 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
         if world == 1:
             fed.aggregate(params, deltas, [float(w.num_samples) for w in wl])
         else:
-            aggregate(coef)
+            aggregate(coef, len(mine))
         fed.correct(params)
         return now + rep.makespan
 
@@ -1164,14 +1187,16 @@ def run_resnet(args, rank, world, local_rank, model="resnet"):
     res = {
         "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
         "value": value, "unit": "client-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic CIFAR-shaped 32x32x3 rows generated in HBM (Gaussian class clusters, "
                                  "Dirichlet(0.5) label mix); random-init " + mname,
         "config": {"workload": cfg_name, "arithmetic": arith,
                    "participants_per_round": n_part, "per_gpu": per_gpu, "fleet": n_fleet,
                    "samples_per_client": n_samp, "batch": bs, "local_steps_per_client": spc,
                    "budgets": "10..100 step 10", "theta": THETA, "scheduler": "resource-aware, dynamic parallelism",
-                   "parallelism": f"clients sharded over {world} GPU(s)",
+                   "parallelism": f"clients LPT-sharded over {world} GPU(s) ({per_gpu} max per GPU)"
+                                  + (", NCCL all-reduce of FedAvg partials" if world > 1 else ""),
                    "l2": "per-client weights + activations (GBs per round) exceed L2; no flush needed"},
         "rounds_per_sec": args.steps / (ms / 1e3), "train_ms": train_ms,
         "client_steps_per_round": total_steps / args.steps,
@@ -1238,15 +1263,31 @@ def run_reference(args, rank, world):
     }
 
 
+def _relaunch_under_torchrun(n: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     global C
     args = parse()
     C = args.classes
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: spawn one rank per GPU ourselves (same contract as the driver's
+        # `torch.distributed.run --nproc-per-node N ... bench.py --gpus N`), rank 0 prints the line
+        sys.exit(_relaunch_under_torchrun(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
-        pass  # torchrun decides the world; --gpus is informational
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or omit torchrun\n")
+        sys.exit(2)
     if args.impl == "reference":
         res = run_reference(args, rank, world)
     elif args.workload == "fedavg":

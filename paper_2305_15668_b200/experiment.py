@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from .errors import ConfigError
+from .errors import AggregationError, ConfigError
 from .roundsim import RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
 from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
@@ -364,7 +364,7 @@ class FederatedRunner:
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
                  plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = False,
-                 green_plan: bool = False):
+                 green_plan: bool = False, test_sharded: bool = False):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -374,10 +374,20 @@ class FederatedRunner:
         self.world, self.rank, self.group = world, rank, group
         self._shard_bounds = shard_bounds
         self.selector = random.Random(f"{cfg.seed}:selection")
+        # accuracy (fl_core.py:154-160): every rank counts a slice of the test rows, one int64 all-reduce.
+        # test_sharded=True: `fed` already holds only this rank's slice (run() then needs n_test_total);
+        # otherwise the runner takes its shard_bounds slice of the full test set itself.
+        self.test_sharded = bool(test_sharded)
+        if world > 1 and not test_sharded:
+            tlo, thi = shard_bounds(fed.n_test, world, rank)
+            self._xt, self._yt, self._nt = fed.x_test[tlo:thi], fed.y_test[tlo:thi], thi - tlo
+        else:
+            self._xt, self._yt, self._nt = fed.x_test, fed.y_test, fed.n_test
         dev = fed.x.device
         self.dev = dev
         self.params = params if params is not None else torch.zeros(fed.P, dtype=torch.float64, device=dev)
-        k_max = max(-(-cfg.participants_per_round // world), 1)
+        # LPT may give a rank more than ceil(n / world) light clients: size the buffers for the worst case
+        k_max = max(cfg.participants_per_round, 1)
         self.deltas = delta_buffer(k_max, fed.P, dev)
         self.partial = torch.empty(fed.P, dtype=torch.float64, device=dev)
         self.one = torch.ones(1, dtype=torch.float64, device=dev)
@@ -448,6 +458,9 @@ class FederatedRunner:
         ns = np.array([fleet[c].workload.num_samples for c in self.ids], np.int64)
         bs = np.array([fleet[c].workload.batch_size for c in self.ids], np.int64)
         self._c_w = ns.astype(np.float64)
+        from .sharding import client_cost, lpt_shards
+        self._lpt = lpt_shards
+        self._c_cost = np.array([client_cost(n, b, rws) for n, b, rws in zip(ns, bs, self._c_rows)], np.float64)
         self._c_bs = bs
         self._c_steps = -(-ns // bs)
         per_epoch = -(-self._c_rows // bs)
@@ -493,13 +506,23 @@ class FederatedRunner:
         else:
             rep = self.sim.run_lean(self._sim_idx[wi], who, cfg, t0=t0, round_index=r)
         t1 = time.perf_counter()
-        lo, hi = self._shard_bounds(len(who), self.world, self.rank)
-        mine = who[lo:hi]
-        mi = np.asarray(who_idx[lo:hi], np.int64)
+        if self.world > 1:   # LPT over the GPU cost (rows processed) of each participant
+            sel = self._lpt(self._c_cost[wi].tolist(), self.world)[self.rank]
+        else:
+            sel = list(range(len(who)))
+        mine = [who[j] for j in sel]
+        mi = wi[sel] if sel else np.zeros(0, np.int64)
         k = len(mine)
         weights_all = self._c_w[np.asarray(who_idx, np.int64)].tolist()
         total = float(sum(weights_all))                      # CPython float sum, as the reference
-        coef = np.asarray(weights_all[lo:hi], np.float64) / total
+        # fl_core.fedavg's validation (fl_core.py:201-212), raised before any device work: the reference
+        # raises it at the round's FedAvg (engine.py:351), after a round that trains nothing useful
+        if not who:
+            raise AggregationError("no deltas to aggregate")
+        if total == 0:
+            raise AggregationError("weights must not all be zero")
+        my_w = [weights_all[j] for j in sel]
+        coef = np.asarray(my_w, np.float64) / total
         reprs = self._repr_ptr[mi] if k else self._repr_ptr[:1]   # const char* per participant
         train_seeds = np.zeros(max(k, 1), np.uint64)
         rng_seeds = np.zeros(max(k, 1), np.uint64)
@@ -545,7 +568,7 @@ class FederatedRunner:
         hs["seeds"] += t2 - t1
         hs["permutations"] += t3 - t2
         hs["descriptors"] += t4 - t3
-        return RoundPlan(r, mine, who, rep, t0, weights_all[lo:hi], coef, slot, at, desc, meta_bytes,
+        return RoundPlan(r, mine, who, rep, t0, my_w, coef, slot, at, desc, meta_bytes,
                          int(rows.max()) if k else 0)
 
     # ---- device side -------------------------------------------------------
@@ -571,9 +594,9 @@ class FederatedRunner:
                                                   self.fed.n_classes, self._bs_max, stream_ptr()))
             fedavg_device(self.deltas[:k], coef_t, self.params, self.params)
             self.correct_dev.zero_()
-            if self.fed.n_test:
-                _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
-                                               self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+            if self._nt:
+                _abi.check(_abi.lib.fedhc_eval(self._xt.data_ptr(), self._yt.data_ptr(),
+                                               self._nt, self.fed.n_features, self.fed.n_classes,
                                                self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
             self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
         self._graphs[slot] = (self._graph_key(p), gp, gr)
@@ -705,11 +728,11 @@ class FederatedRunner:
             es.wait_event(self._ev_agg[slot])
             with torch.cuda.stream(es):
                 self.correct_dev.zero_()
-                if self.fed.n_test:
+                if self._nt:
                     # overlaps the next round's training (one CTA per client): stay on the idle SMs
                     ctas = max(8, self._sms - k)
-                    _abi.check(_abi.lib.fedhc_eval_ctas(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
-                                                        self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+                    _abi.check(_abi.lib.fedhc_eval_ctas(self._xt.data_ptr(), self._yt.data_ptr(),
+                                                        self._nt, self.fed.n_features, self.fed.n_classes,
                                                         self.params.data_ptr(), self.correct_dev.data_ptr(), ctas,
                                                         es.cuda_stream))
                 self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
@@ -717,9 +740,9 @@ class FederatedRunner:
             self._eval_done = self._ev_result[slot]
         else:
             self.correct_dev.zero_()
-            if self.fed.n_test:
-                _abi.check(_abi.lib.fedhc_eval(self.fed.x_test.data_ptr(), self.fed.y_test.data_ptr(),
-                                               self.fed.n_test, self.fed.n_features, self.fed.n_classes,
+            if self._nt:
+                _abi.check(_abi.lib.fedhc_eval(self._xt.data_ptr(), self._yt.data_ptr(),
+                                               self._nt, self.fed.n_features, self.fed.n_classes,
                                                self.params.data_ptr(), self.correct_dev.data_ptr(), stream_ptr()))
             all_reduce_count(self.correct_dev, self.group)
             self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
@@ -738,7 +761,11 @@ class FederatedRunner:
         import queue
         import threading
 
-        n_test = n_test_total if n_test_total is not None else self.fed.n_test
+        if n_test_total is None:
+            if self.test_sharded and self.world > 1:
+                raise ValueError("FederatedRunner(test_sharded=True) needs n_test_total (the global test-set size)")
+            n_test_total = self.fed.n_test
+        n_test = n_test_total
         if rounds <= 0:
             return []
         ready: queue.Queue = queue.Queue(maxsize=self.SLOTS - 1)

@@ -1,8 +1,9 @@
 """Client sharding across GPUs (one process per GPU) and the FedAvg exchange.
 
 A round's participants are independent given the round-start model
-(engine.py:336-347), so they shard over ranks with no data-path traffic; the
-one exchange step is the sum in FedAvg (fl_core.py:215-217):
+(engine.py:336-347), so they shard over ranks with no data-path traffic
+(longest-processing-time on each client's row count, `lpt_shards`); the one
+exchange step is the sum in FedAvg (fl_core.py:215-217):
 
     S_r = sum_{i in shard r} (w_i / W) * delta_i        (fp64, fedavg_kernel, base = NULL)
     S   = all_reduce_sum(S_r)                           (NCCL over NVLink/NVSwitch)
@@ -24,6 +25,38 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)
     return lo, lo + base + (1 if rank < extra else 0)
+
+
+def lpt_shards(costs, world: int) -> list[list[int]]:
+    """Longest-processing-time assignment of items to `world` ranks.
+
+    Items in decreasing cost (ties: lower index first) go to the currently least-loaded rank (ties: lower
+    rank).  Deterministic, so every rank computes the same assignment from the replicated selection.
+    Each rank's list is returned in increasing item index (= selection order), so a rank trains and sums
+    its clients in the reference's list order.
+    """
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    import heapq
+
+    order = sorted(range(len(costs)), key=lambda i: (-float(costs[i]), i))
+    heap = [(0.0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + float(costs[i]), r))
+    for lst in out:
+        lst.sort()
+    return out
+
+
+def client_cost(num_samples: int, batch_size: int, n_rows: int | None = None) -> float:
+    """GPU cost of one client's local_train: rows it processes (fl_core.py:180-189: ceil(n/B) batches
+    of B rows; a shard smaller than its workload reshuffles, so the row count is the workload's)."""
+    if n_rows == 0 or num_samples <= 0:
+        return 0.0
+    return float(-(-int(num_samples) // int(batch_size)) * int(batch_size))
 
 
 def shard_participants(participants: list[str], world: int, rank: int) -> list[str]:

@@ -14,6 +14,11 @@ The reference is imported read-only from /root/reference/pkg/src.  Outputs:
 * round_c10.npz / round_c62.npz -- one FL round at FEMNIST shape
                          (F=784, C=10 / 62, 10 clients x 6400 samples, B=64):
                          participants, final params, accuracy, two deltas.
+* headline_rounds.npz -- bench.py's round shape (128-client fleet, budgets
+                         10..100, 100 participants, F=784, C=10) at 640
+                         samples/client: params after each of 10 rounds
+                         (lr 0.1; headline_rounds_lr1e-3.npz: lr 1e-3).
+* a8.npz              -- acceptance criterion A8's 30 convergence runs.
 
 These fixtures pin the oracle (tests/test_oracle_golden.py) and the product
 (tests/test_gpu_parity.py, tests/test_host_parity.py).
@@ -273,6 +278,75 @@ def gen_round(engine, profiles, fl_core, classes):
     )
 
 
+HEADLINE = dict(n=128, seed=1, budgets=tuple(range(10, 101, 10)), num_samples=640, batch=64, participants=100,
+                theta=100.0, max_executors=18, rounds=10, features=784, classes=10, lr=0.1)
+
+
+def gen_headline(engine, profiles, fl_core, lr=None, name="headline_rounds.npz"):
+    """bench.py's round shape (128-client fleet, budgets 10..100, 100 participants/round, theta 100, 18
+    executors, F=784, C=10) at 640 samples per client, 10 rounds.  The params after EVERY round are
+    captured from the reference's own evaluate_accuracy call (engine.py:352 passes the new params).
+
+    At bench.py's lr = 0.1 the reference's fp64 softmax saturates to an exact one-hot after round 1 (the
+    784-feature Gaussian classes are far apart), so every later delta is exactly 0 and the params stop
+    moving; lr = 1e-3 (headline_rounds_lr1e-3.npz) keeps the gradients alive for all 10 rounds."""
+    h = dict(HEADLINE)
+    if lr is not None:
+        h["lr"] = lr
+    fleet = profiles.generate_fleet(profiles.DistributionSpec(budget_levels=h["budgets"], num_samples=h["num_samples"],
+                                                              batch_size=h["batch"]), h["n"], h["seed"])
+    cfg = profiles.FleetConfig(participants_per_round=h["participants"], rounds=h["rounds"], seed=h["seed"],
+                               theta=h["theta"], max_executors=h["max_executors"])
+    snaps = []
+    orig = fl_core.evaluate_accuracy
+
+    def spy(params, dataset):
+        snaps.append(np.array(params, copy=True))
+        return orig(params, dataset)
+
+    fl_core.evaluate_accuracy = spy
+    try:
+        rep = engine.run_experiment(cfg, fleet, engine.DataParams(features=h["features"], classes=h["classes"],
+                                                                   alpha=0.5),
+                                    engine.TrainParams(enabled=True, lr=h["lr"]))
+    finally:
+        fl_core.evaluate_accuracy = orig
+    assert len(snaps) == h["rounds"]
+    np.savez_compressed(os.path.join(HERE, name), params=np.stack(snaps).astype(np.float64),
+                        acc=np.array(rep.accuracy_series), participants=np.array(rep.participants),
+                        makespans=np.array([r.makespan for r in rep.rounds]), meta=np.array(json.dumps(h)))
+
+
+def gen_a8(engine, profiles):
+    """The reference's acceptance criterion A8 (pkg/tests/test_acceptance.py:300-336): the accuracy series
+    of all 30 convergence runs (5 seeds x 3 comparisons x 2 arms)."""
+    from fedsim.profiles import ClientProfile, WorkloadSpec
+
+    def fleet_of(n, budgets, factor=1.0, samples=100):
+        return [ClientProfile(f"c{i:02d}", budgets[i % len(budgets)],
+                              WorkloadSpec(num_samples=samples, batch_size=50, extra_model_factor=factor))
+                for i in range(n)]
+
+    def run(fleet, k, rounds, seed):
+        cfg = profiles.FleetConfig(participants_per_round=k, rounds=rounds, seed=seed, max_executors=32)
+        return engine.run_experiment(cfg, fleet, engine.DataParams(features=8, classes=12, alpha=0.03),
+                                     engine.TrainParams(enabled=True, lr=0.05))
+
+    out = {}
+    for seed in range(5):
+        arms = {
+            "wide": run(fleet_of(40, [10]), 20, 6, seed), "narrow": run(fleet_of(40, [10]), 5, 12, seed),
+            "light": run(fleet_of(20, [50]), 10, 8, seed), "heavy": run(fleet_of(20, [50], factor=2.0), 10, 8, seed),
+            "uniform": run(fleet_of(20, [100]), 5, 8, seed),
+            "hetero": run(fleet_of(20, [10, 15, 30, 50, 80]), 5, 8, seed),
+        }
+        for name, rep in arms.items():
+            out[f"s{seed}_{name}_acc"] = np.array(rep.accuracy_series)
+            out[f"s{seed}_{name}_params"] = rep.final_params
+            out[f"s{seed}_{name}_total"] = np.array(rep.total_time)
+    np.savez_compressed(os.path.join(HERE, "a8.npz"), **out)
+
+
 def gen_outputs(engine, profiles):
     """Reference `simulate` writers (cli.py:38-87) on one untrained experiment."""
     from pathlib import Path
@@ -299,6 +373,9 @@ def main():
     gen_train_experiments(engine, profiles)
     for c in (10, 62):
         gen_round(engine, profiles, fl_core, c)
+    gen_headline(engine, profiles, fl_core)
+    gen_headline(engine, profiles, fl_core, lr=1e-3, name="headline_rounds_lr1e-3.npz")
+    gen_a8(engine, profiles)
     print("golden fixtures written to", HERE)
 
 

@@ -90,3 +90,34 @@ def test_two_rank_round_matches_single_process(tmp_path):
     want = fm.weighted_average(deltas, [float(by_id[c].workload.num_samples) for c in who], params)
     assert np.max(np.abs(got["params"] - want)) <= 1e-12 * np.max(np.abs(want))
     assert int(got["correct"][0]) == round(fm.accuracy(want, test) * len(test.labels))
+
+
+
+def test_lpt_shards_balance_heterogeneous_round():
+    """The LPT split of a config-4-like round (sample counts 16..1024) is within one client's cost of the
+    average load, where contiguous slices are not."""
+    import random
+    from paper_2305_15668_b200.sharding import client_cost, lpt_shards, shard_bounds
+    rng = random.Random(0)
+    costs = [client_cost(rng.choice([16, 32, 64, 128, 256, 512, 1024]), 32) for _ in range(200)]
+    for world in (2, 4, 8):
+        shards = lpt_shards(costs, world)
+        loads = [sum(costs[i] for i in s) for s in shards]
+        assert max(loads) - min(loads) <= max(costs)
+        contiguous = [sum(costs[slice(*shard_bounds(len(costs), world, r))]) for r in range(world)]
+        assert max(loads) <= max(contiguous)
+
+
+def test_lpt_shards_cover_exactly_once_and_keep_selection_order():
+    from paper_2305_15668_b200.sharding import lpt_shards
+    rng = np.random.default_rng(1)
+    for n in range(0, 30):
+        costs = rng.integers(0, 5, n).tolist()
+        for world in range(1, 6):
+            shards = lpt_shards(costs, world)
+            flat = sorted(i for s in shards for i in s)
+            assert flat == list(range(n))
+            assert all(s == sorted(s) for s in shards)
+            assert shards == lpt_shards(costs, world)   # deterministic on every rank
+    # uniform costs: equal counts
+    assert [len(s) for s in lpt_shards([64.0] * 200, 8)] == [25] * 8

@@ -252,3 +252,38 @@ def test_femnist_round_bit_exact(classes):
     assert out["participants"][0] == list(g["participants"])
     assert np.array_equal(out["final_params"], g["params"])
     assert np.array_equal(np.array(out["accuracy_series"]), g["acc"])
+
+
+@pytest.mark.parametrize("name", ["headline_rounds.npz", "headline_rounds_lr1e-3.npz"])
+def test_headline_rounds_bit_exact(name):
+    """bench.py's round shape at 640 samples/client: the oracle reproduces the reference's 10 rounds (final
+    params, accuracy series, participants, makespans) bit for bit."""
+    g = np.load(os.path.join(GOLDEN, name))
+    h = json.loads(str(g["meta"]))
+    f = oc.fleet(h["n"], h["seed"], budget_levels=tuple(h["budgets"]), num_samples=h["num_samples"],
+                 batch_size=h["batch"])
+    out = oc.experiment(oc.Config(participants_per_round=h["participants"], rounds=h["rounds"], seed=h["seed"],
+                                  theta=h["theta"], max_executors=h["max_executors"]), f, features=h["features"],
+                        classes=h["classes"], alpha=0.5, train=True, lr=h["lr"])
+    assert out["participants"] == [list(p) for p in g["participants"]]
+    assert [r["makespan"] for r in out["rounds"]] == g["makespans"].tolist()
+    assert np.array_equal(out["final_params"], g["params"][-1])
+    assert np.array_equal(np.array(out["accuracy_series"]), g["acc"])
+
+
+def test_a8_runs_bit_exact():
+    """Acceptance criterion A8's convergence runs (reference pkg/tests/test_acceptance.py:300-336)."""
+    g = np.load(os.path.join(GOLDEN, "a8.npz"))
+
+    def fleet_of(n, budgets, factor=1.0, samples=100):
+        return [oc.Client(f"c{i:02d}", budgets[i % len(budgets)],
+                          oc.Workload(num_samples=samples, batch_size=50, extra_model_factor=factor))
+                for i in range(n)]
+
+    for seed in (0, 3):
+        for name, fl, k, rounds in (("wide", fleet_of(40, [10]), 20, 6), ("heavy", fleet_of(20, [50], 2.0), 10, 8),
+                                    ("hetero", fleet_of(20, [10, 15, 30, 50, 80]), 5, 8)):
+            out = oc.experiment(oc.Config(participants_per_round=k, rounds=rounds, seed=seed, max_executors=32), fl,
+                                features=8, classes=12, alpha=0.03, train=True, lr=0.05)
+            assert np.array_equal(np.array(out["accuracy_series"]), g[f"s{seed}_{name}_acc"])
+            assert np.array_equal(out["final_params"], g[f"s{seed}_{name}_params"])
