@@ -52,8 +52,12 @@ int fedhc_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
  * bpe = ceil(n_rows / batch_size), e = s / bpe, j = s % bpe,
  * nb = min(batch_size, n_rows - j*batch_size)   (fl_core.py:180-189),
  * i.e. `perm` is the concatenation of the PCG64 permutations the reference
- * draws (one per started epoch).  Math: fp32 storage, 3xTF32 tensor-core
- * products (fp32-accurate), fp32 SGD state; delta = W_final - W_initial.
+ * draws (one per started epoch).  Math: fp32 storage and SGD state; every
+ * product on the bf16 tensor pipe as "bf16x3" (each fp32 operand split into
+ * bf16 hi + mid, hi*hi + hi*mid + mid*hi accumulated in fp32: ~2^-16 relative
+ * per product, within the north_star 1e-4 bar); delta = W_final - W_initial.
+ * Kernels: tcgen05 F-split clusters (F > 784, or C > 32), mma.sync (C <= 32,
+ * F <= 784), SIMT fallback (F % 4 != 0, C > 64, batch > 64).
  */
 typedef struct fedhc_client {
   const float* x;        /* dev [n_rows, n_features] fp32 row-major          */
@@ -71,6 +75,11 @@ typedef struct fedhc_client {
  * DEVICE array of descriptors.  `max_batch` = max batch_size over clients. */
 int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params,
                       int n_features, int n_classes, int max_batch, void* stream);
+
+/* Diagnostics: phase timestamps (%globaltimer ns, [8 CTAs][32 steps][24
+ * points]) of cluster 0 from the last tcgen05 local_train launch made with
+ * the environment variable FEDHC_TC_TRACE set; host `out`. */
+int fedhc_tc_trace_read(unsigned long long* out);
 
 /* ---- batch order: the PCG64 permutations local_train draws ------------- */
 /* Native, multi-threaded restatement of `np.random.default_rng(seed)` +

@@ -1,3 +1,6 @@
+#include <mutex>
+#include <set>
+#include <utility>
 // C-ABI plumbing: thread-local error message, version, device query.
 #include <string>
 
@@ -12,6 +15,23 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
+}
+
+cudaError_t smem_optin_max(const void* func) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0, max_smem = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({func, dev})) return cudaSuccess;
+  e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, func);  // static shared memory counts against the opt-in
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({func, dev});
+  return e;
 }
 
 int cuda_status(cudaError_t e, const char* what) {

@@ -14,6 +14,9 @@ namespace fedhc {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);
+// Opt `func` in to the device's maximum dynamic shared memory, once per (function, device); thread-safe
+// (launchers run on several host threads).  Launches with less shared memory are unaffected.
+cudaError_t smem_optin_max(const void* func);
 
 #define FEDHC_CUDA_TRY(expr)                                   \
   do {                                                         \

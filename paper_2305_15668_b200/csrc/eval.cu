@@ -16,18 +16,22 @@ namespace fedhc {
 constexpr int kEvalThreads = 512;
 constexpr int kEvalCT = 16;
 
+// GW = false: W^T staged in shared memory (every model the trainers' fast paths cover);
+// GW = true: models too large for shared memory read W (fp64, L2-resident) from global memory.
+template <bool GW>
 __global__ void __launch_bounds__(kEvalThreads, 1)
     eval_kernel(const float* __restrict__ x, const int32_t* __restrict__ y, int64_t n, int F, int C, int Fs,
                 const double* __restrict__ params, unsigned long long* correct) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* Wt = reinterpret_cast<float*>(smem);  // [C][Fs]
-  float* bias = Wt + (size_t)C * Fs;           // [C]
+  float* bias = GW ? Wt : Wt + (size_t)C * Fs;  // [C]
   __shared__ unsigned int s_count;
   if (threadIdx.x == 0) s_count = 0;
-  for (int i = threadIdx.x; i < C * Fs; i += kEvalThreads) {
-    const int c = i / Fs, f = i - c * Fs;
-    Wt[i] = f < F ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
-  }
+  if (!GW)
+    for (int i = threadIdx.x; i < C * Fs; i += kEvalThreads) {
+      const int c = i / Fs, f = i - c * Fs;
+      Wt[i] = f < F ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
+    }
   for (int c = threadIdx.x; c < C; c += kEvalThreads) bias[c] = static_cast<float>(params[(size_t)F * C + c]);
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -42,7 +46,14 @@ __global__ void __launch_bounds__(kEvalThreads, 1)
       float acc[kEvalCT];
 #pragma unroll
       for (int u = 0; u < kEvalCT; ++u) acc[u] = 0.f;
-      if (vec) {
+      if (GW) {
+        for (int f = lane; f < F; f += 32) {
+          const float xv = __ldg(xr + f);
+#pragma unroll
+          for (int u = 0; u < kEvalCT; ++u)
+            if (c0 + u < C) acc[u] = fmaf(xv, static_cast<float>(__ldg(params + (size_t)f * C + c0 + u)), acc[u]);
+        }
+      } else if (vec) {
         for (int f = 4 * lane; f < F; f += 128) {
           const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + f));
 #pragma unroll
@@ -93,20 +104,20 @@ extern "C" int fedhc_eval_ctas(const float* x, const int32_t* y, int64_t n, int 
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int Fs = (n_features + 3) / 4 * 4;
-  const size_t smem = ((size_t)n_classes * Fs + n_classes) * 4;
-  if (smem > (size_t)max_smem) return fail(FEDHC_ERR_UNSUPPORTED, "eval: model too large for shared memory");
-  // raise the opt-in only when needed (keeps launches capturable into CUDA graphs); per device
-  static int smem_set_of[64] = {0};
-  int& smem_set = smem_set_of[dev & 63];
-  if ((int)smem > smem_set) {
-    FEDHC_CUDA_TRY(cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-    smem_set = (int)smem;
-  }
+  size_t smem = ((size_t)n_classes * Fs + n_classes) * 4;
+  const bool gw = smem > (size_t)max_smem;
+  if (gw) smem = (size_t)n_classes * 4;
+  if (smem > (size_t)max_smem) return fail(FEDHC_ERR_UNSUPPORTED, "eval: too many classes");
   const int64_t need = (n + (kEvalThreads / 32) - 1) / (kEvalThreads / 32);
   const int cap = max_ctas > 0 ? std::min(max_ctas, sms) : sms;
   const int blocks = static_cast<int>(std::min<int64_t>(need, (int64_t)cap));
-  eval_kernel<<<blocks, kEvalThreads, smem, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);
+  if (gw) {
+    if (smem > 48 * 1024) FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(eval_kernel<true>)));
+    eval_kernel<true><<<blocks, kEvalThreads, smem, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);
+  } else {
+    if (smem > 48 * 1024) FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(eval_kernel<false>)));
+    eval_kernel<false><<<blocks, kEvalThreads, smem, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);
+  }
   FEDHC_CUDA_TRY(cudaGetLastError());
   return FEDHC_OK;
 }

@@ -218,19 +218,11 @@ extern "C" int fedhc_fedavg(const void* const* deltas, const void* packed, int64
     return fail(FEDHC_ERR_VALUE, "fedavg: dtype must be FEDHC_F32 or FEDHC_F64");
   int dev = 0;
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
-  static int sms_of[64] = {0};       // per device: SM count, 0 = not queried yet
-  static bool attr_of[64] = {false};  // per device: the tile kernel's shared-memory opt-in is set
-  const int di = dev & 63;
-  if (sms_of[di] == 0) FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[di], cudaDevAttrMultiProcessorCount, dev));
-  if (blocks < sms_of[di]) {  // short vector: latency-bound, stage every delta row through shared memory at once
-    bool& attr = attr_of[di];
-    if (!attr) {
-      FEDHC_CUDA_TRY(cudaFuncSetAttribute(fedavg_tile_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kTileBytes));
-      FEDHC_CUDA_TRY(cudaFuncSetAttribute(fedavg_tile_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kTileBytes));
-      attr = true;
-    }
+  int sms = 0;
+  FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (blocks < sms) {  // short vector: latency-bound, stage every delta row through shared memory at once
+    FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(fedavg_tile_kernel<float>)));
+    FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(fedavg_tile_kernel<double>)));
     const unsigned tb = static_cast<unsigned>((n + kTileE - 1) / kTileE);
     if (dtype == FEDHC_F32)
       fedavg_tile_kernel<float><<<tb, kTileE, kTileBytes, st>>>(

@@ -148,13 +148,8 @@ extern "C" int fedhc_batch_permutations_device(const uint64_t* seeds, const int3
   // the kernel also holds 8 KB of draws in static shared memory; larger shards permute in global memory
   const int smem_rows = max_rows * 4 + (int)sizeof(uint32_t) * kDrawChunk + 256 <= max_smem ? max_rows : 0;
   const int smem = smem_rows * 4;
-  // raise the opt-in only when needed (keeps launches graph-capturable); per device
-  static int smem_set_of[64] = {0};
-  int& smem_set = smem_set_of[dev & 63];
-  if (smem > 48 * 1024 && smem > smem_set) {
-    FEDHC_CUDA_TRY(cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    smem_set = smem;
-  }
+  // shared-memory opt-in: once per device, to the maximum (thread-safe: the runner launches from two threads)
+  if (smem > 48 * 1024) FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(perm_kernel)));
   static const PcgJump jump = [] {
     using fedhc_pcg::u128;
     const u128 m = FEDHC_PCG_MULT;

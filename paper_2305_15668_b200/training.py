@@ -4,7 +4,7 @@ Host side (setup, bit-identical to the reference for the same seed):
   stable_seed, Dataset/DatasetShard, make_synthetic_dataset, partition_noniid,
   init_params, batch_permutations (the PCG64 batch order of local_train).
 Device side (libfedhc kernels, no CPU fallback):
-  local_train  -> fedhc_local_train   (fused 3xTF32 SGD, fp32 state)
+  local_train  -> fedhc_local_train   (fused SGD, bf16x3 tensor-core products, fp32 state)
   fedavg       -> fedhc_fedavg        (fp64, bit-identical for fp64 deltas)
   evaluate_accuracy -> fedhc_eval
   loss_and_grad -> fedhc_loss_and_grad (fp64)

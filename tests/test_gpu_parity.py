@@ -2,7 +2,7 @@
 reference goldens.
 
 Tolerances (north_star): aggregated weights max-abs <= 1e-4 x max|ref|
-after a round (fp32 storage, 3xTF32 products; observed ~1e-6); FedAvg and
+after a round (fp32 storage, bf16x3 products; observed ~1e-6); FedAvg and
 loss_and_grad are fp64 (FedAvg bit-exact for fp64 deltas); accuracy within
 2 test rows of the oracle (argmax near-ties can flip under fp32 logits).
 """
@@ -73,6 +73,11 @@ def test_local_train_golden_cases(tr, i):
     (64, 10, 200, 300, 50),      # small F, B not a multiple of 16
     (20, 7, 90, 90, 1),          # batch of one row
     (6, 4, 33, 66, 16),          # F % 4 != 0 -> generic path
+    (3072, 10, 200, 640, 64),    # CIFAR-shaped reference model: tcgen05 trainer, 8-CTA clusters
+    (1000, 40, 150, 300, 32),    # tcgen05 trainer, odd chunk count per CTA, ragged + reshuffle
+    (784, 64, 128, 256, 64),     # tcgen05 trainer at the full 64-class tile
+    (2, 10, 6400, 6400, 6400),   # the reference's default F = 2, one 6400-row batch: generic, row-tiled
+    (16, 100, 300, 300, 64),     # more than 64 classes: generic
 ])
 def test_local_train_vs_oracle(tr, F, C, n, ns, b):
     from paper_2305_15668_b200.spec import WorkloadSpec
@@ -176,6 +181,11 @@ def test_accuracy_vs_oracle(tr):
     got = tr.evaluate_accuracy(p, tr.Dataset(tst.features, tst.labels, 62))
     assert abs(got - fm.accuracy(p, tst)) <= 2 / len(tst.labels)
     assert tr.evaluate_accuracy(p, tr.Dataset(np.zeros((0, 784)), np.zeros(0, int), 62)) == 0.0
+    # a model too large for shared memory (3072 x 100 fp32 = 1.2 MB): W read from global memory
+    trn, tst = fm.synthetic(3072, 100, 3000, seed=4)
+    p = np.random.default_rng(1).standard_normal(3072 * 100 + 100) * 0.01
+    got = tr.evaluate_accuracy(p, tr.Dataset(tst.features, tst.labels, 100))
+    assert abs(got - fm.accuracy(p, tst)) <= 2 / len(tst.labels)
 
 
 def test_accuracy_cta_cap_invariant():
