@@ -114,6 +114,7 @@ SIGNATURES = {
     "fedhc_version": (_i, []),
     "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
+    "fedhc_tc_trace_read": (_i, [_vp]),
     "fedhc_loss_and_grad": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "fedhc_fedavg_coefficients": (_i, [_dp, _i, _dp]),
     "fedhc_fedavg": (_i, [_vp, _vp, _i64, _i, _vp, _i, _vp, _vp, _i64, _vp]),

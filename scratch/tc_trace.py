@@ -18,7 +18,7 @@ for _ in range(2):
     fed.train(params, list(offs), wl, 0.1, list(range(K)))
 torch.cuda.synchronize()
 buf = np.zeros(8 * 32 * 24, dtype=np.uint64)
-_abi.lib.fedhc_tc_trace_read.argtypes = [ctypes.c_void_p]
+
 assert _abi.lib.fedhc_tc_trace_read(buf.ctypes.data) == 0
 t = buf.reshape(8, 32, 24).astype(np.int64)
 names = ["mma_fwd", "-", "q_zfull", "q_zx_arr", "own_soft", "q_e_rdy", "q_e_full", "mma_bwd", "q_gfull", "q_w_rdy",
