@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sublines", action="store_true", help="skip the c62 / f3072 sub-objects of the round line")
     ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "shufflenet", "fedavg", "gemm", "des"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
@@ -417,6 +418,11 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks.summary(),
         "gpu_launches": launches_per_round * args.steps,
     }
+    if C == 10 and not args.no_sublines:
+        # the other reference-model shapes the round is quoted on: FEMNIST's 62 classes (tcgen05 trainer,
+        # 4-CTA clusters) and the CIFAR-shaped F = 3072 model (tcgen05 trainer, 8-CTA clusters)
+        result["c62"] = kernel_subline(62, 784, PER_GPU, N_SAMPLES, 5, 2)
+        result["f3072"] = kernel_subline(10, 3072, PER_GPU, 640, 5, 2)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, _ = cpu_reference(args.cpu_seconds, warmup=1)
         result["cpu_baseline"] = {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port",
@@ -424,6 +430,68 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.destroy_process_group()
     return result
+
+
+def kernel_subline(C_, F_, n_clients, n_samp, rounds, warm, fleet_seed=1):
+    """Device-resident local-SGD rounds at another reference-model shape (same round structure, same
+    100-participant selection stream), for the driver-visible sub-objects of the default bench line:
+    "c62" (FEMNIST's 62 classes) and "f3072" (the CIFAR-shaped reference model).
+    Times fedhc_local_train with CUDA events on its stream; HBM roofline by the same algorithmic bytes."""
+    import torch
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200 import _abi
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.experiment import delta_buffer
+    from paper_2305_15668_b200.training import fedavg_device, stable_seed, stream_ptr
+    from benchlib import roofline_entry
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=BATCH),
+                              FLEET_PER_GPU, fleet_seed)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], F_, C_, alpha=0.5, seed=1234,
+                           n_test=4096)
+    fed = data.federation()
+    P = F_ * C_ + C_
+    params = torch.zeros(P, dtype=torch.float64, device=dev)
+    deltas = delta_buffer(n_clients, P, dev)
+    selector = random.Random(f"{fleet_seed}:selection")
+    plans = []
+    for r in range(rounds + warm):
+        mine = selector.sample(ids, n_clients)
+        wl = [by_id[c].workload for c in mine]
+        packed, meta = fed.plan(mine, wl, [stable_seed("train", fleet_seed, r, c) for c in mine])
+        perm_dev = torch.from_numpy(packed).to(dev)
+        fed._perm_dev = perm_dev
+        plans.append((perm_dev, fed.descriptors(mine, meta, LR, deltas)))
+    coef = torch.full((n_clients,), 1.0 / n_clients, dtype=torch.float64, device=dev)
+    evs = []
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i, (_, desc) in enumerate(plans):
+        if i == warm:
+            torch.cuda.synchronize()
+            t0.record()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _abi.check(_abi.lib.fedhc_local_train(desc.data_ptr(), n_clients, params.data_ptr(), F_, C_, BATCH,
+                                              stream_ptr()))
+        b.record()
+        if i >= warm:
+            evs.append((a, b))
+        fedavg_device(deltas, coef, params, params)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / rounds
+    train_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    steps = n_clients * math.ceil(n_samp / BATCH)
+    bytes_launch = n_clients * math.ceil(n_samp / BATCH) * BATCH * (4 * F_ + 8) + n_clients * P * 12
+    kern = "train_tc_kernel" if (F_ > 784 or C_ > 32) else "train_pipe_kernel"
+    return {"workload": f"femnist-logreg F={F_}, C={C_}: {n_clients} clients x {n_samp} samples, B={BATCH}, "
+                        f"local SGD + FedAvg (device-resident rounds)",
+            "value": steps / (ms / 1e3), "unit": "client-steps/s", "ms_per_round": ms, "train_kernel_ms": train_ms,
+            "rounds": rounds, "roofline": roofline_entry(bytes_launch, train_ms, ROOT, kernel=kern)}
 
 
 def run_fedavg(args, rank, world, local_rank):
