@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sublines", action="store_true", help="skip the c62 / f3072 sub-objects of the round line")
-    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "shufflenet", "fedavg", "gemm", "des"], default="round",
+    ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "shufflenet", "fedavg", "gemm", "des",
+                                           "live"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
@@ -69,6 +70,7 @@ def parse():
     ap.add_argument("--mobilenet-fleet", type=int, default=1000, help="MobileNetV2 fleet size (config 4: >= 1000)")
     ap.add_argument("--mobilenet-max-samples", type=int, default=1024,
                     help="largest per-client sample count (config 4: uniform choice of 16, 32, ..., 1024)")
+    ap.add_argument("--live-samples", type=int, default=640, help="samples per client for --workload live")
     ap.add_argument("--classes", type=int, default=10, help="10 (digits) or 62 (FEMNIST classes, 4-CTA clusters)")
     args = ap.parse_args()
     if args.steps is None:
@@ -492,6 +494,83 @@ def kernel_subline(C_, F_, n_clients, n_samp, rounds, warm, fleet_seed=1):
                         f"local SGD + FedAvg (device-resident rounds)",
             "value": steps / (ms / 1e3), "unit": "client-steps/s", "ms_per_round": ms, "train_kernel_ms": train_ms,
             "rounds": rounds, "roofline": roofline_entry(bytes_launch, train_ms, ROOT, kernel=kern)}
+
+
+def run_live(args, rank, world, local_rank):
+    """--workload live: the paper's runtime -- every launch decided in real time by the
+    executor manager (executor_manager.py:81-238) on CUDA completion events, each client's FEMNIST CNN (config 2's
+    model) running on the green-context SM window its budget buys (k = round(b * G / 100) groups of 8 SMs).
+    value = client local-SGD steps per second of wall time (host-driven dispatch, so wall-clock, not events);
+    also reported: how the measured per-client GPU times track the DES's simulated per-client times (Pearson r of
+    measured vs simulated, and of measured vs 1 / budget), and the live vs simulated makespan."""
+    import torch
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200.cnn import CnnEngine, CnnFederation, init_cnn_params
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.live import GreenPartitions, LiveRound
+    from paper_2305_15668_b200.roundsim import RoundSimulator
+
+    if world > 1:
+        raise SystemExit("--workload live runs on one GPU (a round's partitions are one device's SMs)")
+    torch.cuda.set_device(local_rank)
+    nc, n_samp, bs, lr = 62, args.live_samples, 64, 0.01
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=bs),
+                              FLEET_PER_GPU, 1)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, nc, alpha=0.5, seed=1234,
+                           n_test=1024)
+    fed = CnnFederation.from_arrays(data.x, data.y, data.offsets, data.x_test, data.y_test, nc).attach_engine(1, bs)
+    cfg = fh.FleetConfig(theta=THETA, max_executors=EXECUTORS, participants_per_round=PER_GPU, seed=1)
+    parts = GreenPartitions(local_rank, 8)
+    engines = [CnnEngine(1, bs, nc) for _ in range(cfg.max_executors)]
+    live = LiveRound(fed, by_id, cfg, lr, parts, engines=engines)
+    sim = RoundSimulator(by_id)
+    params = torch.tensor(fed.layout.to_padded(init_cnn_params(nc, 1)), dtype=torch.float64, device="cuda")
+    selector = random.Random(f"{cfg.seed}:selection")
+    steps_per_client = math.ceil(n_samp / bs)
+    meas, simt, budg, spans = [], [], [], []
+    wall = 0.0
+    for r in range(args.warmup + args.steps):
+        who = selector.sample(ids, PER_GPU)
+        t0 = time.perf_counter()
+        deltas, rep, trace, measured = live.run(params, who, round_index=r)
+        live.aggregate(params, deltas, who)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if r < args.warmup:
+            continue
+        wall += dt
+        srep, _ = sim.run(who, cfg, t0=0.0, round_index=r, want_trace=False)
+        spans.append((rep.makespan, srep.makespan))
+        for c in who:
+            meas.append(measured[c])
+            simt.append(srep.per_client_end[c] - srep.per_client_start[c])
+            budg.append(float(by_id[c].resource_budget))
+    meas, simt, budg = np.array(meas), np.array(simt), np.array(budg)
+    r_sim = float(np.corrcoef(meas, simt)[0, 1])
+    r_inv = float(np.corrcoef(meas, 1.0 / budg)[0, 1])
+    by_b = {int(b): float(np.median(meas[budg == b]) * 1e3) for b in sorted(set(budg.tolist()))}
+    total_steps = args.steps * PER_GPU * steps_per_client
+    value = total_steps / wall
+    return {
+        "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",
+        "value": value, "unit": "client-steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic FEMNIST-shaped rows generated in HBM; random-init FEMNIST CNN",
+        "config": {"workload": f"live-femnist-cnn-c{nc}: live dispatch (executor manager on CUDA completion "
+                               f"events), clients on green-context SM windows sized by budget",
+                   "participants_per_round": PER_GPU, "fleet": FLEET_PER_GPU, "samples_per_client": n_samp,
+                   "batch": bs, "budgets": "10..100 step 10", "theta": THETA, "max_executors": EXECUTORS,
+                   "sm_groups": parts.n_groups, "sms_per_group": parts.sms_per_group,
+                   "timing": "wall clock per round (host-driven dispatch, round = live.run + FedAvg)"},
+        "budget_physics": {"pearson_measured_vs_des_client_time": r_sim,
+                           "pearson_measured_vs_inverse_budget": r_inv,
+                           "median_client_ms_by_budget": by_b,
+                           "makespan_live_s_vs_des_s": [float(np.mean([a for a, _ in spans])),
+                                                        float(np.mean([b for _, b in spans]))]},
+        "gpu_launches": args.steps * (PER_GPU * engines[0].launches_per_round(steps_per_client) + 1),
+    }
 
 
 def run_fedavg(args, rank, world, local_rank):
@@ -1370,6 +1449,8 @@ def main():
         res = run_resnet(args, rank, world, local_rank, model="shufflenet")
     elif args.workload == "gemm":
         res = run_gemm(args, rank, world, local_rank)
+    elif args.workload == "live":
+        res = run_live(args, rank, world, local_rank)
     elif args.workload == "des":
         res = run_des(args) if rank == 0 else None
     else:

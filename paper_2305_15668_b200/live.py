@@ -92,11 +92,20 @@ class GreenPartitions:
 
 
 class LiveRound:
-    """One FL round dispatched in real time onto green-context partitions."""
+    """One FL round dispatched in real time onto green-context partitions.
+
+    `engines`: optional per-executor-slot client-model engines (e.g. one `CnnEngine(1, batch, C)` per slot,
+    `fed` the matching federation): a launched client then runs that engine's local SGD on its window's stream,
+    so a multi-CTA model really runs on (and is sped up or slowed down by) the SM share its budget buys.
+    Without engines the client is the reference's logistic model (`fedhc_local_train`, one CTA / cluster).
+    """
 
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
-                 partitions: GreenPartitions):
+                 partitions: GreenPartitions, engines: list | None = None):
         self.fed, self.fleet, self.cfg, self.lr, self.parts = fed, fleet, cfg, float(lr), partitions
+        if engines is not None and len(engines) < cfg.max_executors:
+            raise ValueError("need one client engine per executor slot")
+        self.engines = engines
 
     def run(self, params: torch.Tensor, participants: list[str], round_index: int = 0, poll_s: float = 2e-5):
         cfg, fed = self.cfg, self.fed
@@ -140,9 +149,14 @@ class LiveRound:
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(ext)
                 i = index[cid]
-                _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr() + i * CLIENT_DTYPE.itemsize, 1,
-                                                      params.data_ptr(), fed.n_features, fed.n_classes,
-                                                      wls[i].batch_size, s))
+                if self.engines is not None:
+                    self.engines[entry.executor_id].local_train(d_desc.data_ptr() + i * CLIENT_DTYPE.itemsize, 1,
+                                                                params, meta[i][2], self.lr, use_graph=False,
+                                                                stream=s)
+                else:
+                    _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr() + i * CLIENT_DTYPE.itemsize, 1,
+                                                          params.data_ptr(), fed.n_features, fed.n_classes,
+                                                          wls[i].batch_size, s))
                 ev1.record(ext)
                 running[cid] = (ev0, ev1, entry.executor_id)
                 trace.append({"t": clock(), "kind": "ClientLaunched", "client": cid, "executor": entry.executor_id,

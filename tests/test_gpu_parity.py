@@ -333,8 +333,33 @@ def test_green_partitions_confine_kernels(fh):
     assert not (a & b), (a, b)  # disjoint windows -> disjoint SMs
 
 
-def test_live_round_matches_batched(fh, tr):
-    """Real-time dispatch on green-context partitions: same deltas as the batched launch."""
+def _replay_live_on_oracle(trace, by_id, cfg, participants):
+    """Feed the live round's real-time event order to the ORACLE executor manager (oracle/orchestration.Manager,
+    executor_manager.py:81-238) and check that every launch the live round made is the oracle's decision."""
+    m = oc.Manager(cfg.max_executors, cfg.scheduler_kind, cfg.theta, cfg.dynamic_parallelism)
+    m.begin_round([(c, float(by_id[c].resource_budget)) for c in participants])
+    launches = [(e["client"], e["executor"]) for e in trace if e["kind"] == "ClientLaunched"]
+    expected = []
+
+    def take(decisions):
+        for (cid, _b, ex), _instr in decisions:
+            expected.append((cid, ex))
+            m.request(cid, "register", 0.0)
+
+    take(m.kickoff(0.0))
+    for e in trace:
+        if e["kind"] == "SlotFreed":
+            m.request(e["client"], "training_complete", 0.0)
+            m.request(e["client"], "model_uploaded", 0.0)
+            take(m.slot_freed(e["executor"], 0.0))
+    assert launches == expected
+    return launches
+
+
+def test_live_round_vs_oracle(fh, tr):
+    """Real-time dispatch on green-context partitions (comms.py:94-457 semantics): every launch decision equals
+    the oracle executor manager's under the same completion order, the deltas equal the batched launch's bit for
+    bit, and the aggregated params match the oracle's fp64 round (local_sgd + FedAvg) within the bar."""
     import torch
     from paper_2305_15668_b200.experiment import DeviceFederation
     from paper_2305_15668_b200.live import GreenPartitions, LiveRound
@@ -359,14 +384,44 @@ def test_live_round_matches_batched(fh, tr):
     assert torch.equal(d_live, d_batch)
     assert set(measured) == set(who) and all(v > 0 for v in measured.values())
     assert rep.makespan > 0 and len(rep.per_client_end) == len(who)
-    # first dispatch wave follows the resource-aware scheduler's kickoff
-    launched = [e["client"] for e in trace if e["kind"] == "ClientLaunched"]
-    mgr = fh.planner.ExecutorManager(6, "resource-aware", 100.0) if hasattr(fh, "planner") else None
-    from paper_2305_15668_b200 import planner
-    m = planner.ExecutorManager(6, "resource-aware", 100.0)
-    m.begin_round([planner.Participant(c, float(by_id[c].resource_budget)) for c in who])
-    first = [e.client_id for e, _ in m.kickoff(0.0)]
-    assert launched[:len(first)] == first
+    assert sorted(c for c, _ in _replay_live_on_oracle(trace, by_id, cfg, who)) == who
+    live.aggregate(params, d_live, who)
+    deltas = [fm.local_sgd(np.zeros(F * C + C), fm.Shard(c, shards[c].features, shards[c].labels),
+                           by_id[c].workload.num_samples, 64, 0.1, C, seed=seeds[i]) for i, c in enumerate(who)]
+    want = fm.weighted_average(deltas, [float(by_id[c].workload.num_samples) for c in who], np.zeros(F * C + C))
+    assert rel_err(params.cpu().numpy(), want) <= REL
+
+
+def test_live_cnn_round_budgets_are_physical(fh, tr):
+    """FEMNIST-CNN clients (config 2's model) in the live mode: each client runs its own engine on the SM window
+    its budget buys.  Deltas equal the batched engine's; launches follow the oracle manager; a 10 %-budget client
+    (1 SM group) takes longer than a 80 %-budget client (several groups) for the same work."""
+    import torch
+    from paper_2305_15668_b200.cnn import CnnEngine, CnnFederation, init_cnn_params
+    from paper_2305_15668_b200.live import GreenPartitions, LiveRound
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 80), num_samples=128, batch_size=64), 6, 5)
+    by_id = {p.client_id: p for p in fleet}
+    trn, tst = fm.synthetic(784, 10, 2000, seed=3)
+    shards, at = {}, 0
+    for p in fleet:
+        shards[p.client_id] = tr.DatasetShard(p.client_id, trn.features[at:at + 128], trn.labels[at:at + 128])
+        at += 128
+    fed = CnnFederation(shards, tr.Dataset(tst.features, tst.labels, 10), 784, 10).attach_engine(6, 64)
+    cfg = fh.FleetConfig(participants_per_round=6, max_executors=3, seed=5)
+    who = sorted(by_id)
+    params = torch.tensor(fed.layout.to_padded(init_cnn_params(10, 1)), dtype=torch.float64, device="cuda")
+    parts = GreenPartitions(0, 8)
+    engines = [CnnEngine(1, 64, 10) for _ in range(cfg.max_executors)]
+    live = LiveRound(fed, by_id, cfg, 0.01, parts, engines=engines)
+    live.run(params, who, round_index=0)      # warm-up (plans, module load)
+    d_live, rep, trace, measured = live.run(params, who, round_index=0)
+    seeds = [fm.seed_of("train", cfg.seed, 0, c) for c in who]
+    d_batch = fed.train(params, who, [by_id[c].workload for c in who], 0.01, seeds, use_graph=False)
+    assert torch.allclose(d_live, d_batch, rtol=0, atol=1e-6 * float(d_batch.abs().max()))
+    _replay_live_on_oracle(trace, by_id, cfg, who)
+    lo = [measured[c] for c in who if by_id[c].resource_budget == 10]
+    hi = [measured[c] for c in who if by_id[c].resource_budget == 80]
+    assert lo and hi and min(lo) > max(hi), (lo, hi)
 
 
 @pytest.mark.parametrize("G,M,N,K", [(1, 128, 128, 64), (3, 256, 384, 512), (5, 2048, 128, 3136 // 64 * 64),
