@@ -370,8 +370,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 6) {
     // ---- converters: fp32 stage -> bf16 hi / mid SW128 chunks ------------------------------------
     const int ct = tid - 6 * 32;
-    const int u = ct & 7;
-    const int dq = 16 / NCH, dr = 16 % NCH;  // (row, chunk) advance per 128-item stride
+    // thread -> a fixed (chunk, 4-feature quarter-unit) of every row it converts: 16 threads read one 256-byte
+    // (row, chunk) segment and write one swizzled 128-byte row of the hi and of the mid tile; a row is NCH * 16
+    // threads, 128 / (NCH * 16) rows per pass (NCH <= 8), so the inner loop is pointer arithmetic only
+    const int per_row = NCH * 16, rpp = 128 / per_row;
+    const bool active = ct < rpp * per_row;
+    const int pos = active ? ct % per_row : 0, r_off = active ? ct / per_row : kStageRows;
+    const int ch = pos >> 4, hu = pos & 15, u = hu >> 1;
+    const int fl = ch * 64 + hu * 4;
+    const bool fvalid = fl < Sk;
+    const uint32_t dst_c = s_x + ch * kChunk + (hu & 1) * 8;
     int it = 0;
     for (int s = 0; s < steps; ++s) {
       const BatchRef br = batch_ref(s, n, B);
@@ -381,56 +389,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int slot = it % g.stages, use = it / g.stages;
         mbar_wait(&full[slot], use & 1);
         if (ct == 0) trace_pt(g, crank, s, 12 + j);
-        const float* stage = reinterpret_cast<const float*>(smem + g.off_stage + slot * g.stage_bytes);
-        int rr = (ct >> 3) / NCH, ch = (ct >> 3) - rr * NCH;
-        // two independent items per iteration (ILP); hi = bf16 truncation, mid = bf16(x - hi): |x - hi - mid| <=
-        // 2^-16 |x|
-        auto load = [&](int rr_, int ch_, float4& a, float4& b) {
-          const int fl = ch_ * 64 + u * 8;
-          a = make_float4(0.f, 0.f, 0.f, 0.f);
-          b = a;
-          if (kStageRows * j + rr_ < br.rows) {
-            const float* src = stage + rr_ * S + fl;
-            if (fl < Sk) a = *reinterpret_cast<const float4*>(src);
-            if (fl + 4 < Sk) b = *reinterpret_cast<const float4*>(src + 4);
-          }
-        };
-        auto store = [&](int rr_, int ch_, const float4& a, const float4& b) {
-          const int r = kStageRows * j + rr_;
-          const float xs[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-          uint32_t h[4], m[4];
+        const float* src = reinterpret_cast<const float*>(smem + g.off_stage + slot * g.stage_bytes) + fl;
+        const int nr = br.rows - kStageRows * j;  // valid rows of this stage
+        // 8 rows in flight per thread: all loads first, then the conversions (hides the LDS latency)
+        for (int r0 = r_off; r0 < kStageRows; r0 += 8 * rpp) {
+          float4 v[8];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t x0 = __float_as_uint(xs[2 * e]), x1 = __float_as_uint(xs[2 * e + 1]);
-            h[e] = __byte_perm(x0, x1, 0x7632);
-            const float m0 = xs[2 * e] - __uint_as_float(x0 & 0xffff0000u);
-            const float m1 = xs[2 * e + 1] - __uint_as_float(x1 & 0xffff0000u);
-            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(m[e]) : "f"(m1), "f"(m0));
+          for (int k = 0; k < 8; ++k) {
+            const int rr = r0 + k * rpp;
+            v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (fvalid && rr < nr && rr < kStageRows) v[k] = *reinterpret_cast<const float4*>(src + rr * S);
           }
-          const uint32_t dst = s_x + ch_ * kChunk + r * 128 + ((u ^ (r & 7)) << 4);
-          sts4(dst, h[0], h[1], h[2], h[3]);
-          sts4(dst + 8192, m[0], m[1], m[2], m[3]);
-        };
-        auto advance = [&](int& rr_, int& ch_) {
-          ch_ += dr;
-          rr_ += dq;
-          if (ch_ >= NCH) {
-            ch_ -= NCH;
-            ++rr_;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int rr = r0 + k * rpp;
+            if (rr < kStageRows) {
+              // hi = bf16 truncation, mid = bf16(x - hi): |x - hi - mid| <= 2^-16 |x|
+              const uint32_t x0 = __float_as_uint(v[k].x), x1 = __float_as_uint(v[k].y),
+                             x2 = __float_as_uint(v[k].z), x3 = __float_as_uint(v[k].w);
+              const uint32_t h0 = __byte_perm(x0, x1, 0x7632), h1 = __byte_perm(x2, x3, 0x7632);
+              uint32_t m0, m1;
+              asm("cvt.rn.bf16x2.f32 %0, %1, %2;"
+                  : "=r"(m0)
+                  : "f"(v[k].y - __uint_as_float(x1 & 0xffff0000u)), "f"(v[k].x - __uint_as_float(x0 & 0xffff0000u)));
+              asm("cvt.rn.bf16x2.f32 %0, %1, %2;"
+                  : "=r"(m1)
+                  : "f"(v[k].w - __uint_as_float(x3 & 0xffff0000u)), "f"(v[k].z - __uint_as_float(x2 & 0xffff0000u)));
+              const int r = kStageRows * j + rr;
+              const uint32_t dst = dst_c + r * 128 + ((u ^ (r & 7)) << 4);
+              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(dst), "r"(h0), "r"(h1) : "memory");
+              asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(dst + 8192), "r"(m0), "r"(m1) : "memory");
+            }
           }
-        };
-        while (rr < kStageRows) {
-          int rr2 = rr, ch2 = ch;
-          advance(rr2, ch2);
-          float4 a0, b0, a1, b1;
-          load(rr, ch, a0, b0);
-          const bool two = rr2 < kStageRows;
-          if (two) load(rr2, ch2, a1, b1);
-          store(rr, ch, a0, b0);
-          if (two) store(rr2, ch2, a1, b1);
-          rr = rr2;
-          ch = ch2;
-          if (two) advance(rr, ch);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -648,7 +638,7 @@ static bool plan_cl(int F, int C, int CL, int max_smem, TcGeom& g) {
   g.S = up((F + CL - 1) / CL, 4);
   if (F - (CL - 1) * g.S <= 0) return false;  // every CTA owns features
   g.NCH = (g.S + 63) / 64;
-  if (g.NCH < 2 || 128 / (kRows / CL) > 32 || g.NP % (128 / (kRows / CL)) != 0) return false;
+  if (g.NCH < 2 || g.NCH > 8 || 128 / (kRows / CL) > 32 || g.NP % (128 / (kRows / CL)) != 0) return false;
   g.NT = (g.NCH + 1) / 2;
   const int cols = (2 + 3 * g.NT) * g.NP;  // Z (2 NP) + G tiles (2 NP each) + fp32 master W tiles (NP each)
   if (cols > 512) return false;
