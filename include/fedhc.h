@@ -76,6 +76,25 @@ typedef struct fedhc_client {
 int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params,
                       int n_features, int n_classes, int max_batch, void* stream);
 
+/* ---- native round planning (the serving loop's host work) ------------- */
+/* CPython 3.12 random.Random.sample(range(n), k) on an MT19937 state laid out
+ * as Random.getstate()[1] (624 words + index, updated in place); bit-exact
+ * with the reference's selection (engine.py:302, :327). */
+int fedhc_mt_sample(uint32_t* state, int n, int k, int32_t* out);
+/* CPython >= 3.12 sum() of n floats (Neumaier compensation). */
+double fedhc_py_float_sum(const double* x, int n);
+/* One rank's round plan for k participants (fleet indices `mine`): per-client
+ * seeds (stable_seed chain, fl_core.py:21-24, :181), and the pinned staging
+ * block [PCG64 seeds u64[k] | rows i32[k] | permutations i32[k] | offsets
+ * i64[k] | fedhc_client[k] | coef f64[k] = weight / total] that the runner
+ * copies to the GPU in one transfer.  Per-fleet-client arrays are indexed by
+ * fleet index; perm_base / delta_base are device addresses. */
+int fedhc_round_pack(int64_t seed, int64_t round_index, int k, const int64_t* mine, const char* const* reprs,
+                     const int32_t* rows, const int32_t* n_perms, const int32_t* n_batches,
+                     const int32_t* batch_size, const uint64_t* xptr, const uint64_t* yptr, const double* weight,
+                     double total, float lr, uint64_t perm_base, uint64_t delta_base, int64_t delta_stride,
+                     uint8_t* staging, int64_t* perm_words, int32_t* max_rows);
+
 /* Diagnostics: phase timestamps (%globaltimer ns, [8 CTAs][32 steps][24
  * points]) of cluster 0 from the last tcgen05 local_train launch made with
  * the environment variable FEDHC_TC_TRACE set; host `out`. */

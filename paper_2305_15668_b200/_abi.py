@@ -115,6 +115,10 @@ SIGNATURES = {
     "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
     "fedhc_tc_trace_read": (_i, [_vp]),
+    "fedhc_mt_sample": (_i, [_vp, _i, _i, _vp]),
+    "fedhc_py_float_sum": (C.c_double, [_vp, _i]),
+    "fedhc_round_pack": (_i, [C.c_int64, C.c_int64, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_double,
+                              C.c_float, C.c_uint64, C.c_uint64, C.c_int64, _vp, _vp, _vp]),
     "fedhc_loss_and_grad": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "fedhc_fedavg_coefficients": (_i, [_dp, _i, _dp]),
     "fedhc_fedavg": (_i, [_vp, _vp, _i64, _i, _vp, _i, _vp, _vp, _i64, _vp]),

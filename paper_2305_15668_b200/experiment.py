@@ -473,8 +473,15 @@ class FederatedRunner:
         self.use_graphs = use_graphs and device_permutations and world == 1
         self._graphs = [None] * n
         self._cap_stream = torch.cuda.Stream(device=dev)
-        self._c_xptr = fed.x.data_ptr() + off * (F * 4)
-        self._c_yptr = fed.y.data_ptr() + off * 4
+        self._c_xptr = np.ascontiguousarray((fed.x.data_ptr() + off * (F * 4)).astype(np.uint64))
+        self._c_yptr = np.ascontiguousarray((fed.y.data_ptr() + off * 4).astype(np.uint64))
+        self._c_rows32 = self._c_rows.astype(np.int32)
+        self._c_nperm32 = self._c_nperm.astype(np.int32)
+        self._c_steps32 = self._c_steps.astype(np.int32)
+        self._c_bs32 = self._c_bs.astype(np.int32)
+        # the selector's MT19937 state (Random.getstate(): 624 words + index) for the native sample
+        self._mt = np.array(self.selector.getstate()[1], dtype=np.uint32)
+        self._who_buf = np.zeros(max(cfg.participants_per_round, 1), dtype=np.int32)
         self.now = 0.0
         self.round = 0
         self._prefetch = None  # next run()'s first RoundPlan, planned during the previous run
@@ -497,10 +504,13 @@ class FederatedRunner:
         slot = (r % self.SLOTS) if slot is None else slot
         tick = time.perf_counter()
         # random.sample draws indices from len(population) only: sampling range(n) is the same draw
-        # sequence as sampling the ids (engine.py:327), and gives the fleet indices directly
-        who_idx = self.selector.sample(range(len(self.ids)), cfg.participants_per_round)
-        who = [self.ids[i] for i in who_idx]
-        wi = np.asarray(who_idx, np.int64)
+        # sequence as sampling the ids (engine.py:327), and gives the fleet indices directly.  Native:
+        # CPython's sample on the selector's MT19937 state (fedhc_mt_sample), bit-exact.
+        kp = cfg.participants_per_round
+        wi32 = self._who_buf[:max(kp, 1)]
+        _abi.check(_abi.lib.fedhc_mt_sample(self._mt.ctypes.data, len(self.ids), kp, wi32.ctypes.data))
+        wi = wi32[:kp].astype(np.int64)
+        who = [self.ids[i] for i in wi.tolist()]
         if self._over_theta[wi].any():   # sim.run raises the reference's ConfigError
             rep, _ = self.sim.run(who, cfg, t0=t0, round_index=r, want_trace=False)
         else:
@@ -513,15 +523,17 @@ class FederatedRunner:
         mine = [who[j] for j in sel]
         mi = wi[sel] if sel else np.zeros(0, np.int64)
         k = len(mine)
-        weights_all = self._c_w[np.asarray(who_idx, np.int64)].tolist()
-        total = float(sum(weights_all))                      # CPython float sum, as the reference
+        w_all = np.ascontiguousarray(self._c_w[wi])
+        total = _abi.lib.fedhc_py_float_sum(w_all.ctypes.data, kp)  # CPython 3.12 float sum(), as the reference
         # fl_core.fedavg's validation (fl_core.py:201-212), raised before any device work: the reference
         # raises it at the round's FedAvg (engine.py:351), after a round that trains nothing useful
         if not who:
             raise AggregationError("no deltas to aggregate")
         if total == 0:
             raise AggregationError("weights must not all be zero")
-        my_w = [weights_all[j] for j in sel]
+        my_w = w_all[sel].tolist()
+        if self.device_permutations:
+            return self._plan_packed(r, t0, slot, rep, who, mine, mi, my_w, total, tick, t1)
         coef = np.asarray(my_w, np.float64) / total
         reprs = self._repr_ptr[mi] if k else self._repr_ptr[:1]   # const char* per participant
         train_seeds = np.zeros(max(k, 1), np.uint64)
@@ -570,6 +582,38 @@ class FederatedRunner:
         hs["descriptors"] += t4 - t3
         return RoundPlan(r, mine, who, rep, t0, my_w, coef, slot, at, desc, meta_bytes,
                          int(rows.max()) if k else 0)
+
+    def _plan_packed(self, r, t0, slot, rep, who, mine, mi, my_w, total, tick, t1) -> RoundPlan:
+        """Device batch order: seeds, the [meta | descriptors | coefficients] staging block and the plan
+        buffer in one native call (fedhc_round_pack, GIL released)."""
+        k = len(mine)
+        at = int((self._c_rows[mi] * self._c_nperm[mi]).sum()) if k else 0
+        self._ensure(slot, max(at, 1))
+        pin = self._stage_pin[slot]
+        words, mrows = C.c_int64(), C.c_int32()
+        mi64 = np.ascontiguousarray(mi, dtype=np.int64)
+        _abi.check(_abi.lib.fedhc_round_pack(int(self.cfg.seed), int(r), k, mi64.ctypes.data,
+                                             self._repr_ptr.ctypes.data, self._c_rows32.ctypes.data,
+                                             self._c_nperm32.ctypes.data, self._c_steps32.ctypes.data,
+                                             self._c_bs32.ctypes.data, self._c_xptr.ctypes.data,
+                                             self._c_yptr.ctypes.data, self._c_w.ctypes.data, float(total),
+                                             float(self.lr), self._dev_plan[slot].data_ptr(), self.deltas.data_ptr(),
+                                             self.deltas.stride(0) * 4, pin.data_ptr(), C.byref(words),
+                                             C.byref(mrows)))
+        buf = pin.numpy()
+        nb = k * CLIENT_DTYPE.itemsize
+        meta_bytes = 24 * k if at else 0
+        desc = buf[24 * k:24 * k + nb].view(CLIENT_DTYPE)
+        coef = buf[24 * k + nb:24 * k + nb + 8 * k].view(np.float64)
+        if not at:  # every shard empty: no device permutations (zero deltas), descriptors still launch
+            desc, coef = desc.copy(), coef.copy()
+        t4 = time.perf_counter()
+        hs = self.host_s
+        hs["select+des"] += t1 - tick
+        hs["seeds"] += 0.0
+        hs["permutations"] += 0.0
+        hs["descriptors"] += t4 - t1
+        return RoundPlan(r, mine, who, rep, t0, my_w, coef, slot, at, desc, meta_bytes, int(mrows.value))
 
     # ---- device side -------------------------------------------------------
     def _graph_key(self, p: RoundPlan):
