@@ -217,18 +217,44 @@ __device__ __forceinline__ void st_async1(uint32_t cluster_addr, float v, uint32
                : "memory");
 }
 
-// W[feature fl][0..NP) -> the forward's K-major operand chunk [Wh NP rows][Wm NP rows] x 64 features (SW128)
+// W[feature fl][0..NP) -> the forward's B operand chunk (64 features x [Wh NP | Wm NP], bf16).
+// NP >= 32: MN-major (the 2 NP classes of a feature are contiguous: 64-class SW128 atoms 8 KB apart, a
+//   feature = one 128-byte row of each atom), so a thread writes its row with 16-byte stores;
+// NP = 16: K-major (2 NP = 32 class rows of 64 features), 2-byte stores.
+template <int NP>
+__host__ __device__ constexpr bool w_mn() { return NP >= 32; }
+
 template <int NP>
 __device__ __forceinline__ void write_wsplit(uint32_t s_w, int fl, const float (&w)[NP]) {
-  const int ch = fl >> 6, fe = fl & 63, uu = fe >> 3, e = fe & 7;
-  const uint32_t base = s_w + ch * (2 * NP * 128) + e * 2;
+  const int ch = fl >> 6, fe = fl & 63;
+  if constexpr (w_mn<NP>()) {
+    const uint32_t row = s_w + ch * (2 * NP * 128) + (fe >> 3) * 1024 + (fe & 7) * 128;
+    uint32_t hi[NP / 2], mid[NP / 2];
 #pragma unroll
-  for (int c = 0; c < NP; ++c) {
-    uint16_t hi, mid;
-    split1(w[c], hi, mid);
-    const uint32_t a = base + c * 128 + ((uu ^ (c & 7)) << 4);
-    sts16(a, hi);
-    sts16(a + NP * 128, mid);
+    for (int c = 0; c < NP; c += 2) {
+      uint16_t h0, m0, h1, m1;
+      split1(w[c], h0, m0);
+      split1(w[c + 1], h1, m1);
+      hi[c / 2] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      mid[c / 2] = (uint32_t)m0 | ((uint32_t)m1 << 16);
+    }
+#pragma unroll
+    for (int U = 0; U < NP / 4; ++U) {  // 16-byte units over the 2 NP-class row: [hi NP/8 units | mid NP/8 units]
+      const uint32_t* src = U < NP / 8 ? hi + 4 * U : mid + 4 * (U - NP / 8);
+      const uint32_t a = row + (U >> 3) * 8192 + (((U & 7) ^ (fe & 7)) << 4);
+      sts4(a, src[0], src[1], src[2], src[3]);
+    }
+  } else {
+    const int uu = fe >> 3, e = fe & 7;
+    const uint32_t base = s_w + ch * (2 * NP * 128) + e * 2;
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      uint16_t h, m;
+      split1(w[c], h, m);
+      const uint32_t a = base + c * 128 + ((uu ^ (c & 7)) << 4);
+      sts16(a, h);
+      sts16(a + NP * 128, m);
+    }
   }
 }
 
@@ -332,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---- MMA issuer: hi / mid stacked in M (rows) and in N (classes) --------------------------
-    constexpr uint32_t ID_F = idesc_f16(128, 2 * NP, false, false);
+    constexpr uint32_t ID_F = idesc_f16(128, 2 * NP, false, w_mn<NP>());
     constexpr uint32_t ID_B = idesc_f16(128, 2 * NP, true, false);
     for (int s = 0; s < steps; ++s) {
       mbar_wait(&bars[B_XS_FULL], s & 1);
@@ -343,7 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma(t_z, sw128(s_x + ch * kChunk + kk * 32, 16), sw128(s_w + ch * WCH + kk * 32, 16), ID_F,
+            umma(t_z, sw128(s_x + ch * kChunk + kk * 32, 16),
+                 w_mn<NP>() ? sw128(s_w + ch * WCH + kk * 2048, 8192) : sw128(s_w + ch * WCH + kk * 32, 16), ID_F,
                  (ch | kk) != 0);
         }
         commit(&bars[B_Z_FULL]);
