@@ -288,8 +288,7 @@ def run_ours(args, rank, world, local_rank):
         main = torch.cuda.current_stream()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        _abi.check(_abi.lib.fedhc_local_train(mine_desc.data_ptr(), PER_GPU, params.data_ptr(), F, C, BATCH,
-                                              stream_ptr()))
+        fed.launch_train(mine_desc.data_ptr(), PER_GPU, params, BATCH)
         ev1.record()
         if world == 1:
             if eval_done[0] is not None:
@@ -477,8 +476,7 @@ def kernel_subline(C_, F_, n_clients, n_samp, rounds, warm, fleet_seed=1):
             t0.record()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        _abi.check(_abi.lib.fedhc_local_train(desc.data_ptr(), n_clients, params.data_ptr(), F_, C_, BATCH,
-                                              stream_ptr()))
+        fed.launch_train(desc.data_ptr(), n_clients, params, BATCH)
         b.record()
         if i >= warm:
             evs.append((a, b))

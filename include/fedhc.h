@@ -76,6 +76,22 @@ typedef struct fedhc_client {
 int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params,
                       int n_features, int n_classes, int max_batch, void* stream);
 
+/* Rows re-encoded for the bf16x3 tensor-pipe trainers (setup, once per
+ * federation): fp32 row i of x [n_rows, n_features] becomes n_features bf16
+ * "hi" words followed by n_features bf16 "mid" words (hi = bf16_rn(x),
+ * mid = bf16_rn(x - hi), |x - hi - mid| <= 2^-17 |x|) -- the same 4F bytes,
+ * so `out` has x's byte layout.  n_features even. */
+int fedhc_x_split(const float* x, int64_t n_rows, int n_features, void* out, void* stream);
+
+/* fedhc_local_train (fl_core.py:163-194) whose client rows ALSO exist in the
+ * fedhc_x_split layout at (char*)client.x + split_offset (bytes, signed,
+ * multiple of 16: the distance from the fp32 rows to their split copy).  Shapes with a split-reading kernel (F = 784, C <= 16: the FEMNIST
+ * logistic round) read that copy -- identical products, fewer instructions
+ * per fragment; every other shape reads client.x as fp32.  Results are
+ * bit-identical to fedhc_local_train. */
+int fedhc_local_train_split(const fedhc_client* clients, int n_clients, const double* params,
+                            int n_features, int n_classes, int max_batch, int64_t split_offset, void* stream);
+
 /* ---- native round planning (the serving loop's host work) ------------- */
 /* CPython 3.12 random.Random.sample(range(n), k) on an MT19937 state laid out
  * as Random.getstate()[1] (624 words + index, updated in place); bit-exact
@@ -297,6 +313,9 @@ typedef struct fedhc_gctx_pool fedhc_gctx_pool;
 int fedhc_gctx_pool_create(int device, int min_sms, fedhc_gctx_pool** out, int* n_groups, int* sms_per_group);
 void fedhc_gctx_pool_destroy(fedhc_gctx_pool* pool);
 int fedhc_gctx_stream(fedhc_gctx_pool* pool, int first_group, int n_groups, void** stream, int* sm_count);
+/* As fedhc_gctx_stream, plus the SMs the split left outside every group (n_groups may be 0): side work
+ * (the round loop's batch order / accuracy) that must stay off the SMs a round's training claims. */
+int fedhc_gctx_stream_rest(fedhc_gctx_pool* pool, int first_group, int n_groups, void** stream, int* sm_count);
 /* Diagnostic: `blocks` CTAs on `stream` each write their %smid to out_dev[i]. */
 int fedhc_probe_smid(void* stream, int blocks, int* out_dev);
 

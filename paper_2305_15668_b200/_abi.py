@@ -114,6 +114,8 @@ SIGNATURES = {
     "fedhc_version": (_i, []),
     "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
+    "fedhc_x_split": (_i, [_vp, _i64, _i, _vp, _vp]),
+    "fedhc_local_train_split": (_i, [_vp, _i, _vp, _i, _i, _i, _i64, _vp]),
     "fedhc_tc_trace_read": (_i, [_vp]),
     "fedhc_mt_sample": (_i, [_vp, _i, _i, _vp]),
     "fedhc_py_float_sum": (C.c_double, [_vp, _i]),
@@ -147,6 +149,7 @@ SIGNATURES = {
     "fedhc_gctx_pool_create": (_i, [_i, _i, C.POINTER(_vp), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_gctx_pool_destroy": (None, [_vp]),
     "fedhc_gctx_stream": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_i)]),
+    "fedhc_gctx_stream_rest": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_i)]),
     "fedhc_probe_smid": (_i, [_vp, _i, _vp]),
     "fedhc_gemm_bf16_tn": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "fedhc_gemm": (_i, [C.POINTER(GemmArgs), _vp]),

@@ -168,6 +168,32 @@ extern "C" int fedhc_gctx_stream(fedhc_gctx_pool* p, int first, int count, void*
   return FEDHC_OK;
 }
 
+extern "C" int fedhc_gctx_stream_rest(fedhc_gctx_pool* p, int first, int count, void** stream, int* sm_count) {
+  if (!p || !stream) return fedhc::fail(FEDHC_ERR_VALUE, "gctx: null argument");
+  const int G = static_cast<int>(p->groups.size());
+  if (count < 0 || first < 0 || first + count > G) return fedhc::fail(FEDHC_ERR_VALUE, "gctx: group window out of range");
+  const int rest = static_cast<int>(p->remaining.sm.smCount);
+  if (count == 0 && rest == 0) return fedhc::fail(FEDHC_ERR_VALUE, "gctx: empty window (no remaining SMs)");
+  std::lock_guard<std::mutex> lock(p->mu);
+  auto key = std::make_pair(first, -1 - count);  // windows that include the remaining SMs
+  auto it = p->cache.find(key);
+  if (it == p->cache.end()) {
+    std::vector<CUdevResource> res(p->groups.begin() + first, p->groups.begin() + first + count);
+    if (rest > 0) res.push_back(p->remaining);
+    CUdevResourceDesc desc;
+    Driver& D = driver();
+    DRV_TRY(D.DevResourceGenerateDesc(&desc, res.data(), static_cast<unsigned>(res.size())));
+    CUgreenCtx g;
+    DRV_TRY(D.GreenCtxCreate(&g, desc, p->dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    CUstream s;
+    DRV_TRY(D.GreenCtxStreamCreate(&s, g, CU_STREAM_NON_BLOCKING, 0));
+    it = p->cache.emplace(key, std::make_pair(g, s)).first;
+  }
+  *stream = it->second.second;
+  if (sm_count) *sm_count = count * p->sms_per_group + rest;
+  return FEDHC_OK;
+}
+
 extern "C" int fedhc_probe_smid(void* stream, int blocks, int* out_dev) {
   if (blocks < 1 || !out_dev) return fedhc::fail(FEDHC_ERR_VALUE, "probe: bad arguments");
   probe_smid_kernel<<<blocks, 32, 0, static_cast<cudaStream_t>(stream)>>>(out_dev);

@@ -152,13 +152,37 @@ namespace fedhc {
 bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
                      int max_smem, cudaStream_t st, int* status);
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
-                        int max_smem, cudaStream_t st, int* status);
+                        int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status);
+cudaError_t launch_x_split(const float* x, int64_t n_rows, int F, void* out, cudaStream_t st);
 }
 
 using namespace fedhc;
 
+extern "C" int fedhc_x_split(const float* x, int64_t n_rows, int n_features, void* out, void* stream) {
+  if (n_rows < 0 || n_features < 2 || n_features % 2 != 0)
+    return fail(FEDHC_ERR_VALUE, "x_split: need n_rows >= 0 and an even n_features >= 2");
+  if (n_rows > 0 && (x == nullptr || out == nullptr)) return fail(FEDHC_ERR_VALUE, "x_split: null pointer");
+  FEDHC_CUDA_TRY(launch_x_split(x, n_rows, n_features, out, static_cast<cudaStream_t>(stream)));
+  return FEDHC_OK;
+}
+
+static int local_train_impl(const fedhc_client* clients, int n_clients, const double* params, int n_features,
+                            int n_classes, int max_batch, bool split, int64_t split_off, void* stream);
+
 extern "C" int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params, int n_features,
                                  int n_classes, int max_batch, void* stream) {
+  return local_train_impl(clients, n_clients, params, n_features, n_classes, max_batch, false, 0, stream);
+}
+
+extern "C" int fedhc_local_train_split(const fedhc_client* clients, int n_clients, const double* params,
+                                       int n_features, int n_classes, int max_batch, int64_t split_offset,
+                                       void* stream) {
+  if (split_offset % 16 != 0) return fail(FEDHC_ERR_VALUE, "local_train_split: split_offset must be a multiple of 16");
+  return local_train_impl(clients, n_clients, params, n_features, n_classes, max_batch, true, split_offset, stream);
+}
+
+static int local_train_impl(const fedhc_client* clients, int n_clients, const double* params, int n_features,
+                            int n_classes, int max_batch, bool split, int64_t split_off, void* stream) {
   if (n_clients < 0 || n_features < 1 || n_classes < 2 || max_batch < 1)
     return fail(FEDHC_ERR_VALUE, "local_train: need n_clients >= 0, n_features >= 1, n_classes >= 2, batch >= 1");
   if (n_clients == 0) return FEDHC_OK;
@@ -170,7 +194,7 @@ extern "C" int fedhc_local_train(const fedhc_client* clients, int n_clients, con
   int fused_status = FEDHC_OK;
   if (launch_train_tc(clients, n_clients, params, n_features, n_classes, max_batch, max_smem, st, &fused_status))
     return fused_status;
-  if (launch_train_fused(clients, n_clients, params, n_features, n_classes, max_smem, st, &fused_status))
+  if (launch_train_fused(clients, n_clients, params, n_features, n_classes, max_smem, split, split_off, st, &fused_status))
     return fused_status;
   // generic fallback: W in shared memory, batches in row tiles
   const int64_t P = (int64_t)n_features * n_classes + n_classes;

@@ -428,6 +428,62 @@ __global__ void __launch_bounds__(kFThreads, 1)
   if (CL > 1) cluster_sync_all();  // keep shared memory alive until peers are done with it
 }
 
+// Walks the 16-row stages of a client's SGD steps (batch_ref order, ragged batches included).
+struct StageIter {
+  int n, B, steps, s, r0, rows;
+  int64_t off;
+  bool valid;
+  __device__ StageIter(int n_, int B_, int steps_) : n(n_), B(B_), steps(steps_), s(0), r0(0), rows(0), off(0) {
+    valid = steps > 0;
+    if (valid) set();
+  }
+  __device__ void set() {
+    const BatchRef br = batch_ref(s, n, B);
+    rows = min(kFRows, br.rows - r0);
+    off = br.perm_off + r0;
+  }
+  __device__ void next() {
+    if (!valid) return;
+    const BatchRef br = batch_ref(s, n, B);
+    r0 += kFRows;
+    if (r0 >= br.rows) {
+      r0 = 0;
+      if (++s >= steps) {
+        valid = false;
+        return;
+      }
+    }
+    set();
+  }
+};
+
+// fedhc_x_split: each fp32 row [F] -> [F bf16 hi | F bf16 mid] (the same 4F bytes), hi / mid exactly as
+// split_bf16x2 makes them inside the kernels, so a trainer reading this copy computes the same products.
+__global__ void x_split_kernel(const float* __restrict__ x, int64_t n_pairs, int half_f, uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pairs; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / half_f;
+    const int p = static_cast<int>(i - row * half_f);
+    const float2 v = __ldcs(reinterpret_cast<const float2*>(x) + i);
+    uint32_t hi, mid;
+    split_bf16x2(v.x, v.y, hi, mid);
+    uint32_t* o = out + row * (2 * half_f);
+    o[p] = hi;
+    o[half_f + p] = mid;
+  }
+}
+
+cudaError_t launch_x_split(const float* x, int64_t n_rows, int F, void* out, cudaStream_t st) {
+  const int64_t n_pairs = n_rows * (F / 2);
+  if (n_pairs == 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n_pairs + 255) / 256;
+  const int grid = static_cast<int>(want < 8LL * sms ? want : 8LL * sms);
+  x_split_kernel<<<grid, 256, 0, st>>>(x, n_pairs, F / 2, static_cast<uint32_t*>(out));
+  return cudaGetLastError();
+}
+
 // ============================================================================
 // v4 "pipelined" variant for one CTA per client (C <= 16, F = 784): the
 // softmax moves to a dedicated warp and the compute warps software-pipeline
@@ -449,23 +505,29 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // ============================================================================
 constexpr int kPWarps = 14, kPThreads = 16 * 32, kPStages = 4;
 constexpr int kPSoft = 15, kPProd = 14;
+constexpr int kPEPitch = 48;  // bytes per row of a split bf16 E plane (16 classes + 16 B pad: conflict-free ldmatrix)
 
 struct PipeGeom {
   int Fs, Es, Zs;
   int off_master, off_x, off_zp, off_e, off_lab, off_bar, off_bias, bytes;
 };
 
-static bool plan_pipe(int F, int C, int max_smem, PipeGeom& g) {
+// split: rows arrive pre-split (fedhc_x_split: F bf16 hi words, then F bf16 mid words) and are read with
+// ldmatrix; the row pitch 3152 B = 197 x 16 B makes 8 consecutive rows hit 8 distinct 16-byte bank groups.
+static bool plan_pipe(int F, int C, int max_smem, PipeGeom& g, bool split) {
   if (F != kFWarps * kFK8 * 8 || C > 16) return false;
   g.Fs = F;
-  while (g.Fs % 32 != 8) g.Fs += 4;
+  if (split) g.Fs = F + 4;  // 3152 B
+  else
+    while (g.Fs % 32 != 8) g.Fs += 4;
   g.Es = 20;  // 5 x 16 B per row: conflict-free 128-bit row accesses by 8 consecutive rows
   g.Zs = 20;
   int off = 0;
   g.off_master = off;  // the fp32 master W lives in TMEM (train_pipe_kernel), not in shared memory
   g.off_x = off;      off = a16(off + kPStages * kFRows * g.Fs * 4);
   g.off_zp = off;     off = a16(off + kPWarps * kFRows * g.Zs * 4);
-  g.off_e = off;      off = a16(off + 2 * kFRows * g.Es * 4);
+  // E: fp32 [2 parity][16 rows][Es], or split bf16 [2 parity][hi, mid][16 rows][kPEPitch bytes]
+  g.off_e = off;      off = a16(off + (split ? 2 * 2 * kFRows * kPEPitch : 2 * kFRows * g.Es * 4));
   g.off_lab = off;    off = a16(off + kPStages * kFRows * 4);
   g.off_bar = off;    off = a16(off + 2 * kPStages * 8);
   g.off_bias = off;   off = a16(off + 16 * 4 + 16);  // + the TMEM base address slot
@@ -506,9 +568,13 @@ __device__ __forceinline__ void tmem_ld28(uint32_t taddr, float4 (&m)[kFK8]) {
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// SPLIT: client rows are read at (char*)x + split_off in the fedhc_x_split layout; the fragments come
+// straight from shared memory by ldmatrix (forward) / ldmatrix.trans (backward) instead of fp32 loads +
+// bf16 hi/mid splits, and the softmax warp stores E already split -- the same products, bit for bit.
+template <bool SPLIT>
 __global__ void __launch_bounds__(kPThreads, 1)
     train_pipe_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const int F,
-                      const int C, const PipeGeom g) {
+                      const int C, const PipeGeom g, const int64_t split_off) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* Xb = reinterpret_cast<float*>(smem + g.off_x);
   float* Zp = reinterpret_cast<float*>(smem + g.off_zp);
@@ -530,7 +596,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   fence_proxy_async_smem();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);         // expect_tx + labels stored (producer)
       mbar_init(&empty[s], kPWarps);  // every compute warp releases a stage after its backward
     }
     fence_mbar_init();
@@ -565,29 +631,41 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   if (warp == kPProd) {
     // ===== producer: TMA row gather (one bulk copy per row) =====
+    // The gather indices are prefetched two stages ahead and the labels one stage ahead, so a freed stage
+    // is refilled without two dependent global loads (perm -> y) on the critical path; the stage's full
+    // barrier takes two arrivals: expect_tx before the copies, and one after the labels are stored.
+    StageIter it0(n, B, steps), it1 = it0, it2 = it0;
+    it1.next();
+    it2.next();
+    it2.next();
+    int idx0 = it0.valid && lane < it0.rows ? cl.perm[it0.off + lane] : 0;
+    int idx1 = it1.valid && lane < it1.rows ? cl.perm[it1.off + lane] : 0;
+    int y0 = it0.valid && lane < it0.rows ? cl.y[idx0] : 0;
     int k = 0, st = 0;
-    for (int s = 0; s < steps; ++s) {
-      const BatchRef br = batch_ref(s, n, B);
-      for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
-        const int rows = min(kFRows, br.rows - r0);
-        if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
-        int idx = 0;
-        if (lane < rows) {
-          idx = cl.perm[br.perm_off + r0 + lane];
-          labels[st * kFRows + lane] = cl.y[idx];
-          __threadfence_block();
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows * F * 4));
-        __syncwarp();
-        if (lane < rows) {
-          fence_proxy_async_smem();
-          bulk_g2s(Xb + (size_t)(st * kFRows + lane) * Fs, cl.x + (size_t)idx * F, static_cast<uint32_t>(F * 4),
-                   &full[st]);
-        }
-        ++k;
-        st = (st + 1 == S) ? 0 : st + 1;
+    for (; it0.valid; ++k) {
+      const int rows = it0.rows;
+      const int y1 = it1.valid && lane < it1.rows ? cl.y[idx1] : 0;             // next stage's labels
+      const int idx2 = it2.valid && lane < it2.rows ? cl.perm[it2.off + lane] : 0;  // two stages ahead
+      if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows * F * 4));
+      __syncwarp();
+      if (lane < rows) {
+        fence_proxy_async_smem();
+        const float* src = cl.x + (size_t)idx0 * F;
+        if constexpr (SPLIT) src = reinterpret_cast<const float*>(reinterpret_cast<const char*>(src) + split_off);
+        bulk_g2s(Xb + (size_t)(st * kFRows + lane) * Fs, src, static_cast<uint32_t>(F * 4), &full[st]);
+        labels[st * kFRows + lane] = y0;
+        __threadfence_block();
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[st]);
+      idx0 = idx1;
+      idx1 = idx2;
+      y0 = y1;
+      it0 = it1;
+      it1 = it2;
+      it2.next();
+      st = (st + 1 == S) ? 0 : st + 1;
     }
   } else if (warp == kPSoft) {
     // ===== softmax warp: lane = (row r = lane & 15, class half h = lane >> 4): 8 classes per lane,
@@ -652,9 +730,21 @@ __global__ void __launch_bounds__(kPThreads, 1)
           err[e] = (r < rows && c0 + e < C) ? (z[e] * inv - (c0 + e == y ? 1.f : 0.f)) * inv_nb : 0.f;
           gb[e] += err[e];
         }
-        float* E = Eb + (k & 1) * kFRows * Es + r * Es + c0;
-        *reinterpret_cast<float4*>(E) = make_float4(err[0], err[1], err[2], err[3]);
-        *reinterpret_cast<float4*>(E + 4) = make_float4(err[4], err[5], err[6], err[7]);
+        if constexpr (SPLIT) {
+          uint4 hi, mid;
+          split_bf16x2(err[0], err[1], hi.x, mid.x);
+          split_bf16x2(err[2], err[3], hi.y, mid.y);
+          split_bf16x2(err[4], err[5], hi.z, mid.z);
+          split_bf16x2(err[6], err[7], hi.w, mid.w);
+          unsigned char* E =
+              reinterpret_cast<unsigned char*>(Eb) + (k & 1) * 2 * kFRows * kPEPitch + r * kPEPitch + 2 * c0;
+          *reinterpret_cast<uint4*>(E) = hi;
+          *reinterpret_cast<uint4*>(E + kFRows * kPEPitch) = mid;
+        } else {
+          float* E = Eb + (k & 1) * kFRows * Es + r * Es + c0;
+          *reinterpret_cast<float4*>(E) = make_float4(err[0], err[1], err[2], err[3]);
+          *reinterpret_cast<float4*>(E + 4) = make_float4(err[4], err[5], err[6], err[7]);
+        }
         __syncwarp();
         named_arrive(3 + (k & 1), NCOMP);   // EFULL(k)
         ++k;
@@ -691,7 +781,50 @@ __global__ void __launch_bounds__(kPThreads, 1)
         split_bf16x2(v1.x, v1.y, ah[j][1], am[j][1]);
       }
     };
+    // SPLIT: this lane's ldmatrix row address inside a stage (hi plane; mid = + 2F bytes): row
+    // (lane & 7) + 8 ((lane >> 3) & 1), features 56 warp + 8 (lane >> 4) -- the same address serves the
+    // forward's A fragments (x4: slices j, j + 1) and the backward's transposed B fragments (tiles j, j + 1).
+    // E^T fragments: rows (lane & 7) + 8 (lane >> 4), classes 8 ((lane >> 3) & 1).
+    const uint32_t x_lane = smem_u32(Xb) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * (Fs * 4) +
+                            (kFK8 * 8 * warp + 8 * (lane >> 4)) * 2;
+    const uint32_t e_lane = smem_u32(Eb) + ((lane & 7) + 8 * (lane >> 4)) * kPEPitch + 16 * ((lane >> 3) & 1);
+    const uint32_t mid_off = 2 * F;
+    auto backward_split = [&](int kk, int sst) {
+      named_sync(3 + (kk & 1), NCOMP);  // EFULL(kk)
+      uint32_t eh[4], em[4];
+      const uint32_t ea = e_lane + (kk & 1) * 2 * kFRows * kPEPitch;
+      ldsm_x4_t(ea, eh);
+      ldsm_x4_t(ea + kFRows * kPEPitch, em);
+      const uint32_t xa = x_lane + sst * (kFRows * Fs * 4);
+#pragma unroll
+      for (int j = 0; j + 1 < kFK8; j += 2) {
+        uint32_t bh[4], bm[4];
+        ldsm_x4_t(xa + 16 * j, bh);
+        ldsm_x4_t(xa + 16 * j + mid_off, bm);
+        mma_bf16(G[j], eh, bh[0], bh[1]);
+        mma_bf16(G[j], eh, bm[0], bm[1]);
+        mma_bf16(G[j], em, bh[0], bh[1]);
+        mma_bf16(G[j + 1], eh, bh[2], bh[3]);
+        mma_bf16(G[j + 1], eh, bm[2], bm[3]);
+        mma_bf16(G[j + 1], em, bh[2], bh[3]);
+      }
+      {
+        constexpr int jl = kFK8 - 1;
+        uint32_t bh0, bh1, bm0, bm1;
+        ldsm_x2_t(xa + 16 * jl, bh0, bh1);
+        ldsm_x2_t(xa + 16 * jl + mid_off, bm0, bm1);
+        mma_bf16(G[jl], eh, bh0, bh1);
+        mma_bf16(G[jl], eh, bm0, bm1);
+        mma_bf16(G[jl], em, bh0, bh1);
+        __syncwarp();  // the MMAs above consumed the last fragments: every read of X(kk) has landed
+        if (lane == 0) mbar_arrive(&empty[sst]);
+      }
+    };
     auto backward = [&](int kk, int sst) {
+      if constexpr (SPLIT) {
+        backward_split(kk, sst);
+        return;
+      }
       named_sync(3 + (kk & 1), NCOMP);  // EFULL(kk)
       const float* E = Eb + (kk & 1) * kFRows * Es;
       uint32_t eh[4], em[4];
@@ -724,7 +857,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int e = 0; e < 2; ++e)
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) acc[e][nt][0] = acc[e][nt][1] = acc[e][nt][2] = acc[e][nt][3] = 0.f;
-        {
+        if constexpr (SPLIT) {
+          const uint32_t xa = x_lane + st * (kFRows * Fs * 4);
+#pragma unroll
+          for (int j = 0; j + 1 < kFK8; j += 2) {
+            uint32_t AH[4], AM[4];
+            ldsm_x4(xa + 16 * j, AH);
+            ldsm_x4(xa + 16 * j + mid_off, AM);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AH, wm[j][nt], wm[j + 1][nt]);
+              mma_bf16(acc[(j >> 1) & 1][nt], AM, wh[j][nt], wh[j + 1][nt]);
+            }
+          }
+          constexpr int jl = kFK8 - 1;
+          uint32_t h0, h1, m0, m1;
+          ldsm_x2(xa + 16 * jl, h0, h1);
+          ldsm_x2(xa + 16 * jl + mid_off, m0, m1);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            mma_bf16_k8(acc[1][nt], h0, h1, wh[jl][nt]);
+            mma_bf16_k8(acc[1][nt], h0, h1, wm[jl][nt]);
+            mma_bf16_k8(acc[1][nt], m0, m1, wh[jl][nt]);
+          }
+        } else {
           uint32_t ah[kFK8][2], am[kFK8][2];
           load_split(Xs, ah, am);
 #pragma unroll
@@ -836,23 +993,21 @@ static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, c
   return cudaLaunchKernelEx(&cfg, kern, clients, params, g);
 }
 
-// Launch the fused kernel if the shape fits; returns false to fall back.
+// Launch the fused kernel if the shape fits; returns false to fall back.  split: the client rows also
+// exist in the fedhc_x_split layout at (char*)x + split_off (used by the kernels that read it).
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
-                        int max_smem, cudaStream_t st, int* status) {
+                        int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status) {
   static const bool v3_only = getenv("FEDHC_TRAIN_V3") != nullptr;
   PipeGeom pg{};
-  if (!v3_only && plan_pipe(F, C, max_smem, pg)) {
-    // raise the opt-in only when needed (keeps launches capturable into CUDA graphs); per device
-    static int smem_set_of[64] = {0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    int& smem_set = smem_set_of[dev & 63];
-    if (pg.bytes > smem_set) {
-      e = cudaFuncSetAttribute(train_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pg.bytes);
-      if (e == cudaSuccess) smem_set = pg.bytes;
-    }
+  if (!v3_only && plan_pipe(F, C, max_smem, pg, split)) {
+    // opt in once per (kernel, device) to the maximum dynamic shared memory (thread-safe; keeps launches
+    // capturable into CUDA graphs)
+    const void* fn = split ? reinterpret_cast<const void*>(train_pipe_kernel<true>)
+                           : reinterpret_cast<const void*>(train_pipe_kernel<false>);
+    cudaError_t e = smem_optin_max(fn);
     if (e == cudaSuccess) {
-      train_pipe_kernel<<<n_clients, kPThreads, pg.bytes, st>>>(clients, params, F, C, pg);
+      if (split) train_pipe_kernel<true><<<n_clients, kPThreads, pg.bytes, st>>>(clients, params, F, C, pg, split_off);
+      else train_pipe_kernel<false><<<n_clients, kPThreads, pg.bytes, st>>>(clients, params, F, C, pg, 0);
       e = cudaGetLastError();
     }
     *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_pipe_kernel launch");

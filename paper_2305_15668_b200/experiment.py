@@ -34,7 +34,7 @@ from .roundsim import RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
 from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
                        init_params, make_synthetic_dataset, n_permutations, native_permutations, partition_noniid,
-                       stable_seed, stream_ptr)
+                       split_supported, stable_seed, stream_ptr, train_launch, x_split)
 
 
 @dataclass
@@ -108,6 +108,7 @@ class DeviceFederation:
         self._cap = 0
         self._pinned = None
         self._perm_dev = None
+        self.x_split = x_split(self.x) if split_supported(n_features, n_classes) else None
 
     @classmethod
     def from_arrays(cls, x: torch.Tensor, y: torch.Tensor, offsets: dict[str, tuple[int, int]],
@@ -119,7 +120,14 @@ class DeviceFederation:
         self.x, self.y, self.offset = x, y, dict(offsets)
         self.x_test, self.y_test, self.n_test = x_test, y_test, int(y_test.shape[0])
         self._cap, self._pinned, self._perm_dev = 0, None, None
+        self.x_split = x_split(self.x) if split_supported(self.n_features, n_classes) else None
         return self
+
+    def launch_train(self, desc_ptr: int, k: int, params: torch.Tensor, max_batch: int,
+                     stream: int | None = None) -> None:
+        """fedhc_local_train(_split) for k device descriptors pointing into this federation's rows."""
+        train_launch(desc_ptr, k, params.data_ptr(), self.n_features, self.n_classes, max_batch, self.x,
+                     self.x_split, stream)
 
     # ---- per-round plan (host) ------------------------------------------
     def plan_meta(self, participants: list[str], workloads, seeds):
@@ -212,8 +220,7 @@ class DeviceFederation:
         meta, _ = self.stage_plan(participants, workloads, seeds)
         d_desc = self.descriptors(participants, meta, lr, deltas)
         max_batch = max((wl.batch_size for wl in workloads), default=1)
-        _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr(), k, params.data_ptr(), self.n_features,
-                                              self.n_classes, max_batch, stream_ptr()))
+        self.launch_train(d_desc.data_ptr(), k, params, max_batch)
         self._keepalive = d_desc
         return deltas
 
@@ -364,7 +371,7 @@ class FederatedRunner:
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
                  plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = False,
-                 green_plan: bool = False, test_sharded: bool = False):
+                 green_side: bool = True, test_sharded: bool = False):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -418,22 +425,30 @@ class FederatedRunner:
         self._meta_pin = [torch.empty(k_max * 24, dtype=torch.uint8).pin_memory() for _ in range(n)]
         self._meta_dev = [torch.empty(k_max * 24, dtype=torch.uint8, device=dev) for _ in range(n)]
         self._plan_stream = torch.cuda.Stream(device=dev)
-        # Optional (green_plan=True, experimental): green-context SM partition for the batch-order kernel: the
-        # one-CTA-per-client train kernel needs
-        # k_max SMs with all their shared memory; confining perm_kernel to the remaining SM groups keeps its
-        # CTAs off the SMs the next round's training will claim (otherwise a resident permutation CTA makes
-        # a train CTA wait for it).  Falls back to an ordinary stream without green-context support.
+        # Side-work SM partition (green_side, single GPU): the one-CTA-per-client train kernel needs k_max SMs
+        # with all their shared memory and registers, so a batch-order (perm_kernel) or accuracy CTA resident
+        # on an SM when the next round's training launches makes a train CTA wait for it (measured: those
+        # rounds took 2x).  Both side streams live in green contexts confined to the SM groups the training
+        # does not need -- the permutations on one window, the accuracy on another (they overlap each other
+        # and the training).  The train kernel stays in the primary context.  Falls back to ordinary streams
+        # without green-context support or without spare SM groups.
         self._green = None
-        if green_plan and device_permutations:
+        self._eval_ctas = None
+        if green_side and world == 1:
             try:
                 from .live import GreenPartitions
                 gp = GreenPartitions(dev.index if dev.index is not None else 0)
-                need = -(-k_max // gp.sms_per_group)
-                if gp.n_groups - need >= 1:
-                    raw = gp.stream(need, gp.n_groups - need)
+                need = -(-k_max // gp.sms_per_group)  # groups the training needs (one SM per client)
+                spare = gp.n_groups - need
+                if spare >= 1:
+                    # permutations: the SMs outside every group (+ all spare groups but one); accuracy: one group
                     self._green = gp
-                    self._plan_stream = torch.cuda.ExternalStream(raw, device=dev)
-            except Exception:  # no green-context support in this driver: keep the ordinary stream
+                    if device_permutations:
+                        raw, _ = gp.stream_rest(need, spare - 1)
+                        self._plan_stream = torch.cuda.ExternalStream(raw, device=dev)
+                    self._eval_stream_raw = gp.stream(gp.n_groups - 1, 1)
+                    self._eval_ctas = gp.sms_per_group  # one CTA per SM of the window
+            except Exception:  # no green-context support in this driver: keep the ordinary streams
                 self._green = None
         self._train_done = [None] * n   # event: the slot's train kernel retired (plan buffer reusable)
         # one pinned / device staging block per slot for the device-plan mode: [meta 24k | desc | coef 8k],
@@ -447,7 +462,8 @@ class FederatedRunner:
         self._ev_result = [torch.cuda.Event() for _ in range(n)]
         # single-GPU eager rounds: accuracy of round r runs on its own stream, overlapping round r + 1's
         # training (both only read the params); round r + 1's FedAvg waits for it before writing them
-        self._eval_stream = torch.cuda.Stream(device=dev)
+        self._eval_stream = (torch.cuda.ExternalStream(self._eval_stream_raw, device=dev) if self._green is not None
+                             else torch.cuda.Stream(device=dev))
         self._sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self._ev_agg = [torch.cuda.Event() for _ in range(n)]
         self._eval_done = None
@@ -634,8 +650,7 @@ class FederatedRunner:
                                                                 self._dev_plan[slot].data_ptr(), self._rows_max,
                                                                 stream_ptr()))
         with torch.cuda.graph(gr, stream=self._cap_stream, capture_error_mode="thread_local"):
-            _abi.check(_abi.lib.fedhc_local_train(md + mb, k, self.params.data_ptr(), self.fed.n_features,
-                                                  self.fed.n_classes, self._bs_max, stream_ptr()))
+            self.fed.launch_train(md + mb, k, self.params, self._bs_max)
             fedavg_device(self.deltas[:k], coef_t, self.params, self.params)
             self.correct_dev.zero_()
             if self._nt:
@@ -750,8 +765,7 @@ class FederatedRunner:
             self.h2d_bytes = p.perm_words * 4 + nb + k * 8
         if k:
             max_b = int(p.desc["batch_size"].max())
-            _abi.check(_abi.lib.fedhc_local_train(desc_ptr, k, self.params.data_ptr(), self.fed.n_features,
-                                                  self.fed.n_classes, max_b, stream_ptr()))
+            self.fed.launch_train(desc_ptr, k, self.params, max_b)
         self._ev_train[slot].record()
         self._train_done[slot] = self._ev_train[slot]
         if self.world == 1:
@@ -774,7 +788,7 @@ class FederatedRunner:
                 self.correct_dev.zero_()
                 if self._nt:
                     # overlaps the next round's training (one CTA per client): stay on the idle SMs
-                    ctas = max(8, self._sms - k)
+                    ctas = self._eval_ctas if self._eval_ctas is not None else max(8, self._sms - k)
                     _abi.check(_abi.lib.fedhc_eval_ctas(self._xt.data_ptr(), self._yt.data_ptr(),
                                                         self._nt, self.fed.n_features, self.fed.n_classes,
                                                         self.params.data_ptr(), self.correct_dev.data_ptr(), ctas,

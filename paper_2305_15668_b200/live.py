@@ -35,21 +35,24 @@ from .training import check_aggregation, fedavg_device, n_permutations, native_p
 
 
 class GreenPartitions:
-    """SM groups of the device and budget -> group-window allocation."""
+    """SM groups of the device and budget -> group-window allocation.
+
+    The native pool (green contexts and their streams, one per group window) is shared per (device, min_sms)
+    and lives until process exit: torch keeps events recorded on these streams (pinned-memory copies, the
+    caching allocator) past any Python object's lifetime, and destroying a green context under them makes
+    later frees fail with "invalid device context".  Each instance keeps its own occupancy counters."""
+
+    _pools: dict = {}
 
     def __init__(self, device: int = 0, min_sms: int = 8):
-        pool = C.c_void_p()
-        g, spg = C.c_int(), C.c_int()
-        _abi.check(_abi.lib.fedhc_gctx_pool_create(device, min_sms, C.byref(pool), C.byref(g), C.byref(spg)))
-        self._pool = pool
-        self.n_groups, self.sms_per_group = g.value, spg.value
+        key = (device, min_sms)
+        if key not in GreenPartitions._pools:
+            pool = C.c_void_p()
+            g, spg = C.c_int(), C.c_int()
+            _abi.check(_abi.lib.fedhc_gctx_pool_create(device, min_sms, C.byref(pool), C.byref(g), C.byref(spg)))
+            GreenPartitions._pools[key] = (pool, g.value, spg.value, {})
+        self._pool, self.n_groups, self.sms_per_group, self._streams = GreenPartitions._pools[key]
         self.use = [0] * self.n_groups
-        self._streams = {}
-
-    def __del__(self):
-        if getattr(self, "_pool", None):
-            _abi.lib.fedhc_gctx_pool_destroy(self._pool)
-            self._pool = None
 
     def groups_for(self, budget: float) -> int:
         """Budget b% of the device -> k = max(1, round(b * G / 100)) groups."""
@@ -61,6 +64,15 @@ class GreenPartitions:
             s = C.c_void_p()
             _abi.check(_abi.lib.fedhc_gctx_stream(self._pool, first, count, C.byref(s), None))
             self._streams[key] = s.value
+        return self._streams[key]
+
+    def stream_rest(self, first: int, count: int) -> tuple[int, int]:
+        """(stream, SM count) of a window of `count` groups plus the SMs outside every group."""
+        key = (first, -1 - count)
+        if key not in self._streams:
+            s, n = C.c_void_p(), C.c_int()
+            _abi.check(_abi.lib.fedhc_gctx_stream_rest(self._pool, first, count, C.byref(s), C.byref(n)))
+            self._streams[key] = (s.value, n.value)
         return self._streams[key]
 
     def acquire(self, budget: float) -> tuple[int, int, int]:
@@ -154,9 +166,8 @@ class LiveRound:
                                                                 params, meta[i][2], self.lr, use_graph=False,
                                                                 stream=s)
                 else:
-                    _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr() + i * CLIENT_DTYPE.itemsize, 1,
-                                                          params.data_ptr(), fed.n_features, fed.n_classes,
-                                                          wls[i].batch_size, s))
+                    fed.launch_train(d_desc.data_ptr() + i * CLIENT_DTYPE.itemsize, 1, params, wls[i].batch_size,
+                                     stream=s)
                 ev1.record(ext)
                 running[cid] = (ev0, ev1, entry.executor_id)
                 trace.append({"t": clock(), "kind": "ClientLaunched", "client": cid, "executor": entry.executor_id,

@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -195,6 +196,32 @@ def count_correct(x: torch.Tensor, y: torch.Tensor, params: torch.Tensor, n_clas
     return int(correct.item())
 
 
+def split_supported(n_features: int, n_classes: int) -> bool:
+    """Shapes whose trainer reads the fedhc_x_split row copy (train_pipe_kernel<true>: F = 784, C <= 16).
+    FEDHC_X_SPLIT=0 keeps every launch on the fp32 rows (A/B measurements)."""
+    return n_features == 784 and n_classes <= 16 and os.environ.get("FEDHC_X_SPLIT", "1") != "0"
+
+
+def x_split(x: torch.Tensor) -> torch.Tensor:
+    """The rows of x (fp32 [n, F], device) re-encoded as [F bf16 hi | F bf16 mid] per row: same bytes, so the
+    copy is returned as an opaque fp32-typed tensor of x's shape (fedhc_x_split)."""
+    out = torch.empty_like(x)
+    _abi.check(_abi.lib.fedhc_x_split(x.data_ptr(), int(x.shape[0]), int(x.shape[1]), out.data_ptr(), stream_ptr()))
+    return out
+
+
+def train_launch(desc_ptr: int, k: int, params_ptr: int, n_features: int, n_classes: int, max_batch: int,
+                 x: torch.Tensor | None = None, xs: torch.Tensor | None = None, stream: int | None = None) -> None:
+    """One fedhc_local_train launch for k device descriptors; with a split copy xs of the rows x the
+    descriptors point into, the launch reads the copy where a kernel for it exists (bit-identical results)."""
+    st = stream_ptr() if stream is None else stream
+    if xs is not None:
+        _abi.check(_abi.lib.fedhc_local_train_split(desc_ptr, k, params_ptr, n_features, n_classes, max_batch,
+                                                    xs.data_ptr() - x.data_ptr(), st))
+    else:
+        _abi.check(_abi.lib.fedhc_local_train(desc_ptr, k, params_ptr, n_features, n_classes, max_batch, st))
+
+
 def local_train(params: np.ndarray, shard: DatasetShard, workload, lr: float, n_classes: int,
                 seed: int | str = 0) -> np.ndarray:
     """Mini-batch SGD on one client's shard; returns the delta (fl_core.py:163-194)."""
@@ -211,8 +238,8 @@ def local_train(params: np.ndarray, shard: DatasetShard, workload, lr: float, n_
                                          math.ceil(workload.num_samples / workload.batch_size),
                                          workload.batch_size, float(lr), delta.data_ptr()))
     d_desc = descriptors_to_device(desc)
-    _abi.check(_abi.lib.fedhc_local_train(d_desc.data_ptr(), 1, p.data_ptr(), n_features, n_classes,
-                                          workload.batch_size, stream_ptr()))
+    xs = x_split(x) if split_supported(n_features, n_classes) else None
+    train_launch(d_desc.data_ptr(), 1, p.data_ptr(), n_features, n_classes, workload.batch_size, x, xs)
     return delta.cpu().numpy().astype(np.float64)
 
 

@@ -275,6 +275,59 @@ def test_batched_round_matches_per_client(fh, tr, C):
             assert rel_err(deltas[i], want) <= REL
 
 
+def test_x_split_layout(fh):
+    """fedhc_x_split: each row -> [F bf16 hi | F bf16 mid], hi = bf16_rn(x), mid = bf16_rn(x - hi)."""
+    import torch
+    from paper_2305_15668_b200.training import x_split
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(37, 784, device="cuda", generator=g) * 3
+    x[0, :4] = torch.tensor([0.0, -0.0, 1e-30, -7.5e5])
+    got = x_split(x).view(torch.int16).view(37, 2, 784)
+    hi = x.to(torch.bfloat16)
+    mid = (x - hi.float()).to(torch.bfloat16)
+    assert torch.equal(got[:, 0], hi.view(torch.int16)) and torch.equal(got[:, 1], mid.view(torch.int16))
+
+
+@pytest.mark.parametrize("sizes,b,lr", [
+    ([640, 700, 0, 64, 1000, 333], 64, 0.1),   # ragged batches, reshuffles, an empty shard
+    ([100, 17, 256], 16, 0.05),                 # one stage per batch, partial stages
+    ([90, 1], 1, 0.1),                          # batch of one row
+])
+def test_split_rows_bit_identical(fh, tr, sizes, b, lr):
+    """train_pipe_kernel reading the fedhc_x_split copy (ldmatrix fragments) == reading fp32 rows and splitting
+    in registers, bit for bit (same products, same accumulation order)."""
+    import torch
+    from paper_2305_15668_b200 import _abi
+    from paper_2305_15668_b200.experiment import DeviceFederation, delta_buffer
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    from paper_2305_15668_b200.training import stream_ptr
+    C = 10
+    trn, tst = fm.synthetic(784, C, sum(sizes) + 10, seed=5)
+    shards, at = {}, 0
+    for i, n in enumerate(sizes):
+        shards[f"c{i}"] = tr.DatasetShard(f"c{i}", trn.features[at:at + n], trn.labels[at:at + n])
+        at += n
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, C), 784, C)
+    assert fed.x_split is not None
+    params = torch.from_numpy(np.random.default_rng(4).standard_normal(784 * C + C) * 0.01).cuda()
+    wl = [WorkloadSpec(n if n else 10, b) for n in sizes]
+    seeds = [fm.seed_of("train", 1, 0, f"c{i}") for i in range(len(sizes))]
+    ids = list(shards)
+    meta, _ = fed.stage_plan(ids, wl, seeds)
+    d_split, d_f32 = delta_buffer(len(ids), fed.P, "cuda"), delta_buffer(len(ids), fed.P, "cuda")
+    desc_a = fed.descriptors(ids, meta, lr, d_split)
+    desc_b = fed.descriptors(ids, meta, lr, d_f32)
+    fed.launch_train(desc_a.data_ptr(), len(ids), params, b)
+    _abi.check(_abi.lib.fedhc_local_train(desc_b.data_ptr(), len(ids), params.data_ptr(), 784, C, b, stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(d_split, d_f32)
+    for i, cid in enumerate(ids):
+        if sizes[i]:
+            want = fm.local_sgd(params.cpu().numpy(), fm.Shard(cid, shards[cid].features, shards[cid].labels),
+                                wl[i].num_samples, b, lr, C, seed=seeds[i])
+            assert rel_err(d_split[i, :fed.P].cpu().numpy(), want) <= REL
+
+
 def test_full_size_round_properties(fh):
     """Bench-size round (100 clients x 6400 x 784): finite deltas, determinism, FedAvg linearity."""
     import torch
@@ -544,6 +597,40 @@ def test_device_permutations_match_numpy(fh):
     for s, n, k, o in zip(seeds, rows, perms, offs):
         g = np.random.default_rng(s)
         assert np.array_equal(got[o:o + n * k], np.concatenate([g.permutation(n) for _ in range(k)]))
+
+
+@pytest.mark.parametrize("legacy", [False, True])
+def test_device_permutations_sizes_sweep(fh, legacy, monkeypatch):
+    """perm_fast_kernel (parallel acceptance scan + bucket chains) and the sequential walk vs numpy, at sizes
+    around powers of two (mask changes), tiny shards and several permutations per client."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch
+from paper_2305_15668_b200 import _abi
+rng = np.random.default_rng(11)
+rows = [1, 2, 3, 31, 32, 33, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 4095, 4096, 4097, 6400, 8191, 5000]
+perms = [int(rng.integers(1, 4)) for _ in rows]
+seeds = [int(x) for x in rng.integers(0, 2**32, len(rows))]
+sizes = np.array(rows, np.int64) * np.array(perms, np.int64)
+offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+dev = lambda a, t: torch.from_numpy(np.ascontiguousarray(a, dtype=t)).cuda()
+s_d, r_d, p_d, o_d = dev(seeds, np.uint64), dev(rows, np.int32), dev(perms, np.int32), dev(offs, np.int64)
+out = torch.full((int(sizes.sum()),), -1, dtype=torch.int32, device="cuda")
+_abi.check(_abi.lib.fedhc_batch_permutations_device(s_d.data_ptr(), r_d.data_ptr(), p_d.data_ptr(), o_d.data_ptr(),
+           len(seeds), out.data_ptr(), 6400, torch.cuda.current_stream().cuda_stream))
+got = out.cpu().numpy()
+for s, n, k, o in zip(seeds, rows, perms, offs):
+    g = np.random.default_rng(s)
+    assert np.array_equal(got[o:o + n * k], np.concatenate([g.permutation(n) for _ in range(k)])), (n, k)
+print("ok")
+"""
+    env = dict(os.environ)
+    if legacy:
+        env["FEDHC_PERM_LEGACY"] = "1"
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
 
 
 def test_runner_device_plan_matches_host_plan(fh):
