@@ -254,6 +254,78 @@ int fedhc_des_run_round(fedhc_des* sim, const fedhc_des_client* clients, const c
 int fedhc_des_trace(const fedhc_des* sim, const fedhc_des_event** events, const int32_t** alloc_client,
                     const double** alloc_share, const double** par_t, const int32_t** par_n, int* n_par);
 
+/* ---- native single-GPU round loop (FederatedRunner's serving loop) ------- */
+/* Two GIL-free calls per round replace the Python planning / launch path:
+ *   fedhc_runner_plan   selection (engine.py:327) -> DES (engine.py:53-230) -> seeds, descriptors,
+ *                       coefficients and batch-order block into slot `slot`'s pinned block -> on the plan
+ *                       stream: one H2D copy + the device PCG64 permutations (fl_core.py:181-187);
+ *   fedhc_runner_launch wait for the plan -> local_train of all participants (fl_core.py:163-194) ->
+ *                       sync FedAvg (fl_core.py:197-218, engine.py:350-353) on `stream` -> accuracy
+ *                       (fl_core.py:154-160) on the eval stream, overlapping the next round's training;
+ *   fedhc_runner_result waits for the slot's accuracy count.
+ * Every pointer in the config is borrowed and must outlive the runner. */
+typedef struct fedhc_runner fedhc_runner;
+typedef struct fedhc_runner_config {
+  /* per fleet client, indexed like the sorted client ids */
+  const char* const* reprs;       /* repr(client_id), the stable_seed key                    */
+  const int32_t* rows;            /* shard length                                            */
+  const int32_t* n_perms;         /* permutations local_train draws                          */
+  const int32_t* n_batches;       /* ceil(num_samples / batch_size)                          */
+  const int32_t* batch_size;
+  const uint64_t* xptr;           /* device address of the client's rows / labels            */
+  const uint64_t* yptr;
+  const double* weight;           /* float(num_samples) (engine.py:348)                      */
+  const uint8_t* over_theta;      /* budget > theta: the round must take the raising path    */
+  const int32_t* sim_index;       /* DES client index                                        */
+  uint32_t* mt_state;             /* the selector's MT19937 state (625 words), updated       */
+  fedhc_des* sim;                 /* DES handle, client table and ids (fedhc_des_*)          */
+  const fedhc_des_client* des_clients;
+  const char* const* des_ids;
+  /* device side */
+  double* params;                 /* dev fp64 [P], updated in place by FedAvg               */
+  float* deltas;                  /* dev fp32 [participants, ld]                             */
+  int64_t delta_stride_bytes;     /* 4 * ld                                                  */
+  int64_t split_offset;           /* fedhc_local_train_split offset (split != 0)             */
+  const float* x_test;
+  const int32_t* y_test;
+  int64_t n_test;
+  unsigned long long* correct_dev;   /* dev [slots]                                          */
+  unsigned long long* correct_host;  /* pinned host [slots]                                  */
+  uint8_t* const* stage_host;     /* [slots] pinned blocks, participants * (24 + 48 + 8) B   */
+  uint8_t* const* stage_dev;      /* [slots] device copies                                   */
+  int32_t* const* plan_dev;       /* [slots] device permutation buffers                      */
+  int64_t plan_cap_words;
+  void* plan_stream;
+  void* eval_stream;
+  int64_t seed;
+  double pad_d_;
+  fedhc_des_config des_cfg;
+  float lr;
+  int32_t n_fleet, participants, slots, n_features, n_classes, max_batch, split, eval_ctas, rows_max;
+} fedhc_runner_config;
+
+typedef struct fedhc_runner_plan_info {
+  /* caller-provided host arrays */
+  int32_t* selected;              /* [participants] fleet indices, selection order           */
+  double* starts;                 /* [participants] DES launch / upload times                 */
+  double* ends;
+  int32_t* launch_order;          /* [participants] participant indices in event order       */
+  int32_t* upload_order;
+  double* par_t;                  /* [par_cap] parallelism timeline                          */
+  int32_t* par_n;
+  int32_t par_cap;
+  /* outputs */
+  int32_t n_launched, n_uploaded, n_par, over_theta, degenerate, max_rows;
+  double makespan, utilization, vacancy_area, throughput, total_weight;
+  int64_t perm_words, h2d_bytes;
+} fedhc_runner_plan_info;
+
+int fedhc_runner_create(const fedhc_runner_config* cfg, fedhc_runner** out);
+void fedhc_runner_destroy(fedhc_runner* runner);
+int fedhc_runner_plan(fedhc_runner* runner, int64_t round_index, double t0, int slot, fedhc_runner_plan_info* info);
+int fedhc_runner_launch(fedhc_runner* runner, int slot, void* stream);
+int fedhc_runner_result(fedhc_runner* runner, int slot, int64_t* correct);
+
 /* ---- tcgen05 grouped GEMM (client-model contractions) -------------------- */
 /* D_g[M x N] (fp32) = A_g[M x K] (bf16, row-major) . B_g[N x K]^T (bf16,
  * row-major) for g in [0, G): one launch for all clients of a round.

@@ -91,6 +91,38 @@ class DesReport(C.Structure):
     ]
 
 
+class RunnerConfig(C.Structure):
+    """fedhc_runner_config (include/fedhc.h)."""
+    _fields_ = [
+        ("reprs", C.c_void_p), ("rows", C.c_void_p), ("n_perms", C.c_void_p), ("n_batches", C.c_void_p),
+        ("batch_size", C.c_void_p), ("xptr", C.c_void_p), ("yptr", C.c_void_p), ("weight", C.c_void_p),
+        ("over_theta", C.c_void_p), ("sim_index", C.c_void_p), ("mt_state", C.c_void_p), ("sim", C.c_void_p),
+        ("des_clients", C.c_void_p), ("des_ids", C.c_void_p),
+        ("params", C.c_void_p), ("deltas", C.c_void_p), ("delta_stride_bytes", C.c_int64),
+        ("split_offset", C.c_int64), ("x_test", C.c_void_p), ("y_test", C.c_void_p), ("n_test", C.c_int64),
+        ("correct_dev", C.c_void_p), ("correct_host", C.c_void_p), ("stage_host", C.c_void_p),
+        ("stage_dev", C.c_void_p), ("plan_dev", C.c_void_p), ("plan_cap_words", C.c_int64),
+        ("plan_stream", C.c_void_p), ("eval_stream", C.c_void_p), ("seed", C.c_int64), ("pad_d_", C.c_double),
+        ("des_cfg", DesConfig), ("lr", C.c_float),
+        ("n_fleet", C.c_int32), ("participants", C.c_int32), ("slots", C.c_int32), ("n_features", C.c_int32),
+        ("n_classes", C.c_int32), ("max_batch", C.c_int32), ("split", C.c_int32), ("eval_ctas", C.c_int32),
+        ("rows_max", C.c_int32),
+    ]
+
+
+class RunnerPlanInfo(C.Structure):
+    """fedhc_runner_plan_info (include/fedhc.h)."""
+    _fields_ = [
+        ("selected", C.c_void_p), ("starts", C.c_void_p), ("ends", C.c_void_p), ("launch_order", C.c_void_p),
+        ("upload_order", C.c_void_p), ("par_t", C.c_void_p), ("par_n", C.c_void_p), ("par_cap", C.c_int32),
+        ("n_launched", C.c_int32), ("n_uploaded", C.c_int32), ("n_par", C.c_int32), ("over_theta", C.c_int32),
+        ("degenerate", C.c_int32), ("max_rows", C.c_int32),
+        ("makespan", C.c_double), ("utilization", C.c_double), ("vacancy_area", C.c_double),
+        ("throughput", C.c_double), ("total_weight", C.c_double), ("perm_words", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+    ]
+
+
 class GemmArgs(C.Structure):
     _fields_ = [
         ("G", C.c_int32), ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32),
@@ -115,6 +147,11 @@ SIGNATURES = {
     "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
     "fedhc_x_split": (_i, [_vp, _i64, _i, _vp, _vp]),
+    "fedhc_runner_create": (_i, [_vp, _vp]),
+    "fedhc_runner_destroy": (None, [_vp]),
+    "fedhc_runner_plan": (_i, [_vp, _i64, _d, _i, _vp]),
+    "fedhc_runner_launch": (_i, [_vp, _i, _vp]),
+    "fedhc_runner_result": (_i, [_vp, _i, _vp]),
     "fedhc_local_train_split": (_i, [_vp, _i, _vp, _i, _i, _i, _i64, _vp]),
     "fedhc_tc_trace_read": (_i, [_vp]),
     "fedhc_mt_sample": (_i, [_vp, _i, _i, _vp]),

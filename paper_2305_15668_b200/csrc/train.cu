@@ -169,6 +169,13 @@ extern "C" int fedhc_x_split(const float* x, int64_t n_rows, int n_features, voi
 static int local_train_impl(const fedhc_client* clients, int n_clients, const double* params, int n_features,
                             int n_classes, int max_batch, bool split, int64_t split_off, void* stream);
 
+namespace fedhc {
+int local_train_entry(const fedhc_client* clients, int n_clients, const double* params, int n_features, int n_classes,
+                      int max_batch, bool split, int64_t split_off, void* stream) {
+  return local_train_impl(clients, n_clients, params, n_features, n_classes, max_batch, split, split_off, stream);
+}
+}  // namespace fedhc
+
 extern "C" int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* params, int n_features,
                                  int n_classes, int max_batch, void* stream) {
   return local_train_impl(clients, n_clients, params, n_features, n_classes, max_batch, false, 0, stream);

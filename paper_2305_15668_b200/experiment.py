@@ -30,7 +30,7 @@ import torch
 
 from . import _abi
 from .errors import AggregationError, ConfigError
-from .roundsim import RoundReport, RoundSimulator
+from .roundsim import LeanRoundReport, RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
 from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
                        init_params, make_synthetic_dataset, n_permutations, native_permutations, partition_noniid,
@@ -371,7 +371,7 @@ class FederatedRunner:
     def __init__(self, fed: DeviceFederation, fleet: dict[str, ClientProfile], cfg: FleetConfig, lr: float,
                  params: torch.Tensor | None = None, world: int = 1, rank: int = 0, group=None,
                  plan_threads: int = 0, device_permutations: bool = True, use_graphs: bool = False,
-                 green_side: bool = True, test_sharded: bool = False):
+                 green_side: bool = True, test_sharded: bool = False, native: bool = True):
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
@@ -441,13 +441,21 @@ class FederatedRunner:
                 need = -(-k_max // gp.sms_per_group)  # groups the training needs (one SM per client)
                 spare = gp.n_groups - need
                 if spare >= 1:
-                    # permutations: the SMs outside every group (+ all spare groups but one); accuracy: one group
-                    self._green = gp
+                    # permutations: the SMs outside every group (28 of 148 on a B200: ~0.4 ms for 100 clients
+                    # of 6400 rows); accuracy: the spare groups (2 x 8 SMs)
+                    eval_first, eval_n = need, spare
                     if device_permutations:
-                        raw, _ = gp.stream_rest(need, spare - 1)
+                        try:
+                            raw, _ = gp.stream_rest(need, 0)
+                        except ValueError:  # every SM is in a group: give the permutations one spare group
+                            if spare < 2:
+                                raise
+                            raw = gp.stream(need, 1)
+                            eval_first, eval_n = need + 1, spare - 1
                         self._plan_stream = torch.cuda.ExternalStream(raw, device=dev)
-                    self._eval_stream_raw = gp.stream(gp.n_groups - 1, 1)
-                    self._eval_ctas = gp.sms_per_group  # one CTA per SM of the window
+                    self._eval_stream_raw = gp.stream(eval_first, eval_n)
+                    self._eval_ctas = eval_n * gp.sms_per_group  # one CTA per SM of the window
+                    self._green = gp
             except Exception:  # no green-context support in this driver: keep the ordinary streams
                 self._green = None
         self._train_done = [None] * n   # event: the slot's train kernel retired (plan buffer reusable)
@@ -504,6 +512,168 @@ class FederatedRunner:
         self.h2d_bytes = 0
         self.d2h_bytes = 8
         self.host_s = {"select+des": 0.0, "seeds": 0.0, "permutations": 0.0, "descriptors": 0.0, "launch": 0.0}
+        # native round loop (single GPU, device batch order, eager launches): plan / launch / result are one
+        # GIL-free libfedhc call each (fedhc_runner_*); the Python path below stays for world > 1 and graphs
+        self._native = None
+        if native and world == 1 and device_permutations and not self.use_graphs:
+            self._native_init(k_max)
+
+    def _native_init(self, k_max: int) -> None:
+        fed, cfg, n = self.fed, self.cfg, self.SLOTS
+        dev = self.dev
+        kp = cfg.participants_per_round
+        # plan buffers sized for the kp largest shards (no reallocation inside the loop)
+        words = np.sort(self._c_rows * self._c_nperm)[::-1][:kp].sum() if kp else 0
+        cap = max(int(words), 1)
+        self._n_plan = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(n)]
+        blk = max(kp, 1) * (24 + CLIENT_DTYPE.itemsize + 8)
+        self._n_stage_pin = [torch.empty(blk, dtype=torch.uint8).pin_memory() for _ in range(n)]
+        self._n_stage_dev = [torch.empty(blk, dtype=torch.uint8, device=dev) for _ in range(n)]
+        self._n_correct_dev = torch.zeros(n, dtype=torch.int64, device=dev)
+        self._n_correct_pin = torch.zeros(n, dtype=torch.int64).pin_memory()
+        ptrs = lambda ts: np.array([t.data_ptr() for t in ts], dtype=np.uint64)  # noqa: E731
+        self._n_keep = [ptrs(self._n_stage_pin), ptrs(self._n_stage_dev), ptrs(self._n_plan),
+                        np.ascontiguousarray(self._over_theta.astype(np.uint8)),
+                        np.ascontiguousarray(self._sim_idx.astype(np.int32)), np.ascontiguousarray(self._c_w)]
+        sp, sd, pd, ot, si, w = self._n_keep
+        sim = self.sim
+        des = _abi.DesConfig(float(cfg.theta), int(cfg.max_executors), 0 if cfg.scheduler_kind == "resource-aware"
+                             else 1, int(bool(cfg.dynamic_parallelism)), float(cfg.alpha), float(cfg.beta),
+                             float(cfg.launch_latency), float(cfg.terminate_latency), float(cfg.upload_latency))
+        if cfg.scheduler_kind not in ("resource-aware", "greedy"):
+            raise KeyError(cfg.scheduler_kind)
+        xs = fed.x_split
+        c = _abi.RunnerConfig()
+        c.reprs, c.rows, c.n_perms = self._repr_ptr.ctypes.data, self._c_rows32.ctypes.data, self._c_nperm32.ctypes.data
+        c.n_batches, c.batch_size = self._c_steps32.ctypes.data, self._c_bs32.ctypes.data
+        c.xptr, c.yptr, c.weight = self._c_xptr.ctypes.data, self._c_yptr.ctypes.data, w.ctypes.data
+        c.over_theta, c.sim_index, c.mt_state = ot.ctypes.data, si.ctypes.data, self._mt.ctypes.data
+        c.sim = sim._sim
+        c.des_clients = C.cast(sim._clients, C.c_void_p).value
+        c.des_ids = C.cast(sim._id_arr, C.c_void_p).value
+        c.params, c.deltas = self.params.data_ptr(), self.deltas.data_ptr()
+        c.delta_stride_bytes = self.deltas.stride(0) * 4
+        c.split_offset = (xs.data_ptr() - fed.x.data_ptr()) if xs is not None else 0
+        c.x_test, c.y_test, c.n_test = self._xt.data_ptr(), self._yt.data_ptr(), int(self._nt)
+        c.correct_dev, c.correct_host = self._n_correct_dev.data_ptr(), self._n_correct_pin.data_ptr()
+        c.stage_host, c.stage_dev, c.plan_dev = sp.ctypes.data, sd.ctypes.data, pd.ctypes.data
+        c.plan_cap_words = cap
+        c.plan_stream, c.eval_stream = self._plan_stream.cuda_stream, self._eval_stream.cuda_stream
+        c.seed, c.des_cfg, c.lr = int(cfg.seed), des, self.lr
+        c.n_fleet, c.participants, c.slots = len(self.ids), kp, n
+        c.n_features, c.n_classes, c.max_batch = fed.n_features, fed.n_classes, self._bs_max
+        c.split = 1 if xs is not None else 0
+        c.eval_ctas = self._eval_ctas if self._eval_ctas is not None else max(8, self._sms - kp)
+        c.rows_max = self._rows_max
+        self._n_cfg = c
+        h = C.c_void_p()
+        _abi.check(_abi.lib.fedhc_runner_create(C.byref(c), C.byref(h)))
+        self._native = h
+        # per-slot host outputs of fedhc_runner_plan
+        kq = max(kp, 1)
+        self._n_out = []
+        for _ in range(n):
+            o = {"selected": np.zeros(kq, np.int32), "starts": np.zeros(kq), "ends": np.zeros(kq),
+                 "launch": np.zeros(kq, np.int32), "upload": np.zeros(kq, np.int32),
+                 "par_t": np.zeros(4 * kq + 16), "par_n": np.zeros(4 * kq + 16, np.int32)}
+            info = _abi.RunnerPlanInfo()
+            info.selected, info.starts, info.ends = (o["selected"].ctypes.data, o["starts"].ctypes.data,
+                                                     o["ends"].ctypes.data)
+            info.launch_order, info.upload_order = o["launch"].ctypes.data, o["upload"].ctypes.data
+            info.par_t, info.par_n, info.par_cap = o["par_t"].ctypes.data, o["par_n"].ctypes.data, 4 * kq + 16
+            o["info"] = info
+            self._n_out.append(o)
+
+    def __del__(self):
+        h = getattr(self, "_native", None)
+        if h:
+            _abi.lib.fedhc_runner_destroy(h)
+            self._native = None
+
+    def _native_plan(self, r: int, t0: float, slot: int) -> RoundPlan:
+        """fedhc_runner_plan (selection, DES, packing, H2D + device batch order) -> RoundPlan."""
+        tick = time.perf_counter()
+        o = self._n_out[slot]
+        info = o["info"]
+        _abi.check(_abi.lib.fedhc_runner_plan(self._native, int(r), float(t0), slot, C.byref(info)))
+        kp = self.cfg.participants_per_round
+        who = [self.ids[i] for i in o["selected"][:kp].tolist()]
+        if info.over_theta:  # the reference's ConfigError, from the same selection
+            self.sim.run(who, self.cfg, t0=t0, round_index=r, want_trace=False)
+        npar = info.n_par
+        if npar < 0:
+            raise RuntimeError("runner: parallelism timeline buffer too small")
+        rep = LeanRoundReport(r, info.makespan, info.utilization, info.vacancy_area, info.throughput,
+                              bool(info.degenerate), who, o["launch"][:info.n_launched].copy(),
+                              o["upload"][:info.n_uploaded].copy(), o["starts"][:kp].copy(), o["ends"][:kp].copy(),
+                              o["par_t"][:npar].copy() if npar else None,
+                              o["par_n"][:npar].copy() if npar else None, self.sim.budget)
+        self.h2d_bytes = int(info.h2d_bytes)
+        self.host_s["select+des"] += time.perf_counter() - tick
+        return RoundPlan(r, who, who, rep, t0, [], np.zeros(0), slot, int(info.perm_words), None,
+                         24 * kp, int(info.max_rows), plan_launched=True)
+
+    def _native_run(self, rounds: int, n_test: int, on_round) -> list:
+        """run() on the native loop: a planner thread (fedhc_runner_plan) feeding the launching thread."""
+        import queue
+        import threading
+
+        ready: queue.Queue = queue.Queue(maxsize=self.SLOTS - 1)
+        free: queue.Queue = queue.Queue()
+        for sl in range(self.SLOTS):
+            free.put(sl)
+        failure = []
+        t_start, r0 = self.now, self.round
+
+        def planner():
+            t = t_start
+            try:
+                torch.cuda.set_device(self.dev)
+                for i in range(rounds):
+                    pl = self._native_plan(r0 + i, t, free.get())
+                    t = pl.t0 + pl.report.makespan
+                    ready.put(pl)
+            except BaseException as exc:  # surface planner errors in the caller
+                failure.append(exc)
+                ready.put(None)
+
+        th = threading.Thread(target=planner, daemon=True)
+        th.start()
+        series, pending = [], None
+        hs = self.host_s
+        stream = torch.cuda.current_stream().cuda_stream
+        correct = C.c_int64()
+        try:
+            for _ in range(rounds):
+                t0 = time.perf_counter()
+                p = ready.get()
+                hs["wait_plan"] = hs.get("wait_plan", 0.0) + time.perf_counter() - t0
+                if p is None:
+                    raise failure[0]
+                t1 = time.perf_counter()
+                _abi.check(_abi.lib.fedhc_runner_launch(self._native, p.slot, stream))
+                hs["launch"] += time.perf_counter() - t1
+                if pending is not None:
+                    t0 = time.perf_counter()
+                    _abi.check(_abi.lib.fedhc_runner_result(self._native, pending.slot, C.byref(correct)))
+                    free.put(pending.slot)
+                    hs["wait_gpu"] = hs.get("wait_gpu", 0.0) + time.perf_counter() - t0
+                    series.append(self._native_finish(pending, correct.value, n_test, on_round))
+                pending = p
+            _abi.check(_abi.lib.fedhc_runner_result(self._native, pending.slot, C.byref(correct)))
+            free.put(pending.slot)
+            series.append(self._native_finish(pending, correct.value, n_test, on_round))
+        finally:
+            th.join()
+        self.round += rounds
+        self.now = series[-1][0]
+        return series
+
+    def _native_finish(self, p: RoundPlan, correct: int, n_test: int, on_round) -> tuple[float, float]:
+        acc = correct / n_test if n_test else 0.0
+        if on_round is not None:
+            on_round(p, acc)
+        return (p.t0 + p.report.makespan, acc)
 
     # ---- host side ---------------------------------------------------------
     def _ensure(self, slot: int, words: int):
@@ -826,6 +996,8 @@ class FederatedRunner:
         n_test = n_test_total
         if rounds <= 0:
             return []
+        if self._native is not None:
+            return self._native_run(rounds, n_test, on_round)
         ready: queue.Queue = queue.Queue(maxsize=self.SLOTS - 1)
         free: queue.Queue = queue.Queue()
         # the previous call planned this call's first round while its last round drained (no pipeline fill)

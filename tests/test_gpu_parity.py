@@ -646,11 +646,14 @@ def test_runner_device_plan_matches_host_plan(fh):
     data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, 10, 0.5, seed=3, n_test=2000)
     cfg = fh.FleetConfig(participants_per_round=16, max_executors=8, seed=9)
     outs = []
-    # host plan, device plan (eager launches, the default), device plan replayed from per-slot CUDA graphs
-    for device_perm, graphs in ((False, False), (True, False), (True, True)):
+    # host plan, device plan (native round loop, the default), device plan through the Python launch path,
+    # device plan replayed from per-slot CUDA graphs
+    for device_perm, graphs, native in ((False, False, False), (True, False, True), (True, False, False),
+                                        (True, True, False)):
         params = torch.zeros(7850, dtype=torch.float64, device="cuda")
         r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, device_permutations=device_perm,
-                            use_graphs=graphs)
+                            use_graphs=graphs, native=native)
+        assert (r._native is not None) == native
         series = r.run(4)
         outs.append((params.clone(), series))
     # the same 4 rounds as run(1) + run(3): each call plans the next call's first round while draining
