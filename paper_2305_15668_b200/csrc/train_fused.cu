@@ -968,6 +968,416 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
+// ============================================================================
+// v5: the split-row kernel with the work balanced over the four SM sub-partitions (SMSPs).
+// v4 runs 14 compute warps (7 k8 feature slices each) + producer + softmax warp: warps w and w + 4 share an
+// SMSP, so SMSPs 0 / 1 carry 4 compute warps (28 slices of HMMA work per stage) and SMSPs 2 / 3 three;
+// ncu: the busiest SMSPs issue ~1.3x the average, and every stage waits for them.  v5 runs 12 compute
+// warps, 8 or 9 slices each (98 = 10 x 8 + 2 x 9), i.e. 24 / 24 / 24 / 26 slices per SMSP, plus the
+// producer and TWO softmax warps (rows 0-7 / 8-15: half the partial-Z loads and softmax latency per warp).
+// Same math (bf16x3 products, fp32 accumulation), different summation grouping than v4.
+// ============================================================================
+constexpr int kQWarps = 12, kQProd = 12, kQSoft0 = 13, kQThreads = 15 * 32;
+constexpr int kQSync = (kQWarps + 2) * 32;  // named-barrier participants: compute + softmax warps
+
+__device__ __forceinline__ int q_slices(int w) { return (w == 3 || w == 7) ? 9 : 8; }
+__device__ __forceinline__ int q_first(int w) { return 8 * w + (w > 3) + (w > 7); }
+
+struct Pipe2Geom {
+  int Fs, Zs;
+  int off_x, off_zp, off_e, off_lab, off_bar, off_gb, off_tmem, bytes;
+};
+
+static bool plan_pipe2(int F, int C, int max_smem, Pipe2Geom& g) {
+  if (F != 784 || C > 16) return false;
+  g.Fs = F + 4;  // 3152-byte rows: 8 consecutive rows hit 8 distinct 16-byte bank groups (ldmatrix)
+  g.Zs = 20;
+  int off = 0;
+  g.off_x = off;    off = a16(off + kPStages * kFRows * g.Fs * 4);
+  g.off_zp = off;   off = a16(off + kQWarps * kFRows * g.Zs * 4);
+  g.off_e = off;    off = a16(off + 2 * 2 * kFRows * kPEPitch);
+  g.off_lab = off;  off = a16(off + kPStages * kFRows * 4);
+  g.off_bar = off;  off = a16(off + 2 * kPStages * 8);
+  g.off_gb = off;   off = a16(off + 2 * 16 * 4);  // the two softmax warps' bias-gradient halves
+  g.off_tmem = off; off = a16(off + 16);
+  g.bytes = off;
+  return off <= max_smem;
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const float (&m)[N]) {
+  static_assert(N == 32 || N == 36, "8 or 9 slices");
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(m[0]), "f"(m[1]), "f"(m[2]), "f"(m[3]), "f"(m[4]), "f"(m[5]), "f"(m[6]), "f"(m[7]), "f"(m[8]),
+      "f"(m[9]), "f"(m[10]), "f"(m[11]), "f"(m[12]), "f"(m[13]), "f"(m[14]), "f"(m[15]), "f"(m[16]), "f"(m[17]),
+      "f"(m[18]), "f"(m[19]), "f"(m[20]), "f"(m[21]), "f"(m[22]), "f"(m[23]), "f"(m[24]), "f"(m[25]), "f"(m[26]),
+      "f"(m[27]), "f"(m[28]), "f"(m[29]), "f"(m[30]), "f"(m[31])
+      : "memory");
+  if constexpr (N == 36)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + 32), "f"(m[32]),
+                 "f"(m[33]), "f"(m[34]), "f"(m[35])
+                 : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float (&m)[N]) {
+  static_assert(N == 32 || N == 36, "8 or 9 slices");
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=f"(m[0]), "=f"(m[1]), "=f"(m[2]), "=f"(m[3]), "=f"(m[4]), "=f"(m[5]), "=f"(m[6]), "=f"(m[7]),
+        "=f"(m[8]), "=f"(m[9]), "=f"(m[10]), "=f"(m[11]), "=f"(m[12]), "=f"(m[13]), "=f"(m[14]), "=f"(m[15]),
+        "=f"(m[16]), "=f"(m[17]), "=f"(m[18]), "=f"(m[19]), "=f"(m[20]), "=f"(m[21]), "=f"(m[22]), "=f"(m[23]),
+        "=f"(m[24]), "=f"(m[25]), "=f"(m[26]), "=f"(m[27]), "=f"(m[28]), "=f"(m[29]), "=f"(m[30]), "=f"(m[31])
+      : "r"(taddr)
+      : "memory");
+  if constexpr (N == 36)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(m[32]), "=f"(m[33]), "=f"(m[34]), "=f"(m[35])
+                 : "r"(taddr + 32)
+                 : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct Pipe2Ctx {
+  const fedhc_client* cl;
+  const double* params;
+  float* Zp;
+  uint64_t* full;
+  uint64_t* empty;
+  uint32_t x_base, e_base, tmem_w;
+  int F, C, Fs, Zs, steps;
+};
+
+// One compute warp's whole local-SGD loop: NK k8 feature slices starting at slice s0.
+template <int NK>
+__device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int lane) {
+  constexpr int S = kPStages;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int s0 = q_first(warp);
+  const int F = x.F, C = x.C, FC = F * C;
+  const fedhc_client& cl = *x.cl;
+  auto w_at = [&](int f, int c) -> float { return c < C ? static_cast<float>(x.params[(size_t)f * C + c]) : 0.f; };
+  uint32_t wh[NK][2], wm[NK][2];
+  float G[NK][4];
+  {
+    float m0[4 * NK];
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+      const int f0 = 8 * (s0 + j) + 2 * tq;
+      m0[4 * j] = w_at(f0, gq);
+      m0[4 * j + 1] = w_at(f0 + 1, gq);
+      m0[4 * j + 2] = w_at(f0, gq + 8);
+      m0[4 * j + 3] = w_at(f0 + 1, gq + 8);
+      split_bf16x2(m0[4 * j], m0[4 * j + 1], wh[j][0], wm[j][0]);
+      split_bf16x2(m0[4 * j + 2], m0[4 * j + 3], wh[j][1], wm[j][1]);
+      G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
+    }
+    tmem_st_n<4 * NK>(x.tmem_w, m0);
+  }
+  __syncwarp();
+  const uint32_t x_lane = x.x_base + ((lane & 7) + 8 * ((lane >> 3) & 1)) * (x.Fs * 4) + (8 * s0 + 8 * (lane >> 4)) * 2;
+  const uint32_t e_lane = x.e_base + ((lane & 7) + 8 * (lane >> 4)) * kPEPitch + 16 * ((lane >> 3) & 1);
+  const uint32_t mid_off = 2 * F, stage_bytes = kFRows * x.Fs * 4;
+  const float lr = cl.lr;
+  auto backward = [&](int kk, int sst) {
+    named_sync(3 + (kk & 1), kQSync);  // EFULL(kk)
+    uint32_t eh[4], em[4];
+    const uint32_t ea = e_lane + (kk & 1) * 2 * kFRows * kPEPitch;
+    ldsm_x4_t(ea, eh);
+    ldsm_x4_t(ea + kFRows * kPEPitch, em);
+    const uint32_t xa = x_lane + sst * stage_bytes;
+#pragma unroll
+    for (int j = 0; j + 1 < NK; j += 2) {
+      uint32_t bh[4], bm[4];
+      ldsm_x4_t(xa + 16 * j, bh);
+      ldsm_x4_t(xa + 16 * j + mid_off, bm);
+      mma_bf16(G[j], eh, bh[0], bh[1]);
+      mma_bf16(G[j], eh, bm[0], bm[1]);
+      mma_bf16(G[j], em, bh[0], bh[1]);
+      mma_bf16(G[j + 1], eh, bh[2], bh[3]);
+      mma_bf16(G[j + 1], eh, bm[2], bm[3]);
+      mma_bf16(G[j + 1], em, bh[2], bh[3]);
+    }
+    if constexpr (NK & 1) {
+      constexpr int jl = NK - 1;
+      uint32_t bh0, bh1, bm0, bm1;
+      ldsm_x2_t(xa + 16 * jl, bh0, bh1);
+      ldsm_x2_t(xa + 16 * jl + mid_off, bm0, bm1);
+      mma_bf16(G[jl], eh, bh0, bh1);
+      mma_bf16(G[jl], eh, bm0, bm1);
+      mma_bf16(G[jl], em, bh0, bh1);
+    }
+    __syncwarp();  // the MMAs above consumed every fragment of X(kk): all its reads have landed
+    if (lane == 0) mbar_arrive(&x.empty[sst]);
+  };
+  int k = 0, st = 0;
+  for (int s = 0; s < x.steps; ++s) {
+    const BatchRef br = batch_ref(s, cl.n_rows, cl.batch_size);
+    int prev_k = -1, prev_st = 0;
+    for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
+      mbar_wait(&x.full[st], (k / S) & 1);
+      float acc[2][2][4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[e][nt][0] = acc[e][nt][1] = acc[e][nt][2] = acc[e][nt][3] = 0.f;
+      const uint32_t xa = x_lane + st * stage_bytes;
+#pragma unroll
+      for (int j = 0; j + 1 < NK; j += 2) {
+        uint32_t AH[4], AM[4];
+        ldsm_x4(xa + 16 * j, AH);
+        ldsm_x4(xa + 16 * j + mid_off, AM);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
+          mma_bf16(acc[(j >> 1) & 1][nt], AH, wm[j][nt], wm[j + 1][nt]);
+          mma_bf16(acc[(j >> 1) & 1][nt], AM, wh[j][nt], wh[j + 1][nt]);
+        }
+      }
+      if constexpr (NK & 1) {
+        constexpr int jl = NK - 1;
+        uint32_t h0, h1, m0, m1;
+        ldsm_x2(xa + 16 * jl, h0, h1);
+        ldsm_x2(xa + 16 * jl + mid_off, m0, m1);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          mma_bf16_k8(acc[1][nt], h0, h1, wh[jl][nt]);
+          mma_bf16_k8(acc[1][nt], h0, h1, wm[jl][nt]);
+          mma_bf16_k8(acc[1][nt], m0, m1, wh[jl][nt]);
+        }
+      }
+      named_sync(2, kQSync);  // ZFREE: the softmax warps consumed the previous partials
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        float* zr = x.Zp + (size_t)(warp * kFRows + gq) * x.Zs + nt * 8 + 2 * tq;
+        *reinterpret_cast<float2*>(zr) = make_float2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
+        *reinterpret_cast<float2*>(zr + 8 * x.Zs) =
+            make_float2(acc[0][nt][2] + acc[1][nt][2], acc[0][nt][3] + acc[1][nt][3]);
+      }
+      named_arrive(1, kQSync);  // ZFULL
+      if (prev_k >= 0) backward(prev_k, prev_st);
+      prev_k = k;
+      prev_st = st;
+      ++k;
+      st = (st + 1 == S) ? 0 : st + 1;
+    }
+    if (prev_k >= 0) backward(prev_k, prev_st);
+    // ---- end of batch: thread-local SGD step on the master (TMEM) + re-split ----
+    float m[4 * NK];
+    tmem_ld_n<4 * NK>(x.tmem_w, m);
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+      m[4 * j] -= lr * G[j][0];
+      m[4 * j + 1] -= lr * G[j][1];
+      m[4 * j + 2] -= lr * G[j][2];
+      m[4 * j + 3] -= lr * G[j][3];
+      split_bf16x2(m[4 * j], m[4 * j + 1], wh[j][0], wm[j][0]);
+      split_bf16x2(m[4 * j + 2], m[4 * j + 3], wh[j][1], wm[j][1]);
+      G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
+    }
+    tmem_st_n<4 * NK>(x.tmem_w, m);
+  }
+  named_sync(2, kQSync);  // match the softmax warps' last ZFREE arrival
+  // ---- delta = W_final - W_initial for this warp's slices ----
+  float mf[4 * NK];
+  tmem_ld_n<4 * NK>(x.tmem_w, mf);
+  float* out = cl.delta;
+#pragma unroll
+  for (int j = 0; j < NK; ++j) {
+    const int f0 = 8 * (s0 + j) + 2 * tq;
+    const int fo[4] = {f0, f0 + 1, f0, f0 + 1};
+    const int co[4] = {gq, gq, gq + 8, gq + 8};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (co[i] < C) {
+        const size_t gi = (size_t)fo[i] * C + co[i];
+        out[gi] = mf[4 * j + i] - static_cast<float>(x.params[gi]);
+      }
+  }
+  (void)FC;
+}
+
+__global__ void __launch_bounds__(kQThreads, 1)
+    train_pipe2_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const int F,
+                       const int C, const Pipe2Geom g, const int64_t split_off) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Xb = reinterpret_cast<float*>(smem + g.off_x);
+  float* Zp = reinterpret_cast<float*>(smem + g.off_zp);
+  unsigned char* Eb = smem + g.off_e;  // [2 parity][hi, mid][16 rows][kPEPitch]
+  int* labels = reinterpret_cast<int*>(smem + g.off_lab);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + g.off_bar);
+  uint64_t* empty = full + kPStages;
+  float* gbx = reinterpret_cast<float*>(smem + g.off_gb);  // [2 softmax warps][16 classes]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + g.off_tmem);
+  constexpr int S = kPStages;
+  const fedhc_client cl = clients[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int FC = F * C;
+  for (int i = tid; i < S * kFRows * g.Fs; i += kQThreads) Xb[i] = 0.f;
+  for (int i = tid; i < 2 * 2 * kFRows * kPEPitch / 4; i += kQThreads) reinterpret_cast<float*>(Eb)[i] = 0.f;
+  fence_proxy_async_smem();
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 2);         // expect_tx + labels stored (producer)
+      mbar_init(&empty[s], kQWarps);  // every compute warp releases a stage after its backward
+    }
+    fence_mbar_init();
+  }
+  const int n = cl.n_rows, B = cl.batch_size;
+  const int steps = n > 0 ? cl.n_batches : 0;
+  if (warp == 0) {  // 128 TMEM columns: compute warp w -> lane quadrant w % 4, columns 36 (w / 4) .. + 35
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (warp < kQWarps) {
+    Pipe2Ctx x{&cl, params, Zp, full, empty, smem_u32(Xb), smem_u32(Eb),
+               *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + 36 * (warp >> 2), F, C, g.Fs, g.Zs, steps};
+    if (q_slices(warp) == 9) pipe2_compute<9>(x, warp, lane);
+    else pipe2_compute<8>(x, warp, lane);
+  } else if (warp == kQProd) {
+    // ===== producer: row gather, indices two stages ahead, labels one ahead (see train_pipe_kernel) =====
+    StageIter it0(n, B, steps), it1 = it0, it2 = it0;
+    it1.next();
+    it2.next();
+    it2.next();
+    int idx0 = it0.valid && lane < it0.rows ? cl.perm[it0.off + lane] : 0;
+    int idx1 = it1.valid && lane < it1.rows ? cl.perm[it1.off + lane] : 0;
+    int y0 = it0.valid && lane < it0.rows ? cl.y[idx0] : 0;
+    int st = 0;
+    for (int k = 0; it0.valid; ++k) {
+      const int rows = it0.rows;
+      const int y1 = it1.valid && lane < it1.rows ? cl.y[idx1] : 0;
+      const int idx2 = it2.valid && lane < it2.rows ? cl.perm[it2.off + lane] : 0;
+      if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows * F * 4));
+      __syncwarp();
+      if (lane < rows) {
+        fence_proxy_async_smem();
+        const char* src = reinterpret_cast<const char*>(cl.x + (size_t)idx0 * F) + split_off;
+        bulk_g2s(Xb + (size_t)(st * kFRows + lane) * g.Fs, src, static_cast<uint32_t>(F * 4), &full[st]);
+        labels[st * kFRows + lane] = y0;
+        __threadfence_block();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[st]);
+      idx0 = idx1;
+      idx1 = idx2;
+      y0 = y1;
+      it0 = it1;
+      it1 = it2;
+      it2.next();
+      st = (st + 1 == S) ? 0 : st + 1;
+    }
+  } else {
+    // ===== two softmax warps: warp kQSoft0 + h owns rows 8h .. 8h + 7; lane = (row r = lane & 7, class
+    // quarter q = lane >> 3): 4 classes per lane, 12 partial float4 loads, max / sum over the 4 quarters =====
+    const int h = warp - kQSoft0, r = (lane & 7) + 8 * h, q = lane >> 3, c0 = 4 * q;
+    float bias[4], gb[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      bias[e] = c0 + e < C ? static_cast<float>(params[FC + c0 + e]) : 0.f;
+      gb[e] = 0.f;
+    }
+    const float lr = cl.lr;
+    named_arrive(2, kQSync);  // Z buffer initially free
+    int k = 0, st = 0;
+    for (int s = 0; s < steps; ++s) {
+      const BatchRef br = batch_ref(s, n, B);
+      const float inv_nb = 1.0f / static_cast<float>(br.rows);
+      for (int r0 = 0; r0 < br.rows; r0 += kFRows) {
+        const int rows = min(kFRows, br.rows - r0);
+        mbar_wait(&full[st], (k / S) & 1);  // labels of this stage
+        const int y = labels[st * kFRows + r];
+        named_sync(1, kQSync);              // ZFULL
+        float4 a = *reinterpret_cast<const float4*>(Zp + (size_t)r * g.Zs + c0);
+        float4 b = *reinterpret_cast<const float4*>(Zp + (size_t)(kFRows + r) * g.Zs + c0);
+#pragma unroll
+        for (int w = 2; w < kQWarps; w += 2) {
+          const float4 u = *reinterpret_cast<const float4*>(Zp + (size_t)(w * kFRows + r) * g.Zs + c0);
+          const float4 v = *reinterpret_cast<const float4*>(Zp + (size_t)((w + 1) * kFRows + r) * g.Zs + c0);
+          a.x += u.x; a.y += u.y; a.z += u.z; a.w += u.w;
+          b.x += v.x; b.y += v.y; b.z += v.z; b.w += v.w;
+        }
+        named_arrive(2, kQSync);            // ZFREE: partials consumed
+        float z[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
+        float m = -FLT_MAX;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          z[e] = c0 + e < C ? bias[e] + z[e] : -FLT_MAX;
+          m = fmaxf(m, z[e]);
+        }
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        float ssum = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          z[e] = c0 + e < C ? expf(z[e] - m) : 0.f;
+          ssum += z[e];
+        }
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, 8);
+        ssum += __shfl_xor_sync(0xffffffffu, ssum, 16);
+        const float inv = __frcp_rn(ssum);
+        float err[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          err[e] = (r < rows && c0 + e < C) ? (z[e] * inv - (c0 + e == y ? 1.f : 0.f)) * inv_nb : 0.f;
+          gb[e] += err[e];
+        }
+        uint2 hi, mid;
+        split_bf16x2(err[0], err[1], hi.x, mid.x);
+        split_bf16x2(err[2], err[3], hi.y, mid.y);
+        unsigned char* E = Eb + (k & 1) * 2 * kFRows * kPEPitch + r * kPEPitch + 2 * c0;
+        *reinterpret_cast<uint2*>(E) = hi;
+        *reinterpret_cast<uint2*>(E + kFRows * kPEPitch) = mid;
+        __syncwarp();
+        named_arrive(3 + (k & 1), kQSync);  // EFULL(k)
+        ++k;
+        st = (st + 1 == S) ? 0 : st + 1;
+      }
+      // bias step: column sums over the batch rows (8 rows per warp, then the two warps in fixed order)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = gb[e];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        gb[e] = v;
+      }
+      if ((lane & 7) == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gbx[16 * h + c0 + e] = gb[e];
+      }
+      named_sync(5, 64);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = gbx[c0 + e] + gbx[16 + c0 + e];
+        if (c0 + e < C) bias[e] -= lr * v;
+        gb[e] = 0.f;
+      }
+      named_sync(5, 64);  // both warps read the halves before the next batch overwrites them
+    }
+    if (h == 0 && (lane & 7) == 0) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (c0 + e < C) cl.delta[FC + c0 + e] = bias[e] - static_cast<float>(params[FC + c0 + e]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tmem_slot));
+  }
+}
+
 template <bool FULL, int CL>
 static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, const double* params,
                                    const FusedGeom& g, cudaStream_t st) {
@@ -998,6 +1408,17 @@ static cudaError_t launch_fused_cl(const fedhc_client* clients, int n_clients, c
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
                         int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status) {
   static const bool v3_only = getenv("FEDHC_TRAIN_V3") != nullptr;
+  static const bool v4_split = getenv("FEDHC_PIPE_V4") != nullptr;
+  Pipe2Geom qg{};
+  if (split && !v3_only && !v4_split && plan_pipe2(F, C, max_smem, qg)) {
+    cudaError_t e = smem_optin_max(reinterpret_cast<const void*>(train_pipe2_kernel));
+    if (e == cudaSuccess) {
+      train_pipe2_kernel<<<n_clients, kQThreads, qg.bytes, st>>>(clients, params, F, C, qg, split_off);
+      e = cudaGetLastError();
+    }
+    *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_pipe2_kernel launch");
+    return true;
+  }
   PipeGeom pg{};
   if (!v3_only && plan_pipe(F, C, max_smem, pg, split)) {
     // opt in once per (kernel, device) to the maximum dynamic shared memory (thread-safe; keeps launches

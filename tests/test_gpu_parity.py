@@ -294,8 +294,9 @@ def test_x_split_layout(fh):
     ([90, 1], 1, 0.1),                          # batch of one row
 ])
 def test_split_rows_bit_identical(fh, tr, sizes, b, lr):
-    """train_pipe_kernel reading the fedhc_x_split copy (ldmatrix fragments) == reading fp32 rows and splitting
-    in registers, bit for bit (same products, same accumulation order)."""
+    """The split-row trainer (train_pipe2_kernel: fedhc_x_split copy, ldmatrix fragments, 12 balanced compute
+    warps) vs the fp32-row trainer (train_pipe_kernel, splits in registers): the same bf16x3 products summed in
+    a different grouping -> equal to fp32 rounding (<= 2e-6 of max|delta|); deterministic; both vs the oracle."""
     import torch
     from paper_2305_15668_b200 import _abi
     from paper_2305_15668_b200.experiment import DeviceFederation, delta_buffer
@@ -320,7 +321,12 @@ def test_split_rows_bit_identical(fh, tr, sizes, b, lr):
     fed.launch_train(desc_a.data_ptr(), len(ids), params, b)
     _abi.check(_abi.lib.fedhc_local_train(desc_b.data_ptr(), len(ids), params.data_ptr(), 784, C, b, stream_ptr()))
     torch.cuda.synchronize()
-    assert torch.equal(d_split, d_f32)
+    scale = float(d_f32.abs().max())
+    assert float((d_split - d_f32).abs().max()) <= 2e-6 * scale
+    again = d_split.clone()
+    fed.launch_train(desc_a.data_ptr(), len(ids), params, b)
+    torch.cuda.synchronize()
+    assert torch.equal(again, d_split)
     for i, cid in enumerate(ids):
         if sizes[i]:
             want = fm.local_sgd(params.cpu().numpy(), fm.Shard(cid, shards[cid].features, shards[cid].labels),
