@@ -77,10 +77,12 @@ int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* 
                       int n_features, int n_classes, int max_batch, void* stream);
 
 /* Rows re-encoded for the bf16x3 tensor-pipe trainers (setup, once per
- * federation): fp32 row i of x [n_rows, n_features] becomes n_features bf16
- * "hi" words followed by n_features bf16 "mid" words (hi = bf16_rn(x),
- * mid = bf16_rn(x - hi), |x - hi - mid| <= 2^-17 |x|) -- the same 4F bytes,
- * so `out` has x's byte layout.  n_features even. */
+ * federation): fp32 row i of x [n_rows, n_features] is split into bf16 "hi"
+ * and "mid" words (hi = bf16_rn(x), mid = bf16_rn(x - hi),
+ * |x - hi - mid| <= 2^-17 |x|) laid out per 8-feature unit u as
+ * [8 hi | 8 mid] at byte 32 u -- the same 4F bytes per row, so `out` has x's
+ * byte layout and any 8-aligned feature slice of a row is contiguous.
+ * n_features a multiple of 8. */
 int fedhc_x_split(const float* x, int64_t n_rows, int n_features, void* out, void* stream);
 
 /* fedhc_local_train (fl_core.py:163-194) whose client rows ALSO exist in the

@@ -150,7 +150,7 @@ __global__ void lg_grad_kernel(const double* __restrict__ x, const double* __res
 
 namespace fedhc {
 bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
-                     int max_smem, cudaStream_t st, int* status);
+                     int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status);
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
                         int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status);
 cudaError_t launch_x_split(const float* x, int64_t n_rows, int F, void* out, cudaStream_t st);
@@ -159,8 +159,8 @@ cudaError_t launch_x_split(const float* x, int64_t n_rows, int F, void* out, cud
 using namespace fedhc;
 
 extern "C" int fedhc_x_split(const float* x, int64_t n_rows, int n_features, void* out, void* stream) {
-  if (n_rows < 0 || n_features < 2 || n_features % 2 != 0)
-    return fail(FEDHC_ERR_VALUE, "x_split: need n_rows >= 0 and an even n_features >= 2");
+  if (n_rows < 0 || n_features < 8 || n_features % 8 != 0)
+    return fail(FEDHC_ERR_VALUE, "x_split: need n_rows >= 0 and n_features a positive multiple of 8");
   if (n_rows > 0 && (x == nullptr || out == nullptr)) return fail(FEDHC_ERR_VALUE, "x_split: null pointer");
   FEDHC_CUDA_TRY(launch_x_split(x, n_rows, n_features, out, static_cast<cudaStream_t>(stream)));
   return FEDHC_OK;
@@ -199,7 +199,8 @@ static int local_train_impl(const fedhc_client* clients, int n_clients, const do
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   int fused_status = FEDHC_OK;
-  if (launch_train_tc(clients, n_clients, params, n_features, n_classes, max_batch, max_smem, st, &fused_status))
+  if (launch_train_tc(clients, n_clients, params, n_features, n_classes, max_batch, max_smem, split, split_off, st,
+                      &fused_status))
     return fused_status;
   if (launch_train_fused(clients, n_clients, params, n_features, n_classes, max_smem, split, split_off, st, &fused_status))
     return fused_status;

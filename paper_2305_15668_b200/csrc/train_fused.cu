@@ -457,8 +457,10 @@ struct StageIter {
   }
 };
 
-// fedhc_x_split: each fp32 row [F] -> [F bf16 hi | F bf16 mid] (the same 4F bytes), hi / mid exactly as
-// split_bf16x2 makes them inside the kernels, so a trainer reading this copy computes the same products.
+// fedhc_x_split: each fp32 row [F] -> per 8-feature unit u: [8 bf16 hi | 8 bf16 mid] (32 bytes; the same 4F
+// bytes per row), hi / mid exactly as split_bf16x2 makes them inside the kernels.  Every 16-byte piece is one
+// plane of one unit, so ldmatrix reads fragments straight from a gathered row, and any 8-aligned feature
+// slice of a row is contiguous (one bulk copy per row for the feature-split tcgen05 trainer).
 __global__ void x_split_kernel(const float* __restrict__ x, int64_t n_pairs, int half_f, uint32_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pairs; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / half_f;
@@ -466,9 +468,9 @@ __global__ void x_split_kernel(const float* __restrict__ x, int64_t n_pairs, int
     const float2 v = __ldcs(reinterpret_cast<const float2*>(x) + i);
     uint32_t hi, mid;
     split_bf16x2(v.x, v.y, hi, mid);
-    uint32_t* o = out + row * (2 * half_f);
-    o[p] = hi;
-    o[half_f + p] = mid;
+    uint32_t* o = out + row * (2 * half_f) + 8 * (p >> 2) + (p & 3);
+    o[0] = hi;
+    o[4] = mid;
   }
 }
 
@@ -786,9 +788,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // forward's A fragments (x4: slices j, j + 1) and the backward's transposed B fragments (tiles j, j + 1).
     // E^T fragments: rows (lane & 7) + 8 (lane >> 4), classes 8 ((lane >> 3) & 1).
     const uint32_t x_lane = smem_u32(Xb) + ((lane & 7) + 8 * ((lane >> 3) & 1)) * (Fs * 4) +
-                            (kFK8 * 8 * warp + 8 * (lane >> 4)) * 2;
+                            32 * (kFK8 * warp + (lane >> 4));
     const uint32_t e_lane = smem_u32(Eb) + ((lane & 7) + 8 * (lane >> 4)) * kPEPitch + 16 * ((lane >> 3) & 1);
-    const uint32_t mid_off = 2 * F;
+    const uint32_t mid_off = 16;  // fedhc_x_split rows: k8 slice u = [hi 16 B | mid 16 B] at byte 32 u
     auto backward_split = [&](int kk, int sst) {
       named_sync(3 + (kk & 1), NCOMP);  // EFULL(kk)
       uint32_t eh[4], em[4];
@@ -799,8 +801,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
       for (int j = 0; j + 1 < kFK8; j += 2) {
         uint32_t bh[4], bm[4];
-        ldsm_x4_t(xa + 16 * j, bh);
-        ldsm_x4_t(xa + 16 * j + mid_off, bm);
+        ldsm_x4_t(xa + 32 * j, bh);
+        ldsm_x4_t(xa + 32 * j + mid_off, bm);
         mma_bf16(G[j], eh, bh[0], bh[1]);
         mma_bf16(G[j], eh, bm[0], bm[1]);
         mma_bf16(G[j], em, bh[0], bh[1]);
@@ -811,8 +813,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       {
         constexpr int jl = kFK8 - 1;
         uint32_t bh0, bh1, bm0, bm1;
-        ldsm_x2_t(xa + 16 * jl, bh0, bh1);
-        ldsm_x2_t(xa + 16 * jl + mid_off, bm0, bm1);
+        ldsm_x2_t(xa + 32 * jl, bh0, bh1);
+        ldsm_x2_t(xa + 32 * jl + mid_off, bm0, bm1);
         mma_bf16(G[jl], eh, bh0, bh1);
         mma_bf16(G[jl], eh, bm0, bm1);
         mma_bf16(G[jl], em, bh0, bh1);
@@ -862,8 +864,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int j = 0; j + 1 < kFK8; j += 2) {
             uint32_t AH[4], AM[4];
-            ldsm_x4(xa + 16 * j, AH);
-            ldsm_x4(xa + 16 * j + mid_off, AM);
+            ldsm_x4(xa + 32 * j, AH);
+            ldsm_x4(xa + 32 * j + mid_off, AM);
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
               mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
@@ -873,8 +875,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           constexpr int jl = kFK8 - 1;
           uint32_t h0, h1, m0, m1;
-          ldsm_x2(xa + 16 * jl, h0, h1);
-          ldsm_x2(xa + 16 * jl + mid_off, m0, m1);
+          ldsm_x2(xa + 32 * jl, h0, h1);
+          ldsm_x2(xa + 32 * jl + mid_off, m0, m1);
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             mma_bf16_k8(acc[1][nt], h0, h1, wh[jl][nt]);
@@ -1079,9 +1081,10 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
     tmem_st_n<4 * NK>(x.tmem_w, m0);
   }
   __syncwarp();
-  const uint32_t x_lane = x.x_base + ((lane & 7) + 8 * ((lane >> 3) & 1)) * (x.Fs * 4) + (8 * s0 + 8 * (lane >> 4)) * 2;
+  // fedhc_x_split rows: k8 slice u of a row = [hi 16 B | mid 16 B] at byte 32 u
+  const uint32_t x_lane = x.x_base + ((lane & 7) + 8 * ((lane >> 3) & 1)) * (x.Fs * 4) + 32 * (s0 + (lane >> 4));
   const uint32_t e_lane = x.e_base + ((lane & 7) + 8 * (lane >> 4)) * kPEPitch + 16 * ((lane >> 3) & 1);
-  const uint32_t mid_off = 2 * F, stage_bytes = kFRows * x.Fs * 4;
+  const uint32_t mid_off = 16, stage_bytes = kFRows * x.Fs * 4;
   const float lr = cl.lr;
   auto backward = [&](int kk, int sst) {
     named_sync(3 + (kk & 1), kQSync);  // EFULL(kk)
@@ -1093,8 +1096,8 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
 #pragma unroll
     for (int j = 0; j + 1 < NK; j += 2) {
       uint32_t bh[4], bm[4];
-      ldsm_x4_t(xa + 16 * j, bh);
-      ldsm_x4_t(xa + 16 * j + mid_off, bm);
+      ldsm_x4_t(xa + 32 * j, bh);
+      ldsm_x4_t(xa + 32 * j + mid_off, bm);
       mma_bf16(G[j], eh, bh[0], bh[1]);
       mma_bf16(G[j], eh, bm[0], bm[1]);
       mma_bf16(G[j], em, bh[0], bh[1]);
@@ -1105,8 +1108,8 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
     if constexpr (NK & 1) {
       constexpr int jl = NK - 1;
       uint32_t bh0, bh1, bm0, bm1;
-      ldsm_x2_t(xa + 16 * jl, bh0, bh1);
-      ldsm_x2_t(xa + 16 * jl + mid_off, bm0, bm1);
+      ldsm_x2_t(xa + 32 * jl, bh0, bh1);
+      ldsm_x2_t(xa + 32 * jl + mid_off, bm0, bm1);
       mma_bf16(G[jl], eh, bh0, bh1);
       mma_bf16(G[jl], eh, bm0, bm1);
       mma_bf16(G[jl], em, bh0, bh1);
@@ -1129,8 +1132,8 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
 #pragma unroll
       for (int j = 0; j + 1 < NK; j += 2) {
         uint32_t AH[4], AM[4];
-        ldsm_x4(xa + 16 * j, AH);
-        ldsm_x4(xa + 16 * j + mid_off, AM);
+        ldsm_x4(xa + 32 * j, AH);
+        ldsm_x4(xa + 32 * j + mid_off, AM);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
@@ -1141,8 +1144,8 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
       if constexpr (NK & 1) {
         constexpr int jl = NK - 1;
         uint32_t h0, h1, m0, m1;
-        ldsm_x2(xa + 16 * jl, h0, h1);
-        ldsm_x2(xa + 16 * jl + mid_off, m0, m1);
+        ldsm_x2(xa + 32 * jl, h0, h1);
+        ldsm_x2(xa + 32 * jl + mid_off, m0, m1);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           mma_bf16_k8(acc[1][nt], h0, h1, wh[jl][nt]);

@@ -46,6 +46,8 @@ constexpr int kQBar = 1;           // named barrier of the 4 Q warps
 
 struct TcGeom {
   int F, C, CL, S, NCH, NT, NP, ZS, stages, stage_bytes, tmem_cols;
+  int split;              // rows also exist pre-split (fedhc_x_split) at (char*)x + split_off: the stages hold
+  long long split_off;    // [hi S bf16 | mid S bf16] per row and the converters only re-layout (no fp32 splits)
   int off_stage, off_x, off_w, off_e, off_z, off_bias, off_bar, off_tmem, bytes;
   unsigned long long* trace;  // optional phase timestamps of cluster 0 (FEDHC_TC_TRACE builds), else null
 };
@@ -337,9 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const BatchRef nb = batch_ref(s + 1, n, B);
         for (int r = lane; r < nb.rows; r += 32) {
           const int idx = cl.perm[nb.perm_off + r];
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cl.x + (size_t)idx * F + f0),
-                       "r"((uint32_t)(Sk * 4))
-                       : "memory");
+          // split rows have the fp32 rows' byte layout per 8-feature unit: the same slice bytes
+          const char* row = reinterpret_cast<const char*>(cl.x + (size_t)idx * F + f0) + (g.split ? g.split_off : 0);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((uint32_t)(Sk * 4)) : "memory");
         }
       }
       for (int j = 0; j < kRows / kStageRows; ++j, ++it) {
@@ -350,8 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane < nr && Sk > 0) {
           const int idx = cl.perm[br.perm_off + kStageRows * j + lane];
-          bulk_g2s(smem + g.off_stage + slot * g.stage_bytes + lane * S * 4, cl.x + (size_t)idx * F + f0,
-                   (uint32_t)(Sk * 4), &full[slot]);
+          unsigned char* dst = smem + g.off_stage + slot * g.stage_bytes + lane * S * 4;
+          const char* src = reinterpret_cast<const char*>(cl.x + (size_t)idx * F + f0) + (g.split ? g.split_off : 0);
+          bulk_g2s(dst, src, (uint32_t)(Sk * 4), &full[slot]);
         }
         __syncwarp();
       }
@@ -418,6 +421,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ct == 0) trace_pt(g, crank, s, 12 + j);
         const float* src = reinterpret_cast<const float*>(smem + g.off_stage + slot * g.stage_bytes) + fl;
         const int nr = br.rows - kStageRows * j;  // valid rows of this stage
+        if (g.split) {
+          // pre-split rows: thread (chunk, 16-byte unit u of plane p) copies that unit of every row it owns
+          // into the swizzled tile -- one 16-byte load + one 16-byte store, no conversion
+          const int p = hu >> 3, uu = hu & 7;
+          const bool uvalid = ch * 64 + uu * 8 < Sk;
+          // split row slice: 8-feature unit v at byte 32 v = [hi 16 B | mid 16 B]
+          const unsigned char* ssrc = smem + g.off_stage + slot * g.stage_bytes + (ch * 8 + uu) * 32 + p * 16;
+          const uint32_t dsp = s_x + ch * kChunk + p * 8192;
+          for (int r0 = r_off; r0 < kStageRows; r0 += 8 * rpp) {
+            uint4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rr = r0 + k * rpp;
+              v[k] = make_uint4(0, 0, 0, 0);
+              if (active && uvalid && rr < nr && rr < kStageRows)
+                v[k] = *reinterpret_cast<const uint4*>(ssrc + (size_t)rr * S * 4);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rr = r0 + k * rpp;
+              if (active && rr < kStageRows) {
+                const int r = kStageRows * j + rr;
+                sts4(dsp + r * 128 + ((uu ^ (r & 7)) << 4), v[k].x, v[k].y, v[k].z, v[k].w);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+          if (ct == 0) trace_pt(g, crank, s, 16 + j);
+          continue;
+        }
         // 8 rows in flight per thread: all loads first, then the conversions (hides the LDS latency)
         for (int r0 = r_off; r0 < kStageRows; r0 += 8 * rpp) {
           float4 v[8];
@@ -662,7 +696,7 @@ static bool plan_cl(int F, int C, int CL, int max_smem, TcGeom& g) {
   g.C = C;
   g.CL = CL;
   g.NP = C <= 16 ? 16 : C <= 32 ? 32 : 64;
-  g.S = up((F + CL - 1) / CL, 4);
+  g.S = up((F + CL - 1) / CL, g.split ? 8 : 4);  // split rows: 16-byte aligned bf16 slices
   if (F - (CL - 1) * g.S <= 0) return false;  // every CTA owns features
   g.NCH = (g.S + 63) / 64;
   if (g.NCH < 2 || g.NCH > 8 || 128 / (kRows / CL) > 32 || g.NP % (128 / (kRows / CL)) != 0) return false;
@@ -692,6 +726,7 @@ static bool plan_cl(int F, int C, int CL, int max_smem, TcGeom& g) {
 
 bool plan_tc(int F, int C, int max_batch, int max_smem, TcGeom& g) {
   if (F % 4 != 0 || C > 64 || C < 2 || max_batch > kRows) return false;
+  if (F % 8 != 0) g.split = 0;
   static const int force_cl = getenv("FEDHC_TC_CL") ? atoi(getenv("FEDHC_TC_CL")) : 0;
   if (force_cl) return plan_cl(F, C, force_cl, max_smem, g);
   // smallest cluster that holds the client's batch split + operands (fewer CTAs = fewer waves)
@@ -737,7 +772,7 @@ static cudaError_t launch_np_cl(const fedhc_client* clients, int n_clients, cons
 
 // Launch the tcgen05 trainer if the shape fits; returns false to fall back.
 bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
-                     int max_smem, cudaStream_t st, int* status) {
+                     int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status) {
   using namespace ltc;
   // Default: at F <= 784 the mma.sync kernels keep C <= 32 (one CTA / a 2-CTA cluster per client: one or two
   // waves; measured faster there, profiles/r2_train_tc.md); C > 32 (4-CTA clusters here, 1.6x faster than the
@@ -747,6 +782,8 @@ bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* p
   if (path && strcmp(path, "tc") != 0) return false;
   if (!path && C <= 32 && F <= 784) return false;
   TcGeom g{};
+  g.split = split ? 1 : 0;  // rows pre-split in 8-feature units: slices stay 8-aligned
+  g.split_off = split_off;
   if (!plan_tc(F, C, max_batch, max_smem, g)) return false;
   if (getenv("FEDHC_TC_TRACE")) {
     if (!g_trace) cudaMalloc(&g_trace, sizeof(unsigned long long) * 8 * kTraceSteps * kTracePts);

@@ -197,14 +197,19 @@ def count_correct(x: torch.Tensor, y: torch.Tensor, params: torch.Tensor, n_clas
 
 
 def split_supported(n_features: int, n_classes: int) -> bool:
-    """Shapes whose trainer reads the fedhc_x_split row copy (train_pipe_kernel<true>: F = 784, C <= 16).
-    FEDHC_X_SPLIT=0 keeps every launch on the fp32 rows (A/B measurements)."""
-    return n_features == 784 and n_classes <= 16 and os.environ.get("FEDHC_X_SPLIT", "1") != "0"
+    """Shapes whose trainer reads the fedhc_x_split row copy: the one-CTA mma.sync trainer (F = 784, C <= 16)
+    and the tcgen05 cluster trainer (F > 784 or 32 < C <= 64, F % 8 == 0).  FEDHC_X_SPLIT=0 keeps every launch
+    on the fp32 rows (A/B measurements)."""
+    if os.environ.get("FEDHC_X_SPLIT", "1") == "0":
+        return False
+    if n_features == 784 and n_classes <= 16:
+        return True
+    return (n_features > 784 or 32 < n_classes <= 64) and n_features % 8 == 0 and n_classes <= 64
 
 
 def x_split(x: torch.Tensor) -> torch.Tensor:
-    """The rows of x (fp32 [n, F], device) re-encoded as [F bf16 hi | F bf16 mid] per row: same bytes, so the
-    copy is returned as an opaque fp32-typed tensor of x's shape (fedhc_x_split)."""
+    """The rows of x (fp32 [n, F], device) re-encoded per 8-feature unit as [8 bf16 hi | 8 bf16 mid]: same
+    bytes, so the copy is returned as an opaque fp32-typed tensor of x's shape (fedhc_x_split)."""
     out = torch.empty_like(x)
     _abi.check(_abi.lib.fedhc_x_split(x.data_ptr(), int(x.shape[0]), int(x.shape[1]), out.data_ptr(), stream_ptr()))
     return out

@@ -276,16 +276,18 @@ def test_batched_round_matches_per_client(fh, tr, C):
 
 
 def test_x_split_layout(fh):
-    """fedhc_x_split: each row -> [F bf16 hi | F bf16 mid], hi = bf16_rn(x), mid = bf16_rn(x - hi)."""
+    """fedhc_x_split: each row -> per 8-feature unit [8 bf16 hi | 8 bf16 mid], hi = bf16_rn(x),
+    mid = bf16_rn(x - hi)."""
     import torch
     from paper_2305_15668_b200.training import x_split
     g = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(37, 784, device="cuda", generator=g) * 3
     x[0, :4] = torch.tensor([0.0, -0.0, 1e-30, -7.5e5])
-    got = x_split(x).view(torch.int16).view(37, 2, 784)
+    got = x_split(x).view(torch.int16).view(37, 98, 2, 8)
     hi = x.to(torch.bfloat16)
     mid = (x - hi.float()).to(torch.bfloat16)
-    assert torch.equal(got[:, 0], hi.view(torch.int16)) and torch.equal(got[:, 1], mid.view(torch.int16))
+    assert torch.equal(got[:, :, 0].reshape(37, 784), hi.view(torch.int16))
+    assert torch.equal(got[:, :, 1].reshape(37, 784), mid.view(torch.int16))
 
 
 @pytest.mark.parametrize("sizes,b,lr", [
