@@ -390,7 +390,8 @@ def run_ours(args, rank, world, local_rank):
     from benchlib import roofline_entry
     bytes_per_launch = PER_GPU * steps_per_client * BATCH * (4 * F + 8) + PER_GPU * P * 12
     roof = roofline_entry(bytes_per_launch, train_ms, ROOT,
-                          kernel="train_pipe_kernel" if C <= 16 else "train_fused_kernel")
+                          kernel=("train_pipe2_kernel" if fed.x_split is not None else "train_pipe_kernel") if C <= 16
+                          else "train_fused_kernel")
 
     result = {
         "metric": "client local-steps/sec (FedHC round: local SGD of all participants + FedAvg + accuracy)",

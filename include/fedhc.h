@@ -300,10 +300,16 @@ typedef struct fedhc_runner_config {
   void* plan_stream;
   void* eval_stream;
   int64_t seed;
-  double pad_d_;
+  /* async aggregation (engine.py:354-364; async_buffer = 0: sync FedAvg).  Per slot: pinned [participants]
+   * x (chunk coefficient f64 | delta row address u64) blocks staged after the main block, device copies,
+   * params snapshots [participants][P] f64 (the accuracy of each chunk reads its own snapshot). */
+  uint8_t* const* async_host;
+  uint8_t* const* async_dev;
+  double* const* snapshots;
   fedhc_des_config des_cfg;
   float lr;
   int32_t n_fleet, participants, slots, n_features, n_classes, max_batch, split, eval_ctas, rows_max;
+  int32_t async_buffer;
 } fedhc_runner_config;
 
 typedef struct fedhc_runner_plan_info {
@@ -315,9 +321,10 @@ typedef struct fedhc_runner_plan_info {
   int32_t* upload_order;
   double* par_t;                  /* [par_cap] parallelism timeline                          */
   int32_t* par_n;
+  double* chunk_end;              /* [participants] async: end time of each chunk's last client */
   int32_t par_cap;
   /* outputs */
-  int32_t n_launched, n_uploaded, n_par, over_theta, degenerate, max_rows;
+  int32_t n_launched, n_uploaded, n_par, over_theta, degenerate, max_rows, n_chunks;
   double makespan, utilization, vacancy_area, throughput, total_weight;
   int64_t perm_words, h2d_bytes;
 } fedhc_runner_plan_info;
@@ -326,6 +333,7 @@ int fedhc_runner_create(const fedhc_runner_config* cfg, fedhc_runner** out);
 void fedhc_runner_destroy(fedhc_runner* runner);
 int fedhc_runner_plan(fedhc_runner* runner, int64_t round_index, double t0, int slot, fedhc_runner_plan_info* info);
 int fedhc_runner_launch(fedhc_runner* runner, int slot, void* stream);
+/* correct[n_chunks] (1 for sync FedAvg): the accuracy counts of the slot's round. */
 int fedhc_runner_result(fedhc_runner* runner, int slot, int64_t* correct);
 
 /* ---- tcgen05 grouped GEMM (client-model contractions) -------------------- */

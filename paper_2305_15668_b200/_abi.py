@@ -102,11 +102,12 @@ class RunnerConfig(C.Structure):
         ("split_offset", C.c_int64), ("x_test", C.c_void_p), ("y_test", C.c_void_p), ("n_test", C.c_int64),
         ("correct_dev", C.c_void_p), ("correct_host", C.c_void_p), ("stage_host", C.c_void_p),
         ("stage_dev", C.c_void_p), ("plan_dev", C.c_void_p), ("plan_cap_words", C.c_int64),
-        ("plan_stream", C.c_void_p), ("eval_stream", C.c_void_p), ("seed", C.c_int64), ("pad_d_", C.c_double),
+        ("plan_stream", C.c_void_p), ("eval_stream", C.c_void_p), ("seed", C.c_int64),
+        ("async_host", C.c_void_p), ("async_dev", C.c_void_p), ("snapshots", C.c_void_p),
         ("des_cfg", DesConfig), ("lr", C.c_float),
         ("n_fleet", C.c_int32), ("participants", C.c_int32), ("slots", C.c_int32), ("n_features", C.c_int32),
         ("n_classes", C.c_int32), ("max_batch", C.c_int32), ("split", C.c_int32), ("eval_ctas", C.c_int32),
-        ("rows_max", C.c_int32),
+        ("rows_max", C.c_int32), ("async_buffer", C.c_int32),
     ]
 
 
@@ -114,9 +115,10 @@ class RunnerPlanInfo(C.Structure):
     """fedhc_runner_plan_info (include/fedhc.h)."""
     _fields_ = [
         ("selected", C.c_void_p), ("starts", C.c_void_p), ("ends", C.c_void_p), ("launch_order", C.c_void_p),
-        ("upload_order", C.c_void_p), ("par_t", C.c_void_p), ("par_n", C.c_void_p), ("par_cap", C.c_int32),
+        ("upload_order", C.c_void_p), ("par_t", C.c_void_p), ("par_n", C.c_void_p), ("chunk_end", C.c_void_p),
+        ("par_cap", C.c_int32),
         ("n_launched", C.c_int32), ("n_uploaded", C.c_int32), ("n_par", C.c_int32), ("over_theta", C.c_int32),
-        ("degenerate", C.c_int32), ("max_rows", C.c_int32),
+        ("degenerate", C.c_int32), ("max_rows", C.c_int32), ("n_chunks", C.c_int32),
         ("makespan", C.c_double), ("utilization", C.c_double), ("vacancy_area", C.c_double),
         ("throughput", C.c_double), ("total_weight", C.c_double), ("perm_words", C.c_int64),
         ("h2d_bytes", C.c_int64),

@@ -22,6 +22,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -39,7 +40,10 @@ struct fedhc_runner {
   std::vector<int32_t> order, wi32;
   std::vector<int64_t> wi64;
   std::vector<double> w, starts, ends;
-  std::vector<int32_t> k_of;  // participants per slot (launch needs it)
+  std::vector<int32_t> k_of;        // participants per slot (launch needs it)
+  std::vector<int32_t> chunks_of;   // aggregation chunks per slot (1 for sync FedAvg)
+  std::vector<int32_t> sorted;      // async: participants in (end time, id) order
+  std::vector<std::vector<int32_t>> chunk_len;  // per slot: chunk sizes
 };
 
 namespace {
@@ -77,6 +81,14 @@ extern "C" int fedhc_runner_create(const fedhc_runner_config* cfg, fedhc_runner*
   r->starts.resize(kp + 1);
   r->ends.resize(kp + 1);
   r->k_of.assign(S, 0);
+  r->chunks_of.assign(S, 1);
+  r->sorted.resize(kp + 1);
+  r->chunk_len.assign(S, std::vector<int32_t>(kp + 1, 0));
+  if (cfg->async_buffer < 0 || (cfg->async_buffer > 0 && (!cfg->async_host || !cfg->async_dev || !cfg->snapshots))) {
+    destroy_events(r);
+    delete r;
+    return fail(FEDHC_ERR_VALUE, "runner: async aggregation needs the async blocks and snapshots");
+  }
   *out = r;
   return FEDHC_OK;
 }
@@ -93,6 +105,7 @@ extern "C" int fedhc_runner_plan(fedhc_runner* r, int64_t round_index, double t0
   const fedhc_runner_config& c = r->c;
   const int kp = c.participants;
   info->n_launched = info->n_uploaded = info->n_par = info->over_theta = info->degenerate = info->max_rows = 0;
+  info->n_chunks = 0;
   info->makespan = info->utilization = info->vacancy_area = info->throughput = info->total_weight = 0.0;
   info->perm_words = info->h2d_bytes = 0;
   // ---- selection (engine.py:327): CPython random.sample(range(n_fleet), kp) on the selector state ----
@@ -162,10 +175,41 @@ extern "C" int fedhc_runner_plan(fedhc_runner* r, int64_t round_index, double t0
   info->max_rows = mrows;
   const int64_t tot = (int64_t)kp * (24 + (int64_t)sizeof(fedhc_client) + 8);
   info->h2d_bytes = tot;
+  int n_chunks = 1;
+  if (c.async_buffer > 0) {
+    // engine.py:355-364: participants in (per_client_end, id) order, chunks of async_buffer, each chunk's FedAvg
+    // normalised by its own weights (fl_core.fedavg on the chunk, CPython float sum)
+    for (int i = 0; i < kp; ++i) r->sorted[i] = i;
+    std::sort(r->sorted.begin(), r->sorted.begin() + kp, [&](int a, int b) {
+      if (r->ends[a] != r->ends[b]) return r->ends[a] < r->ends[b];
+      return strcmp(c.des_ids[r->order[a]], c.des_ids[r->order[b]]) < 0;
+    });
+    double* acoef = reinterpret_cast<double*>(c.async_host[slot]);
+    uint64_t* arow = reinterpret_cast<uint64_t*>(c.async_host[slot] + 8 * (size_t)kp);
+    n_chunks = 0;
+    std::vector<double> cw(c.async_buffer);
+    for (int at = 0; at < kp; at += c.async_buffer, ++n_chunks) {
+      const int len = std::min(c.async_buffer, kp - at);
+      for (int j = 0; j < len; ++j) cw[j] = c.weight[r->wi32[r->sorted[at + j]]];
+      const double wc = fedhc_py_float_sum(cw.data(), len);
+      if (wc == 0.0) return fail(FEDHC_ERR_AGGREGATION, "weights must not all be zero");
+      for (int j = 0; j < len; ++j) {
+        const int i = r->sorted[at + j];
+        acoef[at + j] = cw[j] / wc;
+        arow[at + j] = reinterpret_cast<uint64_t>(c.deltas) + (uint64_t)i * (uint64_t)c.delta_stride_bytes;
+      }
+      r->chunk_len[slot][n_chunks] = len;
+      info->chunk_end[n_chunks] = r->ends[r->sorted[at + len - 1]];
+    }
+    info->h2d_bytes = tot + 16 * (int64_t)kp;
+  }
+  info->n_chunks = n_chunks;
   // ---- plan stream: H2D of the block, then the batch order on the device ----
   cudaStream_t ps = static_cast<cudaStream_t>(c.plan_stream);
   e = cudaStreamWaitEvent(ps, r->used[slot], 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c.stage_dev[slot], c.stage_host[slot], tot, cudaMemcpyHostToDevice, ps);
+  if (e == cudaSuccess && c.async_buffer > 0)
+    e = cudaMemcpyAsync(c.async_dev[slot], c.async_host[slot], 16 * (size_t)kp, cudaMemcpyHostToDevice, ps);
   if (e != cudaSuccess) return cuda_status(e, "runner_plan: H2D");
   if (words > 0) {
     uint8_t* md = c.stage_dev[slot];
@@ -179,6 +223,7 @@ extern "C" int fedhc_runner_plan(fedhc_runner* r, int64_t round_index, double t0
   e = cudaEventRecord(r->planned[slot], ps);
   if (e != cudaSuccess) return cuda_status(e, "runner_plan: record");
   r->k_of[slot] = kp;
+  r->chunks_of[slot] = n_chunks;
   return FEDHC_OK;
 }
 
@@ -194,20 +239,53 @@ extern "C" int fedhc_runner_launch(fedhc_runner* r, int slot, void* stream) {
   int rc = local_train_entry(desc, k, c.params, c.n_features, c.n_classes, c.max_batch, c.split != 0, c.split_offset,
                              ms);
   if (rc != FEDHC_OK) return rc;
-  if (r->prev_result) FEDHC_CUDA_TRY(cudaStreamWaitEvent(ms, r->prev_result, 0));  // it reads the params
   const int64_t P = (int64_t)c.n_features * c.n_classes + c.n_classes;
-  rc = fedhc_fedavg(nullptr, c.deltas, c.delta_stride_bytes / 4, FEDHC_F32, coef, k, c.params, c.params, P, ms);
-  if (rc != FEDHC_OK) return rc;
-  FEDHC_CUDA_TRY(cudaEventRecord(r->used[slot], ms));
-  FEDHC_CUDA_TRY(cudaEventRecord(r->agg[slot], ms));
-  FEDHC_CUDA_TRY(cudaStreamWaitEvent(es, r->agg[slot], 0));
-  unsigned long long* cnt = c.correct_dev + slot;
-  FEDHC_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), es));
-  if (c.n_test > 0) {
-    rc = fedhc_eval_ctas(c.x_test, c.y_test, c.n_test, c.n_features, c.n_classes, c.params, cnt, c.eval_ctas, es);
+  const int kp = c.participants > 0 ? c.participants : 1;
+  unsigned long long* cnt = c.correct_dev + (size_t)slot * kp;
+  if (c.async_buffer == 0) {
+    if (r->prev_result) FEDHC_CUDA_TRY(cudaStreamWaitEvent(ms, r->prev_result, 0));  // it reads the params
+    rc = fedhc_fedavg(nullptr, c.deltas, c.delta_stride_bytes / 4, FEDHC_F32, coef, k, c.params, c.params, P, ms);
     if (rc != FEDHC_OK) return rc;
+    FEDHC_CUDA_TRY(cudaEventRecord(r->used[slot], ms));
+    FEDHC_CUDA_TRY(cudaEventRecord(r->agg[slot], ms));
+    FEDHC_CUDA_TRY(cudaStreamWaitEvent(es, r->agg[slot], 0));
+    FEDHC_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), es));
+    if (c.n_test > 0) {
+      rc = fedhc_eval_ctas(c.x_test, c.y_test, c.n_test, c.n_features, c.n_classes, c.params, cnt, c.eval_ctas, es);
+      if (rc != FEDHC_OK) return rc;
+    }
+    FEDHC_CUDA_TRY(cudaMemcpyAsync(c.correct_host + (size_t)slot * kp, cnt, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, es));
+  } else {
+    // chunked FedAvg in (end, id) order on the params; each chunk's result is snapshotted so its accuracy
+    // (eval stream) overlaps the next chunks and the next round's training
+    const uint8_t* ad = c.async_dev[slot];
+    const double* acoef = reinterpret_cast<const double*>(ad);
+    const void* const* arow = reinterpret_cast<const void* const*>(ad + 8 * (size_t)kp);
+    double* snap = c.snapshots[slot];
+    FEDHC_CUDA_TRY(cudaStreamWaitEvent(ms, r->result[slot], 0));  // the slot's previous accuracy read its snapshots
+    int at = 0;
+    for (int ch = 0; ch < r->chunks_of[slot]; ++ch) {
+      const int len = r->chunk_len[slot][ch];
+      rc = fedhc_fedavg(arow + at, nullptr, 0, FEDHC_F32, acoef + at, len, c.params, c.params, P, ms);
+      if (rc != FEDHC_OK) return rc;
+      FEDHC_CUDA_TRY(cudaMemcpyAsync(snap + (size_t)ch * P, c.params, sizeof(double) * P, cudaMemcpyDeviceToDevice, ms));
+      at += len;
+    }
+    FEDHC_CUDA_TRY(cudaEventRecord(r->used[slot], ms));
+    FEDHC_CUDA_TRY(cudaEventRecord(r->agg[slot], ms));
+    FEDHC_CUDA_TRY(cudaStreamWaitEvent(es, r->agg[slot], 0));
+    const int nc = r->chunks_of[slot];
+    FEDHC_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nc, es));
+    if (c.n_test > 0)
+      for (int ch = 0; ch < nc; ++ch) {
+        rc = fedhc_eval_ctas(c.x_test, c.y_test, c.n_test, c.n_features, c.n_classes, snap + (size_t)ch * P, cnt + ch,
+                             c.eval_ctas, es);
+        if (rc != FEDHC_OK) return rc;
+      }
+    FEDHC_CUDA_TRY(cudaMemcpyAsync(c.correct_host + (size_t)slot * kp, cnt, sizeof(unsigned long long) * nc,
+                                   cudaMemcpyDeviceToHost, es));
   }
-  FEDHC_CUDA_TRY(cudaMemcpyAsync(c.correct_host + slot, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, es));
   FEDHC_CUDA_TRY(cudaEventRecord(r->result[slot], es));
   r->prev_result = r->result[slot];
   return FEDHC_OK;
@@ -216,6 +294,8 @@ extern "C" int fedhc_runner_launch(fedhc_runner* r, int slot, void* stream) {
 extern "C" int fedhc_runner_result(fedhc_runner* r, int slot, int64_t* correct) {
   if (!r || !correct || slot < 0 || slot >= r->c.slots) return fail(FEDHC_ERR_VALUE, "runner_result: bad argument");
   FEDHC_CUDA_TRY(cudaEventSynchronize(r->result[slot]));
-  *correct = static_cast<int64_t>(r->c.correct_host[slot]);
+  const int kp = r->c.participants > 0 ? r->c.participants : 1;
+  for (int ch = 0; ch < r->chunks_of[slot]; ++ch)
+    correct[ch] = static_cast<int64_t>(r->c.correct_host[(size_t)slot * kp + ch]);
   return FEDHC_OK;
 }

@@ -281,7 +281,7 @@ def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParam
 
     report = ExperimentReport()
     now = 0.0
-    if fed is not None and cfg.aggregation == "sync" and trace is None:
+    if fed is not None and trace is None:
         # the serving path: pipelined planning + one launch per kernel per round
         runner = FederatedRunner(fed, by_id, cfg, train.lr, params=params)
 
@@ -345,6 +345,7 @@ class RoundPlan:
     meta_bytes: int = 0              # device-plan mode: packed (seed, rows, perms, offset) bytes
     max_rows: int = 0
     plan_launched: bool = False      # its [H2D + permutations] graph is already queued
+    chunks: list | None = None       # async: [(end time, local delta rows, coefficients)] in (end, id) order
 
 
 class FederatedRunner:
@@ -375,6 +376,8 @@ class FederatedRunner:
         from .sharding import shard_bounds
 
         self.fed, self.cfg, self.lr = fed, cfg, float(lr)
+        # engine.py:354-364: async aggregation applies the round's deltas in chunks of async_buffer
+        self.async_buffer = int(cfg.async_buffer) if cfg.aggregation == "async" else 0
         self.by_id = fleet
         self.ids = sorted(fleet)
         self.sim = RoundSimulator(fleet)
@@ -416,6 +419,7 @@ class FederatedRunner:
         self._coef_pin = [torch.empty(k_max, dtype=torch.float64).pin_memory() for _ in range(n)]
         self._coef_dev = [torch.empty(k_max, dtype=torch.float64, device=dev) for _ in range(n)]
         self.correct_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._chunk_dev = None
         self._correct_pin = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(n)]
         self._result_ev = [None] * n
         self.plan_threads = plan_threads
@@ -529,13 +533,21 @@ class FederatedRunner:
         blk = max(kp, 1) * (24 + CLIENT_DTYPE.itemsize + 8)
         self._n_stage_pin = [torch.empty(blk, dtype=torch.uint8).pin_memory() for _ in range(n)]
         self._n_stage_dev = [torch.empty(blk, dtype=torch.uint8, device=dev) for _ in range(n)]
-        self._n_correct_dev = torch.zeros(n, dtype=torch.int64, device=dev)
-        self._n_correct_pin = torch.zeros(n, dtype=torch.int64).pin_memory()
+        kq = max(kp, 1)
+        self._n_correct_dev = torch.zeros(n * kq, dtype=torch.int64, device=dev)
+        self._n_correct_pin = torch.zeros(n * kq, dtype=torch.int64).pin_memory()
+        if self.async_buffer:
+            self._n_async_pin = [torch.empty(16 * kq, dtype=torch.uint8).pin_memory() for _ in range(n)]
+            self._n_async_dev = [torch.empty(16 * kq, dtype=torch.uint8, device=dev) for _ in range(n)]
+            self._n_snap = [torch.empty(kq * fed.P, dtype=torch.float64, device=dev) for _ in range(n)]
+        else:
+            self._n_async_pin = self._n_async_dev = self._n_snap = []
         ptrs = lambda ts: np.array([t.data_ptr() for t in ts], dtype=np.uint64)  # noqa: E731
         self._n_keep = [ptrs(self._n_stage_pin), ptrs(self._n_stage_dev), ptrs(self._n_plan),
                         np.ascontiguousarray(self._over_theta.astype(np.uint8)),
-                        np.ascontiguousarray(self._sim_idx.astype(np.int32)), np.ascontiguousarray(self._c_w)]
-        sp, sd, pd, ot, si, w = self._n_keep
+                        np.ascontiguousarray(self._sim_idx.astype(np.int32)), np.ascontiguousarray(self._c_w),
+                        ptrs(self._n_async_pin), ptrs(self._n_async_dev), ptrs(self._n_snap)]
+        sp, sd, pd, ot, si, w, ah, ad, sn = self._n_keep
         sim = self.sim
         des = _abi.DesConfig(float(cfg.theta), int(cfg.max_executors), 0 if cfg.scheduler_kind == "resource-aware"
                              else 1, int(bool(cfg.dynamic_parallelism)), float(cfg.alpha), float(cfg.beta),
@@ -560,6 +572,9 @@ class FederatedRunner:
         c.plan_cap_words = cap
         c.plan_stream, c.eval_stream = self._plan_stream.cuda_stream, self._eval_stream.cuda_stream
         c.seed, c.des_cfg, c.lr = int(cfg.seed), des, self.lr
+        if self.async_buffer:
+            c.async_host, c.async_dev, c.snapshots = ah.ctypes.data, ad.ctypes.data, sn.ctypes.data
+        c.async_buffer = self.async_buffer
         c.n_fleet, c.participants, c.slots = len(self.ids), kp, n
         c.n_features, c.n_classes, c.max_batch = fed.n_features, fed.n_classes, self._bs_max
         c.split = 1 if xs is not None else 0
@@ -575,12 +590,14 @@ class FederatedRunner:
         for _ in range(n):
             o = {"selected": np.zeros(kq, np.int32), "starts": np.zeros(kq), "ends": np.zeros(kq),
                  "launch": np.zeros(kq, np.int32), "upload": np.zeros(kq, np.int32),
-                 "par_t": np.zeros(4 * kq + 16), "par_n": np.zeros(4 * kq + 16, np.int32)}
+                 "par_t": np.zeros(4 * kq + 16), "par_n": np.zeros(4 * kq + 16, np.int32),
+                 "chunk_end": np.zeros(kq), "counts": np.zeros(kq, np.int64)}
             info = _abi.RunnerPlanInfo()
             info.selected, info.starts, info.ends = (o["selected"].ctypes.data, o["starts"].ctypes.data,
                                                      o["ends"].ctypes.data)
             info.launch_order, info.upload_order = o["launch"].ctypes.data, o["upload"].ctypes.data
             info.par_t, info.par_n, info.par_cap = o["par_t"].ctypes.data, o["par_n"].ctypes.data, 4 * kq + 16
+            info.chunk_end = o["chunk_end"].ctypes.data
             o["info"] = info
             self._n_out.append(o)
 
@@ -610,8 +627,9 @@ class FederatedRunner:
                               o["par_n"][:npar].copy() if npar else None, self.sim.budget)
         self.h2d_bytes = int(info.h2d_bytes)
         self.host_s["select+des"] += time.perf_counter() - tick
+        chunks = [(float(t), None, None) for t in o["chunk_end"][:info.n_chunks]] if self.async_buffer else None
         return RoundPlan(r, who, who, rep, t0, [], np.zeros(0), slot, int(info.perm_words), None,
-                         24 * kp, int(info.max_rows), plan_launched=True)
+                         24 * kp, int(info.max_rows), plan_launched=True, chunks=chunks)
 
     def _native_run(self, rounds: int, n_test: int, on_round) -> list:
         """run() on the native loop: a planner thread (fedhc_runner_plan) feeding the launching thread."""
@@ -642,7 +660,7 @@ class FederatedRunner:
         series, pending = [], None
         hs = self.host_s
         stream = torch.cuda.current_stream().cuda_stream
-        correct = C.c_int64()
+        last = [None]
         try:
             for _ in range(rounds):
                 t0 = time.perf_counter()
@@ -655,25 +673,34 @@ class FederatedRunner:
                 hs["launch"] += time.perf_counter() - t1
                 if pending is not None:
                     t0 = time.perf_counter()
-                    _abi.check(_abi.lib.fedhc_runner_result(self._native, pending.slot, C.byref(correct)))
+                    series.extend(self._native_finish(pending, n_test, on_round))
                     free.put(pending.slot)
                     hs["wait_gpu"] = hs.get("wait_gpu", 0.0) + time.perf_counter() - t0
-                    series.append(self._native_finish(pending, correct.value, n_test, on_round))
+                last[0] = p
                 pending = p
-            _abi.check(_abi.lib.fedhc_runner_result(self._native, pending.slot, C.byref(correct)))
+            series.extend(self._native_finish(pending, n_test, on_round))
             free.put(pending.slot)
-            series.append(self._native_finish(pending, correct.value, n_test, on_round))
         finally:
             th.join()
         self.round += rounds
-        self.now = series[-1][0]
+        self.now = last[0].t0 + last[0].report.makespan
         return series
 
-    def _native_finish(self, p: RoundPlan, correct: int, n_test: int, on_round) -> tuple[float, float]:
-        acc = correct / n_test if n_test else 0.0
+    def _native_finish(self, p: RoundPlan, n_test: int, on_round) -> list:
+        counts = self._n_out[p.slot]["counts"]
+        _abi.check(_abi.lib.fedhc_runner_result(self._native, p.slot, counts.ctypes.data))
+        return self._series_entries(p, counts, n_test, on_round)
+
+    def _series_entries(self, p: RoundPlan, counts, n_test: int, on_round) -> list:
+        """[(time, accuracy)] of a finished round: one entry (sync) or one per aggregation chunk (async)."""
+        if p.chunks is None:
+            acc = int(counts[0]) / n_test if n_test else 0.0
+            out = [(p.t0 + p.report.makespan, acc)]
+        else:
+            out = [(t, int(counts[i]) / n_test if n_test else 0.0) for i, (t, _, _) in enumerate(p.chunks)]
         if on_round is not None:
-            on_round(p, acc)
-        return (p.t0 + p.report.makespan, acc)
+            on_round(p, out[-1][1])
+        return out
 
     # ---- host side ---------------------------------------------------------
     def _ensure(self, slot: int, words: int):
@@ -718,8 +745,11 @@ class FederatedRunner:
         if total == 0:
             raise AggregationError("weights must not all be zero")
         my_w = w_all[sel].tolist()
+        chunks = self._async_chunks(rep, who, w_all, sel) if self.async_buffer else None
         if self.device_permutations:
-            return self._plan_packed(r, t0, slot, rep, who, mine, mi, my_w, total, tick, t1)
+            p = self._plan_packed(r, t0, slot, rep, who, mine, mi, my_w, total, tick, t1)
+            p.chunks = chunks
+            return p
         coef = np.asarray(my_w, np.float64) / total
         reprs = self._repr_ptr[mi] if k else self._repr_ptr[:1]   # const char* per participant
         train_seeds = np.zeros(max(k, 1), np.uint64)
@@ -767,7 +797,24 @@ class FederatedRunner:
         hs["permutations"] += t3 - t2
         hs["descriptors"] += t4 - t3
         return RoundPlan(r, mine, who, rep, t0, my_w, coef, slot, at, desc, meta_bytes,
-                         int(rows.max()) if k else 0)
+                         int(rows.max()) if k else 0, chunks=chunks)
+
+    def _async_chunks(self, rep, who, w_all, sel) -> list:
+        """engine.py:355-364: the round's participants in (per_client_end, id) order, chunks of async_buffer;
+        per chunk (end of its last client, this rank's delta rows, their w_i / W_chunk)."""
+        ends = rep.end_times() if hasattr(rep, "end_times") else np.array([rep.per_client_end[c] for c in who])
+        order = sorted(range(len(who)), key=lambda i: (ends[i], who[i]))
+        local = {g: j for j, g in enumerate(sel)}
+        w = w_all.tolist()
+        out = []
+        for at in range(0, len(order), self.async_buffer):
+            ch = order[at:at + self.async_buffer]
+            wc = float(sum(w[i] for i in ch))  # fl_core.fedavg's total over the chunk (CPython float sum)
+            if wc == 0:
+                raise AggregationError("weights must not all be zero")
+            mine = [i for i in ch if i in local]
+            out.append((float(ends[ch[-1]]), [local[i] for i in mine], [w[i] / wc for i in mine]))
+        return out
 
     def _plan_packed(self, r, t0, slot, rep, who, mine, mi, my_w, total, tick, t1) -> RoundPlan:
         """Device batch order: seeds, the [meta | descriptors | coefficients] staging block and the plan
@@ -938,7 +985,9 @@ class FederatedRunner:
             self.fed.launch_train(desc_ptr, k, self.params, max_b)
         self._ev_train[slot].record()
         self._train_done[slot] = self._ev_train[slot]
-        if self.world == 1:
+        if p.chunks is not None:
+            self._launch_async(p, main)
+        elif self.world == 1:
             if self._eval_done is not None:
                 main.wait_event(self._eval_done)  # the previous round's accuracy is done reading the params
             if k:
@@ -950,7 +999,9 @@ class FederatedRunner:
                 self.partial.zero_()
             combine_partials(self.partial, self.params,
                              lambda s, prm: fedavg_device(s.view(1, -1), self.one, prm, prm), self.group)
-        if self.world == 1:
+        if p.chunks is not None:
+            pass  # accuracy per chunk: _launch_async
+        elif self.world == 1:
             es = self._eval_stream
             self._ev_agg[slot].record(main)
             es.wait_event(self._ev_agg[slot])
@@ -976,13 +1027,49 @@ class FederatedRunner:
             self._correct_pin[slot].copy_(self.correct_dev, non_blocking=True)
             self._ev_result[slot].record()
         self._result_ev[slot] = self._ev_result[slot]
-        if self.use_graphs and k and p.meta_bytes and (gs is None or gs[0] != self._graph_key(p)):
+        if self.use_graphs and p.chunks is None and k and p.meta_bytes and (gs is None or gs[0] != self._graph_key(p)):
             self._capture(p)
         self.host_s["launch"] += time.perf_counter() - tick
 
     def read_correct(self, slot: int) -> int:
         self._result_ev[slot].synchronize()
-        return int(self._correct_pin[slot].item())
+        return int(self._correct_pin[slot][0].item())
+
+    def _launch_async(self, p: RoundPlan, main) -> None:
+        """Async aggregation (engine.py:354-364) on the Python path: per chunk, this rank's partial FedAvg
+        (pointer rows, w_i / W_chunk), one all-reduce of the fp64 partials, the apply, and the chunk's sharded
+        accuracy count; one all-reduce of the round's counts and one D2H."""
+        from .sharding import all_reduce_count, combine_partials
+        slot, nc = p.slot, len(p.chunks)
+        if self._chunk_dev is None or self._chunk_dev.shape[0] < nc:
+            self._chunk_dev = torch.zeros(max(nc, 1), dtype=torch.int64, device=self.dev)
+        counts = self._chunk_dev[:nc]
+        counts.zero_()
+        row0 = self.deltas.data_ptr()
+        stride = self.deltas.stride(0) * 4
+        for ci, (_, rows, coef) in enumerate(p.chunks):
+            if rows:
+                ptr = torch.tensor([row0 + j * stride for j in rows], dtype=torch.int64).to(self.dev, non_blocking=True)
+                cf = torch.tensor(coef, dtype=torch.float64).to(self.dev, non_blocking=True)
+                if self.world == 1:
+                    fedavg_device(self.deltas, cf, self.params, self.params, rows=ptr)
+                else:
+                    fedavg_device(self.deltas, cf, None, self.partial, rows=ptr)
+            elif self.world > 1:
+                self.partial.zero_()
+            if self.world > 1:
+                combine_partials(self.partial, self.params,
+                                 lambda s_, prm: fedavg_device(s_.view(1, -1), self.one, prm, prm), self.group)
+            if self._nt:
+                _abi.check(_abi.lib.fedhc_eval(self._xt.data_ptr(), self._yt.data_ptr(), self._nt,
+                                               self.fed.n_features, self.fed.n_classes, self.params.data_ptr(),
+                                               counts[ci:ci + 1].data_ptr(), stream_ptr()))
+        all_reduce_count(counts, self.group)
+        if self._correct_pin[slot].shape[0] < nc:
+            self._correct_pin[slot] = torch.zeros(nc, dtype=torch.int64).pin_memory()
+        self._correct_pin[slot][:nc].copy_(counts, non_blocking=True)
+        self._ev_result[slot].record()
+        self._eval_done = None
 
     def run(self, rounds: int, n_test_total: int | None = None, on_round=None):
         """Run `rounds` rounds; returns [(round_end_time, accuracy)] (engine.py:350-353 sync semantics)."""
@@ -1049,19 +1136,17 @@ class FederatedRunner:
             self.launch(p)
             if pending is not None:   # read the previous round while this one runs
                 t0 = time.perf_counter()
-                series.append(self._finish(pending, n_test, on_round, free))
+                series.extend(self._finish(pending, n_test, on_round, free))
                 hs["wait_gpu"] = hs.get("wait_gpu", 0.0) + time.perf_counter() - t0
             pending = p
-        series.append(self._finish(pending, n_test, on_round, free))
+        series.extend(self._finish(pending, n_test, on_round, free))
         th.join()
         self.round += rounds
-        self.now = series[-1][0]
+        self.now = pending.t0 + pending.report.makespan
         return series
 
-    def _finish(self, p: RoundPlan, n_test: int, on_round, free) -> tuple[float, float]:
-        correct = self.read_correct(p.slot)
+    def _finish(self, p: RoundPlan, n_test: int, on_round, free) -> list:
+        self._result_ev[p.slot].synchronize()
+        counts = self._correct_pin[p.slot].numpy().copy()
         free.put(p.slot)
-        acc = correct / n_test if n_test else 0.0
-        if on_round is not None:
-            on_round(p, acc)
-        return (p.t0 + p.report.makespan, acc)
+        return self._series_entries(p, counts, n_test, on_round)

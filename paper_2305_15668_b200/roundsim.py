@@ -228,6 +228,10 @@ class LeanRoundReport:
         self._raw = (pid, launch, upload, starts, ends, par_t, par_n, budget)
         self._full = None
 
+    def end_times(self) -> np.ndarray:
+        """ModelUploaded times in participant order (per_client_end without the dict)."""
+        return self._raw[4]
+
     def full(self) -> RoundReport:
         if self._full is None:
             pid, launch, upload, starts, ends, par_t, par_n, budget = self._raw

@@ -674,6 +674,33 @@ def test_runner_device_plan_matches_host_plan(fh):
         assert outs[0][1] == o[1]
 
 
+def test_runner_async_native_matches_python_path(fh):
+    """Async aggregation (engine.py:354-364) in the native round loop (chunked FedAvg on the params, per-chunk
+    snapshots evaluated on the side stream) == the Python launch path (per-chunk FedAvg + accuracy in stream
+    order), bit for bit, and run(1) + run(2) == run(3)."""
+    import torch
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.experiment import FederatedRunner
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=(10, 30, 50, 80), num_samples=[320, 640, 700],
+                                                  batch_size=[32, 64]), 24, 4)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, 10, 0.5, seed=3, n_test=2000)
+    outs = []
+    for native, buf, split_calls in ((True, 3, False), (False, 3, False), (True, 3, True), (True, 16, False)):
+        cfg = fh.FleetConfig(participants_per_round=16, max_executors=8, seed=4, aggregation="async",
+                             async_buffer=buf)
+        params = torch.zeros(7850, dtype=torch.float64, device="cuda")
+        r = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, native=native)
+        assert (r._native is not None) == native
+        series = r.run(1) + r.run(2) if split_calls else r.run(3)
+        assert len(series) == 3 * -(-16 // buf)
+        outs.append((params.clone(), series, r.now))
+    for o in outs[1:3]:
+        assert torch.equal(outs[0][0], o[0]) and outs[0][1] == o[1] and outs[0][2] == o[2]
+    assert outs[3][2] == outs[0][2]  # one chunk of all 16: the same DES times
+
+
 @pytest.mark.parametrize("a_mn", [False, True])
 def test_gemm_strided_operands_vs_torch(fh, a_mn):
     """Row strides (fedhc_gemm_args.lda / ldd): A read as a column slice of a wider row-major tensor (the

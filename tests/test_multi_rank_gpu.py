@@ -23,7 +23,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def _setup():
+def _setup(aggregation="sync"):
     import torch
     import paper_2305_15668_b200 as fh
     from paper_2305_15668_b200.devicedata import DeviceFleetData
@@ -34,11 +34,12 @@ def _setup():
     by_id = {p.client_id: p for p in fleet}
     ids = sorted(by_id)
     data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, 10, 0.5, seed=5, n_test=1999)
-    cfg = fh.FleetConfig(participants_per_round=17, max_executors=8, seed=11)
+    cfg = fh.FleetConfig(participants_per_round=17, max_executors=8, seed=11, aggregation=aggregation,
+                         async_buffer=4)
     return fh, by_id, data, cfg
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, aggregation):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -47,7 +48,7 @@ def _worker(rank, world, port, out_dir):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    fh, by_id, data, cfg = _setup()
+    fh, by_id, data, cfg = _setup(aggregation)
     params = torch.zeros(7850, dtype=torch.float64, device="cuda")
     runner = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params, world=world, rank=rank)
     series = runner.run(ROUNDS)
@@ -59,17 +60,25 @@ def _worker(rank, world, port, out_dir):
 
 
 @pytest.mark.timeout(600)
-def test_two_rank_runner_matches_single_rank(tmp_path):
+@pytest.mark.parametrize("aggregation", ["sync", "async"])
+def test_two_rank_runner_matches_single_rank(tmp_path, aggregation):
+    """Sync: one all-reduce per round.  Async (engine.py:354-364, async_buffer 4): one all-reduce of the chunk's
+    partial sums and one sharded accuracy per chunk; the world = 1 run is the native round loop."""
     import torch
     import torch.multiprocessing as mp
     from paper_2305_15668_b200.experiment import FederatedRunner
 
-    fh, by_id, data, cfg = _setup()
+    fh, by_id, data, cfg = _setup(aggregation)
     params = torch.zeros(7850, dtype=torch.float64, device="cuda")
-    want_series = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params).run(ROUNDS)
+    runner = FederatedRunner(data.federation(), by_id, cfg, 0.1, params=params)
+    assert runner._native is not None
+    want_series = runner.run(ROUNDS)
     want = params.cpu().numpy()
+    if aggregation == "async":
+        assert len(want_series) == ROUNDS * 5  # ceil(17 / 4) chunks per round
 
-    mp.start_processes(_worker, args=(2, free_port(), str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(2, free_port(), str(tmp_path), aggregation), nprocs=2, join=True,
+                       start_method="spawn")
     for rank in range(2):
         got = np.load(tmp_path / f"rank{rank}.npz")
         assert np.max(np.abs(got["params"] - want)) <= 1e-12 * np.max(np.abs(want))
