@@ -404,7 +404,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": "bf16x3",  # bf16 hi/mid products (hi*hi + hi*mid + mid*hi), fp32 accumulate and SGD state
         "data": "synthetic, generated in HBM: Gaussian class clusters + Dirichlet(0.5) non-IID client label mix "
                 "(reference distributions, not the reference's RNG stream)",
         "config": workload_config(world),
