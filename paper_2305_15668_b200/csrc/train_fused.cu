@@ -1055,7 +1055,11 @@ struct Pipe2Ctx {
 };
 
 // One compute warp's whole local-SGD loop: NK k8 feature slices starting at slice s0.
-template <int NK>
+// MODE (forward class tiles): 2 = classes 0-7 and 8-15 (C <= 16, 6 mma.sync per k16 step); 1 = 8 < C <= 12:
+// the second n8 tile packs [Wh 8..11 | Wm 8..11] against Xh and [Wh 8..11 | 0] against Xm, so the three
+// products of classes 8..11 cost 2 mma.sync instead of 3 (5 per k16 step) and lanes tq / tq ^ 2 add the two
+// halves; 0 = C <= 8: classes 0-7 only (3 per step).
+template <int NK, int MODE>
 __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int lane) {
   constexpr int S = kPStages;
   const int gq = lane >> 2, tq = lane & 3;
@@ -1065,6 +1069,17 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
   auto w_at = [&](int f, int c) -> float { return c < C ? static_cast<float>(x.params[(size_t)f * C + c]) : 0.f; };
   uint32_t wh[NK][2], wm[NK][2];
   float G[NK][4];
+  // MODE 1 operand of the packed tile: wm[j][1] <- [Wh 8..11 | Wm 8..11] (lanes gq >= 4 take the Wm of class
+  // 8 + gq - 4 from lane ^ 16); wh[j][1] already is [Wh 8..11 | 0] (classes >= C hold exact zeros)
+  auto pack = [&]() {
+    if constexpr (MODE == 1) {
+#pragma unroll
+      for (int j = 0; j < NK; ++j) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, wm[j][1], 16);
+        wm[j][1] = gq < 4 ? wh[j][1] : other;
+      }
+    }
+  };
   {
     float m0[4 * NK];
 #pragma unroll
@@ -1079,6 +1094,7 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
       G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
     }
     tmem_st_n<4 * NK>(x.tmem_w, m0);
+    pack();
   }
   __syncwarp();
   // fedhc_x_split rows: k8 slice u of a row = [hi 16 B | mid 16 B] at byte 32 u
@@ -1134,11 +1150,16 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
         uint32_t AH[4], AM[4];
         ldsm_x4(xa + 32 * j, AH);
         ldsm_x4(xa + 32 * j + mid_off, AM);
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          mma_bf16(acc[(j >> 1) & 1][nt], AH, wh[j][nt], wh[j + 1][nt]);
-          mma_bf16(acc[(j >> 1) & 1][nt], AH, wm[j][nt], wm[j + 1][nt]);
-          mma_bf16(acc[(j >> 1) & 1][nt], AM, wh[j][nt], wh[j + 1][nt]);
+        mma_bf16(acc[(j >> 1) & 1][0], AH, wh[j][0], wh[j + 1][0]);
+        mma_bf16(acc[(j >> 1) & 1][0], AH, wm[j][0], wm[j + 1][0]);
+        mma_bf16(acc[(j >> 1) & 1][0], AM, wh[j][0], wh[j + 1][0]);
+        if constexpr (MODE == 2) {
+          mma_bf16(acc[(j >> 1) & 1][1], AH, wh[j][1], wh[j + 1][1]);
+          mma_bf16(acc[(j >> 1) & 1][1], AH, wm[j][1], wm[j + 1][1]);
+          mma_bf16(acc[(j >> 1) & 1][1], AM, wh[j][1], wh[j + 1][1]);
+        } else if constexpr (MODE == 1) {
+          mma_bf16(acc[(j >> 1) & 1][1], AH, wm[j][1], wm[j + 1][1]);  // [Wh | Wm] of classes 8..11
+          mma_bf16(acc[(j >> 1) & 1][1], AM, wh[j][1], wh[j + 1][1]);  // [Wh | 0]
         }
       }
       if constexpr (NK & 1) {
@@ -1146,20 +1167,35 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
         uint32_t h0, h1, m0, m1;
         ldsm_x2(xa + 32 * jl, h0, h1);
         ldsm_x2(xa + 32 * jl + mid_off, m0, m1);
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          mma_bf16_k8(acc[1][nt], h0, h1, wh[jl][nt]);
-          mma_bf16_k8(acc[1][nt], h0, h1, wm[jl][nt]);
-          mma_bf16_k8(acc[1][nt], m0, m1, wh[jl][nt]);
+        mma_bf16_k8(acc[1][0], h0, h1, wh[jl][0]);
+        mma_bf16_k8(acc[1][0], h0, h1, wm[jl][0]);
+        mma_bf16_k8(acc[1][0], m0, m1, wh[jl][0]);
+        if constexpr (MODE == 2) {
+          mma_bf16_k8(acc[1][1], h0, h1, wh[jl][1]);
+          mma_bf16_k8(acc[1][1], h0, h1, wm[jl][1]);
+          mma_bf16_k8(acc[1][1], m0, m1, wh[jl][1]);
+        } else if constexpr (MODE == 1) {
+          mma_bf16_k8(acc[1][1], h0, h1, wm[jl][1]);
+          mma_bf16_k8(acc[1][1], m0, m1, wh[jl][1]);
         }
       }
       named_sync(2, kQSync);  // ZFREE: the softmax warps consumed the previous partials
+      float z1[4];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        float* zr = x.Zp + (size_t)(warp * kFRows + gq) * x.Zs + nt * 8 + 2 * tq;
-        *reinterpret_cast<float2*>(zr) = make_float2(acc[0][nt][0] + acc[1][nt][0], acc[0][nt][1] + acc[1][nt][1]);
+      for (int e = 0; e < 4; ++e) z1[e] = acc[0][1][e] + acc[1][1][e];
+      if constexpr (MODE == 1) {  // classes 8..11: the [Wh] half (cols 0-3) + the [Wm] half (cols 4-7, lane ^ 2)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) z1[e] += __shfl_xor_sync(0xffffffffu, z1[e], 2);
+      }
+      {
+        float* zr = x.Zp + (size_t)(warp * kFRows + gq) * x.Zs + 2 * tq;
+        *reinterpret_cast<float2*>(zr) = make_float2(acc[0][0][0] + acc[1][0][0], acc[0][0][1] + acc[1][0][1]);
         *reinterpret_cast<float2*>(zr + 8 * x.Zs) =
-            make_float2(acc[0][nt][2] + acc[1][nt][2], acc[0][nt][3] + acc[1][nt][3]);
+            make_float2(acc[0][0][2] + acc[1][0][2], acc[0][0][3] + acc[1][0][3]);
+        if (MODE == 2 || (MODE == 1 && tq < 2)) {
+          *reinterpret_cast<float2*>(zr + 8) = make_float2(z1[0], z1[1]);
+          *reinterpret_cast<float2*>(zr + 8 + 8 * x.Zs) = make_float2(z1[2], z1[3]);
+        }
       }
       named_arrive(1, kQSync);  // ZFULL
       if (prev_k >= 0) backward(prev_k, prev_st);
@@ -1183,6 +1219,7 @@ __device__ __forceinline__ void pipe2_compute(const Pipe2Ctx& x, int warp, int l
       G[j][0] = G[j][1] = G[j][2] = G[j][3] = 0.f;
     }
     tmem_st_n<4 * NK>(x.tmem_w, m);
+    pack();
   }
   named_sync(2, kQSync);  // match the softmax warps' last ZFREE arrival
   // ---- delta = W_final - W_initial for this warp's slices ----
@@ -1243,8 +1280,16 @@ __global__ void __launch_bounds__(kQThreads, 1)
   if (warp < kQWarps) {
     Pipe2Ctx x{&cl, params, Zp, full, empty, smem_u32(Xb), smem_u32(Eb),
                *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + 36 * (warp >> 2), F, C, g.Fs, g.Zs, steps};
-    if (q_slices(warp) == 9) pipe2_compute<9>(x, warp, lane);
-    else pipe2_compute<8>(x, warp, lane);
+    const int mode = C <= 8 ? 0 : C <= 12 ? 1 : 2;
+    if (q_slices(warp) == 9) {
+      if (mode == 0) pipe2_compute<9, 0>(x, warp, lane);
+      else if (mode == 1) pipe2_compute<9, 1>(x, warp, lane);
+      else pipe2_compute<9, 2>(x, warp, lane);
+    } else {
+      if (mode == 0) pipe2_compute<8, 0>(x, warp, lane);
+      else if (mode == 1) pipe2_compute<8, 1>(x, warp, lane);
+      else pipe2_compute<8, 2>(x, warp, lane);
+    }
   } else if (warp == kQProd) {
     // ===== producer: row gather, indices two stages ahead, labels one ahead (see train_pipe_kernel) =====
     StageIter it0(n, B, steps), it1 = it0, it2 = it0;

@@ -66,6 +66,9 @@ def test_local_train_golden_cases(tr, i):
     (784, 10, 100, 100, 32),     # ragged last batch (100 = 3*32 + 4)
     (784, 32, 256, 256, 64),     # NT=4 fast path
     (784, 3, 128, 128, 64),      # NT=1
+    (784, 8, 200, 200, 64),      # split-row trainer, classes 0-7 only
+    (784, 12, 200, 300, 64),     # split-row trainer, packed [Wh | Wm] tile of classes 8..11, reshuffle
+    (784, 16, 256, 256, 64),     # split-row trainer, two class tiles
     (784, 62, 256, 256, 64),     # FEMNIST 62 classes (4-CTA cluster, softmax merged over DSMEM)
     (784, 62, 100, 300, 64),     # 62 classes, ragged + reshuffle
     (784, 20, 128, 128, 64),     # 2-CTA cluster, partial second class slice
