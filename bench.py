@@ -488,7 +488,7 @@ def kernel_subline(C_, F_, n_clients, n_samp, rounds, warm, fleet_seed=1):
     train_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
     steps = n_clients * math.ceil(n_samp / BATCH)
     bytes_launch = n_clients * math.ceil(n_samp / BATCH) * BATCH * (4 * F_ + 8) + n_clients * P * 12
-    kern = "train_tc_kernel" if (F_ > 784 or C_ > 32) else "train_pipe_kernel"
+    kern = ("train_c64_kernel" if F_ <= 784 else "train_tc_kernel") if (F_ > 784 or C_ > 32) else "train_pipe_kernel"
     return {"workload": f"femnist-logreg F={F_}, C={C_}: {n_clients} clients x {n_samp} samples, B={BATCH}, "
                         f"local SGD + FedAvg (device-resident rounds)",
             "value": steps / (ms / 1e3), "unit": "client-steps/s", "ms_per_round": ms, "train_kernel_ms": train_ms,

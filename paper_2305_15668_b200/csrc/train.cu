@@ -149,6 +149,8 @@ __global__ void lg_grad_kernel(const double* __restrict__ x, const double* __res
 }  // namespace fedhc
 
 namespace fedhc {
+bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
+                      int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status);
 bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
                      int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status);
 bool launch_train_fused(const fedhc_client* clients, int n_clients, const double* params, int F, int C,
@@ -199,6 +201,9 @@ static int local_train_impl(const fedhc_client* clients, int n_clients, const do
   FEDHC_CUDA_TRY(cudaGetDevice(&dev));
   FEDHC_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   int fused_status = FEDHC_OK;
+  if (launch_train_c64(clients, n_clients, params, n_features, n_classes, max_batch, max_smem, split, split_off, st,
+                       &fused_status))
+    return fused_status;
   if (launch_train_tc(clients, n_clients, params, n_features, n_classes, max_batch, max_smem, split, split_off, st,
                       &fused_status))
     return fused_status;

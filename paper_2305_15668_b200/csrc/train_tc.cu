@@ -34,9 +34,11 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tc5.cuh"
 
 namespace fedhc {
 namespace ltc {
+using namespace tc5;
 
 constexpr int kRows = 64;          // rows per SGD step (B <= 64)
 constexpr int kStageRows = 16;
@@ -64,160 +66,6 @@ __device__ __forceinline__ void trace_pt(const TcGeom& g, uint32_t crank, int s,
 }
 
 enum { B_XS_FULL = 0, B_XS_FREE, B_W_READY, B_Z_FULL, B_E_FULL, B_G_FULL, B_ZX_READY, B_E_READY, kFixedBars };
-
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// SWIZZLE_128B shared-memory matrix descriptor (K-major: 8-row groups 1024 B apart; MN-major: 64-element
-// atoms `lbo` bytes apart, 8-row K groups 1024 B apart).
-__device__ __forceinline__ uint64_t sw128(uint32_t addr, uint32_t lbo) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-
-__device__ __forceinline__ void commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-#define FEDHC_TLD16(addr, v, o)                                                                                  \
-  asm volatile(                                                                                                   \
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"     \
-      : "=f"(v[o + 0]), "=f"(v[o + 1]), "=f"(v[o + 2]), "=f"(v[o + 3]), "=f"(v[o + 4]), "=f"(v[o + 5]),            \
-        "=f"(v[o + 6]), "=f"(v[o + 7]), "=f"(v[o + 8]), "=f"(v[o + 9]), "=f"(v[o + 10]), "=f"(v[o + 11]),          \
-        "=f"(v[o + 12]), "=f"(v[o + 13]), "=f"(v[o + 14]), "=f"(v[o + 15])                                       \
-      : "r"(addr))
-
-#define FEDHC_TST16(addr, v, o)                                                                                  \
-  asm volatile(                                                                                                   \
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::  \
-          "r"(addr),                                                                                              \
-      "f"(v[o + 0]), "f"(v[o + 1]), "f"(v[o + 2]), "f"(v[o + 3]), "f"(v[o + 4]), "f"(v[o + 5]), "f"(v[o + 6]),      \
-      "f"(v[o + 7]), "f"(v[o + 8]), "f"(v[o + 9]), "f"(v[o + 10]), "f"(v[o + 11]), "f"(v[o + 12]), "f"(v[o + 13]), \
-      "f"(v[o + 14]), "f"(v[o + 15])                                                                               \
-      : "memory")
-
-template <int N>
-__device__ __forceinline__ void tld_row(uint32_t addr, float (&v)[N]) {
-  FEDHC_TLD16(addr, v, 0);
-  if constexpr (N >= 32) FEDHC_TLD16(addr + 16, v, 16);
-  if constexpr (N >= 64) {
-    FEDHC_TLD16(addr + 32, v, 32);
-    FEDHC_TLD16(addr + 48, v, 48);
-  }
-  if constexpr (N >= 128) {
-    FEDHC_TLD16(addr + 64, v, 64);
-    FEDHC_TLD16(addr + 80, v, 80);
-    FEDHC_TLD16(addr + 96, v, 96);
-    FEDHC_TLD16(addr + 112, v, 112);
-  }
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-template <int N>
-__device__ __forceinline__ void tst_row(uint32_t addr, const float (&v)[N]) {
-  FEDHC_TST16(addr, v, 0);
-  if constexpr (N >= 32) FEDHC_TST16(addr + 16, v, 16);
-  if constexpr (N >= 64) {
-    FEDHC_TST16(addr + 32, v, 32);
-    FEDHC_TST16(addr + 48, v, 48);
-  }
-}
-
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ uint32_t ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-
-__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-
-__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WC_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ float4 ld_dsmem4(uint32_t cluster_addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(cluster_addr)
-               : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void sts4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
-__device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
-  asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
-
-// bf16 hi / mid halves of x (round to nearest): x ~= hi + mid, |x - hi - mid| <= 2^-17 |x|
-__device__ __forceinline__ void split1(float x, uint16_t& hi, uint16_t& mid) {
-  uint32_t h, m;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(0.f), "f"(x));
-  const float r = x - __uint_as_float(h << 16);
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(m) : "f"(0.f), "f"(r));
-  hi = (uint16_t)h;
-  mid = (uint16_t)m;
-}
-
-__device__ __forceinline__ void st_dsmem(uint32_t cluster_addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
-}
-
-__device__ __forceinline__ void st_dsmem4(uint32_t cluster_addr, float4 v) {
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
-
-// Asynchronous DSMEM stores that count their bytes on the DESTINATION CTA's mbarrier (no fence, no remote arrive).
-__device__ __forceinline__ void st_async4(uint32_t cluster_addr, float4 v, uint32_t cluster_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                   cluster_addr),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(cluster_bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void st_async1(uint32_t cluster_addr, float v, uint32_t cluster_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(cluster_addr), "f"(v),
-               "r"(cluster_bar)
-               : "memory");
-}
 
 // W[feature fl][0..NP) -> the forward's B operand chunk (64 features x [Wh NP | Wm NP], bf16).
 // NP >= 32: MN-major (the 2 NP classes of a feature are contiguous: 64-class SW128 atoms 8 KB apart, a

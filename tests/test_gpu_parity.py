@@ -69,8 +69,12 @@ def test_local_train_golden_cases(tr, i):
     (784, 8, 200, 200, 64),      # split-row trainer, classes 0-7 only
     (784, 12, 200, 300, 64),     # split-row trainer, packed [Wh | Wm] tile of classes 8..11, reshuffle
     (784, 16, 256, 256, 64),     # split-row trainer, two class tiles
-    (784, 62, 256, 256, 64),     # FEMNIST 62 classes (4-CTA cluster, softmax merged over DSMEM)
+    (784, 62, 256, 256, 64),     # FEMNIST 62 classes (2-CTA tcgen05 trainer, master in TMEM, SW32 tail)
     (784, 62, 100, 300, 64),     # 62 classes, ragged + reshuffle
+    (744, 50, 150, 300, 64),     # 2-CTA trainer: partial SW128 last chunk (40 features)
+    (200, 40, 120, 240, 48),     # 2-CTA trainer: lone chunk tile + 8-feature SW32 tail, B not a multiple of 16
+    (128, 33, 64, 64, 64),       # 2-CTA trainer: one chunk per CTA
+    (72, 64, 90, 90, 30),        # 2-CTA trainer: CTA 1 holds only the tail
     (784, 20, 128, 128, 64),     # 2-CTA cluster, partial second class slice
     (392, 40, 96, 96, 32),       # cluster path, F not filling all warps
     (64, 10, 200, 300, 50),      # small F, B not a multiple of 16
