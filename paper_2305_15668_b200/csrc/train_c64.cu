@@ -1,31 +1,38 @@
 // Per-client local SGD for 32 < C <= 64 classes at F <= 784 on the 5th-generation tensor cores --
 // fl_core.local_train (fl_core.py:163-194) at FEMNIST's 62 classes.
 //
-// A client is a 2-CTA cluster that splits the FEATURES in 64-feature chunks (F = 784: CTA 0 chunks 0-5,
-// CTA 1 chunks 6-11 + a 16-feature tail), so 74 clients run at once on 148 SMs.  Per CTA:
+// The model is treated as W' = [W; b] ((F + 1) x C: exactly the reference's flat parameter vector, fl_core.py:
+// 126-129) on rows X' = [X, 1]: the bias is feature F, whose column the loaders synthesise, so the forward adds
+// it and the backward updates it with everything else.  A client is a 2-CTA cluster that splits the F + 8
+// features (the bias unit padded to 8) in 64-feature chunks plus SW32 "tail" tiles of <= 16 features
+// (F = 784: CTA 0 chunks 0-5 + features 768-775, CTA 1 chunks 6-11 + features 776-791), so 74 clients run at
+// once on 148 SMs.  Per CTA:
 //
-//   TMEM   the fp32 master W of the CTA's features (lane = feature of a 128-feature tile, 64 class columns
-//          per tile) and the partial logits Z (64 columns).  The backward MMAs accumulate straight into the
-//          master: with E' = -lr (P - Y) / nb the SGD step W -= lr X^T (P - Y) / nb (fl_core.py:193) is
-//          D_master += X^T E' -- no gradient tile, no update pass.
-//   smem   the step's rows X (bf16 hi / mid split, SW128 K-major chunks, loaded ONCE per step by 16-byte
-//          LDGSTS straight from the fedhc_x_split rows into the swizzled positions), the forward's W operand
-//          (bf16 hi / mid, MN-major), E' (bf16 hi / mid, MN-major) and the peer's partial logits.
+//   TMEM   Z (128 stacked hi / mid rows x [Wh | Wm] class halves) and the fp32 master W of the CTA's chunk
+//          features as pair tiles (lane = feature of 128, 64 class columns).  The backward MMAs accumulate
+//          straight into the master: with E' = -lr (P - Y) / nb the SGD step W -= lr X^T (P - Y) / nb
+//          (fl_core.py:193) is W += Xh^T E'h + Xh^T E'm + Xm^T E'h -- no gradient tile, no update pass.
+//   smem   the step's rows X (bf16 hi / mid split, SW128 K-major chunks + the SW32 tail, loaded ONCE per step
+//          straight from the fedhc_x_split rows), the forward's W operand (bf16 hi / mid, MN-major), the tail's
+//          master as hi / mid / lo bf16 planes, E' (bf16 hi / mid, MN-major) and the peer's partial logits.
 //
 // Per SGD step (B <= 64 rows):
-//   forward   Z_k = [Xh; Xm] Wh + [Xh; Xm] Wm over the CTA's chunks (M = 128 stacked hi / mid rows, N = 64)
+//   forward   Z_k = [Xh; Xm] [Wh | Wm] over the CTA's chunks and tail (M = 128 stacked rows, N = 128)
 //   exchange  CTA k owns rows [32k, 32k+32): each CTA pushes the other's rows of its partial Z with st.async
-//             (bytes counted on the receiver's mbarrier); the owner adds bias, takes the max-shifted softmax,
-//             writes E' split into hi / mid and pushes the rows to the peer the same way
-//   backward  D_master[tile] += Xh^T E'h + Xh^T E'm + Xm^T E'h  (A = MN-major views of the same X chunks)
+//             (bytes counted on the receiver's mbarrier); the owner takes the max-shifted softmax on 8 lanes
+//             per row, writes E' split into hi / mid and pushes the rows to the peer the same way
+//   backward  tail first, into Z's (now free) columns: G_t = (Xh + Xm)^T [E'h | E'm], added to the tail master
+//             by the Q warps; then W_tile += Xh^T E'h + Xh^T E'm + Xm^T E'h per pair tile (A = MN-major views
+//             of the same X chunks)
 //   refill    as soon as a tile's backward MMAs complete, its X chunks are reloaded with the next step's rows
 //             (prefetched into L2 one step ahead) and the Q warps re-split its master into the W operand.
 //
-// Accuracy: bf16x3 products (hi*hi + hi*mid + mid*hi, plus mid*mid in the forward), fp32 accumulation and
-// fp32 master -- the arithmetic of the other trainers, within the north_star 1e-4 bar of the fp64 reference.
+// Accuracy: bf16x3 products (hi*hi + hi*mid + mid*hi, plus mid*mid), fp32 accumulation and fp32 masters (the
+// tail's as hi + mid + lo bf16, 24 significant bits) -- the arithmetic of the other trainers, within the
+// north_star 1e-4 bar of the fp64 reference.
 //
-// Roles (13 warps): 0-3 loaders (LDGSTS, one (row, plane) per thread), 4 MMA issuer (+ TMEM owner),
-// 5-12 "Q" warps (two per TMEM lane quadrant, one per 32-column half): Z readout, softmax, W re-split, delta.
+// Roles (16 warps): 0-6 loaders (warp j fills X tile j), 7 MMA issuer (+ TMEM owner), 8-15 "Q" warps (two per
+// TMEM lane quadrant, one per 32-column half): Z readout, softmax, tail update, W re-split, delta.
 #include <float.h>
 #include <stdlib.h>
 #include <string.h>
@@ -41,39 +48,41 @@ namespace c64 {
 using namespace tc5;
 
 constexpr int kRows = 64, NP = 64;
-constexpr int kWarps = 13, kThreads = kWarps * 32;
-constexpr int kLoadWarps = 4, kMmaWarp = 4, kQ0 = 5;
+constexpr int kMaxCh = 7;
+constexpr int kWarps = 16, kThreads = kWarps * 32;
+constexpr int kLoadWarps = kMaxCh, kMmaWarp = 7, kQ0 = 8;  // loader warp j fills X tile j
 constexpr int kChunk = 16384;  // SW128 K-major chunk: [Xh 64 rows x 128 B | Xm 64 rows x 128 B] (W op: MN-major)
 constexpr int kTail = 4096;    // SW32 tail: [Xh 64 rows x 32 B | Xm 64 rows x 32 B]; W op tail [Wh 16 | Wm 16] x 128 B
-constexpr int kMaxCh = 7, kMaxTiles = 4;
-constexpr int kBarQ = 1, kBarSm = 2;  // named barriers: the 8 Q warps; the 2 softmax warps
+constexpr int kTailLo = 2048;  // the tail master's lo plane (16 features x 128 B, the W operand's layout)
+constexpr int kBarQ = 1;       // named barrier of the 8 Q warps
 constexpr uint32_t kSW128 = 2, kSW32 = 6;
 
-enum { B_XF = 0, B_WR = B_XF + kMaxCh, B_BD = B_WR + kMaxCh, B_ZF = B_BD + kMaxTiles, B_EF, B_ZX, B_ER, kBars };
+// B_BD + t: pair tile t's backward MMAs done (t < 3); B_TD: the tail's gradient MMAs done; B_TR: the Q warps
+// have read the tail gradient out of Z's columns (the next forward may overwrite them)
+// B_ST: the next step's rows have landed in the staging area; B_RL: the chunk loaders have re-laid them out
+enum {
+  B_XF = 0, B_WR = B_XF + kMaxCh, B_BD = B_WR + kMaxCh, B_TD = B_BD + 3, B_TR, B_ZF, B_EF, B_ZX, B_ER, B_ST, B_RL,
+  kBars
+};
 
 struct Geom {
   int F, C;
-  int nc[2];    // SW128 chunks of CTA k (the last may be partial)
-  int tail[2];  // CTA k ends with a SW32 tail tile (<= 16 features)
-  int f0[2];    // first feature of CTA k
-  int nf[2];    // features of CTA k
+  int nc[2];     // SW128 chunks of CTA k: features [f0, f0 + nfull) (the last chunk may be partial)
+  int f0[2];
+  int nfull[2];
+  int ft[2];     // SW32 tail tile of CTA k: features [ft, ft + tn), tn <= 16 (0: none)
+  int tn[2];
   long long split_off;
-  int off_x, off_w, off_e, off_zr, off_red, off_bias, off_bar, off_tmem, bytes;
+  int prefetch;               // L2 prefetch of the next step's rows (FEDHC_C64_PREFETCH=0 disables, for A/B)
+  unsigned long long* trace;  // FEDHC_TC_TRACE: %globaltimer phase points of cluster 0 [cta][step][32], else null
+  int off_x, off_w, off_e, off_zr, off_bar, off_tmem, bytes;
 };
 
-// Local feature of TMEM lane L in master tile t (-1: no feature).  Tiles 0..ntp-1 pair chunks (2t, 2t+1)
-// (lane L -> chunk 2t + L/64); tile ntp is the SW32 tail (lanes 0..15).
-__device__ __forceinline__ int tile_feature(int t, int L, int nc, int ntp, int nf) {
-  int f;
-  if (t < ntp) {
-    const int j = 2 * t + (L >> 6);
-    if (j >= nc) return -1;
-    f = 64 * j + (L & 63);
-  } else {
-    if (L >= 16) return -1;
-    f = 64 * nc + L;
-  }
-  return f < nf ? f : -1;
+// Local feature of TMEM lane L in pair tile t (-1: none): tile t pairs chunks (2t, 2t+1), lane L -> chunk
+// 2t + L/64, local feature 64 j + L % 64 < nfull; global feature f0 + f.
+__device__ __forceinline__ int tile_feature(int t, int L, int nc, int nfull) {
+  const int j = 2 * t + (L >> 6), f = 64 * j + (L & 63);
+  return j < nc && f < nfull ? f : -1;
 }
 
 // Scratch row of the partial-logit hi / mid reduction inside the E' region: row r lies where only rows of the
@@ -83,70 +92,108 @@ __device__ __forceinline__ uint32_t scratch_row(uint32_t s_e, int r) {
   return s_e + ((r >> 4) & 1) * 8192 + (r >> 5) * 4096 + (r & 15) * 256;
 }
 
-// The forward's W operand row of local feature f (MN-major SW128: a feature = one 128-byte row of 64 classes
-// per plane), classes [32h, 32h + 32) from w[].
-__device__ __forceinline__ void write_wop(uint32_t s_w, int nc, int f, int h, const float (&w)[32]) {
-  const int j = f >> 6;
-  const bool tail = j >= nc;
-  const int fe = tail ? f - 64 * nc : (f & 63);
-  const uint32_t row = s_w + (tail ? nc * kChunk : j * kChunk) + (fe >> 3) * 1024 + (fe & 7) * 128;
-  const uint32_t mid_off = tail ? 2048 : 8192;
+// A W-operand row (MN-major SW128: feature fe = one 128-byte row of 64 classes per plane, planes `plane` bytes
+// apart), classes [32h, 32h + 32): hi / mid split of w[] (and, with lo_row != 0, the residual's bf16 into a
+// third plane: the tail master).
+__device__ __forceinline__ uint32_t wop_row(uint32_t base, int fe) { return base + (fe >> 3) * 1024 + (fe & 7) * 128; }
+__device__ __forceinline__ void write_wop(uint32_t row, int fe, uint32_t plane, int h, const float (&w)[32],
+                                          uint32_t lo_row = 0) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    uint32_t hw[4], mw[4];
+    uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) split_bf16x2(w[8 * k + 2 * e], w[8 * k + 2 * e + 1], hw[e], mw[e]);
-    const uint32_t a = row + (((4 * h + k) ^ (fe & 7)) << 4);
-    sts4(a, hw[0], hw[1], hw[2], hw[3]);
-    sts4(a + mid_off, mw[0], mw[1], mw[2], mw[3]);
+    for (int e = 0; e < 4; ++e) {
+      const float x0 = w[8 * k + 2 * e], x1 = w[8 * k + 2 * e + 1];
+      split_bf16x2(x0, x1, hw[e], mw[e]);
+      if (lo_row) {
+        const float r0 = x0 - __uint_as_float(hw[e] << 16) - __uint_as_float(mw[e] << 16);
+        const float r1 = x1 - __uint_as_float(hw[e] & 0xffff0000u) - __uint_as_float(mw[e] & 0xffff0000u);
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lw[e]) : "f"(r1), "f"(r0));
+      }
+    }
+    const uint32_t off = ((4 * h + k) ^ (fe & 7)) << 4;
+    sts4(row + off, hw[0], hw[1], hw[2], hw[3]);
+    sts4(row + plane + off, mw[0], mw[1], mw[2], mw[3]);
+    if (lo_row) sts4(lo_row + off, lw[0], lw[1], lw[2], lw[3]);
+  }
+}
+// The tail master's classes [32h, 32h + 32) of feature fe: hi + mid + lo.
+__device__ __forceinline__ void read_tail_master(uint32_t row, int fe, uint32_t plane, uint32_t lo_row, int h,
+                                                 float (&w)[32]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t off = ((4 * h + k) ^ (fe & 7)) << 4;
+    uint4 a, b, c;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "r"(row + off));
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "r"(row + plane + off));
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w)
+                 : "r"(lo_row + off));
+    const uint32_t hv[4] = {a.x, a.y, a.z, a.w}, mv[4] = {b.x, b.y, b.z, b.w}, lv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      w[8 * k + 2 * e] = __uint_as_float(hv[e] << 16) + __uint_as_float(mv[e] << 16) + __uint_as_float(lv[e] << 16);
+      w[8 * k + 2 * e + 1] = __uint_as_float(hv[e] & 0xffff0000u) + __uint_as_float(mv[e] & 0xffff0000u) +
+                             __uint_as_float(lv[e] & 0xffff0000u);
+    }
   }
 }
 
-__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+constexpr int kTraceSteps = 32, kTracePts = 32;
+__device__ __forceinline__ void trace_pt(const Geom& g, uint32_t crank, int s, int pt) {
+  if (g.trace != nullptr && blockIdx.x < 2 && s < kTraceSteps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g.trace[((size_t)crank * kTraceSteps + s) * kTracePts + pt] = t;
+  }
+}
 
-__global__ void __maxnreg__(128)  // 13 warps: 4 share an SM sub-partition (4 x 32 x 128 = its 16K registers)
+__device__ __forceinline__ float4 lds4f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 
+// 16 warps: 4 share an SM sub-partition, so 128 registers per thread is the ceiling (4 x 32 x 128 = its 16K)
+__global__ void __maxnreg__(128)
     train_c64_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const Geom g) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t pad = (1024u - (raw & 1023u)) & 1023u;
-  unsigned char* smem = smem_raw + pad;
-  const uint32_t sb = raw + pad;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const uint32_t sb = smem_u32(smem);
+  if (sb & 1023u) __trap();  // the SW128 tiles are laid out from a 1024-byte aligned base (no slack allocated)
   const uint32_t s_x = sb + g.off_x, s_w = sb + g.off_w, s_e = sb + g.off_e, s_zr = sb + g.off_zr;
-  float* red = reinterpret_cast<float*>(smem + g.off_red);  // [max / sum][half][32 rows]
-  float* bias = reinterpret_cast<float*>(smem + g.off_bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.off_bar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + g.off_tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = ctarank(), peer = crank ^ 1u;
   const fedhc_client cl = clients[blockIdx.x >> 1];
-  const int F = g.F, C = g.C;
-  const int nc = g.nc[crank], has_tail = g.tail[crank], f0 = g.f0[crank], nf = g.nf[crank];
-  const int nch = nc + has_tail;  // X / W operand tiles: chunks 0..nc-1, then the tail
-  const int ntp = (nc + 1) / 2;   // chunk-pair master tiles
-  const int NT = ntp + has_tail;
+  const int F = g.F, C = g.C, FB = F + 1;  // FB: features of W' = [W; b]
+  const int nc = g.nc[crank], f0 = g.f0[crank], nfull = g.nfull[crank], ft = g.ft[crank], tn = g.tn[crank];
+  const int nch = nc + (tn > 0 ? 1 : 0);  // X / W operand tiles: chunks 0..nc-1, then the tail
+  const int ntp = (nc + 1) / 2;           // chunk-pair master tiles in TMEM
   const int n = cl.n_rows, B = cl.batch_size;
   const int steps = n > 0 ? cl.n_batches : 0;
   const float lr = cl.lr;
-  const uint32_t tail_x = s_x + nc * kChunk, tail_w = s_w + nc * kChunk;
+  const uint32_t tail_x = s_x + nc * kChunk, tail_w = s_w + nc * kChunk, tail_lo = tail_w + kTail;
 
   // ---- setup -------------------------------------------------------------------------------------
-  for (int i = tid; i < (g.off_bar - g.off_x) / 16; i += kThreads)  // X, W operand, E', receive buffers, bias
+  for (int i = tid; i < (g.off_bar - g.off_x) / 16; i += kThreads)  // X, W operand, E', receive buffer
     reinterpret_cast<uint4*>(smem + g.off_x)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  if (tid < C) bias[tid] = static_cast<float>(params[(size_t)F * C + tid]);
   if (tid == 0) {
     for (int j = 0; j < kMaxCh; ++j) {
-      mbar_init(&bars[B_XF + j], kLoadWarps);
-      mbar_init(&bars[B_WR + j], 4);
+      mbar_init(&bars[B_XF + j], 1);
+      mbar_init(&bars[B_WR + j], j == nc ? 2 : 4);  // chunks: two quadrants x two halves; the tail: quadrant 0
     }
-    for (int t = 0; t < kMaxTiles; ++t) mbar_init(&bars[B_BD + t], 1);
+    for (int t = 0; t < 3; ++t) mbar_init(&bars[B_BD + t], 1);
+    mbar_init(&bars[B_TD], 1);
+    mbar_init(&bars[B_TR], 2);
     mbar_init(&bars[B_ZF], 1);
-    mbar_init(&bars[B_EF], 2);
+    mbar_init(&bars[B_EF], 8);
     mbar_init(&bars[B_ZX], 1);  // local arrive.expect_tx + the peer's st.async bytes
     mbar_init(&bars[B_ER], 1);
+    mbar_init(&bars[B_ST], 1);
+    mbar_init(&bars[B_RL], nc > 0 ? nc : 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -160,143 +207,249 @@ __global__ void __maxnreg__(128)  // 13 warps: 4 share an SM sub-partition (4 x 
   cluster_sync();  // the peer's barriers are initialised before any st.async reaches them
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_z = tmem, t_w = tmem + 64;
+  // TMEM: Z [128 rows x (Wh | Wm) class halves] (also the tail gradient's home between the softmax and the next
+  // forward); pair tile t's master at 2 NP + NP t
+  const uint32_t t_z = tmem, t_w = tmem + 2 * NP;
 
   if (warp < kLoadWarps) {
-    // ---- loaders: thread = (row, plane); 16-byte LDGSTS from the split row into the swizzled chunk ------
-    const int row = tid >> 1, p = tid & 1;
-    const char* xs = reinterpret_cast<const char*>(cl.x) + g.split_off;
+    // ---- loaders: warp j fills X tile j (chunk j, or the tail for j = nc) each step: lane = (8-feature unit u,
+    // plane p, row parity r0), 32 rows r0 + 2i by 16-byte LDG (16 in flight) + swizzled STS -- the LDGSTS path
+    // gathers these 256-byte row segments at half the rate (tools/microbench/ldgsts_bench.cu).  The bias
+    // feature's unit (global unit F / 8) is synthesised: x = (1, 0, ..., 0) for every live row.
+    const int j = warp;
+    const bool active = j < nch;
+    const bool tail = j >= nc;
+    const int u = lane & 7, p = (lane >> 3) & 1, r0 = lane >> 4;
     const size_t pitch = (size_t)F * 4;
-    const int nu_tail = has_tail ? (nf - 64 * nc + 7) / 8 : 0;  // valid 8-feature units of the tail
-    for (int s = 0; s < steps; ++s) {
+    const char* xsplit = reinterpret_cast<const char*>(cl.x) + g.split_off;
+    const int gf = tail ? ft + 8 * u : f0 + 64 * j + 8 * u;  // first global feature of the lane's unit
+    const bool uval = active && (tail ? 8 * u < tn : 64 * j + 8 * u < nfull);
+    const bool ubias = uval && gf == F;                        // the synthesised bias unit
+    const bool uload = uval && gf < F;
+    const char* src = xsplit + (size_t)(uload ? gf : 0) * 4 + p * 16;
+    const uint32_t dst = tail ? tail_x + p * 2048 : s_x + j * kChunk + p * 8192;
+    const uint4 one = make_uint4(p == 0 ? 0x3f80u : 0u, 0u, 0u, 0u);  // bf16 hi = 1.0 (feature F), mid = 0
+    int ix0 = -1, ix1 = -1;  // source rows 2 lane, 2 lane + 1 of the step (one step ahead)
+    auto load_idx = [&](int s) {
       const BatchRef br = batch_ref(s, n, B);
-      const bool live = row < br.rows;
-      const char* src = xs + (size_t)f0 * 4 + p * 16;
-      if (live) src += (size_t)cl.perm[br.perm_off + row] * pitch;
-      if (p == 0 && s + 1 < steps) {  // next step's slice of this row into L2
-        const BatchRef nb = batch_ref(s + 1, n, B);
-        if (row < nb.rows) prefetch_l2(xs + (size_t)cl.perm[nb.perm_off + row] * pitch + (size_t)f0 * 4, nf * 4);
-      }
-      for (int j = 0; j < nch; ++j) {
-        // chunk j still holds step s-1's rows until its master tile's backward MMAs are done
-        if (s > 0) mbar_wait(&bars[B_BD + (j < nc ? j >> 1 : ntp)], (s - 1) & 1);
-        if (live) {
-          if (j < nc) {
-            const int nu = min(8, (nf - 64 * j) >> 3);
-            const uint32_t dst = s_x + j * kChunk + p * 8192 + row * 128;
-            for (int u = 0; u < nu; ++u) cp_async16(dst + ((u ^ (row & 7)) << 4), src + (8 * j + u) * 32);
-          } else {
-            const uint32_t dst = tail_x + p * 2048 + row * 32;
-            for (int u = 0; u < nu_tail; ++u) cp_async16(dst + ((u ^ ((row >> 2) & 1)) << 4), src + (8 * nc + u) * 32);
+      ix0 = 2 * lane < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane) : -1;
+      ix1 = 2 * lane + 1 < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane + 1) : -1;
+    };
+    if (active && steps > 0) load_idx(0);
+    // staging (steps >= 1): the chunk part of each row, [f0, f0 + ncopy) features, lands by one bulk copy per row
+    // in the W operand's chunk region -- dead from the end of a forward (Z_FULL) until the split that follows the
+    // re-layout -- while the softmax and the backward run; after the backward the chunk warps re-lay it into the
+    // swizzled tiles (shared memory to shared memory) instead of gathering 256-byte row segments from L2
+    const int ncopy = max(0, min(nfull, F - f0));  // real features of the chunk part (the bias unit is synthesised)
+    const uint32_t spitch = (uint32_t)nfull * 4;
+    for (int s = 0; active && s < steps; ++s) {
+      if (tail || s == 0) {
+        // tile j still holds step s-1's rows until its backward MMAs are done
+        if (s > 0) mbar_wait(&bars[B_TD], (s - 1) & 1);
+        if (lane == 0) trace_pt(g, crank, s, 16 + j);
+#pragma unroll 1
+        for (int b = 0; b < 2; ++b) {
+          // every lane shuffles (the index pairs live in lane i) and loads unconditionally (rows past the batch
+          // end read row 0 and are stored as zeros; their E' rows are zero): a predicated load followed by a
+          // zero-fill of its register would wait for the load (WAW) and serialise the batch
+          uint4 v[16];
+          uint32_t live = 0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int i = 16 * b + k;
+            const int a0 = __shfl_sync(0xffffffffu, ix0, i), a1 = __shfl_sync(0xffffffffu, ix1, i);
+            const int rw = r0 ? a1 : a0;
+            live |= (rw >= 0 ? 1u : 0u) << k;
+            v[k] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)max(rw, 0) * pitch));
+          }
+          if (uval) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int row = r0 + 2 * (16 * b + k);
+              const uint32_t d = tail ? dst + row * 32 + ((u ^ ((row >> 2) & 1)) << 4) : dst + row * 128 + ((u ^ (row & 7)) << 4);
+              const bool lv = (live >> k) & 1u;
+              const uint4 x = ubias ? one : v[k];
+              sts4(d, lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u, lv ? x.w : 0u);
+            }
           }
         }
-        cp_async_commit();
-        if (j > 0) {
-          cp_async_wait<1>();
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[B_XF + j - 1]);
+      } else {
+        // re-layout of the staged rows once every backward MMA of step s-1 is done
+        mbar_wait(&bars[B_ST], (s - 1) & 1);
+        mbar_wait(&bars[B_BD + ntp - 1], (s - 1) & 1);
+        if (lane == 0) trace_pt(g, crank, s, 16 + j);
+        const int rows = batch_ref(s, n, B).rows;
+        const uint32_t sbase = s_w + (8 * j + u) * 32 + p * 16;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          uint4 v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int row = r0 + 2 * (8 * b + k);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                         : "r"(sbase + row * spitch));
+          }
+          if (uval) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int row = r0 + 2 * (8 * b + k);
+              const bool lv = row < rows;
+              const uint4 x = ubias ? one : (uload ? v[k] : make_uint4(0, 0, 0, 0));
+              sts4(dst + row * 128 + ((u ^ (row & 7)) << 4), lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u,
+                   lv ? x.w : 0u);
+            }
+          }
         }
       }
-      cp_async_wait<0>();
+      if (j >= 4 && lane == 0) trace_pt(g, crank, s, 25 + j);  // 29..31: tiles 4..6 landed
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_XF + nch - 1]);
-    }
-  } else if (warp == kMmaWarp) {
-    // ---- MMA issuer ------------------------------------------------------------------------------
-    constexpr uint32_t ID_F = idesc_f16(128, NP, false, true);  // A = stacked X rows (K-major), B = W (MN-major)
-    constexpr uint32_t ID_B = idesc_f16(128, NP, true, true);   // A = X^T (MN-major), B = E' (MN-major)
-    for (int s = 0; s < steps; ++s) {
       if (lane == 0) {
-        for (int j = 0; j < nch; ++j) {
-          mbar_wait(&bars[B_XF + j], s & 1);
-          mbar_wait(&bars[B_WR + j], s & 1);
-          fence_after();
-          if (j < nc) {
-            const int kks = min(4, (nf - 64 * j + 15) >> 4);  // K steps holding features
-            for (int kk = 0; kk < kks; ++kk) {
-              const uint64_t a = smem_desc(s_x + j * kChunk + kk * 32, 16, 1024, kSW128);
-              umma(t_z, a, smem_desc(s_w + j * kChunk + kk * 2048, 8192, 1024, kSW128), ID_F, (j | kk) != 0);
-              umma(t_z, a, smem_desc(s_w + j * kChunk + 8192 + kk * 2048, 8192, 1024, kSW128), ID_F, 1);
-            }
-          } else {
-            const uint64_t a = smem_desc(tail_x, 16, 256, kSW32);
-            umma(t_z, a, smem_desc(tail_w, 8192, 1024, kSW128), ID_F, j != 0);
-            umma(t_z, a, smem_desc(tail_w + 2048, 8192, 1024, kSW128), ID_F, 1);
-          }
-        }
-        commit(&bars[B_ZF]);
-        mbar_wait(&bars[B_EF], s & 1);
-        fence_after();
-        for (int t = 0; t < NT; ++t) {
-          const uint32_t d = t_w + 64 * t;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // K = the step's 64 rows
-            uint64_t ah, am;
-            if (t < ntp) {  // 128 features = chunks 2t, 2t+1 (a lone last chunk repeats into unused lanes)
-              const uint32_t xa = s_x + 2 * t * kChunk + kk * 2048;
-              const uint32_t lbo = 2 * t + 1 < nc ? kChunk : 0;
-              ah = smem_desc(xa, lbo, 1024, kSW128);
-              am = smem_desc(xa + 8192, lbo, 1024, kSW128);
-            } else {        // the 16-feature tail (lanes 16..127 repeat it and are never read)
-              ah = smem_desc(tail_x + kk * 512, 0, 256, kSW32);
-              am = smem_desc(tail_x + 2048 + kk * 512, 0, 256, kSW32);
-            }
-            const uint64_t eh = smem_desc(s_e + kk * 2048, 8192, 1024, kSW128);
-            const uint64_t em = smem_desc(s_e + 8192 + kk * 2048, 8192, 1024, kSW128);
-            umma(d, ah, eh, ID_B, 1);
-            umma(d, ah, em, ID_B, 1);
-            umma(d, am, eh, ID_B, 1);
-          }
-          commit(&bars[B_BD + t]);
+        mbar_arrive(&bars[B_XF + j]);
+        if (!tail && s > 0) mbar_arrive(&bars[B_RL]);
+      }
+      if (s + 1 < steps) {
+        load_idx(s + 1);
+        if (j == 0 && ncopy > 0) {
+          // stage step s+1's rows as soon as this step's forward has read the W operand
+          mbar_wait(&bars[B_ZF], s & 1);
+          const BatchRef nb = batch_ref(s + 1, n, B);
+          if (lane == 0) mbar_arrive_expect_tx(&bars[B_ST], (uint32_t)(nb.rows * ncopy * 4));
+          __syncwarp();
+          for (int r = lane; r < nb.rows; r += 32)
+            bulk_g2s(smem + g.off_w + r * spitch, xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch + (size_t)f0 * 4,
+                     (uint32_t)ncopy * 4, &bars[B_ST]);
         }
       }
-      __syncwarp();
+    }
+  } else if (warp == kMmaWarp) {
+    // ---- MMA issuer (the whole warp runs the loop, one elected lane issues) --------------------------------
+    constexpr uint32_t ID_F = idesc_f16(128, 2 * NP, false, true);  // A = [Xh; Xm] rows (K-major), B = [Wh | Wm]
+    constexpr uint32_t ID_B = idesc_f16(128, 2 * NP, true, true);   // A = X^T (MN-major), B = [E'h | E'm]
+    constexpr uint32_t ID_B1 = idesc_f16(128, NP, true, true);      // A = X^T (MN-major), B = E'h or E'm
+    // descriptors advance by (byte offset >> 4) in their start-address field (all addresses < 256 KB)
+    const uint64_t dX = smem_desc(s_x, 16, 1024, kSW128), dW = smem_desc(s_w, 8192, 1024, kSW128);
+    const uint64_t dXt = smem_desc(tail_x, 16, 256, kSW32), dWt = smem_desc(tail_w, 2048, 1024, kSW128);
+    const uint64_t dXtT = smem_desc(tail_x, 0, 256, kSW32);  // the tail as A = X^T (lanes >= 16 repeat it)
+    const uint64_t dE = smem_desc(s_e, 8192, 1024, kSW128);
+    for (int s = 0; s < steps; ++s) {
+      if (lane == 0) trace_pt(g, crank, s, 0);
+      if (s > 0 && tn > 0) mbar_wait(&bars[B_TR], (s - 1) & 1);  // the tail gradient is out of Z's columns
+      for (int j = 0; j < nch; ++j) {
+        mbar_wait(&bars[B_XF + j], s & 1);
+        mbar_wait(&bars[B_WR + j], s & 1);
+        fence_after();
+        if (lane == 0 && j == 0) trace_pt(g, crank, s, 1);
+        if (lane == 0 && j >= 3) trace_pt(g, crank, s, 21 + j);  // 24..27: tiles 3..6 ready
+        if (j < nc) {  // all four hi / mid products in one MMA: D[128 x 128]
+          const uint64_t a = dX + ((j * kChunk) >> 4), b = dW + ((j * kChunk) >> 4);
+          const int kks = min(4, (nfull - 64 * j + 15) >> 4);  // K steps holding features
+          if (kks == 4) {
+            umma_ws(t_z, a, b, ID_F, j != 0);
+            umma_ws(t_z, a + (32 >> 4), b + (2048 >> 4), ID_F, 1);
+            umma_ws(t_z, a + (64 >> 4), b + (4096 >> 4), ID_F, 1);
+            umma_ws(t_z, a + (96 >> 4), b + (6144 >> 4), ID_F, 1);
+          } else {
+            for (int kk = 0; kk < kks; ++kk)
+              umma_ws(t_z, a + ((kk * 32) >> 4), b + ((kk * 2048) >> 4), ID_F, (j | kk) != 0);
+          }
+        } else {
+          umma_ws(t_z, dXt, dWt, ID_F, j != 0);
+        }
+      }
+      commit_ws(&bars[B_ZF]);
+      if (lane == 0) trace_pt(g, crank, s, 2);
+      mbar_wait(&bars[B_EF], s & 1);
+      fence_after();
+      if (lane == 0) trace_pt(g, crank, s, 3);
+      if (tn > 0) {  // the tail's gradient, into Z's columns: G_t = (Xh + Xm)^T [E'h | E'm]
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t e = dE + ((kk * 2048) >> 4);
+          umma_ws(t_z, dXtT + ((kk * 512) >> 4), e, ID_B, kk != 0);
+          umma_ws(t_z, dXtT + ((2048 + kk * 512) >> 4), e, ID_B, 1);
+        }
+        commit_ws(&bars[B_TD]);
+      }
+      for (int t = 0; t < ntp; ++t) {
+        // 128 features = chunks 2t, 2t+1 (a lone last chunk repeats into unused lanes):
+        // W += Xh^T E'h + Xh^T E'm + Xm^T E'h (one 64-column master: the split reads half the TMEM of [Dh | Dm])
+        const uint32_t d = t_w + NP * t;
+        const uint64_t ah = smem_desc(s_x + 2 * t * kChunk, 2 * t + 1 < nc ? kChunk : 0, 1024, kSW128);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = the step's 64 rows
+          const uint64_t eh = dE + ((kk * 2048) >> 4), em = eh + (8192 >> 4);
+          umma_ws(d, ah + ((kk * 2048) >> 4), eh, ID_B1, 1);
+          umma_ws(d, ah + ((kk * 2048) >> 4), em, ID_B1, 1);
+          umma_ws(d, ah + ((8192 + kk * 2048) >> 4), eh, ID_B1, 1);
+        }
+        commit_ws(&bars[B_BD + t]);
+      }
     }
   } else {
     // ---- Q warps: quadrant q = warp % 4 (TMEM lanes 32q..32q+31), column half h ------------------------
     const int q = warp & 3, h = (warp - kQ0) >> 2;
     const uint32_t lq = (uint32_t)(32 * q) << 16;
     const int L = 32 * q + lane;
-    // fp32 master into TMEM and its split into the forward operand
-    for (int t = 0; t < NT; ++t) {
-      const int f = tile_feature(t, L, nc, ntp, nf);
+    const int qt = (warp - kQ0) * 32 + lane;  // 0..255
+    const bool tail_lane = q == 0 && lane < tn;
+    // fp32 masters: pair tiles into TMEM (Dh = W', Dm = 0), the tail as hi / mid / lo bf16 planes; and the split
+    // of both into the forward operand (W' row F = b: params[F C + c], fl_core.py:126-129)
+    for (int t = 0; t < ntp; ++t) {
+      const int f = tile_feature(t, L, nc, nfull);
       float w[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int c = 32 * h + i;
-        w[i] = (f >= 0 && c < C) ? static_cast<float>(params[(size_t)(f0 + f) * C + c]) : 0.f;
+        const int c = 32 * h + i, gfe = f0 + f;
+        w[i] = (f >= 0 && c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
       }
-      tst_row<32>(t_w + 64 * t + 32 * h + lq, w);
-      if (f >= 0) write_wop(s_w, nc, f, h, w);
+      tst_row<32>(t_w + NP * t + 32 * h + lq, w);
+      if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
+    }
+    if (tail_lane) {
+      float w[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = 32 * h + i, gfe = ft + lane;
+        w[i] = (c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
+      }
+      write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     fence_proxy_async_smem();
     fence_before();
     __syncwarp();
-    if (lane == 0)
-      for (int t = 0; t < NT; ++t) {
-        const int j = t < ntp ? 2 * t + (q >> 1) : nc;
-        if ((t < ntp && j < nc) || (t == ntp && q < 2)) mbar_arrive(&bars[B_WR + j]);
-      }
+    if (lane == 0) {
+      for (int t = 0; t < ntp; ++t)
+        if (2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
+      if (tn > 0 && q == 0) mbar_arrive(&bars[B_WR + nc]);
+    }
 
-    const int own = (int)crank;  // the softmax warps: quadrant own (hi rows of the owned block), both halves
-    const bool smx = q == own;
+    const int own = (int)crank;                   // this CTA's softmax rows: [32 own, 32 own + 32)
+    const int srow = qt >> 3, grp = qt & 7;         // softmax: owned row srow, classes [8 grp, 8 grp + 8)
+    const int r_own = 32 * own + srow;
     for (int s = 0; s < steps; ++s) {
       const BatchRef br = batch_ref(s, n, B);
       const int rows = br.rows;
-      const int r_own = 32 * own + lane;
-      const int ylab = (smx && r_own < rows) ? cl.y[cl.perm[br.perm_off + r_own]] : -1;
-      if (smx && h == 0 && lane == 0) {
+      const int ylab = r_own < rows ? cl.y[cl.perm[br.perm_off + r_own]] : -1;
+      if (qt == 0) {
         mbar_arrive_expect_tx(&bars[B_ZX], 32 * NP * 4);
         mbar_arrive_expect_tx(&bars[B_ER], 32 * NP * 4);
       }
       mbar_wait(&bars[B_ZF], s & 1);
       fence_after();
+      const bool tr = qt == 0;
+      if (tr) trace_pt(g, crank, s, 5);
+      // this CTA's partial logits of the lane's row, classes [32h, 32h + 32): Wh and Wm column halves summed
       float z[32];
-      tld_row<32>(t_z + lq + 32 * h, z);
-      // hi + mid partial rows: the mid quadrants hand theirs over through the (idle) E' region
+      {
+        float zm[32];
+        tld_row<32>(t_z + lq + 32 * h, z);
+        tld_row<32>(t_z + lq + NP + 32 * h, zm);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] += zm[i];
+      }
+      // hi + mid rows: the mid quadrants hand theirs over through the (idle) E' region
       if (q >= 2) {
         const uint32_t a = scratch_row(s_e, 32 * (q - 2) + lane) + 128 * h;
 #pragma unroll
@@ -309,118 +462,146 @@ __global__ void __maxnreg__(128)  // 13 warps: 4 share an SM sub-partition (4 x 
         const uint32_t a = scratch_row(s_e, L) + 128 * h;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          float4 v;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(a + 16 * ((k + lane) & 7)));
+          const float4 v = lds4f(a + 16 * ((k + lane) & 7));
           z[4 * k] += v.x;
           z[4 * k + 1] += v.y;
           z[4 * k + 2] += v.z;
           z[4 * k + 3] += v.w;
         }
-        if (!smx) {  // the peer's rows of this CTA's partial logits -> its receive buffer
+        if (q != own) {  // the peer's rows -> its receive buffer
           const uint32_t dst = mapa(s_zr + lane * 256 + 128 * h, peer), bar = mapa(smem_u32(&bars[B_ZX]), peer);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             st_async4b(dst + 16 * ((k + lane) & 7), __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]),
                        __float_as_uint(z[4 * k + 2]), __float_as_uint(z[4 * k + 3]), bar);
+        } else {         // owned rows: back into the scratch row, unrotated, for the 8-lane softmax below
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts4(a + 16 * k, __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]), __float_as_uint(z[4 * k + 2]),
+                 __float_as_uint(z[4 * k + 3]));
         }
       }
-      if (smx) {
-        // softmax of the owned rows (fl_core.py:132-151): own partial + the peer's + bias
-        wait_cluster(&bars[B_ZX], s & 1);
-        const uint32_t a = s_zr + lane * 256 + 128 * h;
+      named_sync(kBarQ, 256);
+      // softmax of the owned rows (fl_core.py:132-151) on all eight Q warps: 8 lanes per row, 8 classes per lane
+      // (the bias is already in the logits: feature F)
+      if (tr) trace_pt(g, crank, s, 6);
+      wait_cluster(&bars[B_ZX], s & 1);
+      if (tr) trace_pt(g, crank, s, 7);
+      float e[8];
+      {
+        const uint32_t za = scratch_row(s_e, r_own) + 128 * (grp >> 2) + 32 * (grp & 3);
+        const uint32_t ra = s_zr + srow * 256;
+        const int c0 = 8 * grp;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          float4 v;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                       : "r"(a + 16 * ((k + lane) & 7)));
-          z[4 * k] += v.x;
-          z[4 * k + 1] += v.y;
-          z[4 * k + 2] += v.z;
-          z[4 * k + 3] += v.w;
+        for (int k = 0; k < 2; ++k) {
+          const float4 a = lds4f(za + 16 * k);
+          // the peer pushed row srow rotated by its lane (= srow) within each 32-class half
+          const float4 b = lds4f(ra + 128 * (c0 >> 5) + 16 * ((((c0 & 31) >> 2) + k + srow) & 7));
+          e[4 * k] = a.x + b.x;
+          e[4 * k + 1] = a.y + b.y;
+          e[4 * k + 2] = a.z + b.z;
+          e[4 * k + 3] = a.w + b.w;
         }
         float mx = -FLT_MAX;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          z[i] += bias[32 * h + i];
-          if (32 * h + i < C) mx = fmaxf(mx, z[i]);
-        }
-        red[32 * h + lane] = mx;
-        named_sync(kBarSm, 64);
-        mx = fmaxf(red[lane], red[32 + lane]);
+        for (int i = 0; i < 8; ++i)
+          if (c0 + i < C) mx = fmaxf(mx, e[i]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
         float sum = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          z[i] = 32 * h + i < C ? __expf(z[i] - mx) : 0.f;
-          sum += z[i];
+        for (int i = 0; i < 8; ++i) {
+          e[i] = c0 + i < C ? __expf(e[i] - mx) : 0.f;
+          sum += e[i];
         }
-        red[64 + 32 * h + lane] = sum;
-        named_sync(kBarSm, 64);
-        sum = red[64 + lane] + red[96 + lane];
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
         const float inv = 1.f / sum, inb = 1.f / (float)rows;
         const bool vrow = r_own < rows;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = 32 * h + i;
-          z[i] = (vrow && c < C) ? -lr * ((z[i] * inv - (c == ylab ? 1.f : 0.f)) * inb) : 0.f;
-        }
-        // E' rows (MN-major [row][class], SW128): local copy + push to the peer
-        const uint32_t row_a = s_e + (r_own >> 3) * 1024 + (r_own & 7) * 128;
-        const uint32_t bar = mapa(smem_u32(&bars[B_ER]), peer);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t hw[4], mw[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) split_bf16x2(z[8 * k + 2 * e], z[8 * k + 2 * e + 1], hw[e], mw[e]);
-          const uint32_t ua = row_a + (((4 * h + k) ^ (r_own & 7)) << 4);
-          sts4(ua, hw[0], hw[1], hw[2], hw[3]);
-          sts4(ua + 8192, mw[0], mw[1], mw[2], mw[3]);
-          st_async4b(mapa(ua, peer), hw[0], hw[1], hw[2], hw[3], bar);
-          st_async4b(mapa(ua + 8192, peer), mw[0], mw[1], mw[2], mw[3], bar);
-        }
-        wait_cluster(&bars[B_ER], s & 1);  // the peer's rows
-        fence_proxy_async_smem();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_EF]);
-        // b -= lr * sum_r (P - Y) / nb = b + sum_r E' over all 64 rows, from the split rows both CTAs hold
-        // (identical bytes, identical order: the two copies of b stay equal)
-        const int c = 32 * h + lane;
-        if (c < C) {
-          float gb = 0.f;
-          const uint32_t u_off = (uint32_t)(c & 7) * 2;
-          for (int r = 0; r < kRows; ++r) {
-            const uint32_t ea = s_e + (r >> 3) * 1024 + (r & 7) * 128 + ((((uint32_t)c >> 3) ^ (r & 7)) << 4) + u_off;
-            uint16_t eh, em;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(eh) : "r"(ea));
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(em) : "r"(ea + 8192));
-            gb += bf16_lo(eh) + bf16_lo(em);
-          }
-          bias[c] += gb;
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + i;
+          e[i] = (vrow && c < C) ? -lr * ((e[i] * inv - (c == ylab ? 1.f : 0.f)) * inb) : 0.f;
         }
       }
-      // next forward's operand: re-split each master tile as soon as its backward MMAs are done
-      for (int t = 0; t < NT; ++t) {
+      named_sync(kBarQ, 256);  // every scratch row is read before E' overwrites the region
+      {
+        // E' row r_own, classes [8 grp, 8 grp + 8): one 16-byte unit per plane (MN-major [row][class], SW128),
+        // locally and pushed to the peer
+        uint32_t hw[4], mw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) split_bf16x2(e[2 * k], e[2 * k + 1], hw[k], mw[k]);
+        const uint32_t ua = s_e + (r_own >> 3) * 1024 + (r_own & 7) * 128 + ((grp ^ (r_own & 7)) << 4);
+        const uint32_t bar = mapa(smem_u32(&bars[B_ER]), peer);
+        sts4(ua, hw[0], hw[1], hw[2], hw[3]);
+        sts4(ua + 8192, mw[0], mw[1], mw[2], mw[3]);
+        st_async4b(mapa(ua, peer), hw[0], hw[1], hw[2], hw[3], bar);
+        st_async4b(mapa(ua + 8192, peer), mw[0], mw[1], mw[2], mw[3], bar);
+      }
+      if (tr) trace_pt(g, crank, s, 8);
+      wait_cluster(&bars[B_ER], s & 1);  // the peer's rows
+      if (tr) trace_pt(g, crank, s, 9);
+      fence_proxy_async_smem();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[B_EF]);
+      if (tn > 0 && q == 0) {
+        // the tail master += its gradient (Z's columns, lanes = tail features), re-split into the operand
+        mbar_wait(&bars[B_TD], s & 1);
+        fence_after();
+        float gr[32];
+        {
+          float gm[32];
+          tld_row<32>(t_z + 32 * h, gr);
+          tld_row<32>(t_z + NP + 32 * h, gm);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) gr[i] += gm[i];
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_TR]);
+        if (tail_lane) {
+          float w[32];
+          read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) w[i] += gr[i];
+          write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_WR + nc]);
+      }
+      if (tr) trace_pt(g, crank, s, 10);
+      // next forward's operand: re-split each master tile once the staged rows are re-laid out (the operand's
+      // chunk region is their staging area; the re-layout waited for every backward MMA)
+      if (s + 1 < steps && nc > 0) mbar_wait(&bars[B_RL], s & 1);
+      for (int t = 0; t < ntp && s + 1 < steps; ++t) {
         mbar_wait(&bars[B_BD + t], s & 1);
         fence_after();
-        const int f = tile_feature(t, L, nc, ntp, nf);
+        const int f = tile_feature(t, L, nc, nfull);
         float w[32];
-        tld_row<32>(t_w + 64 * t + 32 * h + lq, w);
-        if (f >= 0) write_wop(s_w, nc, f, h, w);
+        tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+        if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
         fence_proxy_async_smem();
         fence_before();
         __syncwarp();
-        const int j = t < ntp ? 2 * t + (q >> 1) : nc;
-        if (lane == 0 && ((t < ntp && j < nc) || (t == ntp && q < 2))) mbar_arrive(&bars[B_WR + j]);
+        if (lane == 0 && 2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
+        if (q == 0 && h == 0 && lane == 0) trace_pt(g, crank, s, 11 + t);
       }
     }
-    // delta = new - old (fl_core.py:194), fp32
+    // delta = new - old (fl_core.py:194), fp32; W' row F is the bias
     float* out = cl.delta;
-    for (int t = 0; t < NT; ++t) {
-      const int f = tile_feature(t, L, nc, ntp, nf);
+    for (int t = 0; t < ntp; ++t) {
+      if (steps > 0) {  // the last step's backward MMAs (its split was skipped)
+        mbar_wait(&bars[B_BD + t], (steps - 1) & 1);
+        fence_after();
+      }
+      const int f = tile_feature(t, L, nc, nfull);
       float w[32];
-      tld_row<32>(t_w + 64 * t + 32 * h + lq, w);
-      if (f >= 0) {
+      tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+      if (f >= 0 && f0 + f < FB) {
         const size_t gi = (size_t)(f0 + f) * C;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -429,9 +610,15 @@ __global__ void __maxnreg__(128)  // 13 warps: 4 share an SM sub-partition (4 x 
         }
       }
     }
-    if (crank == 0 && smx) {
-      const int c = 32 * h + lane;
-      if (c < C) out[(size_t)F * C + c] = bias[c] - static_cast<float>(params[(size_t)F * C + c]);
+    if (tail_lane && ft + lane < FB) {
+      float w[32];
+      read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
+      const size_t gi = (size_t)(ft + lane) * C;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = 32 * h + i;
+        if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
+      }
     }
   }
   fence_before();
@@ -444,37 +631,50 @@ __global__ void __maxnreg__(128)  // 13 warps: 4 share an SM sub-partition (4 x 
 }
 
 // Geometry; false if the shape is not this kernel's (F <= 784, F % 8 == 0, 32 < C <= 64, B <= 64).
+// The F + 8 features of W' (the bias unit padded to 8) go to the two CTAs in 64-feature chunks; a remainder of
+// <= 32 features becomes SW32 tail tiles of <= 16 features, split so that the CTAs stay balanced; a larger
+// remainder is a partial last chunk.
 static bool plan(int F, int C, int max_batch, int max_smem, Geom& g) {
   if (C <= 32 || C > NP || F % 8 != 0 || F > 784 || max_batch > kRows) return false;
-  const int tf = F % 64;
-  const bool sw32 = tf > 0 && tf <= 16;
-  const int nct = F / 64 + (tf > 16 ? 1 : 0);  // SW128 chunks (a > 16-feature remainder is a partial chunk)
+  const int F8 = F + 8;
+  const int tf = F8 % 64;
+  const bool tails = tf > 0 && tf <= 32;
+  const int nct = F8 / 64 + (tails || tf == 0 ? 0 : 1);  // SW128 chunks
   g.F = F;
   g.C = C;
   g.nc[0] = (nct + 1) / 2;
   g.nc[1] = nct - g.nc[0];
-  g.tail[0] = 0;
-  g.tail[1] = sw32 ? 1 : 0;
-  if (g.nc[0] == 0 || g.nc[1] + g.tail[1] == 0 || g.nc[0] > 6 || g.nc[1] > 6) return false;
   g.f0[0] = 0;
   g.f0[1] = 64 * g.nc[0];
-  g.nf[0] = 64 * g.nc[0];
-  g.nf[1] = F - g.nf[0];
-  const int xb = std::max(g.nc[0] * kChunk, g.nc[1] * kChunk + g.tail[1] * kTail);
+  g.nfull[0] = 64 * g.nc[0];
+  g.nfull[1] = std::min(F8, 64 * nct) - g.f0[1];
+  g.tn[0] = g.tn[1] = 0;
+  if (tails) {
+    g.tn[1] = (nct % 2) ? std::min(16, tf) : std::min(16, ((tf / 2) + 7) / 8 * 8);
+    g.tn[0] = tf - g.tn[1];
+  }
+  g.ft[0] = 64 * nct;
+  g.ft[1] = 64 * nct + g.tn[0];
+  int xb = 0, wb = 0;
+  for (int k = 0; k < 2; ++k) {
+    if (g.nc[k] > 6 || g.tn[k] > 16 || g.nc[k] + (g.tn[k] > 0) == 0) return false;
+    xb = std::max(xb, g.nc[k] * kChunk + (g.tn[k] > 0 ? kTail : 0));
+    wb = std::max(wb, g.nc[k] * kChunk + (g.tn[k] > 0 ? kTail + kTailLo : 0));
+  }
   int off = 0;
   g.off_x = off;    off += xb;
-  g.off_w = off;    off += xb;
+  g.off_w = off;    off += wb;
   g.off_e = off;    off += 16384;          // E' [Eh 64 x 128 B | Em 64 x 128 B] (+ the hi / mid scratch)
   g.off_zr = off;   off += 32 * NP * 4;    // the peer's partial logits of the owned rows
-  g.off_red = off;  off += 4 * 32 * 4;
-  g.off_bias = off; off += NP * 4;
   g.off_bar = off;  off += (kBars * 8 + 15) / 16 * 16;
   g.off_tmem = off; off += 16;
-  g.bytes = off + 1024;  // alignment slack for the SW128 tiles
+  g.bytes = off;  // the dynamic shared memory base is 1024-byte aligned (checked in the kernel)
   return g.bytes <= max_smem;
 }
 
 }  // namespace c64
+
+unsigned long long* tc_trace_buffer();
 
 // Launch the 2-CTA tensor-core trainer if the shape is its (split rows required); false -> other kernels.
 bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
@@ -485,6 +685,9 @@ bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* 
   Geom g{};
   if (!plan(F, C, max_batch, max_smem, g)) return false;
   g.split_off = split_off;
+  static const char* pf = getenv("FEDHC_C64_PREFETCH");
+  g.prefetch = pf ? atoi(pf) : 1;
+  if (getenv("FEDHC_TC_TRACE")) g.trace = tc_trace_buffer();
   static int smem_set_of[64] = {0};
   static std::mutex mu;
   int dev = 0;

@@ -618,6 +618,12 @@ static cudaError_t launch_np_cl(const fedhc_client* clients, int n_clients, cons
 
 }  // namespace ltc
 
+// Device buffer of the phase timestamps (FEDHC_TC_TRACE diagnostics; shared by the tensor-core trainers).
+unsigned long long* tc_trace_buffer() {
+  if (!ltc::g_trace) cudaMalloc(&ltc::g_trace, sizeof(unsigned long long) * 8 * ltc::kTraceSteps * ltc::kTracePts);
+  return ltc::g_trace;
+}
+
 // Launch the tcgen05 trainer if the shape fits; returns false to fall back.
 bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* params, int F, int C, int max_batch,
                      int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status) {
@@ -633,10 +639,7 @@ bool launch_train_tc(const fedhc_client* clients, int n_clients, const double* p
   g.split = split ? 1 : 0;  // rows pre-split in 8-feature units: slices stay 8-aligned
   g.split_off = split_off;
   if (!plan_tc(F, C, max_batch, max_smem, g)) return false;
-  if (getenv("FEDHC_TC_TRACE")) {
-    if (!g_trace) cudaMalloc(&g_trace, sizeof(unsigned long long) * 8 * kTraceSteps * kTracePts);
-    g.trace = g_trace;
-  }
+  if (getenv("FEDHC_TC_TRACE")) g.trace = tc_trace_buffer();
   cudaError_t e = cudaErrorInvalidValue;
 #define FEDHC_TC_CASE(NPv, CLv) \
   if (g.NP == NPv && g.CL == CLv) e = launch_np_cl<NPv, CLv>(clients, n_clients, params, g, st);
