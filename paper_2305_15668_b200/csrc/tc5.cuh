@@ -183,18 +183,6 @@ __device__ __forceinline__ void commit_ws(uint64_t* bar) {
       : "memory");
 }
 
-// mbarrier wait that suspends the thread until the phase completes (suspend-time hint), for warps whose wait
-// is long and not latency-critical: polling warps steal issue slots from their sub-partition's MMA issuer.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
-      "@!p bra WS_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // st.async of four 32-bit words, bytes counted on the destination CTA's mbarrier.
 __device__ __forceinline__ void st_async4b(uint32_t cluster_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                            uint32_t cluster_bar) {

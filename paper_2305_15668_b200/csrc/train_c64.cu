@@ -24,8 +24,10 @@
 //   backward  tail first, into Z's (now free) columns: G_t = (Xh + Xm)^T [E'h | E'm], added to the tail master
 //             by the Q warps; then W_tile += Xh^T E'h + Xh^T E'm + Xm^T E'h per pair tile (A = MN-major views
 //             of the same X chunks)
-//   refill    as soon as a tile's backward MMAs complete, its X chunks are reloaded with the next step's rows
-//             (prefetched into L2 one step ahead) and the Q warps re-split its master into the W operand.
+//   staging   the next step's rows land in the W operand's chunk region by one bulk copy per row (the region
+//             is dead once the forward MMAs have read it), while the softmax and the backward run
+//   refill    as each tile's backward MMAs complete, the chunk warps re-lay the staged rows into its X tiles
+//             (shared memory to shared memory), then the Q warps re-split the master into the W operand.
 //
 // Accuracy: bf16x3 products (hi*hi + hi*mid + mid*hi, plus mid*mid), fp32 accumulation and fp32 masters (the
 // tail's as hi + mid + lo bf16, 24 significant bits) -- the arithmetic of the other trainers, within the
@@ -59,10 +61,11 @@ constexpr uint32_t kSW128 = 2, kSW32 = 6;
 
 // B_BD + t: pair tile t's backward MMAs done (t < 3); B_TD: the tail's gradient MMAs done; B_TR: the Q warps
 // have read the tail gradient out of Z's columns (the next forward may overwrite them)
-// B_ST: the next step's rows have landed in the staging area; B_RL: the chunk loaders have re-laid them out
+// B_FD + j: the forward MMAs of chunk j are done (its W operand region may take staged rows); B_ST: the next
+// step's rows have landed in the staging area; B_RL: the chunk loaders have re-laid them out
 enum {
-  B_XF = 0, B_WR = B_XF + kMaxCh, B_BD = B_WR + kMaxCh, B_TD = B_BD + 3, B_TR, B_ZF, B_EF, B_ZX, B_ER, B_ST, B_RL,
-  kBars
+  B_XF = 0, B_WR = B_XF + kMaxCh, B_FD = B_WR + kMaxCh, B_BD = B_FD + kMaxCh, B_TD = B_BD + 3, B_TR, B_ZF, B_EF, B_ZX,
+  B_ER, B_ST, B_RL, kBars
 };
 
 struct Geom {
@@ -73,7 +76,6 @@ struct Geom {
   int ft[2];     // SW32 tail tile of CTA k: features [ft, ft + tn), tn <= 16 (0: none)
   int tn[2];
   long long split_off;
-  int prefetch;               // L2 prefetch of the next step's rows (FEDHC_C64_PREFETCH=0 disables, for A/B)
   unsigned long long* trace;  // FEDHC_TC_TRACE: %globaltimer phase points of cluster 0 [cta][step][32], else null
   int off_x, off_w, off_e, off_zr, off_bar, off_tmem, bytes;
 };
@@ -184,6 +186,7 @@ __global__ void __maxnreg__(128)
     for (int j = 0; j < kMaxCh; ++j) {
       mbar_init(&bars[B_XF + j], 1);
       mbar_init(&bars[B_WR + j], j == nc ? 2 : 4);  // chunks: two quadrants x two halves; the tail: quadrant 0
+      mbar_init(&bars[B_FD + j], 1);
     }
     for (int t = 0; t < 3; ++t) mbar_init(&bars[B_BD + t], 1);
     mbar_init(&bars[B_TD], 1);
@@ -274,9 +277,9 @@ __global__ void __maxnreg__(128)
           }
         }
       } else {
-        // re-layout of the staged rows once every backward MMA of step s-1 is done
+        // re-layout of the staged rows as soon as this tile's backward MMAs of step s-1 are done
         mbar_wait(&bars[B_ST], (s - 1) & 1);
-        mbar_wait(&bars[B_BD + ntp - 1], (s - 1) & 1);
+        mbar_wait(&bars[B_BD + (j >> 1)], (s - 1) & 1);
         if (lane == 0) trace_pt(g, crank, s, 16 + j);
         const int rows = batch_ref(s, n, B).rows;
         const uint32_t sbase = s_w + (8 * j + u) * 32 + p * 16;
@@ -311,14 +314,15 @@ __global__ void __maxnreg__(128)
       if (s + 1 < steps) {
         load_idx(s + 1);
         if (j == 0 && ncopy > 0) {
-          // stage step s+1's rows as soon as this step's forward has read the W operand
-          mbar_wait(&bars[B_ZF], s & 1);
+          // stage step s+1's rows: row r as soon as the forward MMAs have read the W operand chunks it overlays
           const BatchRef nb = batch_ref(s + 1, n, B);
           if (lane == 0) mbar_arrive_expect_tx(&bars[B_ST], (uint32_t)(nb.rows * ncopy * 4));
           __syncwarp();
-          for (int r = lane; r < nb.rows; r += 32)
+          for (int r = lane; r < nb.rows; r += 32) {
+            mbar_wait(&bars[B_FD + ((r + 1) * spitch - 1) / kChunk], s & 1);
             bulk_g2s(smem + g.off_w + r * spitch, xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch + (size_t)f0 * 4,
                      (uint32_t)ncopy * 4, &bars[B_ST]);
+          }
         }
       }
     }
@@ -353,6 +357,7 @@ __global__ void __maxnreg__(128)
             for (int kk = 0; kk < kks; ++kk)
               umma_ws(t_z, a + ((kk * 32) >> 4), b + ((kk * 2048) >> 4), ID_F, (j | kk) != 0);
           }
+          commit_ws(&bars[B_FD + j]);
         } else {
           umma_ws(t_z, dXt, dWt, ID_F, j != 0);
         }
@@ -575,7 +580,7 @@ __global__ void __maxnreg__(128)
       }
       if (tr) trace_pt(g, crank, s, 10);
       // next forward's operand: re-split each master tile once the staged rows are re-laid out (the operand's
-      // chunk region is their staging area; the re-layout waited for every backward MMA)
+      // chunk region is their staging area)
       if (s + 1 < steps && nc > 0) mbar_wait(&bars[B_RL], s & 1);
       for (int t = 0; t < ntp && s + 1 < steps; ++t) {
         mbar_wait(&bars[B_BD + t], s & 1);
@@ -685,8 +690,6 @@ bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* 
   Geom g{};
   if (!plan(F, C, max_batch, max_smem, g)) return false;
   g.split_off = split_off;
-  static const char* pf = getenv("FEDHC_C64_PREFETCH");
-  g.prefetch = pf ? atoi(pf) : 1;
   if (getenv("FEDHC_TC_TRACE")) g.trace = tc_trace_buffer();
   static int smem_set_of[64] = {0};
   static std::mutex mu;

@@ -91,7 +91,8 @@ def test_kernels_present_in_sass():
     if not os.path.exists(exe):
         pytest.skip("cuobjdump not available")
     out = subprocess.run([exe, "-sass", _abi.LIB_PATH], capture_output=True, text=True).stdout
-    for kernel in ("train_tc_kernel", "train_generic_kernel", "train_pipe_kernel", "train_fused_kernel", "fedavg_kernel", "eval_kernel",
+    for kernel in ("train_c64_kernel", "train_tc_kernel", "train_generic_kernel", "train_pipe_kernel", "train_fused_kernel",
+                   "train_pipe2_kernel", "fedavg_kernel", "eval_kernel",
                    "grouped_gemm_kernel", "conv1_fwd_kernel", "conv1_bwd_kernel", "perm_kernel"):
         assert kernel in out, kernel
     assert "HMMA" in out and "UBLKCP" in out
