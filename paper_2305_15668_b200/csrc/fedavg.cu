@@ -18,6 +18,10 @@
 // `fedavg_tile_kernel` gives each CTA 128 elements, stages a [KT][128] tile of
 // all its delta rows into shared memory with cp.async (every load in flight
 // at once), then runs the same list-order fp64 chain from shared memory.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fedhc {
@@ -177,6 +181,96 @@ __global__ void __launch_bounds__(kTileE)
   if (e < n) out[e] = acc;
 }
 
+// Streaming FedAvg through the TMA engine: persistent CTAs walk 1024-element segments; a producer warp
+// bulk-copies each delta row's segment (4 KB for fp32) into a ring of shared-memory stages, so one CTA keeps
+// up to kBulkStages * kBulkRows rows in flight with one instruction per 4 KB (the per-thread vector loads of
+// fedavg_kernel hold 128 B per thread and re-fetch a pointer per delta).  The 256 consumer threads run the
+// same list-order fp64 chain on 4 elements each, so the result is bit-identical to fedavg_kernel.
+constexpr int kBulkE = 1024;                       // elements per segment
+constexpr int kBulkRows = 4, kBulkStages = 6;      // rows per stage, stages in the ring
+constexpr int kBulkConsumers = kBulkE / 4;         // 256 threads x 4 elements
+constexpr int kBulkThreads = kBulkConsumers + 32;  // + the producer warp
+
+template <typename T>
+__global__ void __launch_bounds__(kBulkThreads)
+    fedavg_bulk_kernel(const T* const* __restrict__ ptrs, const T* __restrict__ packed, int64_t ld,
+                       const double* __restrict__ coef, int K, const double* base, double* out, int64_t n) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kRowBytes = kBulkE * (int)sizeof(T);
+  T* ring = reinterpret_cast<T*>(smem);  // [stages][rows][kBulkE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kBulkRows * kRowBytes);
+  uint64_t* empty = full + kBulkStages;
+  const int tid = threadIdx.x;
+  const int64_t nseg = (n + kBulkE - 1) / kBulkE;
+  const int groups = (K + kBulkRows - 1) / kBulkRows;  // stage fills per segment
+  if (tid == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= kBulkConsumers) {
+    // ---- producer warp: lane 0 issues the bulk copies of (segment, row group) in consumption order
+    if (tid == kBulkConsumers) {
+      int it = 0;
+      for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        const int64_t e0 = sg * kBulkE;
+        // bytes of this segment (a ragged last segment rounded up to 16 bytes: rows are padded to that)
+        const uint32_t bytes = (uint32_t)((min((int64_t)kBulkE, n - e0) * (int64_t)sizeof(T) + 15) & ~15);
+        for (int gi = 0; gi < groups; ++gi, ++it) {
+          const int s = it % kBulkStages, use = it / kBulkStages;
+          if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+          const int k0 = gi * kBulkRows, kr = min(kBulkRows, K - k0);
+          mbar_arrive_expect_tx(&full[s], bytes * kr);
+          for (int r = 0; r < kr; ++r) {
+            const T* row = ptrs != nullptr ? ptrs[k0 + r] : packed + (int64_t)(k0 + r) * ld;
+            bulk_g2s(ring + ((size_t)s * kBulkRows + r) * kBulkE, row + e0, bytes, &full[s]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: element p = e0 + 4 tid .. + 3
+  int it = 0;
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const int64_t p0 = sg * kBulkE + 4 * tid;
+    const int m = p0 < n ? (int)min((int64_t)4, n - p0) : 0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (base != nullptr)
+      for (int i = 0; i < m; ++i) acc[i] = base[p0 + i];
+    for (int gi = 0; gi < groups; ++gi, ++it) {
+      const int s = it % kBulkStages, use = it / kBulkStages;
+      mbar_wait(&full[s], use & 1);
+      const int k0 = gi * kBulkRows, kr = min(kBulkRows, K - k0);
+      for (int r = 0; r < kr; ++r) {
+        double v[4];
+        const T* q = ring + ((size_t)s * kBulkRows + r) * kBulkE + 4 * tid;
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = *reinterpret_cast<const float4*>(q);
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+          const double2 a = reinterpret_cast<const double2*>(q)[0], b = reinterpret_cast<const double2*>(q)[1];
+          v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        }
+        const double c = __ldg(coef + k0 + r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = __dadd_rn(acc[i], __dmul_rn(c, v[i]));
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    if (m == 4) {
+      reinterpret_cast<double2*>(out + p0)[0] = make_double2(acc[0], acc[1]);
+      reinterpret_cast<double2*>(out + p0)[1] = make_double2(acc[2], acc[3]);
+    } else {
+      for (int i = 0; i < m; ++i) out[p0 + i] = acc[i];
+    }
+  }
+}
+
 }  // namespace fedhc
 
 using namespace fedhc;
@@ -232,6 +326,36 @@ extern "C" int fedhc_fedavg(const void* const* deltas, const void* packed, int64
       fedavg_tile_kernel<double><<<tb, kTileE, kTileBytes, st>>>(
           reinterpret_cast<const double* const*>(deltas), static_cast<const double*>(packed), ld, coef, n_deltas,
           base, out, n);
+    FEDHC_CUDA_TRY(cudaGetLastError());
+    return FEDHC_OK;
+  }
+  // packed rows with a 16-byte pitch, at the sweep points where it measured faster (short vectors: the
+  // per-thread kernel runs few waves; many deltas: it re-fetches a pointer per delta): the TMA-fed persistent
+  // kernel (bit-identical).  Pointer rows keep the per-thread streaming kernel (their alignment is only known on
+  // the device).  profiles/r2c_fedavg.md has both kernels over the config-5 sweep.
+  static const bool no_bulk = getenv("FEDHC_FEDAVG_NO_BULK") != nullptr;
+  const int esz = dtype == FEDHC_F32 ? 4 : 8;
+  if (!no_bulk && deltas == nullptr && (ld * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(packed) & 15) == 0 &&
+      (n <= (4LL << 20) || n_deltas >= 500)) {
+    const int smem = kBulkStages * kBulkRows * kBulkE * esz + 2 * kBulkStages * 8;
+    const void* kern = dtype == FEDHC_F32 ? reinterpret_cast<const void*>(fedavg_bulk_kernel<float>)
+                                          : reinterpret_cast<const void*>(fedavg_bulk_kernel<double>);
+    static int per_sm_of[64][2] = {};  // resident CTAs per SM, per device and dtype (set once; benign race)
+    int& per_sm = per_sm_of[dev & 63][dtype == FEDHC_F32 ? 0 : 1];
+    if (per_sm == 0) {
+      FEDHC_CUDA_TRY(smem_optin_max(kern));
+      int v = 0;
+      FEDHC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kBulkThreads, smem));
+      per_sm = std::max(v, 1);
+    }
+    const int64_t nseg = (n + kBulkE - 1) / kBulkE;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nseg, (int64_t)per_sm * sms));
+    if (dtype == FEDHC_F32)
+      fedavg_bulk_kernel<float><<<grid, kBulkThreads, smem, st>>>(nullptr, static_cast<const float*>(packed), ld,
+                                                                   coef, n_deltas, base, out, n);
+    else
+      fedavg_bulk_kernel<double><<<grid, kBulkThreads, smem, st>>>(nullptr, static_cast<const double*>(packed), ld,
+                                                                    coef, n_deltas, base, out, n);
     FEDHC_CUDA_TRY(cudaGetLastError());
     return FEDHC_OK;
   }

@@ -180,6 +180,30 @@ def test_fedavg_full_size_vs_torch(tr):
     assert torch.equal(out, base + deltas[0].double())
 
 
+@pytest.mark.parametrize("P,K", [(1_000_003, 37), (250_004, 600), (4097, 1000), (2_000_000, 3)])
+def test_fedavg_tma_streamed_vs_torch(tr, P, K):
+    """The TMA-fed persistent FedAvg (packed rows, P <= 4M or K >= 500; ragged last segment, many row groups,
+    fewer rows than one stage): bit-exact vs the same list-order sequence in torch fp64."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(P + K)
+    ld = (P + 3) // 4 * 4
+    deltas = (torch.randn(K, ld, device="cuda", generator=g, dtype=torch.float32) * 1e-3)[:, :P]
+    base = torch.randn(P, device="cuda", generator=g, dtype=torch.float64)
+    w = torch.rand(K, generator=torch.Generator().manual_seed(K), dtype=torch.float64) + 0.1
+    coef = (w / w.sum()).cuda()
+    out = torch.empty_like(base)
+    tr.fedavg_device(deltas, coef, base, out)
+    ref = base.clone()
+    for k in range(K):
+        ref += coef[k].item() * deltas[k].double()
+    assert torch.equal(out, ref)
+    tr.fedavg_device(deltas, coef, None, out)  # partial sums (multi-GPU path): no base
+    ref = torch.zeros_like(base)
+    for k in range(K):
+        ref += coef[k].item() * deltas[k].double()
+    assert torch.equal(out, ref)
+
+
 def test_accuracy_vs_oracle(tr):
     d = fm.Data(FL["acc_x"], FL["acc_y"], 6)
     assert tr.evaluate_accuracy(FL["acc_p"], tr.Dataset(d.features, d.labels, 6)) == fm.accuracy(FL["acc_p"], d)
