@@ -336,7 +336,7 @@ extern "C" int fedhc_fedavg(const void* const* deltas, const void* packed, int64
   static const bool no_bulk = getenv("FEDHC_FEDAVG_NO_BULK") != nullptr;
   const int esz = dtype == FEDHC_F32 ? 4 : 8;
   if (!no_bulk && deltas == nullptr && (ld * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(packed) & 15) == 0 &&
-      (n <= (4LL << 20) || n_deltas >= 500)) {
+      ((n <= (4LL << 20) && n_deltas >= 32) || n_deltas >= 500)) {
     const int smem = kBulkStages * kBulkRows * kBulkE * esz + 2 * kBulkStages * 8;
     const void* kern = dtype == FEDHC_F32 ? reinterpret_cast<const void*>(fedavg_bulk_kernel<float>)
                                           : reinterpret_cast<const void*>(fedavg_bulk_kernel<double>);

@@ -180,7 +180,7 @@ def test_fedavg_full_size_vs_torch(tr):
     assert torch.equal(out, base + deltas[0].double())
 
 
-@pytest.mark.parametrize("P,K", [(1_000_003, 37), (250_004, 600), (4097, 1000), (2_000_000, 3)])
+@pytest.mark.parametrize("P,K", [(1_000_003, 37), (250_004, 600), (4097, 1000), (2_000_000, 33)])
 def test_fedavg_tma_streamed_vs_torch(tr, P, K):
     """The TMA-fed persistent FedAvg (packed rows, P <= 4M or K >= 500; ragged last segment, many row groups,
     fewer rows than one stage): bit-exact vs the same list-order sequence in torch fp64."""
