@@ -306,6 +306,37 @@ def test_batched_round_matches_per_client(fh, tr, C):
             assert rel_err(deltas[i], want) <= REL
 
 
+@pytest.mark.parametrize("F", [784, 720])
+def test_c62_round_with_tail_wave(fh, tr, F):
+    """More participants than 2-CTA clusters fit at once (74 on a B200: a second, partial wave): every client's
+    delta (ragged and reshuffled batches, an empty shard) == the per-client oracle local_train.  F = 720: 11 chunks
+    + a 16-feature tail (uneven CTAs)."""
+    import torch
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    C, K = 62, 96
+    sizes = [96 + (i % 5) * 17 for i in range(K)]
+    sizes[80] = 0
+    trn, tst = fm.synthetic(F, C, sum(sizes) + 200, seed=5)
+    shards, at = {}, 0
+    for i, n in enumerate(sizes):
+        shards[f"c{i}"] = tr.DatasetShard(f"c{i}", trn.features[at:at + n], trn.labels[at:at + n])
+        at += n
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, C), F, C)
+    params = np.random.default_rng(3).standard_normal(F * C + C) * 0.02
+    wl = [WorkloadSpec(2 * n if n else 10, 64) for n in sizes]
+    seeds = [fm.seed_of("train", 2, 0, f"c{i}") for i in range(K)]
+    deltas = fed.train(torch.from_numpy(params).cuda(), list(shards), wl, 0.1, seeds).cpu().numpy()
+    for i in list(range(0, K, 7)) + [73, 74, 75, 79, 80, K - 1]:
+        cid = f"c{i}"
+        if sizes[i] == 0:
+            assert np.all(deltas[i] == 0)
+            continue
+        want = fm.local_sgd(params, fm.Shard(cid, shards[cid].features, shards[cid].labels), wl[i].num_samples,
+                            wl[i].batch_size, 0.1, C, seed=seeds[i])
+        assert rel_err(deltas[i], want) <= REL, (i, rel_err(deltas[i], want))
+
+
 def test_x_split_layout(fh):
     """fedhc_x_split: each row -> per 8-feature unit [8 bf16 hi | 8 bf16 mid], hi = bf16_rn(x),
     mid = bf16_rn(x - hi)."""
