@@ -85,6 +85,14 @@ int fedhc_local_train(const fedhc_client* clients, int n_clients, const double* 
  * n_features a multiple of 8. */
 int fedhc_x_split(const float* x, int64_t n_rows, int n_features, void* out, void* stream);
 
+/* numpy Generator.standard_normal (float64) on the device, value-for-value: n normals from the PCG64 stream
+ * whose state before the first draw is state_words = {state_hi, state_lo, inc_hi, inc_lo}
+ * (rng.bit_generator.state["state"] of a numpy Generator).  Replaces the host draw of the reference's
+ * synthetic features (fl_core.py:47-55) at fleet scale; out: device fp64 [n]; state_after (host, optional):
+ * {state_hi, state_lo} after the draws numpy would have taken.  Synchronous on `stream`. */
+int fedhc_pcg64_standard_normal(const uint64_t* state_words, int64_t n, double* out, uint64_t* state_after,
+                                void* stream);
+
 /* fedhc_local_train (fl_core.py:163-194) whose client rows ALSO exist in the
  * fedhc_x_split layout at (char*)client.x + split_offset (bytes, signed,
  * multiple of 16: the distance from the fp32 rows to their split copy).  Shapes with a split-reading kernel (F = 784, C <= 16: the FEMNIST

@@ -149,6 +149,7 @@ SIGNATURES = {
     "fedhc_device_info": (_i, [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "fedhc_local_train": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
     "fedhc_x_split": (_i, [_vp, _i64, _i, _vp, _vp]),
+    "fedhc_pcg64_standard_normal": (_i, [_vp, _i64, _vp, _vp, _vp]),
     "fedhc_runner_create": (_i, [_vp, _vp]),
     "fedhc_runner_destroy": (None, [_vp]),
     "fedhc_runner_plan": (_i, [_vp, _i64, _d, _i, _vp]),

@@ -71,45 +71,57 @@ def make_synthetic_dataset(n_features: int, n_classes: int, n_total: int, seed: 
     return Dataset(x[n_test:], y[n_test:], n_classes), Dataset(x[:n_test], y[:n_test], n_classes)
 
 
-def partition_noniid(dataset: Dataset, clients: list[tuple[str, int]], alpha: float,
-                     seed: int) -> dict[str, DatasetShard]:
-    """Dirichlet(alpha) label mix per client, drawn without replacement (fl_core.py:62-115)."""
+def partition_rows(labels: np.ndarray, n_classes: int, clients: list[tuple[str, int]], alpha: float,
+                   seed: int) -> dict[str, np.ndarray]:
+    """Row indices of each client's shard: the draws and pool bookkeeping of fl_core.py:62-115.
+
+    Per-class pools are shuffled once (same PCG64 draws for an ndarray as for the
+    reference's list), each client takes floor(Dir(alpha) * n) rows per class plus
+    the largest-remainder fix-up from the pool tails, any shortfall comes from the
+    first richest pool, and the shard's rows are sorted ascending.
+    """
     if alpha <= 0:
         raise ValueError("alpha must be > 0")
     wanted = sum(n for _, n in clients)
-    if wanted > len(dataset.labels):
-        raise ValueError(f"clients want {wanted} samples but dataset has {len(dataset.labels)}")
+    if wanted > len(labels):
+        raise ValueError(f"clients want {wanted} samples but dataset has {len(labels)}")
     rng = np.random.default_rng(seed)
-    n_classes = dataset.num_classes
     pools = []
     for c in range(n_classes):
-        members = list(np.flatnonzero(dataset.labels == c))
+        members = np.flatnonzero(labels == c)
         rng.shuffle(members)
         pools.append(members)
-    shards: dict[str, DatasetShard] = {}
+    live = [len(p) for p in pools]          # pools[c][:live[c]] is what is left of class c
+    out: dict[str, np.ndarray] = {}
     for cid, n in clients:
         mix = rng.dirichlet([alpha] * n_classes)
         counts = np.floor(mix * n).astype(int)
         extra = n - counts.sum()
         for c in np.argsort(-(mix * n - counts), kind="stable")[:extra]:
             counts[c] += 1
-        rows: list[int] = []
+        parts: list[np.ndarray] = []
         short = 0
         for c in range(n_classes):
-            take = int(min(counts[c], len(pools[c])))
+            take = int(min(counts[c], live[c]))
             short += int(counts[c]) - take
             if take:
-                rows += pools[c][len(pools[c]) - take:]
-                del pools[c][len(pools[c]) - take:]
+                parts.append(pools[c][live[c] - take:live[c]])
+                live[c] -= take
         for _ in range(short):
-            lens = [len(p) for p in pools]
-            richest = lens.index(max(lens))
-            if not pools[richest]:
+            richest = live.index(max(live))
+            if not live[richest]:
                 raise ValueError("dataset exhausted during partitioning")
-            rows.append(pools[richest].pop())
-        sel = np.array(sorted(rows), dtype=int)
-        shards[cid] = DatasetShard(cid, dataset.features[sel], dataset.labels[sel])
-    return shards
+            live[richest] -= 1
+            parts.append(pools[richest][live[richest]:live[richest] + 1])
+        out[cid] = np.sort(np.concatenate(parts)) if parts else np.zeros(0, dtype=int)
+    return out
+
+
+def partition_noniid(dataset: Dataset, clients: list[tuple[str, int]], alpha: float,
+                     seed: int) -> dict[str, DatasetShard]:
+    """Dirichlet(alpha) label mix per client, drawn without replacement (fl_core.py:62-115)."""
+    rows = partition_rows(dataset.labels, dataset.num_classes, clients, alpha, seed)
+    return {cid: DatasetShard(cid, dataset.features[sel], dataset.labels[sel]) for cid, sel in rows.items()}
 
 
 def init_params(n_features: int, n_classes: int) -> np.ndarray:
