@@ -29,11 +29,12 @@ import numpy as np
 import torch
 
 from . import _abi
+from .devicedata import reference_federation
 from .errors import AggregationError, ConfigError
 from .roundsim import LeanRoundReport, RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
 from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
-                       init_params, make_synthetic_dataset, n_permutations, native_permutations, partition_noniid,
+                       init_params, n_permutations, native_permutations,
                        split_supported, stable_seed, stream_ptr, train_launch, x_split)
 
 
@@ -272,11 +273,10 @@ def run_experiment(cfg: FleetConfig, fleet: list[ClientProfile], data: DataParam
     fed = params = None
     if train.enabled:
         n_total = sum(p.workload.num_samples for p in fleet)
-        train_ds, test = make_synthetic_dataset(data.features, data.classes, max(math.ceil(n_total / 0.8), 10),
-                                                stable_seed("data", cfg.seed))
-        shards = partition_noniid(train_ds, [(p.client_id, p.workload.num_samples) for p in fleet], data.alpha,
-                                  stable_seed("partition", cfg.seed))
-        fed = DeviceFederation(shards, test, data.features, data.classes)
+        # fl_core.py:41-115's dataset + partition, generated in HBM bit for bit (devicedata.reference_federation)
+        fed = reference_federation([(p.client_id, p.workload.num_samples) for p in fleet], data.features,
+                                   data.classes, max(math.ceil(n_total / 0.8), 10), stable_seed("data", cfg.seed),
+                                   data.alpha, stable_seed("partition", cfg.seed))
         params = torch.from_numpy(init_params(data.features, data.classes)).to(device())
 
     report = ExperimentReport()
