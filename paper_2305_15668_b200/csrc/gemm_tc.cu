@@ -241,44 +241,94 @@ __device__ __forceinline__ void nhwc_tile_origin(const ConvSpec& cv, int g, int 
   }
 }
 
-template <int BM, int BN>
-__device__ __forceinline__ void nhwc_loads(const ConvSpec& cv, uint32_t sa, uint32_t sb, const CUtensorMap* map_a,
-                                           const CUtensorMap* map_b, uint64_t* bar, int g, int m0, int n0, int kb) {
-  const int pad = cv.k >> 1;
-  if (cv.mode == NHWC_FWD || cv.mode == NHWC_DGRAD) {
-    int img0, y0;
-    nhwc_tile_origin(cv, g, m0 / BM, img0, y0);
-    const int cblocks = (cv.mode == NHWC_FWD ? cv.cin : cv.cout) >> 6;
-    const int tap = kb / cblocks, cb = kb - tap * cblocks, kh = tap / cv.k, kw = tap - kh * cv.k;
-    if (cv.mode == NHWC_FWD) {
+// Producer-side walk over the K blocks of one NHWC tile without per-block integer divisions by run-time
+// values (cin, k, blocks per image): the producer thread's address arithmetic (~200 dependent instructions
+// per block with the divisions) was the critical path of the 64-pixel weight-gradient blocks.
+//   FWD / DGRAD: K block kb = (tap, 64-channel block cb), tap = (kh, kw), cb fastest
+//   WIN 3 / 4: K block = (cb, kw), kw fastest; the three kh taps share the window
+//   WGRAD: K block = 64 output pixels (kib images or khb rows); A rows m = tap * cin + channel (fixed per tile)
+template <int BM, int BN, int WIN>
+struct NhwcWalk {
+  int img0, y0;        // tile origin (FWD / DGRAD / WIN) or current 64-pixel block (WGRAD)
+  int kh, kw, cb, tap; // FWD / DGRAD: tap (kh, kw) and channel block; WIN: kw and channel block
+  int cblocks;
+  int ac[BM / 64], ax[BM / 64], ay[BM / 64];  // WGRAD: A box (channel, x offset, y offset or OOB) per 64 rows
+
+  __device__ __forceinline__ void init(const ConvSpec& cv, int g, int m0) {
+    kh = kw = cb = tap = 0;
+    if (WIN >= 3 || cv.mode != NHWC_WGRAD) {
+      nhwc_tile_origin(cv, g, m0 / BM, img0, y0);
+      cblocks = (cv.mode == NHWC_FWD || WIN == 3 ? cv.cin : cv.cout) >> 6;
+    } else {
+      img0 = g * cv.bp;
+      y0 = 0;
+      const int pad = cv.k >> 1;
+#pragma unroll
+      for (int h = 0; h < BM / 64; ++h) {
+        const int m = m0 + 64 * h, t = m / cv.cin, c = m - t * cv.cin, th = t / cv.k, tw = t - th * cv.k;
+        const bool valid = t < cv.k * cv.k;  // rows past k*k*cin (ragged last tile): an all-OOB box (zeros)
+        ac[h] = valid ? c : 0;
+        ax[h] = tw - pad;
+        ay[h] = valid ? th - pad : -4096;
+      }
+    }
+  }
+
+  __device__ __forceinline__ void load(const ConvSpec& cv, uint32_t sa, uint32_t sb, const CUtensorMap* map_a,
+                                       const CUtensorMap* map_b, uint64_t* bar, int g, int n0, int kb) {
+    const int pad = cv.k >> 1;
+    if (WIN == 3) {
+      tma_load_4d(sa, map_a, bar, cb * 64, kw - 1, y0 - 1, img0);
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h)
+          tma_load_3d(sb + t * Cfg<BM, BN, WIN>::kTapBBytes + h * 64 * BK * 2, map_b, bar, n0 + 64 * h,
+                      (t * 3 + kw) * cv.cin + cb * 64, g);
+    } else if (WIN == 4) {
+      tma_load_4d(sa, map_a, bar, cb * 64, 1 - kw, y0 - 1, img0);
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+        tma_load_3d(sb + t * Cfg<BM, BN, WIN>::kTapBBytes, map_b, bar, cb * 64, (t * 3 + kw) * cv.cin + n0, g);
+    } else if (cv.mode == NHWC_FWD) {
       tma_load_4d(sa, map_a, bar, cb * 64, kw - pad, y0 * cv.s + kh - pad, img0);
 #pragma unroll
       for (int h = 0; h < BN / 64; ++h) tma_load_3d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, kb * BK, g);
-    } else {  // data gradient (stride 1): flipped taps, weights [tap][cin][cout] as K-major rows
+    } else if (cv.mode == NHWC_DGRAD) {
       tma_load_4d(sa, map_a, bar, cb * 64, pad - kw, y0 + pad - kh, img0);
       tma_load_3d(sb, map_b, bar, cb * 64, tap * cv.cin + n0, g);
-    }
-  } else {  // NHWC_WGRAD
-    int img0, y0;
-    if (cv.kib > 1) {
-      img0 = g * cv.bp + kb * cv.kib;
-      y0 = 0;
-    } else {
-      const int bpi = cv.ho / cv.khb;
-      img0 = g * cv.bp + kb / bpi;
-      y0 = (kb % bpi) * cv.khb;
-    }
+    } else {  // NHWC_WGRAD
 #pragma unroll
-    for (int h = 0; h < BM / 64; ++h) {
-      const int m = m0 + 64 * h, tap = m / cv.cin, c = m - tap * cv.cin, kh = tap / cv.k, kw = tap - kh * cv.k;
-      // rows past k*k*cin (ragged last tile): a box entirely out of bounds loads zeros
-      tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, tap < cv.k * cv.k ? c : 0, kw - pad,
-                  tap < cv.k * cv.k ? y0 * cv.s + kh - pad : -4096, img0);
-    }
+      for (int h = 0; h < BM / 64; ++h)
+        tma_load_4d(sa + h * 64 * BK * 2, map_a, bar, ac[h], ax[h], ay[h] < -64 ? ay[h] : y0 * cv.s + ay[h], img0);
 #pragma unroll
-    for (int h = 0; h < BN / 64; ++h) tma_load_4d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, 0, y0, img0);
+      for (int h = 0; h < BN / 64; ++h) tma_load_4d(sb + h * 64 * BK * 2, map_b, bar, n0 + 64 * h, 0, y0, img0);
+    }
   }
-}
+
+  __device__ __forceinline__ void next(const ConvSpec& cv) {
+    if (WIN >= 3) {
+      if (++kw == 3) {
+        kw = 0;
+        ++cb;
+      }
+    } else if (cv.mode == NHWC_WGRAD) {
+      if (cv.kib > 1) {
+        img0 += cv.kib;
+      } else if ((y0 += cv.khb) == cv.ho) {
+        y0 = 0;
+        ++img0;
+      }
+    } else if (++cb == cblocks) {
+      cb = 0;
+      ++tap;
+      if (++kw == cv.k) {
+        kw = 0;
+        ++kh;
+      }
+    }
+  }
+};
 
 template <int BM, int BN, bool A_MN, bool B_MN, int WIN = 0>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -351,6 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = t / (tiles_m * tiles_n);
         const int r = t - g * tiles_m * tiles_n;
         const int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+        NhwcWalk<BM, BN, WIN> walk;
+        if (WIN >= 3 || conv.mode >= NHWC_FWD) walk.init(conv, g, m0);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], WIN >= 3 ? (uint32_t)((conv.hb + 2) * conv.wo * 128 + CF::kTileBBytes)
@@ -371,28 +423,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               tma_load_3d(sb, &map_b, &full[s], kb * BK, n0, g);
             }
-          } else if (WIN == 0 && conv.mode >= NHWC_FWD) {
-            nhwc_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
+          } else if (WIN >= 3 || (WIN == 0 && conv.mode >= NHWC_FWD)) {
+            walk.load(conv, sa, sb, &map_a, &map_b, &full[s], g, n0, kb);
+            walk.next(conv);
           } else if (WIN == 0) {
             conv_loads<BM, BN>(conv, sa, sb, &map_a, &map_b, &full[s], g, m0, n0, kb);
-          } else if (WIN >= 3) {  // NHWC 3x3 stride 1: window of hb + 2 rows, shifted by kw, 3 taps (kh)
-            int img0, y0;
-            nhwc_tile_origin(conv, g, m0 / BM, img0, y0);
-            const int kw = kb % 3, cb = kb / 3;
-            if (WIN == 3) {
-              tma_load_4d(sa, &map_a, &full[s], cb * 64, kw - 1, y0 - 1, img0);
-#pragma unroll
-              for (int kh = 0; kh < 3; ++kh)
-#pragma unroll
-                for (int h = 0; h < BN / 64; ++h)
-                  tma_load_3d(sb + kh * CF::kTapBBytes + h * 64 * BK * 2, &map_b, &full[s], n0 + 64 * h,
-                              (kh * 3 + kw) * conv.cin + cb * 64, g);
-            } else {
-              tma_load_4d(sa, &map_a, &full[s], cb * 64, 1 - kw, y0 - 1, img0);
-#pragma unroll
-              for (int kh = 0; kh < 3; ++kh)
-                tma_load_3d(sb + kh * CF::kTapBBytes, &map_b, &full[s], cb * 64, (kh * 3 + kw) * conv.cin + n0, g);
-            }
           } else {
             const int mt = m0 / BM, img = g * conv.bp + (mt >> 1), y0 = (mt & 1) * 8;
             if (WIN == 1) {  // forward: tap-pair column pk = kb; window rows y0 - 2 .. y0 + 9
