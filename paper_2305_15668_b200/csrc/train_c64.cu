@@ -156,9 +156,37 @@ __device__ __forceinline__ float4 lds4f(uint32_t a) {
   return v;
 }
 
+// More clients than resident clusters: the clients' SGD steps are laid out on the resident clusters ("slots")
+// by McNaughton's wrap-around rule -- cut the concatenated step sequence into slot-sized pieces of
+// T = max(ceil(total / slots), longest client) steps -- so a round takes ~total / slots steps instead of two
+// full waves.  A client cut by a slot boundary runs its FIRST steps at the start of the next slot (then saves
+// its state: the fp32 master tiles and the tail planes, exactly) and its LAST steps at the end of this slot
+// (restoring that state once it is published): the same SGD steps in the same order, so the deltas are
+// bit-identical to an uncut run.
+struct Seg {
+  int client, s0, s1;  // steps [s0, s1) of the client
+  int link;            // boundary index whose saved state joins the two parts of a cut client (-1: not cut)
+};
+struct Sched {
+  const Seg* segs;   // null: cluster c runs client c whole
+  const int* start;  // slot c runs segs[start[c] .. start[c + 1])
+  float* state;      // [link][cta][kStateFloats]
+  int* ready;        // [link][cta] == *epoch once the state is saved
+  const int* epoch;  // bumped by the scheduler each launch
+};
+constexpr int kStateFloats = 3 * 128 * NP + (kTail + kTailLo) / 4;
+
+__device__ __forceinline__ int seg_count(const Sched& sc, int c) { return sc.segs ? sc.start[c + 1] - sc.start[c] : 1; }
+__device__ __forceinline__ Seg seg_at(const Sched& sc, const fedhc_client* clients, int c, int i) {
+  if (sc.segs) return sc.segs[sc.start[c] + i];
+  const fedhc_client& cl = clients[c];
+  return Seg{c, 0, cl.n_rows > 0 ? cl.n_batches : 0, -1};
+}
+
 // 16 warps: 4 share an SM sub-partition, so 128 registers per thread is the ceiling (4 x 32 x 128 = its 16K)
 __global__ void __maxnreg__(128)
-    train_c64_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const Geom g) {
+    train_c64_kernel(const fedhc_client* __restrict__ clients, const double* __restrict__ params, const Geom g,
+                     const Sched sc) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const uint32_t sb = smem_u32(smem);
   if (sb & 1023u) __trap();  // the SW128 tiles are laid out from a 1024-byte aligned base (no slack allocated)
@@ -168,14 +196,11 @@ __global__ void __maxnreg__(128)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = ctarank(), peer = crank ^ 1u;
-  const fedhc_client cl = clients[blockIdx.x >> 1];
+  const int slot = blockIdx.x >> 1, nseg = seg_count(sc, slot);
   const int F = g.F, C = g.C, FB = F + 1;  // FB: features of W' = [W; b]
   const int nc = g.nc[crank], f0 = g.f0[crank], nfull = g.nfull[crank], ft = g.ft[crank], tn = g.tn[crank];
   const int nch = nc + (tn > 0 ? 1 : 0);  // X / W operand tiles: chunks 0..nc-1, then the tail
   const int ntp = (nc + 1) / 2;           // chunk-pair master tiles in TMEM
-  const int n = cl.n_rows, B = cl.batch_size;
-  const int steps = n > 0 ? cl.n_batches : 0;
-  const float lr = cl.lr;
   const uint32_t tail_x = s_x + nc * kChunk, tail_w = s_w + nc * kChunk, tail_lo = tail_w + kTail;
 
   // ---- setup -------------------------------------------------------------------------------------
@@ -213,7 +238,7 @@ __global__ void __maxnreg__(128)
   // TMEM: Z [128 rows x (Wh | Wm) class halves] (also the tail gradient's home between the softmax and the next
   // forward); pair tile t's master at 2 NP + NP t
   const uint32_t t_z = tmem, t_w = tmem + 2 * NP;
-
+  // barrier phases run over all steps of all the slot's segments: `it` = steps done so far
   if (warp < kLoadWarps) {
     // ---- loaders: warp j fills X tile j (chunk j, or the tail for j = nc) each step: lane = (8-feature unit u,
     // plane p, row parity r0), 32 rows r0 + 2i by 16-byte LDG (16 in flight) + swizzled STS -- the LDGSTS path
@@ -224,104 +249,112 @@ __global__ void __maxnreg__(128)
     const bool tail = j >= nc;
     const int u = lane & 7, p = (lane >> 3) & 1, r0 = lane >> 4;
     const size_t pitch = (size_t)F * 4;
-    const char* xsplit = reinterpret_cast<const char*>(cl.x) + g.split_off;
     const int gf = tail ? ft + 8 * u : f0 + 64 * j + 8 * u;  // first global feature of the lane's unit
     const bool uval = active && (tail ? 8 * u < tn : 64 * j + 8 * u < nfull);
     const bool ubias = uval && gf == F;                        // the synthesised bias unit
     const bool uload = uval && gf < F;
-    const char* src = xsplit + (size_t)(uload ? gf : 0) * 4 + p * 16;
     const uint32_t dst = tail ? tail_x + p * 2048 : s_x + j * kChunk + p * 8192;
     const uint4 one = make_uint4(p == 0 ? 0x3f80u : 0u, 0u, 0u, 0u);  // bf16 hi = 1.0 (feature F), mid = 0
-    int ix0 = -1, ix1 = -1;  // source rows 2 lane, 2 lane + 1 of the step (one step ahead)
-    auto load_idx = [&](int s) {
-      const BatchRef br = batch_ref(s, n, B);
-      ix0 = 2 * lane < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane) : -1;
-      ix1 = 2 * lane + 1 < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane + 1) : -1;
-    };
-    if (active && steps > 0) load_idx(0);
-    // staging (steps >= 1): the chunk part of each row, [f0, f0 + ncopy) features, lands by one bulk copy per row
-    // in the W operand's chunk region -- dead from the end of a forward (Z_FULL) until the split that follows the
-    // re-layout -- while the softmax and the backward run; after the backward the chunk warps re-lay it into the
-    // swizzled tiles (shared memory to shared memory) instead of gathering 256-byte row segments from L2
+    // staging (steps after a segment's first): the chunk part of each row, [f0, f0 + ncopy) features, lands by
+    // one bulk copy per row in the W operand's chunk region -- dead from the end of a forward (Z_FULL) until the
+    // split that follows the re-layout -- while the softmax and the backward run; after the backward the chunk
+    // warps re-lay it into the swizzled tiles (shared memory to shared memory) instead of gathering 256-byte
+    // row segments from L2
     const int ncopy = max(0, min(nfull, F - f0));  // real features of the chunk part (the bias unit is synthesised)
     const uint32_t spitch = (uint32_t)nfull * 4;
-    for (int s = 0; active && s < steps; ++s) {
-      if (tail || s == 0) {
-        // tile j still holds step s-1's rows until its backward MMAs are done
-        if (s > 0) mbar_wait(&bars[B_TD], (s - 1) & 1);
-        if (lane == 0) trace_pt(g, crank, s, 16 + j);
+    int it = 0, stg = 0;  // steps done, staged batches consumed
+    for (int si = 0; active && si < nseg; ++si) {
+      const Seg sg = seg_at(sc, clients, slot, si);
+      const fedhc_client cl = clients[sg.client];
+      const int n = cl.n_rows, B = cl.batch_size;
+      const char* xsplit = reinterpret_cast<const char*>(cl.x) + g.split_off;
+      const char* src = xsplit + (size_t)(uload ? gf : 0) * 4 + p * 16;
+      int ix0 = -1, ix1 = -1;  // source rows 2 lane, 2 lane + 1 of the step (one step ahead)
+      auto load_idx = [&](int s) {
+        const BatchRef br = batch_ref(s, n, B);
+        ix0 = 2 * lane < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane) : -1;
+        ix1 = 2 * lane + 1 < br.rows ? __ldg(cl.perm + br.perm_off + 2 * lane + 1) : -1;
+      };
+      if (sg.s1 > sg.s0) load_idx(sg.s0);
+      for (int s = sg.s0; s < sg.s1; ++s, ++it) {
+        if (tail || s == sg.s0) {
+          // tile j still holds the previous step's rows until its backward MMAs are done
+          if (it > 0) mbar_wait(&bars[tail ? B_TD : B_BD + (j >> 1)], (it - 1) & 1);
+          if (lane == 0) trace_pt(g, crank, it, 16 + j);
 #pragma unroll 1
-        for (int b = 0; b < 2; ++b) {
-          // every lane shuffles (the index pairs live in lane i) and loads unconditionally (rows past the batch
-          // end read row 0 and are stored as zeros; their E' rows are zero): a predicated load followed by a
-          // zero-fill of its register would wait for the load (WAW) and serialise the batch
-          uint4 v[16];
-          uint32_t live = 0;
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int i = 16 * b + k;
-            const int a0 = __shfl_sync(0xffffffffu, ix0, i), a1 = __shfl_sync(0xffffffffu, ix1, i);
-            const int rw = r0 ? a1 : a0;
-            live |= (rw >= 0 ? 1u : 0u) << k;
-            v[k] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)max(rw, 0) * pitch));
-          }
-          if (uval) {
+          for (int b = 0; b < 2; ++b) {
+            // every lane shuffles (the index pairs live in lane i) and loads unconditionally (rows past the batch
+            // end read row 0 and are stored as zeros; their E' rows are zero): a predicated load followed by a
+            // zero-fill of its register would wait for the load (WAW) and serialise the batch
+            uint4 v[16];
+            uint32_t live = 0;
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-              const int row = r0 + 2 * (16 * b + k);
-              const uint32_t d = tail ? dst + row * 32 + ((u ^ ((row >> 2) & 1)) << 4) : dst + row * 128 + ((u ^ (row & 7)) << 4);
-              const bool lv = (live >> k) & 1u;
-              const uint4 x = ubias ? one : v[k];
-              sts4(d, lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u, lv ? x.w : 0u);
+              const int i = 16 * b + k;
+              const int a0 = __shfl_sync(0xffffffffu, ix0, i), a1 = __shfl_sync(0xffffffffu, ix1, i);
+              const int rw = r0 ? a1 : a0;
+              live |= (rw >= 0 ? 1u : 0u) << k;
+              v[k] = __ldcg(reinterpret_cast<const uint4*>(src + (size_t)max(rw, 0) * pitch));
+            }
+            if (uval) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int row = r0 + 2 * (16 * b + k);
+                const uint32_t d = tail ? dst + row * 32 + ((u ^ ((row >> 2) & 1)) << 4) : dst + row * 128 + ((u ^ (row & 7)) << 4);
+                const bool lv = (live >> k) & 1u;
+                const uint4 x = ubias ? one : v[k];
+                sts4(d, lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u, lv ? x.w : 0u);
+              }
             }
           }
-        }
-      } else {
-        // re-layout of the staged rows as soon as this tile's backward MMAs of step s-1 are done
-        mbar_wait(&bars[B_ST], (s - 1) & 1);
-        mbar_wait(&bars[B_BD + (j >> 1)], (s - 1) & 1);
-        if (lane == 0) trace_pt(g, crank, s, 16 + j);
-        const int rows = batch_ref(s, n, B).rows;
-        const uint32_t sbase = s_w + (8 * j + u) * 32 + p * 16;
+        } else {
+          // re-layout of the staged rows as soon as this tile's backward MMAs of the previous step are done
+          mbar_wait(&bars[B_ST], stg & 1);
+          ++stg;
+          mbar_wait(&bars[B_BD + (j >> 1)], (it - 1) & 1);
+          if (lane == 0) trace_pt(g, crank, it, 16 + j);
+          const int rows = batch_ref(s, n, B).rows;
+          const uint32_t sbase = s_w + (8 * j + u) * 32 + p * 16;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          uint4 v[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int row = r0 + 2 * (8 * b + k);
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
-                         : "r"(sbase + row * spitch));
-          }
-          if (uval) {
+          for (int b = 0; b < 4; ++b) {
+            uint4 v[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int row = r0 + 2 * (8 * b + k);
-              const bool lv = row < rows;
-              const uint4 x = ubias ? one : (uload ? v[k] : make_uint4(0, 0, 0, 0));
-              sts4(dst + row * 128 + ((u ^ (row & 7)) << 4), lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u,
-                   lv ? x.w : 0u);
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
+                           : "r"(sbase + row * spitch));
+            }
+            if (uval) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int row = r0 + 2 * (8 * b + k);
+                const bool lv = row < rows;
+                const uint4 x = ubias ? one : (uload ? v[k] : make_uint4(0, 0, 0, 0));
+                sts4(dst + row * 128 + ((u ^ (row & 7)) << 4), lv ? x.x : 0u, lv ? x.y : 0u, lv ? x.z : 0u,
+                     lv ? x.w : 0u);
+              }
             }
           }
         }
-      }
-      if (j >= 4 && lane == 0) trace_pt(g, crank, s, 25 + j);  // 29..31: tiles 4..6 landed
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&bars[B_XF + j]);
-        if (!tail && s > 0) mbar_arrive(&bars[B_RL]);
-      }
-      if (s + 1 < steps) {
-        load_idx(s + 1);
-        if (j == 0 && ncopy > 0) {
-          // stage step s+1's rows: row r as soon as the forward MMAs have read the W operand chunks it overlays
-          const BatchRef nb = batch_ref(s + 1, n, B);
-          if (lane == 0) mbar_arrive_expect_tx(&bars[B_ST], (uint32_t)(nb.rows * ncopy * 4));
-          __syncwarp();
-          for (int r = lane; r < nb.rows; r += 32) {
-            mbar_wait(&bars[B_FD + ((r + 1) * spitch - 1) / kChunk], s & 1);
-            bulk_g2s(smem + g.off_w + r * spitch, xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch + (size_t)f0 * 4,
-                     (uint32_t)ncopy * 4, &bars[B_ST]);
+        if (j >= 4 && lane == 0) trace_pt(g, crank, it, 25 + j);  // 29..31: tiles 4..6 landed
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&bars[B_XF + j]);
+          if (!tail && s > sg.s0) mbar_arrive(&bars[B_RL]);
+        }
+        if (s + 1 < sg.s1) {
+          load_idx(s + 1);
+          if (j == 0 && ncopy > 0) {
+            // stage step s+1's rows: row r as soon as the forward MMAs have read the W operand chunks it overlays
+            const BatchRef nb = batch_ref(s + 1, n, B);
+            if (lane == 0) mbar_arrive_expect_tx(&bars[B_ST], (uint32_t)(nb.rows * ncopy * 4));
+            __syncwarp();
+            for (int r = lane; r < nb.rows; r += 32) {
+              mbar_wait(&bars[B_FD + ((r + 1) * spitch - 1) / kChunk], it & 1);
+              bulk_g2s(smem + g.off_w + r * spitch, xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch + (size_t)f0 * 4,
+                       (uint32_t)ncopy * 4, &bars[B_ST]);
+            }
           }
         }
       }
@@ -336,15 +369,18 @@ __global__ void __maxnreg__(128)
     const uint64_t dXt = smem_desc(tail_x, 16, 256, kSW32), dWt = smem_desc(tail_w, 2048, 1024, kSW128);
     const uint64_t dXtT = smem_desc(tail_x, 0, 256, kSW32);  // the tail as A = X^T (lanes >= 16 repeat it)
     const uint64_t dE = smem_desc(s_e, 8192, 1024, kSW128);
-    for (int s = 0; s < steps; ++s) {
-      if (lane == 0) trace_pt(g, crank, s, 0);
-      if (s > 0 && tn > 0) mbar_wait(&bars[B_TR], (s - 1) & 1);  // the tail gradient is out of Z's columns
+    int it = 0;
+    for (int si = 0; si < nseg; ++si) {
+     const Seg sg = seg_at(sc, clients, slot, si);
+     for (int s = sg.s0; s < sg.s1; ++s, ++it) {
+      if (lane == 0) trace_pt(g, crank, it, 0);
+      if (it > 0 && tn > 0) mbar_wait(&bars[B_TR], (it - 1) & 1);  // the tail gradient is out of Z's columns
       for (int j = 0; j < nch; ++j) {
-        mbar_wait(&bars[B_XF + j], s & 1);
-        mbar_wait(&bars[B_WR + j], s & 1);
+        mbar_wait(&bars[B_XF + j], it & 1);
+        mbar_wait(&bars[B_WR + j], it & 1);
         fence_after();
-        if (lane == 0 && j == 0) trace_pt(g, crank, s, 1);
-        if (lane == 0 && j >= 3) trace_pt(g, crank, s, 21 + j);  // 24..27: tiles 3..6 ready
+        if (lane == 0 && j == 0) trace_pt(g, crank, it, 1);
+        if (lane == 0 && j >= 3) trace_pt(g, crank, it, 21 + j);  // 24..27: tiles 3..6 ready
         if (j < nc) {  // all four hi / mid products in one MMA: D[128 x 128]
           const uint64_t a = dX + ((j * kChunk) >> 4), b = dW + ((j * kChunk) >> 4);
           const int kks = min(4, (nfull - 64 * j + 15) >> 4);  // K steps holding features
@@ -363,10 +399,10 @@ __global__ void __maxnreg__(128)
         }
       }
       commit_ws(&bars[B_ZF]);
-      if (lane == 0) trace_pt(g, crank, s, 2);
-      mbar_wait(&bars[B_EF], s & 1);
+      if (lane == 0) trace_pt(g, crank, it, 2);
+      mbar_wait(&bars[B_EF], it & 1);
       fence_after();
-      if (lane == 0) trace_pt(g, crank, s, 3);
+      if (lane == 0) trace_pt(g, crank, it, 3);
       if (tn > 0) {  // the tail's gradient, into Z's columns: G_t = (Xh + Xm)^T [E'h | E'm]
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -390,6 +426,7 @@ __global__ void __maxnreg__(128)
         }
         commit_ws(&bars[B_BD + t]);
       }
+     }
     }
   } else {
     // ---- Q warps: quadrant q = warp % 4 (TMEM lanes 32q..32q+31), column half h ------------------------
@@ -398,232 +435,310 @@ __global__ void __maxnreg__(128)
     const int L = 32 * q + lane;
     const int qt = (warp - kQ0) * 32 + lane;  // 0..255
     const bool tail_lane = q == 0 && lane < tn;
-    // fp32 masters: pair tiles into TMEM (Dh = W', Dm = 0), the tail as hi / mid / lo bf16 planes; and the split
-    // of both into the forward operand (W' row F = b: params[F C + c], fl_core.py:126-129)
-    for (int t = 0; t < ntp; ++t) {
-      const int f = tile_feature(t, L, nc, nfull);
-      float w[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = 32 * h + i, gfe = f0 + f;
-        w[i] = (f >= 0 && c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
-      }
-      tst_row<32>(t_w + NP * t + 32 * h + lq, w);
-      if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
-    }
-    if (tail_lane) {
-      float w[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = 32 * h + i, gfe = ft + lane;
-        w[i] = (c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
-      }
-      write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    fence_proxy_async_smem();
-    fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      for (int t = 0; t < ntp; ++t)
-        if (2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
-      if (tn > 0 && q == 0) mbar_arrive(&bars[B_WR + nc]);
-    }
-
     const int own = (int)crank;                   // this CTA's softmax rows: [32 own, 32 own + 32)
     const int srow = qt >> 3, grp = qt & 7;         // softmax: owned row srow, classes [8 grp, 8 grp + 8)
     const int r_own = 32 * own + srow;
-    for (int s = 0; s < steps; ++s) {
-      const BatchRef br = batch_ref(s, n, B);
-      const int rows = br.rows;
-      const int ylab = r_own < rows ? cl.y[cl.perm[br.perm_off + r_own]] : -1;
-      if (qt == 0) {
-        mbar_arrive_expect_tx(&bars[B_ZX], 32 * NP * 4);
-        mbar_arrive_expect_tx(&bars[B_ER], 32 * NP * 4);
-      }
-      mbar_wait(&bars[B_ZF], s & 1);
-      fence_after();
-      const bool tr = qt == 0;
-      if (tr) trace_pt(g, crank, s, 5);
-      // this CTA's partial logits of the lane's row, classes [32h, 32h + 32): Wh and Wm column halves summed
-      float z[32];
-      {
-        float zm[32];
-        tld_row<32>(t_z + lq + 32 * h, z);
-        tld_row<32>(t_z + lq + NP + 32 * h, zm);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) z[i] += zm[i];
-      }
-      // hi + mid rows: the mid quadrants hand theirs over through the (idle) E' region
-      if (q >= 2) {
-        const uint32_t a = scratch_row(s_e, 32 * (q - 2) + lane) + 128 * h;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          sts4(a + 16 * ((k + lane) & 7), __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]),
-               __float_as_uint(z[4 * k + 2]), __float_as_uint(z[4 * k + 3]));
-      }
-      named_sync(kBarQ, 256);
-      if (q < 2) {
-        const uint32_t a = scratch_row(s_e, L) + 128 * h;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 v = lds4f(a + 16 * ((k + lane) & 7));
-          z[4 * k] += v.x;
-          z[4 * k + 1] += v.y;
-          z[4 * k + 2] += v.z;
-          z[4 * k + 3] += v.w;
+    int it = 0, rl = 0;  // steps done, re-layouts consumed
+    for (int si = 0; si < nseg; ++si) {
+      const Seg sg = seg_at(sc, clients, slot, si);
+      const fedhc_client cl = clients[sg.client];
+      const int n = cl.n_rows, B = cl.batch_size;
+      const int steps = n > 0 ? cl.n_batches : 0;
+      const float lr = cl.lr;
+      // fp32 masters: pair tiles into TMEM (Dh = W', Dm = 0), the tail as hi / mid / lo bf16 planes; and the
+      // split of both into the forward operand (W' row F = b: params[F C + c], fl_core.py:126-129).  The later
+      // part of a cut client restores them from the state its first part saved.
+      const float* saved = nullptr;
+      if (sg.s0 > 0) {
+        const int* flag = sc.ready + 2 * sg.link + crank;
+        if (qt == 0) {
+          const int want = *sc.epoch;
+          int v;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if (v == want) break;
+            __nanosleep(256);
+          }
         }
-        if (q != own) {  // the peer's rows -> its receive buffer
-          const uint32_t dst = mapa(s_zr + lane * 256 + 128 * h, peer), bar = mapa(smem_u32(&bars[B_ZX]), peer);
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            st_async4b(dst + 16 * ((k + lane) & 7), __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]),
-                       __float_as_uint(z[4 * k + 2]), __float_as_uint(z[4 * k + 3]), bar);
-        } else {         // owned rows: back into the scratch row, unrotated, for the 8-lane softmax below
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            sts4(a + 16 * k, __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]), __float_as_uint(z[4 * k + 2]),
-                 __float_as_uint(z[4 * k + 3]));
-        }
+        named_sync(kBarQ, 256);
+        saved = sc.state + ((size_t)sg.link * 2 + crank) * kStateFloats;
       }
-      named_sync(kBarQ, 256);
-      // softmax of the owned rows (fl_core.py:132-151) on all eight Q warps: 8 lanes per row, 8 classes per lane
-      // (the bias is already in the logits: feature F)
-      if (tr) trace_pt(g, crank, s, 6);
-      wait_cluster(&bars[B_ZX], s & 1);
-      if (tr) trace_pt(g, crank, s, 7);
-      float e[8];
-      {
-        const uint32_t za = scratch_row(s_e, r_own) + 128 * (grp >> 2) + 32 * (grp & 3);
-        const uint32_t ra = s_zr + srow * 256;
-        const int c0 = 8 * grp;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const float4 a = lds4f(za + 16 * k);
-          // the peer pushed row srow rotated by its lane (= srow) within each 32-class half
-          const float4 b = lds4f(ra + 128 * (c0 >> 5) + 16 * ((((c0 & 31) >> 2) + k + srow) & 7));
-          e[4 * k] = a.x + b.x;
-          e[4 * k + 1] = a.y + b.y;
-          e[4 * k + 2] = a.z + b.z;
-          e[4 * k + 3] = a.w + b.w;
-        }
-        float mx = -FLT_MAX;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (c0 + i < C) mx = fmaxf(mx, e[i]);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-        float sum = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          e[i] = c0 + i < C ? __expf(e[i] - mx) : 0.f;
-          sum += e[i];
-        }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-        const float inv = 1.f / sum, inb = 1.f / (float)rows;
-        const bool vrow = r_own < rows;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = c0 + i;
-          e[i] = (vrow && c < C) ? -lr * ((e[i] * inv - (c == ylab ? 1.f : 0.f)) * inb) : 0.f;
-        }
-      }
-      named_sync(kBarQ, 256);  // every scratch row is read before E' overwrites the region
-      {
-        // E' row r_own, classes [8 grp, 8 grp + 8): one 16-byte unit per plane (MN-major [row][class], SW128),
-        // locally and pushed to the peer
-        uint32_t hw[4], mw[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) split_bf16x2(e[2 * k], e[2 * k + 1], hw[k], mw[k]);
-        const uint32_t ua = s_e + (r_own >> 3) * 1024 + (r_own & 7) * 128 + ((grp ^ (r_own & 7)) << 4);
-        const uint32_t bar = mapa(smem_u32(&bars[B_ER]), peer);
-        sts4(ua, hw[0], hw[1], hw[2], hw[3]);
-        sts4(ua + 8192, mw[0], mw[1], mw[2], mw[3]);
-        st_async4b(mapa(ua, peer), hw[0], hw[1], hw[2], hw[3], bar);
-        st_async4b(mapa(ua + 8192, peer), mw[0], mw[1], mw[2], mw[3], bar);
-      }
-      if (tr) trace_pt(g, crank, s, 8);
-      wait_cluster(&bars[B_ER], s & 1);  // the peer's rows
-      if (tr) trace_pt(g, crank, s, 9);
-      fence_proxy_async_smem();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[B_EF]);
-      if (tn > 0 && q == 0) {
-        // the tail master += its gradient (Z's columns, lanes = tail features), re-split into the operand
-        mbar_wait(&bars[B_TD], s & 1);
-        fence_after();
-        float gr[32];
-        {
-          float gm[32];
-          tld_row<32>(t_z + 32 * h, gr);
-          tld_row<32>(t_z + NP + 32 * h, gm);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) gr[i] += gm[i];
-        }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_TR]);
-        if (tail_lane) {
-          float w[32];
-          read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) w[i] += gr[i];
-          write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_WR + nc]);
-      }
-      if (tr) trace_pt(g, crank, s, 10);
-      // next forward's operand: re-split each master tile once the staged rows are re-laid out (the operand's
-      // chunk region is their staging area)
-      if (s + 1 < steps && nc > 0) mbar_wait(&bars[B_RL], s & 1);
-      for (int t = 0; t < ntp && s + 1 < steps; ++t) {
-        mbar_wait(&bars[B_BD + t], s & 1);
-        fence_after();
+      for (int t = 0; t < ntp; ++t) {
         const int f = tile_feature(t, L, nc, nfull);
         float w[32];
-        tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+        if (saved) {
+          const float4* sv = reinterpret_cast<const float4*>(saved + ((size_t)t * 128 + L) * NP + 32 * h);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 x = __ldcg(sv + i);
+            w[4 * i] = x.x;
+            w[4 * i + 1] = x.y;
+            w[4 * i + 2] = x.z;
+            w[4 * i + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int c = 32 * h + i, gfe = f0 + f;
+            w[i] = (f >= 0 && c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
+          }
+        }
+        tst_row<32>(t_w + NP * t + 32 * h + lq, w);
         if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
+      }
+      if (saved) {  // the tail planes, raw (hi / mid operand + lo): 6 KB
+        const uint4* sv = reinterpret_cast<const uint4*>(saved + 3 * 128 * NP);
+        for (int i = qt; i < (kTail + kTailLo) / 16; i += 256) {
+          const uint4 x = __ldcg(sv + i);
+          sts4(tail_w + 16 * i, x.x, x.y, x.z, x.w);
+        }
+      } else if (tail_lane) {
+        float w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = 32 * h + i, gfe = ft + lane;
+          w[i] = (c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
+        }
+        write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_proxy_async_smem();
+      fence_before();
+      if (saved) named_sync(kBarQ, 256);  // the restored tail planes come from all 8 warps
+      __syncwarp();
+      // (a client without steps only writes its zero delta: no forward consumes an operand arrival)
+      if (lane == 0 && sg.s1 > sg.s0) {
+        for (int t = 0; t < ntp; ++t)
+          if (2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
+        if (tn > 0 && q == 0) mbar_arrive(&bars[B_WR + nc]);
+      }
+
+      for (int s = sg.s0; s < sg.s1; ++s, ++it) {
+        const BatchRef br = batch_ref(s, n, B);
+        const int rows = br.rows;
+        const int ylab = r_own < rows ? cl.y[cl.perm[br.perm_off + r_own]] : -1;
+        if (qt == 0) {
+          mbar_arrive_expect_tx(&bars[B_ZX], 32 * NP * 4);
+          mbar_arrive_expect_tx(&bars[B_ER], 32 * NP * 4);
+        }
+        mbar_wait(&bars[B_ZF], it & 1);
+        fence_after();
+        const bool tr = qt == 0;
+        if (tr) trace_pt(g, crank, it, 5);
+        // this CTA's partial logits of the lane's row, classes [32h, 32h + 32): Wh and Wm column halves summed
+        float z[32];
+        {
+          float zm[32];
+          tld_row<32>(t_z + lq + 32 * h, z);
+          tld_row<32>(t_z + lq + NP + 32 * h, zm);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] += zm[i];
+        }
+        // hi + mid rows: the mid quadrants hand theirs over through the (idle) E' region
+        if (q >= 2) {
+          const uint32_t a = scratch_row(s_e, 32 * (q - 2) + lane) + 128 * h;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts4(a + 16 * ((k + lane) & 7), __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]),
+                 __float_as_uint(z[4 * k + 2]), __float_as_uint(z[4 * k + 3]));
+        }
+        named_sync(kBarQ, 256);
+        if (q < 2) {
+          const uint32_t a = scratch_row(s_e, L) + 128 * h;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float4 v = lds4f(a + 16 * ((k + lane) & 7));
+            z[4 * k] += v.x;
+            z[4 * k + 1] += v.y;
+            z[4 * k + 2] += v.z;
+            z[4 * k + 3] += v.w;
+          }
+          if (q != own) {  // the peer's rows -> its receive buffer
+            const uint32_t dst = mapa(s_zr + lane * 256 + 128 * h, peer), bar = mapa(smem_u32(&bars[B_ZX]), peer);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              st_async4b(dst + 16 * ((k + lane) & 7), __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]),
+                         __float_as_uint(z[4 * k + 2]), __float_as_uint(z[4 * k + 3]), bar);
+          } else {         // owned rows: back into the scratch row, unrotated, for the 8-lane softmax below
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              sts4(a + 16 * k, __float_as_uint(z[4 * k]), __float_as_uint(z[4 * k + 1]), __float_as_uint(z[4 * k + 2]),
+                   __float_as_uint(z[4 * k + 3]));
+          }
+        }
+        named_sync(kBarQ, 256);
+        // softmax of the owned rows (fl_core.py:132-151) on all eight Q warps: 8 lanes per row, 8 classes per
+        // lane (the bias is already in the logits: feature F)
+        if (tr) trace_pt(g, crank, it, 6);
+        wait_cluster(&bars[B_ZX], it & 1);
+        if (tr) trace_pt(g, crank, it, 7);
+        float e[8];
+        {
+          const uint32_t za = scratch_row(s_e, r_own) + 128 * (grp >> 2) + 32 * (grp & 3);
+          const uint32_t ra = s_zr + srow * 256;
+          const int c0 = 8 * grp;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float4 a = lds4f(za + 16 * k);
+            // the peer pushed row srow rotated by its lane (= srow) within each 32-class half
+            const float4 b = lds4f(ra + 128 * (c0 >> 5) + 16 * ((((c0 & 31) >> 2) + k + srow) & 7));
+            e[4 * k] = a.x + b.x;
+            e[4 * k + 1] = a.y + b.y;
+            e[4 * k + 2] = a.z + b.z;
+            e[4 * k + 3] = a.w + b.w;
+          }
+          float mx = -FLT_MAX;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (c0 + i < C) mx = fmaxf(mx, e[i]);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+          float sum = 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            e[i] = c0 + i < C ? __expf(e[i] - mx) : 0.f;
+            sum += e[i];
+          }
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+          const float inv = 1.f / sum, inb = 1.f / (float)rows;
+          const bool vrow = r_own < rows;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = c0 + i;
+            e[i] = (vrow && c < C) ? -lr * ((e[i] * inv - (c == ylab ? 1.f : 0.f)) * inb) : 0.f;
+          }
+        }
+        named_sync(kBarQ, 256);  // every scratch row is read before E' overwrites the region
+        {
+          // E' row r_own, classes [8 grp, 8 grp + 8): one 16-byte unit per plane (MN-major [row][class], SW128),
+          // locally and pushed to the peer
+          uint32_t hw[4], mw[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) split_bf16x2(e[2 * k], e[2 * k + 1], hw[k], mw[k]);
+          const uint32_t ua = s_e + (r_own >> 3) * 1024 + (r_own & 7) * 128 + ((grp ^ (r_own & 7)) << 4);
+          const uint32_t bar = mapa(smem_u32(&bars[B_ER]), peer);
+          sts4(ua, hw[0], hw[1], hw[2], hw[3]);
+          sts4(ua + 8192, mw[0], mw[1], mw[2], mw[3]);
+          st_async4b(mapa(ua, peer), hw[0], hw[1], hw[2], hw[3], bar);
+          st_async4b(mapa(ua + 8192, peer), mw[0], mw[1], mw[2], mw[3], bar);
+        }
+        if (tr) trace_pt(g, crank, it, 8);
+        wait_cluster(&bars[B_ER], it & 1);  // the peer's rows
+        if (tr) trace_pt(g, crank, it, 9);
         fence_proxy_async_smem();
         fence_before();
         __syncwarp();
-        if (lane == 0 && 2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
-        if (q == 0 && h == 0 && lane == 0) trace_pt(g, crank, s, 11 + t);
-      }
-    }
-    // delta = new - old (fl_core.py:194), fp32; W' row F is the bias
-    float* out = cl.delta;
-    for (int t = 0; t < ntp; ++t) {
-      if (steps > 0) {  // the last step's backward MMAs (its split was skipped)
-        mbar_wait(&bars[B_BD + t], (steps - 1) & 1);
-        fence_after();
-      }
-      const int f = tile_feature(t, L, nc, nfull);
-      float w[32];
-      tld_row<32>(t_w + NP * t + 32 * h + lq, w);
-      if (f >= 0 && f0 + f < FB) {
-        const size_t gi = (size_t)(f0 + f) * C;
+        if (lane == 0) mbar_arrive(&bars[B_EF]);
+        if (tn > 0 && q == 0) {
+          // the tail master += its gradient (Z's columns, lanes = tail features), re-split into the operand
+          mbar_wait(&bars[B_TD], it & 1);
+          fence_after();
+          float gr[32];
+          {
+            float gm[32];
+            tld_row<32>(t_z + 32 * h, gr);
+            tld_row<32>(t_z + NP + 32 * h, gm);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = 32 * h + i;
-          if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
+            for (int i = 0; i < 32; ++i) gr[i] += gm[i];
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[B_TR]);
+          if (tail_lane) {
+            float w[32];
+            read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] += gr[i];
+            write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          // the next forward's tail operand (a segment's first step gets it from the master set-up)
+          if (lane == 0 && s + 1 < sg.s1) mbar_arrive(&bars[B_WR + nc]);
+        }
+        if (tr) trace_pt(g, crank, it, 10);
+        // next forward's operand: re-split each master tile once the staged rows are re-laid out (the operand's
+        // chunk region is their staging area)
+        if (s + 1 < sg.s1 && nc > 0) {
+          mbar_wait(&bars[B_RL], rl & 1);
+          ++rl;
+        }
+        for (int t = 0; t < ntp && s + 1 < sg.s1; ++t) {
+          mbar_wait(&bars[B_BD + t], it & 1);
+          fence_after();
+          const int f = tile_feature(t, L, nc, nfull);
+          float w[32];
+          tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+          if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
+          fence_proxy_async_smem();
+          fence_before();
+          __syncwarp();
+          if (lane == 0 && 2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
+          if (q == 0 && h == 0 && lane == 0) trace_pt(g, crank, it, 11 + t);
         }
       }
-    }
-    if (tail_lane && ft + lane < FB) {
-      float w[32];
-      read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
-      const size_t gi = (size_t)(ft + lane) * C;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = 32 * h + i;
-        if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
+      // the segment's last backward MMAs (its split was skipped)
+      if (sg.s1 > sg.s0) {
+        for (int t = 0; t < ntp; ++t) mbar_wait(&bars[B_BD + t], (it - 1) & 1);
+        fence_after();
       }
+      if (sg.s1 < steps) {
+        // the first part of a cut client: save the exact state for the slot that finishes it
+        float* out = sc.state + ((size_t)sg.link * 2 + crank) * kStateFloats;
+        for (int t = 0; t < ntp; ++t) {
+          float w[32];
+          tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+          float4* o = reinterpret_cast<float4*>(out + ((size_t)t * 128 + L) * NP + 32 * h);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) __stcg(o + i, make_float4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]));
+        }
+        named_sync(kBarQ, 256);  // the tail update of the last step (quadrant-0 warps) is in the planes
+        uint4* o = reinterpret_cast<uint4*>(out + 3 * 128 * NP);
+        for (int i = qt; i < (kTail + kTailLo) / 16; i += 256) {
+          uint4 x;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                       : "r"(tail_w + 16 * i));
+          __stcg(o + i, x);
+        }
+        __threadfence();
+        named_sync(kBarQ, 256);
+        if (qt == 0) {
+          int* flag = sc.ready + 2 * sg.link + crank;
+          const int v = *sc.epoch;
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+        }
+      } else {
+        // delta = new - old (fl_core.py:194), fp32; W' row F is the bias
+        float* out = cl.delta;
+        for (int t = 0; t < ntp; ++t) {
+          const int f = tile_feature(t, L, nc, nfull);
+          float w[32];
+          tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+          if (f >= 0 && f0 + f < FB) {
+            const size_t gi = (size_t)(f0 + f) * C;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int c = 32 * h + i;
+              if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
+            }
+          }
+        }
+        if (tail_lane && ft + lane < FB) {
+          float w[32];
+          read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
+          const size_t gi = (size_t)(ft + lane) * C;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int c = 32 * h + i;
+            if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
+          }
+        }
+      }
+      fence_before();
+      named_sync(kBarQ, 256);  // every Q warp is done with this segment's masters before the next one's set-up
     }
   }
   fence_before();
@@ -633,6 +748,50 @@ __global__ void __maxnreg__(128)
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+}
+
+// The wrap-around schedule of n clients' steps over `slots` clusters (one thread; run before the trainer on the
+// same stream).  Output: segs (<= n + slots), start[slots + 1]; epoch bumped.
+__global__ void c64_schedule_kernel(const fedhc_client* __restrict__ clients, int n, int slots, Seg* segs, int* start,
+                                    int* epoch) {
+  extern __shared__ int steps_s[];
+  long long total = 0;
+  int longest = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int st = clients[i].n_rows > 0 ? clients[i].n_batches : 0;
+    steps_s[i] = st;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < n; ++i) {
+    total += steps_s[i];
+    longest = max(longest, steps_s[i]);
+  }
+  const long long T = max((long long)longest, (total + slots - 1) / slots);
+  int k = 0, cnt = 0;
+  long long pos = 0;
+  start[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    const int pj = steps_s[i];
+    if (pos + pj <= T || k == slots - 1) {
+      segs[cnt++] = Seg{i, 0, pj, -1};
+      pos += pj;
+    } else {
+      // cut at the slot boundary: this slot ends with the client's LAST steps, the next slot starts with its
+      // first ones (they run earlier: a = pj - (T - pos) <= pos because pj <= T)
+      const int a = (int)(pj - (T - pos));
+      segs[cnt++] = Seg{i, a, pj, k + 1};
+      start[++k] = cnt;
+      segs[cnt++] = Seg{i, 0, a, k};
+      pos = a;
+    }
+    if (pos == T && k < slots - 1 && i + 1 < n) {
+      start[++k] = cnt;
+      pos = 0;
+    }
+  }
+  while (k < slots) start[++k] = cnt;
+  *epoch += 1;
 }
 
 // Geometry; false if the shape is not this kernel's (F <= 784, F % 8 == 0, 32 < C <= 64, B <= 64).
@@ -686,37 +845,87 @@ bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* 
                       int max_smem, bool split, int64_t split_off, cudaStream_t st, int* status) {
   using namespace c64;
   static const char* path = getenv("FEDHC_TRAIN_PATH");
+  static const bool no_wrap = getenv("FEDHC_C64_NO_WRAP") != nullptr;
   if (!split || (path && strcmp(path, "c64") != 0)) return false;
   Geom g{};
   if (!plan(F, C, max_batch, max_smem, g)) return false;
   g.split_off = split_off;
   if (getenv("FEDHC_TC_TRACE")) g.trace = tc_trace_buffer();
-  static int smem_set_of[64] = {0};
+  // per device: shared-memory opt-in, resident clusters, and the wrap-around schedule's buffers
+  struct Dev {
+    int smem = 0, resident = 0, cap_segs = 0, cap_links = 0;
+    Seg* segs = nullptr;
+    int *start = nullptr, *ready = nullptr, *epoch = nullptr;
+    float* state = nullptr;
+  };
+  static Dev devs[64];
   static std::mutex mu;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g.bytes;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  Sched sc{};
+  int slots = n_clients;
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(mu);
-    int& set = smem_set_of[dev & 63];
-    if (g.bytes > set) {
+    Dev& d = devs[dev & 63];
+    if (g.bytes > d.smem) {
       e = cudaFuncSetAttribute(train_c64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.bytes);
-      if (e == cudaSuccess) set = g.bytes;
+      if (e == cudaSuccess) {
+        d.smem = g.bytes;
+        cfg.gridDim = dim3(2);
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, train_c64_kernel, &cfg) == cudaSuccess) d.resident = clusters;
+        else cudaGetLastError();
+      }
+    }
+    if (e == cudaSuccess && !no_wrap && d.resident > 0 && n_clients > d.resident && n_clients <= 12000) {
+      slots = d.resident;
+      const int need_segs = n_clients + slots, need_links = slots + 1;
+      if (need_segs > d.cap_segs) {
+        cudaFree(d.segs);
+        cudaFree(d.start);
+        d.segs = nullptr;
+        d.start = nullptr;
+        e = cudaMalloc(&d.segs, sizeof(Seg) * need_segs);
+        if (e == cudaSuccess) e = cudaMalloc(&d.start, sizeof(int) * (need_segs + 1));
+        d.cap_segs = e == cudaSuccess ? need_segs : 0;
+      }
+      if (e == cudaSuccess && need_links > d.cap_links) {
+        cudaFree(d.state);
+        cudaFree(d.ready);
+        d.state = nullptr;
+        d.ready = nullptr;
+        e = cudaMalloc(&d.state, sizeof(float) * (size_t)kStateFloats * 2 * need_links);
+        if (e == cudaSuccess) e = cudaMalloc(&d.ready, sizeof(int) * 2 * need_links);
+        if (e == cudaSuccess) e = cudaMemset(d.ready, 0, sizeof(int) * 2 * need_links);
+        if (e == cudaSuccess && !d.epoch) {
+          e = cudaMalloc(&d.epoch, sizeof(int));
+          if (e == cudaSuccess) e = cudaMemset(d.epoch, 0, sizeof(int));
+        }
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the memsets land before the first schedule
+        d.cap_links = e == cudaSuccess ? need_links : 0;
+      }
+      if (e == cudaSuccess) {
+        sc = Sched{d.segs, d.start, d.state, d.ready, d.epoch};
+        c64_schedule_kernel<<<1, 256, sizeof(int) * n_clients, st>>>(clients, n_clients, slots, d.segs, d.start,
+                                                                        d.epoch);
+        e = cudaGetLastError();
+      }
     }
   }
   if (e == cudaSuccess) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * n_clients);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = g.bytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, train_c64_kernel, clients, params, g);
+    cfg.gridDim = dim3(2 * slots);
+    e = cudaLaunchKernelEx(&cfg, train_c64_kernel, clients, params, g, sc);
   }
   *status = e == cudaSuccess ? FEDHC_OK : cuda_status(e, "train_c64_kernel launch");
   return true;

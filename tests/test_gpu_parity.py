@@ -337,6 +337,39 @@ def test_c62_round_with_tail_wave(fh, tr, F):
         assert rel_err(deltas[i], want) <= REL, (i, rel_err(deltas[i], want))
 
 
+@pytest.mark.parametrize("F", [784, 720])
+def test_c62_wrap_schedule_bit_identical(fh, tr, F):
+    """More clients than resident 2-CTA clusters: train_c64_kernel lays the clients' steps out on the resident
+    clusters by McNaughton's wrap-around rule, so a client cut at a slot boundary runs its first steps on one
+    cluster, saves its state, and finishes on another.  Same steps, same order: the deltas must equal, bit for
+    bit, the ones of launches small enough to run every client whole on one cluster."""
+    import torch
+    from paper_2305_15668_b200.experiment import DeviceFederation
+    from paper_2305_15668_b200.spec import WorkloadSpec
+    C, K = 62, 170
+    sizes = [40 + (i * 37) % 150 for i in range(K)]
+    sizes[9] = 0
+    sizes[100] = 1
+    trn, tst = fm.synthetic(F, C, sum(sizes) + 200, seed=6)
+    shards, at = {}, 0
+    for i, n in enumerate(sizes):
+        shards[f"c{i}"] = tr.DatasetShard(f"c{i}", trn.features[at:at + n], trn.labels[at:at + n])
+        at += n
+    fed = DeviceFederation(shards, tr.Dataset(tst.features, tst.labels, C), F, C)
+    params = torch.from_numpy(np.random.default_rng(4).standard_normal(F * C + C) * 0.02).cuda()
+    wl = [WorkloadSpec(3 * n if n else 10, 64) for n in sizes]   # several reshuffles, ragged batches
+    ids = list(shards)
+    seeds = [fm.seed_of("train", 3, 0, c) for c in ids]
+    whole = fed.train(params, ids, wl, 0.1, seeds).cpu().numpy()
+    parts = [fed.train(params, ids[a:a + 40], wl[a:a + 40], 0.1, seeds[a:a + 40]).cpu().numpy()
+             for a in range(0, K, 40)]
+    cut = np.concatenate(parts)
+    assert whole.shape == cut.shape
+    bad = [i for i in range(K) if not np.array_equal(whole[i], cut[i])]
+    assert not bad, bad[:10]
+    assert np.all(whole[9] == 0)
+
+
 def test_x_split_layout(fh):
     """fedhc_x_split: each row -> per 8-feature unit [8 bf16 hi | 8 bf16 mid], hi = bf16_rn(x),
     mid = bf16_rn(x - hi)."""
