@@ -888,9 +888,13 @@ bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* 
         else cudaGetLastError();
       }
     }
-    if (e == cudaSuccess && !no_wrap && d.resident > 0 && n_clients > d.resident && n_clients <= 12000) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
+    const int need_segs = n_clients + d.resident, need_links = d.resident + 1;
+    // (while a graph is being captured the schedule's buffers cannot be allocated: wrap only with them in place)
+    const bool can_alloc = cap == cudaStreamCaptureStatusNone || (need_segs <= d.cap_segs && need_links <= d.cap_links);
+    if (e == cudaSuccess && !no_wrap && d.resident > 0 && n_clients > d.resident && n_clients <= 12000 && can_alloc) {
       slots = d.resident;
-      const int need_segs = n_clients + slots, need_links = slots + 1;
       if (need_segs > d.cap_segs) {
         cudaFree(d.segs);
         cudaFree(d.start);
