@@ -90,28 +90,31 @@ __global__ void __launch_bounds__(kEvalThreads, 1)
   if (threadIdx.x == 0 && s_count) atomicAdd(correct, static_cast<unsigned long long>(s_count));
 }
 
-// Fast path for F % 4 == 0, F <= 128 * NCH, C <= 16 (the logistic models of the round loop): a warp takes
+// Fast path for F % 4 == 0, F <= 128 * NCH, C <= 16 NG (the logistic models of the round loop): a warp takes
 // kER rows at a time and issues all of their 16-byte loads before any arithmetic (the warp-per-row loop
 // above waited on one load per 128 features), each W^T float4 read from shared memory serves kER rows (W^T
-// re-reads were the bound: 50 KB of shared-memory traffic per row), the 16 class sums are reduced with a
-// halving butterfly (16 shuffles per row instead of 5 per class) and the first-max argmax is a
-// (value, class) warp max.  Used by the round loop's accuracy, which runs on a few side SMs.
+// re-reads were the bound: 50 KB of shared-memory traffic per row), each 16-class group's sums are reduced
+// with a halving butterfly (16 shuffles per row instead of 5 per class), every lane keeps its first-max
+// candidate over the groups, and one (value, class) warp max ends the row.  Used by the round loop's
+// accuracy, which runs on a few side SMs; NG = 4 covers FEMNIST's 62 classes (the per-class warp sums of
+// eval_kernel made that 0.86 ms on 48 SMs for 16k rows).
 constexpr int kRowsThreads = 256;
 constexpr int kER = 4;
-template <int NCH>
+template <int NCH, int NG>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     eval_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ y, int64_t n, int F, int C, int Fs,
                      const double* __restrict__ params, unsigned long long* correct) {
+  constexpr int CP = 16 * NG;  // padded classes
   extern __shared__ __align__(16) unsigned char smem[];
-  float* Wt = reinterpret_cast<float*>(smem);  // [16][Fs], classes >= C zero
-  float* bias = Wt + (size_t)16 * Fs;          // [16]
+  float* Wt = reinterpret_cast<float*>(smem);  // [CP][Fs], classes >= C zero
+  float* bias = Wt + (size_t)CP * Fs;          // [CP]
   __shared__ unsigned int s_count;
   if (threadIdx.x == 0) s_count = 0;
-  for (int i = threadIdx.x; i < 16 * Fs; i += kRowsThreads) {
+  for (int i = threadIdx.x; i < CP * Fs; i += kRowsThreads) {
     const int c = i / Fs, f = i - c * Fs;
     Wt[i] = (c < C && f < F) ? static_cast<float>(params[(size_t)f * C + c]) : 0.f;
   }
-  for (int c = threadIdx.x; c < 16; c += kRowsThreads) bias[c] = c < C ? static_cast<float>(params[(size_t)F * C + c]) : 0.f;
+  for (int c = threadIdx.x; c < CP; c += kRowsThreads) bias[c] = c < C ? static_cast<float>(params[(size_t)F * C + c]) : 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int cls = 8 * ((lane >> 4) & 1) + 4 * ((lane >> 3) & 1) + 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
@@ -132,50 +135,70 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     int yr[kER];
 #pragma unroll
     for (int q = 0; q < kER; ++q) yr[q] = r0 + q < n ? y[r0 + q] : -1;
-    float v[kER][16];
+    float best[kER];
+    int bi[kER];
 #pragma unroll
-    for (int q = 0; q < kER; ++q)
+    for (int q = 0; q < kER; ++q) {
+      best[q] = -FLT_MAX;
+      bi[q] = CP;
+    }
+#pragma unroll 1
+    for (int gi = 0; gi < NG; ++gi) {
+      const float* Wg = Wt + (size_t)16 * gi * Fs;
+      float v[kER][16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[q][u] = 0.f;
+      for (int q = 0; q < kER; ++q)
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int f = 4 * lane + 128 * j;
-      if (f < Fs) {
+        for (int u = 0; u < 16; ++u) v[q][u] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const float4 w = *reinterpret_cast<const float4*>(Wt + (size_t)u * Fs + f);
+      for (int j = 0; j < NCH; ++j) {
+        const int f = 4 * lane + 128 * j;
+        if (f < Fs) {
 #pragma unroll
-          for (int q = 0; q < kER; ++q)
-            v[q][u] = fmaf(xv[q][j].x, w.x, fmaf(xv[q][j].y, w.y, fmaf(xv[q][j].z, w.z, fmaf(xv[q][j].w, w.w, v[q][u]))));
+          for (int u = 0; u < 16; ++u) {
+            const float4 w = *reinterpret_cast<const float4*>(Wg + (size_t)u * Fs + f);
+#pragma unroll
+            for (int q = 0; q < kER; ++q)
+              v[q][u] = fmaf(xv[q][j].x, w.x, fmaf(xv[q][j].y, w.y, fmaf(xv[q][j].z, w.z, fmaf(xv[q][j].w, w.w, v[q][u]))));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kER; ++q) {
+        // halving butterfly: after offset o a lane keeps the half of its classes selected by (lane & o)
+#pragma unroll
+        for (int o = 16, h = 8; o >= 2; o >>= 1, h >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int j = 0; j < h; ++j) {
+            const float send = up ? v[q][j] : v[q][j + h];
+            const float keep = up ? v[q][j + h] : v[q][j];
+            v[q][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        const int c = 16 * gi + cls;
+        float s = v[q][0] + __shfl_xor_sync(0xffffffffu, v[q][0], 1);
+        s = c < C ? s + bias[c] : -FLT_MAX;
+        if (s > best[q]) {  // groups in class order: strict keeps the first maximum
+          best[q] = s;
+          bi[q] = c;
         }
       }
     }
 #pragma unroll
     for (int q = 0; q < kER; ++q) {
-      // halving butterfly: after offset o a lane keeps the half of its classes selected by (lane & o)
-#pragma unroll
-      for (int o = 16, h = 8; o >= 2; o >>= 1, h >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int j = 0; j < h; ++j) {
-          const float send = up ? v[q][j] : v[q][j + h];
-          const float keep = up ? v[q][j + h] : v[q][j];
-          v[q][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      float best = v[q][0] + __shfl_xor_sync(0xffffffffu, v[q][0], 1);
-      best = cls < C ? best + bias[cls] : -FLT_MAX;
-      int bi = cls;
+      float bv = best[q];
+      int bc = bi[q];
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {  // (value, class) max; ties -> the smaller class (np.argmax)
-        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) {
-          best = ov;
-          bi = oi;
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (ov > bv || (ov == bv && oi < bc)) {
+          bv = ov;
+          bc = oi;
         }
       }
-      if (lane == 0 && bi == yr[q]) ++mine;
+      if (lane == 0 && bc == yr[q]) ++mine;
     }
   }
   if (lane == 0 && mine) atomicAdd(&s_count, mine);
@@ -205,19 +228,29 @@ extern "C" int fedhc_eval_ctas(const float* x, const int32_t* y, int64_t n, int 
   const int cap = max_ctas > 0 ? std::min(max_ctas, sms) : sms;
   const int blocks = static_cast<int>(std::min<int64_t>(need, (int64_t)cap));
   const int nch = (n_features + 127) / 128;
-  const size_t smem16 = ((size_t)16 * Fs + 16) * 4;
-  if (n_features % 4 == 0 && n_classes <= 16 && nch <= 8 && smem16 <= (size_t)max_smem) {
+  const int ng = n_classes <= 16 ? 1 : n_classes <= 32 ? 2 : n_classes <= 64 ? 4 : 0;
+  const size_t smemg = ((size_t)16 * ng * Fs + 16 * ng) * 4;
+  if (n_features % 4 == 0 && ng > 0 && nch <= 8 && smemg <= (size_t)max_smem) {
     const int64_t need2 = (n + kER * (kRowsThreads / 32) - 1) / (kER * (kRowsThreads / 32));
-    const int b2 = static_cast<int>(std::min<int64_t>(need2, (int64_t)cap));  // one CTA per SM (215 registers)
-#define FEDHC_EVAL_ROWS(N)                                                                                       \
-  case N:                                                                                                       \
-    if (smem16 > 48 * 1024) FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(eval_rows_kernel<N>))); \
-    eval_rows_kernel<N><<<b2, kRowsThreads, smem16, st>>>(x, y, n, n_features, n_classes, Fs, params, correct); \
+    const int b2 = static_cast<int>(std::min<int64_t>(need2, (int64_t)cap));  // one CTA per SM (~215 registers)
+#define FEDHC_EVAL_ROWS(N, G)                                                                                        \
+  case N:                                                                                                           \
+    if (smemg > 48 * 1024) FEDHC_CUDA_TRY(smem_optin_max(reinterpret_cast<const void*>(eval_rows_kernel<N, G>)));  \
+    eval_rows_kernel<N, G><<<b2, kRowsThreads, smemg, st>>>(x, y, n, n_features, n_classes, Fs, params, correct);   \
     break;
-    switch (nch) {
-      FEDHC_EVAL_ROWS(1) FEDHC_EVAL_ROWS(2) FEDHC_EVAL_ROWS(3) FEDHC_EVAL_ROWS(4)
-      FEDHC_EVAL_ROWS(5) FEDHC_EVAL_ROWS(6) FEDHC_EVAL_ROWS(7) FEDHC_EVAL_ROWS(8)
+#define FEDHC_EVAL_NCH(G)                                                                                            \
+    switch (nch) {                                                                                                  \
+      FEDHC_EVAL_ROWS(1, G) FEDHC_EVAL_ROWS(2, G) FEDHC_EVAL_ROWS(3, G) FEDHC_EVAL_ROWS(4, G)                       \
+      FEDHC_EVAL_ROWS(5, G) FEDHC_EVAL_ROWS(6, G) FEDHC_EVAL_ROWS(7, G) FEDHC_EVAL_ROWS(8, G)                       \
     }
+    if (ng == 1) {
+      FEDHC_EVAL_NCH(1)
+    } else if (ng == 2) {
+      FEDHC_EVAL_NCH(2)
+    } else {
+      FEDHC_EVAL_NCH(4)
+    }
+#undef FEDHC_EVAL_NCH
 #undef FEDHC_EVAL_ROWS
     FEDHC_CUDA_TRY(cudaGetLastError());
     return FEDHC_OK;

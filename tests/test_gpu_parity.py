@@ -241,6 +241,29 @@ def test_accuracy_cta_cap_invariant():
             assert int(got.item()) == int(ref.item()), (n, cap)
 
 
+def test_accuracy_first_max_ties_class_groups():
+    """The row kernel's 16-class groups (C <= 64): all-tied logits pick class 0 (np.argmax's first maximum),
+    and a maximum in a later group or the last real class is found; padding classes never win."""
+    import torch
+    from paper_2305_15668_b200 import _abi
+    g = torch.Generator(device="cuda").manual_seed(9)
+    st = torch.cuda.current_stream().cuda_stream
+    for C in (20, 40, 62, 64):
+        F, n = 784, 777
+        x = torch.randn(n, F, device="cuda", generator=g)
+        y = torch.randint(0, C, (n,), device="cuda", generator=g, dtype=torch.int32)
+        p = torch.zeros(F * C + C, device="cuda", dtype=torch.float64)
+        got = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _abi.check(_abi.lib.fedhc_eval(x.data_ptr(), y.data_ptr(), n, F, C, p.data_ptr(), got.data_ptr(), st))
+        assert int(got.item()) == int((y == 0).sum())
+        for top in (C - 1, 17 % C, 33 % C):  # the bias alone decides: a single maximum at class `top`
+            p.zero_()
+            p[F * C + top] = 1.0
+            got.zero_()
+            _abi.check(_abi.lib.fedhc_eval(x.data_ptr(), y.data_ptr(), n, F, C, p.data_ptr(), got.data_ptr(), st))
+            assert int(got.item()) == int((y == top).sum()), (C, top)
+
+
 def test_loss_and_grad_vs_oracle(tr):
     loss, grad = tr.loss_and_grad(FL["lg_p"], FL["lg_x"], FL["lg_y"], 4)
     assert loss == pytest.approx(float(FL["lg_loss"]), rel=1e-12)
