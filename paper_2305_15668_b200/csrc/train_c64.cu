@@ -76,7 +76,8 @@ struct Geom {
   int ft[2];     // SW32 tail tile of CTA k: features [ft, ft + tn), tn <= 16 (0: none)
   int tn[2];
   long long split_off;
-  unsigned long long* trace;  // FEDHC_TC_TRACE: %globaltimer phase points of cluster 0 [cta][step][32], else null
+  unsigned long long* trace;  // FEDHC_TC_TRACE: %globaltimer phase points of cluster 0 [cta][step][48], else null
+  int trace_off;              // first traced step (FEDHC_TC_TRACE_OFF)
   int off_x, off_w, off_e, off_zr, off_bar, off_tmem, bytes;
 };
 
@@ -141,9 +142,10 @@ __device__ __forceinline__ void read_tail_master(uint32_t row, int fe, uint32_t 
   }
 }
 
-constexpr int kTraceSteps = 32, kTracePts = 32;
+constexpr int kTraceSteps = 32, kTracePts = 48;  // 2 x 32 x 48 <= the shared trace buffer (8 x 32 x 24)
 __device__ __forceinline__ void trace_pt(const Geom& g, uint32_t crank, int s, int pt) {
-  if (g.trace != nullptr && blockIdx.x < 2 && s < kTraceSteps) {
+  s -= g.trace_off;
+  if (g.trace != nullptr && blockIdx.x < 2 && s >= 0 && s < kTraceSteps) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g.trace[((size_t)crank * kTraceSteps + s) * kTracePts + pt] = t;
@@ -181,6 +183,29 @@ __device__ __forceinline__ Seg seg_at(const Sched& sc, const fedhc_client* clien
   if (sc.segs) return sc.segs[sc.start[c] + i];
   const fedhc_client& cl = clients[c];
   return Seg{c, 0, cl.n_rows > 0 ? cl.n_batches : 0, -1};
+}
+
+// Classes [32h, 32h + 32) of W' row `row` (fp64 params, fl_core.py:126-129) as fp32, zero past C or for a row
+// outside W' (row < 0 or row >= F + 1).  Every load is unconditional (clamped address, zero selected after).
+__device__ __forceinline__ void params_row(const double* __restrict__ params, int row, int FB, int C, int h,
+                                           float (&w)[32]) {
+  const bool live = row >= 0 && row < FB;
+  const double* p = params + (size_t)(live ? row : 0) * C;
+  if ((C & 1) == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(p) + min(16 * h + i, C / 2 - 1));
+      const bool ok = live && 32 * h + 2 * i < C;
+      w[2 * i] = ok ? static_cast<float>(v.x) : 0.f;
+      w[2 * i + 1] = ok ? static_cast<float>(v.y) : 0.f;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const double v = __ldg(p + min(32 * h + i, C - 1));
+      w[i] = (live && 32 * h + i < C) ? static_cast<float>(v) : 0.f;
+    }
+  }
 }
 
 // 16 warps: 4 share an SM sub-partition, so 128 registers per thread is the ceiling (4 x 32 x 128 = its 16K)
@@ -236,8 +261,9 @@ __global__ void __maxnreg__(128)
   fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: Z [128 rows x (Wh | Wm) class halves] (also the tail gradient's home between the softmax and the next
-  // forward); pair tile t's master at 2 NP + NP t
+  // forward); pair tile t's master at 2 NP + NP t, its initial value at 5 NP + NP t
   const uint32_t t_z = tmem, t_w = tmem + 2 * NP;
+  const uint32_t t_i = t_w + 3 * NP;  // fp32(params) of the master tiles, for the delta (the free 192 columns)
   // barrier phases run over all steps of all the slot's segments: `it` = steps done so far
   if (warp < kLoadWarps) {
     // ---- loaders: warp j fills X tile j (chunk j, or the tail for j = nc) each step: lane = (8-feature unit u,
@@ -449,6 +475,7 @@ __global__ void __maxnreg__(128)
       // split of both into the forward operand (W' row F = b: params[F C + c], fl_core.py:126-129).  The later
       // part of a cut client restores them from the state its first part saved.
       const float* saved = nullptr;
+      if (qt == 0) trace_pt(g, crank, it, 4);  // set-up start
       if (sg.s0 > 0) {
         const int* flag = sc.ready + 2 * sg.link + crank;
         if (qt == 0) {
@@ -477,15 +504,21 @@ __global__ void __maxnreg__(128)
             w[4 * i + 3] = x.w;
           }
         } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int c = 32 * h + i, gfe = f0 + f;
-            w[i] = (f >= 0 && c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
-          }
+          params_row(params, f >= 0 ? f0 + f : -1, FB, C, h, w);
         }
         tst_row<32>(t_w + NP * t + 32 * h + lq, w);
+        if (sg.s1 == steps) {  // the segment that writes the delta keeps fp32(params) in the free columns
+          if (saved) {
+            float p0[32];
+            params_row(params, f >= 0 ? f0 + f : -1, FB, C, h, p0);
+            tst_row<32>(t_i + NP * t + 32 * h + lq, p0);
+          } else {
+            tst_row<32>(t_i + NP * t + 32 * h + lq, w);
+          }
+        }
         if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
       }
+      if (qt == 0) trace_pt(g, crank, it, 28);  // master tiles set
       if (saved) {  // the tail planes, raw (hi / mid operand + lo): 6 KB
         const uint4* sv = reinterpret_cast<const uint4*>(saved + 3 * 128 * NP);
         for (int i = qt; i < (kTail + kTailLo) / 16; i += 256) {
@@ -494,11 +527,7 @@ __global__ void __maxnreg__(128)
         }
       } else if (tail_lane) {
         float w[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = 32 * h + i, gfe = ft + lane;
-          w[i] = (c < C && gfe < FB) ? static_cast<float>(params[(size_t)gfe * C + c]) : 0.f;
-        }
+        params_row(params, ft + lane, FB, C, h, w);
         write_wop(wop_row(tail_w, lane), lane, 2048, h, w, wop_row(tail_lo, lane));
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -685,6 +714,7 @@ __global__ void __maxnreg__(128)
         for (int t = 0; t < ntp; ++t) mbar_wait(&bars[B_BD + t], (it - 1) & 1);
         fence_after();
       }
+      if (qt == 0) trace_pt(g, crank, it - 1, 32);  // finalize start
       if (sg.s1 < steps) {
         // the first part of a cut client: save the exact state for the slot that finishes it
         float* out = sc.state + ((size_t)sg.link * 2 + crank) * kStateFloats;
@@ -715,30 +745,30 @@ __global__ void __maxnreg__(128)
         float* out = cl.delta;
         for (int t = 0; t < ntp; ++t) {
           const int f = tile_feature(t, L, nc, nfull);
-          float w[32];
+          float w[32], p0[32];
           tld_row<32>(t_w + NP * t + 32 * h + lq, w);
+          tld_row<32>(t_i + NP * t + 32 * h + lq, p0);
           if (f >= 0 && f0 + f < FB) {
-            const size_t gi = (size_t)(f0 + f) * C;
+            float* o = out + (size_t)(f0 + f) * C + 32 * h;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int c = 32 * h + i;
-              if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
-            }
+            for (int i = 0; i < 32; ++i)
+              if (32 * h + i < C) o[i] = w[i] - p0[i];
           }
         }
         if (tail_lane && ft + lane < FB) {
-          float w[32];
+          float w[32], p0[32];
           read_tail_master(wop_row(tail_w, lane), lane, 2048, wop_row(tail_lo, lane), h, w);
-          const size_t gi = (size_t)(ft + lane) * C;
+          params_row(params, ft + lane, FB, C, h, p0);
+          float* o = out + (size_t)(ft + lane) * C + 32 * h;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int c = 32 * h + i;
-            if (c < C) out[gi + c] = w[i] - static_cast<float>(params[gi + c]);
-          }
+          for (int i = 0; i < 32; ++i)
+            if (32 * h + i < C) o[i] = w[i] - p0[i];
         }
       }
+      if (qt == 0) trace_pt(g, crank, it - 1, 33);  // finalize stores issued
       fence_before();
       named_sync(kBarQ, 256);  // every Q warp is done with this segment's masters before the next one's set-up
+      if (qt == 0) trace_pt(g, crank, it - 1, 34);  // all Q warps done
     }
   }
   fence_before();
@@ -850,7 +880,11 @@ bool launch_train_c64(const fedhc_client* clients, int n_clients, const double* 
   Geom g{};
   if (!plan(F, C, max_batch, max_smem, g)) return false;
   g.split_off = split_off;
-  if (getenv("FEDHC_TC_TRACE")) g.trace = tc_trace_buffer();
+  if (getenv("FEDHC_TC_TRACE")) {
+    g.trace = tc_trace_buffer();
+    const char* off = getenv("FEDHC_TC_TRACE_OFF");
+    g.trace_off = off ? atoi(off) : 0;
+  }
   // per device: shared-memory opt-in, resident clusters, and the wrap-around schedule's buffers
   struct Dev {
     int smem = 0, resident = 0, cap_segs = 0, cap_links = 0;
