@@ -36,7 +36,7 @@ from .roundsim import LeanRoundReport, RoundReport, RoundSimulator
 from .spec import ClientProfile, FleetConfig
 from .training import (Dataset, DatasetShard, check_aggregation, count_correct, device, fedavg_device,
                        init_params, n_permutations, native_permutations,
-                       split_supported, stable_seed, stream_ptr, train_launch, x_split)
+                       split_supported, stable_seed, stream_ptr, train_launch, train_sms_per_client, x_split)
 
 
 @dataclass
@@ -443,7 +443,10 @@ class FederatedRunner:
             try:
                 from .live import GreenPartitions
                 gp = GreenPartitions(dev.index if dev.index is not None else 0)
-                need = -(-k_max // gp.sms_per_group)  # groups the training needs (one SM per client)
+                # groups the training needs: one SM per client for the one-CTA trainers; the cluster trainers
+                # (62 classes, F > 784) fill the GPU, so no window is spare and side work shares the device
+                spc = train_sms_per_client(fed.n_features, fed.n_classes)
+                need = -(-k_max * spc // gp.sms_per_group)
                 spare = gp.n_groups - need
                 if spare >= 1:
                     # permutations: the SMs outside every group (28 of 148 on a B200: ~0.4 ms for 100 clients
@@ -582,7 +585,7 @@ class FederatedRunner:
         c.n_fleet, c.participants, c.slots = len(self.ids), kp, n
         c.n_features, c.n_classes, c.max_batch = fed.n_features, fed.n_classes, self._bs_max
         c.split = 1 if xs is not None else 0
-        c.eval_ctas = self._eval_ctas if self._eval_ctas is not None else max(8, self._sms - kp)
+        c.eval_ctas = self._eval_ctas if self._eval_ctas is not None else self._side_ctas(kp)
         c.rows_max = self._rows_max
         self._n_cfg = c
         h = C.c_void_p()
@@ -1013,7 +1016,7 @@ class FederatedRunner:
                 self.correct_dev.zero_()
                 if self._nt:
                     # overlaps the next round's training (one CTA per client): stay on the idle SMs
-                    ctas = self._eval_ctas if self._eval_ctas is not None else max(8, self._sms - k)
+                    ctas = self._eval_ctas if self._eval_ctas is not None else self._side_ctas(k)
                     _abi.check(_abi.lib.fedhc_eval_ctas(self._xt.data_ptr(), self._yt.data_ptr(),
                                                         self._nt, self.fed.n_features, self.fed.n_classes,
                                                         self.params.data_ptr(), self.correct_dev.data_ptr(), ctas,
@@ -1034,6 +1037,13 @@ class FederatedRunner:
         if self.use_graphs and p.chunks is None and k and p.meta_bytes and (gs is None or gs[0] != self._graph_key(p)):
             self._capture(p)
         self.host_s["launch"] += time.perf_counter() - tick
+
+    def _side_ctas(self, k: int) -> int:
+        """Accuracy CTAs without a green window: the SMs the one-CTA trainers leave idle beside k clients; the
+        cluster trainers fill the GPU (the accuracy then runs between trainings), so it takes every SM."""
+        if train_sms_per_client(self.fed.n_features, self.fed.n_classes) > 1:
+            return self._sms
+        return max(8, self._sms - k)
 
     def read_correct(self, slot: int) -> int:
         self._result_ev[slot].synchronize()

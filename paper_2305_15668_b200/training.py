@@ -208,6 +208,16 @@ def count_correct(x: torch.Tensor, y: torch.Tensor, params: torch.Tensor, n_clas
     return int(correct.item())
 
 
+def train_sms_per_client(n_features: int, n_classes: int) -> int:
+    """SMs one client's local SGD occupies in fedhc_local_train's dispatch (csrc/train.cu local_train_impl):
+    the one-CTA trainers (F <= 784, C <= 16), 2-CTA clusters (16 < C <= 64 at F <= 784: train_fused /
+    train_c64_kernel), the F-split tcgen05 clusters of train_tc_kernel above F = 784 (4 or 8 CTAs; 8 taken as
+    the bound).  The round loop sizes its side-work SM windows from this."""
+    if n_features <= 784:
+        return 1 if n_classes <= 16 else 2
+    return 8
+
+
 def split_supported(n_features: int, n_classes: int) -> bool:
     """Shapes whose trainer reads the fedhc_x_split row copy: the one-CTA mma.sync trainer (F = 784, C <= 16)
     and the tcgen05 cluster trainer (F > 784 or 32 < C <= 64, F % 8 == 0).  FEDHC_X_SPLIT=0 keeps every launch
