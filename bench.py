@@ -425,6 +425,7 @@ def run_ours(args, rank, world, local_rank):
         # 4-CTA clusters) and the CIFAR-shaped F = 3072 model (tcgen05 trainer, 8-CTA clusters)
         result["c62"] = kernel_subline(62, 784, PER_GPU, N_SAMPLES, 5, 2)
         result["f3072"] = kernel_subline(10, 3072, PER_GPU, 640, 5, 2)
+        result["cnn"] = cnn_subline(62, PER_GPU, 640, 3, 1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, _ = cpu_reference(args.cpu_seconds, warmup=1)
         result["cpu_baseline"] = {"value": v, "unit": "client-steps/s", "cores": cores, "kind": "port",
@@ -493,6 +494,85 @@ def kernel_subline(C_, F_, n_clients, n_samp, rounds, warm, fleet_seed=1):
                         f"local SGD + FedAvg (device-resident rounds)",
             "value": steps / (ms / 1e3), "unit": "client-steps/s", "ms_per_round": ms, "train_kernel_ms": train_ms,
             "rounds": rounds, "roofline": roofline_entry(bytes_launch, train_ms, ROOT, kernel=kern)}
+
+
+def cnn_subline(nc, n_clients, n_samp, rounds, warm, fleet_seed=1):
+    """BASELINE config 2's model (FEMNIST CNN, tcgen05 grouped implicit GEMMs, one CUDA graph per round) as a
+    driver-visible sub-object of the default line: device-resident rounds of n_clients x n_samp samples (the
+    full config-2 shape is `--workload cnn`), local SGD + FedAvg + accuracy, train phase timed with CUDA events;
+    tensor roofline by the algorithmic FLOPs, HBM roofline by the fp32 master traffic."""
+    import torch
+    import paper_2305_15668_b200 as fh
+    from paper_2305_15668_b200.cnn import CnnFederation, init_cnn_params
+    from paper_2305_15668_b200.devicedata import DeviceFleetData
+    from paper_2305_15668_b200.experiment import delta_buffer
+    from paper_2305_15668_b200.training import fedavg_device, stable_seed
+    from benchlib import hbm_peak
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bs, lr = 64, 0.01
+    fleet = fh.generate_fleet(fh.DistributionSpec(budget_levels=BUDGETS, num_samples=n_samp, batch_size=bs),
+                              FLEET_PER_GPU, fleet_seed)
+    by_id = {p.client_id: p for p in fleet}
+    ids = sorted(by_id)
+    data = DeviceFleetData(ids, [by_id[c].workload.num_samples for c in ids], 784, nc, alpha=0.5, seed=1234,
+                           n_test=4096)
+    fed = CnnFederation.from_arrays(data.x, data.y, data.offsets, data.x_test, data.y_test, nc).attach_engine(
+        n_clients, bs)
+    params = torch.tensor(fed.layout.to_padded(init_cnn_params(nc, 1)), dtype=torch.float64, device=dev)
+    deltas = delta_buffer(n_clients, fed.P, dev)
+    selector = random.Random(f"{fleet_seed}:selection")
+    plans = []
+    for r in range(rounds + warm):
+        mine = selector.sample(ids, n_clients)
+        wl = [by_id[c].workload for c in mine]
+        packed, meta = fed.plan(mine, wl, [stable_seed("train", fleet_seed, r, c) for c in mine])
+        perm_dev = torch.from_numpy(packed).to(dev)
+        fed._perm_dev = perm_dev
+        plans.append((perm_dev, fed.descriptors(mine, meta, lr, deltas), max(m[2] for m in meta)))
+    coef = torch.full((n_clients,), 1.0 / n_clients, dtype=torch.float64, device=dev)
+    counts = torch.zeros(rounds + warm, dtype=torch.int64, device=dev)
+    evs = []
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i, (_, desc, steps) in enumerate(plans):
+        if i == warm:
+            torch.cuda.synchronize()
+            t0.record()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fed.engine.local_train(desc.data_ptr(), n_clients, params, steps, lr, True)
+        b.record()
+        if i >= warm:
+            evs.append((a, b))
+        fedavg_device(deltas, coef, params, params)
+        fed.engine.correct_into(params, fed.x_test, fed.y_test, counts[i:i + 1])
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / rounds
+    train_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    steps = n_clients * math.ceil(n_samp / bs)
+    flops = cnn_flop_per_sample(nc) * n_clients * n_samp
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, src = float(peaks["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (cuBLAS, measured)"
+    except (OSError, KeyError, ValueError):
+        peak, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    tf = flops / (train_ms * 1e-3) / 1e12
+    hbm_v, hbm_src = hbm_peak(ROOT)
+    hbm_alg = float(steps * (8 * fed.layout.canonical_count + bs * (784 * 4 + 4)))
+    return {"workload": f"femnist-cnn-c{nc} (BASELINE config 2's model): {n_clients} clients x {n_samp} samples, "
+                        f"B={bs}, local SGD + FedAvg + accuracy (device-resident rounds; the full config-2 round is "
+                        f"--workload cnn)",
+            "value": steps / (ms / 1e3), "unit": "client-steps/s", "ms_per_round": ms, "train_ms": train_ms,
+            "rounds": rounds, "dtype": "bf16 operands (tcgen05), fp32 accumulation and masters",
+            "roofline_tensor": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                                "frac": tf / peak, "algorithmic_flop_per_launch": flops, "peak_source": src,
+                                "kernel": "train phase (one CUDA graph of grouped_gemm_kernel + conv1/pool/CE)"},
+            "roofline": {"bound": "hbm", "achieved": hbm_alg / (train_ms * 1e-3) / 1e9, "peak": hbm_v,
+                         "unit": "GB/s", "frac": hbm_alg / (train_ms * 1e-3) / 1e9 / hbm_v,
+                         "algorithmic_bytes_per_launch": hbm_alg, "peak_source": hbm_src},
+            "accuracy_last_round": counts[-1].item() / 4096}
 
 
 def run_live(args, rank, world, local_rank):
