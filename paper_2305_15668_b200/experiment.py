@@ -439,6 +439,7 @@ class FederatedRunner:
         # without green-context support or without spare SM groups.
         self._green = None
         self._eval_ctas = None
+        # FEDHC_NO_GREEN_SIDE=1: ordinary side streams (ncu cannot replay kernels launched into green contexts)
         if green_side and world == 1 and not os.environ.get("FEDHC_NO_GREEN_SIDE"):
             try:
                 from .live import GreenPartitions
@@ -480,9 +481,6 @@ class FederatedRunner:
         # training (both only read the params); round r + 1's FedAvg waits for it before writing them
         self._eval_stream = (torch.cuda.ExternalStream(self._eval_stream_raw, device=dev) if self._green is not None
                              else torch.cuda.Stream(device=dev))
-        if os.environ.get("FEDHC_SERIAL_SIDE"):  # experiment: side work on the training stream
-            self._plan_stream = torch.cuda.current_stream(dev)
-            self._eval_stream = torch.cuda.current_stream(dev)
         self._sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self._ev_agg = [torch.cuda.Event() for _ in range(n)]
         self._eval_done = None
