@@ -263,7 +263,7 @@ __global__ void __maxnreg__(128)
   // TMEM: Z [128 rows x (Wh | Wm) class halves] (also the tail gradient's home between the softmax and the next
   // forward); pair tile t's master at 2 NP + NP t, its initial value at 5 NP + NP t
   const uint32_t t_z = tmem, t_w = tmem + 2 * NP;
-  const uint32_t t_i = t_w + 3 * NP;  // fp32(params) of the master tiles, for the delta (the free 192 columns)
+  const uint32_t t_i = t_w + 3 * NP;  // fp32(params) of the master tiles (the free 192 columns), loaded once
   // barrier phases run over all steps of all the slot's segments: `it` = steps done so far
   if (warp < kLoadWarps) {
     // ---- loaders: warp j fills X tile j (chunk j, or the tail for j = nc) each step: lane = (8-feature unit u,
@@ -490,6 +490,17 @@ __global__ void __maxnreg__(128)
         named_sync(kBarQ, 256);
         saved = sc.state + ((size_t)sg.link * 2 + crank) * kStateFloats;
       }
+      // fp32(params) of the master tiles: the same for every client of the launch (all start from the round's
+      // params), so it is loaded once per CTA into the free TMEM columns; a fresh client's master is a TMEM copy
+      // of it and every delta subtracts it
+      if (si == 0) {
+        for (int t = 0; t < ntp; ++t) {
+          const int f = tile_feature(t, L, nc, nfull);
+          float p0[32];
+          params_row(params, f >= 0 ? f0 + f : -1, FB, C, h, p0);
+          tst_row<32>(t_i + NP * t + 32 * h + lq, p0);
+        }
+      }
       for (int t = 0; t < ntp; ++t) {
         const int f = tile_feature(t, L, nc, nfull);
         float w[32];
@@ -504,18 +515,9 @@ __global__ void __maxnreg__(128)
             w[4 * i + 3] = x.w;
           }
         } else {
-          params_row(params, f >= 0 ? f0 + f : -1, FB, C, h, w);
+          tld_row<32>(t_i + NP * t + 32 * h + lq, w);
         }
         tst_row<32>(t_w + NP * t + 32 * h + lq, w);
-        if (sg.s1 == steps) {  // the segment that writes the delta keeps fp32(params) in the free columns
-          if (saved) {
-            float p0[32];
-            params_row(params, f >= 0 ? f0 + f : -1, FB, C, h, p0);
-            tst_row<32>(t_i + NP * t + 32 * h + lq, p0);
-          } else {
-            tst_row<32>(t_i + NP * t + 32 * h + lq, w);
-          }
-        }
         if (f >= 0) write_wop(wop_row(s_w + (f >> 6) * kChunk, f & 63), f & 63, 8192, h, w);
       }
       if (qt == 0) trace_pt(g, crank, it, 28);  // master tiles set
