@@ -752,9 +752,16 @@ __global__ void __maxnreg__(128)
           tld_row<32>(t_i + NP * t + 32 * h + lq, p0);
           if (f >= 0 && f0 + f < FB) {
             float* o = out + (size_t)(f0 + f) * C + 32 * h;
+            if ((C & 1) == 0) {  // 8-byte aligned rows: half the (row-per-thread) store instructions
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (32 * h + i < C) o[i] = w[i] - p0[i];
+              for (int i = 0; i < 16; ++i)
+                if (32 * h + 2 * i < C)
+                  reinterpret_cast<float2*>(o)[i] = make_float2(w[2 * i] - p0[2 * i], w[2 * i + 1] - p0[2 * i + 1]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (32 * h + i < C) o[i] = w[i] - p0[i];
+            }
           }
         }
         if (tail_lane && ft + lane < FB) {
