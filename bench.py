@@ -421,8 +421,9 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches_per_round * args.steps,
     }
     if C == 10 and not args.no_sublines:
-        # the other reference-model shapes the round is quoted on: FEMNIST's 62 classes (tcgen05 trainer,
-        # 4-CTA clusters) and the CIFAR-shaped F = 3072 model (tcgen05 trainer, 8-CTA clusters)
+        # the other reference-model shapes the round is quoted on: FEMNIST's 62 classes (train_c64_kernel,
+        # 2-CTA tcgen05 clusters), the CIFAR-shaped F = 3072 model (train_tc_kernel, 8-CTA clusters), and
+        # config 2's FEMNIST CNN
         result["c62"] = kernel_subline(62, 784, PER_GPU, N_SAMPLES, 5, 2)
         result["f3072"] = kernel_subline(10, 3072, PER_GPU, 640, 5, 2)
         result["cnn"] = cnn_subline(62, PER_GPU, 640, 3, 1)
