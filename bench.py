@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sublines", action="store_true", help="skip the c62 / f3072 sub-objects of the round line")
     ap.add_argument("--workload", choices=["round", "cnn", "resnet", "mobilenet", "shufflenet", "fedavg", "gemm", "des",
-                                           "live"], default="round",
+                                           "live", "data"], default="round",
                     help="round: the FL round (headline); fedavg: config-5 aggregation sweep point")
     ap.add_argument("--fedavg-k", type=int, default=100)
     ap.add_argument("--fedavg-p", type=int, default=11_170_000)
@@ -719,6 +719,60 @@ def run_fedavg(args, rank, world, local_rank):
         "roofline": roofline_entry(alg_bytes, ms, ROOT, kernel="fedavg_kernel"),
         "clocks": clocks.summary(), "gpu_launches": args.steps * (1 if world == 1 else 2),
     }
+    return res
+
+
+def run_data(args, local_rank):
+    """SURVEY §8f rank 2 (fl_core.py:41-115): the reference experiment's synthetic dataset + non-IID partition at
+    fleet scale, bit-identical to the reference, built in HBM (devicedata.reference_federation: host centres /
+    labels / partition bookkeeping, device ziggurat normals).  value = dataset rows produced per second; the
+    CPU baseline runs the reference algorithm (numpy make_synthetic_dataset + partition_noniid, the oracle's
+    restatement) on a bounded sample."""
+    import torch
+
+    from paper_2305_15668_b200.devicedata import reference_federation
+    torch.cuda.set_device(local_rank)
+    n_clients, n_samp, F, C = 1000, 600, 784, 10
+    clients = [(f"c{i:04d}", n_samp) for i in range(n_clients)]
+    n_total = math.ceil(n_clients * n_samp / 0.8)
+
+    def build(seed):
+        fed = reference_federation(clients, F, C, n_total, seed, 0.5, seed + 1)
+        torch.cuda.synchronize()
+        return fed
+
+    for i in range(args.warmup):
+        build(100 + i)
+    times = []
+    with ClockSampler(local_rank) as clocks:
+        for i in range(args.steps):
+            t = time.perf_counter()
+            build(1000 + i)
+            times.append(time.perf_counter() - t)
+    s_med = float(np.median(times))
+    res = {
+        "metric": "synthetic dataset + non-IID partition rows generated per second (fl_core.py:41-115)",
+        "value": n_total / s_med, "unit": "rows/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": s_med * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "the reference's own synthetic data, bit for bit (numpy PCG64 streams reproduced)",
+        "config": {"workload": f"reference experiment data: {n_clients} clients x {n_samp} samples, F={F}, C={C}, "
+                               f"n_total={n_total} (test = n_total // 5), Dirichlet(0.5)",
+                   "timing": "wall clock per build incl. host labels / partition and H2D (device-synchronised)"},
+        "clocks": clocks.summary(),
+        # per build: fedhc_pcg64_standard_normal's two kernels per 2^18-row chunk, fedhc_x_split once
+        "gpu_launches": args.steps * (2 * math.ceil(n_total / (1 << 18)) + 1),
+    }
+    if not args.no_cpu_baseline:
+        import oracle.flmath as fm
+        n_small = max(10, int(n_total * 0.05))
+        small = [(c, n) for c, n in clients[:int(n_clients * 0.05)]]
+        t = time.perf_counter()
+        trn, _ = fm.synthetic(F, C, n_small, 7)
+        fm.dirichlet_partition(trn, small, 0.5, 8)
+        dt = time.perf_counter() - t
+        res["cpu_baseline"] = {"value": n_small / dt, "unit": "rows/s", "cores": 1, "kind": "port",
+                               "sample": f"{n_small} rows ({len(small)} clients) through the oracle's numpy "
+                                         f"restatement of make_synthetic_dataset + partition_noniid"}
     return res
 
 
@@ -1533,6 +1587,8 @@ def main():
         res = run_live(args, rank, world, local_rank)
     elif args.workload == "des":
         res = run_des(args) if rank == 0 else None
+    elif args.workload == "data":
+        res = run_data(args, local_rank) if rank == 0 else None
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:
