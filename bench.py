@@ -277,8 +277,12 @@ def run_ours(args, rank, world, local_rank):
         return rep, mine, wl, seeds, coef
 
     eval_stream = torch.cuda.Stream()
-    # the accuracy overlaps the next round's training (one CTA per client): keep it on the idle SMs
-    eval_ctas = max(8, torch.cuda.get_device_properties(dev).multi_processor_count - PER_GPU)
+    # the accuracy overlaps the next round's training: with the one-CTA-per-client trainer keep it on the idle
+    # SMs; the cluster trainers (62 classes) fill the GPU, so it takes every SM between trainings (as
+    # FederatedRunner._side_ctas)
+    from paper_2305_15668_b200.training import train_sms_per_client
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    eval_ctas = n_sms if train_sms_per_client(F, C) > 1 else max(8, n_sms - PER_GPU)
     eval_done = [None]
 
     def device_round(mine_desc, coef_dev, correct):
