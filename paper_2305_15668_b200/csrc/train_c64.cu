@@ -62,10 +62,11 @@ constexpr uint32_t kSW128 = 2, kSW32 = 6;
 // B_BD + t: pair tile t's backward MMAs done (t < 3); B_TD: the tail's gradient MMAs done; B_TR: the Q warps
 // have read the tail gradient out of Z's columns (the next forward may overwrite them)
 // B_FD + j: the forward MMAs of chunk j are done (its W operand region may take staged rows); B_ST: the next
-// step's rows have landed in the staging area; B_RL: the chunk loaders have re-laid them out
+// step's rows have landed in the staging area; B_RLP + t: the chunk loaders have re-laid out every staged row that
+// overlays pair tile t's W operand region (rows are re-laid in order, so tile 0's split need not wait for the last rows)
 enum {
   B_XF = 0, B_WR = B_XF + kMaxCh, B_FD = B_WR + kMaxCh, B_BD = B_FD + kMaxCh, B_TD = B_BD + 3, B_TR, B_ZF, B_EF, B_ZX,
-  B_ER, B_ST, B_RL, kBars
+  B_ER, B_ST, B_RLP, kBars = B_RLP + 3
 };
 
 struct Geom {
@@ -246,7 +247,7 @@ __global__ void __maxnreg__(128)
     mbar_init(&bars[B_ZX], 1);  // local arrive.expect_tx + the peer's st.async bytes
     mbar_init(&bars[B_ER], 1);
     mbar_init(&bars[B_ST], 1);
-    mbar_init(&bars[B_RL], nc > 0 ? nc : 1);
+    for (int t = 0; t < 3; ++t) mbar_init(&bars[B_RLP + t], nc > 0 ? nc : 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -341,6 +342,10 @@ __global__ void __maxnreg__(128)
           if (lane == 0) trace_pt(g, crank, it, 16 + j);
           const int rows = batch_ref(s, n, B).rows;
           const uint32_t sbase = s_w + (8 * j + u) * 32 + p * 16;
+          // last staged row overlaying pair tile t's W operand chunks [32 KB t, 32 KB (t + 1))
+          int rlast[3];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) rlast[t] = min(kRows - 1, (int)((2u * kChunk * (t + 1) + spitch - 1) / spitch) - 1);
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             uint4 v[8];
@@ -360,6 +365,13 @@ __global__ void __maxnreg__(128)
                      lv ? x.w : 0u);
               }
             }
+            // rows [16 b, 16 b + 16) read: release the W operand regions whose last staged row is among them
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+              for (int t = 0; t < 3; ++t)
+                if (t < ntp && rlast[t] >= 16 * b && rlast[t] < 16 * (b + 1)) mbar_arrive(&bars[B_RLP + t]);
+            }
           }
         }
         if (j >= 4 && lane == 0) trace_pt(g, crank, it, 25 + j);  // 29..31: tiles 4..6 landed
@@ -367,7 +379,6 @@ __global__ void __maxnreg__(128)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&bars[B_XF + j]);
-          if (!tail && s > sg.s0) mbar_arrive(&bars[B_RL]);
         }
         if (s + 1 < sg.s1) {
           load_idx(s + 1);
@@ -693,11 +704,8 @@ __global__ void __maxnreg__(128)
         if (tr) trace_pt(g, crank, it, 10);
         // next forward's operand: re-split each master tile once the staged rows are re-laid out (the operand's
         // chunk region is their staging area)
-        if (s + 1 < sg.s1 && nc > 0) {
-          mbar_wait(&bars[B_RL], rl & 1);
-          ++rl;
-        }
         for (int t = 0; t < ntp && s + 1 < sg.s1; ++t) {
+          if (nc > 0) mbar_wait(&bars[B_RLP + t], rl & 1);
           mbar_wait(&bars[B_BD + t], it & 1);
           fence_after();
           const int f = tile_feature(t, L, nc, nfull);
@@ -710,6 +718,7 @@ __global__ void __maxnreg__(128)
           if (lane == 0 && 2 * t + (q >> 1) < nc) mbar_arrive(&bars[B_WR + 2 * t + (q >> 1)]);
           if (q == 0 && h == 0 && lane == 0) trace_pt(g, crank, it, 11 + t);
         }
+        if (s + 1 < sg.s1 && nc > 0) ++rl;
       }
       // the segment's last backward MMAs (its split was skipped)
       if (sg.s1 > sg.s0) {
