@@ -388,9 +388,11 @@ __global__ void __maxnreg__(128)
             if (lane == 0) mbar_arrive_expect_tx(&bars[B_ST], (uint32_t)(nb.rows * ncopy * 4));
             __syncwarp();
             for (int r = lane; r < nb.rows; r += 32) {
+              const char* rowp = xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch;
+              // the tail warp gathers the row's tail features straight from global next step: pull them into L2
+              if (tn > 0) prefetch_l2(rowp + (size_t)ft * 4, (uint32_t)tn * 4);
               mbar_wait(&bars[B_FD + ((r + 1) * spitch - 1) / kChunk], it & 1);
-              bulk_g2s(smem + g.off_w + r * spitch, xsplit + (size_t)cl.perm[nb.perm_off + r] * pitch + (size_t)f0 * 4,
-                       (uint32_t)ncopy * 4, &bars[B_ST]);
+              bulk_g2s(smem + g.off_w + r * spitch, rowp + (size_t)f0 * 4, (uint32_t)ncopy * 4, &bars[B_ST]);
             }
           }
         }
