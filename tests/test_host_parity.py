@@ -278,3 +278,21 @@ def test_lean_round_report_matches_full_run():
         assert lean.makespan == full.makespan
         assert lean.full() == full
         assert lean.per_client_times == full.per_client_times  # attribute access materialises
+
+
+@pytest.mark.parametrize("alpha,seed", [(0.05, 3), (0.3, 7), (5.0, 1)])
+def test_partition_rows_vs_oracle_shortfall(alpha, seed):
+    """training.partition_rows (ndarray pools, the device dataset's partition) == the oracle's list-pool
+    restatement of fl_core.py:62-115, including the richest-pool shortfall path (a dataset that the clients
+    nearly exhaust, so late clients run out of their Dirichlet classes) and empty clients."""
+    tr, _ = training.make_synthetic_dataset(3, 7, 1500, seed=seed)
+    n_train = len(tr.labels)
+    sizes = [37, 0, 150, 1, 90, 200, 64, 128, 0, 300]
+    sizes.append(n_train - sum(sizes) - 3)  # all but 3 rows taken: the tail clients hit empty class pools
+    clients = [(f"p{i}", n) for i, n in enumerate(sizes)]
+    got = training.partition_rows(tr.labels, 7, clients, alpha, seed + 100)
+    want = fm.dirichlet_partition(fm.Data(tr.features, tr.labels, 7), clients, alpha, seed + 100)
+    for cid, n in clients:
+        assert len(got[cid]) == n
+        assert np.array_equal(tr.labels[got[cid]], want[cid].labels)
+        assert np.array_equal(tr.features[got[cid]], want[cid].features)
